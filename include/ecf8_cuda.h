@@ -1,0 +1,107 @@
+/*
+ * ecf8_cuda.h -- the drop-in boundary: a C ABI over the B200 ECF8 decoder.
+ *
+ * Plain pointers, sizes and int status codes; no C++ or torch types.  The C++
+ * API in include/ecf8/ headers (the reference's own interface) is implemented on
+ * top of these calls, and Python/ctypes binds them directly
+ * (paper_2510_02676_b200/_lib.py).  Each entry point names the reference
+ * function it replaces (/root/reference/proj/...).
+ *
+ * Threading: every call is reentrant.  Device calls are stream-ordered and
+ * asynchronous unless stated; host-span calls are synchronous.
+ * Errors: a non-zero ecf8_status plus a thread-local message from
+ * ecf8_last_error() carrying the reference's exception text.
+ */
+#ifndef ECF8_CUDA_H
+#define ECF8_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum ecf8_status {
+  ECF8_OK = 0,
+  ECF8_EINVAL = 1,  /* std::invalid_argument in the C++ API            */
+  ECF8_EFORMAT = 2, /* ecf8::FormatError                               */
+  ECF8_ECUDA = 3,   /* CUDA runtime failure or no sm_100 device        */
+  ECF8_ENOMEM = 4,  /* device / pinned allocation failed               */
+  ECF8_EIO = 5      /* ecf8::IoError                                   */
+} ecf8_status;
+
+/* One tensor's container sections (container.hpp:18-30 layout).  Whether
+ * the pointers are host or device memory is stated per call. */
+typedef struct ecf8_sections {
+  uint64_t n_elem;
+  uint32_t threads_per_block; /* T, power of two in [1, 1024]            */
+  uint8_t lengths[16];        /* canonical code lengths, 0 = absent       */
+  const uint8_t *encoded;
+  uint64_t encoded_len; /* n_blocks * T * 8 + 2                          */
+  const uint8_t *gaps;
+  uint64_t gaps_len; /* (n_blocks * T + 1) / 2                              */
+  const uint64_t *outpos;
+  uint64_t n_outpos; /* n_blocks + 1                                        */
+  const uint8_t *packed;
+  uint64_t packed_len; /* (n_elem + 1) / 2                                  */
+} ecf8_sections;
+
+/* Device-resident tensor: sections copied to HBM (zero-padded for 16-byte
+ * vector access) plus the device decode tables built from `lengths`. */
+typedef struct ecf8_dev_tensor ecf8_dev_tensor;
+
+/* A prepared multi-tensor decode (one launch for many tensors). */
+typedef struct ecf8_batch ecf8_batch;
+
+const char *ecf8_last_error(void);
+/* 0 when no usable device; never falls back to the CPU. */
+int ecf8_device_count(void);
+/* Kernel build info ("sm_100a ..."), for logs. */
+const char *ecf8_build_info(void);
+
+/* ---- host-span entry points (synchronous) ------------------------------ */
+
+/* Replaces ecf8::decode_parallel_into (codec.cpp:256-273): validates like
+ * the reference ("output size mismatch", "inconsistent block offsets"),
+ * stages the sections to the device, decodes on the B200, copies `out` back. */
+int ecf8_decode_host(const ecf8_sections *host, uint8_t *out, uint64_t out_len);
+
+/* Replaces ecf8::decode_block (codec.cpp:201-254): decodes block `block`
+ * into out[outpos[block], outpos[block+1]). out_len must be n_elem. */
+int ecf8_decode_block_host(const ecf8_sections *host, uint64_t block, uint8_t *out,
+                           uint64_t out_len);
+
+/* Replaces ecf8::count_phase (codec.cpp:133-161) on one window. */
+int ecf8_count_window(const uint8_t window10[10], unsigned gap, const uint8_t lengths[16],
+                      uint32_t *count);
+
+/* ---- device-resident path --------------------------------------------- */
+
+/* Device load path (container.cpp:324-352 per-tensor setup + lut.cpp:47-97):
+ * validates the sections, copies them to HBM on `stream` (cudaStream_t or
+ * NULL), builds the device tables. */
+int ecf8_tensor_upload(const ecf8_sections *host, void *stream, ecf8_dev_tensor **out);
+void ecf8_tensor_free(ecf8_dev_tensor *t);
+uint64_t ecf8_tensor_n_elem(const ecf8_dev_tensor *t);
+/* Container bytes the decoder reads + n_elem written (roofline numerator). */
+uint64_t ecf8_tensor_algorithmic_bytes(const ecf8_dev_tensor *t);
+uint64_t ecf8_tensor_device_bytes(const ecf8_dev_tensor *t);
+
+/* Decode into device memory d_out (n_elem bytes, 16-byte aligned). */
+int ecf8_decode_device(const ecf8_dev_tensor *t, uint8_t *d_out, void *stream);
+
+/* Many tensors, one launch.  The batch copies its descriptors to the device
+ * once; ecf8_batch_decode may then be called repeatedly (and captured in a
+ * CUDA graph). */
+int ecf8_batch_create(const ecf8_dev_tensor *const *ts, uint8_t *const *d_outs, int count,
+                      ecf8_batch **out);
+int ecf8_batch_decode(const ecf8_batch *b, void *stream);
+void ecf8_batch_free(ecf8_batch *b);
+/* Launches of the decode kernel issued by one ecf8_batch_decode call. */
+int ecf8_batch_launches(const ecf8_batch *b);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ECF8_CUDA_H */

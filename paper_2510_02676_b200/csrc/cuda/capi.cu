@@ -1,0 +1,438 @@
+// capi.cu -- implementation of the C ABI in include/ecf8_cuda.h.
+//
+// Host orchestration only: validation with the reference's messages, HBM
+// layout of a device tensor, descriptor setup, launches.  The decode itself
+// is decode.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "decode.cuh"
+#include "ecf8_cuda.h"
+#include "tables.hpp"
+
+using ecf8::dev::TensorDesc;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int status, const std::string& msg) {
+  g_last_error = msg;
+  return status;
+}
+
+struct CudaFailure {
+  cudaError_t err;
+  const char* what;
+};
+
+inline void cu(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaFailure{e, what};
+}
+
+// Runs f, mapping C++ / CUDA failures onto status codes.
+template <class F>
+int guarded(F&& f) {
+  try {
+    return f();
+  } catch (const CudaFailure& e) {
+    cudaGetLastError();  // clear sticky-free errors
+    return fail(ECF8_ECUDA, std::string(e.what) + ": " + cudaGetErrorString(e.err));
+  } catch (const std::bad_alloc&) {
+    return fail(ECF8_ENOMEM, "host allocation failed");
+  } catch (const std::invalid_argument& e) {
+    return fail(ECF8_EINVAL, e.what());
+  } catch (const std::exception& e) {
+    return fail(ECF8_ECUDA, e.what());
+  }
+}
+
+int require_device() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    return fail(ECF8_ECUDA, "no CUDA device: the ECF8 decoder runs on the B200 only (no CPU fallback)");
+  }
+  int dev = 0, major = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  if (major != 10) return fail(ECF8_ECUDA, "device is not sm_100 (kernels are built for sm_100a only)");
+  return ECF8_OK;
+}
+
+// Reference checks (codec.cpp:259-261, container.cpp:196-242) plus the
+// bounds the kernel relies on.
+int validate(const ecf8_sections* s, std::uint64_t* n_blocks_out) {
+  if (!s) return fail(ECF8_EINVAL, "null sections");
+  const std::uint32_t T = s->threads_per_block;
+  if (T < 1 || T > 1024 || (T & (T - 1)))
+    return fail(ECF8_EINVAL, "threads per block must be a power of two in [1, 1024]");
+  const std::uint64_t bb = std::uint64_t{T} * 8;
+  if (s->encoded_len < 2 || (s->encoded_len - 2) % bb != 0)
+    return fail(ECF8_EINVAL, "encoded section length mismatch");
+  const std::uint64_t nb = (s->encoded_len - 2) / bb;
+  if (s->n_outpos != nb + 1 || !s->outpos || s->outpos[nb] != s->n_elem || s->outpos[0] != 0)
+    return fail(ECF8_EINVAL, "inconsistent block offsets");
+  const std::uint64_t cap = std::uint64_t{T} * 64;
+  for (std::uint64_t b = 0; b < nb; ++b)
+    if (s->outpos[b + 1] < s->outpos[b] || s->outpos[b + 1] - s->outpos[b] > cap)
+      return fail(ECF8_EINVAL, "inconsistent block offsets");
+  if (s->gaps_len < (nb * T + 1) / 2) return fail(ECF8_EINVAL, "gap section length mismatch");
+  if (s->packed_len < (s->n_elem + 1) / 2) return fail(ECF8_EINVAL, "packed section length mismatch");
+  if (s->n_elem > 0 && (nb == 0 || !s->encoded || !s->gaps || !s->packed))
+    return fail(ECF8_EINVAL, "encoded section length mismatch");
+  if (s->n_elem > 0) {
+    try {
+      (void)ecf8::dev::tables_for(s->lengths);
+    } catch (const std::invalid_argument&) {
+      return fail(ECF8_EINVAL, "invalid length vector");
+    }
+  }
+  *n_blocks_out = nb;
+  return ECF8_OK;
+}
+
+std::uint64_t align_up(std::uint64_t x, std::uint64_t a) { return (x + a - 1) / a * a; }
+
+// Device copies of the decode tables, shared by every tensor with the same
+// code lengths (per device).
+struct DevTables {
+  std::uint32_t* fast = nullptr;
+  std::uint8_t* cascade = nullptr;
+  std::uint32_t n_luts = 0;
+  std::uint64_t lenpack = 0;
+};
+
+const DevTables& device_tables(const std::uint8_t lengths[16]) {
+  static std::mutex mu;
+  static std::map<std::pair<int, std::array<std::uint8_t, 16>>, DevTables> cache;
+  int dev = 0;
+  cu(cudaGetDevice(&dev), "cudaGetDevice");
+  std::array<std::uint8_t, 16> key{};
+  std::memcpy(key.data(), lengths, 16);
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find({dev, key});
+  if (it != cache.end()) return it->second;
+  const auto t = ecf8::dev::tables_for(lengths);
+  DevTables d;
+  d.n_luts = t->n_luts;
+  d.lenpack = t->lenpack;
+  void* p = nullptr;
+  cu(cudaMalloc(&p, t->fast.size() * 4 + t->cascade.size()), "cudaMalloc(tables)");
+  d.fast = static_cast<std::uint32_t*>(p);
+  d.cascade = static_cast<std::uint8_t*>(p) + t->fast.size() * 4;
+  cu(cudaMemcpy(d.fast, t->fast.data(), t->fast.size() * 4, cudaMemcpyHostToDevice), "upload tables");
+  cu(cudaMemcpy(d.cascade, t->cascade.data(), t->cascade.size(), cudaMemcpyHostToDevice), "upload tables");
+  return cache.emplace(std::make_pair(dev, key), d).first->second;
+}
+
+}  // namespace
+
+// One HBM allocation per tensor, sections at 256-byte aligned offsets, each
+// followed by zero padding (kernels over-read whole 16-byte vectors).
+struct ecf8_dev_tensor {
+  void* arena = nullptr;
+  std::uint64_t arena_bytes = 0;
+  std::uint64_t n_elem = 0, n_blocks = 0;
+  std::uint64_t algo_bytes = 0;
+  std::uint32_t T = 0;
+  TensorDesc desc{};  // out / tile fields filled per launch
+};
+
+struct ecf8_batch {
+  std::vector<TensorDesc*> d_descs;  // one device array per kwin group
+  std::vector<int> counts;
+  std::vector<int> kwins;
+  std::vector<std::uint64_t> tiles;
+};
+
+namespace {
+
+void upload_into(ecf8_dev_tensor* t, const ecf8_sections* s, std::uint64_t nb, cudaStream_t st) {
+  const std::uint64_t P = ecf8::dev::kPad;
+  const std::uint64_t off_enc = 0;
+  const std::uint64_t off_gap = align_up(off_enc + s->encoded_len + P, 256);
+  const std::uint64_t off_pos = align_up(off_gap + s->gaps_len + P, 256);
+  const std::uint64_t off_pak = align_up(off_pos + 8 * s->n_outpos, 256);
+  const std::uint64_t total = align_up(off_pak + s->packed_len + P, 256);
+  cu(cudaMalloc(&t->arena, total), "cudaMalloc(tensor)");
+  t->arena_bytes = total;
+  auto* base = static_cast<std::uint8_t*>(t->arena);
+  cu(cudaMemsetAsync(base, 0, total, st), "cudaMemset");
+  cu(cudaMemcpyAsync(base + off_enc, s->encoded, s->encoded_len, cudaMemcpyHostToDevice, st), "H2D encoded");
+  if (s->gaps_len) cu(cudaMemcpyAsync(base + off_gap, s->gaps, s->gaps_len, cudaMemcpyHostToDevice, st), "H2D gaps");
+  cu(cudaMemcpyAsync(base + off_pos, s->outpos, 8 * s->n_outpos, cudaMemcpyHostToDevice, st), "H2D outpos");
+  if (s->packed_len) cu(cudaMemcpyAsync(base + off_pak, s->packed, s->packed_len, cudaMemcpyHostToDevice, st), "H2D packed");
+
+  t->n_elem = s->n_elem;
+  t->n_blocks = nb;
+  t->T = s->threads_per_block;
+  t->algo_bytes = s->encoded_len + s->gaps_len + 8 * s->n_outpos + s->packed_len + s->n_elem;
+  TensorDesc& d = t->desc;
+  d.encoded = base + off_enc;
+  d.gaps = base + off_gap;
+  d.outpos = reinterpret_cast<const std::uint64_t*>(base + off_pos);
+  d.packed = base + off_pak;
+  d.n_elem = s->n_elem;
+  d.blk_begin = 0;
+  d.blk_end = nb;
+  d.T = s->threads_per_block;
+  if (s->n_elem) {
+    const DevTables& tb = device_tables(s->lengths);
+    d.fast = tb.fast;
+    d.cascade = tb.cascade;
+    d.n_luts = tb.n_luts;
+    d.lenpack = tb.lenpack;
+  }
+}
+
+// Single-descriptor launch: the descriptor rides in the kernel parameters.
+int launch_one(const TensorDesc& d, cudaStream_t st) {
+  if (d.blk_end <= d.blk_begin) return ECF8_OK;
+  ecf8::dev::LaunchArgs a{};
+  a.descs = nullptr;
+  a.n_desc = 1;
+  a.total_tiles = ecf8::dev::tiles_of(d.T, d.blk_end - d.blk_begin);
+  a.inline_desc = d;
+  a.inline_desc.tile_begin = 0;
+  cu(ecf8::dev::launch_decode(a, ecf8::dev::windows_per_thread(d.T), st), "decode launch");
+  return ECF8_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ecf8_last_error(void) { return g_last_error.c_str(); }
+
+int ecf8_internal_set_error(int status, const char* msg) { return fail(status, msg ? msg : ""); }
+
+int ecf8_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+const char* ecf8_build_info(void) {
+  return "ecf8-b200: sm_100a decode kernels (persistent tiles, multi-symbol tables)";
+}
+
+int ecf8_tensor_upload(const ecf8_sections* s, void* stream, ecf8_dev_tensor** out) {
+  return guarded([&]() -> int {
+    if (!out) return fail(ECF8_EINVAL, "null output handle");
+    *out = nullptr;
+    std::uint64_t nb = 0;
+    if (int rc = validate(s, &nb)) return rc;
+    if (int rc = require_device()) return rc;
+    auto t = std::make_unique<ecf8_dev_tensor>();
+    try {
+      upload_into(t.get(), s, nb, static_cast<cudaStream_t>(stream));
+    } catch (...) {
+      if (t->arena) cudaFree(t->arena);
+      throw;
+    }
+    *out = t.release();
+    return ECF8_OK;
+  });
+}
+
+void ecf8_tensor_free(ecf8_dev_tensor* t) {
+  if (!t) return;
+  if (t->arena) cudaFree(t->arena);
+  delete t;
+}
+
+uint64_t ecf8_tensor_n_elem(const ecf8_dev_tensor* t) { return t ? t->n_elem : 0; }
+uint64_t ecf8_tensor_algorithmic_bytes(const ecf8_dev_tensor* t) { return t ? t->algo_bytes : 0; }
+uint64_t ecf8_tensor_device_bytes(const ecf8_dev_tensor* t) { return t ? t->arena_bytes : 0; }
+
+int ecf8_decode_device(const ecf8_dev_tensor* t, uint8_t* d_out, void* stream) {
+  return guarded([&]() -> int {
+    if (!t) return fail(ECF8_EINVAL, "null tensor");
+    if (t->n_elem == 0) return ECF8_OK;
+    if (!d_out || (reinterpret_cast<std::uintptr_t>(d_out) & 15))
+      return fail(ECF8_EINVAL, "device output must be 16-byte aligned");
+    TensorDesc d = t->desc;
+    d.out = d_out;
+    d.out_offset = 0;
+    d.tile_begin = 0;
+    return launch_one(d, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int ecf8_batch_create(const ecf8_dev_tensor* const* ts, uint8_t* const* d_outs, int count,
+                      ecf8_batch** out) {
+  return guarded([&]() -> int {
+    if (!out || (count > 0 && (!ts || !d_outs))) return fail(ECF8_EINVAL, "null argument");
+    *out = nullptr;
+    auto b = std::make_unique<ecf8_batch>();
+    for (int kw : {1, 2, 4}) {
+      std::vector<TensorDesc> group;
+      std::uint64_t tiles = 0;
+      for (int i = 0; i < count; ++i) {
+        const ecf8_dev_tensor* t = ts[i];
+        if (!t) return fail(ECF8_EINVAL, "null tensor");
+        if (t->n_elem == 0 || ecf8::dev::windows_per_thread(t->T) != kw) continue;
+        if (!d_outs[i] || (reinterpret_cast<std::uintptr_t>(d_outs[i]) & 15))
+          return fail(ECF8_EINVAL, "device output must be 16-byte aligned");
+        TensorDesc d = t->desc;
+        d.out = d_outs[i];
+        d.out_offset = 0;
+        d.tile_begin = tiles;
+        tiles += ecf8::dev::tiles_of(d.T, t->n_blocks);
+        group.push_back(d);
+      }
+      if (group.empty()) continue;
+      TensorDesc* dd = nullptr;
+      cu(cudaMalloc(&dd, sizeof(TensorDesc) * group.size()), "cudaMalloc(batch)");
+      cu(cudaMemcpy(dd, group.data(), sizeof(TensorDesc) * group.size(), cudaMemcpyHostToDevice), "H2D batch");
+      b->d_descs.push_back(dd);
+      b->counts.push_back(static_cast<int>(group.size()));
+      b->kwins.push_back(kw);
+      b->tiles.push_back(tiles);
+    }
+    *out = b.release();
+    return ECF8_OK;
+  });
+}
+
+int ecf8_batch_decode(const ecf8_batch* b, void* stream) {
+  return guarded([&]() -> int {
+    if (!b) return fail(ECF8_EINVAL, "null batch");
+    for (std::size_t g = 0; g < b->d_descs.size(); ++g) {
+      ecf8::dev::LaunchArgs a{};
+      a.descs = b->d_descs[g];
+      a.n_desc = b->counts[g];
+      a.total_tiles = b->tiles[g];
+      cu(ecf8::dev::launch_decode(a, b->kwins[g], static_cast<cudaStream_t>(stream)), "decode launch");
+    }
+    return ECF8_OK;
+  });
+}
+
+int ecf8_batch_launches(const ecf8_batch* b) { return b ? static_cast<int>(b->d_descs.size()) : 0; }
+
+void ecf8_batch_free(ecf8_batch* b) {
+  if (!b) return;
+  for (TensorDesc* p : b->d_descs) cudaFree(p);
+  delete b;
+}
+
+int ecf8_decode_host(const ecf8_sections* s, uint8_t* out, uint64_t out_len) {
+  return guarded([&]() -> int {
+    if (!s) return fail(ECF8_EINVAL, "null sections");
+    if (out_len != s->n_elem) return fail(ECF8_EINVAL, "output size mismatch");
+    std::uint64_t nb = 0;
+    if (int rc = validate(s, &nb)) return rc;
+    if (s->n_elem == 0) return ECF8_OK;
+    if (int rc = require_device()) return rc;
+    ecf8_dev_tensor t;
+    upload_into(&t, s, nb, nullptr);
+    std::uint8_t* d_out = nullptr;
+    const cudaError_t ae = cudaMalloc(&d_out, align_up(s->n_elem, 16) + 16);
+    if (ae != cudaSuccess) {
+      cudaFree(t.arena);
+      cu(ae, "cudaMalloc(out)");
+    }
+    int rc = ECF8_OK;
+    try {
+      TensorDesc d = t.desc;
+      d.out = d_out;
+      rc = launch_one(d, nullptr);
+      if (rc == ECF8_OK) {
+        cu(cudaMemcpy(out, d_out, s->n_elem, cudaMemcpyDeviceToHost), "D2H out");
+      }
+    } catch (...) {
+      cudaFree(d_out);
+      cudaFree(t.arena);
+      throw;
+    }
+    cudaFree(d_out);
+    cudaFree(t.arena);
+    return rc;
+  });
+}
+
+int ecf8_decode_block_host(const ecf8_sections* s, uint64_t block, uint8_t* out, uint64_t out_len) {
+  return guarded([&]() -> int {
+    std::uint64_t nb = 0;
+    if (int rc = validate(s, &nb)) return rc;
+    if (block >= nb) return fail(ECF8_EINVAL, "block index out of range");
+    if (out_len < s->outpos[block + 1]) return fail(ECF8_EINVAL, "output size mismatch");
+    const std::uint64_t lo = s->outpos[block], hi = s->outpos[block + 1];
+    if (hi == lo) return ECF8_OK;
+    if (int rc = require_device()) return rc;
+    ecf8_dev_tensor t;
+    upload_into(&t, s, nb, nullptr);
+    const std::uint64_t off = lo & ~std::uint64_t{15};
+    std::uint8_t* d_out = nullptr;
+    const cudaError_t ae = cudaMalloc(&d_out, align_up(hi - off, 16) + 16);
+    if (ae != cudaSuccess) {
+      cudaFree(t.arena);
+      cu(ae, "cudaMalloc(out)");
+    }
+    int rc = ECF8_OK;
+    try {
+      TensorDesc d = t.desc;
+      d.out = d_out;
+      d.out_offset = off;
+      d.blk_begin = block;
+      d.blk_end = block + 1;
+      rc = launch_one(d, nullptr);
+      if (rc == ECF8_OK) cu(cudaMemcpy(out + lo, d_out + (lo - off), hi - lo, cudaMemcpyDeviceToHost), "D2H block");
+    } catch (...) {
+      cudaFree(d_out);
+      cudaFree(t.arena);
+      throw;
+    }
+    cudaFree(d_out);
+    cudaFree(t.arena);
+    return rc;
+  });
+}
+
+int ecf8_count_window(const uint8_t window10[10], unsigned gap, const uint8_t lengths[16],
+                      uint32_t* count) {
+  return guarded([&]() -> int {
+    if (!window10 || !lengths || !count) return fail(ECF8_EINVAL, "null argument");
+    try {
+      (void)ecf8::dev::tables_for(lengths);
+    } catch (const std::invalid_argument&) {
+      return fail(ECF8_EINVAL, "invalid length vector");
+    }
+    if (int rc = require_device()) return rc;
+    const DevTables& tb = device_tables(lengths);
+    struct Scratch {
+      std::uint8_t* win = nullptr;
+      std::uint32_t* cnt = nullptr;
+    };
+    thread_local Scratch sc;
+    if (!sc.win) {
+      cu(cudaMalloc(&sc.win, 16), "cudaMalloc");
+      cu(cudaMalloc(&sc.cnt, 4), "cudaMalloc");
+    }
+    std::uint8_t w16[16] = {0};
+    std::memcpy(w16, window10, 10);
+    cu(cudaMemcpy(sc.win, w16, 16, cudaMemcpyHostToDevice), "H2D window");
+    cu(ecf8::dev::launch_count_window(sc.win, gap & 15, tb.fast, tb.cascade, tb.n_luts, tb.lenpack,
+                                      sc.cnt, nullptr),
+       "count launch");
+    cu(cudaMemcpy(count, sc.cnt, 4, cudaMemcpyDeviceToHost), "D2H count");
+    return ECF8_OK;
+  });
+}
+
+}  // extern "C"

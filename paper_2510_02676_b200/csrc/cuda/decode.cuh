@@ -1,0 +1,62 @@
+// decode.cuh -- device descriptors and launchers for the ECF8 decode kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace ecf8::dev {
+
+// One tensor (or one block range of it) in a decode launch.  All pointers
+// are device memory.  encoded / gaps / packed carry >= 64 zero bytes of
+// padding so the kernels may over-read by whole 16-byte vectors.
+struct TensorDesc {
+  const std::uint8_t* encoded;
+  const std::uint8_t* gaps;
+  const std::uint64_t* outpos;
+  const std::uint8_t* packed;
+  const std::uint32_t* fast;     // tables.hpp fast table
+  const std::uint8_t* cascade;   // reference cascade (slow path)
+  std::uint8_t* out;             // element i lands at out[i - out_offset]
+  std::uint64_t out_offset;      // multiple of 16
+  std::uint64_t n_elem;
+  std::uint64_t blk_begin;       // decode blocks [blk_begin, blk_end)
+  std::uint64_t blk_end;
+  std::uint64_t lenpack;
+  std::uint64_t tile_begin;      // first tile of this desc within its launch
+  std::uint32_t T;
+  std::uint32_t n_luts;
+};
+
+constexpr int kThreads = 256;
+constexpr std::uint64_t kPad = 64;
+
+// Windows per thread the launch is compiled for: T <= 256 -> 1, 512 -> 2,
+// 1024 -> 4.
+inline int windows_per_thread(std::uint32_t T) { return T <= 256 ? 1 : static_cast<int>(T / 256); }
+
+inline std::uint64_t tiles_of(std::uint32_t T, std::uint64_t n_blocks) {
+  const std::uint64_t m = T >= 256 ? 1 : 256 / T;  // blocks per tile
+  return (n_blocks + m - 1) / m;
+}
+
+// Kernel parameters: either a device array of descriptors (batched, tile
+// ranges given by tile_begin) or, when descs == nullptr, one descriptor
+// passed by value (no host->device copy on the single-tensor path).
+struct LaunchArgs {
+  const TensorDesc* descs;
+  int n_desc;
+  std::uint64_t total_tiles;
+  TensorDesc inline_desc;
+};
+
+// One decode launch; every descriptor has windows_per_thread(T) == kwin.
+cudaError_t launch_decode(const LaunchArgs& args, int kwin, cudaStream_t stream);
+
+// count_phase on one window (window10 staged as 16 bytes in device memory).
+cudaError_t launch_count_window(const std::uint8_t* d_window16, unsigned gap,
+                                const std::uint32_t* d_fast, const std::uint8_t* d_cascade,
+                                std::uint32_t n_luts, std::uint64_t lenpack,
+                                std::uint32_t* d_count, cudaStream_t stream);
+
+}  // namespace ecf8::dev

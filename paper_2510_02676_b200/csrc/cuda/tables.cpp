@@ -1,0 +1,86 @@
+// tables.cpp -- host builder for the device decode tables (see tables.hpp).
+#include "tables.hpp"
+
+#include <map>
+#include <mutex>
+#include <stdexcept>
+
+#include "ecf8/huffman.hpp"
+#include "ecf8/lut.hpp"
+
+namespace ecf8::dev {
+
+namespace {
+constexpr std::uint16_t kUndetermined = 0xFFFF;
+
+inline std::uint16_t pack_step(unsigned sym, unsigned len) {
+  return static_cast<std::uint16_t>(sym | (len << 4));
+}
+}  // namespace
+
+DecodeTables build_tables(const std::uint8_t lengths[16]) {
+  std::array<std::uint8_t, 16> len{};
+  for (int s = 0; s < 16; ++s) len[s] = lengths[s];
+  const CodeTable code = canonical_codes(len);  // validates cap + Kraft
+  const CascadedLut lut = build_lut(code);
+
+  DecodeTables t;
+  t.lengths = len;
+  t.cascade = lut.entries;
+  t.n_luts = lut.n_luts;
+  for (int s = 0; s < 16; ++s) t.lenpack |= std::uint64_t{len[s] & 15u} << (4 * s);
+
+  // same[r][v]: the cascade's (symbol, length) common to every 16-bit window
+  // whose first r bits are v, or kUndetermined.  r = 16 is the cascade
+  // itself; coarser prefixes agree when both halves agree.
+  std::vector<std::vector<std::uint16_t>> same(17);
+  same[16].resize(1u << 16);
+  for (std::uint32_t w = 0; w < (1u << 16); ++w) {
+    const DecodeStep d = decode_one(lut, static_cast<std::uint16_t>(w));
+    same[16][w] = pack_step(d.symbol, d.bits);
+  }
+  for (int r = 15; r >= 1; --r) {
+    same[r].resize(1u << r);
+    const auto& fine = same[r + 1];
+    for (std::uint32_t v = 0; v < (1u << r); ++v) {
+      const std::uint16_t a = fine[2 * v], b = fine[2 * v + 1];
+      same[r][v] = (a == b) ? a : kUndetermined;
+    }
+  }
+
+  t.fast.resize(kFastEntries);
+  for (std::uint32_t idx = 0; idx < static_cast<std::uint32_t>(kFastEntries); ++idx) {
+    unsigned pos = 0, n = 0;
+    std::uint32_t syms = 0;
+    while (n < kMaxPerEntry && pos < static_cast<unsigned>(kFastBits)) {
+      const unsigned r = kFastBits - pos;            // visible bits left
+      const std::uint32_t v = idx & ((1u << r) - 1);  // they are idx's low r bits
+      const std::uint16_t st = same[r][v];
+      if (st == kUndetermined) break;
+      const unsigned sym = st & 15, l = st >> 4;
+      if (l == 0 || l > r) break;  // word runs past what the index shows
+      syms |= sym << (4 * n);
+      ++n;
+      pos += l;
+    }
+    t.fast[idx] = pos | (n << 5) | (syms << 8);
+  }
+  return t;
+}
+
+std::shared_ptr<const DecodeTables> tables_for(const std::uint8_t lengths[16]) {
+  static std::mutex mu;
+  static std::map<std::array<std::uint8_t, 16>, std::shared_ptr<const DecodeTables>> cache;
+  std::array<std::uint8_t, 16> key{};
+  for (int s = 0; s < 16; ++s) key[s] = lengths[s];
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+  }
+  auto built = std::make_shared<const DecodeTables>(build_tables(lengths));
+  std::lock_guard<std::mutex> lock(mu);
+  return cache.emplace(key, std::move(built)).first->second;
+}
+
+}  // namespace ecf8::dev

@@ -1,0 +1,84 @@
+"""Device-resident ECF8 tensors driven from PyTorch streams.
+
+PyTorch is plumbing here: it provides device memory for outputs, the CUDA
+stream handle and CUDA events.  The decode itself is the sm_100a kernel in
+libecf8_b200.so, reached through the C ABI (include/ecf8_cuda.h).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from ._lib import check, lib
+from .codec import EncodedTensor
+
+
+def _stream_ptr(stream: torch.cuda.Stream | None) -> int | None:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream or None
+
+
+class DeviceTensor:
+    """ecf8_tensor_upload: container sections + decode tables in HBM."""
+
+    def __init__(self, t: EncodedTensor, stream: torch.cuda.Stream | None = None):
+        self.n_elem = t.n_elem
+        self._sections = t.sections()
+        self._src = t  # keep host arrays alive until the async copy completes
+        h = C.c_void_p()
+        check(lib.ecf8_tensor_upload(C.byref(self._sections), _stream_ptr(stream), C.byref(h)))
+        self.handle = h
+        self.algorithmic_bytes = int(lib.ecf8_tensor_algorithmic_bytes(h))
+        self.device_bytes = int(lib.ecf8_tensor_device_bytes(h))
+
+    def decode_into(self, out: torch.Tensor, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+        if out.dtype not in (torch.uint8, torch.float8_e4m3fn, torch.float8_e5m2) or not out.is_cuda:
+            raise ValueError("out must be a CUDA uint8/float8 tensor")
+        if out.numel() != self.n_elem or not out.is_contiguous():
+            raise ValueError("output size mismatch")
+        check(lib.ecf8_decode_device(self.handle, C.c_void_p(out.data_ptr()), _stream_ptr(stream)))
+        return out
+
+    def decode(self, stream: torch.cuda.Stream | None = None, dtype=torch.uint8) -> torch.Tensor:
+        out = torch.empty(self.n_elem, dtype=dtype, device="cuda")
+        return self.decode_into(out, stream)
+
+    def free(self):
+        if getattr(self, "handle", None):
+            lib.ecf8_tensor_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        self.free()
+
+
+class Batch:
+    """ecf8_batch: many tensors decoded by one launch per window width."""
+
+    def __init__(self, tensors: list[DeviceTensor], outs: list[torch.Tensor]):
+        if len(tensors) != len(outs):
+            raise ValueError("one output per tensor")
+        for t, o in zip(tensors, outs):
+            if o.numel() != t.n_elem or not o.is_cuda or not o.is_contiguous():
+                raise ValueError("output size mismatch")
+        n = len(tensors)
+        ts = (C.c_void_p * n)(*[t.handle.value for t in tensors])
+        os_ = (C.c_void_p * n)(*[o.data_ptr() for o in outs])
+        h = C.c_void_p()
+        check(lib.ecf8_batch_create(ts, os_, n, C.byref(h)))
+        self.handle = h
+        self.tensors, self.outs = tensors, outs
+        self.launches = int(lib.ecf8_batch_launches(h))
+        self.algorithmic_bytes = sum(t.algorithmic_bytes for t in tensors)
+
+    def decode(self, stream: torch.cuda.Stream | None = None) -> None:
+        check(lib.ecf8_batch_decode(self.handle, _stream_ptr(stream)))
+
+    def free(self):
+        if getattr(self, "handle", None):
+            lib.ecf8_batch_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        self.free()

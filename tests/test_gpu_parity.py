@@ -1,0 +1,158 @@
+"""B200 decode parity: every decode goes through the C ABI on the GPU and is
+compared bit-for-bit with the CPU oracle (oracle/ecf8_oracle.c) and the
+original bytes.  Cases follow the reference suite
+(/root/reference/proj/tests/test_codec.cpp, acceptance.cpp).
+"""
+import numpy as np
+import pytest
+
+from paper_2510_02676_b200 import codec
+
+from _oracle import tensor_dict
+
+pytestmark = pytest.mark.gpu
+
+TS = (1, 2, 32, 256, 512, 1024)
+LADDER = np.array([1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 16, 16], np.uint8)
+
+
+def check(orc, x, T, lengths=None):
+    t = codec.encode_tensor(x, T, lengths)
+    got = codec.decode_parallel(t)
+    want = orc.decode_parallel(tensor_dict(t))
+    assert np.array_equal(want, x)
+    if not np.array_equal(got, want):
+        bad = np.flatnonzero(got != want)
+        raise AssertionError(f"T={T} n={x.size}: {bad.size} mismatches, first at {bad[0]}")
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 7, 8, 63, 64, 65, 100, 513, 4096, 100000])
+def test_sizes_distributions_widths(orc, n):
+    # test_codec.cpp:307-332
+    rng = np.random.default_rng(41 + n)
+    for dist in range(3):
+        if dist == 0:
+            x = rng.integers(0, 256, n, dtype=np.uint8)
+        elif dist == 1:
+            x = np.where(rng.random(n) < 0.9, 0x38, rng.integers(0, 256, n)).astype(np.uint8)
+        else:
+            x = np.full(n, 0xB8, np.uint8)
+        for T in TS:
+            check(orc, x, T)
+
+
+def test_empty_tensor():
+    t = codec.encode_tensor(np.zeros(0, np.uint8), 256)
+    assert codec.decode_parallel(t).size == 0
+
+
+def test_gap15_straddle(orc):
+    # test_codec.cpp:282-305
+    sym = np.array([0] * 63 + [15, 14] + [0] * 200, np.uint8)
+    i = np.arange(sym.size)
+    x = ((sym << 3) | ((i % 16) << 4 & 0x80) | (i % 8)).astype(np.uint8)
+    for T in TS:
+        check(orc, x, T, LADDER)
+
+
+def test_all_256_bytes(orc):
+    x = (np.arange(100000) & 0xFF).astype(np.uint8)
+    for T in TS:
+        check(orc, x, T)
+
+
+def test_alpha_stable_config1(orc):
+    # config 1: 4096 x 4096 E4M3, alpha 1.8, gamma 0.05, seed 1, T=256
+    x = codec.synth(1.8, 0.05, 4096 * 4096, 1)
+    t = codec.encode_tensor(x, 256)
+    got = codec.decode_parallel(t)
+    assert np.array_equal(got, x)
+    assert np.array_equal(orc.decode_parallel(tensor_dict(t), nthreads=0), got)
+
+
+@pytest.mark.parametrize("gamma", [0.02, 0.05, 1.0])
+def test_alpha_stable_widths(orc, gamma):
+    x = codec.synth(1.8, gamma, 300001, 7)
+    for T in TS:
+        check(orc, x, T)
+
+
+def test_e5m2_bytes(orc):
+    x = codec.synth(1.8, 0.05, 200000, 5, fmt="e5m2")
+    for T in (32, 256, 1024):
+        check(orc, x, T)
+
+
+def test_crafted_incomplete_codes(orc):
+    """Kraft < 1 codes (accepted by parse_container): fallback symbols."""
+    from test_tables import random_lengths
+
+    rng = np.random.default_rng(77)
+    for _ in range(30):
+        l = random_lengths(rng)
+        present = np.flatnonzero(l)
+        sym = rng.choice(present, 5000).astype(np.uint8)
+        x = ((sym << 3) | rng.integers(0, 256, sym.size).astype(np.uint8) & 0x87).astype(np.uint8)
+        check(orc, x, int(rng.choice(TS)), l)
+
+
+def test_decode_block_matches_oracle(orc):
+    # test_codec.cpp:334-367: any block, any (permuted) order, same bytes
+    rng = np.random.default_rng(43)
+    x = rng.integers(0, 256, 40000, dtype=np.uint8)
+    for T in (2, 32, 256, 1024):
+        t = codec.encode_tensor(x, T)
+        out = np.zeros(x.size, np.uint8)
+        for b in reversed(range(t.n_blocks)):
+            codec.decode_block(t, b, out)
+        assert np.array_equal(out, x)
+
+
+def test_count_phase_known_answers():
+    # test_codec.cpp:206-233 on the device count routine
+    l = np.zeros(16, np.uint8)
+    l[5] = 1
+    assert codec.count_phase(np.zeros(10, np.uint8), 0, l) == 64
+    l = np.zeros(16, np.uint8)
+    l[0], l[15] = 1, 16
+    w = np.zeros(10, np.uint8)
+    w[1] = 1
+    assert codec.count_phase(w, 15, l) == 34
+    assert codec.count_phase(np.zeros(10, np.uint8), 15, l) == 49
+    assert codec.count_phase(np.zeros(10, np.uint8), 0, l) == 64
+
+
+def test_count_phase_random_windows(orc):
+    from test_tables import length_sets
+
+    rng = np.random.default_rng(5)
+    sets = length_sets()
+    for k in range(300):
+        l = sets[k % len(sets)]
+        w = rng.integers(0, 256, 10, dtype=np.uint8)
+        g = int(rng.integers(0, 16))
+        assert codec.count_phase(w, g, l) == orc.count_phase(w, g, l)
+
+
+def test_container_streaming_roundtrip():
+    # test_container.cpp:227-263 + acceptance criterion 8
+    rng = np.random.default_rng(56)
+    tensors, largest = [], 0
+    for i in range(100):
+        n = int(rng.integers(0, 2000))
+        largest = max(largest, n)
+        tensors.append((f"t{i}", [n], rng.integers(0, 256, n, dtype=np.uint8)))
+    raw = codec.raw_file(tensors)
+    blob = codec.compress_raw(raw, 256)
+    out, allocs, cap = codec.decompress(blob)
+    assert out == raw and allocs == 1 and cap == largest
+
+
+def test_invalid_lengths_rejected_by_device_path():
+    t = codec.encode_tensor(np.arange(64, dtype=np.uint8), 32)
+    bad = t.copy()
+    bad.lengths[:] = 1
+    from paper_2510_02676_b200._lib import InvalidArgument
+
+    with pytest.raises(InvalidArgument, match="invalid length vector"):
+        codec.decode_parallel(bad)
