@@ -209,6 +209,111 @@ int launch_one(const TensorDesc& d, cudaStream_t st) {
   return ECF8_OK;
 }
 
+// Per-thread state of the host-span path: three streams (copy-in, decode,
+// copy-out), grow-only device buffers.  Deliberately never freed: CUDA may
+// already be torn down when thread_local destructors run at exit.
+struct HostCtx {
+  int dev = -1;
+  cudaStream_t s_in = nullptr, s_run = nullptr, s_out = nullptr;
+  std::vector<cudaEvent_t> ev_in, ev_run;
+  std::uint8_t* arena = nullptr;
+  std::uint64_t arena_cap = 0;
+  std::uint8_t* dout = nullptr;
+  std::uint64_t dout_cap = 0;
+};
+
+HostCtx& host_ctx() {
+  thread_local HostCtx c;
+  int dev = 0;
+  cu(cudaGetDevice(&dev), "cudaGetDevice");
+  if (c.dev != dev) {
+    c = HostCtx{};
+    c.dev = dev;
+    cu(cudaStreamCreateWithFlags(&c.s_in, cudaStreamNonBlocking), "stream");
+    cu(cudaStreamCreateWithFlags(&c.s_run, cudaStreamNonBlocking), "stream");
+    cu(cudaStreamCreateWithFlags(&c.s_out, cudaStreamNonBlocking), "stream");
+  }
+  return c;
+}
+
+void ensure(std::uint8_t** p, std::uint64_t* cap, std::uint64_t need) {
+  if (need <= *cap) return;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  *cap = 0;
+  cu(cudaMalloc(p, need), "cudaMalloc(staging)");
+  cu(cudaMemset(*p, 0, need), "cudaMemset(staging)");
+  *cap = need;
+}
+
+// decode_parallel_into on host spans: the tensor is cut into chunks of whole
+// tiles; chunk c's sections go H2D on s_in while chunk c-1 decodes on s_run
+// and chunk c-2's bytes come back on s_out.  With pinned host memory the
+// two PCIe directions and the decode overlap.
+int host_pipeline(const ecf8_sections* s, std::uint64_t nb, std::uint8_t* out) {
+  HostCtx& c = host_ctx();
+  const std::uint64_t P = ecf8::dev::kPad;
+  const std::uint64_t off_gap = align_up(s->encoded_len + P, 256);
+  const std::uint64_t off_pos = align_up(off_gap + s->gaps_len + P, 256);
+  const std::uint64_t off_pak = align_up(off_pos + 8 * s->n_outpos, 256);
+  const std::uint64_t total = align_up(off_pak + s->packed_len + P, 256);
+  ensure(&c.arena, &c.arena_cap, total);
+  ensure(&c.dout, &c.dout_cap, align_up(s->n_elem, 16) + 16);
+
+  const std::uint32_t T = s->threads_per_block;
+  const std::uint64_t m = T >= 256 ? 1 : 256 / T;  // blocks per tile
+  const std::uint64_t target = std::uint64_t{8} << 20;
+  std::uint64_t per = std::max<std::uint64_t>(m, target / (std::uint64_t{T} * 8) / m * m);
+  if (s->encoded_len < 2 * target) per = nb;
+  const std::uint64_t n_chunks = (nb + per - 1) / per;
+  while (c.ev_in.size() < n_chunks) {
+    cudaEvent_t a, b;
+    cu(cudaEventCreateWithFlags(&a, cudaEventDisableTiming), "event");
+    cu(cudaEventCreateWithFlags(&b, cudaEventDisableTiming), "event");
+    c.ev_in.push_back(a);
+    c.ev_run.push_back(b);
+  }
+
+  TensorDesc d{};
+  d.encoded = c.arena;
+  d.gaps = c.arena + off_gap;
+  d.outpos = reinterpret_cast<const std::uint64_t*>(c.arena + off_pos);
+  d.packed = c.arena + off_pak;
+  d.out = c.dout;
+  d.n_elem = s->n_elem;
+  d.T = T;
+  const DevTables& tb = device_tables(s->lengths);
+  d.fast = tb.fast;
+  d.cascade = tb.cascade;
+  d.n_luts = tb.n_luts;
+  d.lenpack = tb.lenpack;
+
+  cu(cudaMemcpyAsync(c.arena + off_pos, s->outpos, 8 * s->n_outpos, cudaMemcpyHostToDevice, c.s_in), "H2D outpos");
+  for (std::uint64_t k = 0; k < n_chunks; ++k) {
+    const std::uint64_t lo = k * per, hi = std::min(nb, lo + per);
+    const std::uint64_t e0 = lo * T * 8, e1 = hi * T * 8 + 2;
+    cu(cudaMemcpyAsync(c.arena + e0, s->encoded + e0, e1 - e0, cudaMemcpyHostToDevice, c.s_in), "H2D encoded");
+    const std::uint64_t g0 = lo * T / 2, g1 = std::min(s->gaps_len, (hi * T + 1) / 2);
+    if (g1 > g0) cu(cudaMemcpyAsync(c.arena + off_gap + g0, s->gaps + g0, g1 - g0, cudaMemcpyHostToDevice, c.s_in), "H2D gaps");
+    const std::uint64_t p0 = s->outpos[lo] / 2, p1 = std::min(s->packed_len, (s->outpos[hi] + 1) / 2);
+    if (p1 > p0) cu(cudaMemcpyAsync(c.arena + off_pak + p0, s->packed + p0, p1 - p0, cudaMemcpyHostToDevice, c.s_in), "H2D packed");
+    cu(cudaEventRecord(c.ev_in[k], c.s_in), "record");
+
+    cu(cudaStreamWaitEvent(c.s_run, c.ev_in[k], 0), "wait");
+    TensorDesc dk = d;
+    dk.blk_begin = lo;
+    dk.blk_end = hi;
+    if (int rc = launch_one(dk, c.s_run)) return rc;
+    cu(cudaEventRecord(c.ev_run[k], c.s_run), "record");
+
+    cu(cudaStreamWaitEvent(c.s_out, c.ev_run[k], 0), "wait");
+    const std::uint64_t o0 = s->outpos[lo], o1 = s->outpos[hi];
+    if (o1 > o0) cu(cudaMemcpyAsync(out + o0, c.dout + o0, o1 - o0, cudaMemcpyDeviceToHost, c.s_out), "D2H out");
+  }
+  cu(cudaStreamSynchronize(c.s_out), "sync");
+  return ECF8_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -339,30 +444,7 @@ int ecf8_decode_host(const ecf8_sections* s, uint8_t* out, uint64_t out_len) {
     if (int rc = validate(s, &nb)) return rc;
     if (s->n_elem == 0) return ECF8_OK;
     if (int rc = require_device()) return rc;
-    ecf8_dev_tensor t;
-    upload_into(&t, s, nb, nullptr);
-    std::uint8_t* d_out = nullptr;
-    const cudaError_t ae = cudaMalloc(&d_out, align_up(s->n_elem, 16) + 16);
-    if (ae != cudaSuccess) {
-      cudaFree(t.arena);
-      cu(ae, "cudaMalloc(out)");
-    }
-    int rc = ECF8_OK;
-    try {
-      TensorDesc d = t.desc;
-      d.out = d_out;
-      rc = launch_one(d, nullptr);
-      if (rc == ECF8_OK) {
-        cu(cudaMemcpy(out, d_out, s->n_elem, cudaMemcpyDeviceToHost), "D2H out");
-      }
-    } catch (...) {
-      cudaFree(d_out);
-      cudaFree(t.arena);
-      throw;
-    }
-    cudaFree(d_out);
-    cudaFree(t.arena);
-    return rc;
+    return host_pipeline(s, nb, out);
   });
 }
 
