@@ -28,10 +28,10 @@ void ecf8_host_free(void *p);
 int ecf8_host_build_code(const uint64_t counts[16], uint8_t lengths[16]);
 /* build_lut (lut.cpp:47-97): entries needs 18*256 bytes. */
 int ecf8_host_build_lut(const uint8_t lengths[16], uint8_t *entries, uint32_t *n_luts);
-/* The device tables for `lengths` (tables.hpp): fast needs 4096 u32,
- * cascade 18*256 bytes. */
-int ecf8_host_device_tables(const uint8_t lengths[16], uint32_t *fast, uint8_t *cascade,
-                            uint32_t *n_luts, uint32_t *fast_bits);
+/* The device tables for `lengths` (tables.hpp): fast needs 1 << 16 u32,
+ * smask 1 << 16 u16, cascade 18*256 bytes (first 1 << fast_bits used). */
+int ecf8_host_device_tables(const uint8_t lengths[16], uint32_t *fast, uint16_t *smask,
+                            uint8_t *cascade, uint32_t *n_luts, uint32_t *fast_bits);
 
 /* encode_tensor (codec.cpp:100-109) with the tensor's own build_code;
  * lengths may be NULL (histogram code) or a caller-chosen code. */

@@ -59,15 +59,17 @@ def build_lut(lengths) -> tuple[np.ndarray, int]:
     return buf[: 256 * n.value].copy(), n.value
 
 
-def device_tables(lengths) -> tuple[np.ndarray, np.ndarray, int, int]:
-    """(fast u32[4096], cascade bytes, n_luts, fast_bits) as uploaded to HBM."""
+def device_tables(lengths) -> tuple[np.ndarray, np.ndarray, np.ndarray, int, int]:
+    """(fast u32, start masks u16, cascade bytes, n_luts, fast_bits) as uploaded to HBM."""
     l = _u8(lengths)
     fast = np.zeros(1 << 16, np.uint32)
+    smask = np.zeros(1 << 16, np.uint16)
     casc = np.zeros(18 * 256, np.uint8)
     n = C.c_uint32()
     fb = C.c_uint32()
-    check(lib.ecf8_host_device_tables(_ptr(l), _ptr(fast), _ptr(casc), C.byref(n), C.byref(fb)))
-    return fast[: 1 << fb.value].copy(), casc[: 256 * n.value].copy(), n.value, fb.value
+    check(lib.ecf8_host_device_tables(_ptr(l), _ptr(fast), _ptr(smask), _ptr(casc), C.byref(n), C.byref(fb)))
+    k = 1 << fb.value
+    return fast[:k].copy(), smask[:k].copy(), casc[: 256 * n.value].copy(), n.value, fb.value
 
 
 # --------------------------------------------------------------- tensors

@@ -108,6 +108,7 @@ std::uint64_t align_up(std::uint64_t x, std::uint64_t a) { return (x + a - 1) / 
 // code lengths (per device).
 struct DevTables {
   std::uint32_t* fast = nullptr;
+  std::uint16_t* smask = nullptr;
   std::uint8_t* cascade = nullptr;
   std::uint32_t n_luts = 0;
   std::uint64_t lenpack = 0;
@@ -128,10 +129,12 @@ const DevTables& device_tables(const std::uint8_t lengths[16]) {
   d.n_luts = t->n_luts;
   d.lenpack = t->lenpack;
   void* p = nullptr;
-  cu(cudaMalloc(&p, t->fast.size() * 4 + t->cascade.size()), "cudaMalloc(tables)");
+  cu(cudaMalloc(&p, t->fast.size() * 4 + t->smask.size() * 2 + t->cascade.size()), "cudaMalloc(tables)");
   d.fast = static_cast<std::uint32_t*>(p);
-  d.cascade = static_cast<std::uint8_t*>(p) + t->fast.size() * 4;
+  d.smask = reinterpret_cast<std::uint16_t*>(static_cast<std::uint8_t*>(p) + t->fast.size() * 4);
+  d.cascade = static_cast<std::uint8_t*>(p) + t->fast.size() * 4 + t->smask.size() * 2;
   cu(cudaMemcpy(d.fast, t->fast.data(), t->fast.size() * 4, cudaMemcpyHostToDevice), "upload tables");
+  cu(cudaMemcpy(d.smask, t->smask.data(), t->smask.size() * 2, cudaMemcpyHostToDevice), "upload tables");
   cu(cudaMemcpy(d.cascade, t->cascade.data(), t->cascade.size(), cudaMemcpyHostToDevice), "upload tables");
   return cache.emplace(std::make_pair(dev, key), d).first->second;
 }
@@ -190,6 +193,7 @@ void upload_into(ecf8_dev_tensor* t, const ecf8_sections* s, std::uint64_t nb, c
   if (s->n_elem) {
     const DevTables& tb = device_tables(s->lengths);
     d.fast = tb.fast;
+    d.smask = tb.smask;
     d.cascade = tb.cascade;
     d.n_luts = tb.n_luts;
     d.lenpack = tb.lenpack;
@@ -284,6 +288,7 @@ int host_pipeline(const ecf8_sections* s, std::uint64_t nb, std::uint8_t* out) {
   d.T = T;
   const DevTables& tb = device_tables(s->lengths);
   d.fast = tb.fast;
+  d.smask = tb.smask;
   d.cascade = tb.cascade;
   d.n_luts = tb.n_luts;
   d.lenpack = tb.lenpack;
@@ -509,7 +514,7 @@ int ecf8_count_window(const uint8_t window10[10], unsigned gap, const uint8_t le
     std::uint8_t w16[16] = {0};
     std::memcpy(w16, window10, 10);
     cu(cudaMemcpy(sc.win, w16, 16, cudaMemcpyHostToDevice), "H2D window");
-    cu(ecf8::dev::launch_count_window(sc.win, gap & 15, tb.fast, tb.cascade, tb.n_luts, tb.lenpack,
+    cu(ecf8::dev::launch_count_window(sc.win, gap & 15, tb.fast, tb.smask, tb.cascade, tb.n_luts,
                                       sc.cnt, nullptr),
        "count launch");
     cu(cudaMemcpy(count, sc.cnt, 4, cudaMemcpyDeviceToHost), "D2H count");

@@ -2,24 +2,30 @@
 //
 // Replaces the reference's OpenMP block decoder
 // (/root/reference/proj/src/codec.cpp:133-273: count_phase, Blelloch scan,
-// emit_phase, staging copy) with a persistent CTA-per-SM kernel:
+// emit_phase, staging copy).  The reference decodes every symbol twice
+// (count, then emit); this kernel decodes once:
 //
-//   * a CTA owns a contiguous range of "tiles"; a tile is whole reference
-//     blocks covering 256 * kwin windows (T <= 256: 256/T blocks, one window
-//     per thread; T = 512/1024: one block, 2/4 windows per thread), so every
-//     tile starts at an outpos[] boundary and needs nothing from neighbours;
-//   * the tile's bitstream is staged to shared memory as big-endian 32-bit
-//     words (16-byte vector loads), the decode tables once per tensor;
-//   * pass 1 counts the words starting in each 64-bit window with the
-//     multi-symbol table (tables.hpp), several symbols per shared load;
-//   * a warp-shuffle + cross-warp scan of the counts, seeded by outpos[] per
-//     reference block, gives each window its output offset; counts past a
-//     block's outpos limit are clamped exactly as codec.cpp:239-246 does;
-//   * pass 2 re-decodes and drops exponent bytes (x << 3) into a shared
-//     staging tile;
-//   * write-back merges staging with the sign/mantissa nibbles in SWAR form
-//     and stores 16 output bytes per thread-iteration (edges byte-wise, so
-//     neighbouring tiles never touch the same byte).
+//   * persistent CTAs, each owning a contiguous run of "tiles"; a tile is
+//     whole reference blocks covering 256 * KWIN windows (T <= 256: 256/T
+//     blocks, one window per thread; T = 512/1024: one block, 2/4 windows per
+//     thread), so a tile starts at an outpos[] boundary;
+//   * decode tables (tables.hpp) live in shared memory per tensor;
+//   * each thread pulls its window bits straight into registers (two 8-byte
+//     loads, coalesced across the warp) and walks them with a 64-bit register
+//     window, up to five symbols per table load; the symbols that start
+//     before the window's 64-bit boundary are taken exactly, the last entry
+//     partially via a start-bit mask + popcount (codec.cpp:143-160 rule);
+//     symbols are packed as nibbles into a private shared-memory slot;
+//   * a warp-shuffle + cross-warp scan of the per-thread counts, seeded by
+//     outpos[] per reference block, gives every thread its output offset;
+//     counts past a block's outpos limit are clamped (codec.cpp:239-246);
+//   * each thread copies its nibbles to their final place in a nibble
+//     staging tile (funnel shifts, whole words); words shared by
+//     neighbouring threads are assembled by one owner from published
+//     partial words -- no atomics;
+//   * write-back merges exponent nibbles with the sign/mantissa nibbles in
+//     SWAR form and stores 16 bytes per thread-step; tile edges are written
+//     byte-wise so neighbouring tiles never touch the same byte.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -34,103 +40,143 @@ namespace {
 constexpr int kWarps = kThreads / 32;
 constexpr int kFastShift = 32 - kFastBits;
 
+struct Tables {
+  std::uint32_t fast[kFastEntries];
+  std::uint16_t smask[kFastEntries];
+  std::uint8_t cascade[18 * 256];
+};
+
 template <int KWIN>
 struct Smem {
-  static constexpr int kWindows = kThreads * KWIN;
-  static constexpr int kStreamWords = kWindows * 2 + 8;     // + lookahead / overread
-  static constexpr int kStagingBytes = kWindows * 64 + 32;  // <= T*64 per block, +align
-  std::uint32_t fast[kFastEntries];
-  std::uint32_t stream[kStreamWords];
-  std::uint64_t outpos[kThreads + 1];
-  std::uint32_t prefix[kThreads];
+  static constexpr int kSlotStride = KWIN * 8 + 1;             // words; odd => no bank conflicts
+  static constexpr int kStageWords = KWIN * kThreads * 8 + 8;  // tile nibbles + 16-nibble slack
+  Tables tb;
+  std::uint32_t slot[kThreads * kSlotStride];
+  alignas(16) std::uint32_t stage[kStageWords];
+  std::uint32_t rs[kThreads];
+  std::uint32_t re[kThreads];
+  std::uint32_t head[kThreads];
+  std::uint32_t excl[kThreads];
+  std::uint32_t blk[kThreads + 1];
   std::uint32_t warp_sum[kWarps];
-  std::uint8_t cascade[18 * 256];
-  alignas(16) std::uint8_t staging[kStagingBytes];
 };
 
-__device__ __forceinline__ std::uint32_t peek32(const std::uint32_t* sw, std::uint32_t p) {
-  const std::uint32_t j = p >> 5;
-  return __funnelshift_l(sw[j + 1], sw[j], p & 31);
-}
+// ---------------------------------------------------------------- sinks
 
-struct Step {
-  std::uint32_t sym, len;
+// Packs 4-bit symbols into consecutive 32-bit words (first symbol lowest).
+struct SlotSink {
+  std::uint32_t* ptr;
+  std::uint32_t lo = 0;  // partial word
+  std::uint32_t q4 = 0;  // bits used in lo, < 32
+  __device__ __forceinline__ void put(std::uint32_t syms, std::uint32_t n4) {
+    const std::uint32_t nl = lo | (syms << q4);
+    const std::uint32_t nh = __funnelshift_l(syms, 0u, q4);
+    q4 += n4;
+    if (q4 >= 32) {
+      *ptr++ = nl;
+      lo = nh;
+      q4 -= 32;
+    } else {
+      lo = nl;
+    }
+  }
 };
 
-// One reference decode_one at the head of x (top 16 bits), or the first
-// symbol of a fast entry.
-__device__ __forceinline__ Step single_step(std::uint32_t e, std::uint32_t n, std::uint32_t x,
-                                            const std::uint8_t* casc, std::uint32_t n_luts,
-                                            std::uint64_t lenpack) {
-  Step s;
-  if (n != 0) {
-    s.sym = (e >> 8) & 15;
-    const std::uint32_t l = static_cast<std::uint32_t>(lenpack >> (4 * s.sym)) & 15;
-    s.len = l ? l : 16;
-  } else {
-    const std::uint32_t w = x >> 16;
-    std::uint32_t v = casc[w >> 8];
-    if (v >= 240) v = casc[((256u - v) << 8) | (w & 255u)];
-    s.sym = v;
-    s.len = casc[((n_luts - 1) << 8) + v];
-  }
-  return s;
+struct CountSink {
+  std::uint32_t n4 = 0;
+  __device__ __forceinline__ void put(std::uint32_t, std::uint32_t k4) { n4 += k4; }
+};
+
+// The reference cascade (lut.hpp:43-49) on a 16-bit window: symbol.
+__device__ __forceinline__ std::uint32_t cascade_symbol(std::uint32_t w16, const Tables& tb) {
+  std::uint32_t v = tb.cascade[w16 >> 8];
+  if (v >= 240) v = tb.cascade[((256u - v) << 8) | (w16 & 255u)];
+  return v;
 }
 
-// Words starting in [p, end): codec.cpp:133-161 semantics.
-__device__ __forceinline__ std::uint32_t count_window(const std::uint32_t* sw, std::uint32_t p,
-                                                      std::uint32_t end, const std::uint32_t* fast,
-                                                      const std::uint8_t* casc,
-                                                      std::uint32_t n_luts, std::uint64_t lenpack) {
-  std::uint32_t c = 0;
-  do {
-    const std::uint32_t x = peek32(sw, p);
-    const std::uint32_t e = fast[x >> kFastShift];
-    const std::uint32_t b = e & 31, n = (e >> 5) & 7;
-    if (n != 0 && p + b <= end) {
-      c += n;
-      p += b;
+// Decodes the words that start in [gap, 64) of one 64-bit window
+// (codec.cpp:133-190 semantics); w0..w3 = window bits 0..127, big-endian.
+template <class Sink>
+__device__ __forceinline__ void decode_window(std::uint32_t w0, std::uint32_t w1, std::uint32_t w2,
+                                              std::uint32_t w3, std::uint32_t gap,
+                                              const Tables& tb, std::uint32_t len_off,
+                                              Sink& sink) {
+  std::uint32_t hi = __funnelshift_l(w1, w0, gap);
+  std::uint32_t lo = __funnelshift_l(w2, w1, gap);
+  std::uint32_t p = gap;
+  // Phase A: at least 32 valid bits remain in the register window.
+  while (p < 32) {
+    const std::uint32_t e = tb.fast[hi >> kFastShift];
+    const std::uint32_t n4 = (e >> 5) & 31;
+    std::uint32_t adv;
+    if (n4) {
+      sink.put(e >> 12, n4);
+      adv = e & 31;
     } else {
-      c += 1;
-      p += single_step(e, n, x, casc, n_luts, lenpack).len;
+      const std::uint32_t v = cascade_symbol(hi >> 16, tb);
+      sink.put(v, 4);
+      adv = tb.cascade[len_off + v];
     }
-  } while (p < end);
-  return c;
-}
-
-// codec.cpp:168-190: emit staging[q .. q_end) from bit p.
-__device__ __forceinline__ void emit_window(const std::uint32_t* sw, std::uint32_t p,
-                                            std::uint32_t q, std::uint32_t q_end,
-                                            std::uint8_t* stage, const std::uint32_t* fast,
-                                            const std::uint8_t* casc, std::uint32_t n_luts,
-                                            std::uint64_t lenpack) {
-  while (q < q_end) {
-    const std::uint32_t x = peek32(sw, p);
-    const std::uint32_t e = fast[x >> kFastShift];
-    const std::uint32_t b = e & 31, n = (e >> 5) & 7;
-    if (n != 0 && q + n <= q_end) {
-      std::uint32_t syms = e >> 8;
-      for (std::uint32_t i = 0; i < n; ++i, syms >>= 4) stage[q + i] = static_cast<std::uint8_t>((syms & 15) << 3);
-      q += n;
-      p += b;
-    } else {
-      const Step s = single_step(e, n, x, casc, n_luts, lenpack);
-      stage[q++] = static_cast<std::uint8_t>(s.sym << 3);
-      p += s.len;
+    hi = __funnelshift_l(lo, hi, adv);
+    lo = __funnelshift_l(0u, lo, adv);
+    p += adv;
+  }
+  // Refill once: p in [32, 48); window = bits [p, p + 64).
+  hi = __funnelshift_l(w2, w1, p - 32);
+  lo = __funnelshift_l(w3, w2, p - 32);
+  for (;;) {
+    const std::uint32_t idx = hi >> kFastShift;
+    const std::uint32_t e = tb.fast[idx];
+    const std::uint32_t n4 = (e >> 5) & 31;
+    const std::uint32_t r = 64 - p;  // bits left before the window boundary
+    if (n4 == 0) {
+      const std::uint32_t v = cascade_symbol(hi >> 16, tb);
+      sink.put(v, 4);
+      const std::uint32_t len = tb.cascade[len_off + v];
+      p += len;
+      if (p >= 64) break;
+      hi = __funnelshift_l(lo, hi, len);
+      lo = __funnelshift_l(0u, lo, len);
+      continue;
     }
+    const std::uint32_t b = e & 31;
+    if (b >= r) {  // last entry: only the symbols that start before bit 64
+      const std::uint32_t k4 = 4 * __popc(tb.smask[idx] & ((1u << r) - 1));
+      sink.put((e >> 12) & ((1u << k4) - 1), k4);
+      break;
+    }
+    sink.put(e >> 12, n4);
+    hi = __funnelshift_l(lo, hi, e);  // shift amount = e & 31 = b
+    lo = __funnelshift_l(0u, lo, e);
+    p += b;
   }
 }
 
-// Exponent bytes (x << 3) merged with four sign/mantissa nibbles taken from
-// two packed bytes (element 2i in the high half).  v = [q0, q0, q1, q1].
-__device__ __forceinline__ std::uint32_t merge4(std::uint32_t xbytes, std::uint32_t v) {
-  return xbytes | (v & 0x00800080u) | ((v >> 4) & 0x00070007u) | ((v << 4) & 0x80008000u) |
-         (v & 0x07000700u);
+__device__ __forceinline__ std::uint32_t bswap32(std::uint32_t x) { return __byte_perm(x, 0, 0x0123); }
+
+__device__ __forceinline__ std::uint32_t sel(std::uint32_t a, std::uint32_t b, std::uint32_t m) {
+  return (a & m) | (b & ~m);
 }
 
-__device__ __forceinline__ std::uint8_t merge1(std::uint8_t xbyte, std::uint8_t qb, std::uint64_t i) {
-  const std::uint32_t qh = (i & 1) ? (static_cast<std::uint32_t>(qb) << 4) : qb;
-  return static_cast<std::uint8_t>(xbyte | (qh & 0x80u) | ((qh >> 4) & 7u));
+// Eight FP8 bytes from eight exponent nibbles S (element i at bits 4i..4i+3)
+// and four packed sign/mantissa bytes P (element 2j in the high nibble of
+// byte j): byte = sign << 7 | exponent << 3 | mantissa.
+__device__ __forceinline__ void merge8(std::uint32_t S, std::uint32_t P, std::uint32_t& o0,
+                                       std::uint32_t& o1) {
+  const std::uint32_t even = sel(sel(S << 3, P, 0x78787878u), P >> 4, 0xF8F8F8F8u);
+  const std::uint32_t odd = sel(sel(S >> 1, P << 4, 0x78787878u), P, 0xF8F8F8F8u);
+  o0 = __byte_perm(even, odd, 0x5140);
+  o1 = __byte_perm(even, odd, 0x7362);
+}
+
+__device__ __forceinline__ std::uint8_t merge1(std::uint32_t x, std::uint32_t qb, std::uint64_t i) {
+  const std::uint32_t qh = (i & 1) ? (qb << 4) : qb;
+  return static_cast<std::uint8_t>((x << 3) | (qh & 0x80u) | ((qh >> 4) & 7u));
+}
+
+__device__ __forceinline__ std::uint32_t nib_mask(std::uint32_t lo_n, std::uint32_t hi_n) {
+  const std::uint32_t top = hi_n >= 8 ? 0xFFFFFFFFu : ((1u << (4 * hi_n)) - 1);
+  return top & ~((1u << (4 * lo_n)) - 1);
 }
 
 __device__ __forceinline__ int find_desc(const TensorDesc* descs, int n, std::uint64_t tile) {
@@ -145,167 +191,203 @@ __device__ __forceinline__ int find_desc(const TensorDesc* descs, int n, std::ui
 
 template <int KWIN>
 __global__ void __launch_bounds__(kThreads) decode_kernel(const LaunchArgs args) {
-  const TensorDesc* __restrict__ descs = args.descs;
-  const int n_desc = args.n_desc;
-  const std::uint64_t total_tiles = args.total_tiles;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem<KWIN>& sm = *reinterpret_cast<Smem<KWIN>*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const std::uint64_t total_tiles = args.total_tiles;
 
-  // Contiguous tile range per CTA: few tensor switches, tables reused.
   const std::uint64_t t_lo = total_tiles * blockIdx.x / gridDim.x;
   const std::uint64_t t_hi = total_tiles * (blockIdx.x + 1) / gridDim.x;
   int di = -1;
   std::uint64_t next_begin = 0;
   TensorDesc d;
+  std::uint32_t len_off = 0;
 
   for (std::uint64_t tile = t_lo; tile < t_hi; ++tile) {
     if (di < 0 || tile >= next_begin) {
-      if (descs) {
-        di = find_desc(descs, n_desc, tile);
-        d = descs[di];
-        next_begin = (di + 1 < n_desc) ? descs[di + 1].tile_begin : total_tiles;
+      if (args.descs) {
+        di = find_desc(args.descs, args.n_desc, tile);
+        d = args.descs[di];
+        next_begin = (di + 1 < args.n_desc) ? args.descs[di + 1].tile_begin : total_tiles;
       } else {
         di = 0;
         d = args.inline_desc;
         next_begin = total_tiles;
       }
-      __syncthreads();  // previous tile done with the old tables
-      for (int i = tid; i < kFastEntries; i += kThreads) sm.fast[i] = d.fast[i];
-      for (int i = tid; i < static_cast<int>(d.n_luts) * 256; i += kThreads) sm.cascade[i] = d.cascade[i];
+      __syncthreads();  // everyone is past the previous tile's decode
+      const uint4* f4 = reinterpret_cast<const uint4*>(d.fast);
+      uint4* sf4 = reinterpret_cast<uint4*>(sm.tb.fast);
+      for (int i = tid; i < kFastEntries / 4; i += kThreads) sf4[i] = __ldg(f4 + i);
+      const uint4* m4 = reinterpret_cast<const uint4*>(d.smask);
+      uint4* sm4 = reinterpret_cast<uint4*>(sm.tb.smask);
+      for (int i = tid; i < kFastEntries / 8; i += kThreads) sm4[i] = __ldg(m4 + i);
+      for (int i = tid; i < static_cast<int>(d.n_luts) * 256; i += kThreads) sm.tb.cascade[i] = d.cascade[i];
+      len_off = (d.n_luts - 1) << 8;
+      __syncthreads();
     }
     const std::uint32_t T = d.T;
     const std::uint32_t m = T >= 256 ? 1u : 256u / T;
     const std::uint64_t b0 = d.blk_begin + (tile - d.tile_begin) * m;
     const std::uint32_t nblk = static_cast<std::uint32_t>(d.blk_end - b0 < m ? d.blk_end - b0 : m);
     const std::uint32_t nwin = nblk * T;
-    const std::uint64_t w0 = b0 * T;
+    const std::uint64_t w0g = b0 * T;
+    const std::uint64_t A = __ldg(d.outpos + b0);
+    const std::uint64_t E = __ldg(d.outpos + b0 + nblk);
+    for (std::uint32_t i = tid; i <= nblk; i += kThreads)
+      sm.blk[i] = static_cast<std::uint32_t>(__ldg(d.outpos + b0 + i) - A);
 
-    // ---- stage bitstream words and block offsets
-    {
-      const uint4* src = reinterpret_cast<const uint4*>(d.encoded + w0 * 8);
-      const std::uint32_t nvec = (nwin * 8 + 16 + 15) / 16;
-      for (std::uint32_t v = tid; v < nvec; v += kThreads) {
-        const uint4 q = __ldg(src + v);
-        sm.stream[4 * v + 0] = __byte_perm(q.x, 0, 0x0123);
-        sm.stream[4 * v + 1] = __byte_perm(q.y, 0, 0x0123);
-        sm.stream[4 * v + 2] = __byte_perm(q.z, 0, 0x0123);
-        sm.stream[4 * v + 3] = __byte_perm(q.w, 0, 0x0123);
-      }
-      for (std::uint32_t i = tid; i <= nblk; i += kThreads) sm.outpos[i] = d.outpos[b0 + i];
-    }
-    __syncthreads();
-
-    // ---- pass 1: per-window counts
-    std::uint32_t cnt[KWIN];
-    std::uint32_t total = 0;
+    // ---- decode my windows into my slot
+    std::uint32_t* const my_slot = sm.slot + tid * Smem<KWIN>::kSlotStride;
+    SlotSink sink{my_slot};
 #pragma unroll
     for (int i = 0; i < KWIN; ++i) {
       const std::uint32_t wl = tid * KWIN + i;
-      cnt[i] = 0;
       if (wl < nwin) {
-        const std::uint64_t wg = w0 + wl;
-        const std::uint32_t gap = (d.gaps[wg >> 1] >> ((wg & 1) ? 0 : 4)) & 15;
-        cnt[i] = count_window(sm.stream, wl * 64 + gap, wl * 64 + 64, sm.fast, sm.cascade,
-                              d.n_luts, d.lenpack);
+        const std::uint64_t wg = w0g + wl;
+        const uint2 a = __ldg(reinterpret_cast<const uint2*>(d.encoded + 8 * wg));
+        const uint2 b = __ldg(reinterpret_cast<const uint2*>(d.encoded + 8 * wg + 8));
+        const std::uint32_t gap = (__ldg(d.gaps + (wg >> 1)) >> ((wg & 1) ? 0 : 4)) & 15u;
+        decode_window(bswap32(a.x), bswap32(a.y), bswap32(b.x), bswap32(b.y), gap, sm.tb, len_off, sink);
       }
-      total += cnt[i];
     }
+    if (sink.q4) *sink.ptr = sink.lo;
+    const std::uint32_t cnt = static_cast<std::uint32_t>(sink.ptr - my_slot) * 8 + (sink.q4 >> 2);
 
-    // ---- exclusive scan of per-thread totals (warp shuffles + warp sums)
-    std::uint32_t incl = total;
+    // ---- exclusive scan of the per-thread counts
+    std::uint32_t incl = cnt;
 #pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const std::uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
-      if (lane >= off) incl += y;
+    for (int o = 1; o < 32; o <<= 1) {
+      const std::uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
     }
     if (lane == 31) sm.warp_sum[warp] = incl;
     __syncthreads();
-    std::uint32_t warp_base = 0;
+    std::uint32_t excl = incl - cnt;
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w) warp_base += (w < warp) ? sm.warp_sum[w] : 0u;
-    const std::uint32_t excl = warp_base + incl - total;
-    sm.prefix[tid] = excl;
+    for (int w = 0; w < kWarps; ++w) excl += (w < warp) ? sm.warp_sum[w] : 0u;
+    sm.excl[tid] = excl;
     __syncthreads();
 
-    // ---- pass 2: emit exponent bytes into staging
-    const std::uint64_t A = sm.outpos[0];
-    const std::uint64_t S0 = A & ~std::uint64_t{15};
-    {
-      std::uint32_t run = excl;
+    // ---- my output range, clamped to my reference block's outpos limit
+    const std::uint32_t bl = (T < 256) ? static_cast<std::uint32_t>(tid) / T : 0u;
+    const std::uint32_t first = (T < 256) ? sm.excl[bl * T] : 0u;
+    const std::uint32_t start_rel = sm.blk[bl] + excl - first;
+    const std::uint32_t lim_rel = sm.blk[bl + 1];
+    std::uint32_t cc = 0;
+    if (static_cast<std::uint32_t>(tid) * KWIN < nwin && start_rel < lim_rel)
+      cc = min(cnt, lim_rel - start_rel);
+    const std::uint32_t off = static_cast<std::uint32_t>(A & 15);  // staging nibble of element A
+    const std::uint32_t d0 = start_rel + off, dend = d0 + cc;
+    const std::uint32_t data_end = off + static_cast<std::uint32_t>(E - A);
+    sm.rs[tid] = d0;
+    sm.re[tid] = dend;
+
+    // ---- copy my nibbles to their final place; publish partial words
+    std::uint32_t headv = 0, tailv = 0;
+    const std::uint32_t fw = d0 >> 3, lw = (dend - 1) >> 3;
+    if (cc) {
+      const std::uint32_t f4 = (d0 & 7) * 4;
+      std::uint32_t prev = 0;
+      for (std::uint32_t k = fw; k <= lw; ++k) {
+        const std::uint32_t cur = my_slot[k - fw];
+        std::uint32_t v = __funnelshift_l(prev, cur, f4);
+        prev = cur;
+        const std::uint32_t lo_n = (k == fw) ? (d0 & 7) : 0u;
+        const std::uint32_t hi_n = (k == lw) ? ((dend - 1) & 7) + 1 : 8u;
+        v &= nib_mask(lo_n, hi_n);
+        if (lo_n == 0 && hi_n == 8) sm.stage[k] = v;
+        else if (k == fw) headv = v;
+        else tailv = v;
+      }
+    }
+    sm.head[tid] = headv;
+    __syncthreads();
+
+    // ---- owners assemble words shared between threads
+    if (cc) {
+      const bool starts_fw = ((d0 & 7) == 0) || (d0 == off);
+      const bool fw_full = ((d0 & 7) == 0) && (dend >= 8 * fw + 8);
 #pragma unroll
-      for (int i = 0; i < KWIN; ++i) {
-        const std::uint32_t wl = tid * KWIN + i;
-        if (wl < nwin && cnt[i] != 0) {
-          const std::uint32_t bl = wl / T;
-          const std::uint64_t base = sm.outpos[bl];
-          const std::uint64_t lim = sm.outpos[bl + 1];
-          const std::uint64_t o_start = base + run - sm.prefix[(bl * T) / KWIN];
-          if (o_start < lim) {
-            const std::uint64_t o_end = o_start + cnt[i] < lim ? o_start + cnt[i] : lim;
-            const std::uint64_t wg = w0 + wl;
-            const std::uint32_t gap = (d.gaps[wg >> 1] >> ((wg & 1) ? 0 : 4)) & 15;
-            emit_window(sm.stream, wl * 64 + gap, static_cast<std::uint32_t>(o_start - S0),
-                        static_cast<std::uint32_t>(o_end - S0), sm.staging, sm.fast, sm.cascade,
-                        d.n_luts, d.lenpack);
+      for (int pass = 0; pass < 2; ++pass) {
+        std::uint32_t k, v;
+        if (pass == 0) {
+          if (!starts_fw || fw_full) continue;
+          k = fw;
+          v = headv;
+        } else {
+          if (lw == fw || (dend & 7) == 0) continue;
+          k = lw;
+          v = tailv;
+        }
+        const std::uint32_t wend = min(8 * k + 8, data_end);
+        std::uint32_t covered = dend;
+        for (int j = tid + 1; covered < wend && j < kThreads; ++j) {
+          if (sm.re[j] > sm.rs[j]) {
+            v |= sm.head[j];
+            covered = sm.re[j];
           }
         }
-        run += cnt[i];
+        sm.stage[k] = v;
       }
     }
     __syncthreads();
 
-    // ---- write-back: staging + nibbles -> FP8 bytes, 16 per step
+    // ---- write-back: exponent nibbles + sign/mantissa nibbles -> FP8 bytes
     {
-      const std::uint64_t E = sm.outpos[nblk];
-      const std::uint64_t nchunk = (E - S0 + 15) / 16;
+      const std::uint64_t S0 = A - off;
+      const std::uint32_t nchunk = (data_end + 15) >> 4;
       std::uint8_t* out = d.out;
-      for (std::uint64_t ci = tid; ci < nchunk; ci += kThreads) {
-        const std::uint64_t g = S0 + 16 * ci;
+      for (std::uint32_t ci = tid; ci < nchunk; ci += kThreads) {
+        const std::uint64_t g = S0 + 16ull * ci;
         if (g >= A && g + 16 <= E) {
-          const uint4 xs = *reinterpret_cast<const uint4*>(sm.staging + (g - S0));
-          const uint2 q = __ldg(reinterpret_cast<const uint2*>(d.packed + g / 2));
+          const uint2 s = *reinterpret_cast<const uint2*>(sm.stage + 2 * ci);
+          const uint2 q = __ldg(reinterpret_cast<const uint2*>(d.packed + (g >> 1)));
           uint4 r;
-          r.x = merge4(xs.x, __byte_perm(q.x, 0, 0x1100));
-          r.y = merge4(xs.y, __byte_perm(q.x, 0, 0x3322));
-          r.z = merge4(xs.z, __byte_perm(q.y, 0, 0x1100));
-          r.w = merge4(xs.w, __byte_perm(q.y, 0, 0x3322));
+          merge8(s.x, q.x, r.x, r.y);
+          merge8(s.y, q.y, r.z, r.w);
           *reinterpret_cast<uint4*>(out + (g - d.out_offset)) = r;
         } else {
           const std::uint64_t lo = g < A ? A : g;
           const std::uint64_t hi = g + 16 < E ? g + 16 : E;
-          for (std::uint64_t i = lo; i < hi; ++i)
-            out[i - d.out_offset] = merge1(sm.staging[i - S0], d.packed[i >> 1], i);
+          for (std::uint64_t i = lo; i < hi; ++i) {
+            const std::uint32_t nidx = static_cast<std::uint32_t>(i - S0);
+            const std::uint32_t x = (sm.stage[nidx >> 3] >> (4 * (nidx & 7))) & 15u;
+            out[i - d.out_offset] = merge1(x, d.packed[i >> 1], i);
+          }
         }
       }
     }
-    __syncthreads();
   }
 }
 
 __global__ void count_window_kernel(const std::uint8_t* w16, unsigned gap, const std::uint32_t* fast,
-                                    const std::uint8_t* casc, std::uint32_t n_luts,
-                                    std::uint64_t lenpack, std::uint32_t* out) {
-  __shared__ std::uint32_t sw[8];
-  __shared__ std::uint32_t sfast[kFastEntries];
-  __shared__ std::uint8_t scasc[18 * 256];
-  for (int i = threadIdx.x; i < kFastEntries; i += blockDim.x) sfast[i] = fast[i];
-  for (int i = threadIdx.x; i < static_cast<int>(n_luts) * 256; i += blockDim.x) scasc[i] = casc[i];
-  if (threadIdx.x < 8) {
-    std::uint32_t v = 0;
-    for (int k = 0; k < 4; ++k) {
-      const int idx = 4 * threadIdx.x + k;
-      v = (v << 8) | (idx < 10 ? w16[idx] : 0u);  // only the 10 window bytes exist
-    }
-    sw[threadIdx.x] = v;
+                                    const std::uint16_t* smask, const std::uint8_t* casc,
+                                    std::uint32_t n_luts, std::uint32_t* out) {
+  __shared__ Tables tb;
+  for (int i = threadIdx.x; i < kFastEntries; i += blockDim.x) {
+    tb.fast[i] = fast[i];
+    tb.smask[i] = smask[i];
   }
+  for (int i = threadIdx.x; i < static_cast<int>(n_luts) * 256; i += blockDim.x) tb.cascade[i] = casc[i];
   __syncthreads();
-  if (threadIdx.x == 0) *out = count_window(sw, gap, 64, sfast, scasc, n_luts, lenpack);
+  if (threadIdx.x == 0) {
+    std::uint32_t w[4];
+    for (int k = 0; k < 4; ++k) {
+      std::uint32_t v = 0;
+      for (int j = 0; j < 4; ++j) {
+        const int idx = 4 * k + j;
+        v = (v << 8) | (idx < 10 ? w16[idx] : 0u);  // only the 10 window bytes exist
+      }
+      w[k] = v;
+    }
+    CountSink c;
+    decode_window(w[0], w[1], w[2], w[3], gap & 15u, tb, (n_luts - 1) << 8, c);
+    *out = c.n4 >> 2;
+  }
 }
 
 template <int KWIN>
 cudaError_t launch_k(const LaunchArgs& args, cudaStream_t s) {
-  const std::uint64_t total_tiles = args.total_tiles;
   static int grid_cap = 0;
   const int smem = static_cast<int>(sizeof(Smem<KWIN>));
   if (grid_cap == 0) {
@@ -318,7 +400,8 @@ cudaError_t launch_k(const LaunchArgs& args, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     grid_cap = sms * (per_sm > 0 ? per_sm : 1);
   }
-  const std::uint64_t grid = total_tiles < static_cast<std::uint64_t>(grid_cap) ? total_tiles : grid_cap;
+  const std::uint64_t total = args.total_tiles;
+  const std::uint64_t grid = total < static_cast<std::uint64_t>(grid_cap) ? total : grid_cap;
   if (grid == 0) return cudaSuccess;
   decode_kernel<KWIN><<<static_cast<unsigned>(grid), kThreads, smem, s>>>(args);
   return cudaGetLastError();
@@ -336,9 +419,9 @@ cudaError_t launch_decode(const LaunchArgs& args, int kwin, cudaStream_t stream)
 }
 
 cudaError_t launch_count_window(const std::uint8_t* d_window16, unsigned gap, const std::uint32_t* d_fast,
-                                const std::uint8_t* d_cascade, std::uint32_t n_luts,
-                                std::uint64_t lenpack, std::uint32_t* d_count, cudaStream_t stream) {
-  count_window_kernel<<<1, 128, 0, stream>>>(d_window16, gap, d_fast, d_cascade, n_luts, lenpack, d_count);
+                                const std::uint16_t* d_smask, const std::uint8_t* d_cascade,
+                                std::uint32_t n_luts, std::uint32_t* d_count, cudaStream_t stream) {
+  count_window_kernel<<<1, 128, 0, stream>>>(d_window16, gap, d_fast, d_smask, d_cascade, n_luts, d_count);
   return cudaGetLastError();
 }
 

@@ -16,6 +16,7 @@ struct TensorDesc {
   const std::uint64_t* outpos;
   const std::uint8_t* packed;
   const std::uint32_t* fast;     // tables.hpp fast table
+  const std::uint16_t* smask;    // tables.hpp start masks
   const std::uint8_t* cascade;   // reference cascade (slow path)
   std::uint8_t* out;             // element i lands at out[i - out_offset]
   std::uint64_t out_offset;      // multiple of 16
@@ -55,8 +56,8 @@ cudaError_t launch_decode(const LaunchArgs& args, int kwin, cudaStream_t stream)
 
 // count_phase on one window (window10 staged as 16 bytes in device memory).
 cudaError_t launch_count_window(const std::uint8_t* d_window16, unsigned gap,
-                                const std::uint32_t* d_fast, const std::uint8_t* d_cascade,
-                                std::uint32_t n_luts, std::uint64_t lenpack,
+                                const std::uint32_t* d_fast, const std::uint16_t* d_smask,
+                                const std::uint8_t* d_cascade, std::uint32_t n_luts,
                                 std::uint32_t* d_count, cudaStream_t stream);
 
 }  // namespace ecf8::dev

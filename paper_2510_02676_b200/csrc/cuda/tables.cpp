@@ -49,9 +49,10 @@ DecodeTables build_tables(const std::uint8_t lengths[16]) {
   }
 
   t.fast.resize(kFastEntries);
+  t.smask.resize(kFastEntries);
   for (std::uint32_t idx = 0; idx < static_cast<std::uint32_t>(kFastEntries); ++idx) {
     unsigned pos = 0, n = 0;
-    std::uint32_t syms = 0;
+    std::uint32_t syms = 0, starts = 0;
     while (n < kMaxPerEntry && pos < static_cast<unsigned>(kFastBits)) {
       const unsigned r = kFastBits - pos;            // visible bits left
       const std::uint32_t v = idx & ((1u << r) - 1);  // they are idx's low r bits
@@ -60,10 +61,12 @@ DecodeTables build_tables(const std::uint8_t lengths[16]) {
       const unsigned sym = st & 15, l = st >> 4;
       if (l == 0 || l > r) break;  // word runs past what the index shows
       syms |= sym << (4 * n);
+      starts |= 1u << pos;
       ++n;
       pos += l;
     }
-    t.fast[idx] = pos | (n << 5) | (syms << 8);
+    t.fast[idx] = pos | ((4 * n) << 5) | (syms << 12);
+    t.smask[idx] = static_cast<std::uint16_t>(starts);
   }
   return t;
 }

@@ -100,11 +100,12 @@ int ecf8_host_build_lut(const uint8_t lengths[16], uint8_t* entries, uint32_t* n
   });
 }
 
-int ecf8_host_device_tables(const uint8_t lengths[16], uint32_t* fast, uint8_t* cascade,
-                            uint32_t* n_luts, uint32_t* fast_bits) {
+int ecf8_host_device_tables(const uint8_t lengths[16], uint32_t* fast, uint16_t* smask,
+                            uint8_t* cascade, uint32_t* n_luts, uint32_t* fast_bits) {
   return guarded([&] {
     const ecf8::dev::DecodeTables t = ecf8::dev::build_tables(lengths);
     std::memcpy(fast, t.fast.data(), t.fast.size() * 4);
+    std::memcpy(smask, t.smask.data(), t.smask.size() * 2);
     std::memcpy(cascade, t.cascade.data(), t.cascade.size());
     *n_luts = t.n_luts;
     *fast_bits = ecf8::dev::kFastBits;

@@ -59,28 +59,33 @@ def length_sets():
 @pytest.mark.parametrize("case", range(46))
 def test_fast_entries_equal_cascade_walk(case):
     lengths = length_sets()[case]
-    fast, casc, n_luts, K = codec.device_tables(lengths)
+    fast, smask, casc, n_luts, K = codec.device_tables(lengths)
     assert fast.size == 1 << K
     rng = np.random.default_rng(case)
     idx = np.repeat(np.arange(1 << K, dtype=np.uint64), 8)
     tail = rng.integers(0, 1 << 62, idx.size, dtype=np.uint64) >> np.uint64(K - 2)
     stream = (idx << np.uint64(64 - K)) | tail
-    e = fast[idx.astype(np.int64)].astype(np.int64)
-    b, n, syms = e & 31, (e >> 5) & 7, e >> 8
+    ii = idx.astype(np.int64)
+    e = fast[ii].astype(np.int64)
+    b, n, syms = e & 31, ((e >> 5) & 31) // 4, e >> 12
+    assert np.all(((e >> 5) & 3) == 0) and np.all(n <= 5)
     pos = np.zeros(idx.size, np.int64)
+    starts = np.zeros(idx.size, np.int64)
     for i in range(6):
         live = n > i
         if not live.any():
             break
+        starts |= np.where(live, 1 << pos, 0)
         s, bits = cascade_walk(casc, n_luts, stream, pos)
         assert np.all(s[live] == ((syms[live] >> (4 * i)) & 15))
         pos = np.where(live, pos + bits, pos)
     assert np.all(pos == b)
     assert np.all(b <= K)
+    assert np.array_equal(smask[ii].astype(np.int64), starts)
 
 
-def count_model(fast, casc, n_luts, K, lenpack, window10, gap):
-    """numpy/Python model of decode.cu count_window on one window."""
+def count_model(fast, smask, casc, n_luts, K, window10, gap):
+    """Python model of decode.cu decode_window (count mode) on one window."""
     bits = np.unpackbits(np.concatenate([window10, np.zeros(8, np.uint8)]))
     stream = int("".join(map(str, bits)), 2)  # 144-bit integer
     nbits = bits.size
@@ -90,34 +95,32 @@ def count_model(fast, casc, n_luts, K, lenpack, window10, gap):
 
     p, c = gap, 0
     while True:
-        e = int(fast[peek(p, K)])
-        b, n = e & 31, (e >> 5) & 7
-        if n and p + b <= 64:
-            c, p = c + n, p + b
-        else:
-            if n:
-                sym = (e >> 8) & 15
-                ln = (lenpack >> (4 * sym)) & 15 or 16
-            else:
-                w = peek(p, 16)
-                v = int(casc[w >> 8])
-                if v >= 240:
-                    v = int(casc[(256 - v) * 256 + (w & 255)])
-                ln = int(casc[(n_luts - 1) * 256 + v])
-            c, p = c + 1, p + ln
-        if p >= 64:
-            return c
+        idx = peek(p, K)
+        e = int(fast[idx])
+        b, n = e & 31, ((e >> 5) & 31) // 4
+        if n == 0:  # reference cascade on 16 bits
+            w = peek(p, 16)
+            v = int(casc[w >> 8])
+            if v >= 240:
+                v = int(casc[(256 - v) * 256 + (w & 255)])
+            c, p = c + 1, p + int(casc[(n_luts - 1) * 256 + v])
+            if p >= 64:
+                return c
+            continue
+        r = 64 - p
+        if b >= r:
+            return c + bin(int(smask[idx]) & ((1 << r) - 1)).count("1")
+        c, p = c + n, p + b
 
 
 @pytest.mark.parametrize("case", range(0, 46, 3))
 def test_count_model_matches_oracle(orc, case):
     lengths = length_sets()[case]
-    fast, casc, n_luts, K = codec.device_tables(lengths)
-    lenpack = sum((int(lengths[s]) & 15) << (4 * s) for s in range(16))
+    fast, smask, casc, n_luts, K = codec.device_tables(lengths)
     rng = np.random.default_rng(100 + case)
     for _ in range(60):
         w = rng.integers(0, 256, 10, dtype=np.uint8)
         if rng.random() < 0.3:
             w[:] = 0
         g = int(rng.integers(0, 16))
-        assert count_model(fast, casc, n_luts, K, lenpack, w, g) == orc.count_phase(w, g, lengths)
+        assert count_model(fast, smask, casc, n_luts, K, w, g) == orc.count_phase(w, g, lengths)
