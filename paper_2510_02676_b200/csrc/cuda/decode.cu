@@ -5,24 +5,24 @@
 // emit_phase, staging copy).  The reference decodes every symbol twice
 // (count, then emit); this kernel decodes once:
 //
-//   * persistent CTAs, each owning a contiguous run of "tiles"; a tile is
-//     whole reference blocks covering 256 * KWIN windows (T <= 256: 256/T
-//     blocks, one window per thread; T = 512/1024: one block, 2/4 windows per
-//     thread), so a tile starts at an outpos[] boundary;
+//   * persistent CTAs (256 threads), each owning a contiguous run of tiles;
+//     a tile is 256 * KWIN consecutive 64-bit windows made of whole
+//     reference blocks, KWIN consecutive windows per thread inside one
+//     block, so a tile starts at an outpos[] boundary;
 //   * decode tables (tables.hpp) live in shared memory per tensor;
-//   * each thread pulls its window bits straight into registers (two 8-byte
-//     loads, coalesced across the warp) and walks them with a 64-bit register
-//     window, up to five symbols per table load; the symbols that start
-//     before the window's 64-bit boundary are taken exactly, the last entry
-//     partially via a start-bit mask + popcount (codec.cpp:143-160 rule);
-//     symbols are packed as nibbles into a private shared-memory slot;
-//   * a warp-shuffle + cross-warp scan of the per-thread counts, seeded by
-//     outpos[] per reference block, gives every thread its output offset;
+//   * each thread's window bits arrive in registers (8-byte loads, coalesced
+//     across the warp), prefetched one tile ahead; a 64-bit register window
+//     walks them with up to five symbols per table load; the symbols that
+//     start before the window's 64-bit boundary are taken exactly -- the last
+//     entry partially, via a start-bit mask and a popcount (the
+//     codec.cpp:143-160 rule); symbols are packed as nibbles into a private
+//     shared-memory slot;
+//   * a warp-shuffle scan plus a cross-warp prefix (one barrier), seeded by
+//     outpos[] per reference block, gives each thread its output offset;
 //     counts past a block's outpos limit are clamped (codec.cpp:239-246);
-//   * each thread copies its nibbles to their final place in a nibble
-//     staging tile (funnel shifts, whole words); words shared by
-//     neighbouring threads are assembled by one owner from published
-//     partial words -- no atomics;
+//   * each thread moves its nibbles to their final place in a nibble staging
+//     tile (funnel shifts, whole words); words shared with neighbours are
+//     assembled by one owner from published partial words -- no atomics;
 //   * write-back merges exponent nibbles with the sign/mantissa nibbles in
 //     SWAR form and stores 16 bytes per thread-step; tile edges are written
 //     byte-wise so neighbouring tiles never touch the same byte.
@@ -56,10 +56,13 @@ struct Smem {
   std::uint32_t rs[kThreads];
   std::uint32_t re[kThreads];
   std::uint32_t head[kThreads];
-  std::uint32_t excl[kThreads];
-  std::uint32_t blk[kThreads + 1];
-  std::uint32_t warp_sum[kWarps];
+  alignas(16) std::uint32_t warp_sum[kWarps];
 };
+
+template <int KWIN>
+constexpr int min_blocks_per_sm() {
+  return KWIN == 1 ? 4 : (KWIN == 2 ? 3 : 2);
+}
 
 // ---------------------------------------------------------------- sinks
 
@@ -87,11 +90,14 @@ struct CountSink {
   __device__ __forceinline__ void put(std::uint32_t, std::uint32_t k4) { n4 += k4; }
 };
 
-// The reference cascade (lut.hpp:43-49) on a 16-bit window: symbol.
-__device__ __forceinline__ std::uint32_t cascade_symbol(std::uint32_t w16, const Tables& tb) {
+// A fast-table-format entry for the word at the head of `hi`, decoded by
+// the reference cascade (lut.hpp:43-49): one symbol, its length as b.
+__device__ __forceinline__ std::uint32_t slow_entry(std::uint32_t hi, const Tables& tb,
+                                                    std::uint32_t len_off) {
+  const std::uint32_t w16 = hi >> 16;
   std::uint32_t v = tb.cascade[w16 >> 8];
   if (v >= 240) v = tb.cascade[((256u - v) << 8) | (w16 & 255u)];
-  return v;
+  return (v << 12) | (4u << 5) | tb.cascade[len_off + v];
 }
 
 // Decodes the words that start in [gap, 64) of one 64-bit window
@@ -104,49 +110,33 @@ __device__ __forceinline__ void decode_window(std::uint32_t w0, std::uint32_t w1
   std::uint32_t hi = __funnelshift_l(w1, w0, gap);
   std::uint32_t lo = __funnelshift_l(w2, w1, gap);
   std::uint32_t p = gap;
-  // Phase A: at least 32 valid bits remain in the register window.
+  // Phase A: at least 32 valid bits remain in the register window and the
+  // window boundary is out of reach of one entry.
   while (p < 32) {
-    const std::uint32_t e = tb.fast[hi >> kFastShift];
-    const std::uint32_t n4 = (e >> 5) & 31;
-    std::uint32_t adv;
-    if (n4) {
-      sink.put(e >> 12, n4);
-      adv = e & 31;
-    } else {
-      const std::uint32_t v = cascade_symbol(hi >> 16, tb);
-      sink.put(v, 4);
-      adv = tb.cascade[len_off + v];
-    }
-    hi = __funnelshift_l(lo, hi, adv);
-    lo = __funnelshift_l(0u, lo, adv);
-    p += adv;
+    std::uint32_t e = tb.fast[hi >> kFastShift];
+    if (((e >> 5) & 31) == 0) e = slow_entry(hi, tb, len_off);
+    sink.put(e >> 12, (e >> 5) & 31);
+    hi = __funnelshift_l(lo, hi, e);  // shift amount = e & 31 = bits consumed
+    lo = __funnelshift_l(0u, lo, e);
+    p += e & 31;
   }
-  // Refill once: p in [32, 48); window = bits [p, p + 64).
+  // Refill once: p in [32, 48); register window = bits [p, p + 64).
   hi = __funnelshift_l(w2, w1, p - 32);
   lo = __funnelshift_l(w3, w2, p - 32);
   for (;;) {
     const std::uint32_t idx = hi >> kFastShift;
-    const std::uint32_t e = tb.fast[idx];
-    const std::uint32_t n4 = (e >> 5) & 31;
-    const std::uint32_t r = 64 - p;  // bits left before the window boundary
-    if (n4 == 0) {
-      const std::uint32_t v = cascade_symbol(hi >> 16, tb);
-      sink.put(v, 4);
-      const std::uint32_t len = tb.cascade[len_off + v];
-      p += len;
-      if (p >= 64) break;
-      hi = __funnelshift_l(lo, hi, len);
-      lo = __funnelshift_l(0u, lo, len);
-      continue;
-    }
-    const std::uint32_t b = e & 31;
+    std::uint32_t e = tb.fast[idx];
+    const bool fast_hit = ((e >> 5) & 31) != 0;
+    if (!fast_hit) e = slow_entry(hi, tb, len_off);
+    const std::uint32_t b = e & 31, r = 64 - p;
     if (b >= r) {  // last entry: only the symbols that start before bit 64
-      const std::uint32_t k4 = 4 * __popc(tb.smask[idx] & ((1u << r) - 1));
+      const std::uint32_t starts = fast_hit ? tb.smask[idx] : 1u;
+      const std::uint32_t k4 = 4 * __popc(starts & ((1u << r) - 1));
       sink.put((e >> 12) & ((1u << k4) - 1), k4);
-      break;
+      return;
     }
-    sink.put(e >> 12, n4);
-    hi = __funnelshift_l(lo, hi, e);  // shift amount = e & 31 = b
+    sink.put(e >> 12, (e >> 5) & 31);
+    hi = __funnelshift_l(lo, hi, e);
     lo = __funnelshift_l(0u, lo, e);
     p += b;
   }
@@ -160,7 +150,7 @@ __device__ __forceinline__ std::uint32_t sel(std::uint32_t a, std::uint32_t b, s
 
 // Eight FP8 bytes from eight exponent nibbles S (element i at bits 4i..4i+3)
 // and four packed sign/mantissa bytes P (element 2j in the high nibble of
-// byte j): byte = sign << 7 | exponent << 3 | mantissa.
+// byte j): byte = sign << 7 | exponent << 3 | mantissa  (fp8.hpp assemble).
 __device__ __forceinline__ void merge8(std::uint32_t S, std::uint32_t P, std::uint32_t& o0,
                                        std::uint32_t& o1) {
   const std::uint32_t even = sel(sel(S << 3, P, 0x78787878u), P >> 4, 0xF8F8F8F8u);
@@ -169,14 +159,13 @@ __device__ __forceinline__ void merge8(std::uint32_t S, std::uint32_t P, std::ui
   o1 = __byte_perm(even, odd, 0x7362);
 }
 
-__device__ __forceinline__ std::uint8_t merge1(std::uint32_t x, std::uint32_t qb, std::uint64_t i) {
-  const std::uint32_t qh = (i & 1) ? (qb << 4) : qb;
+__device__ __forceinline__ std::uint8_t merge1(std::uint32_t x, std::uint32_t qb, std::uint32_t odd) {
+  const std::uint32_t qh = odd ? (qb << 4) : qb;
   return static_cast<std::uint8_t>((x << 3) | (qh & 0x80u) | ((qh >> 4) & 7u));
 }
 
-__device__ __forceinline__ std::uint32_t nib_mask(std::uint32_t lo_n, std::uint32_t hi_n) {
-  const std::uint32_t top = hi_n >= 8 ? 0xFFFFFFFFu : ((1u << (4 * hi_n)) - 1);
-  return top & ~((1u << (4 * lo_n)) - 1);
+__device__ __forceinline__ std::uint32_t low_nibbles(std::uint32_t n) {  // n in 1..8
+  return n >= 8 ? 0xFFFFFFFFu : ((1u << (4 * n)) - 1);
 }
 
 __device__ __forceinline__ int find_desc(const TensorDesc* descs, int n, std::uint64_t tile) {
@@ -189,8 +178,55 @@ __device__ __forceinline__ int find_desc(const TensorDesc* descs, int n, std::ui
   return lo;
 }
 
+// Everything a thread reads from HBM for one tile except the sign/mantissa
+// nibbles (read at write-back); loaded one tile ahead.
 template <int KWIN>
-__global__ void __launch_bounds__(kThreads) decode_kernel(const LaunchArgs args) {
+struct TileIn {
+  uint2 win[KWIN + 1];   // window bytes, little-endian words
+  std::uint32_t gaps;    // raw gap byte(s) covering my windows
+  std::uint64_t A, E;    // tile output range
+  std::uint64_t o0, o1;  // my reference block's output range
+  std::uint32_t nwin;    // windows in the tile
+  std::uint32_t nblk;
+};
+
+template <int KWIN>
+__device__ __forceinline__ void load_tile(const TensorDesc& d, std::uint64_t tile, int tid,
+                                          TileIn<KWIN>& in) {
+  const std::uint32_t T = d.T;
+  const std::uint32_t m = T >= 256u * KWIN ? 1u : 256u * KWIN / T;
+  const std::uint64_t b0 = d.blk_begin + (tile - d.tile_begin) * m;
+  in.nblk = static_cast<std::uint32_t>(d.blk_end - b0 < m ? d.blk_end - b0 : m);
+  in.nwin = in.nblk * T;
+  const std::uint64_t w0g = b0 * T;
+  in.A = __ldg(d.outpos + b0);
+  in.E = __ldg(d.outpos + b0 + in.nblk);
+  const std::uint32_t wl = static_cast<std::uint32_t>(tid) * KWIN;
+  if (wl < in.nwin) {
+    const uint2* src = reinterpret_cast<const uint2*>(d.encoded) + (w0g + wl);
+#pragma unroll
+    for (int i = 0; i <= KWIN; ++i) in.win[i] = __ldg(src + i);
+    if (KWIN == 1) in.gaps = __ldg(d.gaps + ((w0g + wl) >> 1));
+    else if (KWIN == 2) in.gaps = __ldg(d.gaps + (w0g >> 1) + tid);
+    else in.gaps = __ldg(reinterpret_cast<const std::uint16_t*>(d.gaps + (w0g >> 1)) + tid);
+    const std::uint32_t bl = wl / T;
+    in.o0 = __ldg(d.outpos + b0 + bl);
+    in.o1 = __ldg(d.outpos + b0 + bl + 1);
+  } else {
+    in.o0 = in.o1 = in.E;
+  }
+}
+
+template <int KWIN>
+__device__ __forceinline__ std::uint32_t gap_of(const TileIn<KWIN>& in, int i, std::uint32_t wl) {
+  if (KWIN == 1) return (in.gaps >> ((wl & 1) ? 0 : 4)) & 15u;
+  // byte j holds windows 2j (high nibble) and 2j + 1 (low nibble)
+  return (in.gaps >> (8 * (i >> 1) + ((i & 1) ? 0 : 4))) & 15u;
+}
+
+template <int KWIN>
+__global__ void __launch_bounds__(kThreads, min_blocks_per_sm<KWIN>())
+    decode_kernel(const LaunchArgs args) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem<KWIN>& sm = *reinterpret_cast<Smem<KWIN>*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -202,6 +238,9 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(const LaunchArgs args)
   std::uint64_t next_begin = 0;
   TensorDesc d;
   std::uint32_t len_off = 0;
+  TileIn<KWIN> nxt;
+  bool have_next = false;
+  std::uint32_t* const my_slot = sm.slot + tid * Smem<KWIN>::kSlotStride;
 
   for (std::uint64_t tile = t_lo; tile < t_hi; ++tile) {
     if (di < 0 || tile >= next_begin) {
@@ -214,6 +253,7 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(const LaunchArgs args)
         d = args.inline_desc;
         next_begin = total_tiles;
       }
+      have_next = false;
       __syncthreads();  // everyone is past the previous tile's decode
       const uint4* f4 = reinterpret_cast<const uint4*>(d.fast);
       uint4* sf4 = reinterpret_cast<uint4*>(sm.tb.fast);
@@ -225,29 +265,24 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(const LaunchArgs args)
       len_off = (d.n_luts - 1) << 8;
       __syncthreads();
     }
+    TileIn<KWIN> cur;
+    if (have_next) cur = nxt;
+    else load_tile(d, tile, tid, cur);
+    have_next = tile + 1 < t_hi && tile + 1 < next_begin;
+    if (have_next) load_tile(d, tile + 1, tid, nxt);
+
     const std::uint32_t T = d.T;
-    const std::uint32_t m = T >= 256 ? 1u : 256u / T;
-    const std::uint64_t b0 = d.blk_begin + (tile - d.tile_begin) * m;
-    const std::uint32_t nblk = static_cast<std::uint32_t>(d.blk_end - b0 < m ? d.blk_end - b0 : m);
-    const std::uint32_t nwin = nblk * T;
-    const std::uint64_t w0g = b0 * T;
-    const std::uint64_t A = __ldg(d.outpos + b0);
-    const std::uint64_t E = __ldg(d.outpos + b0 + nblk);
-    for (std::uint32_t i = tid; i <= nblk; i += kThreads)
-      sm.blk[i] = static_cast<std::uint32_t>(__ldg(d.outpos + b0 + i) - A);
+    const std::uint32_t wl0 = static_cast<std::uint32_t>(tid) * KWIN;
+    const bool active = wl0 < cur.nwin;
 
     // ---- decode my windows into my slot
-    std::uint32_t* const my_slot = sm.slot + tid * Smem<KWIN>::kSlotStride;
     SlotSink sink{my_slot};
+    if (active) {
 #pragma unroll
-    for (int i = 0; i < KWIN; ++i) {
-      const std::uint32_t wl = tid * KWIN + i;
-      if (wl < nwin) {
-        const std::uint64_t wg = w0g + wl;
-        const uint2 a = __ldg(reinterpret_cast<const uint2*>(d.encoded + 8 * wg));
-        const uint2 b = __ldg(reinterpret_cast<const uint2*>(d.encoded + 8 * wg + 8));
-        const std::uint32_t gap = (__ldg(d.gaps + (wg >> 1)) >> ((wg & 1) ? 0 : 4)) & 15u;
-        decode_window(bswap32(a.x), bswap32(a.y), bswap32(b.x), bswap32(b.y), gap, sm.tb, len_off, sink);
+      for (int i = 0; i < KWIN; ++i) {
+        if (wl0 + i < cur.nwin)
+          decode_window(bswap32(cur.win[i].x), bswap32(cur.win[i].y), bswap32(cur.win[i + 1].x),
+                        bswap32(cur.win[i + 1].y), gap_of<KWIN>(cur, i, wl0 + i), sm.tb, len_off, sink);
       }
     }
     if (sink.q4) *sink.ptr = sink.lo;
@@ -262,41 +297,55 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(const LaunchArgs args)
     }
     if (lane == 31) sm.warp_sum[warp] = incl;
     __syncthreads();
-    std::uint32_t excl = incl - cnt;
+    const uint4 s0 = *reinterpret_cast<const uint4*>(sm.warp_sum);
+    const uint4 s1 = *reinterpret_cast<const uint4*>(sm.warp_sum + 4);
+    const std::uint32_t ws[kWarps] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+    // threads per reference block; the block's first thread and its warp
+    const std::uint32_t tpb = T / KWIN;
+    const std::uint32_t first_tid = tpb >= kThreads ? 0u : (tid & ~(tpb - 1));
+    const std::uint32_t first_warp = first_tid >> 5;
+    std::uint32_t base = 0, first_base = 0;
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w) excl += (w < warp) ? sm.warp_sum[w] : 0u;
-    sm.excl[tid] = excl;
-    __syncthreads();
+    for (int w = 0; w < kWarps; ++w) {
+      base += (w < warp) ? ws[w] : 0u;
+      first_base += (static_cast<std::uint32_t>(w) < first_warp) ? ws[w] : 0u;
+    }
+    const std::uint32_t excl = base + incl - cnt;
+    const std::uint32_t in_warp_first = __shfl_sync(0xffffffffu, incl - cnt, first_tid & 31);
+    const std::uint32_t first_excl = first_base + (tpb < 32 ? in_warp_first : 0u);
 
     // ---- my output range, clamped to my reference block's outpos limit
-    const std::uint32_t bl = (T < 256) ? static_cast<std::uint32_t>(tid) / T : 0u;
-    const std::uint32_t first = (T < 256) ? sm.excl[bl * T] : 0u;
-    const std::uint32_t start_rel = sm.blk[bl] + excl - first;
-    const std::uint32_t lim_rel = sm.blk[bl + 1];
-    std::uint32_t cc = 0;
-    if (static_cast<std::uint32_t>(tid) * KWIN < nwin && start_rel < lim_rel)
-      cc = min(cnt, lim_rel - start_rel);
-    const std::uint32_t off = static_cast<std::uint32_t>(A & 15);  // staging nibble of element A
+    const std::uint32_t start_rel = static_cast<std::uint32_t>(cur.o0 - cur.A) + excl - first_excl;
+    const std::uint32_t lim_rel = static_cast<std::uint32_t>(cur.o1 - cur.A);
+    const std::uint32_t cc = (active && start_rel < lim_rel) ? min(cnt, lim_rel - start_rel) : 0u;
+    const std::uint32_t off = static_cast<std::uint32_t>(cur.A & 15);  // staging nibble of element A
     const std::uint32_t d0 = start_rel + off, dend = d0 + cc;
-    const std::uint32_t data_end = off + static_cast<std::uint32_t>(E - A);
+    const std::uint32_t data_end = off + static_cast<std::uint32_t>(cur.E - cur.A);
     sm.rs[tid] = d0;
     sm.re[tid] = dend;
 
-    // ---- copy my nibbles to their final place; publish partial words
+    // ---- move my nibbles to their final place; publish partial words
     std::uint32_t headv = 0, tailv = 0;
     const std::uint32_t fw = d0 >> 3, lw = (dend - 1) >> 3;
+    const std::uint32_t f4 = (d0 & 7) * 4, lastn = ((dend - 1) & 7) + 1;
     if (cc) {
-      const std::uint32_t f4 = (d0 & 7) * 4;
-      std::uint32_t prev = 0;
-      for (std::uint32_t k = fw; k <= lw; ++k) {
-        const std::uint32_t cur = my_slot[k - fw];
-        std::uint32_t v = __funnelshift_l(prev, cur, f4);
-        prev = cur;
-        const std::uint32_t lo_n = (k == fw) ? (d0 & 7) : 0u;
-        const std::uint32_t hi_n = (k == lw) ? ((dend - 1) & 7) + 1 : 8u;
-        v &= nib_mask(lo_n, hi_n);
-        if (lo_n == 0 && hi_n == 8) sm.stage[k] = v;
-        else if (k == fw) headv = v;
+      std::uint32_t prev = my_slot[0];
+      const std::uint32_t v0 = prev << f4;
+      if (fw == lw) {
+        const std::uint32_t v = v0 & low_nibbles(lastn);
+        if (f4 == 0 && lastn == 8) sm.stage[fw] = v;
+        else headv = v;
+      } else {
+        if (f4 == 0) sm.stage[fw] = v0;
+        else headv = v0;
+        std::uint32_t j = 1;
+        for (std::uint32_t k = fw + 1; k < lw; ++k, ++j) {
+          const std::uint32_t c = my_slot[j];
+          sm.stage[k] = __funnelshift_l(prev, c, f4);
+          prev = c;
+        }
+        const std::uint32_t v = __funnelshift_l(prev, my_slot[j], f4) & low_nibbles(lastn);
+        if (lastn == 8) sm.stage[lw] = v;
         else tailv = v;
       }
     }
@@ -305,26 +354,20 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(const LaunchArgs args)
 
     // ---- owners assemble words shared between threads
     if (cc) {
-      const bool starts_fw = ((d0 & 7) == 0) || (d0 == off);
-      const bool fw_full = ((d0 & 7) == 0) && (dend >= 8 * fw + 8);
+      const bool start_owner = (f4 == 0 || d0 == off) && !(f4 == 0 && (fw < lw || lastn == 8));
+      const bool tail_owner = fw != lw && lastn != 8;
 #pragma unroll
       for (int pass = 0; pass < 2; ++pass) {
-        std::uint32_t k, v;
-        if (pass == 0) {
-          if (!starts_fw || fw_full) continue;
-          k = fw;
-          v = headv;
-        } else {
-          if (lw == fw || (dend & 7) == 0) continue;
-          k = lw;
-          v = tailv;
-        }
+        if (pass == 0 ? !start_owner : !tail_owner) continue;
+        const std::uint32_t k = pass == 0 ? fw : lw;
+        std::uint32_t v = pass == 0 ? headv : tailv;
         const std::uint32_t wend = min(8 * k + 8, data_end);
         std::uint32_t covered = dend;
         for (int j = tid + 1; covered < wend && j < kThreads; ++j) {
-          if (sm.re[j] > sm.rs[j]) {
+          const std::uint32_t rj = sm.rs[j], ej = sm.re[j];
+          if (ej > rj) {
             v |= sm.head[j];
-            covered = sm.re[j];
+            covered = ej;
           }
         }
         sm.stage[k] = v;
@@ -334,25 +377,25 @@ __global__ void __launch_bounds__(kThreads) decode_kernel(const LaunchArgs args)
 
     // ---- write-back: exponent nibbles + sign/mantissa nibbles -> FP8 bytes
     {
-      const std::uint64_t S0 = A - off;
-      const std::uint32_t nchunk = (data_end + 15) >> 4;
-      std::uint8_t* out = d.out;
-      for (std::uint32_t ci = tid; ci < nchunk; ci += kThreads) {
-        const std::uint64_t g = S0 + 16ull * ci;
-        if (g >= A && g + 16 <= E) {
+      const std::uint64_t S0 = cur.A - off;
+      std::uint8_t* const out = d.out + (S0 - d.out_offset);
+      const std::uint8_t* const pk = d.packed + (S0 >> 1);
+      const std::uint32_t nch = (data_end + 15) >> 4;
+      for (std::uint32_t ci = tid; ci < nch; ci += kThreads) {
+        const std::uint32_t g = 16 * ci;
+        if (g >= off && g + 16 <= data_end) {
           const uint2 s = *reinterpret_cast<const uint2*>(sm.stage + 2 * ci);
-          const uint2 q = __ldg(reinterpret_cast<const uint2*>(d.packed + (g >> 1)));
+          const uint2 q = __ldg(reinterpret_cast<const uint2*>(pk + 8 * ci));
           uint4 r;
           merge8(s.x, q.x, r.x, r.y);
           merge8(s.y, q.y, r.z, r.w);
-          *reinterpret_cast<uint4*>(out + (g - d.out_offset)) = r;
+          *reinterpret_cast<uint4*>(out + g) = r;
         } else {
-          const std::uint64_t lo = g < A ? A : g;
-          const std::uint64_t hi = g + 16 < E ? g + 16 : E;
-          for (std::uint64_t i = lo; i < hi; ++i) {
-            const std::uint32_t nidx = static_cast<std::uint32_t>(i - S0);
-            const std::uint32_t x = (sm.stage[nidx >> 3] >> (4 * (nidx & 7))) & 15u;
-            out[i - d.out_offset] = merge1(x, d.packed[i >> 1], i);
+          const std::uint32_t lo = g < off ? off : g;
+          const std::uint32_t hi = g + 16 < data_end ? g + 16 : data_end;
+          for (std::uint32_t i = lo; i < hi; ++i) {
+            const std::uint32_t x = (sm.stage[i >> 3] >> (4 * (i & 7))) & 15u;
+            out[i] = merge1(x, pk[i >> 1], i & 1);
           }
         }
       }

@@ -32,12 +32,17 @@ struct TensorDesc {
 constexpr int kThreads = 256;
 constexpr std::uint64_t kPad = 64;
 
-// Windows per thread the launch is compiled for: T <= 256 -> 1, 512 -> 2,
-// 1024 -> 4.
-inline int windows_per_thread(std::uint32_t T) { return T <= 256 ? 1 : static_cast<int>(T / 256); }
+// Windows per thread (consecutive, always inside one reference block):
+// T = 1 -> 1, T = 2..512 -> 2, T = 1024 -> 4.  A tile is 256 * KWIN windows.
+inline int windows_per_thread(std::uint32_t T) { return T == 1 ? 1 : (T <= 512 ? 2 : 4); }
+
+inline std::uint64_t blocks_per_tile(std::uint32_t T) {
+  const std::uint64_t w = 256ull * windows_per_thread(T);
+  return T >= w ? 1 : w / T;
+}
 
 inline std::uint64_t tiles_of(std::uint32_t T, std::uint64_t n_blocks) {
-  const std::uint64_t m = T >= 256 ? 1 : 256 / T;  // blocks per tile
+  const std::uint64_t m = blocks_per_tile(T);
   return (n_blocks + m - 1) / m;
 }
 
