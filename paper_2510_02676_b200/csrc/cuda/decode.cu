@@ -5,21 +5,23 @@
 // emit_phase, staging copy).  The reference decodes every symbol twice
 // (count, then emit); this kernel decodes once:
 //
-//   * persistent CTAs (256 threads), each owning a contiguous run of tiles;
-//     a tile is 256 * KWIN consecutive 64-bit windows made of whole
-//     reference blocks, KWIN consecutive windows per thread inside one
+//   * persistent CTAs of kThreads (512) threads, each owning a contiguous run
+//     of tiles; a tile is kThreads * KWIN consecutive 64-bit windows made of
+//     whole reference blocks, KWIN consecutive windows per thread inside one
 //     block, so a tile starts at an outpos[] boundary;
 //   * decode tables (tables.hpp) live in shared memory per tensor;
 //   * each thread's window bits arrive in registers (8-byte loads, coalesced
-//     across the warp), prefetched one tile ahead; a 64-bit register window
-//     walks them with up to five symbols per table load; the symbols that
-//     start before the window's 64-bit boundary are taken exactly -- the last
-//     entry partially, via a start-bit mask and a popcount (the
-//     codec.cpp:143-160 rule); symbols are packed as nibbles into a private
-//     shared-memory slot;
-//   * a warp-shuffle scan plus a cross-warp prefix (one barrier), seeded by
-//     outpos[] per reference block, gives each thread its output offset;
-//     counts past a block's outpos limit are clamped (codec.cpp:239-246);
+//     across the warp), prefetched one tile ahead, and the tile's
+//     sign/mantissa bytes are pulled into L2 by one bulk (TMA) prefetch; a
+//     64-bit register window walks the bits with up to five symbols per table
+//     load; the symbols that start before the window's 64-bit boundary are
+//     taken exactly -- the last entry partially, via a start-bit mask and a
+//     popcount (the codec.cpp:143-160 rule); symbols are packed as nibbles
+//     into a private shared-memory slot;
+//   * a warp-shuffle scan plus a lane-parallel cross-warp prefix (one
+//     barrier), seeded by outpos[] per reference block, gives each thread its
+//     output offset; counts past a block's outpos limit are clamped
+//     (codec.cpp:239-246);
 //   * each thread moves its nibbles to their final place in a nibble staging
 //     tile (funnel shifts, whole words); words shared with neighbours are
 //     assembled by one owner from published partial words -- no atomics;
@@ -56,12 +58,13 @@ struct Smem {
   std::uint32_t rs[kThreads];
   std::uint32_t re[kThreads];
   std::uint32_t head[kThreads];
-  alignas(16) std::uint32_t warp_sum[kWarps];
+  std::uint64_t blk[2][kThreads + 1];  // outpos[b0 .. b0 + nblk], by tile parity
+  std::uint32_t warp_sum[kWarps];
 };
 
 template <int KWIN>
 constexpr int min_blocks_per_sm() {
-  return KWIN == 1 ? 4 : (KWIN == 2 ? 3 : 2);
+  return KWIN == 4 ? 1 : 2;
 }
 
 // ---------------------------------------------------------------- sinks
@@ -178,50 +181,51 @@ __device__ __forceinline__ int find_desc(const TensorDesc* descs, int n, std::ui
   return lo;
 }
 
-// Everything a thread reads from HBM for one tile except the sign/mantissa
-// nibbles (read at write-back); loaded one tile ahead.
-template <int KWIN>
-struct TileIn {
-  uint2 win[KWIN + 1];   // window bytes, little-endian words
-  std::uint32_t gaps;    // raw gap byte(s) covering my windows
-  std::uint64_t A, E;    // tile output range
-  std::uint64_t o0, o1;  // my reference block's output range
-  std::uint32_t nwin;    // windows in the tile
-  std::uint32_t nblk;
+// Tile geometry (uniform across the CTA).
+struct TileGeo {
+  std::uint64_t b0;    // first reference block
+  std::uint32_t nblk;  // blocks in the tile
+  std::uint32_t nwin;  // windows in the tile
 };
 
 template <int KWIN>
-__device__ __forceinline__ void load_tile(const TensorDesc& d, std::uint64_t tile, int tid,
-                                          TileIn<KWIN>& in) {
-  const std::uint32_t T = d.T;
-  const std::uint32_t m = T >= 256u * KWIN ? 1u : 256u * KWIN / T;
-  const std::uint64_t b0 = d.blk_begin + (tile - d.tile_begin) * m;
-  in.nblk = static_cast<std::uint32_t>(d.blk_end - b0 < m ? d.blk_end - b0 : m);
-  in.nwin = in.nblk * T;
-  const std::uint64_t w0g = b0 * T;
-  in.A = __ldg(d.outpos + b0);
-  in.E = __ldg(d.outpos + b0 + in.nblk);
+__device__ __forceinline__ TileGeo tile_geo(const TensorDesc& d, std::uint64_t tile, std::uint32_t log2T) {
+  constexpr std::uint32_t kTileWin = static_cast<std::uint32_t>(kThreads) * KWIN;
+  const std::uint32_t m = d.T >= kTileWin ? 1u : (kTileWin >> log2T);
+  TileGeo g;
+  g.b0 = d.blk_begin + (tile - d.tile_begin) * m;
+  g.nblk = static_cast<std::uint32_t>(d.blk_end - g.b0 < m ? d.blk_end - g.b0 : m);
+  g.nwin = g.nblk << log2T;
+  return g;
+}
+
+// Bitstream words and gaps of one thread's windows; loaded a tile ahead.
+template <int KWIN>
+struct TileIn {
+  uint2 win[KWIN + 1];  // window bytes, little-endian words
+  std::uint32_t gaps;   // raw gap byte(s) covering my windows
+};
+
+template <int KWIN>
+__device__ __forceinline__ void load_tile(const TensorDesc& d, const TileGeo& g, std::uint32_t log2T,
+                                          int tid, TileIn<KWIN>& in) {
   const std::uint32_t wl = static_cast<std::uint32_t>(tid) * KWIN;
-  if (wl < in.nwin) {
+  if (wl < g.nwin) {
+    const std::uint64_t w0g = g.b0 << log2T;
     const uint2* src = reinterpret_cast<const uint2*>(d.encoded) + (w0g + wl);
 #pragma unroll
     for (int i = 0; i <= KWIN; ++i) in.win[i] = __ldg(src + i);
     if (KWIN == 1) in.gaps = __ldg(d.gaps + ((w0g + wl) >> 1));
     else if (KWIN == 2) in.gaps = __ldg(d.gaps + (w0g >> 1) + tid);
     else in.gaps = __ldg(reinterpret_cast<const std::uint16_t*>(d.gaps + (w0g >> 1)) + tid);
-    const std::uint32_t bl = wl / T;
-    in.o0 = __ldg(d.outpos + b0 + bl);
-    in.o1 = __ldg(d.outpos + b0 + bl + 1);
-  } else {
-    in.o0 = in.o1 = in.E;
   }
 }
 
 template <int KWIN>
-__device__ __forceinline__ std::uint32_t gap_of(const TileIn<KWIN>& in, int i, std::uint32_t wl) {
-  if (KWIN == 1) return (in.gaps >> ((wl & 1) ? 0 : 4)) & 15u;
+__device__ __forceinline__ std::uint32_t gap_of(std::uint32_t gaps, int i, std::uint32_t wl) {
+  if (KWIN == 1) return (gaps >> ((wl & 1) ? 0 : 4)) & 15u;
   // byte j holds windows 2j (high nibble) and 2j + 1 (low nibble)
-  return (in.gaps >> (8 * (i >> 1) + ((i & 1) ? 0 : 4))) & 15u;
+  return (gaps >> (8 * (i >> 1) + ((i & 1) ? 0 : 4))) & 15u;
 }
 
 template <int KWIN>
@@ -237,12 +241,14 @@ __global__ void __launch_bounds__(kThreads, min_blocks_per_sm<KWIN>())
   int di = -1;
   std::uint64_t next_begin = 0;
   TensorDesc d;
-  std::uint32_t len_off = 0;
+  std::uint32_t len_off = 0, log2T = 0;
   TileIn<KWIN> nxt;
   bool have_next = false;
   std::uint32_t* const my_slot = sm.slot + tid * Smem<KWIN>::kSlotStride;
+  std::uint32_t parity = 0;
+  std::uint64_t nA = 0, nE = 0;  // thread 0: outpos bounds of the prefetched tile
 
-  for (std::uint64_t tile = t_lo; tile < t_hi; ++tile) {
+  for (std::uint64_t tile = t_lo; tile < t_hi; ++tile, parity ^= 1) {
     if (di < 0 || tile >= next_begin) {
       if (args.descs) {
         di = find_desc(args.descs, args.n_desc, tile);
@@ -253,6 +259,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks_per_sm<KWIN>())
         d = args.inline_desc;
         next_begin = total_tiles;
       }
+      log2T = 31 - __clz(d.T);
       have_next = false;
       __syncthreads();  // everyone is past the previous tile's decode
       const uint4* f4 = reinterpret_cast<const uint4*>(d.fast);
@@ -265,24 +272,48 @@ __global__ void __launch_bounds__(kThreads, min_blocks_per_sm<KWIN>())
       len_off = (d.n_luts - 1) << 8;
       __syncthreads();
     }
+    const TileGeo g = tile_geo<KWIN>(d, tile, log2T);
     TileIn<KWIN> cur;
     if (have_next) cur = nxt;
-    else load_tile(d, tile, tid, cur);
+    else load_tile<KWIN>(d, g, log2T, tid, cur);
+    // outpos[b0 .. b0 + nblk] for this tile (read after the scan barrier)
+    std::uint64_t* const blk = sm.blk[parity];
+    for (std::uint32_t i = tid; i <= g.nblk; i += kThreads) blk[i] = __ldg(d.outpos + g.b0 + i);
+    if (tid == 0) {
+      // The tile's sign/mantissa nibbles are needed only at write-back: pull
+      // them into L2 now with one bulk (TMA) prefetch.  The tile's outpos
+      // bounds were fetched a tile ahead.
+      if (!have_next) {
+        nA = __ldg(d.outpos + g.b0);
+        nE = __ldg(d.outpos + g.b0 + g.nblk);
+      }
+      const std::uint64_t p0 = (nA >> 1) & ~std::uint64_t{15};
+      const std::uint32_t bytes = static_cast<std::uint32_t>((((nE + 1) >> 1) - p0 + 15) & ~std::uint64_t{15});
+      if (bytes)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(d.packed + p0), "r"(bytes) : "memory");
+    }
     have_next = tile + 1 < t_hi && tile + 1 < next_begin;
-    if (have_next) load_tile(d, tile + 1, tid, nxt);
+    if (have_next) {
+      const TileGeo g1 = tile_geo<KWIN>(d, tile + 1, log2T);
+      load_tile<KWIN>(d, g1, log2T, tid, nxt);
+      if (tid == 0) {
+        nA = __ldg(d.outpos + g1.b0);
+        nE = __ldg(d.outpos + g1.b0 + g1.nblk);
+      }
+    }
 
-    const std::uint32_t T = d.T;
     const std::uint32_t wl0 = static_cast<std::uint32_t>(tid) * KWIN;
-    const bool active = wl0 < cur.nwin;
+    const bool active = wl0 < g.nwin;
 
     // ---- decode my windows into my slot
     SlotSink sink{my_slot};
     if (active) {
 #pragma unroll
       for (int i = 0; i < KWIN; ++i) {
-        if (wl0 + i < cur.nwin)
+        if (wl0 + i < g.nwin)
           decode_window(bswap32(cur.win[i].x), bswap32(cur.win[i].y), bswap32(cur.win[i + 1].x),
-                        bswap32(cur.win[i + 1].y), gap_of<KWIN>(cur, i, wl0 + i), sm.tb, len_off, sink);
+                        bswap32(cur.win[i + 1].y), gap_of<KWIN>(cur.gaps, i, wl0 + i), sm.tb, len_off,
+                        sink);
       }
     }
     if (sink.q4) *sink.ptr = sink.lo;
@@ -297,30 +328,34 @@ __global__ void __launch_bounds__(kThreads, min_blocks_per_sm<KWIN>())
     }
     if (lane == 31) sm.warp_sum[warp] = incl;
     __syncthreads();
-    const uint4 s0 = *reinterpret_cast<const uint4*>(sm.warp_sum);
-    const uint4 s1 = *reinterpret_cast<const uint4*>(sm.warp_sum + 4);
-    const std::uint32_t ws[kWarps] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
-    // threads per reference block; the block's first thread and its warp
-    const std::uint32_t tpb = T / KWIN;
-    const std::uint32_t first_tid = tpb >= kThreads ? 0u : (tid & ~(tpb - 1));
-    const std::uint32_t first_warp = first_tid >> 5;
-    std::uint32_t base = 0, first_base = 0;
+    // lane-parallel exclusive prefix of the warp sums
+    const std::uint32_t wsum = lane < kWarps ? sm.warp_sum[lane] : 0u;
+    std::uint32_t wincl = wsum;
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w) {
-      base += (w < warp) ? ws[w] : 0u;
-      first_base += (static_cast<std::uint32_t>(w) < first_warp) ? ws[w] : 0u;
+    for (int o = 1; o < kWarps; o <<= 1) {
+      const std::uint32_t y = __shfl_up_sync(0xffffffffu, wincl, o);
+      if (lane >= o) wincl += y;
     }
-    const std::uint32_t excl = base + incl - cnt;
-    const std::uint32_t in_warp_first = __shfl_sync(0xffffffffu, incl - cnt, first_tid & 31);
-    const std::uint32_t first_excl = first_base + (tpb < 32 ? in_warp_first : 0u);
+    const std::uint32_t wexcl = wincl - wsum;
+    // the first thread of my reference block (threads per block is a power of 2)
+    const std::uint32_t log2tpb = log2T >= static_cast<std::uint32_t>(__ffs(KWIN) - 1) ? log2T - (__ffs(KWIN) - 1) : 0u;
+    const std::uint32_t first_tid = log2tpb >= 31 ? 0u : (static_cast<std::uint32_t>(tid) & ~((1u << log2tpb) - 1));
+    const std::uint32_t lexcl = incl - cnt;
+    const std::uint32_t excl = __shfl_sync(0xffffffffu, wexcl, warp) + lexcl;
+    const std::uint32_t first_excl = __shfl_sync(0xffffffffu, wexcl, (first_tid >> 5) & 31) +
+                                     __shfl_sync(0xffffffffu, lexcl, first_tid & 31) *
+                                         ((first_tid >> 5) == static_cast<std::uint32_t>(warp) ? 1u : 0u);
 
     // ---- my output range, clamped to my reference block's outpos limit
-    const std::uint32_t start_rel = static_cast<std::uint32_t>(cur.o0 - cur.A) + excl - first_excl;
-    const std::uint32_t lim_rel = static_cast<std::uint32_t>(cur.o1 - cur.A);
+    const std::uint64_t A = blk[0];
+    const std::uint32_t bl = wl0 >> log2T;
+    const std::uint32_t bl_c = bl < g.nblk ? bl : g.nblk - 1;
+    const std::uint32_t start_rel = static_cast<std::uint32_t>(blk[bl_c] - A) + excl - first_excl;
+    const std::uint32_t lim_rel = static_cast<std::uint32_t>(blk[bl_c + 1] - A);
     const std::uint32_t cc = (active && start_rel < lim_rel) ? min(cnt, lim_rel - start_rel) : 0u;
-    const std::uint32_t off = static_cast<std::uint32_t>(cur.A & 15);  // staging nibble of element A
+    const std::uint32_t off = static_cast<std::uint32_t>(A & 15);  // staging nibble of element A
     const std::uint32_t d0 = start_rel + off, dend = d0 + cc;
-    const std::uint32_t data_end = off + static_cast<std::uint32_t>(cur.E - cur.A);
+    const std::uint32_t data_end = off + static_cast<std::uint32_t>(blk[g.nblk] - A);
     sm.rs[tid] = d0;
     sm.re[tid] = dend;
 
@@ -356,41 +391,51 @@ __global__ void __launch_bounds__(kThreads, min_blocks_per_sm<KWIN>())
     if (cc) {
       const bool start_owner = (f4 == 0 || d0 == off) && !(f4 == 0 && (fw < lw || lastn == 8));
       const bool tail_owner = fw != lw && lastn != 8;
+      if (start_owner || tail_owner) {
 #pragma unroll
-      for (int pass = 0; pass < 2; ++pass) {
-        if (pass == 0 ? !start_owner : !tail_owner) continue;
-        const std::uint32_t k = pass == 0 ? fw : lw;
-        std::uint32_t v = pass == 0 ? headv : tailv;
-        const std::uint32_t wend = min(8 * k + 8, data_end);
-        std::uint32_t covered = dend;
-        for (int j = tid + 1; covered < wend && j < kThreads; ++j) {
-          const std::uint32_t rj = sm.rs[j], ej = sm.re[j];
-          if (ej > rj) {
-            v |= sm.head[j];
-            covered = ej;
+        for (int pass = 0; pass < 2; ++pass) {
+          if (pass == 0 ? !start_owner : !tail_owner) continue;
+          const std::uint32_t k = pass == 0 ? fw : lw;
+          std::uint32_t v = pass == 0 ? headv : tailv;
+          const std::uint32_t wend = min(8 * k + 8, data_end);
+          std::uint32_t covered = dend;
+          for (int j = tid + 1; covered < wend && j < kThreads; ++j) {
+            const std::uint32_t rj = sm.rs[j], ej = sm.re[j];
+            if (ej > rj) {
+              v |= sm.head[j];
+              covered = ej;
+            }
           }
+          sm.stage[k] = v;
         }
-        sm.stage[k] = v;
       }
     }
     __syncthreads();
 
     // ---- write-back: exponent nibbles + sign/mantissa nibbles -> FP8 bytes
     {
-      const std::uint64_t S0 = cur.A - off;
+      const std::uint64_t S0 = A - off;
       std::uint8_t* const out = d.out + (S0 - d.out_offset);
       const std::uint8_t* const pk = d.packed + (S0 >> 1);
       const std::uint32_t nch = (data_end + 15) >> 4;
-      for (std::uint32_t ci = tid; ci < nch; ci += kThreads) {
-        const std::uint32_t g = 16 * ci;
-        if (g >= off && g + 16 <= data_end) {
-          const uint2 s = *reinterpret_cast<const uint2*>(sm.stage + 2 * ci);
-          const uint2 q = __ldg(reinterpret_cast<const uint2*>(pk + 8 * ci));
-          uint4 r;
-          merge8(s.x, q.x, r.x, r.y);
-          merge8(s.y, q.y, r.z, r.w);
-          *reinterpret_cast<uint4*>(out + g) = r;
-        } else {
+      const std::uint32_t full_lo = (off + 15) >> 4, full_hi = data_end >> 4;  // full chunks [lo, hi)
+      const uint2* sp = reinterpret_cast<const uint2*>(sm.stage);
+      const uint2* pp = reinterpret_cast<const uint2*>(pk);
+      uint4* op = reinterpret_cast<uint4*>(out);
+      for (std::uint32_t ci = full_lo + tid; ci < full_hi; ci += kThreads) {
+        const uint2 s = sp[ci];
+        const uint2 q = __ldg(pp + ci);
+        uint4 r;
+        merge8(s.x, q.x, r.x, r.y);
+        merge8(s.y, q.y, r.z, r.w);
+        op[ci] = r;
+      }
+      // partial edge chunks (at most two), byte-wise
+      if (tid < 2) {
+        const std::uint32_t ci = tid == 0 ? 0u : nch - 1;
+        const bool partial = tid == 0 ? (full_lo > 0 && nch > 0) : (full_hi < nch && !(nch == 1 && full_lo > 0));
+        if (partial) {
+          const std::uint32_t g = 16 * ci;
           const std::uint32_t lo = g < off ? off : g;
           const std::uint32_t hi = g + 16 < data_end ? g + 16 : data_end;
           for (std::uint32_t i = lo; i < hi; ++i) {

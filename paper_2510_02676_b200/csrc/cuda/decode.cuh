@@ -29,15 +29,16 @@ struct TensorDesc {
   std::uint32_t n_luts;
 };
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 512;
 constexpr std::uint64_t kPad = 64;
 
 // Windows per thread (consecutive, always inside one reference block):
-// T = 1 -> 1, T = 2..512 -> 2, T = 1024 -> 4.  A tile is 256 * KWIN windows.
+// T = 1 -> 1, T = 2..512 -> 2, T = 1024 -> 4.  A tile is kThreads * KWIN
+// windows.
 inline int windows_per_thread(std::uint32_t T) { return T == 1 ? 1 : (T <= 512 ? 2 : 4); }
 
 inline std::uint64_t blocks_per_tile(std::uint32_t T) {
-  const std::uint64_t w = 256ull * windows_per_thread(T);
+  const std::uint64_t w = static_cast<std::uint64_t>(kThreads) * windows_per_thread(T);
   return T >= w ? 1 : w / T;
 }
 
