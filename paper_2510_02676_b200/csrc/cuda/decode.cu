@@ -5,11 +5,13 @@
 // emit_phase, staging copy).  The reference decodes every symbol twice
 // (count, then emit); this kernel decodes once:
 //
-//   * persistent CTAs of kThreads (512) threads, each owning a contiguous run
-//     of tiles; a tile is kThreads * KWIN consecutive 64-bit windows made of
-//     whole reference blocks, KWIN consecutive windows per thread inside one
+//   * persistent CTAs (one per SM) made of GROUPS independent tile groups of
+//     256 threads; the groups share one shared-memory copy of the decode
+//     tables (tables.hpp) and synchronise only with their own named barrier,
+//     so one group's barrier wait is covered by the others' work;
+//   * a tile is 256 * KWIN consecutive 64-bit windows made of whole
+//     reference blocks, KWIN consecutive windows per thread inside one
 //     block, so a tile starts at an outpos[] boundary;
-//   * decode tables (tables.hpp) live in shared memory per tensor;
 //   * each thread's window bits arrive in registers (8-byte loads, coalesced
 //     across the warp), prefetched one tile ahead, and the tile's
 //     sign/mantissa bytes are pulled into L2 by one bulk (TMA) prefetch; a
@@ -26,8 +28,9 @@
 //     tile (funnel shifts, whole words); words shared with neighbours are
 //     assembled by one owner from published partial words -- no atomics;
 //   * write-back merges exponent nibbles with the sign/mantissa nibbles in
-//     SWAR form and stores 16 bytes per thread-step; tile edges are written
-//     byte-wise so neighbouring tiles never touch the same byte.
+//     SWAR form and stores 16 bytes per thread-step (loads batched four
+//     chunks deep); tile edges are written byte-wise so neighbouring tiles
+//     never touch the same byte.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -39,7 +42,7 @@ namespace ecf8::dev {
 
 namespace {
 
-constexpr int kWarps = kThreads / 32;
+constexpr int kWarps = kThreads / 32;  // warps per group
 constexpr int kFastShift = 32 - kFastBits;
 
 struct Tables {
@@ -49,10 +52,9 @@ struct Tables {
 };
 
 template <int KWIN>
-struct Smem {
+struct GroupSmem {
   static constexpr int kSlotStride = KWIN * 8 + 1;             // words; odd => no bank conflicts
   static constexpr int kStageWords = KWIN * kThreads * 8 + 8;  // tile nibbles + 16-nibble slack
-  Tables tb;
   std::uint32_t slot[kThreads * kSlotStride];
   alignas(16) std::uint32_t stage[kStageWords];
   std::uint32_t rs[kThreads];
@@ -62,9 +64,19 @@ struct Smem {
   std::uint32_t warp_sum[kWarps];
 };
 
+template <int KWIN, int GROUPS>
+struct Smem {
+  Tables tb;
+  GroupSmem<KWIN> g[GROUPS];
+};
+
 template <int KWIN>
-constexpr int min_blocks_per_sm() {
-  return KWIN == 4 ? 1 : 2;
+constexpr int groups_for() {
+  return KWIN == 4 ? 2 : 4;
+}
+
+__device__ __forceinline__ void group_sync(int group) {
+  asm volatile("bar.sync %0, %1;" ::"r"(group + 1), "r"(kThreads) : "memory");
 }
 
 // ---------------------------------------------------------------- sinks
@@ -181,7 +193,7 @@ __device__ __forceinline__ int find_desc(const TensorDesc* descs, int n, std::ui
   return lo;
 }
 
-// Tile geometry (uniform across the CTA).
+// Tile geometry (uniform across a group).
 struct TileGeo {
   std::uint64_t b0;    // first reference block
   std::uint32_t nblk;  // blocks in the tile
@@ -228,223 +240,243 @@ __device__ __forceinline__ std::uint32_t gap_of(std::uint32_t gaps, int i, std::
   return (gaps >> (8 * (i >> 1) + ((i & 1) ? 0 : 4))) & 15u;
 }
 
+// One group decodes one tile: windows -> slots -> scan -> staging -> HBM.
 template <int KWIN>
-__global__ void __launch_bounds__(kThreads, min_blocks_per_sm<KWIN>())
-    decode_kernel(const LaunchArgs args) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  Smem<KWIN>& sm = *reinterpret_cast<Smem<KWIN>*>(smem_raw);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const std::uint64_t total_tiles = args.total_tiles;
+__device__ __forceinline__ void decode_tile(const TensorDesc& d, const TileGeo& g, const TileIn<KWIN>& cur,
+                                            const std::uint64_t* blk, const Tables& tb,
+                                            GroupSmem<KWIN>& gs, std::uint32_t log2T,
+                                            std::uint32_t len_off, int group, int tid) {
+  const int lane = tid & 31, warp = tid >> 5;
+  std::uint32_t* const my_slot = gs.slot + tid * GroupSmem<KWIN>::kSlotStride;
+  const std::uint32_t wl0 = static_cast<std::uint32_t>(tid) * KWIN;
+  const bool active = wl0 < g.nwin;
 
-  const std::uint64_t t_lo = total_tiles * blockIdx.x / gridDim.x;
-  const std::uint64_t t_hi = total_tiles * (blockIdx.x + 1) / gridDim.x;
-  int di = -1;
-  std::uint64_t next_begin = 0;
-  TensorDesc d;
-  std::uint32_t len_off = 0, log2T = 0;
-  TileIn<KWIN> nxt;
-  bool have_next = false;
-  std::uint32_t* const my_slot = sm.slot + tid * Smem<KWIN>::kSlotStride;
-  std::uint32_t parity = 0;
-  std::uint64_t nA = 0, nE = 0;  // thread 0: outpos bounds of the prefetched tile
-
-  for (std::uint64_t tile = t_lo; tile < t_hi; ++tile, parity ^= 1) {
-    if (di < 0 || tile >= next_begin) {
-      if (args.descs) {
-        di = find_desc(args.descs, args.n_desc, tile);
-        d = args.descs[di];
-        next_begin = (di + 1 < args.n_desc) ? args.descs[di + 1].tile_begin : total_tiles;
-      } else {
-        di = 0;
-        d = args.inline_desc;
-        next_begin = total_tiles;
-      }
-      log2T = 31 - __clz(d.T);
-      have_next = false;
-      __syncthreads();  // everyone is past the previous tile's decode
-      const uint4* f4 = reinterpret_cast<const uint4*>(d.fast);
-      uint4* sf4 = reinterpret_cast<uint4*>(sm.tb.fast);
-      for (int i = tid; i < kFastEntries / 4; i += kThreads) sf4[i] = __ldg(f4 + i);
-      const uint4* m4 = reinterpret_cast<const uint4*>(d.smask);
-      uint4* sm4 = reinterpret_cast<uint4*>(sm.tb.smask);
-      for (int i = tid; i < kFastEntries / 8; i += kThreads) sm4[i] = __ldg(m4 + i);
-      for (int i = tid; i < static_cast<int>(d.n_luts) * 256; i += kThreads) sm.tb.cascade[i] = d.cascade[i];
-      len_off = (d.n_luts - 1) << 8;
-      __syncthreads();
-    }
-    const TileGeo g = tile_geo<KWIN>(d, tile, log2T);
-    TileIn<KWIN> cur;
-    if (have_next) cur = nxt;
-    else load_tile<KWIN>(d, g, log2T, tid, cur);
-    // outpos[b0 .. b0 + nblk] for this tile (read after the scan barrier)
-    std::uint64_t* const blk = sm.blk[parity];
-    for (std::uint32_t i = tid; i <= g.nblk; i += kThreads) blk[i] = __ldg(d.outpos + g.b0 + i);
-    if (tid == 0) {
-      // The tile's sign/mantissa nibbles are needed only at write-back: pull
-      // them into L2 now with one bulk (TMA) prefetch.  The tile's outpos
-      // bounds were fetched a tile ahead.
-      if (!have_next) {
-        nA = __ldg(d.outpos + g.b0);
-        nE = __ldg(d.outpos + g.b0 + g.nblk);
-      }
-      const std::uint64_t p0 = (nA >> 1) & ~std::uint64_t{15};
-      const std::uint32_t bytes = static_cast<std::uint32_t>((((nE + 1) >> 1) - p0 + 15) & ~std::uint64_t{15});
-      if (bytes)
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(d.packed + p0), "r"(bytes) : "memory");
-    }
-    have_next = tile + 1 < t_hi && tile + 1 < next_begin;
-    if (have_next) {
-      const TileGeo g1 = tile_geo<KWIN>(d, tile + 1, log2T);
-      load_tile<KWIN>(d, g1, log2T, tid, nxt);
-      if (tid == 0) {
-        nA = __ldg(d.outpos + g1.b0);
-        nE = __ldg(d.outpos + g1.b0 + g1.nblk);
-      }
-    }
-
-    const std::uint32_t wl0 = static_cast<std::uint32_t>(tid) * KWIN;
-    const bool active = wl0 < g.nwin;
-
-    // ---- decode my windows into my slot
-    SlotSink sink{my_slot};
-    if (active) {
+  // ---- decode my windows into my slot
+  SlotSink sink{my_slot};
+  if (active) {
 #pragma unroll
-      for (int i = 0; i < KWIN; ++i) {
-        if (wl0 + i < g.nwin)
-          decode_window(bswap32(cur.win[i].x), bswap32(cur.win[i].y), bswap32(cur.win[i + 1].x),
-                        bswap32(cur.win[i + 1].y), gap_of<KWIN>(cur.gaps, i, wl0 + i), sm.tb, len_off,
-                        sink);
+    for (int i = 0; i < KWIN; ++i) {
+      if (wl0 + i < g.nwin)
+        decode_window(bswap32(cur.win[i].x), bswap32(cur.win[i].y), bswap32(cur.win[i + 1].x),
+                      bswap32(cur.win[i + 1].y), gap_of<KWIN>(cur.gaps, i, wl0 + i), tb, len_off, sink);
+    }
+  }
+  if (sink.q4) *sink.ptr = sink.lo;
+  const std::uint32_t cnt = static_cast<std::uint32_t>(sink.ptr - my_slot) * 8 + (sink.q4 >> 2);
+
+  // ---- exclusive scan of the per-thread counts
+  std::uint32_t incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const std::uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) gs.warp_sum[warp] = incl;
+  group_sync(group);
+  // lane-parallel exclusive prefix of the warp sums
+  const std::uint32_t wsum = lane < kWarps ? gs.warp_sum[lane] : 0u;
+  std::uint32_t wincl = wsum;
+#pragma unroll
+  for (int o = 1; o < kWarps; o <<= 1) {
+    const std::uint32_t y = __shfl_up_sync(0xffffffffu, wincl, o);
+    if (lane >= o) wincl += y;
+  }
+  const std::uint32_t wexcl = wincl - wsum;
+  // the first thread of my reference block (threads per block: 2^log2tpb)
+  constexpr std::uint32_t kLogKwin = KWIN == 1 ? 0 : (KWIN == 2 ? 1 : 2);
+  const std::uint32_t log2tpb = log2T - kLogKwin;
+  const std::uint32_t first_tid = log2tpb >= 8 ? 0u : (static_cast<std::uint32_t>(tid) & ~((1u << log2tpb) - 1));
+  const std::uint32_t lexcl = incl - cnt;
+  const std::uint32_t excl = __shfl_sync(0xffffffffu, wexcl, warp) + lexcl;
+  const std::uint32_t first_lex = __shfl_sync(0xffffffffu, lexcl, first_tid & 31);
+  const std::uint32_t first_excl = __shfl_sync(0xffffffffu, wexcl, first_tid >> 5) +
+                                   ((first_tid >> 5) == static_cast<std::uint32_t>(warp) ? first_lex : 0u);
+
+  // ---- my output range, clamped to my reference block's outpos limit
+  const std::uint64_t A = blk[0];
+  const std::uint32_t bl = wl0 >> log2T;
+  const std::uint32_t bl_c = bl < g.nblk ? bl : g.nblk - 1;
+  const std::uint32_t start_rel = static_cast<std::uint32_t>(blk[bl_c] - A) + excl - first_excl;
+  const std::uint32_t lim_rel = static_cast<std::uint32_t>(blk[bl_c + 1] - A);
+  const std::uint32_t cc = (active && start_rel < lim_rel) ? min(cnt, lim_rel - start_rel) : 0u;
+  const std::uint32_t off = static_cast<std::uint32_t>(A & 15);  // staging nibble of element A
+  const std::uint32_t d0 = start_rel + off, dend = d0 + cc;
+  const std::uint32_t data_end = off + static_cast<std::uint32_t>(blk[g.nblk] - A);
+  gs.rs[tid] = d0;
+  gs.re[tid] = dend;
+
+  // ---- move my nibbles to their final place; publish partial words
+  std::uint32_t headv = 0, tailv = 0;
+  const std::uint32_t fw = d0 >> 3, lw = (dend - 1) >> 3;
+  const std::uint32_t f4 = (d0 & 7) * 4, lastn = ((dend - 1) & 7) + 1;
+  if (cc) {
+    std::uint32_t prev = my_slot[0];
+    const std::uint32_t v0 = prev << f4;
+    if (fw == lw) {
+      const std::uint32_t v = v0 & low_nibbles(lastn);
+      if (f4 == 0 && lastn == 8) gs.stage[fw] = v;
+      else headv = v;
+    } else {
+      if (f4 == 0) gs.stage[fw] = v0;
+      else headv = v0;
+      std::uint32_t j = 1;
+      for (std::uint32_t k = fw + 1; k < lw; ++k, ++j) {
+        const std::uint32_t c = my_slot[j];
+        gs.stage[k] = __funnelshift_l(prev, c, f4);
+        prev = c;
       }
+      const std::uint32_t v = __funnelshift_l(prev, my_slot[j], f4) & low_nibbles(lastn);
+      if (lastn == 8) gs.stage[lw] = v;
+      else tailv = v;
     }
-    if (sink.q4) *sink.ptr = sink.lo;
-    const std::uint32_t cnt = static_cast<std::uint32_t>(sink.ptr - my_slot) * 8 + (sink.q4 >> 2);
+  }
+  gs.head[tid] = headv;
+  group_sync(group);
 
-    // ---- exclusive scan of the per-thread counts
-    std::uint32_t incl = cnt;
+  // ---- owners assemble words shared between threads
+  if (cc) {
+    const bool start_owner = (f4 == 0 || d0 == off) && !(f4 == 0 && (fw < lw || lastn == 8));
+    const bool tail_owner = fw != lw && lastn != 8;
+    if (start_owner || tail_owner) {
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const std::uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    if (lane == 31) sm.warp_sum[warp] = incl;
-    __syncthreads();
-    // lane-parallel exclusive prefix of the warp sums
-    const std::uint32_t wsum = lane < kWarps ? sm.warp_sum[lane] : 0u;
-    std::uint32_t wincl = wsum;
-#pragma unroll
-    for (int o = 1; o < kWarps; o <<= 1) {
-      const std::uint32_t y = __shfl_up_sync(0xffffffffu, wincl, o);
-      if (lane >= o) wincl += y;
-    }
-    const std::uint32_t wexcl = wincl - wsum;
-    // the first thread of my reference block (threads per block is a power of 2)
-    const std::uint32_t log2tpb = log2T >= static_cast<std::uint32_t>(__ffs(KWIN) - 1) ? log2T - (__ffs(KWIN) - 1) : 0u;
-    const std::uint32_t first_tid = log2tpb >= 31 ? 0u : (static_cast<std::uint32_t>(tid) & ~((1u << log2tpb) - 1));
-    const std::uint32_t lexcl = incl - cnt;
-    const std::uint32_t excl = __shfl_sync(0xffffffffu, wexcl, warp) + lexcl;
-    const std::uint32_t first_excl = __shfl_sync(0xffffffffu, wexcl, (first_tid >> 5) & 31) +
-                                     __shfl_sync(0xffffffffu, lexcl, first_tid & 31) *
-                                         ((first_tid >> 5) == static_cast<std::uint32_t>(warp) ? 1u : 0u);
-
-    // ---- my output range, clamped to my reference block's outpos limit
-    const std::uint64_t A = blk[0];
-    const std::uint32_t bl = wl0 >> log2T;
-    const std::uint32_t bl_c = bl < g.nblk ? bl : g.nblk - 1;
-    const std::uint32_t start_rel = static_cast<std::uint32_t>(blk[bl_c] - A) + excl - first_excl;
-    const std::uint32_t lim_rel = static_cast<std::uint32_t>(blk[bl_c + 1] - A);
-    const std::uint32_t cc = (active && start_rel < lim_rel) ? min(cnt, lim_rel - start_rel) : 0u;
-    const std::uint32_t off = static_cast<std::uint32_t>(A & 15);  // staging nibble of element A
-    const std::uint32_t d0 = start_rel + off, dend = d0 + cc;
-    const std::uint32_t data_end = off + static_cast<std::uint32_t>(blk[g.nblk] - A);
-    sm.rs[tid] = d0;
-    sm.re[tid] = dend;
-
-    // ---- move my nibbles to their final place; publish partial words
-    std::uint32_t headv = 0, tailv = 0;
-    const std::uint32_t fw = d0 >> 3, lw = (dend - 1) >> 3;
-    const std::uint32_t f4 = (d0 & 7) * 4, lastn = ((dend - 1) & 7) + 1;
-    if (cc) {
-      std::uint32_t prev = my_slot[0];
-      const std::uint32_t v0 = prev << f4;
-      if (fw == lw) {
-        const std::uint32_t v = v0 & low_nibbles(lastn);
-        if (f4 == 0 && lastn == 8) sm.stage[fw] = v;
-        else headv = v;
-      } else {
-        if (f4 == 0) sm.stage[fw] = v0;
-        else headv = v0;
-        std::uint32_t j = 1;
-        for (std::uint32_t k = fw + 1; k < lw; ++k, ++j) {
-          const std::uint32_t c = my_slot[j];
-          sm.stage[k] = __funnelshift_l(prev, c, f4);
-          prev = c;
-        }
-        const std::uint32_t v = __funnelshift_l(prev, my_slot[j], f4) & low_nibbles(lastn);
-        if (lastn == 8) sm.stage[lw] = v;
-        else tailv = v;
-      }
-    }
-    sm.head[tid] = headv;
-    __syncthreads();
-
-    // ---- owners assemble words shared between threads
-    if (cc) {
-      const bool start_owner = (f4 == 0 || d0 == off) && !(f4 == 0 && (fw < lw || lastn == 8));
-      const bool tail_owner = fw != lw && lastn != 8;
-      if (start_owner || tail_owner) {
-#pragma unroll
-        for (int pass = 0; pass < 2; ++pass) {
-          if (pass == 0 ? !start_owner : !tail_owner) continue;
-          const std::uint32_t k = pass == 0 ? fw : lw;
-          std::uint32_t v = pass == 0 ? headv : tailv;
-          const std::uint32_t wend = min(8 * k + 8, data_end);
-          std::uint32_t covered = dend;
-          for (int j = tid + 1; covered < wend && j < kThreads; ++j) {
-            const std::uint32_t rj = sm.rs[j], ej = sm.re[j];
-            if (ej > rj) {
-              v |= sm.head[j];
-              covered = ej;
-            }
+      for (int pass = 0; pass < 2; ++pass) {
+        if (pass == 0 ? !start_owner : !tail_owner) continue;
+        const std::uint32_t k = pass == 0 ? fw : lw;
+        std::uint32_t v = pass == 0 ? headv : tailv;
+        const std::uint32_t wend = min(8 * k + 8, data_end);
+        std::uint32_t covered = dend;
+        for (int j = tid + 1; covered < wend && j < kThreads; ++j) {
+          const std::uint32_t rj = gs.rs[j], ej = gs.re[j];
+          if (ej > rj) {
+            v |= gs.head[j];
+            covered = ej;
           }
-          sm.stage[k] = v;
         }
+        gs.stage[k] = v;
       }
     }
-    __syncthreads();
+  }
+  group_sync(group);
 
-    // ---- write-back: exponent nibbles + sign/mantissa nibbles -> FP8 bytes
-    {
-      const std::uint64_t S0 = A - off;
-      std::uint8_t* const out = d.out + (S0 - d.out_offset);
-      const std::uint8_t* const pk = d.packed + (S0 >> 1);
-      const std::uint32_t nch = (data_end + 15) >> 4;
-      const std::uint32_t full_lo = (off + 15) >> 4, full_hi = data_end >> 4;  // full chunks [lo, hi)
-      const uint2* sp = reinterpret_cast<const uint2*>(sm.stage);
-      const uint2* pp = reinterpret_cast<const uint2*>(pk);
-      uint4* op = reinterpret_cast<uint4*>(out);
-      for (std::uint32_t ci = full_lo + tid; ci < full_hi; ci += kThreads) {
+  // ---- write-back: exponent nibbles + sign/mantissa nibbles -> FP8 bytes
+  const std::uint64_t S0 = A - off;
+  std::uint8_t* const out = d.out + (S0 - d.out_offset);
+  const std::uint8_t* const pk = d.packed + (S0 >> 1);
+  const std::uint32_t nch = (data_end + 15) >> 4;
+  const std::uint32_t full_lo = (off + 15) >> 4, full_hi = data_end >> 4;  // full chunks [lo, hi)
+  const uint2* sp = reinterpret_cast<const uint2*>(gs.stage);
+  const uint2* pp = reinterpret_cast<const uint2*>(pk);
+  uint4* op = reinterpret_cast<uint4*>(out);
+  for (std::uint32_t c0 = full_lo + tid; c0 < full_hi; c0 += 4 * kThreads) {
+    uint2 q[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {  // all loads first: four L2 round trips overlap
+      const std::uint32_t ci = c0 + u * kThreads;
+      if (ci < full_hi) q[u] = __ldg(pp + ci);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const std::uint32_t ci = c0 + u * kThreads;
+      if (ci < full_hi) {
         const uint2 s = sp[ci];
-        const uint2 q = __ldg(pp + ci);
         uint4 r;
-        merge8(s.x, q.x, r.x, r.y);
-        merge8(s.y, q.y, r.z, r.w);
+        merge8(s.x, q[u].x, r.x, r.y);
+        merge8(s.y, q[u].y, r.z, r.w);
         op[ci] = r;
       }
-      // partial edge chunks (at most two), byte-wise
-      if (tid < 2) {
-        const std::uint32_t ci = tid == 0 ? 0u : nch - 1;
-        const bool partial = tid == 0 ? (full_lo > 0 && nch > 0) : (full_hi < nch && !(nch == 1 && full_lo > 0));
-        if (partial) {
-          const std::uint32_t g = 16 * ci;
-          const std::uint32_t lo = g < off ? off : g;
-          const std::uint32_t hi = g + 16 < data_end ? g + 16 : data_end;
-          for (std::uint32_t i = lo; i < hi; ++i) {
-            const std::uint32_t x = (sm.stage[i >> 3] >> (4 * (i & 7))) & 15u;
-            out[i] = merge1(x, pk[i >> 1], i & 1);
-          }
-        }
+    }
+  }
+  // partial edge chunks (at most two), byte-wise
+  if (tid < 2) {
+    const std::uint32_t ci = tid == 0 ? 0u : nch - 1;
+    const bool partial = tid == 0 ? (full_lo > 0 && nch > 0) : (full_hi < nch && !(nch == 1 && full_lo > 0));
+    if (partial) {
+      const std::uint32_t g16 = 16 * ci;
+      const std::uint32_t lo = g16 < off ? off : g16;
+      const std::uint32_t hi = g16 + 16 < data_end ? g16 + 16 : data_end;
+      for (std::uint32_t i = lo; i < hi; ++i) {
+        const std::uint32_t x = (gs.stage[i >> 3] >> (4 * (i & 7))) & 15u;
+        out[i] = merge1(x, pk[i >> 1], i & 1);
       }
     }
+  }
+}
+
+template <int KWIN, int GROUPS>
+__global__ void __launch_bounds__(kThreads * GROUPS, 1) decode_kernel(const LaunchArgs args) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Smem<KWIN, GROUPS>& sm = *reinterpret_cast<Smem<KWIN, GROUPS>*>(smem_raw);
+  const int group = threadIdx.x / kThreads, tid = threadIdx.x % kThreads;
+  GroupSmem<KWIN>& gs = sm.g[group];
+  const std::uint64_t total_tiles = args.total_tiles;
+  const std::uint64_t t_lo = total_tiles * blockIdx.x / gridDim.x;
+  const std::uint64_t t_hi = total_tiles * (blockIdx.x + 1) / gridDim.x;
+  std::uint32_t parity = 0;
+
+  // Segments of the CTA's tile range that lie in one tensor: tables are
+  // (re)loaded CTA-wide between segments, groups take tiles round robin.
+  for (std::uint64_t seg = t_lo; seg < t_hi;) {
+    TensorDesc d;
+    std::uint64_t seg_end;
+    if (args.descs) {
+      const int di = find_desc(args.descs, args.n_desc, seg);
+      d = args.descs[di];
+      seg_end = (di + 1 < args.n_desc) ? args.descs[di + 1].tile_begin : total_tiles;
+    } else {
+      d = args.inline_desc;
+      seg_end = total_tiles;
+    }
+    if (seg_end > t_hi) seg_end = t_hi;
+    const std::uint32_t log2T = 31 - __clz(d.T);
+    __syncthreads();  // every group is done with the previous tables
+    {
+      const uint4* f4 = reinterpret_cast<const uint4*>(d.fast);
+      uint4* sf4 = reinterpret_cast<uint4*>(sm.tb.fast);
+      for (int i = threadIdx.x; i < kFastEntries / 4; i += kThreads * GROUPS) sf4[i] = __ldg(f4 + i);
+      const uint4* m4 = reinterpret_cast<const uint4*>(d.smask);
+      uint4* sm4 = reinterpret_cast<uint4*>(sm.tb.smask);
+      for (int i = threadIdx.x; i < kFastEntries / 8; i += kThreads * GROUPS) sm4[i] = __ldg(m4 + i);
+      for (int i = threadIdx.x; i < static_cast<int>(d.n_luts) * 256; i += kThreads * GROUPS)
+        sm.tb.cascade[i] = d.cascade[i];
+    }
+    const std::uint32_t len_off = (d.n_luts - 1) << 8;
+    __syncthreads();
+
+    TileIn<KWIN> nxt;
+    std::uint64_t nA = 0, nE = 0;  // tid 0: outpos bounds of the prefetched tile
+    std::uint64_t tile = seg + group;
+    if (tile < seg_end) {
+      const TileGeo g0 = tile_geo<KWIN>(d, tile, log2T);
+      load_tile<KWIN>(d, g0, log2T, tid, nxt);
+      if (tid == 0) {
+        nA = __ldg(d.outpos + g0.b0);
+        nE = __ldg(d.outpos + g0.b0 + g0.nblk);
+      }
+    }
+    for (; tile < seg_end; tile += GROUPS, parity ^= 1) {
+      const TileGeo g = tile_geo<KWIN>(d, tile, log2T);
+      const TileIn<KWIN> cur = nxt;
+      std::uint64_t* const blk = gs.blk[parity];
+      for (std::uint32_t i = tid; i <= g.nblk; i += kThreads) blk[i] = __ldg(d.outpos + g.b0 + i);
+      if (tid == 0) {
+        // The tile's sign/mantissa nibbles are needed only at write-back:
+        // pull them into L2 now with one bulk (TMA) prefetch.
+        const std::uint64_t p0 = (nA >> 1) & ~std::uint64_t{15};
+        const std::uint32_t bytes = static_cast<std::uint32_t>((((nE + 1) >> 1) - p0 + 15) & ~std::uint64_t{15});
+        if (bytes)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(d.packed + p0), "r"(bytes) : "memory");
+      }
+      if (tile + GROUPS < seg_end) {
+        const TileGeo g1 = tile_geo<KWIN>(d, tile + GROUPS, log2T);
+        load_tile<KWIN>(d, g1, log2T, tid, nxt);
+        if (tid == 0) {
+          nA = __ldg(d.outpos + g1.b0);
+          nE = __ldg(d.outpos + g1.b0 + g1.nblk);
+        }
+      }
+      decode_tile<KWIN>(d, g, cur, blk, sm.tb, gs, log2T, len_off, group, tid);
+    }
+    seg = seg_end;
   }
 }
 
@@ -476,22 +508,24 @@ __global__ void count_window_kernel(const std::uint8_t* w16, unsigned gap, const
 
 template <int KWIN>
 cudaError_t launch_k(const LaunchArgs& args, cudaStream_t s) {
+  constexpr int G = groups_for<KWIN>();
   static int grid_cap = 0;
-  const int smem = static_cast<int>(sizeof(Smem<KWIN>));
+  const int smem = static_cast<int>(sizeof(Smem<KWIN, G>));
   if (grid_cap == 0) {
-    cudaError_t e = cudaFuncSetAttribute(decode_kernel<KWIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = cudaFuncSetAttribute(decode_kernel<KWIN, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_kernel<KWIN>, kThreads, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_kernel<KWIN, G>, kThreads * G, smem);
     if (e != cudaSuccess) return e;
     grid_cap = sms * (per_sm > 0 ? per_sm : 1);
   }
-  const std::uint64_t total = args.total_tiles;
-  const std::uint64_t grid = total < static_cast<std::uint64_t>(grid_cap) ? total : grid_cap;
+  // Enough tiles per CTA for every group to get work.
+  const std::uint64_t want = (args.total_tiles + G - 1) / G;
+  const std::uint64_t grid = want < static_cast<std::uint64_t>(grid_cap) ? want : grid_cap;
   if (grid == 0) return cudaSuccess;
-  decode_kernel<KWIN><<<static_cast<unsigned>(grid), kThreads, smem, s>>>(args);
+  decode_kernel<KWIN, G><<<static_cast<unsigned>(grid), kThreads * G, smem, s>>>(args);
   return cudaGetLastError();
 }
 

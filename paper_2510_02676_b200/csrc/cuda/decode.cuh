@@ -29,7 +29,7 @@ struct TensorDesc {
   std::uint32_t n_luts;
 };
 
-constexpr int kThreads = 512;
+constexpr int kThreads = 256;  // threads of one tile group (a CTA runs several groups)
 constexpr std::uint64_t kPad = 64;
 
 // Windows per thread (consecutive, always inside one reference block):
