@@ -104,6 +104,13 @@ int validate(const ecf8_sections* s, std::uint64_t* n_blocks_out) {
 
 std::uint64_t align_up(std::uint64_t x, std::uint64_t a) { return (x + a - 1) / a * a; }
 
+std::uint32_t lmin_of(const std::uint8_t lengths[16]) {
+  std::uint32_t m = 16;
+  for (int s = 0; s < 16; ++s)
+    if (lengths[s] && lengths[s] < m) m = lengths[s];
+  return m;
+}
+
 // Device copies of the decode tables, shared by every tensor with the same
 // code lengths (per device).
 struct DevTables {
@@ -190,6 +197,7 @@ void upload_into(ecf8_dev_tensor* t, const ecf8_sections* s, std::uint64_t nb, c
   d.blk_begin = 0;
   d.blk_end = nb;
   d.T = s->threads_per_block;
+  d.lmin = lmin_of(s->lengths);
   if (s->n_elem) {
     const DevTables& tb = device_tables(s->lengths);
     d.fast = tb.fast;
@@ -203,13 +211,14 @@ void upload_into(ecf8_dev_tensor* t, const ecf8_sections* s, std::uint64_t nb, c
 // Single-descriptor launch: the descriptor rides in the kernel parameters.
 int launch_one(const TensorDesc& d, cudaStream_t st) {
   if (d.blk_end <= d.blk_begin) return ECF8_OK;
+  const ecf8::dev::Variant v = ecf8::dev::variant_for(d.T, d.lmin);
   ecf8::dev::LaunchArgs a{};
   a.descs = nullptr;
   a.n_desc = 1;
-  a.total_tiles = ecf8::dev::tiles_of(d.T, d.blk_end - d.blk_begin);
+  a.total_tiles = ecf8::dev::tiles_of(d.T, v.kwin, d.blk_end - d.blk_begin);
   a.inline_desc = d;
   a.inline_desc.tile_begin = 0;
-  cu(ecf8::dev::launch_decode(a, ecf8::dev::windows_per_thread(d.T), st), "decode launch");
+  cu(ecf8::dev::launch_decode(a, v.id, st), "decode launch");
   return ECF8_OK;
 }
 
@@ -265,7 +274,7 @@ int host_pipeline(const ecf8_sections* s, std::uint64_t nb, std::uint8_t* out) {
   ensure(&c.dout, &c.dout_cap, align_up(s->n_elem, 16) + 16);
 
   const std::uint32_t T = s->threads_per_block;
-  const std::uint64_t m = T >= 256 ? 1 : 256 / T;  // blocks per tile
+  const std::uint64_t m = ecf8::dev::blocks_per_tile(T, ecf8::dev::variant_for(T, lmin_of(s->lengths)).kwin);
   const std::uint64_t target = std::uint64_t{8} << 20;
   std::uint64_t per = std::max<std::uint64_t>(m, target / (std::uint64_t{T} * 8) / m * m);
   if (s->encoded_len < 2 * target) per = nb;
@@ -292,6 +301,7 @@ int host_pipeline(const ecf8_sections* s, std::uint64_t nb, std::uint8_t* out) {
   d.cascade = tb.cascade;
   d.n_luts = tb.n_luts;
   d.lenpack = tb.lenpack;
+  d.lmin = lmin_of(s->lengths);
 
   cu(cudaMemcpyAsync(c.arena + off_pos, s->outpos, 8 * s->n_outpos, cudaMemcpyHostToDevice, c.s_in), "H2D outpos");
   for (std::uint64_t k = 0; k < n_chunks; ++k) {
@@ -389,20 +399,23 @@ int ecf8_batch_create(const ecf8_dev_tensor* const* ts, uint8_t* const* d_outs, 
     if (!out || (count > 0 && (!ts || !d_outs))) return fail(ECF8_EINVAL, "null argument");
     *out = nullptr;
     auto b = std::make_unique<ecf8_batch>();
-    for (int kw : {1, 2, 4}) {
+    for (int kw = 0; kw < 4; ++kw) {  // one launch per kernel variant present
       std::vector<TensorDesc> group;
       std::uint64_t tiles = 0;
+      int kwin = 1;
       for (int i = 0; i < count; ++i) {
         const ecf8_dev_tensor* t = ts[i];
         if (!t) return fail(ECF8_EINVAL, "null tensor");
-        if (t->n_elem == 0 || ecf8::dev::windows_per_thread(t->T) != kw) continue;
+        const ecf8::dev::Variant v = ecf8::dev::variant_for(t->T, t->desc.lmin);
+        if (t->n_elem == 0 || v.id != kw) continue;
+        kwin = v.kwin;
         if (!d_outs[i] || (reinterpret_cast<std::uintptr_t>(d_outs[i]) & 15))
           return fail(ECF8_EINVAL, "device output must be 16-byte aligned");
         TensorDesc d = t->desc;
         d.out = d_outs[i];
         d.out_offset = 0;
         d.tile_begin = tiles;
-        tiles += ecf8::dev::tiles_of(d.T, t->n_blocks);
+        tiles += ecf8::dev::tiles_of(d.T, kwin, t->n_blocks);
         group.push_back(d);
       }
       if (group.empty()) continue;

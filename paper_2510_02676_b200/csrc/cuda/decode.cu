@@ -34,6 +34,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "decode.cuh"
 #include "tables.hpp"
@@ -51,10 +52,10 @@ struct Tables {
   std::uint8_t cascade[18 * 256];
 };
 
-template <int KWIN>
+template <int SLOTW>
 struct GroupSmem {
-  static constexpr int kSlotStride = KWIN * 8 + 1;             // words; odd => no bank conflicts
-  static constexpr int kStageWords = KWIN * kThreads * 8 + 8;  // tile nibbles + 16-nibble slack
+  static constexpr int kSlotStride = SLOTW + 1;               // words; odd => no bank conflicts
+  static constexpr int kStageWords = kThreads * SLOTW + 8;    // tile nibbles + 16-nibble slack
   std::uint32_t slot[kThreads * kSlotStride];
   alignas(16) std::uint32_t stage[kStageWords];
   std::uint32_t rs[kThreads];
@@ -64,15 +65,15 @@ struct GroupSmem {
   std::uint32_t warp_sum[kWarps];
 };
 
-template <int KWIN, int GROUPS>
+template <int SLOTW, int GROUPS>
 struct Smem {
   Tables tb;
-  GroupSmem<KWIN> g[GROUPS];
+  GroupSmem<SLOTW> g[GROUPS];
 };
 
-template <int KWIN>
+template <int SLOTW>
 constexpr int groups_for() {
-  return KWIN == 4 ? 2 : 4;
+  return SLOTW >= 32 ? 2 : 4;
 }
 
 __device__ __forceinline__ void group_sync(int group) {
@@ -241,13 +242,13 @@ __device__ __forceinline__ std::uint32_t gap_of(std::uint32_t gaps, int i, std::
 }
 
 // One group decodes one tile: windows -> slots -> scan -> staging -> HBM.
-template <int KWIN>
+template <int KWIN, int SLOTW>
 __device__ __forceinline__ void decode_tile(const TensorDesc& d, const TileGeo& g, const TileIn<KWIN>& cur,
                                             const std::uint64_t* blk, const Tables& tb,
-                                            GroupSmem<KWIN>& gs, std::uint32_t log2T,
+                                            GroupSmem<SLOTW>& gs, std::uint32_t log2T,
                                             std::uint32_t len_off, int group, int tid) {
   const int lane = tid & 31, warp = tid >> 5;
-  std::uint32_t* const my_slot = gs.slot + tid * GroupSmem<KWIN>::kSlotStride;
+  std::uint32_t* const my_slot = gs.slot + tid * GroupSmem<SLOTW>::kSlotStride;
   const std::uint32_t wl0 = static_cast<std::uint32_t>(tid) * KWIN;
   const bool active = wl0 < g.nwin;
 
@@ -402,12 +403,12 @@ __device__ __forceinline__ void decode_tile(const TensorDesc& d, const TileGeo& 
   }
 }
 
-template <int KWIN, int GROUPS>
+template <int KWIN, int SLOTW, int GROUPS>
 __global__ void __launch_bounds__(kThreads * GROUPS, 1) decode_kernel(const LaunchArgs args) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  Smem<KWIN, GROUPS>& sm = *reinterpret_cast<Smem<KWIN, GROUPS>*>(smem_raw);
+  Smem<SLOTW, GROUPS>& sm = *reinterpret_cast<Smem<SLOTW, GROUPS>*>(smem_raw);
   const int group = threadIdx.x / kThreads, tid = threadIdx.x % kThreads;
-  GroupSmem<KWIN>& gs = sm.g[group];
+  GroupSmem<SLOTW>& gs = sm.g[group];
   const std::uint64_t total_tiles = args.total_tiles;
   const std::uint64_t t_lo = total_tiles * blockIdx.x / gridDim.x;
   const std::uint64_t t_hi = total_tiles * (blockIdx.x + 1) / gridDim.x;
@@ -474,7 +475,7 @@ __global__ void __launch_bounds__(kThreads * GROUPS, 1) decode_kernel(const Laun
           nE = __ldg(d.outpos + g1.b0 + g1.nblk);
         }
       }
-      decode_tile<KWIN>(d, g, cur, blk, sm.tb, gs, log2T, len_off, group, tid);
+      decode_tile<KWIN, SLOTW>(d, g, cur, blk, sm.tb, gs, log2T, len_off, group, tid);
     }
     seg = seg_end;
   }
@@ -506,18 +507,17 @@ __global__ void count_window_kernel(const std::uint8_t* w16, unsigned gap, const
   }
 }
 
-template <int KWIN>
+template <int KWIN, int SLOTW, int G>
 cudaError_t launch_k(const LaunchArgs& args, cudaStream_t s) {
-  constexpr int G = groups_for<KWIN>();
   static int grid_cap = 0;
-  const int smem = static_cast<int>(sizeof(Smem<KWIN, G>));
+  const int smem = static_cast<int>(sizeof(Smem<SLOTW, G>));
   if (grid_cap == 0) {
-    cudaError_t e = cudaFuncSetAttribute(decode_kernel<KWIN, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = cudaFuncSetAttribute(decode_kernel<KWIN, SLOTW, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_kernel<KWIN, G>, kThreads * G, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_kernel<KWIN, SLOTW, G>, kThreads * G, smem);
     if (e != cudaSuccess) return e;
     grid_cap = sms * (per_sm > 0 ? per_sm : 1);
   }
@@ -525,17 +525,24 @@ cudaError_t launch_k(const LaunchArgs& args, cudaStream_t s) {
   const std::uint64_t want = (args.total_tiles + G - 1) / G;
   const std::uint64_t grid = want < static_cast<std::uint64_t>(grid_cap) ? want : grid_cap;
   if (grid == 0) return cudaSuccess;
-  decode_kernel<KWIN, G><<<static_cast<unsigned>(grid), kThreads * G, smem, s>>>(args);
+  decode_kernel<KWIN, SLOTW, G><<<static_cast<unsigned>(grid), kThreads * G, smem, s>>>(args);
   return cudaGetLastError();
 }
 
 }  // namespace
 
-cudaError_t launch_decode(const LaunchArgs& args, int kwin, cudaStream_t stream) {
-  switch (kwin) {
-    case 1: return launch_k<1>(args, stream);
-    case 2: return launch_k<2>(args, stream);
-    case 4: return launch_k<4>(args, stream);
+cudaError_t launch_decode(const LaunchArgs& args, int variant, cudaStream_t stream) {
+  // Groups per CTA: 3 x 256 threads keeps <= 85 registers (no spills) at 24
+  // warps/SM; ECF8_GROUPS=4 selects the 32-warp build for experiments.
+  static const int four = [] {
+    const char* e = std::getenv("ECF8_GROUPS");
+    return e && e[0] == '4';
+  }();
+  switch (variant) {  // ids of variant_for() in decode.cuh
+    case 0: return four ? launch_k<1, 8, 4>(args, stream) : launch_k<1, 8, 3>(args, stream);
+    case 1: return four ? launch_k<2, 16, 4>(args, stream) : launch_k<2, 16, 3>(args, stream);
+    case 2: return four ? launch_k<4, 16, 4>(args, stream) : launch_k<4, 16, 3>(args, stream);
+    case 3: return launch_k<4, 32, 2>(args, stream);
     default: return cudaErrorInvalidValue;
   }
 }

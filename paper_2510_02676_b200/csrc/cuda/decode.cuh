@@ -27,23 +27,39 @@ struct TensorDesc {
   std::uint64_t tile_begin;      // first tile of this desc within its launch
   std::uint32_t T;
   std::uint32_t n_luts;
+  std::uint32_t lmin;  // shortest code length (selects the variant)
 };
 
 constexpr int kThreads = 256;  // threads of one tile group (a CTA runs several groups)
 constexpr std::uint64_t kPad = 64;
 
-// Windows per thread (consecutive, always inside one reference block):
-// T = 1 -> 1, T = 2..512 -> 2, T = 1024 -> 4.  A tile is kThreads * KWIN
-// windows.
-inline int windows_per_thread(std::uint32_t T) { return T == 1 ? 1 : (T <= 512 ? 2 : 4); }
+// Kernel variant.  A thread decodes KWIN consecutive windows (always inside
+// one reference block) into a private slot of SLOTW 32-bit words; a tile is
+// kThreads * KWIN windows.  A window holds at most ceil(64 / Lmin) symbols
+// (every code word, garbage fallbacks included, is >= Lmin bits), so the
+// shortest code length of the tensor bounds the slot: Lmin >= 2 allows four
+// windows in the slot that two windows need when Lmin == 1.
+struct Variant {
+  int kwin;
+  int slotw;
+  int id;  // index into the compiled variants
+};
 
-inline std::uint64_t blocks_per_tile(std::uint32_t T) {
-  const std::uint64_t w = static_cast<std::uint64_t>(kThreads) * windows_per_thread(T);
+inline Variant variant_for(std::uint32_t T, std::uint32_t lmin) {
+  if (T == 1) return {1, 8, 0};
+  if (T == 2) return {2, 16, 1};
+  if (lmin >= 2) return {4, 16, 2};
+  if (T == 1024) return {4, 32, 3};
+  return {2, 16, 1};
+}
+
+inline std::uint64_t blocks_per_tile(std::uint32_t T, int kwin) {
+  const std::uint64_t w = static_cast<std::uint64_t>(kThreads) * kwin;
   return T >= w ? 1 : w / T;
 }
 
-inline std::uint64_t tiles_of(std::uint32_t T, std::uint64_t n_blocks) {
-  const std::uint64_t m = blocks_per_tile(T);
+inline std::uint64_t tiles_of(std::uint32_t T, int kwin, std::uint64_t n_blocks) {
+  const std::uint64_t m = blocks_per_tile(T, kwin);
   return (n_blocks + m - 1) / m;
 }
 
@@ -57,8 +73,8 @@ struct LaunchArgs {
   TensorDesc inline_desc;
 };
 
-// One decode launch; every descriptor has windows_per_thread(T) == kwin.
-cudaError_t launch_decode(const LaunchArgs& args, int kwin, cudaStream_t stream);
+// One decode launch; every descriptor was prepared for variant `variant`.
+cudaError_t launch_decode(const LaunchArgs& args, int variant, cudaStream_t stream);
 
 // count_phase on one window (window10 staged as 16 bytes in device memory).
 cudaError_t launch_count_window(const std::uint8_t* d_window16, unsigned gap,
