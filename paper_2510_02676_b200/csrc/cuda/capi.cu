@@ -215,7 +215,7 @@ int launch_one(const TensorDesc& d, cudaStream_t st) {
   ecf8::dev::LaunchArgs a{};
   a.descs = nullptr;
   a.n_desc = 1;
-  a.total_tiles = ecf8::dev::tiles_of(d.T, v.kwin, d.blk_end - d.blk_begin);
+  a.total_tiles = ecf8::dev::tiles_of(d.T, v.tile_win, d.blk_end - d.blk_begin);
   a.inline_desc = d;
   a.inline_desc.tile_begin = 0;
   cu(ecf8::dev::launch_decode(a, v.id, st), "decode launch");
@@ -274,7 +274,7 @@ int host_pipeline(const ecf8_sections* s, std::uint64_t nb, std::uint8_t* out) {
   ensure(&c.dout, &c.dout_cap, align_up(s->n_elem, 16) + 16);
 
   const std::uint32_t T = s->threads_per_block;
-  const std::uint64_t m = ecf8::dev::blocks_per_tile(T, ecf8::dev::variant_for(T, lmin_of(s->lengths)).kwin);
+  const std::uint64_t m = ecf8::dev::blocks_per_tile(T, ecf8::dev::variant_for(T, lmin_of(s->lengths)).tile_win);
   const std::uint64_t target = std::uint64_t{8} << 20;
   std::uint64_t per = std::max<std::uint64_t>(m, target / (std::uint64_t{T} * 8) / m * m);
   if (s->encoded_len < 2 * target) per = nb;
@@ -399,23 +399,23 @@ int ecf8_batch_create(const ecf8_dev_tensor* const* ts, uint8_t* const* d_outs, 
     if (!out || (count > 0 && (!ts || !d_outs))) return fail(ECF8_EINVAL, "null argument");
     *out = nullptr;
     auto b = std::make_unique<ecf8_batch>();
-    for (int kw = 0; kw < 4; ++kw) {  // one launch per kernel variant present
+    for (int kw = 0; kw < 5; ++kw) {  // one launch per kernel variant present
       std::vector<TensorDesc> group;
       std::uint64_t tiles = 0;
-      int kwin = 1;
+      int kwin_tile = 1;
       for (int i = 0; i < count; ++i) {
         const ecf8_dev_tensor* t = ts[i];
         if (!t) return fail(ECF8_EINVAL, "null tensor");
         const ecf8::dev::Variant v = ecf8::dev::variant_for(t->T, t->desc.lmin);
         if (t->n_elem == 0 || v.id != kw) continue;
-        kwin = v.kwin;
+        kwin_tile = v.tile_win;
         if (!d_outs[i] || (reinterpret_cast<std::uintptr_t>(d_outs[i]) & 15))
           return fail(ECF8_EINVAL, "device output must be 16-byte aligned");
         TensorDesc d = t->desc;
         d.out = d_outs[i];
         d.out_offset = 0;
         d.tile_begin = tiles;
-        tiles += ecf8::dev::tiles_of(d.T, kwin, t->n_blocks);
+        tiles += ecf8::dev::tiles_of(d.T, kwin_tile, t->n_blocks);
         group.push_back(d);
       }
       if (group.empty()) continue;
@@ -527,9 +527,12 @@ int ecf8_count_window(const uint8_t window10[10], unsigned gap, const uint8_t le
     std::uint8_t w16[16] = {0};
     std::memcpy(w16, window10, 10);
     cu(cudaMemcpy(sc.win, w16, 16, cudaMemcpyHostToDevice), "H2D window");
-    cu(ecf8::dev::launch_count_window(sc.win, gap & 15, tb.fast, tb.smask, tb.cascade, tb.n_luts,
-                                      sc.cnt, nullptr),
-       "count launch");
+    TensorDesc td{};
+    td.fast = tb.fast;
+    td.smask = tb.smask;
+    td.cascade = tb.cascade;
+    td.n_luts = tb.n_luts;
+    cu(ecf8::dev::launch_count_window(sc.win, gap & 15, td, sc.cnt, nullptr), "count launch");
     cu(cudaMemcpy(count, sc.cnt, 4, cudaMemcpyDeviceToHost), "D2H count");
     return ECF8_OK;
   });

@@ -1,61 +1,52 @@
-// decode.cu -- ECF8 -> FP8 decode kernels for sm_100a (B200).
+// decode.cu -- ECF8 -> FP8 decode kernels for sm_100a (B200): tile-group
+// kernel, count_phase kernel, launch dispatch.
 //
 // Replaces the reference's OpenMP block decoder
 // (/root/reference/proj/src/codec.cpp:133-273: count_phase, Blelloch scan,
 // emit_phase, staging copy).  The reference decodes every symbol twice
-// (count, then emit); this kernel decodes once:
+// (count, then emit); these kernels decode once.  Two kernel shapes:
 //
-//   * persistent CTAs (one per SM) made of GROUPS independent tile groups of
-//     256 threads; the groups share one shared-memory copy of the decode
-//     tables (tables.hpp) and synchronise only with their own named barrier,
-//     so one group's barrier wait is covered by the others' work;
-//   * a tile is 256 * KWIN consecutive 64-bit windows made of whole
-//     reference blocks, KWIN consecutive windows per thread inside one
-//     block, so a tile starts at an outpos[] boundary;
-//   * each thread's window bits arrive in registers (8-byte loads, coalesced
-//     across the warp), prefetched one tile ahead, and the tile's
-//     sign/mantissa bytes are pulled into L2 by one bulk (TMA) prefetch; a
-//     64-bit register window walks the bits with up to five symbols per table
-//     load; the symbols that start before the window's 64-bit boundary are
-//     taken exactly -- the last entry partially, via a start-bit mask and a
-//     popcount (the codec.cpp:143-160 rule); symbols are packed as nibbles
-//     into a private shared-memory slot;
-//   * a warp-shuffle scan plus a lane-parallel cross-warp prefix (one
-//     barrier), seeded by outpos[] per reference block, gives each thread its
-//     output offset; counts past a block's outpos limit are clamped
-//     (codec.cpp:239-246);
-//   * each thread moves its nibbles to their final place in a nibble staging
-//     tile (funnel shifts, whole words); words shared with neighbours are
-//     assembled by one owner from published partial words -- no atomics;
-//   * write-back merges exponent nibbles with the sign/mantissa nibbles in
-//     SWAR form and stores 16 bytes per thread-step (loads batched four
-//     chunks deep); tile edges are written byte-wise so neighbouring tiles
-//     never touch the same byte.
+//   decode_warp.cu  one warp owns a 256-window tile (T in [8, 256], shortest
+//                   code >= 2 bits -- the common case); warp-synchronous.
+//   this file       GROUPS independent 256-thread tile groups per CTA for
+//                   the remaining geometries (T = 1, 2, 512, 1024 or 1-bit
+//                   codes); the groups share one shared-memory copy of the
+//                   tables and synchronise with their own named barrier.
+//
+// Per tile (a run of whole reference blocks): window bits -> registers
+// (prefetched a tile ahead) -> table walk (decode_common.cuh) -> nibble
+// slots -> scan of counts seeded by outpos[] and clamped to the block limits
+// (codec.cpp:239-246) -> funnel-shift compaction into a nibble staging tile
+// -> SWAR merge with the sign/mantissa nibbles -> 16-byte stores; tile edges
+// byte-wise.
 #include <cuda_runtime.h>
 
 #include <cstdint>
 #include <cstdlib>
 
 #include "decode.cuh"
-#include "tables.hpp"
+#include "decode_common.cuh"
 
 namespace ecf8::dev {
+
+bool warp_variant_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("ECF8_NO_WARP_KERNEL");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+
+cudaError_t launch_decode_warp(const LaunchArgs& args, cudaStream_t s);  // decode_warp.cu
 
 namespace {
 
 constexpr int kWarps = kThreads / 32;  // warps per group
-constexpr int kFastShift = 32 - kFastBits;
-
-struct Tables {
-  std::uint32_t fast[kFastEntries];
-  std::uint16_t smask[kFastEntries];
-  std::uint8_t cascade[18 * 256];
-};
 
 template <int SLOTW>
 struct GroupSmem {
-  static constexpr int kSlotStride = SLOTW + 1;               // words; odd => no bank conflicts
-  static constexpr int kStageWords = kThreads * SLOTW + 8;    // tile nibbles + 16-nibble slack
+  static constexpr int kSlotStride = SLOTW + 1;             // words; odd => no bank conflicts
+  static constexpr int kStageWords = kThreads * SLOTW + 8;  // tile nibbles + 16-nibble slack
   std::uint32_t slot[kThreads * kSlotStride];
   alignas(16) std::uint32_t stage[kStageWords];
   std::uint32_t rs[kThreads];
@@ -71,127 +62,8 @@ struct Smem {
   GroupSmem<SLOTW> g[GROUPS];
 };
 
-template <int SLOTW>
-constexpr int groups_for() {
-  return SLOTW >= 32 ? 2 : 4;
-}
-
 __device__ __forceinline__ void group_sync(int group) {
   asm volatile("bar.sync %0, %1;" ::"r"(group + 1), "r"(kThreads) : "memory");
-}
-
-// ---------------------------------------------------------------- sinks
-
-// Packs 4-bit symbols into consecutive 32-bit words (first symbol lowest).
-struct SlotSink {
-  std::uint32_t* ptr;
-  std::uint32_t lo = 0;  // partial word
-  std::uint32_t q4 = 0;  // bits used in lo, < 32
-  __device__ __forceinline__ void put(std::uint32_t syms, std::uint32_t n4) {
-    const std::uint32_t nl = lo | (syms << q4);
-    const std::uint32_t nh = __funnelshift_l(syms, 0u, q4);
-    q4 += n4;
-    if (q4 >= 32) {
-      *ptr++ = nl;
-      lo = nh;
-      q4 -= 32;
-    } else {
-      lo = nl;
-    }
-  }
-};
-
-struct CountSink {
-  std::uint32_t n4 = 0;
-  __device__ __forceinline__ void put(std::uint32_t, std::uint32_t k4) { n4 += k4; }
-};
-
-// A fast-table-format entry for the word at the head of `hi`, decoded by
-// the reference cascade (lut.hpp:43-49): one symbol, its length as b.
-__device__ __forceinline__ std::uint32_t slow_entry(std::uint32_t hi, const Tables& tb,
-                                                    std::uint32_t len_off) {
-  const std::uint32_t w16 = hi >> 16;
-  std::uint32_t v = tb.cascade[w16 >> 8];
-  if (v >= 240) v = tb.cascade[((256u - v) << 8) | (w16 & 255u)];
-  return (v << 12) | (4u << 5) | tb.cascade[len_off + v];
-}
-
-// Decodes the words that start in [gap, 64) of one 64-bit window
-// (codec.cpp:133-190 semantics); w0..w3 = window bits 0..127, big-endian.
-template <class Sink>
-__device__ __forceinline__ void decode_window(std::uint32_t w0, std::uint32_t w1, std::uint32_t w2,
-                                              std::uint32_t w3, std::uint32_t gap,
-                                              const Tables& tb, std::uint32_t len_off,
-                                              Sink& sink) {
-  std::uint32_t hi = __funnelshift_l(w1, w0, gap);
-  std::uint32_t lo = __funnelshift_l(w2, w1, gap);
-  std::uint32_t p = gap;
-  // Phase A: at least 32 valid bits remain in the register window and the
-  // window boundary is out of reach of one entry.
-  while (p < 32) {
-    std::uint32_t e = tb.fast[hi >> kFastShift];
-    if (((e >> 5) & 31) == 0) e = slow_entry(hi, tb, len_off);
-    sink.put(e >> 12, (e >> 5) & 31);
-    hi = __funnelshift_l(lo, hi, e);  // shift amount = e & 31 = bits consumed
-    lo = __funnelshift_l(0u, lo, e);
-    p += e & 31;
-  }
-  // Refill once: p in [32, 48); register window = bits [p, p + 64).
-  hi = __funnelshift_l(w2, w1, p - 32);
-  lo = __funnelshift_l(w3, w2, p - 32);
-  for (;;) {
-    const std::uint32_t idx = hi >> kFastShift;
-    std::uint32_t e = tb.fast[idx];
-    const bool fast_hit = ((e >> 5) & 31) != 0;
-    if (!fast_hit) e = slow_entry(hi, tb, len_off);
-    const std::uint32_t b = e & 31, r = 64 - p;
-    if (b >= r) {  // last entry: only the symbols that start before bit 64
-      const std::uint32_t starts = fast_hit ? tb.smask[idx] : 1u;
-      const std::uint32_t k4 = 4 * __popc(starts & ((1u << r) - 1));
-      sink.put((e >> 12) & ((1u << k4) - 1), k4);
-      return;
-    }
-    sink.put(e >> 12, (e >> 5) & 31);
-    hi = __funnelshift_l(lo, hi, e);
-    lo = __funnelshift_l(0u, lo, e);
-    p += b;
-  }
-}
-
-__device__ __forceinline__ std::uint32_t bswap32(std::uint32_t x) { return __byte_perm(x, 0, 0x0123); }
-
-__device__ __forceinline__ std::uint32_t sel(std::uint32_t a, std::uint32_t b, std::uint32_t m) {
-  return (a & m) | (b & ~m);
-}
-
-// Eight FP8 bytes from eight exponent nibbles S (element i at bits 4i..4i+3)
-// and four packed sign/mantissa bytes P (element 2j in the high nibble of
-// byte j): byte = sign << 7 | exponent << 3 | mantissa  (fp8.hpp assemble).
-__device__ __forceinline__ void merge8(std::uint32_t S, std::uint32_t P, std::uint32_t& o0,
-                                       std::uint32_t& o1) {
-  const std::uint32_t even = sel(sel(S << 3, P, 0x78787878u), P >> 4, 0xF8F8F8F8u);
-  const std::uint32_t odd = sel(sel(S >> 1, P << 4, 0x78787878u), P, 0xF8F8F8F8u);
-  o0 = __byte_perm(even, odd, 0x5140);
-  o1 = __byte_perm(even, odd, 0x7362);
-}
-
-__device__ __forceinline__ std::uint8_t merge1(std::uint32_t x, std::uint32_t qb, std::uint32_t odd) {
-  const std::uint32_t qh = odd ? (qb << 4) : qb;
-  return static_cast<std::uint8_t>((x << 3) | (qh & 0x80u) | ((qh >> 4) & 7u));
-}
-
-__device__ __forceinline__ std::uint32_t low_nibbles(std::uint32_t n) {  // n in 1..8
-  return n >= 8 ? 0xFFFFFFFFu : ((1u << (4 * n)) - 1);
-}
-
-__device__ __forceinline__ int find_desc(const TensorDesc* descs, int n, std::uint64_t tile) {
-  int lo = 0, hi = n - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (descs[mid].tile_begin <= tile) lo = mid;
-    else hi = mid - 1;
-  }
-  return lo;
 }
 
 // Tile geometry (uniform across a group).
@@ -274,7 +146,6 @@ __device__ __forceinline__ void decode_tile(const TensorDesc& d, const TileGeo& 
   }
   if (lane == 31) gs.warp_sum[warp] = incl;
   group_sync(group);
-  // lane-parallel exclusive prefix of the warp sums
   const std::uint32_t wsum = lane < kWarps ? gs.warp_sum[lane] : 0u;
   std::uint32_t wincl = wsum;
 #pragma unroll
@@ -283,9 +154,8 @@ __device__ __forceinline__ void decode_tile(const TensorDesc& d, const TileGeo& 
     if (lane >= o) wincl += y;
   }
   const std::uint32_t wexcl = wincl - wsum;
-  // the first thread of my reference block (threads per block: 2^log2tpb)
   constexpr std::uint32_t kLogKwin = KWIN == 1 ? 0 : (KWIN == 2 ? 1 : 2);
-  const std::uint32_t log2tpb = log2T - kLogKwin;
+  const std::uint32_t log2tpb = log2T - kLogKwin;  // threads per reference block
   const std::uint32_t first_tid = log2tpb >= 8 ? 0u : (static_cast<std::uint32_t>(tid) & ~((1u << log2tpb) - 1));
   const std::uint32_t lexcl = incl - cnt;
   const std::uint32_t excl = __shfl_sync(0xffffffffu, wexcl, warp) + lexcl;
@@ -387,18 +257,12 @@ __device__ __forceinline__ void decode_tile(const TensorDesc& d, const TileGeo& 
       }
     }
   }
-  // partial edge chunks (at most two), byte-wise
-  if (tid < 2) {
+  if (tid < 2) {  // partial edge chunks (at most two), byte-wise
     const std::uint32_t ci = tid == 0 ? 0u : nch - 1;
     const bool partial = tid == 0 ? (full_lo > 0 && nch > 0) : (full_hi < nch && !(nch == 1 && full_lo > 0));
     if (partial) {
       const std::uint32_t g16 = 16 * ci;
-      const std::uint32_t lo = g16 < off ? off : g16;
-      const std::uint32_t hi = g16 + 16 < data_end ? g16 + 16 : data_end;
-      for (std::uint32_t i = lo; i < hi; ++i) {
-        const std::uint32_t x = (gs.stage[i >> 3] >> (4 * (i & 7))) & 15u;
-        out[i] = merge1(x, pk[i >> 1], i & 1);
-      }
+      write_edge(gs.stage, out, pk, g16 < off ? off : g16, g16 + 16 < data_end ? g16 + 16 : data_end);
     }
   }
 }
@@ -430,16 +294,7 @@ __global__ void __launch_bounds__(kThreads * GROUPS, 1) decode_kernel(const Laun
     if (seg_end > t_hi) seg_end = t_hi;
     const std::uint32_t log2T = 31 - __clz(d.T);
     __syncthreads();  // every group is done with the previous tables
-    {
-      const uint4* f4 = reinterpret_cast<const uint4*>(d.fast);
-      uint4* sf4 = reinterpret_cast<uint4*>(sm.tb.fast);
-      for (int i = threadIdx.x; i < kFastEntries / 4; i += kThreads * GROUPS) sf4[i] = __ldg(f4 + i);
-      const uint4* m4 = reinterpret_cast<const uint4*>(d.smask);
-      uint4* sm4 = reinterpret_cast<uint4*>(sm.tb.smask);
-      for (int i = threadIdx.x; i < kFastEntries / 8; i += kThreads * GROUPS) sm4[i] = __ldg(m4 + i);
-      for (int i = threadIdx.x; i < static_cast<int>(d.n_luts) * 256; i += kThreads * GROUPS)
-        sm.tb.cascade[i] = d.cascade[i];
-    }
+    stage_tables(d, sm.tb, threadIdx.x, kThreads * GROUPS);
     const std::uint32_t len_off = (d.n_luts - 1) << 8;
     __syncthreads();
 
@@ -459,9 +314,7 @@ __global__ void __launch_bounds__(kThreads * GROUPS, 1) decode_kernel(const Laun
       const TileIn<KWIN> cur = nxt;
       std::uint64_t* const blk = gs.blk[parity];
       for (std::uint32_t i = tid; i <= g.nblk; i += kThreads) blk[i] = __ldg(d.outpos + g.b0 + i);
-      if (tid == 0) {
-        // The tile's sign/mantissa nibbles are needed only at write-back:
-        // pull them into L2 now with one bulk (TMA) prefetch.
+      if (tid == 0) {  // sign/mantissa bytes of this tile -> L2 (one bulk TMA prefetch)
         const std::uint64_t p0 = (nA >> 1) & ~std::uint64_t{15};
         const std::uint32_t bytes = static_cast<std::uint32_t>((((nE + 1) >> 1) - p0 + 15) & ~std::uint64_t{15});
         if (bytes)
@@ -481,15 +334,9 @@ __global__ void __launch_bounds__(kThreads * GROUPS, 1) decode_kernel(const Laun
   }
 }
 
-__global__ void count_window_kernel(const std::uint8_t* w16, unsigned gap, const std::uint32_t* fast,
-                                    const std::uint16_t* smask, const std::uint8_t* casc,
-                                    std::uint32_t n_luts, std::uint32_t* out) {
+__global__ void count_window_kernel(const std::uint8_t* w16, unsigned gap, TensorDesc d, std::uint32_t* out) {
   __shared__ Tables tb;
-  for (int i = threadIdx.x; i < kFastEntries; i += blockDim.x) {
-    tb.fast[i] = fast[i];
-    tb.smask[i] = smask[i];
-  }
-  for (int i = threadIdx.x; i < static_cast<int>(n_luts) * 256; i += blockDim.x) tb.cascade[i] = casc[i];
+  stage_tables(d, tb, threadIdx.x, blockDim.x);
   __syncthreads();
   if (threadIdx.x == 0) {
     std::uint32_t w[4];
@@ -502,7 +349,7 @@ __global__ void count_window_kernel(const std::uint8_t* w16, unsigned gap, const
       w[k] = v;
     }
     CountSink c;
-    decode_window(w[0], w[1], w[2], w[3], gap & 15u, tb, (n_luts - 1) << 8, c);
+    decode_window_exact(w[0], w[1], w[2], w[3], gap & 15u, tb, (d.n_luts - 1) << 8, c);
     *out = c.n4 >> 2;
   }
 }
@@ -521,8 +368,7 @@ cudaError_t launch_k(const LaunchArgs& args, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     grid_cap = sms * (per_sm > 0 ? per_sm : 1);
   }
-  // Enough tiles per CTA for every group to get work.
-  const std::uint64_t want = (args.total_tiles + G - 1) / G;
+  const std::uint64_t want = (args.total_tiles + G - 1) / G;  // every group gets work
   const std::uint64_t grid = want < static_cast<std::uint64_t>(grid_cap) ? want : grid_cap;
   if (grid == 0) return cudaSuccess;
   decode_kernel<KWIN, SLOTW, G><<<static_cast<unsigned>(grid), kThreads * G, smem, s>>>(args);
@@ -532,25 +378,21 @@ cudaError_t launch_k(const LaunchArgs& args, cudaStream_t s) {
 }  // namespace
 
 cudaError_t launch_decode(const LaunchArgs& args, int variant, cudaStream_t stream) {
-  // Groups per CTA: 3 x 256 threads keeps <= 85 registers (no spills) at 24
-  // warps/SM; ECF8_GROUPS=4 selects the 32-warp build for experiments.
-  static const int four = [] {
-    const char* e = std::getenv("ECF8_GROUPS");
-    return e && e[0] == '4';
-  }();
+  // Three 256-thread groups per CTA keep <= 85 registers (no spills) at 24
+  // warps/SM.
   switch (variant) {  // ids of variant_for() in decode.cuh
-    case 0: return four ? launch_k<1, 8, 4>(args, stream) : launch_k<1, 8, 3>(args, stream);
-    case 1: return four ? launch_k<2, 16, 4>(args, stream) : launch_k<2, 16, 3>(args, stream);
-    case 2: return four ? launch_k<4, 16, 4>(args, stream) : launch_k<4, 16, 3>(args, stream);
+    case 0: return launch_k<1, 8, 3>(args, stream);
+    case 1: return launch_k<2, 16, 3>(args, stream);
+    case 2: return launch_k<4, 16, 3>(args, stream);
     case 3: return launch_k<4, 32, 2>(args, stream);
+    case 4: return launch_decode_warp(args, stream);
     default: return cudaErrorInvalidValue;
   }
 }
 
-cudaError_t launch_count_window(const std::uint8_t* d_window16, unsigned gap, const std::uint32_t* d_fast,
-                                const std::uint16_t* d_smask, const std::uint8_t* d_cascade,
-                                std::uint32_t n_luts, std::uint32_t* d_count, cudaStream_t stream) {
-  count_window_kernel<<<1, 128, 0, stream>>>(d_window16, gap, d_fast, d_smask, d_cascade, n_luts, d_count);
+cudaError_t launch_count_window(const std::uint8_t* d_window16, unsigned gap, const TensorDesc& d,
+                                std::uint32_t* d_count, cudaStream_t stream) {
+  count_window_kernel<<<1, 128, 0, stream>>>(d_window16, gap, d, d_count);
   return cudaGetLastError();
 }
 

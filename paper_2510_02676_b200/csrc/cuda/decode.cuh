@@ -39,27 +39,35 @@ constexpr std::uint64_t kPad = 64;
 // (every code word, garbage fallbacks included, is >= Lmin bits), so the
 // shortest code length of the tensor bounds the slot: Lmin >= 2 allows four
 // windows in the slot that two windows need when Lmin == 1.
+//
+// Variant 4 is the warp-autonomous kernel (decode_warp.cu): one warp owns a
+// 256-window tile, eight windows per lane; it needs T in [8, 256] (whole
+// blocks per tile, whole lanes per block) and Lmin >= 2.
 struct Variant {
   int kwin;
   int slotw;
-  int id;  // index into the compiled variants
+  int id;        // index into the compiled variants
+  int tile_win;  // windows per tile
 };
 
+bool warp_variant_enabled();  // false when ECF8_NO_WARP_KERNEL=1 (A/B runs)
+
 inline Variant variant_for(std::uint32_t T, std::uint32_t lmin) {
-  if (T == 1) return {1, 8, 0};
-  if (T == 2) return {2, 16, 1};
-  if (lmin >= 2) return {4, 16, 2};
-  if (T == 1024) return {4, 32, 3};
-  return {2, 16, 1};
+  if (lmin >= 2 && T >= 8 && T <= 256 && warp_variant_enabled()) return {8, 32, 4, 256};
+  if (T == 1) return {1, 8, 0, kThreads};
+  if (T == 2) return {2, 16, 1, 2 * kThreads};
+  if (lmin >= 2) return {4, 16, 2, 4 * kThreads};
+  if (T == 1024) return {4, 32, 3, 4 * kThreads};
+  return {2, 16, 1, 2 * kThreads};
 }
 
-inline std::uint64_t blocks_per_tile(std::uint32_t T, int kwin) {
-  const std::uint64_t w = static_cast<std::uint64_t>(kThreads) * kwin;
+inline std::uint64_t blocks_per_tile(std::uint32_t T, int tile_win) {
+  const std::uint64_t w = static_cast<std::uint64_t>(tile_win);
   return T >= w ? 1 : w / T;
 }
 
-inline std::uint64_t tiles_of(std::uint32_t T, int kwin, std::uint64_t n_blocks) {
-  const std::uint64_t m = blocks_per_tile(T, kwin);
+inline std::uint64_t tiles_of(std::uint32_t T, int tile_win, std::uint64_t n_blocks) {
+  const std::uint64_t m = blocks_per_tile(T, tile_win);
   return (n_blocks + m - 1) / m;
 }
 
@@ -77,9 +85,8 @@ struct LaunchArgs {
 cudaError_t launch_decode(const LaunchArgs& args, int variant, cudaStream_t stream);
 
 // count_phase on one window (window10 staged as 16 bytes in device memory).
-cudaError_t launch_count_window(const std::uint8_t* d_window16, unsigned gap,
-                                const std::uint32_t* d_fast, const std::uint16_t* d_smask,
-                                const std::uint8_t* d_cascade, std::uint32_t n_luts,
+// Only the table fields of `tables` are used.
+cudaError_t launch_count_window(const std::uint8_t* d_window16, unsigned gap, const TensorDesc& tables,
                                 std::uint32_t* d_count, cudaStream_t stream);
 
 }  // namespace ecf8::dev

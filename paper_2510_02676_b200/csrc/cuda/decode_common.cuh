@@ -1,0 +1,225 @@
+// decode_common.cuh -- device building blocks shared by the ECF8 decode
+// kernels (decode.cu: 256-thread tile groups; decode_warp.cu: warp tiles).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "decode.cuh"
+#include "tables.hpp"
+
+namespace ecf8::dev {
+
+constexpr int kFastShift = 32 - kFastBits;
+
+// Decode tables as staged in shared memory (see tables.hpp).  Entries of
+// the fast table whose first word is not resolvable from kFastBits bits are
+// rewritten on staging to the "flagged" form below.
+struct Tables {
+  std::uint32_t fast[kFastEntries];
+  std::uint16_t smask[kFastEntries];
+  std::uint8_t cascade[18 * 256];
+};
+
+// A fast entry with n == 0 is staged as: advance 1 bit, emit nothing, set
+// kSlowFlag.  The fast walk then runs branch-free; a window that met such an
+// entry is decoded again exactly by the slow walk (rare: code words longer
+// than kFastBits bits, or garbage windows of incomplete codes).
+constexpr std::uint32_t kSlowFlag = 1u << 11;
+__host__ __device__ constexpr std::uint32_t stage_entry(std::uint32_t e) {
+  return ((e >> 5) & 31) ? e : (kSlowFlag | 1u);
+}
+
+// Packs 4-bit symbols into consecutive 32-bit words (first symbol lowest).
+struct SlotSink {
+  std::uint32_t* ptr;
+  std::uint32_t lo = 0;  // partial word
+  std::uint32_t q4 = 0;  // bits used in lo, < 32
+  __device__ __forceinline__ void put(std::uint32_t syms, std::uint32_t n4) {
+    const std::uint32_t nl = lo | (syms << q4);
+    const std::uint32_t nh = __funnelshift_l(syms, 0u, q4);
+    q4 += n4;
+    if (q4 >= 32) {
+      *ptr++ = nl;
+      lo = nh;
+      q4 -= 32;
+    } else {
+      lo = nl;
+    }
+  }
+};
+
+struct CountSink {
+  std::uint32_t n4 = 0;
+  __device__ __forceinline__ void put(std::uint32_t, std::uint32_t k4) { n4 += k4; }
+};
+
+// The reference cascade (lut.hpp:43-49) on the 16-bit head of `hi`, as a
+// fast-format entry: one symbol, its length as b.
+__device__ __forceinline__ std::uint32_t slow_entry(std::uint32_t hi, const Tables& tb,
+                                                    std::uint32_t len_off) {
+  const std::uint32_t w16 = hi >> 16;
+  std::uint32_t v = tb.cascade[w16 >> 8];
+  if (v >= 240) v = tb.cascade[((256u - v) << 8) | (w16 & 255u)];
+  return (v << 12) | (4u << 5) | tb.cascade[len_off + v];
+}
+
+// Exact walk of one 64-bit window: the code words that start in [gap, 64)
+// (codec.cpp:133-190 semantics); w0..w3 = window bits 0..127, big-endian.
+// Handles every entry kind; used for count_phase and for flagged windows.
+template <class Sink>
+__device__ __forceinline__ void decode_window_exact(std::uint32_t w0, std::uint32_t w1,
+                                                    std::uint32_t w2, std::uint32_t w3,
+                                                    std::uint32_t gap, const Tables& tb,
+                                                    std::uint32_t len_off, Sink& sink) {
+  std::uint32_t hi = __funnelshift_l(w1, w0, gap);
+  std::uint32_t lo = __funnelshift_l(w2, w1, gap);
+  std::uint32_t p = gap;
+  while (p < 32) {
+    std::uint32_t e = tb.fast[hi >> kFastShift];
+    if (e & kSlowFlag) e = slow_entry(hi, tb, len_off);
+    sink.put(e >> 12, (e >> 5) & 31);
+    hi = __funnelshift_l(lo, hi, e);
+    lo = __funnelshift_l(0u, lo, e);
+    p += e & 31;
+  }
+  hi = __funnelshift_l(w2, w1, p - 32);
+  lo = __funnelshift_l(w3, w2, p - 32);
+  for (;;) {
+    const std::uint32_t idx = hi >> kFastShift;
+    std::uint32_t e = tb.fast[idx];
+    const bool fast_hit = !(e & kSlowFlag);
+    if (!fast_hit) e = slow_entry(hi, tb, len_off);
+    const std::uint32_t b = e & 31, r = 64 - p;
+    if (b >= r) {
+      const std::uint32_t starts = fast_hit ? tb.smask[idx] : 1u;
+      const std::uint32_t k4 = 4 * __popc(starts & ((1u << r) - 1));
+      sink.put((e >> 12) & ((1u << k4) - 1), k4);
+      return;
+    }
+    sink.put(e >> 12, (e >> 5) & 31);
+    hi = __funnelshift_l(lo, hi, e);
+    lo = __funnelshift_l(0u, lo, e);
+    p += b;
+  }
+}
+
+// Branch-free fast walk of one window; returns false (sink contents then
+// garbage) if a flagged entry was met -- the caller rewinds and uses the
+// exact walk.
+//
+// Phase A runs while at least 32 valid bits remain in the 64-bit register
+// window (one entry never reaches the window boundary from there); one
+// refill; phase B takes whole entries until the next one would cross bit 64
+// and then exactly the symbols that start before it (start-bit mask +
+// popcount, the codec.cpp:143-160 rule).
+__device__ __forceinline__ bool decode_window_fast(std::uint32_t w0, std::uint32_t w1, std::uint32_t w2,
+                                                   std::uint32_t w3, std::uint32_t gap,
+                                                   const Tables& tb, SlotSink& sink) {
+  std::uint32_t hi = __funnelshift_l(w1, w0, gap);
+  std::uint32_t lo = __funnelshift_l(w2, w1, gap);
+  std::uint32_t p = gap, flags = 0;
+  while (p < 32) {
+    const std::uint32_t e = tb.fast[hi >> kFastShift];
+    flags |= e;
+    sink.put(e >> 12, (e >> 5) & 31);
+    hi = __funnelshift_l(lo, hi, e);  // shift amount = e & 31 = bits consumed
+    lo = __funnelshift_l(0u, lo, e);
+    p += e & 31;
+  }
+  hi = __funnelshift_l(w2, w1, p - 32);  // p in [32, 44): window = bits [p, p + 64)
+  lo = __funnelshift_l(w3, w2, p - 32);
+  for (;;) {
+    const std::uint32_t idx = hi >> kFastShift;
+    const std::uint32_t e = tb.fast[idx];
+    flags |= e;
+    const std::uint32_t b = e & 31, r = 64 - p;
+    if (b >= r) {
+      const std::uint32_t k4 = 4 * __popc(tb.smask[idx] & ((1u << r) - 1));
+      sink.put((e >> 12) & ((1u << k4) - 1), k4);
+      break;
+    }
+    sink.put(e >> 12, (e >> 5) & 31);
+    hi = __funnelshift_l(lo, hi, e);
+    lo = __funnelshift_l(0u, lo, e);
+    p += b;
+  }
+  return !(flags & kSlowFlag);
+}
+
+__device__ __forceinline__ void decode_window(std::uint32_t w0, std::uint32_t w1, std::uint32_t w2,
+                                              std::uint32_t w3, std::uint32_t gap, const Tables& tb,
+                                              std::uint32_t len_off, SlotSink& sink) {
+  const SlotSink saved = sink;
+  if (!decode_window_fast(w0, w1, w2, w3, gap, tb, sink)) {
+    sink = saved;
+    decode_window_exact(w0, w1, w2, w3, gap, tb, len_off, sink);
+  }
+}
+
+__device__ __forceinline__ std::uint32_t bswap32(std::uint32_t x) { return __byte_perm(x, 0, 0x0123); }
+
+__device__ __forceinline__ std::uint32_t sel(std::uint32_t a, std::uint32_t b, std::uint32_t m) {
+  return (a & m) | (b & ~m);
+}
+
+// Eight FP8 bytes from eight exponent nibbles S (element i at bits 4i..4i+3)
+// and four packed sign/mantissa bytes P (element 2j in the high nibble of
+// byte j): byte = sign << 7 | exponent << 3 | mantissa  (fp8.hpp assemble).
+__device__ __forceinline__ void merge8(std::uint32_t S, std::uint32_t P, std::uint32_t& o0,
+                                       std::uint32_t& o1) {
+  const std::uint32_t even = sel(sel(S << 3, P, 0x78787878u), P >> 4, 0xF8F8F8F8u);
+  const std::uint32_t odd = sel(sel(S >> 1, P << 4, 0x78787878u), P, 0xF8F8F8F8u);
+  o0 = __byte_perm(even, odd, 0x5140);
+  o1 = __byte_perm(even, odd, 0x7362);
+}
+
+__device__ __forceinline__ std::uint8_t merge1(std::uint32_t x, std::uint32_t qb, std::uint32_t odd) {
+  const std::uint32_t qh = odd ? (qb << 4) : qb;
+  return static_cast<std::uint8_t>((x << 3) | (qh & 0x80u) | ((qh >> 4) & 7u));
+}
+
+__device__ __forceinline__ std::uint32_t low_nibbles(std::uint32_t n) {  // n in 1..8
+  return n >= 8 ? 0xFFFFFFFFu : ((1u << (4 * n)) - 1);
+}
+
+__device__ __forceinline__ int find_desc(const TensorDesc* descs, int n, std::uint64_t tile) {
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (descs[mid].tile_begin <= tile) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+// Stage a tensor's tables into shared memory (all threads of the CTA).
+__device__ __forceinline__ void stage_tables(const TensorDesc& d, Tables& tb, int tid, int nthreads) {
+  const uint4* f4 = reinterpret_cast<const uint4*>(d.fast);
+  uint4* sf4 = reinterpret_cast<uint4*>(tb.fast);
+  for (int i = tid; i < kFastEntries / 4; i += nthreads) {
+    uint4 v = __ldg(f4 + i);
+    v.x = stage_entry(v.x);
+    v.y = stage_entry(v.y);
+    v.z = stage_entry(v.z);
+    v.w = stage_entry(v.w);
+    sf4[i] = v;
+  }
+  const uint4* m4 = reinterpret_cast<const uint4*>(d.smask);
+  uint4* sm4 = reinterpret_cast<uint4*>(tb.smask);
+  for (int i = tid; i < kFastEntries / 8; i += nthreads) sm4[i] = __ldg(m4 + i);
+  for (int i = tid; i < static_cast<int>(d.n_luts) * 256; i += nthreads) tb.cascade[i] = d.cascade[i];
+}
+
+// Byte-wise write of output elements [lo, hi) (staging nibble coordinates)
+// for tile edges shared with neighbouring tiles.
+__device__ __forceinline__ void write_edge(const std::uint32_t* stage, std::uint8_t* out,
+                                           const std::uint8_t* pk, std::uint32_t lo, std::uint32_t hi) {
+  for (std::uint32_t i = lo; i < hi; ++i) {
+    const std::uint32_t x = (stage[i >> 3] >> (4 * (i & 7))) & 15u;
+    out[i] = merge1(x, pk[i >> 1], i & 1);
+  }
+}
+
+}  // namespace ecf8::dev

@@ -1,0 +1,308 @@
+// decode_warp.cu -- warp-autonomous ECF8 decode kernel (sm_100a).
+//
+// Variant for the common case T in [8, 256] and shortest code length >= 2
+// (every FP8 weight tensor we have seen): one warp owns a tile of 256
+// consecutive 64-bit windows = 256/T whole reference blocks, eight windows
+// per lane.  A window then holds at most 32 symbols, so a lane's slot is 32
+// words and the tile's output at most 8192 nibbles.  Everything after the
+// table staging is warp-synchronous: no CTA or group barriers, no cross-warp
+// scan -- the reference block's offsets come straight from outpos[]
+// (codec.cpp:212-253 restated per warp).  Phases per tile:
+//
+//   decode   each lane walks its 8 windows (decode_common.cuh fast walk,
+//            exact walk for flagged windows) into its nibble slot;
+//   scan     5-step warp shuffle scan of the lane counts, segmented by
+//            reference block, clamped to outpos limits (codec.cpp:239-246);
+//   compact  funnel-shift copy of each lane's nibbles to their final place
+//            in the warp's staging tile; shared words assembled by owners;
+//   write    16 output bytes per lane-step (SWAR merge with the
+//            sign/mantissa nibbles, prefetched into L2 by one bulk TMA
+//            prefetch), tile edges byte-wise.
+//
+// The next tile's window words, gaps and outpos bounds are loaded into
+// registers one tile ahead.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdlib>
+
+#include "decode.cuh"
+#include "decode_common.cuh"
+
+namespace ecf8::dev {
+
+namespace {
+
+constexpr int kLaneWin = 8;  // windows per lane
+
+struct WarpSmem {
+  static constexpr int kSlotW = 32;  // 8 windows x 32 symbols / 8 nibbles per word
+  static constexpr int kStride = kSlotW + 1;
+  static constexpr int kStageWords = 32 * kSlotW + 8;
+  std::uint32_t slot[32 * kStride];
+  alignas(16) std::uint32_t stage[kStageWords];
+  std::uint32_t rs[32];
+  std::uint32_t re[32];
+  std::uint32_t head[32];
+};
+
+__shared__ Tables g_tb;
+
+struct WarpIn {
+  uint4 w01, w23, w45, w67;  // window bytes (little-endian 32-bit words)
+  uint2 w8;                  // first 8 bytes of the next window (lookahead)
+  std::uint32_t gaps;        // 8 gap nibbles, window 2j in the high nibble of byte j
+  std::uint64_t A, E;        // tile output range
+  std::uint64_t o0, o1;      // my reference block's output range
+  std::uint32_t nblk, nwin;
+  std::uint64_t b0;
+};
+
+__device__ __forceinline__ void load_warp_tile(const TensorDesc& d, std::uint64_t tile, std::uint32_t log2T,
+                                               int lane, WarpIn& in) {
+  const std::uint32_t m = 256u >> log2T;  // blocks per tile
+  in.b0 = d.blk_begin + (tile - d.tile_begin) * m;
+  in.nblk = static_cast<std::uint32_t>(d.blk_end - in.b0 < m ? d.blk_end - in.b0 : m);
+  in.nwin = in.nblk << log2T;
+  const std::uint64_t w0g = in.b0 << log2T;
+  const std::uint32_t wl = static_cast<std::uint32_t>(lane) * kLaneWin;
+  in.A = __ldg(d.outpos + in.b0);
+  in.E = __ldg(d.outpos + in.b0 + in.nblk);
+  if (wl < in.nwin) {
+    const uint4* src = reinterpret_cast<const uint4*>(d.encoded + 8 * (w0g + wl));
+    in.w01 = __ldg(src);
+    in.w23 = __ldg(src + 1);
+    in.w45 = __ldg(src + 2);
+    in.w67 = __ldg(src + 3);
+    in.w8 = __ldg(reinterpret_cast<const uint2*>(src + 4));
+    in.gaps = __ldg(reinterpret_cast<const std::uint32_t*>(d.gaps + (w0g >> 1)) + lane);
+    const std::uint32_t bl = wl >> log2T;
+    in.o0 = __ldg(d.outpos + in.b0 + bl);
+    in.o1 = __ldg(d.outpos + in.b0 + bl + 1);
+  } else {
+    in.o0 = in.o1 = in.E;
+  }
+}
+
+__device__ __forceinline__ void warp_tile(const TensorDesc& d, const WarpIn& in, std::uint32_t log2T,
+                                          std::uint32_t len_off, WarpSmem& ws, int lane) {
+  std::uint32_t* const my_slot = ws.slot + lane * WarpSmem::kStride;
+  const std::uint32_t wl0 = static_cast<std::uint32_t>(lane) * kLaneWin;
+  const bool active = wl0 < in.nwin;
+
+  // ---- decode my 8 windows into my slot (window words rotate through
+  //      registers so the loop body is emitted once)
+  SlotSink sink{my_slot};
+  if (active) {
+    std::uint32_t a0 = bswap32(in.w01.x), a1 = bswap32(in.w01.y);
+    std::uint32_t r[14] = {bswap32(in.w01.z), bswap32(in.w01.w), bswap32(in.w23.x), bswap32(in.w23.y),
+                           bswap32(in.w23.z), bswap32(in.w23.w), bswap32(in.w45.x), bswap32(in.w45.y),
+                           bswap32(in.w45.z), bswap32(in.w45.w), bswap32(in.w67.x), bswap32(in.w67.y),
+                           bswap32(in.w67.z), bswap32(in.w67.w)};
+    const std::uint32_t n = min(in.nwin - wl0, static_cast<std::uint32_t>(kLaneWin));
+#pragma unroll 1
+    for (std::uint32_t i = 0; i < n; ++i) {
+      // byte j of the gap word: window 2j in the high nibble, 2j + 1 low
+      const std::uint32_t gap = (in.gaps >> (8 * (i >> 1) + ((i & 1) ? 0 : 4))) & 15u;
+      decode_window(a0, a1, r[0], r[1], gap, g_tb, len_off, sink);
+      // rotate the next window's words to the front
+      a0 = r[0];
+      a1 = r[1];
+#pragma unroll
+      for (int k = 0; k < 12; ++k) r[k] = r[k + 2];
+      r[12] = bswap32(in.w8.x);
+      r[13] = bswap32(in.w8.y);
+    }
+  }
+  if (sink.q4) *sink.ptr = sink.lo;
+  const std::uint32_t cnt = static_cast<std::uint32_t>(sink.ptr - my_slot) * 8 + (sink.q4 >> 2);
+
+  // ---- warp scan, segmented by reference block (2^(log2T-3) lanes each)
+  std::uint32_t incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const std::uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const std::uint32_t excl = incl - cnt;
+  const std::uint32_t lpb_mask = (1u << (log2T - 3)) - 1;  // lanes per block - 1
+  const std::uint32_t first_excl = __shfl_sync(0xffffffffu, excl, static_cast<std::uint32_t>(lane) & ~lpb_mask);
+  const std::uint32_t start_rel = static_cast<std::uint32_t>(in.o0 - in.A) + excl - first_excl;
+  const std::uint32_t lim_rel = static_cast<std::uint32_t>(in.o1 - in.A);
+  const std::uint32_t cc = (active && start_rel < lim_rel) ? min(cnt, lim_rel - start_rel) : 0u;
+  const std::uint32_t off = static_cast<std::uint32_t>(in.A & 15);  // staging nibble of element A
+  const std::uint32_t d0 = start_rel + off, dend = d0 + cc;
+  const std::uint32_t data_end = off + static_cast<std::uint32_t>(in.E - in.A);
+  __syncwarp();  // previous tile's write-back is done with the staging
+  ws.rs[lane] = d0;
+  ws.re[lane] = dend;
+
+  // ---- move my nibbles to their final place; publish partial words
+  std::uint32_t headv = 0, tailv = 0;
+  const std::uint32_t fw = d0 >> 3, lw = (dend - 1) >> 3;
+  const std::uint32_t f4 = (d0 & 7) * 4, lastn = ((dend - 1) & 7) + 1;
+  if (cc) {
+    std::uint32_t prev = my_slot[0];
+    const std::uint32_t v0 = prev << f4;
+    if (fw == lw) {
+      const std::uint32_t v = v0 & low_nibbles(lastn);
+      if (f4 == 0 && lastn == 8) ws.stage[fw] = v;
+      else headv = v;
+    } else {
+      if (f4 == 0) ws.stage[fw] = v0;
+      else headv = v0;
+      std::uint32_t j = 1;
+#pragma unroll 4
+      for (std::uint32_t k = fw + 1; k < lw; ++k, ++j) {
+        const std::uint32_t c = my_slot[j];
+        ws.stage[k] = __funnelshift_l(prev, c, f4);
+        prev = c;
+      }
+      const std::uint32_t v = __funnelshift_l(prev, my_slot[j], f4) & low_nibbles(lastn);
+      if (lastn == 8) ws.stage[lw] = v;
+      else tailv = v;
+    }
+  }
+  ws.head[lane] = headv;
+  __syncwarp();
+
+  // ---- owners assemble words shared between lanes
+  if (cc) {
+    const bool start_owner = (f4 == 0 || d0 == off) && !(f4 == 0 && (fw < lw || lastn == 8));
+    const bool tail_owner = fw != lw && lastn != 8;
+#pragma unroll
+    for (int pass = 0; pass < 2; ++pass) {
+      if (pass == 0 ? !start_owner : !tail_owner) continue;
+      const std::uint32_t k = pass == 0 ? fw : lw;
+      std::uint32_t v = pass == 0 ? headv : tailv;
+      const std::uint32_t wend = min(8 * k + 8, data_end);
+      std::uint32_t covered = dend;
+      for (int j = lane + 1; covered < wend && j < 32; ++j) {
+        const std::uint32_t rj = ws.rs[j], ej = ws.re[j];
+        if (ej > rj) {
+          v |= ws.head[j];
+          covered = ej;
+        }
+      }
+      ws.stage[k] = v;
+    }
+  }
+  __syncwarp();
+
+  // ---- write-back
+  const std::uint64_t S0 = in.A - off;
+  std::uint8_t* const out = d.out + (S0 - d.out_offset);
+  const std::uint8_t* const pk = d.packed + (S0 >> 1);
+  const std::uint32_t nch = (data_end + 15) >> 4;
+  const std::uint32_t full_lo = (off + 15) >> 4, full_hi = data_end >> 4;
+  const uint2* sp = reinterpret_cast<const uint2*>(ws.stage);
+  const uint2* pp = reinterpret_cast<const uint2*>(pk);
+  uint4* op = reinterpret_cast<uint4*>(out);
+  for (std::uint32_t c0 = full_lo + lane; c0 < full_hi; c0 += 4 * 32) {
+    uint2 q[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const std::uint32_t ci = c0 + 32 * u;
+      if (ci < full_hi) q[u] = __ldg(pp + ci);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const std::uint32_t ci = c0 + 32 * u;
+      if (ci < full_hi) {
+        const uint2 s = sp[ci];
+        uint4 r;
+        merge8(s.x, q[u].x, r.x, r.y);
+        merge8(s.y, q[u].y, r.z, r.w);
+        op[ci] = r;
+      }
+    }
+  }
+  if (lane < 2) {
+    const std::uint32_t ci = lane == 0 ? 0u : nch - 1;
+    const bool partial = lane == 0 ? (full_lo > 0 && nch > 0) : (full_hi < nch && !(nch == 1 && full_lo > 0));
+    if (partial) {
+      const std::uint32_t g16 = 16 * ci;
+      write_edge(ws.stage, out, pk, g16 < off ? off : g16, g16 + 16 < data_end ? g16 + 16 : data_end);
+    }
+  }
+}
+
+template <int NW>
+__global__ void __launch_bounds__(NW * 32, 1) decode_warp_kernel(const LaunchArgs args) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  WarpSmem& ws = reinterpret_cast<WarpSmem*>(smem_raw)[warp];
+  const std::uint64_t total_tiles = args.total_tiles;
+  const std::uint64_t t_lo = total_tiles * blockIdx.x / gridDim.x;
+  const std::uint64_t t_hi = total_tiles * (blockIdx.x + 1) / gridDim.x;
+
+  for (std::uint64_t seg = t_lo; seg < t_hi;) {
+    TensorDesc d;
+    std::uint64_t seg_end;
+    if (args.descs) {
+      const int di = find_desc(args.descs, args.n_desc, seg);
+      d = args.descs[di];
+      seg_end = (di + 1 < args.n_desc) ? args.descs[di + 1].tile_begin : total_tiles;
+    } else {
+      d = args.inline_desc;
+      seg_end = total_tiles;
+    }
+    if (seg_end > t_hi) seg_end = t_hi;
+    const std::uint32_t log2T = 31 - __clz(d.T);
+    __syncthreads();  // every warp is done with the previous tables
+    stage_tables(d, g_tb, threadIdx.x, NW * 32);
+    const std::uint32_t len_off = (d.n_luts - 1) << 8;
+    __syncthreads();
+
+    WarpIn nxt;
+    std::uint64_t tile = seg + warp;
+    if (tile < seg_end) load_warp_tile(d, tile, log2T, lane, nxt);
+    for (; tile < seg_end; tile += NW) {
+      const WarpIn cur = nxt;
+      if (lane == 0) {  // sign/mantissa bytes of this tile -> L2 (one bulk TMA prefetch)
+        const std::uint64_t p0 = (cur.A >> 1) & ~std::uint64_t{15};
+        const std::uint32_t bytes = static_cast<std::uint32_t>((((cur.E + 1) >> 1) - p0 + 15) & ~std::uint64_t{15});
+        if (bytes)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(d.packed + p0), "r"(bytes) : "memory");
+      }
+      if (tile + NW < seg_end) load_warp_tile(d, tile + NW, log2T, lane, nxt);
+      warp_tile(d, cur, log2T, len_off, ws, lane);
+    }
+    seg = seg_end;
+  }
+}
+
+template <int NW>
+cudaError_t launch_nw(const LaunchArgs& args, cudaStream_t s) {
+  static int grid_cap = 0;
+  const int smem = static_cast<int>(sizeof(WarpSmem)) * NW;
+  if (grid_cap == 0) {
+    cudaError_t e = cudaFuncSetAttribute(decode_warp_kernel<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_warp_kernel<NW>, NW * 32, smem);
+    if (e != cudaSuccess) return e;
+    grid_cap = sms * (per_sm > 0 ? per_sm : 1);
+  }
+  const std::uint64_t want = (args.total_tiles + NW - 1) / NW;
+  const std::uint64_t grid = want < static_cast<std::uint64_t>(grid_cap) ? want : grid_cap;
+  if (grid == 0) return cudaSuccess;
+  decode_warp_kernel<NW><<<static_cast<unsigned>(grid), NW * 32, smem, s>>>(args);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+// Warps per CTA: 20 x 8.7 KB of warp state + 28.6 KB of tables fill an SM;
+// ECF8_WARPS=16 trades occupancy for registers (A/B runs).
+cudaError_t launch_decode_warp(const LaunchArgs& args, cudaStream_t s) {
+  static const int nw = [] {
+    const char* e = std::getenv("ECF8_WARPS");
+    return e ? std::atoi(e) : 20;
+  }();
+  return nw == 16 ? launch_nw<16>(args, s) : launch_nw<20>(args, s);
+}
+
+}  // namespace ecf8::dev
