@@ -198,32 +198,40 @@ __device__ __forceinline__ void warp_tile(const TensorDesc& d, const WarpIn& in,
   const uint2* sp = reinterpret_cast<const uint2*>(ws.stage);
   const uint2* pp = reinterpret_cast<const uint2*>(pk);
   uint4* op = reinterpret_cast<uint4*>(out);
-  for (std::uint32_t c0 = full_lo + lane; c0 < full_hi; c0 += 4 * 32) {
+  const std::uint32_t nfull = full_hi > full_lo ? full_hi - full_lo : 0u;
+  const uint2* sl = sp + full_lo + lane;
+  const uint2* pl = pp + full_lo + lane;
+  uint4* ol = op + full_lo + lane;
+  std::uint32_t k = lane;
+  for (; k + 96 < nfull; k += 128, sl += 128, pl += 128, ol += 128) {
     uint2 q[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const std::uint32_t ci = c0 + 32 * u;
-      if (ci < full_hi) q[u] = __ldg(pp + ci);
-    }
+    for (int u = 0; u < 4; ++u) q[u] = __ldg(pl + 32 * u);  // four L2 round trips overlap
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const std::uint32_t ci = c0 + 32 * u;
-      if (ci < full_hi) {
-        const uint2 s = sp[ci];
-        uint4 r;
-        merge8(s.x, q[u].x, r.x, r.y);
-        merge8(s.y, q[u].y, r.z, r.w);
-        op[ci] = r;
-      }
+      const uint2 s = sl[32 * u];
+      uint4 r;
+      merge8(s.x, q[u].x, r.x, r.y);
+      merge8(s.y, q[u].y, r.z, r.w);
+      ol[32 * u] = r;
     }
   }
-  if (lane < 2) {
-    const std::uint32_t ci = lane == 0 ? 0u : nch - 1;
-    const bool partial = lane == 0 ? (full_lo > 0 && nch > 0) : (full_hi < nch && !(nch == 1 && full_lo > 0));
-    if (partial) {
-      const std::uint32_t g16 = 16 * ci;
-      write_edge(ws.stage, out, pk, g16 < off ? off : g16, g16 + 16 < data_end ? g16 + 16 : data_end);
-    }
+  for (; k < nfull; k += 32, sl += 32, pl += 32, ol += 32) {
+    const uint2 q = __ldg(pl);
+    const uint2 s = *sl;
+    uint4 r;
+    merge8(s.x, q.x, r.x, r.y);
+    merge8(s.y, q.y, r.z, r.w);
+    *ol = r;
+  }
+  // partial edge chunks, one byte per lane: lanes 0-15 the first chunk,
+  // lanes 16-31 the last one
+  const std::uint32_t i = lane < 16 ? static_cast<std::uint32_t>(lane) : 16 * (nch - 1) + (lane - 16);
+  const bool edge = lane < 16 ? (full_lo > 0 && i >= off && i < data_end)
+                              : (full_hi < nch && !(nch == 1 && full_lo > 0) && i < data_end);
+  if (edge) {
+    const std::uint32_t x = (ws.stage[i >> 3] >> (4 * (i & 7))) & 15u;
+    out[i] = merge1(x, pk[i >> 1], i & 1);
   }
 }
 
@@ -295,12 +303,12 @@ cudaError_t launch_nw(const LaunchArgs& args, cudaStream_t s) {
 
 }  // namespace
 
-// Warps per CTA: 20 x 8.7 KB of warp state + 28.6 KB of tables fill an SM;
-// ECF8_WARPS=16 trades occupancy for registers (A/B runs).
+// Warps per CTA: 16 (<= 128 registers, no spills); 20 x 8.7 KB of warp state
+// + 28.6 KB of tables also fit (ECF8_WARPS=20, spills at 96 registers).
 cudaError_t launch_decode_warp(const LaunchArgs& args, cudaStream_t s) {
   static const int nw = [] {
     const char* e = std::getenv("ECF8_WARPS");
-    return e ? std::atoi(e) : 20;
+    return e ? std::atoi(e) : 16;
   }();
   return nw == 16 ? launch_nw<16>(args, s) : launch_nw<20>(args, s);
 }
