@@ -125,7 +125,8 @@ __device__ __forceinline__ void decode_tile(const TensorDesc& d, const TileGeo& 
   const bool active = wl0 < g.nwin;
 
   // ---- decode my windows into my slot
-  SlotSink sink{my_slot};
+  const std::uint32_t slot_base = smem_addr(my_slot);
+  SlotSink sink{slot_base};
   if (active) {
 #pragma unroll
     for (int i = 0; i < KWIN; ++i) {
@@ -134,8 +135,7 @@ __device__ __forceinline__ void decode_tile(const TensorDesc& d, const TileGeo& 
                       bswap32(cur.win[i + 1].y), gap_of<KWIN>(cur.gaps, i, wl0 + i), tb, len_off, sink);
     }
   }
-  if (sink.q4) *sink.ptr = sink.lo;
-  const std::uint32_t cnt = static_cast<std::uint32_t>(sink.ptr - my_slot) * 8 + (sink.q4 >> 2);
+  const std::uint32_t cnt = sink.finish(slot_base);
 
   // ---- exclusive scan of the per-thread counts
   std::uint32_t incl = cnt;

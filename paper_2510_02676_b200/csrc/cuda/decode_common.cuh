@@ -31,9 +31,29 @@ __host__ __device__ constexpr std::uint32_t stage_entry(std::uint32_t e) {
   return ((e >> 5) & 31) ? e : (kSlowFlag | 1u);
 }
 
-// Packs 4-bit symbols into consecutive 32-bit words (first symbol lowest).
+// Shared-memory accesses by 32-bit shared-window address: one register per
+// address and no generic-to-shared conversion in the hot loops.
+__device__ __forceinline__ std::uint32_t smem_addr(const void* p) {
+  return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ std::uint32_t lds32(std::uint32_t a) {
+  std::uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ std::uint32_t lds16(std::uint32_t a) {
+  std::uint16_t v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts32(std::uint32_t a, std::uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
+// Packs 4-bit symbols into consecutive 32-bit words (first symbol lowest)
+// at shared address `addr`.
 struct SlotSink {
-  std::uint32_t* ptr;
+  std::uint32_t addr;    // next word
   std::uint32_t lo = 0;  // partial word
   std::uint32_t q4 = 0;  // bits used in lo, < 32
   __device__ __forceinline__ void put(std::uint32_t syms, std::uint32_t n4) {
@@ -41,12 +61,18 @@ struct SlotSink {
     const std::uint32_t nh = __funnelshift_l(syms, 0u, q4);
     q4 += n4;
     if (q4 >= 32) {
-      *ptr++ = nl;
+      sts32(addr, nl);
+      addr += 4;
       lo = nh;
       q4 -= 32;
     } else {
       lo = nl;
     }
+  }
+  // Flush the partial word; returns the symbol count since `base`.
+  __device__ __forceinline__ std::uint32_t finish(std::uint32_t base) {
+    if (q4) sts32(addr, lo);
+    return (addr - base) * 2 + (q4 >> 2);
   }
 };
 
@@ -114,14 +140,15 @@ __device__ __forceinline__ void decode_window_exact(std::uint32_t w0, std::uint3
 // refill; phase B takes whole entries until the next one would cross bit 64
 // and then exactly the symbols that start before it (start-bit mask +
 // popcount, the codec.cpp:143-160 rule).
+// fast = shared address of tb.fast, smask = shared address of tb.smask.
 __device__ __forceinline__ bool decode_window_fast(std::uint32_t w0, std::uint32_t w1, std::uint32_t w2,
-                                                   std::uint32_t w3, std::uint32_t gap,
-                                                   const Tables& tb, SlotSink& sink) {
+                                                   std::uint32_t w3, std::uint32_t gap, std::uint32_t fast,
+                                                   std::uint32_t smask, SlotSink& sink) {
   std::uint32_t hi = __funnelshift_l(w1, w0, gap);
   std::uint32_t lo = __funnelshift_l(w2, w1, gap);
   std::uint32_t p = gap, flags = 0;
   while (p < 32) {
-    const std::uint32_t e = tb.fast[hi >> kFastShift];
+    const std::uint32_t e = lds32(fast + ((hi >> (kFastShift - 2)) & ~3u));
     flags |= e;
     sink.put(e >> 12, (e >> 5) & 31);
     hi = __funnelshift_l(lo, hi, e);  // shift amount = e & 31 = bits consumed
@@ -132,11 +159,11 @@ __device__ __forceinline__ bool decode_window_fast(std::uint32_t w0, std::uint32
   lo = __funnelshift_l(w3, w2, p - 32);
   for (;;) {
     const std::uint32_t idx = hi >> kFastShift;
-    const std::uint32_t e = tb.fast[idx];
+    const std::uint32_t e = lds32(fast + 4 * idx);
     flags |= e;
     const std::uint32_t b = e & 31, r = 64 - p;
     if (b >= r) {
-      const std::uint32_t k4 = 4 * __popc(tb.smask[idx] & ((1u << r) - 1));
+      const std::uint32_t k4 = 4 * __popc(lds16(smask + 2 * idx) & ((1u << r) - 1));
       sink.put((e >> 12) & ((1u << k4) - 1), k4);
       break;
     }
@@ -152,7 +179,7 @@ __device__ __forceinline__ void decode_window(std::uint32_t w0, std::uint32_t w1
                                               std::uint32_t w3, std::uint32_t gap, const Tables& tb,
                                               std::uint32_t len_off, SlotSink& sink) {
   const SlotSink saved = sink;
-  if (!decode_window_fast(w0, w1, w2, w3, gap, tb, sink)) {
+  if (!decode_window_fast(w0, w1, w2, w3, gap, smem_addr(tb.fast), smem_addr(tb.smask), sink)) {
     sink = saved;
     decode_window_exact(w0, w1, w2, w3, gap, tb, len_off, sink);
   }

@@ -92,30 +92,25 @@ __device__ __forceinline__ void warp_tile(const TensorDesc& d, const WarpIn& in,
 
   // ---- decode my 8 windows into my slot (window words rotate through
   //      registers so the loop body is emitted once)
-  SlotSink sink{my_slot};
+  const std::uint32_t slot_base = smem_addr(my_slot);
+  SlotSink sink{slot_base};
   if (active) {
-    std::uint32_t a0 = bswap32(in.w01.x), a1 = bswap32(in.w01.y);
-    std::uint32_t r[14] = {bswap32(in.w01.z), bswap32(in.w01.w), bswap32(in.w23.x), bswap32(in.w23.y),
-                           bswap32(in.w23.z), bswap32(in.w23.w), bswap32(in.w45.x), bswap32(in.w45.y),
-                           bswap32(in.w45.z), bswap32(in.w45.w), bswap32(in.w67.x), bswap32(in.w67.y),
-                           bswap32(in.w67.z), bswap32(in.w67.w)};
+    const std::uint32_t w[18] = {bswap32(in.w01.x), bswap32(in.w01.y), bswap32(in.w01.z), bswap32(in.w01.w),
+                                 bswap32(in.w23.x), bswap32(in.w23.y), bswap32(in.w23.z), bswap32(in.w23.w),
+                                 bswap32(in.w45.x), bswap32(in.w45.y), bswap32(in.w45.z), bswap32(in.w45.w),
+                                 bswap32(in.w67.x), bswap32(in.w67.y), bswap32(in.w67.z), bswap32(in.w67.w),
+                                 bswap32(in.w8.x),  bswap32(in.w8.y)};
     const std::uint32_t n = min(in.nwin - wl0, static_cast<std::uint32_t>(kLaneWin));
-#pragma unroll 1
-    for (std::uint32_t i = 0; i < n; ++i) {
-      // byte j of the gap word: window 2j in the high nibble, 2j + 1 low
-      const std::uint32_t gap = (in.gaps >> (8 * (i >> 1) + ((i & 1) ? 0 : 4))) & 15u;
-      decode_window(a0, a1, r[0], r[1], gap, g_tb, len_off, sink);
-      // rotate the next window's words to the front
-      a0 = r[0];
-      a1 = r[1];
 #pragma unroll
-      for (int k = 0; k < 12; ++k) r[k] = r[k + 2];
-      r[12] = bswap32(in.w8.x);
-      r[13] = bswap32(in.w8.y);
+    for (int i = 0; i < kLaneWin; ++i) {
+      if (static_cast<std::uint32_t>(i) < n) {
+        // byte j of the gap word: window 2j in the high nibble, 2j + 1 low
+        const std::uint32_t gap = (in.gaps >> (8 * (i >> 1) + ((i & 1) ? 0 : 4))) & 15u;
+        decode_window(w[2 * i], w[2 * i + 1], w[2 * i + 2], w[2 * i + 3], gap, g_tb, len_off, sink);
+      }
     }
   }
-  if (sink.q4) *sink.ptr = sink.lo;
-  const std::uint32_t cnt = static_cast<std::uint32_t>(sink.ptr - my_slot) * 8 + (sink.q4 >> 2);
+  const std::uint32_t cnt = sink.finish(slot_base);
 
   // ---- warp scan, segmented by reference block (2^(log2T-3) lanes each)
   std::uint32_t incl = cnt;
