@@ -175,104 +175,6 @@ __device__ __forceinline__ bool decode_window_fast(std::uint32_t w0, std::uint32
   return !(flags & kSlowFlag);
 }
 
-// Two independent windows walked in lockstep (two dependency chains per
-// thread).  Each chain is the branch-free fast walk above; a finished or
-// absent chain is fed the null entry (b = n = 0), which is a no-op.
-struct Walk {
-  std::uint32_t hi, lo, p, flags;
-  bool live;
-};
-
-__device__ __forceinline__ Walk walk_begin(std::uint32_t w0, std::uint32_t w1, std::uint32_t w2,
-                                           std::uint32_t gap, bool live) {
-  return Walk{__funnelshift_l(w1, w0, gap), __funnelshift_l(w2, w1, gap), gap, 0u, live};
-}
-
-__device__ __forceinline__ void walk_step_a(Walk& s, std::uint32_t fast, SlotSink& sink) {
-  const std::uint32_t e0 = lds32(fast + ((s.hi >> (kFastShift - 2)) & ~3u));
-  const std::uint32_t e = (s.live && s.p < 32) ? e0 : 0u;
-  s.flags |= e;
-  sink.put(e >> 12, (e >> 5) & 31);
-  s.hi = __funnelshift_l(s.lo, s.hi, e);
-  s.lo = __funnelshift_l(0u, s.lo, e);
-  s.p += e & 31;
-}
-
-__device__ __forceinline__ void walk_refill(Walk& s, std::uint32_t w1, std::uint32_t w2, std::uint32_t w3) {
-  const std::uint32_t sh = s.p - 32;  // p in [32, 44) for live walks
-  s.hi = __funnelshift_l(w2, w1, sh);
-  s.lo = __funnelshift_l(w3, w2, sh);
-}
-
-__device__ __forceinline__ void walk_step_b(Walk& s, std::uint32_t fast, std::uint32_t smask, SlotSink& sink) {
-  const std::uint32_t idx = s.hi >> kFastShift;
-  const std::uint32_t e0 = lds32(fast + 4 * idx);
-  const std::uint32_t e = s.live ? e0 : 0u;
-  s.flags |= e;
-  const std::uint32_t b = e & 31, r = 64 - s.p;
-  const bool tail = b >= r;  // never for a dead walk (b = 0 < r)
-  std::uint32_t syms = e >> 12, k4 = (e >> 5) & 31;
-  if (tail) {  // only the symbols that start before bit 64
-    k4 = 4 * __popc(lds16(smask + 2 * idx) & ((1u << (r < 16 ? r : 16)) - 1));
-    syms &= (1u << k4) - 1;
-    s.live = false;
-  }
-  sink.put(syms, k4);
-  s.hi = __funnelshift_l(s.lo, s.hi, e);
-  s.lo = __funnelshift_l(0u, s.lo, e);
-  s.p += b;
-}
-
-// Windows (a0..a3, ga) -> sink_a and (b0..b3, gb) -> sink_b, interleaved.
-// Flagged windows are rewound and decoded by the exact walk.
-__device__ __forceinline__ void decode_window_pair(const std::uint32_t* wa, std::uint32_t ga, bool la,
-                                                   SlotSink& sa, const std::uint32_t* wb, std::uint32_t gb,
-                                                   bool lb, SlotSink& sb, const Tables& tb,
-                                                   std::uint32_t fast, std::uint32_t smask,
-                                                   std::uint32_t len_off) {
-  const SlotSink save_a = sa, save_b = sb;
-  Walk A = walk_begin(wa[0], wa[1], wa[2], ga, la);
-  Walk B = walk_begin(wb[0], wb[1], wb[2], gb, lb);
-  while ((A.live && A.p < 32) || (B.live && B.p < 32)) {
-    walk_step_a(A, fast, sa);
-    walk_step_a(B, fast, sb);
-  }
-  walk_refill(A, wa[1], wa[2], wa[3]);
-  walk_refill(B, wb[1], wb[2], wb[3]);
-  while (A.live || B.live) {
-    walk_step_b(A, fast, smask, sa);
-    walk_step_b(B, fast, smask, sb);
-  }
-  if (la && (A.flags & kSlowFlag)) {
-    sa = save_a;
-    decode_window_exact(wa[0], wa[1], wa[2], wa[3], ga, tb, len_off, sa);
-  }
-  if (lb && (B.flags & kSlowFlag)) {
-    sb = save_b;
-    decode_window_exact(wb[0], wb[1], wb[2], wb[3], gb, tb, len_off, sb);
-  }
-}
-
-// Appends the `nb` nibbles at slot words [src, ...) to the `na` nibbles at
-// slot words [dst, ...) (shared addresses; dst + na/8 <= src, so every
-// source word is read before it can be overwritten).
-__device__ __forceinline__ void join_nibbles(std::uint32_t dst, std::uint32_t na, std::uint32_t src,
-                                             std::uint32_t nb) {
-  if (nb == 0) return;
-  const std::uint32_t f4 = (na & 7) * 4;
-  std::uint32_t at = dst + 4 * (na >> 3);
-  const std::uint32_t nw = (nb + 7) >> 3;
-  std::uint32_t prev = f4 ? (lds32(at) & ((1u << f4) - 1)) : 0u;  // head of the first piece
-  std::uint32_t carry = prev;
-  for (std::uint32_t k = 0; k < nw; ++k, at += 4) {
-    const std::uint32_t cur = lds32(src + 4 * k);
-    sts32(at, (cur << f4) | carry);
-    carry = f4 ? (cur >> (32 - f4)) : 0u;
-  }
-  if (f4) sts32(at, carry);
-  (void)prev;
-}
-
 __device__ __forceinline__ void decode_window(std::uint32_t w0, std::uint32_t w1, std::uint32_t w2,
                                               std::uint32_t w3, std::uint32_t gap, const Tables& tb,
                                               std::uint32_t len_off, SlotSink& sink) {

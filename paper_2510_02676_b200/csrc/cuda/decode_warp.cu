@@ -92,12 +92,8 @@ __device__ __forceinline__ void warp_tile(const TensorDesc& d, const WarpIn& in,
 
   // ---- decode my 8 windows into my slot (window words rotate through
   //      registers so the loop body is emitted once)
-  // Windows i and i + 4 are walked together (two dependency chains per
-  // lane); window i's symbols go to slot words [0, 16), window i + 4's to
-  // [16, 32), then the second run is appended to the first.
   const std::uint32_t slot_base = smem_addr(my_slot);
-  const std::uint32_t half = slot_base + 4 * (WarpSmem::kSlotW / 2);
-  SlotSink sa{slot_base}, sb{half};
+  SlotSink sink{slot_base};
   if (active) {
     const std::uint32_t w[18] = {bswap32(in.w01.x), bswap32(in.w01.y), bswap32(in.w01.z), bswap32(in.w01.w),
                                  bswap32(in.w23.x), bswap32(in.w23.y), bswap32(in.w23.z), bswap32(in.w23.w),
@@ -105,19 +101,16 @@ __device__ __forceinline__ void warp_tile(const TensorDesc& d, const WarpIn& in,
                                  bswap32(in.w67.x), bswap32(in.w67.y), bswap32(in.w67.z), bswap32(in.w67.w),
                                  bswap32(in.w8.x),  bswap32(in.w8.y)};
     const std::uint32_t n = min(in.nwin - wl0, static_cast<std::uint32_t>(kLaneWin));
-    const std::uint32_t fast = smem_addr(g_tb.fast), smask = smem_addr(g_tb.smask);
 #pragma unroll
-    for (int i = 0; i < kLaneWin / 2; ++i) {
-      // byte j of the gap word: window 2j in the high nibble, 2j + 1 low
-      const std::uint32_t ga = (in.gaps >> (8 * (i >> 1) + ((i & 1) ? 0 : 4))) & 15u;
-      const std::uint32_t gb = (in.gaps >> (8 * ((i + 4) >> 1) + ((i & 1) ? 0 : 4))) & 15u;
-      decode_window_pair(&w[2 * i], ga, static_cast<std::uint32_t>(i) < n, sa, &w[2 * i + 8], gb,
-                         static_cast<std::uint32_t>(i + 4) < n, sb, g_tb, fast, smask, len_off);
+    for (int i = 0; i < kLaneWin; ++i) {
+      if (static_cast<std::uint32_t>(i) < n) {
+        // byte j of the gap word: window 2j in the high nibble, 2j + 1 low
+        const std::uint32_t gap = (in.gaps >> (8 * (i >> 1) + ((i & 1) ? 0 : 4))) & 15u;
+        decode_window(w[2 * i], w[2 * i + 1], w[2 * i + 2], w[2 * i + 3], gap, g_tb, len_off, sink);
+      }
     }
   }
-  const std::uint32_t cnt_a = sa.finish(slot_base), cnt_b = sb.finish(half);
-  join_nibbles(slot_base, cnt_a, half, cnt_b);
-  const std::uint32_t cnt = cnt_a + cnt_b;
+  const std::uint32_t cnt = sink.finish(slot_base);
 
   // ---- warp scan, segmented by reference block (2^(log2T-3) lanes each)
   std::uint32_t incl = cnt;
@@ -310,7 +303,7 @@ cudaError_t launch_nw(const LaunchArgs& args, cudaStream_t s) {
 cudaError_t launch_decode_warp(const LaunchArgs& args, cudaStream_t s) {
   static const int nw = [] {
     const char* e = std::getenv("ECF8_WARPS");
-    return e ? std::atoi(e) : 20;
+    return e ? std::atoi(e) : 16;
   }();
   return nw == 16 ? launch_nw<16>(args, s) : launch_nw<20>(args, s);
 }
