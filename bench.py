@@ -69,8 +69,12 @@ def build_layer(layer: int, nthreads: int = 0):
 
 
 def shard_layers(rank: int, world: int, n_layers: int):
-    """Weak scaling: rank r owns layers [r*n, (r+1)*n) of a world*n-layer stack."""
-    return list(range(rank * n_layers, (rank + 1) * n_layers))
+    """Weak scaling: a world*n-layer stack, LPT-partitioned by layer cost
+    (paper_2510_02676_b200/shard.py); equal layers give each rank n of them."""
+    from paper_2510_02676_b200.shard import ShardPlan
+
+    per_layer = sum(r * c for _, r, c in LLAMA8B)
+    return ShardPlan.build([per_layer] * (world * n_layers), rank, world, "lpt").mine
 
 
 # ------------------------------------------------------------- clock probe
@@ -172,6 +176,11 @@ def load_peaks():
             d = json.load(f)
         return float(d["hbm_gbs"]), "measured"
     return 6650.0, "fallback"
+
+
+def kernel_name():
+    nw = os.environ.get("ECF8_WARPS", "20")
+    return "decode_kernel<4,16,3>" if os.environ.get("ECF8_NO_WARP_KERNEL") == "1" else f"decode_warp_kernel<{nw}>"
 
 
 def load_traffic():
@@ -399,7 +408,7 @@ def main():
             },
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic, "peak_kind": peak_kind,
-                         "kernel": "ecf8 decode_kernel<1>", "algorithmic_bytes_per_launch": int(per_launch_bytes)},
+                         "kernel": kernel_name(), "algorithmic_bytes_per_launch": int(per_launch_bytes)},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clocks,

@@ -146,8 +146,10 @@ void decode_block(const EncodedTensor& t, const CascadedLut& lut, std::uint64_t 
 }
 
 void decode_parallel_into(const EncodedTensor& t, const CascadedLut& lut, std::span<Fp8Byte> out) {
-  (void)lut;
-  const ecf8_sections sec = host::sections_of(t);
+  // The reference decodes with the caller's LUT (codec.cpp:256-273); the
+  // device rebuilds the same tables from the LUT's symbol->length map.
+  ecf8_sections sec = host::sections_of(t);
+  host::lengths_from_lut(lut, sec.lengths);
   host::check(ecf8_decode_host(&sec, out.data(), out.size()));
 }
 
