@@ -337,7 +337,7 @@ def main():
 
     # ---- e2e: host buffers through the drop-in C ABI call
     e2e = None
-    if rank == 0 or True:
+    if args.e2e_steps > 0:
         import ctypes as C
 
         # pin the host sections once (the contract: inputs from pinned host memory)
