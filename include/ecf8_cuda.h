@@ -67,6 +67,13 @@ const char *ecf8_build_info(void);
  * stages the sections to the device, decodes on the B200, copies `out` back. */
 int ecf8_decode_host(const ecf8_sections *host, uint8_t *out, uint64_t out_len);
 
+/* decode_parallel_into for many tensors in one call (a layer, or a whole
+ * container as in decompress_streaming, container.cpp:324-352): the chunked
+ * H2D / decode / D2H pipeline runs across tensor boundaries instead of
+ * draining after each tensor.  Same validation and messages per tensor. */
+int ecf8_decode_host_many(const ecf8_sections *const *host, uint8_t *const *outs, const uint64_t *out_lens,
+                          int count);
+
 /* Replaces ecf8::decode_block (codec.cpp:201-254): decodes block `block`
  * into out[outpos[block], outpos[block+1]). out_len must be n_elem. */
 int ecf8_decode_block_host(const ecf8_sections *host, uint64_t block, uint8_t *out,

@@ -82,6 +82,7 @@ _SIGS = {
     "ecf8_device_count": (C.c_int, []),
     "ecf8_build_info": (C.c_char_p, []),
     "ecf8_decode_host": (C.c_int, [C.POINTER(Sections), _P, C.c_uint64]),
+    "ecf8_decode_host_many": (C.c_int, [C.POINTER(C.POINTER(Sections)), C.POINTER(_P), C.POINTER(C.c_uint64), C.c_int]),
     "ecf8_decode_block_host": (C.c_int, [C.POINTER(Sections), C.c_uint64, _P, C.c_uint64]),
     "ecf8_count_window": (C.c_int, [_P, C.c_uint, _P, _U32P]),
     "ecf8_tensor_upload": (C.c_int, [C.POINTER(Sections), _P, C.POINTER(_P)]),

@@ -206,6 +206,28 @@ def decode_parallel(t: EncodedTensor) -> np.ndarray:
     return out
 
 
+def decode_many_into(ts: list[EncodedTensor], outs: list[np.ndarray]) -> None:
+    """decode_parallel_into for a list of tensors in one pipelined call
+    (ecf8_decode_host_many): host -> B200 -> host, overlapped across tensors."""
+    if len(ts) != len(outs):
+        raise ValueError("one output per tensor")
+    for o in outs:
+        if o.dtype != np.uint8 or not o.flags.c_contiguous:
+            raise ValueError("out must be a contiguous uint8 array")
+    n = len(ts)
+    secs = [t.sections() for t in ts]
+    sp = (C.POINTER(Sections) * n)(*[C.pointer(s) for s in secs])
+    op = (C.c_void_p * n)(*[_ptr(o) for o in outs])
+    lens = (C.c_uint64 * n)(*[o.size for o in outs])
+    check(lib.ecf8_decode_host_many(sp, op, lens, n))
+
+
+def decode_many(ts: list[EncodedTensor]) -> list[np.ndarray]:
+    outs = [np.empty(t.n_elem, np.uint8) for t in ts]
+    decode_many_into(ts, outs)
+    return outs
+
+
 def decode_block(t: EncodedTensor, block: int, out: np.ndarray) -> None:
     s = t.sections()
     check(lib.ecf8_decode_block_host(C.byref(s), block, _ptr(out), out.size))

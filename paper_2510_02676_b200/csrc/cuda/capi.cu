@@ -223,16 +223,21 @@ int launch_one(const TensorDesc& d, cudaStream_t st) {
 }
 
 // Per-thread state of the host-span path: three streams (copy-in, decode,
-// copy-out), grow-only device buffers.  Deliberately never freed: CUDA may
-// already be torn down when thread_local destructors run at exit.
+// copy-out) and a ring of chunk slots in HBM.  Deliberately never freed:
+// CUDA may already be torn down when thread_local destructors run at exit.
 struct HostCtx {
+  static constexpr int kSlots = 4;
+  static constexpr std::uint64_t kEncChunk = std::uint64_t{2} << 20;   // encoded bytes per chunk
+  static constexpr std::uint64_t kElemChunk = std::uint64_t{8} << 20;  // elements per chunk
+  static constexpr std::uint64_t kSlack = 4096;
   int dev = -1;
   cudaStream_t s_in = nullptr, s_run = nullptr, s_out = nullptr;
-  std::vector<cudaEvent_t> ev_in, ev_run;
-  std::uint8_t* arena = nullptr;
-  std::uint64_t arena_cap = 0;
-  std::uint8_t* dout = nullptr;
-  std::uint64_t dout_cap = 0;
+  struct Slot {
+    std::uint8_t *enc, *gaps, *pak, *out;
+    std::uint64_t* pos;
+    cudaEvent_t in, run, out_done;
+    bool used;
+  } slot[kSlots]{};
 };
 
 HostCtx& host_ctx() {
@@ -241,89 +246,112 @@ HostCtx& host_ctx() {
   cu(cudaGetDevice(&dev), "cudaGetDevice");
   if (c.dev != dev) {
     c = HostCtx{};
-    c.dev = dev;
     cu(cudaStreamCreateWithFlags(&c.s_in, cudaStreamNonBlocking), "stream");
     cu(cudaStreamCreateWithFlags(&c.s_run, cudaStreamNonBlocking), "stream");
     cu(cudaStreamCreateWithFlags(&c.s_out, cudaStreamNonBlocking), "stream");
+    const std::uint64_t S = HostCtx::kSlack;
+    const std::uint64_t b_enc = align_up(HostCtx::kEncChunk + ecf8::dev::kTileBytesMax + S, 256);
+    const std::uint64_t b_gap = align_up(b_enc / 16 + S, 256);
+    const std::uint64_t b_pos = align_up(8 * (b_enc / 8 + 2) + S, 256);
+    const std::uint64_t b_pak = align_up(HostCtx::kElemChunk / 2 + ecf8::dev::kTileElemsMax + S, 256);
+    const std::uint64_t b_out = align_up(HostCtx::kElemChunk + 2 * ecf8::dev::kTileElemsMax + S, 256);
+    for (auto& sl : c.slot) {
+      void* p = nullptr;
+      cu(cudaMalloc(&p, b_enc + b_gap + b_pos + b_pak + b_out), "cudaMalloc(staging)");
+      cu(cudaMemset(p, 0, b_enc + b_gap + b_pos + b_pak + b_out), "cudaMemset(staging)");
+      auto* base = static_cast<std::uint8_t*>(p);
+      sl.enc = base;
+      sl.gaps = base + b_enc;
+      sl.pos = reinterpret_cast<std::uint64_t*>(base + b_enc + b_gap);
+      sl.pak = base + b_enc + b_gap + b_pos;
+      sl.out = base + b_enc + b_gap + b_pos + b_pak;
+      cu(cudaEventCreateWithFlags(&sl.in, cudaEventDisableTiming), "event");
+      cu(cudaEventCreateWithFlags(&sl.run, cudaEventDisableTiming), "event");
+      cu(cudaEventCreateWithFlags(&sl.out_done, cudaEventDisableTiming), "event");
+      sl.used = false;
+    }
+    c.dev = dev;
   }
   return c;
 }
 
-void ensure(std::uint8_t** p, std::uint64_t* cap, std::uint64_t need) {
-  if (need <= *cap) return;
-  if (*p) cudaFree(*p);
-  *p = nullptr;
-  *cap = 0;
-  cu(cudaMalloc(p, need), "cudaMalloc(staging)");
-  cu(cudaMemset(*p, 0, need), "cudaMemset(staging)");
-  *cap = need;
+// Pointer whose element `lo` is `slot` (the kernels index sections with
+// global block / window / element numbers; only [lo, hi) is dereferenced).
+template <class P>
+P rebase(P slot, std::uint64_t lo_bytes) {
+  return reinterpret_cast<P>(reinterpret_cast<std::uintptr_t>(slot) - lo_bytes);
 }
 
-// decode_parallel_into on host spans: the tensor is cut into chunks of whole
-// tiles; chunk c's sections go H2D on s_in while chunk c-1 decodes on s_run
-// and chunk c-2's bytes come back on s_out.  With pinned host memory the
-// two PCIe directions and the decode overlap.
-int host_pipeline(const ecf8_sections* s, std::uint64_t nb, std::uint8_t* out) {
+// decode_parallel_into on host spans, for one or many tensors: every tensor
+// is cut into chunks of whole tiles (<= 2 MB encoded, <= 8 M elements);
+// chunk k's sections go H2D on s_in into slot k%4 while chunk k-1 decodes
+// on s_run and chunk k-2's bytes come back on s_out, across tensor
+// boundaries.  With pinned host memory both PCIe directions and the
+// decode overlap; the call returns when every byte is in `outs`.
+int host_pipeline(const ecf8_sections* const* ss, const std::uint64_t* nbs, std::uint8_t* const* outs, int count) {
   HostCtx& c = host_ctx();
-  const std::uint64_t P = ecf8::dev::kPad;
-  const std::uint64_t off_gap = align_up(s->encoded_len + P, 256);
-  const std::uint64_t off_pos = align_up(off_gap + s->gaps_len + P, 256);
-  const std::uint64_t off_pak = align_up(off_pos + 8 * s->n_outpos, 256);
-  const std::uint64_t total = align_up(off_pak + s->packed_len + P, 256);
-  ensure(&c.arena, &c.arena_cap, total);
-  ensure(&c.dout, &c.dout_cap, align_up(s->n_elem, 16) + 16);
+  std::uint64_t k = 0;
+  for (int i = 0; i < count; ++i) {
+    const ecf8_sections* s = ss[i];
+    const std::uint64_t nb = nbs[i];
+    if (s->n_elem == 0) continue;
+    std::uint8_t* const out = outs[i];
+    const std::uint32_t T = s->threads_per_block;
+    const ecf8::dev::Variant v = ecf8::dev::variant_for(T, lmin_of(s->lengths));
+    const std::uint64_t m = ecf8::dev::blocks_per_tile(T, v.tile_win);
+    const std::uint64_t tile_enc = m * T * 8;
+    const DevTables& tb = device_tables(s->lengths);
+    TensorDesc d{};
+    d.n_elem = s->n_elem;
+    d.T = T;
+    d.fast = tb.fast;
+    d.smask = tb.smask;
+    d.cascade = tb.cascade;
+    d.n_luts = tb.n_luts;
+    d.lenpack = tb.lenpack;
+    d.lmin = lmin_of(s->lengths);
+    for (std::uint64_t lo = 0; lo < nb; ++k) {
+      // grow the chunk tile by tile up to the slot limits
+      std::uint64_t hi = std::min(nb, lo + m);
+      while (hi < nb) {
+        const std::uint64_t nh = std::min(nb, hi + m);
+        if ((nh - lo) * T * 8 > HostCtx::kEncChunk || s->outpos[nh] - s->outpos[lo] > HostCtx::kElemChunk) break;
+        hi = nh;
+      }
+      (void)tile_enc;
+      HostCtx::Slot& sl = c.slot[k % HostCtx::kSlots];
+      if (sl.used) cu(cudaStreamWaitEvent(c.s_in, sl.out_done, 0), "wait");
+      sl.used = true;
+      const std::uint64_t e0 = lo * T * 8, e1 = hi * T * 8 + 2;
+      cu(cudaMemcpyAsync(sl.enc, s->encoded + e0, e1 - e0, cudaMemcpyHostToDevice, c.s_in), "H2D encoded");
+      const std::uint64_t g0 = lo * T / 2, g1 = std::min(s->gaps_len, (hi * T + 1) / 2);
+      if (g1 > g0) cu(cudaMemcpyAsync(sl.gaps, s->gaps + g0, g1 - g0, cudaMemcpyHostToDevice, c.s_in), "H2D gaps");
+      cu(cudaMemcpyAsync(sl.pos, s->outpos + lo, 8 * (hi - lo + 1), cudaMemcpyHostToDevice, c.s_in), "H2D outpos");
+      const std::uint64_t o0 = s->outpos[lo], o1 = s->outpos[hi];
+      const std::uint64_t p0 = (o0 / 2) & ~std::uint64_t{15}, p1 = std::min(s->packed_len, (o1 + 1) / 2);
+      if (p1 > p0) cu(cudaMemcpyAsync(sl.pak, s->packed + p0, p1 - p0, cudaMemcpyHostToDevice, c.s_in), "H2D packed");
+      cu(cudaEventRecord(sl.in, c.s_in), "record");
 
-  const std::uint32_t T = s->threads_per_block;
-  const std::uint64_t m = ecf8::dev::blocks_per_tile(T, ecf8::dev::variant_for(T, lmin_of(s->lengths)).tile_win);
-  const std::uint64_t target = std::uint64_t{8} << 20;
-  std::uint64_t per = std::max<std::uint64_t>(m, target / (std::uint64_t{T} * 8) / m * m);
-  if (s->encoded_len < 2 * target) per = nb;
-  const std::uint64_t n_chunks = (nb + per - 1) / per;
-  while (c.ev_in.size() < n_chunks) {
-    cudaEvent_t a, b;
-    cu(cudaEventCreateWithFlags(&a, cudaEventDisableTiming), "event");
-    cu(cudaEventCreateWithFlags(&b, cudaEventDisableTiming), "event");
-    c.ev_in.push_back(a);
-    c.ev_run.push_back(b);
-  }
+      cu(cudaStreamWaitEvent(c.s_run, sl.in, 0), "wait");
+      TensorDesc dk = d;
+      dk.encoded = rebase(static_cast<const std::uint8_t*>(sl.enc), e0);
+      dk.gaps = rebase(static_cast<const std::uint8_t*>(sl.gaps), g0);
+      dk.outpos = rebase(static_cast<const std::uint64_t*>(sl.pos), 8 * lo);
+      dk.packed = rebase(static_cast<const std::uint8_t*>(sl.pak), p0);
+      dk.out = sl.out;
+      dk.out_offset = o0 & ~std::uint64_t{15};
+      dk.blk_begin = lo;
+      dk.blk_end = hi;
+      if (int rc = launch_one(dk, c.s_run)) return rc;
+      cu(cudaEventRecord(sl.run, c.s_run), "record");
 
-  TensorDesc d{};
-  d.encoded = c.arena;
-  d.gaps = c.arena + off_gap;
-  d.outpos = reinterpret_cast<const std::uint64_t*>(c.arena + off_pos);
-  d.packed = c.arena + off_pak;
-  d.out = c.dout;
-  d.n_elem = s->n_elem;
-  d.T = T;
-  const DevTables& tb = device_tables(s->lengths);
-  d.fast = tb.fast;
-  d.smask = tb.smask;
-  d.cascade = tb.cascade;
-  d.n_luts = tb.n_luts;
-  d.lenpack = tb.lenpack;
-  d.lmin = lmin_of(s->lengths);
-
-  cu(cudaMemcpyAsync(c.arena + off_pos, s->outpos, 8 * s->n_outpos, cudaMemcpyHostToDevice, c.s_in), "H2D outpos");
-  for (std::uint64_t k = 0; k < n_chunks; ++k) {
-    const std::uint64_t lo = k * per, hi = std::min(nb, lo + per);
-    const std::uint64_t e0 = lo * T * 8, e1 = hi * T * 8 + 2;
-    cu(cudaMemcpyAsync(c.arena + e0, s->encoded + e0, e1 - e0, cudaMemcpyHostToDevice, c.s_in), "H2D encoded");
-    const std::uint64_t g0 = lo * T / 2, g1 = std::min(s->gaps_len, (hi * T + 1) / 2);
-    if (g1 > g0) cu(cudaMemcpyAsync(c.arena + off_gap + g0, s->gaps + g0, g1 - g0, cudaMemcpyHostToDevice, c.s_in), "H2D gaps");
-    const std::uint64_t p0 = s->outpos[lo] / 2, p1 = std::min(s->packed_len, (s->outpos[hi] + 1) / 2);
-    if (p1 > p0) cu(cudaMemcpyAsync(c.arena + off_pak + p0, s->packed + p0, p1 - p0, cudaMemcpyHostToDevice, c.s_in), "H2D packed");
-    cu(cudaEventRecord(c.ev_in[k], c.s_in), "record");
-
-    cu(cudaStreamWaitEvent(c.s_run, c.ev_in[k], 0), "wait");
-    TensorDesc dk = d;
-    dk.blk_begin = lo;
-    dk.blk_end = hi;
-    if (int rc = launch_one(dk, c.s_run)) return rc;
-    cu(cudaEventRecord(c.ev_run[k], c.s_run), "record");
-
-    cu(cudaStreamWaitEvent(c.s_out, c.ev_run[k], 0), "wait");
-    const std::uint64_t o0 = s->outpos[lo], o1 = s->outpos[hi];
-    if (o1 > o0) cu(cudaMemcpyAsync(out + o0, c.dout + o0, o1 - o0, cudaMemcpyDeviceToHost, c.s_out), "D2H out");
+      cu(cudaStreamWaitEvent(c.s_out, sl.run, 0), "wait");
+      if (o1 > o0)
+        cu(cudaMemcpyAsync(out + o0, sl.out + (o0 - dk.out_offset), o1 - o0, cudaMemcpyDeviceToHost, c.s_out),
+           "D2H out");
+      cu(cudaEventRecord(sl.out_done, c.s_out), "record");
+      lo = hi;
+    }
   }
   cu(cudaStreamSynchronize(c.s_out), "sync");
   return ECF8_OK;
@@ -462,7 +490,26 @@ int ecf8_decode_host(const ecf8_sections* s, uint8_t* out, uint64_t out_len) {
     if (int rc = validate(s, &nb)) return rc;
     if (s->n_elem == 0) return ECF8_OK;
     if (int rc = require_device()) return rc;
-    return host_pipeline(s, nb, out);
+    return host_pipeline(&s, &nb, &out, 1);
+  });
+}
+
+int ecf8_decode_host_many(const ecf8_sections* const* ss, uint8_t* const* outs, const uint64_t* out_lens,
+                          int count) {
+  return guarded([&]() -> int {
+    if (count < 0 || (count > 0 && (!ss || !outs || !out_lens))) return fail(ECF8_EINVAL, "null argument");
+    std::vector<std::uint64_t> nbs(static_cast<std::size_t>(count));
+    bool any = false;
+    for (int i = 0; i < count; ++i) {
+      if (!ss[i]) return fail(ECF8_EINVAL, "null sections");
+      if (out_lens[i] != ss[i]->n_elem) return fail(ECF8_EINVAL, "output size mismatch");
+      if (int rc = validate(ss[i], &nbs[i])) return rc;
+      if (ss[i]->n_elem && !outs[i]) return fail(ECF8_EINVAL, "null argument");
+      any |= ss[i]->n_elem > 0;
+    }
+    if (!any) return ECF8_OK;
+    if (int rc = require_device()) return rc;
+    return host_pipeline(ss, nbs.data(), outs, count);
   });
 }
 

@@ -32,6 +32,9 @@ struct TensorDesc {
 
 constexpr int kThreads = 256;  // threads of one tile group (a CTA runs several groups)
 constexpr std::uint64_t kPad = 64;
+// Largest tile of any variant: 1024 windows -> 8 KB encoded, <= 64 Ki elements.
+constexpr std::uint64_t kTileBytesMax = 1024 * 8;
+constexpr std::uint64_t kTileElemsMax = 1024 * 64;
 
 // Kernel variant.  A thread decodes KWIN consecutive windows (always inside
 // one reference block) into a private slot of SLOTW 32-bit words; a tile is
