@@ -7,6 +7,8 @@
 
 #include <algorithm>
 #include <array>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -227,17 +229,31 @@ int launch_one(const TensorDesc& d, cudaStream_t st) {
 // CUDA may already be torn down when thread_local destructors run at exit.
 struct HostCtx {
   static constexpr int kSlots = 4;
-  static constexpr std::uint64_t kEncChunk = std::uint64_t{2} << 20;   // encoded bytes per chunk
-  static constexpr std::uint64_t kElemChunk = std::uint64_t{8} << 20;  // elements per chunk
+  // Chunk limits.  PCIe copies pay ~15 us each, so chunks are large (32 M
+  // elements = 32 MB D2H) in the steady state and ramp from 4 M at the start
+  // and towards the end of a call (short pipeline fill and drain).  Measured
+  // on one Llama-8B layer (tools/e2e_probe.py): 2/16 M 62 GB/s, 4/16 M 70,
+  // 4/32 M 73, 4/64 M 71.
+  static constexpr std::uint64_t kEncChunk = std::uint64_t{8} << 20;    // encoded bytes per chunk (min)
+  static constexpr std::uint64_t kElemChunk = std::uint64_t{32} << 20;  // elements per chunk
+  static constexpr std::uint64_t kElemMin = std::uint64_t{4} << 20;
+  std::uint64_t elem_chunk = kElemChunk, elem_min = kElemMin, enc_chunk = kEncChunk;  // ECF8_CHUNK_M / ECF8_CHUNK_MIN_M (M elements)
   static constexpr std::uint64_t kSlack = 4096;
   int dev = -1;
   cudaStream_t s_in = nullptr, s_run = nullptr, s_out = nullptr;
   struct Slot {
-    std::uint8_t *enc, *gaps, *pak, *out;
-    std::uint64_t* pos;
+    std::uint8_t *enc, *pak, *out;
     cudaEvent_t in, run, out_done;
     bool used;
   } slot[kSlots]{};
+  // Per-tensor gaps + outpos (one copy each per tensor, not per chunk),
+  // double-buffered by tensor parity.
+  struct Meta {
+    std::uint8_t* buf = nullptr;
+    std::uint64_t cap = 0;
+    cudaEvent_t done = nullptr;
+    bool used = false;
+  } meta[2];
 };
 
 HostCtx& host_ctx() {
@@ -249,27 +265,27 @@ HostCtx& host_ctx() {
     cu(cudaStreamCreateWithFlags(&c.s_in, cudaStreamNonBlocking), "stream");
     cu(cudaStreamCreateWithFlags(&c.s_run, cudaStreamNonBlocking), "stream");
     cu(cudaStreamCreateWithFlags(&c.s_out, cudaStreamNonBlocking), "stream");
+    if (const char* e = std::getenv("ECF8_CHUNK_M")) c.elem_chunk = std::min<std::uint64_t>(std::atoi(e), 128) << 20;
+    if (const char* e = std::getenv("ECF8_CHUNK_MIN_M")) c.elem_min = std::min<std::uint64_t>(std::atoi(e), 16) << 20;
     const std::uint64_t S = HostCtx::kSlack;
-    const std::uint64_t b_enc = align_up(HostCtx::kEncChunk + ecf8::dev::kTileBytesMax + S, 256);
-    const std::uint64_t b_gap = align_up(b_enc / 16 + S, 256);
-    const std::uint64_t b_pos = align_up(8 * (b_enc / 8 + 2) + S, 256);
-    const std::uint64_t b_pak = align_up(HostCtx::kElemChunk / 2 + ecf8::dev::kTileElemsMax + S, 256);
-    const std::uint64_t b_out = align_up(HostCtx::kElemChunk + 2 * ecf8::dev::kTileElemsMax + S, 256);
+    c.enc_chunk = std::max(HostCtx::kEncChunk, c.elem_chunk / 2);
+    const std::uint64_t b_enc = align_up(c.enc_chunk + ecf8::dev::kTileBytesMax + S, 256);
+    const std::uint64_t b_pak = align_up(c.elem_chunk / 2 + ecf8::dev::kTileElemsMax + S, 256);
+    const std::uint64_t b_out = align_up(c.elem_chunk + 2 * ecf8::dev::kTileElemsMax + S, 256);
     for (auto& sl : c.slot) {
       void* p = nullptr;
-      cu(cudaMalloc(&p, b_enc + b_gap + b_pos + b_pak + b_out), "cudaMalloc(staging)");
-      cu(cudaMemset(p, 0, b_enc + b_gap + b_pos + b_pak + b_out), "cudaMemset(staging)");
+      cu(cudaMalloc(&p, b_enc + b_pak + b_out), "cudaMalloc(staging)");
+      cu(cudaMemset(p, 0, b_enc + b_pak + b_out), "cudaMemset(staging)");
       auto* base = static_cast<std::uint8_t*>(p);
       sl.enc = base;
-      sl.gaps = base + b_enc;
-      sl.pos = reinterpret_cast<std::uint64_t*>(base + b_enc + b_gap);
-      sl.pak = base + b_enc + b_gap + b_pos;
-      sl.out = base + b_enc + b_gap + b_pos + b_pak;
+      sl.pak = base + b_enc;
+      sl.out = base + b_enc + b_pak;
       cu(cudaEventCreateWithFlags(&sl.in, cudaEventDisableTiming), "event");
       cu(cudaEventCreateWithFlags(&sl.run, cudaEventDisableTiming), "event");
       cu(cudaEventCreateWithFlags(&sl.out_done, cudaEventDisableTiming), "event");
       sl.used = false;
     }
+    for (auto& mt : c.meta) cu(cudaEventCreateWithFlags(&mt.done, cudaEventDisableTiming), "event");
     c.dev = dev;
   }
   return c;
@@ -290,7 +306,11 @@ P rebase(P slot, std::uint64_t lo_bytes) {
 // decode overlap; the call returns when every byte is in `outs`.
 int host_pipeline(const ecf8_sections* const* ss, const std::uint64_t* nbs, std::uint8_t* const* outs, int count) {
   HostCtx& c = host_ctx();
-  std::uint64_t k = 0;
+  std::uint64_t k = 0, remaining = 0;
+  for (int i = 0; i < count; ++i) remaining += ss[i]->n_elem;
+  std::uint64_t target = c.elem_min;
+  int parity = 0;
+  static const bool skip_kernel = std::getenv("ECF8_DIAG_NO_KERNEL") != nullptr;  // PCIe-only diagnostics
   for (int i = 0; i < count; ++i) {
     const ecf8_sections* s = ss[i];
     const std::uint64_t nb = nbs[i];
@@ -310,23 +330,44 @@ int host_pipeline(const ecf8_sections* const* ss, const std::uint64_t* nbs, std:
     d.n_luts = tb.n_luts;
     d.lenpack = tb.lenpack;
     d.lmin = lmin_of(s->lengths);
+
+    HostCtx::Meta& mt = c.meta[parity];
+    parity ^= 1;
+    const std::uint64_t off_pos = align_up(s->gaps_len + ecf8::dev::kPad, 256);
+    const std::uint64_t need = off_pos + 8 * s->n_outpos;
+    if (need > mt.cap) {
+      if (mt.used) cu(cudaEventSynchronize(mt.done), "sync");
+      if (mt.buf) cudaFree(mt.buf);
+      mt.buf = nullptr;
+      mt.cap = 0;
+      cu(cudaMalloc(&mt.buf, need + (need >> 2)), "cudaMalloc(staging)");
+      mt.cap = need + (need >> 2);
+    } else if (mt.used) {
+      cu(cudaStreamWaitEvent(c.s_in, mt.done, 0), "wait");
+    }
+    mt.used = true;
+    cu(cudaMemcpyAsync(mt.buf, s->gaps, s->gaps_len, cudaMemcpyHostToDevice, c.s_in), "H2D gaps");
+    cu(cudaMemcpyAsync(mt.buf + off_pos, s->outpos, 8 * s->n_outpos, cudaMemcpyHostToDevice, c.s_in), "H2D outpos");
+    d.gaps = mt.buf;
+    d.outpos = reinterpret_cast<const std::uint64_t*>(mt.buf + off_pos);
     for (std::uint64_t lo = 0; lo < nb; ++k) {
-      // grow the chunk tile by tile up to the slot limits
+      // grow the chunk tile by tile up to the ramped target and slot limits
+      const std::uint64_t want =
+          std::max(c.elem_min, std::min({target, c.elem_chunk, remaining / 3}));
       std::uint64_t hi = std::min(nb, lo + m);
       while (hi < nb) {
         const std::uint64_t nh = std::min(nb, hi + m);
-        if ((nh - lo) * T * 8 > HostCtx::kEncChunk || s->outpos[nh] - s->outpos[lo] > HostCtx::kElemChunk) break;
+        if ((nh - lo) * T * 8 > c.enc_chunk || s->outpos[nh] - s->outpos[lo] > want) break;
         hi = nh;
       }
       (void)tile_enc;
+      target *= 2;
+      remaining -= s->outpos[hi] - s->outpos[lo];
       HostCtx::Slot& sl = c.slot[k % HostCtx::kSlots];
       if (sl.used) cu(cudaStreamWaitEvent(c.s_in, sl.out_done, 0), "wait");
       sl.used = true;
       const std::uint64_t e0 = lo * T * 8, e1 = hi * T * 8 + 2;
       cu(cudaMemcpyAsync(sl.enc, s->encoded + e0, e1 - e0, cudaMemcpyHostToDevice, c.s_in), "H2D encoded");
-      const std::uint64_t g0 = lo * T / 2, g1 = std::min(s->gaps_len, (hi * T + 1) / 2);
-      if (g1 > g0) cu(cudaMemcpyAsync(sl.gaps, s->gaps + g0, g1 - g0, cudaMemcpyHostToDevice, c.s_in), "H2D gaps");
-      cu(cudaMemcpyAsync(sl.pos, s->outpos + lo, 8 * (hi - lo + 1), cudaMemcpyHostToDevice, c.s_in), "H2D outpos");
       const std::uint64_t o0 = s->outpos[lo], o1 = s->outpos[hi];
       const std::uint64_t p0 = (o0 / 2) & ~std::uint64_t{15}, p1 = std::min(s->packed_len, (o1 + 1) / 2);
       if (p1 > p0) cu(cudaMemcpyAsync(sl.pak, s->packed + p0, p1 - p0, cudaMemcpyHostToDevice, c.s_in), "H2D packed");
@@ -335,14 +376,13 @@ int host_pipeline(const ecf8_sections* const* ss, const std::uint64_t* nbs, std:
       cu(cudaStreamWaitEvent(c.s_run, sl.in, 0), "wait");
       TensorDesc dk = d;
       dk.encoded = rebase(static_cast<const std::uint8_t*>(sl.enc), e0);
-      dk.gaps = rebase(static_cast<const std::uint8_t*>(sl.gaps), g0);
-      dk.outpos = rebase(static_cast<const std::uint64_t*>(sl.pos), 8 * lo);
       dk.packed = rebase(static_cast<const std::uint8_t*>(sl.pak), p0);
       dk.out = sl.out;
       dk.out_offset = o0 & ~std::uint64_t{15};
       dk.blk_begin = lo;
       dk.blk_end = hi;
-      if (int rc = launch_one(dk, c.s_run)) return rc;
+      if (!skip_kernel)
+        if (int rc = launch_one(dk, c.s_run)) return rc;
       cu(cudaEventRecord(sl.run, c.s_run), "record");
 
       cu(cudaStreamWaitEvent(c.s_out, sl.run, 0), "wait");
@@ -352,6 +392,7 @@ int host_pipeline(const ecf8_sections* const* ss, const std::uint64_t* nbs, std:
       cu(cudaEventRecord(sl.out_done, c.s_out), "record");
       lo = hi;
     }
+    cu(cudaEventRecord(mt.done, c.s_run), "record");
   }
   cu(cudaStreamSynchronize(c.s_out), "sync");
   return ECF8_OK;
