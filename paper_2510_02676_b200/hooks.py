@@ -65,8 +65,9 @@ class ECF8Linear(nn.Module):
 
     ``weight_fp8``: uint8 array [out_features, in_features] of FP8 bytes
     (``fmt`` "e4m3" or "e5m2"); ``scale_w``: per-tensor dequant scale.
-    Activations are quantised per tensor to ``fmt`` with ``scale_x``
-    (computed from the batch when None)."""
+    Activations are quantised per tensor to E4M3 with ``scale_x`` (computed
+    from the batch when None); cuBLASLt has no E5M2 x E5M2 GEMM, E4M3 x E5M2
+    is supported."""
 
     def __init__(self, weight_fp8: np.ndarray, bias: torch.Tensor | None = None, scale_w: float = 1.0,
                  fmt: str = "e4m3", threads_per_block: int = 256, arena: DecodeArena | None = None):
@@ -105,11 +106,12 @@ class ECF8Linear(nn.Module):
         w = self.decode_weight()
         lead = x.shape[:-1]
         x2 = x.reshape(-1, self.in_features)
-        if x2.dtype != _FP8[self.fmt]:
+        act = torch.float8_e4m3fn
+        if x2.dtype != act:
             if scale_x is None:
                 amax = x2.abs().amax().float().clamp_min(1e-12)
-                scale_x = amax / torch.finfo(_FP8[self.fmt]).max
-            x2 = (x2.float() / scale_x).to(_FP8[self.fmt])
+                scale_x = amax / torch.finfo(act).max
+            x2 = (x2.float() / scale_x).to(act)
         elif scale_x is None:
             scale_x = torch.tensor(1.0, device=x.device)
         m = x2.shape[0]

@@ -28,7 +28,7 @@ def test_ecf8_linear_matches_fp8_gemm_on_reference_decoded_weights(orc, fmt, m):
     x = torch.randn(m, k, device="cuda")
     sx = torch.tensor(0.01, device="cuda")
     y = lin(x, sx)
-    xq = (x / sx).to(_FP8[fmt])
+    xq = (x / sx).to(torch.float8_e4m3fn)
     pad = (-m) % 16
     xq = torch.cat([xq, xq.new_zeros(pad, k)]) if pad else xq
     wt = torch.from_numpy(wd).cuda().view(_FP8[fmt])
