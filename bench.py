@@ -1,18 +1,25 @@
 """ECF8 decode benchmark (driver contract: one JSON line on rank 0).
 
-Workload (BASELINE.json configs[1]): Llama-3.1-8B-shaped FP8 E4M3 linear
-weights, all 32 layers (q/o 4096x4096, k/v 1024x4096, gate/up 14336x4096,
-down 4096x14336 = 218.1 M elements per layer, 6.98 G per step), synthetic
-alpha-stable (alpha 1.8, gamma 0.05, seed 1000*layer + matrix), ECF8-encoded
-on the host with T = 256, decoded layer by layer (one batched launch per
-layer) into two alternating layer-sized HBM buffers.  A step = decoding all
-32 layers.  Inputs (5.7 GB compressed per step) are far larger than L2.
+Default workload (BASELINE.json configs[1]): Llama-3.1-8B-shaped FP8 E4M3
+linear weights, all 32 layers (q/o 4096x4096, k/v 1024x4096, gate/up
+14336x4096, down 4096x14336 = 218.1 M elements per layer, 6.98 G per step),
+synthetic alpha-stable (alpha 1.8, gamma 0.05, seed 1000*layer + matrix),
+ECF8-encoded on the host with T = 256, decoded layer by layer (one batched
+launch per layer) into two alternating layer-sized HBM buffers.  A step =
+decoding all 32 layers.  Inputs (5.7 GB compressed per step) are far larger
+than L2.
 
   value  device-resident: compressed sections already in HBM; GB/s of
          algorithmic bytes (container sections read + FP8 bytes written).
-  e2e    the drop-in host call ecf8_decode_host (decode_parallel_into) per
-         tensor: pinned host sections -> H2D -> decode -> D2H into one reused
-         pinned host buffer (ReusableBuffer pattern), all inside the timing.
+  e2e    the drop-in host path: ecf8_decode_host_many (decode_parallel_into
+         over one layer's tensors, chunked H2D / decode / D2H pipeline) from
+         pinned host sections into pinned host outputs, inside the timing.
+
+Other workloads (--workload), same line format:
+  llama3-70b           80 layers of Llama-3-70B linears (855.6 M elements/layer)
+  deepseek-v3-experts  MoE expert FP8 weights, experts e -> rank e mod world
+                       (EP), one step = every local expert of --layers MoE layers
+  dit-e5m2             FLUX/Wan DiT-shaped E5M2 tensors, size sweep 1 MB - 1 GB
 
 --impl reference: the unmodified reference decoder (oracle/_ref, built from
 /root/reference/proj/src) -- or the C oracle port if _ref is absent -- on the
@@ -44,8 +51,29 @@ LLAMA8B = [  # (name, rows, cols)
     ("up_proj", 14336, 4096),
     ("down_proj", 4096, 14336),
 ]
+LLAMA70B = [
+    ("q_proj", 8192, 8192),
+    ("k_proj", 1024, 8192),
+    ("v_proj", 1024, 8192),
+    ("o_proj", 8192, 8192),
+    ("gate_proj", 28672, 8192),
+    ("up_proj", 28672, 8192),
+    ("down_proj", 8192, 28672),
+]
+DSV3_EXPERT = [("gate_proj", 2048, 7168), ("up_proj", 2048, 7168), ("down_proj", 7168, 2048)]
+DSV3_EXPERTS_PER_LAYER = 256
+DIT_SIZES_MB = [1, 4, 16, 64, 256, 1024]
 ALPHA, GAMMA, T_BLOCK = 1.8, 0.05, 256
 METRIC = "ECF8 decode GB/s (FP8 out, % HBM peak), bit-exact"
+
+WORKLOADS = {
+    "llama3.1-8b": dict(layers=32, distinct=8, desc="llama3.1-8b fp8 linears, all 32 layers, layer-by-layer batched decode"),
+    "llama3-70b": dict(layers=80, distinct=2, desc="llama3-70b fp8 linears, all 80 layers, layer-by-layer batched decode"),
+    "deepseek-v3-experts": dict(layers=2, distinct=8,
+                                desc="deepseek-v3 routed-expert fp8 weights, EP (expert e on rank e mod world), "
+                                     "one batched launch per MoE layer"),
+    "dit-e5m2": dict(layers=1, distinct=1, desc="FLUX/Wan DiT-shaped E5M2 tensors, size sweep"),
+}
 
 
 def log(*a):
@@ -59,22 +87,62 @@ def layer_seeds(layer: int):
     return [1000 * layer + j for j in range(len(LLAMA8B))]
 
 
-def build_layer(layer: int, nthreads: int = 0):
+def build_layer(layer: int, nthreads: int = 0, shapes=LLAMA8B):
     """Synthesize + encode one layer (host).  Returns (raw arrays, encoded)."""
     from paper_2510_02676_b200 import codec
 
-    raws = [codec.synth(ALPHA, GAMMA, r * c, s, nthreads=nthreads) for (_, r, c), s in zip(LLAMA8B, layer_seeds(layer))]
+    raws = [codec.synth(ALPHA, GAMMA, r * c, 1000 * layer + j, nthreads=nthreads) for j, (_, r, c) in enumerate(shapes)]
     encs = codec.encode_many(raws, T_BLOCK, nthreads)
     return raws, encs
 
 
-def shard_layers(rank: int, world: int, n_layers: int):
+def shard_layers(rank: int, world: int, n_layers: int, shapes=LLAMA8B):
     """Weak scaling: a world*n-layer stack, LPT-partitioned by layer cost
     (paper_2510_02676_b200/shard.py); equal layers give each rank n of them."""
     from paper_2510_02676_b200.shard import ShardPlan
 
-    per_layer = sum(r * c for _, r, c in LLAMA8B)
+    per_layer = sum(r * c for _, r, c in shapes)
     return ShardPlan.build([per_layer] * (world * n_layers), rank, world, "lpt").mine
+
+
+class Groups:
+    """This rank's decode groups (one batched launch each) for a workload.
+
+    groups[g] = list of (seed, rows, cols); tensors with equal seeds are
+    synthesised once and uploaded to distinct HBM buffers per group."""
+
+    def __init__(self, workload: str, rank: int, world: int, n_layers: int, distinct: int):
+        self.workload = workload
+        if workload in ("llama3.1-8b", "llama3-70b"):
+            shapes = LLAMA8B if workload == "llama3.1-8b" else LLAMA70B
+            mine = shard_layers(rank, world, n_layers, shapes)
+            self.units = mine
+            base = mine[:max(1, min(distinct, len(mine)))]
+            self.groups = [[(1000 * base[i % len(base)] + j, r, c) for j, (_, r, c) in enumerate(shapes)]
+                           for i in range(len(mine))]
+            self.shape_set = [(r, c) for _, r, c in shapes]
+        elif workload == "deepseek-v3-experts":
+            from paper_2510_02676_b200.shard import round_robin_partition
+
+            experts = round_robin_partition(DSV3_EXPERTS_PER_LAYER, world)[rank]
+            self.units = experts
+            d = max(1, distinct)
+            self.groups = []
+            for layer in range(n_layers):
+                g = []
+                for e in experts:
+                    g += [(5_000_000 + 10 * (e % d) + j, r, c) for j, (_, r, c) in enumerate(DSV3_EXPERT)]
+                self.groups.append(g)
+            self.shape_set = [(r, c) for _ in experts for _, r, c in DSV3_EXPERT]
+        else:
+            raise ValueError(workload)
+
+    def distinct_seeds(self):
+        seen = {}
+        for g in self.groups:
+            for s, r, c in g:
+                seen.setdefault(s, r * c)
+        return seen
 
 
 # ------------------------------------------------------------- clock probe
@@ -166,7 +234,7 @@ def cpu_reference_decode(encs, seconds: float, nthreads: int):
     return algo * reps / dt / 1e9, "port", cores, reps, dt
 
 
-# ------------------------------------------------------------------ main
+# ------------------------------------------------------------------ helpers
 
 
 def load_peaks():
@@ -193,6 +261,16 @@ def load_traffic():
     return d.get("dram_bytes_per_launch")
 
 
+def base_line(args, world, value, ms_per_step, workload_cfg):
+    return {
+        "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": f"synthetic alpha-stable (alpha {ALPHA}, gamma {GAMMA}), ECF8-encoded on host",
+        "config": workload_cfg,
+    }
+
+
 def run_reference_arm(args, rank, world):
     if rank != 0:
         return
@@ -206,18 +284,91 @@ def run_reference_arm(args, rank, world):
     algo = sum(e.algorithmic_bytes() for e in encs)
     value = statistics.mean(step_gbs)
     ms = algo / (value * 1e9) * 1e3
-    line = {
-        "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u8", "data": "synthetic alpha-stable (alpha 1.8, gamma 0.05)",
-        "impl": "reference",
-        "config": {"workload": "llama3.1-8b fp8 linears, ECF8 T=256 (one layer per step: bounded CPU sample)",
-                   "elements_per_step": int(sum(e.n_elem for e in encs)), "threads_per_block": T_BLOCK},
-        "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": cores, "kind": kind,
-                         "sample": "layer 0 of the Llama-3.1-8B shapes (7 tensors, 218.1 M elements) per step"},
-        "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
+    line = base_line(args, world, value, ms, {
+        "workload": "llama3.1-8b fp8 linears, ECF8 T=256 (one layer per step: bounded CPU sample)",
+        "elements_per_step": int(sum(e.n_elem for e in encs)), "threads_per_block": T_BLOCK})
+    line["impl"] = "reference"
+    line["cpu_baseline"] = {"value": round(value, 3), "unit": "GB/s", "cores": cores, "kind": kind,
+                            "sample": "layer 0 of the Llama-3.1-8B shapes (7 tensors, 218.1 M elements) per step"}
+    line["e2e"] = {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
     print(json.dumps(line), flush=True)
+
+
+def timed_region(torch, dist, local, stream, batches, steps, warmup):
+    """Warm-up, then EXACTLY `steps` steps bracketed by barrier + sync; CUDA
+    events per launch on the launching stream.  Returns (elapsed_ms max over
+    ranks, per-launch ms list, clocks)."""
+    for _ in range(warmup):
+        for b in batches:
+            b.decode(stream)
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(steps * len(batches))]
+    step_start = torch.cuda.Event(enable_timing=True)
+    step_end = torch.cuda.Event(enable_timing=True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockProbe(local) as probe:
+        step_start.record(stream)
+        k = 0
+        for _ in range(steps):
+            for b in batches:
+                ev[k][0].record(stream)
+                b.decode(stream)
+                ev[k][1].record(stream)
+                k += 1
+        step_end.record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    elapsed_ms = step_start.elapsed_time(step_end)
+    launch_ms = [s.elapsed_time(e) for s, e in ev]
+    if dist:
+        t = torch.tensor([elapsed_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+    return elapsed_ms, launch_ms, probe.summary()
+
+
+# ------------------------------------------------------------------ DiT sweep
+
+
+def run_dit_sweep(args, torch, dist, local, world):
+    """Config 5: E5M2 tensors of 1 MB .. 1 GB (rows of 3072 / 5120), one
+    launch per tensor, rotating over replicas so every size streams >= 2 GB
+    through HBM per measurement (defeats L2)."""
+    from paper_2510_02676_b200 import codec
+    from paper_2510_02676_b200.device import Batch, DeviceTensor
+
+    stream = torch.cuda.current_stream()
+    sweep, total_launches = [], 0
+    for mb in DIT_SIZES_MB:
+        width = 3072 if mb < 64 else 5120
+        rows = max(1, (mb << 20) // width)
+        n = rows * width
+        raw = codec.synth(ALPHA, GAMMA, n, 7000 + mb, fmt="e5m2")
+        enc = codec.encode_tensor(raw, T_BLOCK)
+        reps = max(2, min(64, (2 << 30) // max(1, enc.algorithmic_bytes())))
+        devs = [DeviceTensor(enc) for _ in range(reps)]
+        outs = [torch.empty(n, dtype=torch.uint8, device="cuda") for _ in range(2)]
+        batches = [Batch([d], [outs[i % 2]]) for i, d in enumerate(devs)]
+        batches[0].decode(stream)
+        torch.cuda.synchronize()
+        ok = bool(torch.equal(outs[0], torch.from_numpy(raw).cuda()))
+        elapsed, launch_ms, clocks = timed_region(torch, dist, local, stream, batches, args.steps, args.warmup)
+        algo = enc.algorithmic_bytes()
+        gbs = world * algo * len(batches) * args.steps / (elapsed * 1e-3) / 1e9
+        sweep.append({"size_mb": mb, "shape": [rows, width], "gbs": round(gbs, 1),
+                      "us_per_launch": round(statistics.median(launch_ms) * 1e3, 2),
+                      "bytes_per_elem": round(algo / n, 4), "verified_bit_exact": ok})
+        total_launches += len(batches) * args.steps
+        log(f"[bench] dit-e5m2 {mb} MB: {gbs:.1f} GB/s")
+        del devs, batches, outs
+    return sweep, total_launches
+
+
+# ------------------------------------------------------------------ main
 
 
 def main():
@@ -226,16 +377,23 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--layers", type=int, default=32)
-    ap.add_argument("--distinct-layers", type=int, default=8,
-                    help="distinct synthetic layers; the rest are HBM replicas in distinct buffers")
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--workload", default="llama3.1-8b", choices=sorted(WORKLOADS))
+    ap.add_argument("--layers", type=int, default=None)
+    ap.add_argument("--distinct-layers", type=int, default=None,
+                    help="distinct synthetic layers/experts; the rest are HBM replicas in distinct buffers")
+    ap.add_argument("--e2e-steps", type=int, default=None,
+                    help="default 2 (llama3.1-8b), 1 (llama3-70b), 0 (experts: 11 GB of pinned outputs)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--cpu-threads", type=int, default=0)
     ap.add_argument("--no-verify", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    wl = WORKLOADS[args.workload]
+    args.layers = args.layers or wl["layers"]
+    args.distinct_layers = args.distinct_layers or wl["distinct"]
+    if args.e2e_steps is None:
+        args.e2e_steps = {"llama3.1-8b": 2, "llama3-70b": 1}.get(args.workload, 0)
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -256,26 +414,45 @@ def main():
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    peak, peak_kind = load_peaks()
 
-    # ---- workload: this rank's layers (weak scaling across ranks)
+    if args.workload == "dit-e5m2":
+        sweep, launches = run_dit_sweep(args, torch, dist, local, world)
+        if rank == 0:
+            big = sweep[-1]
+            line = base_line(args, world, big["gbs"], big["us_per_launch"] / 1e3, {
+                "workload": wl["desc"], "sizes_mb": DIT_SIZES_MB, "fmt": "e5m2", "threads_per_block": T_BLOCK,
+                "parallelism": f"shard{world} (replicas per rank, no collective)"})
+            line["sweep"] = sweep
+            line["roofline"] = {"bound": "hbm", "achieved": big["gbs"] / world, "peak": peak, "unit": "GB/s",
+                                "frac": round(big["gbs"] / world / peak, 4), "traffic": None, "peak_kind": peak_kind,
+                                "kernel": kernel_name()}
+            line["gpu_launches"] = launches
+            print(json.dumps(line), flush=True)
+        if dist:
+            dist.destroy_process_group()
+        return
+
+    # ---- workload: this rank's groups (weak scaling across ranks)
     t0 = time.time()
-    my_layers = shard_layers(rank, world, args.layers)
-    distinct = max(1, min(args.distinct_layers, args.layers))
-    pool = {}  # distinct layer id -> (raws, encs)
-    for k in range(distinct):
-        pool[k] = build_layer(my_layers[k])
-    log(f"[bench] rank {rank}: synth+encode {distinct} layers in {time.time() - t0:.1f}s")
+    G = Groups(args.workload, rank, world, args.layers, args.distinct_layers)
+    seeds = G.distinct_seeds()
+    raw_of, enc_of = {}, {}
+    for s, n in seeds.items():
+        raw_of[s] = codec.synth(ALPHA, GAMMA, n, s)
+    order = list(seeds)
+    for s, e in zip(order, codec.encode_many([raw_of[s] for s in order], T_BLOCK)):
+        enc_of[s] = e
+    log(f"[bench] rank {rank}: synth+encode {len(seeds)} distinct tensors in {time.time() - t0:.1f}s")
 
-    # ---- device-resident copies: every layer its own HBM buffers
-    dev_layers = []
-    for i, _ in enumerate(my_layers):
-        _, encs = pool[i % distinct]
-        dev_layers.append([DeviceTensor(e) for e in encs])
-    layer_elems = sum(r * c for _, r, c in LLAMA8B)
-    outs = [[torch.empty(r * c, dtype=torch.uint8, device="cuda") for _, r, c in LLAMA8B] for _ in range(2)]
-    batches = [Batch(dev_layers[i], outs[i % 2]) for i in range(len(dev_layers))]
+    # ---- device-resident copies: every group its own HBM buffers
+    dev_groups = [[DeviceTensor(enc_of[s]) for s, _, _ in g] for g in G.groups]
+    group_shapes = [r * c for _, r, c in G.groups[0]]
+    outs = [[torch.empty(n, dtype=torch.uint8, device="cuda") for n in group_shapes] for _ in range(2)]
+    batches = [Batch(dev_groups[i], outs[i % 2]) for i in range(len(dev_groups))]
     step_bytes = sum(b.algorithmic_bytes for b in batches)
-    step_elems = layer_elems * len(dev_layers)
+    group_elems = sum(group_shapes)
+    step_elems = group_elems * len(batches)
     launches_per_step = sum(b.launches for b in batches)
     torch.cuda.synchronize()
 
@@ -283,13 +460,16 @@ def main():
     verified = None
     if not args.no_verify:
         stream = torch.cuda.current_stream()
-        ok = True
-        for i in range(len(batches)):
+        ok, checked = True, set()
+        for i, g in enumerate(G.groups):
+            fresh = [j for j, (s, _, _) in enumerate(g) if s not in checked]
+            if not fresh:
+                continue
             batches[i].decode(stream)
-            if i < distinct:
-                raws, _ = pool[i]
-                for o, r in zip(outs[i % 2], raws):
-                    ok &= bool(torch.equal(o, torch.from_numpy(r).to("cuda", non_blocking=False)))
+            for j in fresh:
+                s = g[j][0]
+                ok &= bool(torch.equal(outs[i % 2][j], torch.from_numpy(raw_of[s]).to("cuda")))
+                checked.add(s)
         torch.cuda.synchronize()
         verified = ok
         if not ok:
@@ -297,43 +477,12 @@ def main():
 
     # ---- device-resident timed region
     stream = torch.cuda.current_stream()
-    for _ in range(args.warmup):
-        for b in batches:
-            b.decode(stream)
-    torch.cuda.synchronize()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps * len(batches))]
-    step_start = torch.cuda.Event(enable_timing=True)
-    step_end = torch.cuda.Event(enable_timing=True)
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    with ClockProbe(local) as probe:
-        step_start.record(stream)
-        k = 0
-        for _ in range(args.steps):
-            for b in batches:
-                ev[k][0].record(stream)
-                b.decode(stream)
-                ev[k][1].record(stream)
-                k += 1
-        step_end.record(stream)
-        torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    elapsed_ms = step_start.elapsed_time(step_end)
-    launch_ms = [s.elapsed_time(e) for s, e in ev]
-    if dist:
-        t = torch.tensor([elapsed_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed_ms = float(t.item())
+    elapsed_ms, launch_ms, clocks = timed_region(torch, dist, local, stream, batches, args.steps, args.warmup)
     ms_per_step = elapsed_ms / args.steps
     value = world * step_bytes * args.steps / (elapsed_ms * 1e-3) / 1e9
     per_launch_bytes = step_bytes / len(batches)
     achieved = per_launch_bytes / (statistics.mean(launch_ms) * 1e-3) / 1e9
-    peak, peak_kind = load_peaks()
-    traffic = load_traffic()
-    clocks = probe.summary()
+    traffic = load_traffic() if args.workload == "llama3.1-8b" else None
 
     # ---- e2e: host buffers through the drop-in C ABI call
     e2e = None
@@ -343,35 +492,28 @@ def main():
         # pin the host sections once (the contract: inputs from pinned host memory)
         pinned = []
         cudart = torch.cuda.cudart()
-        host_secs = []
-        h2d = 0
-        for i in range(len(my_layers)):
-            _, encs = pool[i % distinct]
-            for e in encs:
-                host_secs.append(e)
-                h2d += e.compressed_bytes()
-        for k in range(distinct):
-            for e in pool[k][1]:
-                for a in (e.encoded, e.gaps, e.outpos, e.packed):
-                    if a.nbytes:
-                        rc = cudart.cudaHostRegister(a.ctypes.data, a.nbytes, 0)
-                        if int(rc) == 0:
-                            pinned.append(a.ctypes.data)
-        # one pinned host buffer per layer tensor, reused every layer (ReusableBuffer pattern)
-        host_outs = [torch.empty(r * c, dtype=torch.uint8).pin_memory() for _, r, c in LLAMA8B]
-        n7 = len(LLAMA8B)
-        layer_calls = []
-        for li in range(len(my_layers)):
-            encs = host_secs[li * n7:(li + 1) * n7]
+        for e in enc_of.values():
+            for a in (e.encoded, e.gaps, e.outpos, e.packed):
+                if a.nbytes:
+                    rc = cudart.cudaHostRegister(a.ctypes.data, a.nbytes, 0)
+                    if int(rc) == 0:
+                        pinned.append(a.ctypes.data)
+        # one pinned host buffer per group tensor, reused every group (ReusableBuffer pattern)
+        host_outs = [torch.empty(n, dtype=torch.uint8).pin_memory() for n in group_shapes]
+        ng = len(group_shapes)
+        calls, h2d = [], 0
+        for g in G.groups:
+            encs = [enc_of[s] for s, _, _ in g]
+            h2d += sum(e.compressed_bytes() for e in encs)
             secs = [e.sections() for e in encs]
-            sp = (C.POINTER(Sections) * n7)(*[C.pointer(x) for x in secs])
-            op = (C.c_void_p * n7)(*[h.data_ptr() for h in host_outs])
-            ln = (C.c_uint64 * n7)(*[e.n_elem for e in encs])
-            layer_calls.append((secs, sp, op, ln))
+            sp = (C.POINTER(Sections) * ng)(*[C.pointer(x) for x in secs])
+            op = (C.c_void_p * ng)(*[h.data_ptr() for h in host_outs])
+            ln = (C.c_uint64 * ng)(*[e.n_elem for e in encs])
+            calls.append((secs, sp, op, ln))
 
         def e2e_step():
-            for _, sp, op, ln in layer_calls:
-                check(lib.ecf8_decode_host_many(sp, op, ln, n7))
+            for _, sp, op, ln in calls:
+                check(lib.ecf8_decode_host_many(sp, op, ln, ng))
 
         e2e_step()  # warm the staging buffers
         torch.cuda.synchronize()
@@ -389,39 +531,38 @@ def main():
         e2e = {"value": round(world * step_bytes * args.e2e_steps / dt / 1e9, 3), "unit": "GB/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(step_elems),
                "ms_per_step": round(dt / args.e2e_steps * 1e3, 2),
-               "path": "ecf8_decode_host_many per layer (decode_parallel_into over the layer's 7 tensors, one pipelined call), pinned host buffers"}
+               "path": "ecf8_decode_host_many per group (decode_parallel_into over the group's tensors in one "
+                       "pipelined call), pinned host buffers"}
         for p in pinned:
             cudart.cudaHostUnregister(p)
 
-    # ---- CPU baseline (rank 0, N = 1 only)
+    # ---- CPU baseline (rank 0, N = 1 only): the first group's distinct tensors
     cpu = None
     if rank == 0 and world == 1 and args.cpu_seconds > 0:
-        gbs, kind, cores, reps, dt = cpu_reference_decode(pool[0][1], args.cpu_seconds, args.cpu_threads)
+        first = list(dict.fromkeys(s for s, _, _ in G.groups[0]))
+        sample = [enc_of[s] for s in first]
+        gbs, kind, cores, reps, dt = cpu_reference_decode(sample, args.cpu_seconds, args.cpu_threads)
         cpu = {"value": round(gbs, 3), "unit": "GB/s", "cores": cores, "kind": kind,
-               "sample": f"layer 0 (7 tensors, {layer_elems / 1e6:.1f} M elements) decoded {reps}x, {dt:.1f} s"}
+               "sample": f"group 0 ({len(sample)} tensors, {sum(e.n_elem for e in sample) / 1e6:.1f} M elements) "
+                         f"decoded {reps}x, {dt:.1f} s"}
 
     if rank == 0:
-        line = {
-            "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
-            "data": "synthetic alpha-stable (alpha 1.8, gamma 0.05), ECF8-encoded on host",
-            "config": {
-                "workload": "llama3.1-8b fp8 linears, all 32 layers, layer-by-layer batched decode",
-                "layers_per_gpu": len(my_layers), "distinct_layers": distinct,
-                "elements_per_step_per_gpu": int(step_elems), "threads_per_block": T_BLOCK,
-                "alpha": ALPHA, "gamma": GAMMA, "parallelism": f"shard{world} (independent layers, no collective)",
-                "l2": "inputs 5.7 GB/step >> 126 MB L2; outputs alternate two 218 MB buffers",
-                "bytes_per_step_per_gpu": int(step_bytes), "verified_bit_exact": verified,
-            },
-            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4), "traffic": traffic, "peak_kind": peak_kind,
-                         "kernel": kernel_name(), "algorithmic_bytes_per_launch": int(per_launch_bytes)},
-            "cpu_baseline": cpu,
-            "e2e": e2e,
-            "clocks": clocks,
-            "gpu_launches": int(launches_per_step * args.steps),
-        }
+        line = base_line(args, world, value, ms_per_step, {
+            "workload": wl["desc"],
+            "groups_per_gpu": len(batches), "distinct_tensors": len(seeds), "units_per_gpu": len(G.units),
+            "elements_per_step_per_gpu": int(step_elems), "threads_per_block": T_BLOCK,
+            "alpha": ALPHA, "gamma": GAMMA, "parallelism": f"shard{world} (independent tensors, no collective)",
+            "l2": f"inputs {step_bytes / 1e9:.1f} GB/step >> 126 MB L2; outputs alternate two "
+                  f"{group_elems / 1e6:.0f} MB buffers",
+            "bytes_per_step_per_gpu": int(step_bytes), "verified_bit_exact": verified,
+        })
+        line["roofline"] = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                            "frac": round(achieved / peak, 4), "traffic": traffic, "peak_kind": peak_kind,
+                            "kernel": kernel_name(), "algorithmic_bytes_per_launch": int(per_launch_bytes)}
+        line["cpu_baseline"] = cpu
+        line["e2e"] = e2e
+        line["clocks"] = clocks
+        line["gpu_launches"] = int(launches_per_step * args.steps)
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
