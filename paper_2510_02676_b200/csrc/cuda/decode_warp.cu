@@ -47,6 +47,7 @@ struct WarpSmem {
 };
 
 __shared__ Tables g_tb;
+__shared__ unsigned long long g_next_tile;  // CTA-local work queue of the current segment
 
 struct WarpIn {
   uint4 w01, w23, w45, w67;  // window bytes (little-endian 32-bit words)
@@ -255,12 +256,17 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_warp_kernel(const LaunchArg
     __syncthreads();  // every warp is done with the previous tables
     stage_tables(d, g_tb, threadIdx.x, NW * 32);
     const std::uint32_t len_off = (d.n_luts - 1) << 8;
+    if (threadIdx.x == 0) g_next_tile = seg + NW;
     __syncthreads();
 
+    // Tiles are handed out dynamically inside the CTA (warp w starts with
+    // tile seg + w, then takes the next unclaimed one), so the warps of a
+    // segment finish within one tile of each other whatever the per-tile
+    // cost.  The next tile is claimed and its inputs loaded one tile ahead.
     WarpIn nxt;
     std::uint64_t tile = seg + warp;
     if (tile < seg_end) load_warp_tile(d, tile, log2T, lane, nxt);
-    for (; tile < seg_end; tile += NW) {
+    while (tile < seg_end) {
       const WarpIn cur = nxt;
       if (lane == 0) {  // sign/mantissa bytes of this tile -> L2 (one bulk TMA prefetch)
         const std::uint64_t p0 = (cur.A >> 1) & ~std::uint64_t{15};
@@ -268,8 +274,12 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_warp_kernel(const LaunchArg
         if (bytes)
           asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(d.packed + p0), "r"(bytes) : "memory");
       }
-      if (tile + NW < seg_end) load_warp_tile(d, tile + NW, log2T, lane, nxt);
+      unsigned long long claim = 0;
+      if (lane == 0) claim = atomicAdd(&g_next_tile, 1ull);
+      const std::uint64_t next = __shfl_sync(0xffffffffu, claim, 0);
+      if (next < seg_end) load_warp_tile(d, next, log2T, lane, nxt);
       warp_tile(d, cur, log2T, len_off, ws, lane);
+      tile = next;
     }
     seg = seg_end;
   }
