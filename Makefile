@@ -16,7 +16,7 @@ LIB     := $(LIBDIR)/libecf8_b200.so
 
 CXXFLAGS  := -std=c++20 -O3 -fPIC -fopenmp -Wall -Wextra -Iinclude -I$(CUDA)/include
 NVCCFLAGS := -std=c++20 -O3 $(ARCH) -lineinfo -Xcompiler -fPIC -Xptxas -v \
-             -Iinclude -I$(PKG)/csrc/cuda --expt-relaxed-constexpr
+             -Iinclude -I$(PKG)/csrc/cuda --expt-relaxed-constexpr $(EXTRA)
 
 HOST_SRCS := $(wildcard $(PKG)/csrc/host/*.cpp) $(PKG)/csrc/cuda/tables.cpp
 CU_SRCS   := $(wildcard $(PKG)/csrc/cuda/*.cu)
@@ -35,12 +35,17 @@ $(OBJ)/%.o: $(PKG)/csrc/%.cu $(HEADERS)
 	$(NVCC) $(NVCCFLAGS) -c $< -o $@ 2> $@.ptxas.log || (cat $@.ptxas.log; false)
 
 $(LIB): $(HOST_OBJS) $(CU_OBJS)
-	@mkdir -p $(LIBDIR)
+	@mkdir -p $(dir $@)
 	g++ -shared -o $@ $^ -fopenmp -L$(CUDA)/lib64 -lcudart_static -ldl -lrt -lpthread \
 	    -Wl,--no-undefined
 
 oracle:
 	$(MAKE) -C oracle
+
+# A/B kernel experiments: make variant V=name VFLAGS="-DECF8_WB_DEPTH=4"
+# -> build/var/name/libecf8_b200.so (load with ECF8_LIB=...)
+variant:
+	$(MAKE) OBJ=build/var/$(V)/obj LIB=build/var/$(V)/libecf8_b200.so EXTRA="$(VFLAGS)" build/var/$(V)/libecf8_b200.so
 
 # The reference's own unit + acceptance suites, compiled from
 # /root/reference/proj/tests (never copied) against OUR headers and library.
@@ -67,4 +72,4 @@ clean:
 	rm -rf build $(LIBDIR)
 	$(MAKE) -C oracle clean
 
-.PHONY: all oracle refsuites clean
+.PHONY: all oracle refsuites clean variant

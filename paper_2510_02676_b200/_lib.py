@@ -11,7 +11,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libecf8_b200.so")
+# ECF8_LIB: load an alternative build (A/B kernel experiments, tools/build_variant.sh)
+LIB_PATH = os.environ.get("ECF8_LIB") or os.path.join(_HERE, "lib", "libecf8_b200.so")
 
 ECF8_OK, ECF8_EINVAL, ECF8_EFORMAT, ECF8_ECUDA, ECF8_ENOMEM, ECF8_EIO = range(6)
 
