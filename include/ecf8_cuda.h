@@ -54,6 +54,9 @@ typedef struct ecf8_dev_tensor ecf8_dev_tensor;
 /* A prepared multi-tensor decode (one launch for many tensors). */
 typedef struct ecf8_batch ecf8_batch;
 
+/* A weight prepared for the decode-fused FP8 GEMM. */
+typedef struct ecf8_fused ecf8_fused;
+
 const char *ecf8_last_error(void);
 /* 0 when no usable device; never falls back to the CPU. */
 int ecf8_device_count(void);
@@ -107,6 +110,23 @@ int ecf8_batch_decode(const ecf8_batch *b, void *stream);
 void ecf8_batch_free(ecf8_batch *b);
 /* Launches of the decode kernel issued by one ecf8_batch_decode call. */
 int ecf8_batch_launches(const ecf8_batch *b);
+
+/* ---- decode-fused tcgen05 FP8 GEMM (no reference counterpart; the paper's
+ * decode-then-use, fused into one kernel) --------------
+ *
+ * `t` holds an n x k FP8 weight W in the tiled layout of
+ * ecf8_host_fused_layout (128 x 128 tiles, each in the swizzled shared-memory
+ * image the tensor core reads), ECF8-encoded with T in [8, 256].  The GEMM
+ *   y[m, n] = scale * sum_k x[m, k] * W[n, k]     (fp32 accumulate / out)
+ * decodes W tile by tile into shared memory; decoded weights never reach
+ * HBM.  x: m x k E4M3 row-major on the device (16-byte aligned), 1 <= m <=
+ * 256; y: m x n fp32 row-major.  w_fmt: 0 = E4M3, 1 = E5M2 weights.  The
+ * fused handle keeps a pointer to `t`, which must outlive it. */
+int ecf8_fused_create(const ecf8_dev_tensor *t, uint64_t n, uint64_t k, int w_fmt, ecf8_fused **out);
+int ecf8_fused_gemm(const ecf8_fused *f, const uint8_t *d_x, uint32_t m, float scale, float *d_y, void *stream);
+/* K splits per 128-row tile chosen for the SM count (partials summed in y). */
+int ecf8_fused_split_k(const ecf8_fused *f);
+void ecf8_fused_free(ecf8_fused *f);
 
 #ifdef __cplusplus
 }

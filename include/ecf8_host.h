@@ -65,6 +65,15 @@ int ecf8_host_synth(double alpha, double gamma, uint64_t n, uint64_t seed, int f
 
 int ecf8_host_max_threads(void);
 
+/* Weight layout for the decode-fused GEMM (ecf8_cuda.h ecf8_fused_*): an
+ * n x k row-major FP8 matrix -> 128 x 128 tiles in row-major tile order,
+ * each tile as its 16384-byte shared-memory image (K-major, 128-byte rows,
+ * 16-byte chunk c of row r at r*128 + ((c ^ (r & 7)) << 4)).  inverse != 0
+ * maps the tiled sequence back to row-major.  n, k multiples of 128.  (New:
+ * the reference has no GEMM; the tiled bytes are an ordinary tensor for the
+ * unchanged encoder and container.) */
+int ecf8_host_fused_layout(const uint8_t *w, uint64_t n, uint64_t k, uint8_t *out, int inverse);
+
 #ifdef __cplusplus
 }
 #endif

@@ -96,8 +96,13 @@ _SIGS = {
     "ecf8_batch_decode": (C.c_int, [_P, _P]),
     "ecf8_batch_free": (None, [_P]),
     "ecf8_batch_launches": (C.c_int, [_P]),
+    "ecf8_fused_create": (C.c_int, [_P, C.c_uint64, C.c_uint64, C.c_int, C.POINTER(_P)]),
+    "ecf8_fused_gemm": (C.c_int, [_P, _P, C.c_uint32, C.c_float, _P, _P]),
+    "ecf8_fused_split_k": (C.c_int, [_P]),
+    "ecf8_fused_free": (None, [_P]),
     # ecf8_host.h
     "ecf8_host_free": (None, [_P]),
+    "ecf8_host_fused_layout": (C.c_int, [_P, C.c_uint64, C.c_uint64, _P, C.c_int]),
     "ecf8_host_build_code": (C.c_int, [_P, _P]),
     "ecf8_host_build_lut": (C.c_int, [_P, _P, _U32P]),
     "ecf8_host_device_tables": (C.c_int, [_P, _P, _P, _P, _U32P, _U32P]),

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <array>
 #include <cstdio>
 #include <cstdlib>
@@ -19,6 +20,7 @@
 #include <vector>
 
 #include "decode.cuh"
+#include "fused_gemm.cuh"
 #include "ecf8_cuda.h"
 #include "tables.hpp"
 
@@ -159,6 +161,14 @@ struct ecf8_dev_tensor {
   std::uint64_t algo_bytes = 0;
   std::uint32_t T = 0;
   TensorDesc desc{};  // out / tile fields filled per launch
+};
+
+struct ecf8_fused {
+  const ecf8_dev_tensor* w = nullptr;
+  ecf8::dev::FusedCta* d_plan = nullptr;
+  std::uint32_t n_cta = 0, split_k = 1;
+  std::uint64_t n = 0, k = 0;
+  std::uint32_t w_fmt = 0;
 };
 
 struct ecf8_batch {
@@ -624,6 +634,105 @@ int ecf8_count_window(const uint8_t window10[10], unsigned gap, const uint8_t le
     cu(cudaMemcpy(count, sc.cnt, 4, cudaMemcpyDeviceToHost), "D2H count");
     return ECF8_OK;
   });
+}
+
+
+// ---- decode-fused FP8 GEMM (fused_gemm.cu) -------------------------------
+
+int ecf8_fused_create(const ecf8_dev_tensor* t, uint64_t n, uint64_t k, int w_fmt, ecf8_fused** out) {
+  return guarded([&]() -> int {
+    if (!t || !out) return fail(ECF8_EINVAL, "null argument");
+    *out = nullptr;
+    if (n == 0 || k == 0 || n % 128 || k % 128) return fail(ECF8_EINVAL, "fused GEMM needs n, k multiples of 128");
+    if (t->n_elem != n * k) return fail(ECF8_EINVAL, "output size mismatch");
+    if (w_fmt != 0 && w_fmt != 1) return fail(ECF8_EINVAL, "weight format must be 0 (E4M3) or 1 (E5M2)");
+    if (ecf8::dev::variant_for(t->T, t->desc.lmin).id != 4)
+      return fail(ECF8_EINVAL, "fused GEMM needs T in [8, 256] and a shortest code of >= 2 bits");
+    if (int rc = require_device()) return rc;
+    std::vector<std::uint64_t> outpos(t->n_blocks + 1);
+    cu(cudaMemcpy(outpos.data(), t->desc.outpos, 8 * outpos.size(), cudaMemcpyDeviceToHost), "D2H outpos");
+    // split-K so that the CTA count fills whole waves of the SMs
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const std::uint64_t nt = n / 128, KT = k / 128;
+    std::uint32_t best = 1;
+    double best_eff = 0;
+    for (std::uint32_t sk = 1; sk <= 16 && KT / sk >= 4; ++sk) {
+      const double ctas = static_cast<double>(nt * sk);
+      const double eff = ctas / (sms * std::ceil(ctas / sms));
+      if (eff > best_eff + 0.02) {
+        best_eff = eff;
+        best = sk;
+      }
+    }
+    auto f = std::make_unique<ecf8_fused>();
+    f->w = t;
+    f->n = n;
+    f->k = k;
+    f->w_fmt = static_cast<std::uint32_t>(w_fmt);
+    f->split_k = best;
+    std::vector<ecf8::dev::FusedCta> plan;
+    for (std::uint64_t r = 0; r < nt; ++r)
+      for (std::uint32_t sk = 0; sk < best; ++sk) {
+        ecf8::dev::FusedCta c{};
+        c.nt = static_cast<std::uint32_t>(r);
+        c.kt0 = static_cast<std::uint32_t>(KT * sk / best);
+        c.kt1 = static_cast<std::uint32_t>(KT * (sk + 1) / best);
+        c.e0 = (r * KT + c.kt0) * 16384;
+        c.e1 = (r * KT + c.kt1) * 16384;
+        // blocks overlapping [e0, e1): last block starting <= e0 .. first block starting >= e1
+        auto ub = std::upper_bound(outpos.begin(), outpos.end() - 1, c.e0);
+        c.blk_begin = static_cast<std::uint64_t>(ub - outpos.begin()) - 1;
+        auto lb = std::lower_bound(outpos.begin(), outpos.end(), c.e1);
+        c.blk_end = static_cast<std::uint64_t>(lb - outpos.begin());
+        if (c.blk_end > t->n_blocks) c.blk_end = t->n_blocks;
+        plan.push_back(c);
+      }
+    f->n_cta = static_cast<std::uint32_t>(plan.size());
+    cu(cudaMalloc(&f->d_plan, sizeof(ecf8::dev::FusedCta) * plan.size()), "cudaMalloc(plan)");
+    cu(cudaMemcpy(f->d_plan, plan.data(), sizeof(ecf8::dev::FusedCta) * plan.size(), cudaMemcpyHostToDevice),
+       "H2D plan");
+    *out = f.release();
+    return ECF8_OK;
+  });
+}
+
+int ecf8_fused_split_k(const ecf8_fused* f) { return f ? static_cast<int>(f->split_k) : 0; }
+
+int ecf8_fused_gemm(const ecf8_fused* f, const uint8_t* d_x, uint32_t m, float scale, float* d_y, void* stream) {
+  return guarded([&]() -> int {
+    if (!f || !d_x || !d_y) return fail(ECF8_EINVAL, "null argument");
+    if (m == 0 || m > 256) return fail(ECF8_EINVAL, "fused GEMM supports 1 <= m <= 256 tokens");
+    if ((reinterpret_cast<std::uintptr_t>(d_x) & 15) || (reinterpret_cast<std::uintptr_t>(d_y) & 3))
+      return fail(ECF8_EINVAL, "x must be 16-byte aligned");
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    ecf8::dev::FusedArgs a{};
+    a.w = f->w->desc;
+    a.plan = f->d_plan;
+    a.x = d_x;
+    a.y = d_y;
+    a.m = m;
+    a.m_pad = (m + 15) / 16 * 16;
+    a.n = static_cast<std::uint32_t>(f->n);
+    a.k = static_cast<std::uint32_t>(f->k);
+    a.split_k = f->split_k;
+    a.stages_a = ecf8::dev::fused_stages_a(a.m_pad);
+    if (a.stages_a < 2) return fail(ECF8_EINVAL, "fused GEMM: shared memory too small for this m");
+    a.tmem_cols = 32;
+    while (a.tmem_cols < a.m_pad) a.tmem_cols <<= 1;
+    a.w_fmt = f->w_fmt;
+    a.scale = scale;
+    if (f->split_k > 1) cu(cudaMemsetAsync(d_y, 0, sizeof(float) * m * f->n, st), "memset y");
+    cu(ecf8::dev::launch_fused_gemm(a, f->n_cta, st), "fused GEMM launch");
+    return ECF8_OK;
+  });
+}
+
+void ecf8_fused_free(ecf8_fused* f) {
+  if (!f) return;
+  if (f->d_plan) cudaFree(f->d_plan);
+  delete f;
 }
 
 }  // extern "C"

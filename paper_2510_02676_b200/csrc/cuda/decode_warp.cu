@@ -28,15 +28,14 @@
 
 #include "decode.cuh"
 #include "decode_common.cuh"
+#include "decode_warp.cuh"
 
 namespace ecf8::dev {
 
 namespace {
 
-constexpr int kLaneWin = 8;  // windows per lane
-
 struct WarpSmem {
-  static constexpr int kSlotW = 32;  // 8 windows x 32 symbols / 8 nibbles per word
+  static constexpr int kSlotW = kSlotWords;
   static constexpr int kStride = kSlotW + 1;
   static constexpr int kStageWords = 32 * kSlotW + 8;
   std::uint32_t slot[32 * kStride];
@@ -49,85 +48,13 @@ struct WarpSmem {
 __shared__ Tables g_tb;
 __shared__ unsigned long long g_next_tile;  // CTA-local work queue of the current segment
 
-struct WarpIn {
-  uint4 w01, w23, w45, w67;  // window bytes (little-endian 32-bit words)
-  uint2 w8;                  // first 8 bytes of the next window (lookahead)
-  std::uint32_t gaps;        // 8 gap nibbles, window 2j in the high nibble of byte j
-  std::uint64_t A, E;        // tile output range
-  std::uint64_t o0, o1;      // my reference block's output range
-  std::uint32_t nblk, nwin;
-  std::uint64_t b0;
-};
-
-__device__ __forceinline__ void load_warp_tile(const TensorDesc& d, std::uint64_t tile, std::uint32_t log2T,
-                                               int lane, WarpIn& in) {
-  const std::uint32_t m = 256u >> log2T;  // blocks per tile
-  in.b0 = d.blk_begin + (tile - d.tile_begin) * m;
-  in.nblk = static_cast<std::uint32_t>(d.blk_end - in.b0 < m ? d.blk_end - in.b0 : m);
-  in.nwin = in.nblk << log2T;
-  const std::uint64_t w0g = in.b0 << log2T;
-  const std::uint32_t wl = static_cast<std::uint32_t>(lane) * kLaneWin;
-  in.A = __ldg(d.outpos + in.b0);
-  in.E = __ldg(d.outpos + in.b0 + in.nblk);
-  if (wl < in.nwin) {
-    const uint4* src = reinterpret_cast<const uint4*>(d.encoded + 8 * (w0g + wl));
-    in.w01 = __ldg(src);
-    in.w23 = __ldg(src + 1);
-    in.w45 = __ldg(src + 2);
-    in.w67 = __ldg(src + 3);
-    in.w8 = __ldg(reinterpret_cast<const uint2*>(src + 4));
-    in.gaps = __ldg(reinterpret_cast<const std::uint32_t*>(d.gaps + (w0g >> 1)) + lane);
-    const std::uint32_t bl = wl >> log2T;
-    in.o0 = __ldg(d.outpos + in.b0 + bl);
-    in.o1 = __ldg(d.outpos + in.b0 + bl + 1);
-  } else {
-    in.o0 = in.o1 = in.E;
-  }
-}
-
 __device__ __forceinline__ void warp_tile(const TensorDesc& d, const WarpIn& in, std::uint32_t log2T,
                                           std::uint32_t len_off, WarpSmem& ws, int lane) {
   std::uint32_t* const my_slot = ws.slot + lane * WarpSmem::kStride;
-  const std::uint32_t wl0 = static_cast<std::uint32_t>(lane) * kLaneWin;
-  const bool active = wl0 < in.nwin;
-
-  // ---- decode my 8 windows into my slot (window words rotate through
-  //      registers so the loop body is emitted once)
-  const std::uint32_t slot_base = smem_addr(my_slot);
-  SlotSink sink{slot_base};
-  if (active) {
-    const std::uint32_t w[18] = {bswap32(in.w01.x), bswap32(in.w01.y), bswap32(in.w01.z), bswap32(in.w01.w),
-                                 bswap32(in.w23.x), bswap32(in.w23.y), bswap32(in.w23.z), bswap32(in.w23.w),
-                                 bswap32(in.w45.x), bswap32(in.w45.y), bswap32(in.w45.z), bswap32(in.w45.w),
-                                 bswap32(in.w67.x), bswap32(in.w67.y), bswap32(in.w67.z), bswap32(in.w67.w),
-                                 bswap32(in.w8.x),  bswap32(in.w8.y)};
-    const std::uint32_t n = min(in.nwin - wl0, static_cast<std::uint32_t>(kLaneWin));
-#pragma unroll
-    for (int i = 0; i < kLaneWin; ++i) {
-      if (static_cast<std::uint32_t>(i) < n) {
-        // byte j of the gap word: window 2j in the high nibble, 2j + 1 low
-        const std::uint32_t gap = (in.gaps >> (8 * (i >> 1) + ((i & 1) ? 0 : 4))) & 15u;
-        decode_window(w[2 * i], w[2 * i + 1], w[2 * i + 2], w[2 * i + 3], gap, g_tb, len_off, sink);
-      }
-    }
-  }
-  const std::uint32_t cnt = sink.finish(slot_base);
-
-  // ---- warp scan, segmented by reference block (2^(log2T-3) lanes each)
-  std::uint32_t incl = cnt;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const std::uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += y;
-  }
-  const std::uint32_t excl = incl - cnt;
-  const std::uint32_t lpb_mask = (1u << (log2T - 3)) - 1;  // lanes per block - 1
-  const std::uint32_t first_excl = __shfl_sync(0xffffffffu, excl, static_cast<std::uint32_t>(lane) & ~lpb_mask);
-  const std::uint32_t start_rel = static_cast<std::uint32_t>(in.o0 - in.A) + excl - first_excl;
-  const std::uint32_t lim_rel = static_cast<std::uint32_t>(in.o1 - in.A);
-  const std::uint32_t cc = (active && start_rel < lim_rel) ? min(cnt, lim_rel - start_rel) : 0u;
+  const LaneRun run = warp_decode_scan(in, log2T, len_off, g_tb, my_slot, lane);
+  const std::uint32_t cc = run.len;
   const std::uint32_t off = static_cast<std::uint32_t>(in.A & 15);  // staging nibble of element A
-  const std::uint32_t d0 = start_rel + off, dend = d0 + cc;
+  const std::uint32_t d0 = run.start + off, dend = d0 + cc;
   const std::uint32_t data_end = off + static_cast<std::uint32_t>(in.E - in.A);
   __syncwarp();  // previous tile's write-back is done with the staging
   ws.rs[lane] = d0;

@@ -1,0 +1,367 @@
+// fused_gemm.cu -- decode-fused tcgen05 FP8 GEMM.
+//
+//   Y[M, N] (fp32) = scale * X[M, K] (E4M3) . W[N, K]^T (E4M3 / E5M2)
+//
+// W stays ECF8-compressed in HBM and is decoded straight into shared memory;
+// the decoded weights never touch HBM.  There is no reference counterpart:
+// the paper decodes a layer into a buffer and then runs the GEMM
+// (PAPER.md:170-173); this kernel fuses the two.
+//
+// Fused weight layout ("tiled" ECF8 tensor, ecf8_host_fused_layout): W is cut
+// into 128 x 128 tiles, tile (nt, kt) in row-major tile order, and each
+// tile's 16384 bytes are stored in the exact shared-memory image the tensor
+// core reads: K-major, 128-byte rows, 128B swizzle (16-byte chunk c of row r
+// at r*128 + ((c ^ (r & 7)) << 4)).  The tiled byte sequence is an ordinary
+// 1-D tensor for the (unchanged) ECF8 encoder.  A decoded element's tile-
+// major index therefore IS its shared-memory offset within its tile.
+//
+// CTA = one 128-row n-tile x a contiguous K range [kt0, kt1) (split-K when
+// N/128 alone would under-fill the 148 SMs; partial sums are added with
+// red.global.add.f32).  Warp roles:
+//   decode warps (kDecodeWarps)  claim ECF8 tiles (256 windows, decode_warp.cuh)
+//       covering the CTA's element range in order, decode them into their
+//       nibble slots, then merge exponent + sign/mantissa nibbles and store
+//       the FP8 bytes straight into the A ring stage of their K tile; each
+//       warp arrives on the stage's "full" mbarrier with the number of bytes
+//       it wrote (a stage completes at 16384 bytes).
+//   control warp   allocates TMEM, loads X K-tiles into a 2-stage B ring
+//       (swizzled like A), and one elected lane issues
+//       tcgen05.mma.cta_group::1.kind::f8f6f4 (M = 128 W rows, N = padded
+//       token count, K = 32 per instruction, 4 per K tile) with the fp32
+//       accumulator in TMEM; tcgen05.commit frees A / B stages.
+//   epilogue       decode warps 0-3 (TMEM lane quadrants) read the
+//       accumulator with tcgen05.ld.32x32b and write Y^T rows coalesced.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdlib>
+
+#include "decode.cuh"
+#include "decode_common.cuh"
+#include "decode_warp.cuh"
+#include "fused_gemm.cuh"
+
+namespace ecf8::dev {
+
+namespace {
+
+constexpr int kDecodeWarps = 20;
+constexpr int kThreadsF = (kDecodeWarps + 1) * 32;
+constexpr int kCtrlWarp = kDecodeWarps;
+constexpr std::uint32_t kTileElems = 128 * 128;  // one K tile of A (bytes)
+constexpr int kSlotStride = kSlotWords + 1;
+
+__shared__ Tables g_tbf;
+__shared__ unsigned long long g_qnext;
+__shared__ alignas(8) unsigned long long g_full[kMaxStagesA];
+__shared__ alignas(8) unsigned long long g_empty[kMaxStagesA];
+__shared__ alignas(8) unsigned long long g_bfree[2];
+__shared__ alignas(8) unsigned long long g_done;
+__shared__ std::uint32_t g_tmem;
+
+// ---- PTX helpers ---------------------------------------------------------
+
+__device__ __forceinline__ void mbar_init(std::uint32_t bar, std::uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(std::uint32_t bar, std::uint32_t count) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.release.cta.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(bar),
+               "r"(count)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(std::uint32_t bar, std::uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tc_commit(std::uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+               : "memory");
+}
+
+// K-major, 128-byte rows, 128B swizzle, 8-row groups 1024 bytes apart.
+__device__ __forceinline__ std::uint64_t smem_desc(std::uint32_t saddr) {
+  std::uint64_t d = 0;
+  d |= static_cast<std::uint64_t>((saddr >> 4) & 0x3FFF);  // start address
+  d |= static_cast<std::uint64_t>(1) << 16;                 // leading byte offset (unused for SW128 K-major)
+  d |= static_cast<std::uint64_t>(1024 >> 4) << 32;         // stride byte offset
+  d |= static_cast<std::uint64_t>(1) << 46;                 // descriptor version (sm_100)
+  d |= static_cast<std::uint64_t>(2) << 61;                 // SWIZZLE_128B
+  return d;
+}
+
+__device__ __forceinline__ void mma_f8(std::uint32_t tmem_d, std::uint64_t adesc, std::uint64_t bdesc,
+                                       std::uint32_t idesc, std::uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld8(std::uint32_t taddr, float (&v)[8]) {
+  std::uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr)
+               : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// ---- decode warps: one ECF8 tile -> FP8 bytes in the A ring ---------------
+
+struct Ring {
+  std::uint32_t a_base;  // shared address of A stage 0 (1024-aligned)
+  std::uint32_t stages;  // A stages
+  std::uint64_t e0, e1;  // CTA element range (tile-major), multiples of 16384
+};
+
+__device__ __forceinline__ void wait_stage_free(const Ring& R, std::uint32_t t) {
+  if (t < R.stages) return;
+  const std::uint32_t s = t % R.stages;
+  mbar_wait(smem_addr(&g_empty[s]), ((t / R.stages) - 1) & 1u);
+}
+
+// Bytes of element range [lo, hi) that fall in ring tile t.
+__device__ __forceinline__ std::uint32_t overlap(std::uint64_t lo, std::uint64_t hi, std::uint64_t t0,
+                                                 std::uint64_t t1) {
+  const std::uint64_t a = lo > t0 ? lo : t0, b = hi < t1 ? hi : t1;
+  return b > a ? static_cast<std::uint32_t>(b - a) : 0u;
+}
+
+__device__ __forceinline__ void ring_tile(const TensorDesc& d, const WarpIn& in, std::uint32_t log2T,
+                                          std::uint32_t len_off, std::uint32_t* slot, const Ring& R, int lane) {
+  const LaneRun run = warp_decode_scan(in, log2T, len_off, g_tbf, slot, lane);
+
+  // this ECF8 tile's part of the CTA range, in ring tiles tf (and tf + 1)
+  const std::uint64_t A = in.A > R.e0 ? in.A : R.e0;
+  const std::uint64_t E = in.E < R.e1 ? in.E : R.e1;
+  if (A >= E) return;
+  const std::uint32_t tf = static_cast<std::uint32_t>((A - R.e0) >> 14);
+  const std::uint32_t tl = static_cast<std::uint32_t>((E - 1 - R.e0) >> 14);
+  wait_stage_free(R, tf);
+  if (tl != tf) wait_stage_free(R, tl);
+
+  const std::uint64_t R0 = in.A + run.start, R1 = R0 + run.len;
+  const std::uint64_t lo = R0 > R.e0 ? R0 : R.e0, hi = R1 < R.e1 ? R1 : R.e1;
+  if (lo < hi) {
+    const std::uint32_t slot_base = smem_addr(slot);
+    const std::uint32_t* pk = reinterpret_cast<const std::uint32_t*>(d.packed);
+    for (std::uint64_t g = lo & ~std::uint64_t{7}; g < hi; g += 8) {
+      // exponent nibbles of elements g .. g+7 (run nibble ig = g - R0)
+      const long long ig = static_cast<long long>(g - R0);
+      std::uint32_t x;
+      if (ig >= 0) {
+        const std::uint32_t w = static_cast<std::uint32_t>(ig >> 3), sh = static_cast<std::uint32_t>(ig & 7) * 4;
+        x = __funnelshift_r(lds32(slot_base + 4 * w), lds32(slot_base + 4 * w + 4), sh);
+      } else {
+        x = lds32(slot_base) << static_cast<std::uint32_t>(-ig * 4);
+      }
+      const std::uint32_t p = __ldg(pk + (g >> 3));
+      std::uint32_t r0, r1;
+      merge8(x, p, r0, r1);
+      const std::uint64_t rel = g - R.e0;  // g >= e0 since e0 % 8 == 0
+      const std::uint32_t t = static_cast<std::uint32_t>(rel >> 14);
+      const std::uint32_t dst = R.a_base + (t % R.stages) * kTileElems + static_cast<std::uint32_t>(rel & 16383);
+      if (g >= lo && g + 8 <= hi) {
+        asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(dst), "r"(r0), "r"(r1) : "memory");
+      } else {
+        const std::uint64_t b0 = g < lo ? lo : g, b1 = g + 8 < hi ? g + 8 : hi;
+        for (std::uint64_t o = b0; o < b1; ++o) {
+          const std::uint32_t j = static_cast<std::uint32_t>(o - g);
+          const std::uint32_t byte = ((j < 4 ? r0 : r1) >> (8 * (j & 3))) & 0xFFu;
+          asm volatile("st.shared.u8 [%0], %1;" ::"r"(dst + j), "r"(byte) : "memory");
+        }
+      }
+    }
+  }
+  // publish: every writer fences its generic-proxy stores for the tensor
+  // core's async proxy, then lane 0 arrives with the warp's byte counts
+  const std::uint64_t t0 = R.e0 + (static_cast<std::uint64_t>(tf) << 14);
+  std::uint32_t bf = lo < hi ? overlap(lo, hi, t0, t0 + kTileElems) : 0u;
+  std::uint32_t bl = (lo < hi && tl != tf) ? overlap(lo, hi, t0 + kTileElems, t0 + 2 * kTileElems) : 0u;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    bf += __shfl_xor_sync(0xffffffffu, bf, o);
+    bl += __shfl_xor_sync(0xffffffffu, bl, o);
+  }
+  fence_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    if (bf) mbar_arrive(smem_addr(&g_full[tf % R.stages]), bf);
+    if (bl) mbar_arrive(smem_addr(&g_full[tl % R.stages]), bl);
+  }
+}
+
+__global__ void __launch_bounds__(kThreadsF, 1) fused_gemm_kernel(const FusedArgs args) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const FusedCta cta = args.plan[blockIdx.x];
+  const std::uint32_t n_kt = cta.kt1 - cta.kt0;
+
+  // dynamic smem: [pad to 1024][A ring][B ring x2][decode slots]
+  const std::uint32_t raw = smem_addr(smem_raw);
+  const std::uint32_t a_base = (raw + 1023u) & ~1023u;
+  const std::uint32_t b_base = a_base + args.stages_a * kTileElems;
+  const std::uint32_t b_bytes = args.m_pad * 128u;
+  std::uint32_t* const slots =
+      reinterpret_cast<std::uint32_t*>(smem_raw + (b_base + 2 * b_bytes - raw));
+
+  TensorDesc d = args.w;
+  d.blk_begin = cta.blk_begin;
+  d.blk_end = cta.blk_end;
+  d.tile_begin = 0;
+  const std::uint32_t log2T = 31 - __clz(d.T);
+  const std::uint32_t m_blk = 256u >> log2T;
+  const std::uint64_t n_tiles = (cta.blk_end - cta.blk_begin + m_blk - 1) / m_blk;
+
+  if (warp == kCtrlWarp) {
+    // TMEM accumulator: 128 lanes x m_pad fp32 columns (power of two >= 32)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&g_tmem)),
+                 "r"(args.tmem_cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if (lane == 0) {
+      for (std::uint32_t s = 0; s < args.stages_a; ++s) {
+        mbar_init(smem_addr(&g_full[s]), kTileElems);
+        mbar_init(smem_addr(&g_empty[s]), 1);
+      }
+      mbar_init(smem_addr(&g_bfree[0]), 1);
+      mbar_init(smem_addr(&g_bfree[1]), 1);
+      mbar_init(smem_addr(&g_done), 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      g_qnext = kDecodeWarps;
+    }
+  }
+  stage_tables(d, g_tbf, threadIdx.x, kThreadsF);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const std::uint32_t tmem_d = g_tmem;
+
+  if (warp < kDecodeWarps) {
+    // ---- decode warps: dynamic queue over the CTA's ECF8 tiles, in order
+    const Ring R{a_base, args.stages_a, cta.e0, cta.e1};
+    const std::uint32_t len_off = (d.n_luts - 1) << 8;
+    std::uint32_t* const slot = slots + (warp * 32 + lane) * kSlotStride;
+    WarpIn nxt;
+    std::uint64_t tile = warp;
+    if (tile < n_tiles) load_warp_tile(d, tile, log2T, lane, nxt);
+    while (tile < n_tiles) {
+      const WarpIn cur = nxt;
+      unsigned long long claim = 0;
+      if (lane == 0) claim = atomicAdd(&g_qnext, 1ull);
+      const std::uint64_t next = __shfl_sync(0xffffffffu, claim, 0);
+      if (next < n_tiles) load_warp_tile(d, next, log2T, lane, nxt);
+      ring_tile(d, cur, log2T, len_off, slot, R, lane);
+      tile = next;
+    }
+  } else {
+    // ---- control warp: X tiles -> B ring, one lane issues the MMAs
+    const std::uint32_t idesc = (1u << 4)                       // D = f32
+                                | (args.w_fmt << 7)             // A = W (E4M3 0 / E5M2 1)
+                                | (0u << 10)                    // B = X E4M3
+                                | ((args.m_pad >> 3) << 17)     // N
+                                | ((128u >> 4) << 24);          // M
+    const std::uint32_t chunks = args.m_pad * 8;  // 16-byte chunks per B tile
+    for (std::uint32_t t = 0; t < n_kt; ++t) {
+      const std::uint32_t bs = t & 1;
+      if (t >= 2) mbar_wait(smem_addr(&g_bfree[bs]), ((t >> 1) - 1) & 1u);
+      const std::uint32_t bdst = b_base + bs * b_bytes;
+      const std::uint64_t kcol = static_cast<std::uint64_t>(cta.kt0 + t) * 128;
+      for (std::uint32_t c = lane; c < chunks; c += 32) {
+        const std::uint32_t r = c >> 3, ch = c & 7;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (r < args.m) v = __ldg(reinterpret_cast<const uint4*>(args.x + static_cast<std::uint64_t>(r) * args.k + kcol) + ch);
+        const std::uint32_t dst = bdst + r * 128 + ((ch ^ (r & 7)) << 4);
+        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(dst), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                     : "memory");
+      }
+      fence_async_smem();
+      __syncwarp();
+      const std::uint32_t s = t % args.stages_a;
+      mbar_wait(smem_addr(&g_full[s]), (t / args.stages_a) & 1u);
+      tc_fence_after();
+      if (lane == 0) {
+        const std::uint32_t a_st = a_base + s * kTileElems;
+#pragma unroll
+        for (std::uint32_t k = 0; k < 4; ++k)
+          mma_f8(tmem_d, smem_desc(a_st + 32 * k), smem_desc(bdst + 32 * k), idesc, (t | k) != 0);
+        tc_commit(smem_addr(&g_empty[s]));
+        tc_commit(smem_addr(&g_bfree[bs]));
+        if (t + 1 == n_kt) tc_commit(smem_addr(&g_done));
+      }
+      __syncwarp();
+    }
+  }
+
+  // ---- epilogue: warps 0-3 own TMEM lanes 32w .. 32w+31 (= W rows)
+  if (warp < 4) {
+    mbar_wait(smem_addr(&g_done), 0);
+    tc_fence_after();
+    const std::uint32_t row = warp * 32 + lane;
+    const std::uint64_t n = static_cast<std::uint64_t>(cta.nt) * 128 + row;
+    const std::uint32_t tq = tmem_d + (static_cast<std::uint32_t>(warp * 32) << 16);
+    for (std::uint32_t c0 = 0; c0 < args.m; c0 += 8) {
+      float v[8];
+      tmem_ld8(tq + c0, v);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const std::uint32_t mcol = c0 + j;
+        if (mcol < args.m) {
+          float* dst = args.y + static_cast<std::uint64_t>(mcol) * args.n + n;
+          const float val = v[j] * args.scale;
+          if (args.split_k > 1) atomicAdd(dst, val);
+          else *dst = val;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kCtrlWarp) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d), "r"(args.tmem_cols)
+                 : "memory");
+  }
+}
+
+}  // namespace
+
+std::uint32_t fused_stages_a(std::uint32_t m_pad) {
+  // 227 KB per CTA: tables 28.6 KB static, slots 20 x 32 x 33 x 4 B,
+  // B ring 2 x m_pad x 128 B, A ring stages x 16 KB, 1 KB alignment slack
+  const std::uint32_t budget = 232448 - 30 * 1024;
+  const std::uint32_t fixed = kDecodeWarps * 32 * kSlotStride * 4 + 2 * m_pad * 128 + 1024;
+  const std::uint32_t s = fixed < budget ? (budget - fixed) / kTileElems : 0;
+  return s > kMaxStagesA ? kMaxStagesA : s;
+}
+
+std::uint32_t fused_smem_bytes(std::uint32_t m_pad, std::uint32_t stages_a) {
+  return 1024 + stages_a * kTileElems + 2 * m_pad * 128 + kDecodeWarps * 32 * kSlotStride * 4;
+}
+
+cudaError_t launch_fused_gemm(const FusedArgs& args, std::uint32_t n_cta, cudaStream_t s) {
+  const std::uint32_t smem = fused_smem_bytes(args.m_pad, args.stages_a);
+  cudaError_t e = cudaFuncSetAttribute(fused_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  fused_gemm_kernel<<<n_cta, kThreadsF, smem, s>>>(args);
+  return cudaGetLastError();
+}
+
+}  // namespace ecf8::dev

@@ -216,6 +216,30 @@ int ecf8_host_decompress(const uint8_t* bytes, size_t len, uint8_t** out, size_t
   });
 }
 
+int ecf8_host_fused_layout(const uint8_t* w, uint64_t n, uint64_t k, uint8_t* out, int inverse) {
+  return guarded([&] {
+    if (!w || !out) throw std::invalid_argument("null argument");
+    if (n % 128 || k % 128) throw std::invalid_argument("fused layout needs n, k multiples of 128");
+    const std::uint64_t KT = k / 128, NT = n / 128;
+#pragma omp parallel for schedule(static)
+    for (std::int64_t t = 0; t < static_cast<std::int64_t>(NT * KT); ++t) {
+      const std::uint64_t nt = static_cast<std::uint64_t>(t) / KT, kt = static_cast<std::uint64_t>(t) % KT;
+      std::uint8_t* tile = out + static_cast<std::uint64_t>(t) * 16384;
+      const std::uint8_t* itile = w + static_cast<std::uint64_t>(t) * 16384;
+      for (std::uint64_t r = 0; r < 128; ++r) {
+        const std::uint64_t row = (nt * 128 + r) * k + kt * 128;
+        for (std::uint64_t c = 0; c < 8; ++c) {  // 16-byte chunks, 128B swizzle
+          const std::uint64_t img = r * 128 + ((c ^ (r & 7)) << 4);
+          if (inverse)
+            std::memcpy(out + row + 16 * c, itile + img, 16);
+          else
+            std::memcpy(tile + img, w + row + 16 * c, 16);
+        }
+      }
+    }
+  });
+}
+
 int ecf8_host_synth(double alpha, double gamma, uint64_t n, uint64_t seed, int fmt, uint8_t* out,
                     int nthreads) {
   return guarded([&] {
