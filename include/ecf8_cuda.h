@@ -124,7 +124,9 @@ int ecf8_batch_launches(const ecf8_batch *b);
  * fused handle keeps a pointer to `t`, which must outlive it. */
 int ecf8_fused_create(const ecf8_dev_tensor *t, uint64_t n, uint64_t k, int w_fmt, ecf8_fused **out);
 int ecf8_fused_gemm(const ecf8_fused *f, const uint8_t *d_x, uint32_t m, float scale, float *d_y, void *stream);
-/* K splits per 128-row tile chosen for the SM count (partials summed in y). */
+/* CTAs sharing one 128-row tile of W (rounded up): the launch is cut into
+ * balanced runs of weight tiles for whole waves of the SMs; partial sums are
+ * added into y. */
 int ecf8_fused_split_k(const ecf8_fused *f);
 void ecf8_fused_free(ecf8_fused *f);
 

@@ -167,6 +167,8 @@ struct ecf8_fused {
   const ecf8_dev_tensor* w = nullptr;
   ecf8::dev::FusedCta* d_plan = nullptr;
   std::uint32_t n_cta = 0, split_k = 1;
+  std::uint8_t* xt = nullptr;  // swizzled-X workspace (grow-only)
+  std::uint64_t xt_cap = 0;
   std::uint64_t n = 0, k = 0;
   std::uint32_t w_fmt = 0;
 };
@@ -646,49 +648,40 @@ int ecf8_fused_create(const ecf8_dev_tensor* t, uint64_t n, uint64_t k, int w_fm
     if (n == 0 || k == 0 || n % 128 || k % 128) return fail(ECF8_EINVAL, "fused GEMM needs n, k multiples of 128");
     if (t->n_elem != n * k) return fail(ECF8_EINVAL, "output size mismatch");
     if (w_fmt != 0 && w_fmt != 1) return fail(ECF8_EINVAL, "weight format must be 0 (E4M3) or 1 (E5M2)");
-    if (ecf8::dev::variant_for(t->T, t->desc.lmin).id != 4)
-      return fail(ECF8_EINVAL, "fused GEMM needs T in [8, 256] and a shortest code of >= 2 bits");
+    if (ecf8::dev::fused_lane_windows(t->T, t->desc.lmin) == 0)
+      return fail(ECF8_EINVAL, "fused GEMM needs T in [8, 256] (T <= 128 when a code word is 1 bit)");
     if (int rc = require_device()) return rc;
     std::vector<std::uint64_t> outpos(t->n_blocks + 1);
     cu(cudaMemcpy(outpos.data(), t->desc.outpos, 8 * outpos.size(), cudaMemcpyDeviceToHost), "D2H outpos");
-    // split-K so that the CTA count fills whole waves of the SMs
+    // whole waves of the SMs (one CTA per SM); enough waves that a CTA's run
+    // of tiles spans at most two n-tiles (two TMEM accumulators)
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const std::uint64_t nt = n / 128, KT = k / 128;
-    std::uint32_t best = 1;
-    double best_eff = 0;
-    for (std::uint32_t sk = 1; sk <= 16 && KT / sk >= 4; ++sk) {
-      const double ctas = static_cast<double>(nt * sk);
-      const double eff = ctas / (sms * std::ceil(ctas / sms));
-      if (eff > best_eff + 0.02) {
-        best_eff = eff;
-        best = sk;
-      }
-    }
+    const std::uint64_t KT = k / 128, total = (n / 128) * KT;
+    std::uint64_t waves = (total + static_cast<std::uint64_t>(sms) * KT - 1) / (static_cast<std::uint64_t>(sms) * KT);
+    if (waves == 0) waves = 1;
+    std::uint64_t ctas = std::min<std::uint64_t>(total, waves * static_cast<std::uint64_t>(sms));
     auto f = std::make_unique<ecf8_fused>();
     f->w = t;
     f->n = n;
     f->k = k;
     f->w_fmt = static_cast<std::uint32_t>(w_fmt);
-    f->split_k = best;
+    f->split_k = static_cast<std::uint32_t>((ctas + n / 128 - 1) / (n / 128));
     std::vector<ecf8::dev::FusedCta> plan;
-    for (std::uint64_t r = 0; r < nt; ++r)
-      for (std::uint32_t sk = 0; sk < best; ++sk) {
-        ecf8::dev::FusedCta c{};
-        c.nt = static_cast<std::uint32_t>(r);
-        c.kt0 = static_cast<std::uint32_t>(KT * sk / best);
-        c.kt1 = static_cast<std::uint32_t>(KT * (sk + 1) / best);
-        c.e0 = (r * KT + c.kt0) * 16384;
-        c.e1 = (r * KT + c.kt1) * 16384;
-        // blocks overlapping [e0, e1): last block starting <= e0 .. first block starting >= e1
-        auto ub = std::upper_bound(outpos.begin(), outpos.end() - 1, c.e0);
-        c.blk_begin = static_cast<std::uint64_t>(ub - outpos.begin()) - 1;
-        auto lb = std::lower_bound(outpos.begin(), outpos.end(), c.e1);
-        c.blk_end = static_cast<std::uint64_t>(lb - outpos.begin());
-        if (c.blk_end > t->n_blocks) c.blk_end = t->n_blocks;
-        plan.push_back(c);
-      }
+    for (std::uint64_t c = 0; c < ctas; ++c) {
+      ecf8::dev::FusedCta p{};
+      p.tile0 = static_cast<std::uint32_t>(total * c / ctas);
+      p.tile1 = static_cast<std::uint32_t>(total * (c + 1) / ctas);
+      p.e0 = std::uint64_t{p.tile0} * 16384;
+      p.e1 = std::uint64_t{p.tile1} * 16384;
+      // blocks overlapping [e0, e1): the block holding element e0 .. first block starting >= e1
+      auto ub = std::upper_bound(outpos.begin(), outpos.end() - 1, p.e0);
+      p.blk_begin = static_cast<std::uint64_t>(ub - outpos.begin()) - 1;
+      auto lb = std::lower_bound(outpos.begin(), outpos.end(), p.e1);
+      p.blk_end = std::min<std::uint64_t>(static_cast<std::uint64_t>(lb - outpos.begin()), t->n_blocks);
+      plan.push_back(p);
+    }
     f->n_cta = static_cast<std::uint32_t>(plan.size());
     cu(cudaMalloc(&f->d_plan, sizeof(ecf8::dev::FusedCta) * plan.size()), "cudaMalloc(plan)");
     cu(cudaMemcpy(f->d_plan, plan.data(), sizeof(ecf8::dev::FusedCta) * plan.size(), cudaMemcpyHostToDevice),
@@ -712,6 +705,17 @@ int ecf8_fused_gemm(const ecf8_fused* f, const uint8_t* d_x, uint32_t m, float s
     a.plan = f->d_plan;
     a.x = d_x;
     a.y = d_y;
+    auto* mf = const_cast<ecf8_fused*>(f);
+    const std::uint64_t xt_need = f->k * ((m + 15) / 16 * 16);
+    if (xt_need > mf->xt_cap) {
+      cu(cudaStreamSynchronize(st), "sync");
+      if (mf->xt) cudaFree(mf->xt);
+      mf->xt = nullptr;
+      mf->xt_cap = 0;
+      cu(cudaMalloc(&mf->xt, xt_need), "cudaMalloc(x tiles)");
+      mf->xt_cap = xt_need;
+    }
+    a.xt = mf->xt;
     a.m = m;
     a.m_pad = (m + 15) / 16 * 16;
     a.n = static_cast<std::uint32_t>(f->n);
@@ -719,11 +723,12 @@ int ecf8_fused_gemm(const ecf8_fused* f, const uint8_t* d_x, uint32_t m, float s
     a.split_k = f->split_k;
     a.stages_a = ecf8::dev::fused_stages_a(a.m_pad);
     if (a.stages_a < 2) return fail(ECF8_EINVAL, "fused GEMM: shared memory too small for this m");
-    a.tmem_cols = 32;
-    while (a.tmem_cols < a.m_pad) a.tmem_cols <<= 1;
+    a.acc_cols = 32;
+    while (a.acc_cols < a.m_pad) a.acc_cols <<= 1;
+    a.tmem_cols = 2 * a.acc_cols;
     a.w_fmt = f->w_fmt;
     a.scale = scale;
-    if (f->split_k > 1) cu(cudaMemsetAsync(d_y, 0, sizeof(float) * m * f->n, st), "memset y");
+    cu(cudaMemsetAsync(d_y, 0, sizeof(float) * m * f->n, st), "memset y");
     cu(ecf8::dev::launch_fused_gemm(a, f->n_cta, st), "fused GEMM launch");
     return ECF8_OK;
   });
@@ -732,6 +737,7 @@ int ecf8_fused_gemm(const ecf8_fused* f, const uint8_t* d_x, uint32_t m, float s
 void ecf8_fused_free(ecf8_fused* f) {
   if (!f) return;
   if (f->d_plan) cudaFree(f->d_plan);
+  if (f->xt) cudaFree(f->xt);
   delete f;
 }
 

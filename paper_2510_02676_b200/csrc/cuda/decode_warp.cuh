@@ -1,12 +1,15 @@
 // decode_warp.cuh -- the per-warp ECF8 tile decode shared by the standalone
 // decode kernel (decode_warp.cu) and the decode-fused GEMM (fused_gemm.cu).
 //
-// A warp owns a tile of 256 consecutive 64-bit windows = 256/T whole
-// reference blocks (T in [8, 256], shortest code >= 2 bits), eight windows
-// per lane.  warp_decode_scan() walks each lane's windows into its 32-word
-// nibble slot and returns the lane's clamped output run relative to the
-// tile's first element -- codec.cpp:201-253 (count, scan, clamp) restated
-// per warp with the block offsets taken from outpos[].
+// A warp owns a tile of 32 * LW consecutive 64-bit windows = 32*LW/T whole
+// reference blocks, LW windows per lane.  A window holds at most
+// ceil(64 / Lmin) symbols, so a lane's 32-word (256-nibble) slot takes
+//   LW = 8 windows when the shortest code Lmin >= 2 (T in [8, 256]),
+//   LW = 4 windows when Lmin == 1 (T in [4, 128]).
+// warp_decode_scan() walks each lane's windows into its nibble slot and
+// returns the lane's clamped output run relative to the tile's first element
+// -- codec.cpp:201-253 (count, scan, clamp) restated per warp with the block
+// offsets taken from outpos[].
 #pragma once
 
 #include <cstdint>
@@ -16,10 +19,11 @@
 
 namespace ecf8::dev {
 
-constexpr int kLaneWin = 8;   // windows per lane
-constexpr int kSlotWords = 32;  // 8 windows x 32 symbols / 8 nibbles per word
+constexpr int kLaneWin = 8;     // windows per lane (Lmin >= 2)
+constexpr int kSlotWords = 32;  // 256 nibbles: 8 windows x 32 or 4 x 64 symbols
 
-struct WarpIn {
+template <int LW>
+struct WarpInT {
   uint4 w01, w23, w45, w67;  // window bytes (little-endian 32-bit words)
   uint2 w8;                  // first 8 bytes of the next window (lookahead)
   std::uint32_t gaps;        // 8 gap nibbles, window 2j in the high nibble of byte j
@@ -28,25 +32,33 @@ struct WarpIn {
   std::uint32_t nblk, nwin;
   std::uint64_t b0;
 };
+using WarpIn = WarpInT<kLaneWin>;
 
+template <int LW>
 __device__ __forceinline__ void load_warp_tile(const TensorDesc& d, std::uint64_t tile, std::uint32_t log2T,
-                                               int lane, WarpIn& in) {
-  const std::uint32_t m = 256u >> log2T;  // blocks per tile
+                                               int lane, WarpInT<LW>& in) {
+  const std::uint32_t m = (32u * LW) >> log2T;  // blocks per tile
   in.b0 = d.blk_begin + (tile - d.tile_begin) * m;
   in.nblk = static_cast<std::uint32_t>(d.blk_end - in.b0 < m ? d.blk_end - in.b0 : m);
   in.nwin = in.nblk << log2T;
   const std::uint64_t w0g = in.b0 << log2T;
-  const std::uint32_t wl = static_cast<std::uint32_t>(lane) * kLaneWin;
+  const std::uint32_t wl = static_cast<std::uint32_t>(lane) * LW;
   in.A = __ldg(d.outpos + in.b0);
   in.E = __ldg(d.outpos + in.b0 + in.nblk);
   if (wl < in.nwin) {
     const uint4* src = reinterpret_cast<const uint4*>(d.encoded + 8 * (w0g + wl));
     in.w01 = __ldg(src);
     in.w23 = __ldg(src + 1);
-    in.w45 = __ldg(src + 2);
-    in.w67 = __ldg(src + 3);
-    in.w8 = __ldg(reinterpret_cast<const uint2*>(src + 4));
-    in.gaps = __ldg(reinterpret_cast<const std::uint32_t*>(d.gaps + (w0g >> 1)) + lane);
+    if constexpr (LW == 8) {
+      in.w45 = __ldg(src + 2);
+      in.w67 = __ldg(src + 3);
+      in.w8 = __ldg(reinterpret_cast<const uint2*>(src + 4));
+      in.gaps = __ldg(reinterpret_cast<const std::uint32_t*>(d.gaps + (w0g >> 1)) + lane);
+    } else {
+      static_assert(LW == 4, "4 or 8 windows per lane");
+      in.w8 = __ldg(reinterpret_cast<const uint2*>(src + 2));
+      in.gaps = __ldg(reinterpret_cast<const std::uint16_t*>(d.gaps + (w0g >> 1)) + lane);
+    }
     const std::uint32_t bl = wl >> log2T;
     in.o0 = __ldg(d.outpos + in.b0 + bl);
     in.o1 = __ldg(d.outpos + in.b0 + bl + 1);
@@ -64,21 +76,26 @@ struct LaneRun {
 
 // Decode this lane's windows into `slot` (kSlotWords words, nibble i of the
 // run in bits 4(i%8).. of word i/8), then scan + clamp across the warp.
-__device__ __forceinline__ LaneRun warp_decode_scan(const WarpIn& in, std::uint32_t log2T, std::uint32_t len_off,
-                                                   const Tables& tb, std::uint32_t* slot, int lane) {
-  const std::uint32_t wl0 = static_cast<std::uint32_t>(lane) * kLaneWin;
+template <int LW>
+__device__ __forceinline__ LaneRun warp_decode_scan(const WarpInT<LW>& in, std::uint32_t log2T,
+                                                   std::uint32_t len_off, const Tables& tb, std::uint32_t* slot,
+                                                   int lane) {
+  const std::uint32_t wl0 = static_cast<std::uint32_t>(lane) * LW;
   const bool active = wl0 < in.nwin;
   const std::uint32_t slot_base = smem_addr(slot);
   SlotSink sink{slot_base};
   if (active) {
-    const std::uint32_t w[18] = {bswap32(in.w01.x), bswap32(in.w01.y), bswap32(in.w01.z), bswap32(in.w01.w),
-                                 bswap32(in.w23.x), bswap32(in.w23.y), bswap32(in.w23.z), bswap32(in.w23.w),
-                                 bswap32(in.w45.x), bswap32(in.w45.y), bswap32(in.w45.z), bswap32(in.w45.w),
-                                 bswap32(in.w67.x), bswap32(in.w67.y), bswap32(in.w67.z), bswap32(in.w67.w),
-                                 bswap32(in.w8.x),  bswap32(in.w8.y)};
-    const std::uint32_t n = min(in.nwin - wl0, static_cast<std::uint32_t>(kLaneWin));
+    std::uint32_t w[2 * LW + 2];
+    w[0] = bswap32(in.w01.x), w[1] = bswap32(in.w01.y), w[2] = bswap32(in.w01.z), w[3] = bswap32(in.w01.w);
+    w[4] = bswap32(in.w23.x), w[5] = bswap32(in.w23.y), w[6] = bswap32(in.w23.z), w[7] = bswap32(in.w23.w);
+    if constexpr (LW == 8) {
+      w[8] = bswap32(in.w45.x), w[9] = bswap32(in.w45.y), w[10] = bswap32(in.w45.z), w[11] = bswap32(in.w45.w);
+      w[12] = bswap32(in.w67.x), w[13] = bswap32(in.w67.y), w[14] = bswap32(in.w67.z), w[15] = bswap32(in.w67.w);
+    }
+    w[2 * LW] = bswap32(in.w8.x), w[2 * LW + 1] = bswap32(in.w8.y);
+    const std::uint32_t n = min(in.nwin - wl0, static_cast<std::uint32_t>(LW));
 #pragma unroll
-    for (int i = 0; i < kLaneWin; ++i) {
+    for (int i = 0; i < LW; ++i) {
       if (static_cast<std::uint32_t>(i) < n) {
         // byte j of the gap word: window 2j in the high nibble, 2j + 1 low
         const std::uint32_t gap = (in.gaps >> (8 * (i >> 1) + ((i & 1) ? 0 : 4))) & 15u;
@@ -96,7 +113,8 @@ __device__ __forceinline__ LaneRun warp_decode_scan(const WarpIn& in, std::uint3
     if (lane >= o) incl += y;
   }
   const std::uint32_t excl = incl - cnt;
-  const std::uint32_t lpb_mask = (1u << (log2T - 3)) - 1;  // lanes per block - 1
+  constexpr std::uint32_t kLog2LW = LW == 8 ? 3 : 2;
+  const std::uint32_t lpb_mask = (1u << (log2T - kLog2LW)) - 1;  // lanes per block - 1
   const std::uint32_t first_excl = __shfl_sync(0xffffffffu, excl, static_cast<std::uint32_t>(lane) & ~lpb_mask);
   const std::uint32_t start_rel = static_cast<std::uint32_t>(in.o0 - in.A) + excl - first_excl;
   const std::uint32_t lim_rel = static_cast<std::uint32_t>(in.o1 - in.A);

@@ -15,17 +15,19 @@
 // 1-D tensor for the (unchanged) ECF8 encoder.  A decoded element's tile-
 // major index therefore IS its shared-memory offset within its tile.
 //
-// CTA = one 128-row n-tile x a contiguous K range [kt0, kt1) (split-K when
-// N/128 alone would under-fill the 148 SMs; partial sums are added with
-// red.global.add.f32).  Warp roles:
+// CTA = a contiguous run of weight tiles in tile-major order, balanced over
+// the launch (a whole number of waves of the 148 SMs, one CTA per SM); a run
+// spans at most two n-tiles, each accumulated in its own TMEM block, and the
+// partial rows are added into y with red.global.add.f32.  Warp roles:
 //   decode warps (kDecodeWarps)  claim ECF8 tiles (256 windows, decode_warp.cuh)
 //       covering the CTA's element range in order, decode them into their
 //       nibble slots, then merge exponent + sign/mantissa nibbles and store
 //       the FP8 bytes straight into the A ring stage of their K tile; each
 //       warp arrives on the stage's "full" mbarrier with the number of bytes
 //       it wrote (a stage completes at 16384 bytes).
-//   control warp   allocates TMEM, loads X K-tiles into a 2-stage B ring
-//       (swizzled like A), and one elected lane issues
+//   control warp   allocates TMEM, streams X K-tiles (pre-swizzled by
+//       x_tiles_kernel) into a 2-stage B ring by bulk async copy, and one lane
+//       issues
 //       tcgen05.mma.cta_group::1.kind::f8f6f4 (M = 128 W rows, N = padded
 //       token count, K = 32 per instruction, 4 per K tile) with the fp32
 //       accumulator in TMEM; tcgen05.commit frees A / B stages.
@@ -56,9 +58,10 @@ __shared__ Tables g_tbf;
 __shared__ unsigned long long g_qnext;
 __shared__ alignas(8) unsigned long long g_full[kMaxStagesA];
 __shared__ alignas(8) unsigned long long g_empty[kMaxStagesA];
-__shared__ alignas(8) unsigned long long g_bfree[2];
+__shared__ alignas(8) unsigned long long g_bfull[2];
 __shared__ alignas(8) unsigned long long g_done;
 __shared__ std::uint32_t g_tmem;
+__shared__ std::uint32_t g_consumed;  // K tiles whose MMAs have completed (stage reusable)
 
 // ---- PTX helpers ---------------------------------------------------------
 
@@ -130,10 +133,21 @@ struct Ring {
   std::uint64_t e0, e1;  // CTA element range (tile-major), multiples of 16384
 };
 
+// Decode warps run up to ~20 ECF8 tiles (~8 K tiles) ahead of the MMA, more
+// than the ring holds, so a parity wait on the stage's "empty" barrier could
+// alias a phase two completions back.  The control warp instead publishes a
+// monotonic count of consumed K tiles; K tile t may be written once tile
+// t - stages has been consumed.
 __device__ __forceinline__ void wait_stage_free(const Ring& R, std::uint32_t t) {
   if (t < R.stages) return;
-  const std::uint32_t s = t % R.stages;
-  mbar_wait(smem_addr(&g_empty[s]), ((t / R.stages) - 1) & 1u);
+  const std::uint32_t need = t - R.stages + 1;
+  const std::uint32_t addr = smem_addr(&g_consumed);
+  while (true) {
+    std::uint32_t v;
+    asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+    if (v >= need) break;
+    __nanosleep(64);
+  }
 }
 
 // Bytes of element range [lo, hi) that fall in ring tile t.
@@ -143,7 +157,8 @@ __device__ __forceinline__ std::uint32_t overlap(std::uint64_t lo, std::uint64_t
   return b > a ? static_cast<std::uint32_t>(b - a) : 0u;
 }
 
-__device__ __forceinline__ void ring_tile(const TensorDesc& d, const WarpIn& in, std::uint32_t log2T,
+template <int LW>
+__device__ __forceinline__ void ring_tile(const TensorDesc& d, const WarpInT<LW>& in, std::uint32_t log2T,
                                           std::uint32_t len_off, std::uint32_t* slot, const Ring& R, int lane) {
   const LaneRun run = warp_decode_scan(in, log2T, len_off, g_tbf, slot, lane);
 
@@ -207,11 +222,14 @@ __device__ __forceinline__ void ring_tile(const TensorDesc& d, const WarpIn& in,
   }
 }
 
+template <int LW>
 __global__ void __launch_bounds__(kThreadsF, 1) fused_gemm_kernel(const FusedArgs args) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const FusedCta cta = args.plan[blockIdx.x];
-  const std::uint32_t n_kt = cta.kt1 - cta.kt0;
+  const std::uint32_t n_kt = cta.tile1 - cta.tile0;
+  const std::uint32_t KT = args.k / 128;
+  const std::uint32_t nt0 = cta.tile0 / KT;  // first n-tile (segment 0)
 
   // dynamic smem: [pad to 1024][A ring][B ring x2][decode slots]
   const std::uint32_t raw = smem_addr(smem_raw);
@@ -226,7 +244,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) fused_gemm_kernel(const FusedArg
   d.blk_end = cta.blk_end;
   d.tile_begin = 0;
   const std::uint32_t log2T = 31 - __clz(d.T);
-  const std::uint32_t m_blk = 256u >> log2T;
+  const std::uint32_t m_blk = (32u * LW) >> log2T;
   const std::uint64_t n_tiles = (cta.blk_end - cta.blk_begin + m_blk - 1) / m_blk;
 
   if (warp == kCtrlWarp) {
@@ -240,11 +258,12 @@ __global__ void __launch_bounds__(kThreadsF, 1) fused_gemm_kernel(const FusedArg
         mbar_init(smem_addr(&g_full[s]), kTileElems);
         mbar_init(smem_addr(&g_empty[s]), 1);
       }
-      mbar_init(smem_addr(&g_bfree[0]), 1);
-      mbar_init(smem_addr(&g_bfree[1]), 1);
+      mbar_init(smem_addr(&g_bfull[0]), 1);
+      mbar_init(smem_addr(&g_bfull[1]), 1);
       mbar_init(smem_addr(&g_done), 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       g_qnext = kDecodeWarps;
+      g_consumed = 0;
     }
   }
   stage_tables(d, g_tbf, threadIdx.x, kThreadsF);
@@ -258,13 +277,20 @@ __global__ void __launch_bounds__(kThreadsF, 1) fused_gemm_kernel(const FusedArg
     const Ring R{a_base, args.stages_a, cta.e0, cta.e1};
     const std::uint32_t len_off = (d.n_luts - 1) << 8;
     std::uint32_t* const slot = slots + (warp * 32 + lane) * kSlotStride;
-    WarpIn nxt;
+    WarpInT<LW> nxt;
     std::uint64_t tile = warp;
     if (tile < n_tiles) load_warp_tile(d, tile, log2T, lane, nxt);
     while (tile < n_tiles) {
-      const WarpIn cur = nxt;
+      const WarpInT<LW> cur = nxt;
       unsigned long long claim = 0;
-      if (lane == 0) claim = atomicAdd(&g_qnext, 1ull);
+      if (lane == 0) {
+        claim = atomicAdd(&g_qnext, 1ull);
+        // sign/mantissa bytes of this tile -> L2 while it decodes
+        const std::uint64_t p0 = (cur.A >> 1) & ~std::uint64_t{15};
+        const std::uint32_t bytes = static_cast<std::uint32_t>((((cur.E + 1) >> 1) - p0 + 15) & ~std::uint64_t{15});
+        if (bytes)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(d.packed + p0), "r"(bytes) : "memory");
+      }
       const std::uint64_t next = __shfl_sync(0xffffffffu, claim, 0);
       if (next < n_tiles) load_warp_tile(d, next, log2T, lane, nxt);
       ring_tile(d, cur, log2T, len_off, slot, R, lane);
@@ -277,22 +303,31 @@ __global__ void __launch_bounds__(kThreadsF, 1) fused_gemm_kernel(const FusedArg
                                 | (0u << 10)                    // B = X E4M3
                                 | ((args.m_pad >> 3) << 17)     // N
                                 | ((128u >> 4) << 24);          // M
-    const std::uint32_t chunks = args.m_pad * 8;  // 16-byte chunks per B tile
+    // X K-tiles arrive by bulk async copy (TMA engine) from the pre-swizzled
+    // xt (x_tiles_kernel): one contiguous m_pad x 128-byte image per K tile
+    auto issue_x = [&](std::uint32_t t) {
+      const std::uint32_t bsl = t & 1;
+      const std::uint32_t kt = (cta.tile0 + t) % KT;
+      const std::uint32_t bar = smem_addr(&g_bfull[bsl]);
+      asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(bar),
+                   "r"(b_bytes)
+                   : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       b_base + bsl * b_bytes),
+                   "l"(args.xt + static_cast<std::uint64_t>(kt) * b_bytes), "r"(b_bytes), "r"(bar)
+                   : "memory");
+    };
+    if (lane == 0 && n_kt) issue_x(0);
     for (std::uint32_t t = 0; t < n_kt; ++t) {
       const std::uint32_t bs = t & 1;
-      if (t >= 2) mbar_wait(smem_addr(&g_bfree[bs]), ((t >> 1) - 1) & 1u);
       const std::uint32_t bdst = b_base + bs * b_bytes;
-      const std::uint64_t kcol = static_cast<std::uint64_t>(cta.kt0 + t) * 128;
-      for (std::uint32_t c = lane; c < chunks; c += 32) {
-        const std::uint32_t r = c >> 3, ch = c & 7;
-        uint4 v = make_uint4(0, 0, 0, 0);
-        if (r < args.m) v = __ldg(reinterpret_cast<const uint4*>(args.x + static_cast<std::uint64_t>(r) * args.k + kcol) + ch);
-        const std::uint32_t dst = bdst + r * 128 + ((ch ^ (r & 7)) << 4);
-        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(dst), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
-                     : "memory");
-      }
-      fence_async_smem();
-      __syncwarp();
+      const std::uint32_t g = cta.tile0 + t;
+      const std::uint32_t seg = g / KT - nt0;
+      const bool first_of_seg = t == 0 || g % KT == 0;
+      // next K tile's X into the other stage (its previous reader, the MMAs
+      // of tile t-1, completed: waited on below at the end of iteration t-1)
+      if (lane == 0 && t + 1 < n_kt) issue_x(t + 1);
+      mbar_wait(smem_addr(&g_bfull[bs]), (t >> 1) & 1u);
       const std::uint32_t s = t % args.stages_a;
       mbar_wait(smem_addr(&g_full[s]), (t / args.stages_a) & 1u);
       tc_fence_after();
@@ -300,33 +335,36 @@ __global__ void __launch_bounds__(kThreadsF, 1) fused_gemm_kernel(const FusedArg
         const std::uint32_t a_st = a_base + s * kTileElems;
 #pragma unroll
         for (std::uint32_t k = 0; k < 4; ++k)
-          mma_f8(tmem_d, smem_desc(a_st + 32 * k), smem_desc(bdst + 32 * k), idesc, (t | k) != 0);
+          mma_f8(tmem_d + seg * args.acc_cols, smem_desc(a_st + 32 * k), smem_desc(bdst + 32 * k), idesc,
+                 !(first_of_seg && k == 0));
         tc_commit(smem_addr(&g_empty[s]));
-        tc_commit(smem_addr(&g_bfree[bs]));
         if (t + 1 == n_kt) tc_commit(smem_addr(&g_done));
+        // the MMAs of tile t have read stage s: publish it to the decode warps
+        mbar_wait(smem_addr(&g_empty[s]), (t / args.stages_a) & 1u);
+        asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_addr(&g_consumed)), "r"(t + 1)
+                     : "memory");
       }
       __syncwarp();
     }
   }
 
-  // ---- epilogue: warps 0-3 own TMEM lanes 32w .. 32w+31 (= W rows)
+  // ---- epilogue: warps 0-3 own TMEM lanes 32w .. 32w+31 (= W rows); one
+  //      accumulator block per n-tile segment, partial sums added into y
   if (warp < 4) {
     mbar_wait(smem_addr(&g_done), 0);
     tc_fence_after();
     const std::uint32_t row = warp * 32 + lane;
-    const std::uint64_t n = static_cast<std::uint64_t>(cta.nt) * 128 + row;
-    const std::uint32_t tq = tmem_d + (static_cast<std::uint32_t>(warp * 32) << 16);
-    for (std::uint32_t c0 = 0; c0 < args.m; c0 += 8) {
-      float v[8];
-      tmem_ld8(tq + c0, v);
+    const std::uint32_t nseg = (cta.tile1 - 1) / KT - nt0 + 1;
+    for (std::uint32_t sg = 0; sg < nseg; ++sg) {
+      const std::uint64_t n = static_cast<std::uint64_t>(nt0 + sg) * 128 + row;
+      const std::uint32_t tq = tmem_d + sg * args.acc_cols + (static_cast<std::uint32_t>(warp * 32) << 16);
+      for (std::uint32_t c0 = 0; c0 < args.m; c0 += 8) {
+        float v[8];
+        tmem_ld8(tq + c0, v);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const std::uint32_t mcol = c0 + j;
-        if (mcol < args.m) {
-          float* dst = args.y + static_cast<std::uint64_t>(mcol) * args.n + n;
-          const float val = v[j] * args.scale;
-          if (args.split_k > 1) atomicAdd(dst, val);
-          else *dst = val;
+        for (int j = 0; j < 8; ++j) {
+          const std::uint32_t mcol = c0 + j;
+          if (mcol < args.m) atomicAdd(args.y + static_cast<std::uint64_t>(mcol) * args.n + n, v[j] * args.scale);
         }
       }
     }
@@ -337,6 +375,24 @@ __global__ void __launch_bounds__(kThreadsF, 1) fused_gemm_kernel(const FusedArg
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d), "r"(args.tmem_cols)
                  : "memory");
+  }
+}
+
+// x [m, k] row-major -> xt [k/128][m_pad][128 B] in the 128B-swizzled
+// K-major image (rows >= m zero), so every B tile is one contiguous copy.
+__global__ void x_tiles_kernel(const std::uint8_t* __restrict__ x, std::uint8_t* __restrict__ xt, std::uint32_t m,
+                               std::uint32_t m_pad, std::uint32_t k) {
+  const std::uint64_t chunks = static_cast<std::uint64_t>(k / 128) * m_pad * 8;
+  for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < chunks;
+       i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+    const std::uint32_t ch = static_cast<std::uint32_t>(i & 7);
+    const std::uint64_t rr = i >> 3;
+    const std::uint32_t r = static_cast<std::uint32_t>(rr % m_pad);
+    const std::uint32_t kt = static_cast<std::uint32_t>(rr / m_pad);
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (r < m) v = __ldg(reinterpret_cast<const uint4*>(x + static_cast<std::uint64_t>(r) * k + kt * 128u) + ch);
+    const std::uint64_t dst = (static_cast<std::uint64_t>(kt) * m_pad + r) * 128 + ((ch ^ (r & 7u)) << 4);
+    *reinterpret_cast<uint4*>(xt + dst) = v;
   }
 }
 
@@ -355,13 +411,28 @@ std::uint32_t fused_smem_bytes(std::uint32_t m_pad, std::uint32_t stages_a) {
   return 1024 + stages_a * kTileElems + 2 * m_pad * 128 + kDecodeWarps * 32 * kSlotStride * 4;
 }
 
-cudaError_t launch_fused_gemm(const FusedArgs& args, std::uint32_t n_cta, cudaStream_t s) {
+template <int LW>
+cudaError_t launch_lw(const FusedArgs& args, std::uint32_t n_cta, cudaStream_t s) {
   const std::uint32_t smem = fused_smem_bytes(args.m_pad, args.stages_a);
-  cudaError_t e = cudaFuncSetAttribute(fused_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(fused_gemm_kernel<LW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  fused_gemm_kernel<<<n_cta, kThreadsF, smem, s>>>(args);
+  fused_gemm_kernel<LW><<<n_cta, kThreadsF, smem, s>>>(args);
   return cudaGetLastError();
+}
+
+int fused_lane_windows(std::uint32_t T, std::uint32_t lmin) {
+  if (lmin >= 2 && T >= 8 && T <= 256) return 8;
+  if (lmin >= 1 && T >= 4 && T <= 128) return 4;
+  return 0;
+}
+
+cudaError_t launch_fused_gemm(const FusedArgs& args, std::uint32_t n_cta, cudaStream_t s) {
+  const std::uint64_t chunks = static_cast<std::uint64_t>(args.k / 128) * args.m_pad * 8;
+  const unsigned blocks = static_cast<unsigned>(std::min<std::uint64_t>((chunks + 255) / 256, 4 * 148));
+  x_tiles_kernel<<<blocks, 256, 0, s>>>(args.x, const_cast<std::uint8_t*>(args.xt), args.m, args.m_pad, args.k);
+  if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) return e;
+  return fused_lane_windows(args.w.T, args.w.lmin) == 8 ? launch_lw<8>(args, n_cta, s) : launch_lw<4>(args, n_cta, s);
 }
 
 }  // namespace ecf8::dev

@@ -11,28 +11,35 @@ namespace ecf8::dev {
 
 constexpr std::uint32_t kMaxStagesA = 8;
 
-// One CTA's work: 128 W rows (n-tile nt) x K tiles [kt0, kt1); its elements
-// [e0, e1) of the tiled tensor live in ECF8 blocks [blk_begin, blk_end).
+// One CTA's work: the contiguous run of 128x128 weight tiles [tile0, tile1)
+// in tile-major (nt, kt) order -- at most two n-tiles ("segments"), each
+// accumulated in its own TMEM column block.  Its elements [e0, e1) of the
+// tiled tensor live in ECF8 blocks [blk_begin, blk_end).
 struct FusedCta {
   std::uint64_t blk_begin, blk_end;
   std::uint64_t e0, e1;
-  std::uint32_t nt, kt0, kt1, pad;
+  std::uint32_t tile0, tile1;
 };
 
 struct FusedArgs {
   TensorDesc w;              // the tiled ECF8 weight tensor (blk range set per CTA)
   const FusedCta* plan;      // one entry per CTA
   const std::uint8_t* x;     // [m, k] E4M3, row-major
-  float* y;                  // [m, n] fp32, row-major (zeroed when split_k > 1)
+  const std::uint8_t* xt;    // workspace: k * m_pad bytes (swizzled X tiles)
+  float* y;                  // [m, n] fp32, row-major, zeroed before the launch
   std::uint32_t m, m_pad;    // tokens; padded to a multiple of 16 (MMA N)
   std::uint32_t n, k;
   std::uint32_t split_k;
   std::uint32_t stages_a;
-  std::uint32_t tmem_cols;
+  std::uint32_t tmem_cols;  // allocation: 2 accumulators of acc_cols
+  std::uint32_t acc_cols;   // power of two >= max(32, m_pad)
   std::uint32_t w_fmt;       // 0 E4M3, 1 E5M2
   float scale;
 };
 
+// Windows per decode lane for a tiled weight: 8 (Lmin >= 2, T in [8, 256]),
+// 4 (Lmin == 1, T in [4, 128]), 0 = unsupported.
+int fused_lane_windows(std::uint32_t T, std::uint32_t lmin);
 std::uint32_t fused_stages_a(std::uint32_t m_pad);
 std::uint32_t fused_smem_bytes(std::uint32_t m_pad, std::uint32_t stages_a);
 cudaError_t launch_fused_gemm(const FusedArgs& args, std::uint32_t n_cta, cudaStream_t s);

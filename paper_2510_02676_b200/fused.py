@@ -41,9 +41,10 @@ def fused_layout_inverse(seq: np.ndarray, n: int, k: int) -> np.ndarray:
 class FusedLinear:
     """An ECF8-compressed FP8 weight [n, k] served by the decode-fused GEMM."""
 
-    def __init__(self, w_fp8: np.ndarray, fmt: str = "e4m3", threads_per_block: int = 256):
+    def __init__(self, w_fp8: np.ndarray, fmt: str = "e4m3", threads_per_block: int = 128):
         self.n, self.k = map(int, w_fp8.shape)
         self.fmt = fmt
+        # T = 128 serves both decode-lane widths (1-bit codes need T <= 128)
         self.encoded = codec.encode_tensor(fused_layout(w_fp8), threads_per_block)
         self.dev = DeviceTensor(self.encoded)
         h = C.c_void_p()
