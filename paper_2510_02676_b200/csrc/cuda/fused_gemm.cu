@@ -133,28 +133,25 @@ struct Ring {
   std::uint64_t e0, e1;  // CTA element range (tile-major), multiples of 16384
 };
 
-// Decode warps run up to ~20 ECF8 tiles (~8 K tiles) ahead of the MMA, more
-// than the ring holds, so a parity wait on the stage's "empty" barrier could
-// alias a phase two completions back.  The control warp instead publishes a
-// monotonic count of consumed K tiles; K tile t may be written once tile
-// t - stages has been consumed.
+// Writers of K tile t need stage t % S back from the MMAs of tile t - S
+// (completion u - 1 of that stage's "empty" barrier, u = t / S).  Decode
+// warps run up to ~8 K tiles ahead of the MMA, so a bare parity wait could
+// alias a completion two phases back; the control warp's monotonic count of
+// consumed K tiles first guarantees the barrier is at most one phase behind
+// (tile t - 2S consumed), then the hardware parity wait does the rest.
 __device__ __forceinline__ void wait_stage_free(const Ring& R, std::uint32_t t) {
   if (t < R.stages) return;
-  const std::uint32_t need = t - R.stages + 1;
-  const std::uint32_t addr = smem_addr(&g_consumed);
-  while (true) {
-    std::uint32_t v;
-    asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
-    if (v >= need) break;
-    __nanosleep(64);
+  if (t >= 2 * R.stages) {
+    const std::uint32_t need = t - 2 * R.stages + 1;
+    const std::uint32_t addr = smem_addr(&g_consumed);
+    while (true) {
+      std::uint32_t v;
+      asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+      if (v >= need) break;
+      __nanosleep(128);
+    }
   }
-}
-
-// Bytes of element range [lo, hi) that fall in ring tile t.
-__device__ __forceinline__ std::uint32_t overlap(std::uint64_t lo, std::uint64_t hi, std::uint64_t t0,
-                                                 std::uint64_t t1) {
-  const std::uint64_t a = lo > t0 ? lo : t0, b = hi < t1 ? hi : t1;
-  return b > a ? static_cast<std::uint32_t>(b - a) : 0u;
+  mbar_wait(smem_addr(&g_empty[t % R.stages]), ((t / R.stages) - 1) & 1u);
 }
 
 template <int LW>
@@ -171,44 +168,71 @@ __device__ __forceinline__ void ring_tile(const TensorDesc& d, const WarpInT<LW>
   wait_stage_free(R, tf);
   if (tl != tf) wait_stage_free(R, tl);
 
-  const std::uint64_t R0 = in.A + run.start, R1 = R0 + run.len;
-  const std::uint64_t lo = R0 > R.e0 ? R0 : R.e0, hi = R1 < R.e1 ? R1 : R.e1;
-  if (lo < hi) {
-    const std::uint32_t slot_base = smem_addr(slot);
-    const std::uint32_t* pk = reinterpret_cast<const std::uint32_t*>(d.packed);
-    for (std::uint64_t g = lo & ~std::uint64_t{7}; g < hi; g += 8) {
-      // exponent nibbles of elements g .. g+7 (run nibble ig = g - R0)
-      const long long ig = static_cast<long long>(g - R0);
+  // my run in CTA-relative element coordinates (a CTA run is < 2^31 elements)
+  const int rr0 = static_cast<int>(static_cast<long long>(in.A + run.start) - static_cast<long long>(R.e0));
+  const int span = static_cast<int>(R.e1 - R.e0);
+  const int lo_r = rr0 > 0 ? rr0 : 0;
+  const int hi_r = rr0 + static_cast<int>(run.len) < span ? rr0 + static_cast<int>(run.len) : span;
+  const std::uint32_t bnd = (tf + 1) << 14;  // first element of ring tile tf + 1
+  if (lo_r < hi_r) {
+    const std::uint32_t offA = R.a_base + (tf % R.stages) * kTileElems - (tf << 14);
+    const std::uint32_t offB = R.a_base + ((tf + 1) % R.stages) * kTileElems - bnd;
+    const std::uint32_t* pk = reinterpret_cast<const std::uint32_t*>(d.packed + (R.e0 >> 1));
+    const std::uint32_t sb = smem_addr(slot);
+    // a group of 8 elements starting at g (multiple of 8), bytes [b0, b1)
+    auto partial = [&](int g, int b0, int b1) {
+      const int ig = g - rr0;
       std::uint32_t x;
       if (ig >= 0) {
-        const std::uint32_t w = static_cast<std::uint32_t>(ig >> 3), sh = static_cast<std::uint32_t>(ig & 7) * 4;
-        x = __funnelshift_r(lds32(slot_base + 4 * w), lds32(slot_base + 4 * w + 4), sh);
+        const std::uint32_t w = static_cast<std::uint32_t>(ig) >> 3, sh = (static_cast<std::uint32_t>(ig) & 7) * 4;
+        x = __funnelshift_r(lds32(sb + 4 * w), lds32(sb + 4 * w + 4), sh);
       } else {
-        x = lds32(slot_base) << static_cast<std::uint32_t>(-ig * 4);
+        x = lds32(sb) << static_cast<std::uint32_t>(-ig * 4);
       }
-      const std::uint32_t p = __ldg(pk + (g >> 3));
       std::uint32_t r0, r1;
-      merge8(x, p, r0, r1);
-      const std::uint64_t rel = g - R.e0;  // g >= e0 since e0 % 8 == 0
-      const std::uint32_t t = static_cast<std::uint32_t>(rel >> 14);
-      const std::uint32_t dst = R.a_base + (t % R.stages) * kTileElems + static_cast<std::uint32_t>(rel & 16383);
-      if (g >= lo && g + 8 <= hi) {
-        asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(dst), "r"(r0), "r"(r1) : "memory");
-      } else {
-        const std::uint64_t b0 = g < lo ? lo : g, b1 = g + 8 < hi ? g + 8 : hi;
-        for (std::uint64_t o = b0; o < b1; ++o) {
-          const std::uint32_t j = static_cast<std::uint32_t>(o - g);
-          const std::uint32_t byte = ((j < 4 ? r0 : r1) >> (8 * (j & 3))) & 0xFFu;
-          asm volatile("st.shared.u8 [%0], %1;" ::"r"(dst + j), "r"(byte) : "memory");
+      merge8(x, __ldg(pk + (g >> 3)), r0, r1);
+      const std::uint32_t dst = (static_cast<std::uint32_t>(g) < bnd ? offA : offB) + static_cast<std::uint32_t>(g);
+      for (int o = b0; o < b1; ++o) {
+        const int j = o - g;
+        const std::uint32_t byte = ((j < 4 ? r0 : r1) >> (8 * (j & 3))) & 0xFFu;
+        asm volatile("st.shared.u8 [%0], %1;" ::"r"(dst + j), "r"(byte) : "memory");
+      }
+    };
+    const int g1 = (lo_r + 7) & ~7, g2 = hi_r & ~7;
+    if (g1 > g2) {
+      partial(lo_r & ~7, lo_r, hi_r);
+    } else {
+      if (lo_r < g1) partial(g1 - 8, lo_r, g1);
+      if (g1 < g2) {
+        // full groups: the run's nibbles slide through one word at a time
+        const std::uint32_t ig = static_cast<std::uint32_t>(g1 - rr0);
+        const std::uint32_t sh = (ig & 7) * 4;
+        std::uint32_t sa = sb + 4 * (ig >> 3);
+        std::uint32_t prev = lds32(sa);
+        for (int g = g1; g < g2; g += 8) {
+          sa += 4;
+          const std::uint32_t nxt = lds32(sa);
+          const std::uint32_t x = __funnelshift_r(prev, nxt, sh);
+          prev = nxt;
+          std::uint32_t r0, r1;
+          merge8(x, __ldg(pk + (g >> 3)), r0, r1);
+          const std::uint32_t dst = (static_cast<std::uint32_t>(g) < bnd ? offA : offB) + static_cast<std::uint32_t>(g);
+          asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(dst), "r"(r0), "r"(r1) : "memory");
         }
       }
+      if (g2 < hi_r) partial(g2, g2, hi_r);
     }
   }
   // publish: every writer fences its generic-proxy stores for the tensor
   // core's async proxy, then lane 0 arrives with the warp's byte counts
-  const std::uint64_t t0 = R.e0 + (static_cast<std::uint64_t>(tf) << 14);
-  std::uint32_t bf = lo < hi ? overlap(lo, hi, t0, t0 + kTileElems) : 0u;
-  std::uint32_t bl = (lo < hi && tl != tf) ? overlap(lo, hi, t0 + kTileElems, t0 + 2 * kTileElems) : 0u;
+  const int t0 = static_cast<int>(tf << 14), t1 = static_cast<int>(bnd), t2 = t1 + static_cast<int>(kTileElems);
+  std::uint32_t bf = 0, bl = 0;
+  if (lo_r < hi_r) {
+    const int a0 = lo_r > t0 ? lo_r : t0, a1 = hi_r < t1 ? hi_r : t1;
+    const int c0 = lo_r > t1 ? lo_r : t1, c1 = hi_r < t2 ? hi_r : t2;
+    bf = a1 > a0 ? static_cast<std::uint32_t>(a1 - a0) : 0u;
+    bl = c1 > c0 ? static_cast<std::uint32_t>(c1 - c0) : 0u;
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     bf += __shfl_xor_sync(0xffffffffu, bf, o);
@@ -218,7 +242,7 @@ __device__ __forceinline__ void ring_tile(const TensorDesc& d, const WarpInT<LW>
   __syncwarp();
   if (lane == 0) {
     if (bf) mbar_arrive(smem_addr(&g_full[tf % R.stages]), bf);
-    if (bl) mbar_arrive(smem_addr(&g_full[tl % R.stages]), bl);
+    if (bl) mbar_arrive(smem_addr(&g_full[(tf + 1) % R.stages]), bl);
   }
 }
 
