@@ -722,6 +722,7 @@ int ecf8_fused_gemm(const ecf8_fused* f, const uint8_t* d_x, uint32_t m, float s
     a.k = static_cast<std::uint32_t>(f->k);
     a.split_k = f->split_k;
     a.stages_a = ecf8::dev::fused_stages_a(a.m_pad);
+    a.stages_b = ecf8::dev::fused_stages_b(a.m_pad);
     if (a.stages_a < 2) return fail(ECF8_EINVAL, "fused GEMM: shared memory too small for this m");
     a.acc_cols = 32;
     while (a.acc_cols < a.m_pad) a.acc_cols <<= 1;

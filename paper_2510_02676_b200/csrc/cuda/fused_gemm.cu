@@ -26,7 +26,8 @@
 //       warp arrives on the stage's "full" mbarrier with the number of bytes
 //       it wrote (a stage completes at 16384 bytes).
 //   control warp   allocates TMEM, streams X K-tiles (pre-swizzled by
-//       x_tiles_kernel) into a 2-stage B ring by bulk async copy, and one lane
+//       x_tiles_kernel) into a B ring (2 stages; 1 when m > 128 so the A ring
+//       keeps 5 stages) by bulk async copy, and one lane
 //       issues
 //       tcgen05.mma.cta_group::1.kind::f8f6f4 (M = 128 W rows, N = padded
 //       token count, K = 32 per instruction, 4 per K tile) with the fp32
@@ -261,7 +262,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) fused_gemm_kernel(const FusedArg
   const std::uint32_t b_base = a_base + args.stages_a * kTileElems;
   const std::uint32_t b_bytes = args.m_pad * 128u;
   std::uint32_t* const slots =
-      reinterpret_cast<std::uint32_t*>(smem_raw + (b_base + 2 * b_bytes - raw));
+      reinterpret_cast<std::uint32_t*>(smem_raw + (b_base + args.stages_b * b_bytes - raw));
 
   TensorDesc d = args.w;
   d.blk_begin = cta.blk_begin;
@@ -330,7 +331,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) fused_gemm_kernel(const FusedArg
     // X K-tiles arrive by bulk async copy (TMA engine) from the pre-swizzled
     // xt (x_tiles_kernel): one contiguous m_pad x 128-byte image per K tile
     auto issue_x = [&](std::uint32_t t) {
-      const std::uint32_t bsl = t & 1;
+      const std::uint32_t bsl = t % args.stages_b;
       const std::uint32_t kt = (cta.tile0 + t) % KT;
       const std::uint32_t bar = smem_addr(&g_bfull[bsl]);
       asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(bar),
@@ -343,15 +344,16 @@ __global__ void __launch_bounds__(kThreadsF, 1) fused_gemm_kernel(const FusedArg
     };
     if (lane == 0 && n_kt) issue_x(0);
     for (std::uint32_t t = 0; t < n_kt; ++t) {
-      const std::uint32_t bs = t & 1;
+      const std::uint32_t bs = t % args.stages_b;
       const std::uint32_t bdst = b_base + bs * b_bytes;
       const std::uint32_t g = cta.tile0 + t;
       const std::uint32_t seg = g / KT - nt0;
       const bool first_of_seg = t == 0 || g % KT == 0;
-      // next K tile's X into the other stage (its previous reader, the MMAs
-      // of tile t-1, completed: waited on below at the end of iteration t-1)
-      if (lane == 0 && t + 1 < n_kt) issue_x(t + 1);
-      mbar_wait(smem_addr(&g_bfull[bs]), (t >> 1) & 1u);
+      // two B stages: next K tile's X into the other stage now (its previous
+      // reader, the MMAs of tile t-1, completed: waited on at the end of
+      // iteration t-1); one stage (m_pad > 128): after this tile's MMAs
+      if (lane == 0 && args.stages_b == 2 && t + 1 < n_kt) issue_x(t + 1);
+      mbar_wait(smem_addr(&g_bfull[bs]), (t / args.stages_b) & 1u);
       const std::uint32_t s = t % args.stages_a;
       mbar_wait(smem_addr(&g_full[s]), (t / args.stages_a) & 1u);
       tc_fence_after();
@@ -367,6 +369,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) fused_gemm_kernel(const FusedArg
         mbar_wait(smem_addr(&g_empty[s]), (t / args.stages_a) & 1u);
         asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_addr(&g_consumed)), "r"(t + 1)
                      : "memory");
+        if (args.stages_b == 1 && t + 1 < n_kt) issue_x(t + 1);
       }
       __syncwarp();
     }
@@ -422,17 +425,19 @@ __global__ void x_tiles_kernel(const std::uint8_t* __restrict__ x, std::uint8_t*
 
 }  // namespace
 
+std::uint32_t fused_stages_b(std::uint32_t m_pad) { return m_pad > 128 ? 1u : 2u; }
+
 std::uint32_t fused_stages_a(std::uint32_t m_pad) {
   // 227 KB per CTA: tables 28.6 KB static, slots 20 x 32 x 33 x 4 B,
   // B ring 2 x m_pad x 128 B, A ring stages x 16 KB, 1 KB alignment slack
   const std::uint32_t budget = 232448 - 30 * 1024;
-  const std::uint32_t fixed = kDecodeWarps * 32 * kSlotStride * 4 + 2 * m_pad * 128 + 1024;
+  const std::uint32_t fixed = kDecodeWarps * 32 * kSlotStride * 4 + fused_stages_b(m_pad) * m_pad * 128 + 1024;
   const std::uint32_t s = fixed < budget ? (budget - fixed) / kTileElems : 0;
   return s > kMaxStagesA ? kMaxStagesA : s;
 }
 
 std::uint32_t fused_smem_bytes(std::uint32_t m_pad, std::uint32_t stages_a) {
-  return 1024 + stages_a * kTileElems + 2 * m_pad * 128 + kDecodeWarps * 32 * kSlotStride * 4;
+  return 1024 + stages_a * kTileElems + fused_stages_b(m_pad) * m_pad * 128 + kDecodeWarps * 32 * kSlotStride * 4;
 }
 
 template <int LW>
