@@ -73,7 +73,11 @@ WORKLOADS = {
                                 desc="deepseek-v3 routed-expert fp8 weights, EP (expert e on rank e mod world), "
                                      "one batched launch per MoE layer"),
     "dit-e5m2": dict(layers=1, distinct=1, desc="FLUX/Wan DiT-shaped E5M2 tensors, size sweep"),
+    "llama3-70b-fused": dict(layers=1, distinct=1,
+                             desc="llama3-70b fp8 linears (one layer), decode-fused tcgen05 FP8 GEMM, "
+                                  "column TP over the ranks + NCCL all-gather"),
 }
+FUSED_MS = [1, 16, 64, 256]
 
 
 def log(*a):
@@ -368,6 +372,113 @@ def run_dit_sweep(args, torch, dist, local, world):
     return sweep, total_launches
 
 
+# ------------------------------------------------------------------ fused GEMM
+
+
+def run_fused(args, torch, dist, local, rank, world):
+    """Config 3: one Llama-3-70B layer's 7 linears through the decode-fused
+    GEMM, W column-sharded over the ranks (each shard its own ECF8 stream),
+    y all-gathered (NCCL) -- tokens/s per batch size M.  Comparators on the
+    same shards: decode into HBM + cuBLASLt FP8 GEMM, and the plain FP8 GEMM
+    on uncompressed weights."""
+    from paper_2510_02676_b200 import codec
+    from paper_2510_02676_b200.device import Batch, DeviceTensor
+    from paper_2510_02676_b200.tp import TPFusedLinear, gather_columns
+
+    t0 = time.time()
+    lins, plains, decs = [], [], []
+    for j, (name, n, k) in enumerate(LLAMA70B):
+        w = codec.synth(ALPHA, GAMMA, n * k, 1000 * 0 + j).reshape(n, k)
+        tp = TPFusedLinear(w, rank, world)
+        lo, hi = tp.rows
+        shard = np.ascontiguousarray(w[lo:hi])
+        lins.append(tp)
+        plains.append(torch.from_numpy(shard).cuda().view(torch.float8_e4m3fn))
+        enc = codec.encode_tensor(shard.reshape(-1), T_BLOCK)
+        dt = DeviceTensor(enc)
+        buf = torch.empty(shard.size, dtype=torch.uint8, device="cuda")
+        decs.append((dt, buf, Batch([dt], [buf]), hi - lo, k))
+    log(f"[bench] rank {rank}: fused layer prepared in {time.time() - t0:.1f}s")
+    comp = sum(l.local.compressed_bytes for l in lins)
+    flops_per_token = 2 * sum((l.rows[1] - l.rows[0]) * l.k for l in lins)
+    one = torch.tensor(1.0, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def timed(fn):
+        for _ in range(args.warmup):
+            fn()
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.steps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / args.steps
+        if dist:
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    sweep, launches = [], 0
+    peak, _ = load_peaks()
+    fp8_peak = 2 * float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"]) \
+        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 4500.0
+    with ClockProbe(local) as probe:
+        for m in FUSED_MS:
+            xs = [(torch.randn(m, l.k, device="cuda") * 4).to(torch.float8_e4m3fn) for l in lins]
+            mp_ = max(16, (m + 15) // 16 * 16)
+            xps = [torch.cat([x, x.new_zeros(mp_ - m, x.shape[1])]) if mp_ != m else x for x in xs]
+            outs = [torch.empty(m, l.rows[1] - l.rows[0], device="cuda") for l in lins]
+
+            def fused_layer():
+                for l, x, o in zip(lins, xs, outs):
+                    gather_columns(l.local(x, 1.0, o), world)
+
+            def decode_gemm_layer():
+                for (dt, buf, bt, nn, kk), xp in zip(decs, xps):
+                    bt.decode(stream)
+                    y = torch._scaled_mm(xp, buf.view(torch.float8_e4m3fn).view(nn, kk).t(), scale_a=one, scale_b=one,
+                                         out_dtype=torch.float32)
+                    gather_columns(y[:m], world)
+
+            def plain_layer():
+                for wpl, xp in zip(plains, xps):
+                    y = torch._scaled_mm(xp, wpl.t(), scale_a=one, scale_b=one, out_dtype=torch.float32)
+                    gather_columns(y[:m], world)
+
+            tf = timed(fused_layer)
+            td = timed(decode_gemm_layer)
+            tpl = timed(plain_layer)
+            launches += args.steps * len(lins) * 2  # x tiles + fused GEMM per linear
+            sweep.append({"m": m, "fused_ms": round(tf, 4), "tokens_per_s": round(m / (tf * 1e-3), 1),
+                          "decode_then_gemm_ms": round(td, 4), "plain_fp8_gemm_ms": round(tpl, 4),
+                          "compressed_gbs": round(world * comp / (tf * 1e-3) / 1e9, 1),
+                          "tensor_tflops": round(world * flops_per_token * m / (tf * 1e-3) / 1e12, 2)})
+            log(f"[bench] fused m={m}: {tf:.3f} ms/layer ({m / tf * 1e3:.0f} tok/s), decode+gemm {td:.3f}, plain {tpl:.3f}")
+    if rank == 0:
+        top = sweep[-1]
+        line = base_line(args, world, top["tokens_per_s"], top["fused_ms"], {
+            "workload": WORKLOADS["llama3-70b-fused"]["desc"], "batch_sizes": FUSED_MS,
+            "parallelism": f"tp{world} (column shards, each ECF8-encoded; NCCL all-gather of y)",
+            "threads_per_block": 128, "compressed_bytes_per_layer": int(world * comp)})
+        line["metric"] = "ECF8 decode-fused FP8 GEMM tokens/s (one Llama-3-70B layer, 7 linears)"
+        line["unit"] = "tokens/s"
+        line["dtype"] = "fp8-e4m3 x fp8-e4m3 -> fp32"
+        line["scaling"] = "strong"
+        line["sweep"] = sweep
+        line["roofline"] = {"bound": "hbm", "achieved": top["compressed_gbs"] / world, "peak": peak, "unit": "GB/s",
+                            "frac": round(top["compressed_gbs"] / world / peak, 4), "traffic": None,
+                            "tensor_tflops": top["tensor_tflops"] / world, "tensor_peak_tflops": fp8_peak,
+                            "kernel": "fused_gemm_kernel<8>"}
+        line["clocks"] = probe.summary()
+        line["gpu_launches"] = launches
+        print(json.dumps(line), flush=True)
+
+
 # ------------------------------------------------------------------ main
 
 
@@ -415,6 +526,12 @@ def main():
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     peak, peak_kind = load_peaks()
+
+    if args.workload == "llama3-70b-fused":
+        run_fused(args, torch, dist, local, rank, world)
+        if dist:
+            dist.destroy_process_group()
+        return
 
     if args.workload == "dit-e5m2":
         sweep, launches = run_dit_sweep(args, torch, dist, local, world)
