@@ -34,7 +34,11 @@ def test_ecf8_linear_matches_fp8_gemm_on_reference_decoded_weights(orc, fmt, m):
     wt = torch.from_numpy(wd).cuda().view(_FP8[fmt])
     want = torch._scaled_mm(xq, wt.t(), scale_a=sx, scale_b=torch.tensor(0.5, device="cuda"),
                             out_dtype=torch.bfloat16)[:m]
-    assert torch.equal(y, want)
+    # the arena holds exactly the reference-decoded bytes ...
+    assert np.array_equal(lin.decode_weight().view(torch.uint8).cpu().numpy(), wd)
+    # ... and the GEMM on them matches cuBLASLt on the reference bytes (cuBLASLt
+    # may pick a different split per call: equal up to bf16 rounding)
+    torch.testing.assert_close(y.float(), want.float(), rtol=1e-2, atol=1e-2 * want.abs().max().item())
     # and against an fp32 dequantised reference within FP8-GEMM tolerance
     ref = (xq[:m].float() * sx) @ (wt.float() * 0.5).t()
     torch.testing.assert_close(y.float(), ref, rtol=2e-2, atol=2e-2 * ref.abs().max().item())
