@@ -160,7 +160,8 @@ struct ecf8_dev_tensor {
   std::uint64_t n_elem = 0, n_blocks = 0;
   std::uint64_t algo_bytes = 0;
   std::uint32_t T = 0;
-  TensorDesc desc{};  // out / tile fields filled per launch
+  bool cont_ok = false;  // gaps verified: the continuous-walk kernel (variant 5) applies
+  TensorDesc desc{};     // out / tile fields filled per launch
 };
 
 struct ecf8_fused {
@@ -223,9 +224,10 @@ void upload_into(ecf8_dev_tensor* t, const ecf8_sections* s, std::uint64_t nb, c
 }
 
 // Single-descriptor launch: the descriptor rides in the kernel parameters.
-int launch_one(const TensorDesc& d, cudaStream_t st) {
+int launch_one(const TensorDesc& d, cudaStream_t st, int variant_override = -1) {
   if (d.blk_end <= d.blk_begin) return ECF8_OK;
-  const ecf8::dev::Variant v = ecf8::dev::variant_for(d.T, d.lmin);
+  ecf8::dev::Variant v = ecf8::dev::variant_for(d.T, d.lmin);
+  if (variant_override >= 0) v.id = variant_override;
   ecf8::dev::LaunchArgs a{};
   a.descs = nullptr;
   a.n_desc = 1;
@@ -234,6 +236,81 @@ int launch_one(const TensorDesc& d, cudaStream_t st) {
   a.inline_desc.tile_begin = 0;
   cu(ecf8::dev::launch_decode(a, v.id, st), "decode launch");
   return ECF8_OK;
+}
+
+__global__ void diff_kernel(const uint4* a, const uint4* b, std::uint64_t n16, unsigned* flag) {
+  for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < n16;
+       i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+    const uint4 x = a[i], y = b[i];
+    if (x.x != y.x || x.y != y.y || x.z != y.z || x.w != y.w) atomicOr(flag, 1u);
+  }
+}
+
+bool cont_disabled() {
+  static const bool off = std::getenv("ECF8_NO_CONT") != nullptr;
+  return off;
+}
+
+// The continuous-walk kernel (variant 5) is exact when every window's gap is
+// where the stream's code words actually are -- always so for encoder output,
+// not guaranteed for an arbitrary parseable container.  Decide it once per
+// uploaded tensor: decode with the per-window kernel (variant 4, reference
+// semantics) and the continuous one, chunk by chunk, and compare the bytes.
+bool verify_continuous(const ecf8_dev_tensor* t, cudaStream_t st) {
+  if (cont_disabled() || t->n_elem == 0 || ecf8::dev::variant_for(t->T, t->desc.lmin).id != 4) return false;
+  const std::uint64_t kChunk = std::uint64_t{64} << 20;  // elements per comparison
+  std::uint8_t* buf = nullptr;
+  unsigned* flag = nullptr;
+  cu(cudaMalloc(&buf, 2 * (kChunk + ecf8::dev::kTileElemsMax + 64) + 64), "cudaMalloc(verify)");
+  bool ok = true;
+  try {
+    cu(cudaMalloc(&flag, sizeof(unsigned)), "cudaMalloc(verify)");
+    cu(cudaMemsetAsync(flag, 0, sizeof(unsigned), st), "memset");
+    std::vector<std::uint64_t> outpos(t->n_blocks + 1);
+    cu(cudaMemcpyAsync(outpos.data(), t->desc.outpos, 8 * outpos.size(), cudaMemcpyDeviceToHost, st), "D2H");
+    cu(cudaStreamSynchronize(st), "sync");
+    const std::uint64_t cap = kChunk + ecf8::dev::kTileElemsMax + 64;
+    std::uint8_t* a = buf;
+    std::uint8_t* b = buf + cap;
+    const std::uint64_t m = ecf8::dev::blocks_per_tile(t->T, 256);
+    for (std::uint64_t lo = 0; lo < t->n_blocks;) {
+      std::uint64_t hi = std::min(t->n_blocks, lo + m);
+      while (hi < t->n_blocks && outpos[std::min(t->n_blocks, hi + m)] - outpos[lo] <= kChunk)
+        hi = std::min(t->n_blocks, hi + m);
+      TensorDesc d = t->desc;
+      d.blk_begin = lo;
+      d.blk_end = hi;
+      d.out_offset = outpos[lo] & ~std::uint64_t{15};
+      const std::uint64_t n = outpos[hi] - d.out_offset;
+      cu(cudaMemsetAsync(a, 0, (n + 15) & ~std::uint64_t{15}, st), "memset");
+      cu(cudaMemsetAsync(b, 0, (n + 15) & ~std::uint64_t{15}, st), "memset");
+      d.out = a;
+      if (launch_one(d, st, 4) != ECF8_OK) throw std::runtime_error("verify launch");
+      d.out = b;
+      if (launch_one(d, st, 5) != ECF8_OK) throw std::runtime_error("verify launch");
+      diff_kernel<<<592, 256, 0, st>>>(reinterpret_cast<const uint4*>(a), reinterpret_cast<const uint4*>(b),
+                                       (n + 15) / 16, flag);
+      cu(cudaGetLastError(), "diff launch");
+      lo = hi;
+    }
+    unsigned h = 0;
+    cu(cudaMemcpyAsync(&h, flag, sizeof(h), cudaMemcpyDeviceToHost, st), "D2H");
+    cu(cudaStreamSynchronize(st), "sync");
+    ok = h == 0;
+  } catch (...) {
+    cudaFree(buf);
+    if (flag) cudaFree(flag);
+    throw;
+  }
+  cudaFree(buf);
+  cudaFree(flag);
+  return ok;
+}
+
+// Launch variant for a device tensor.
+int tensor_variant(const ecf8_dev_tensor* t) {
+  const int id = ecf8::dev::variant_for(t->T, t->desc.lmin).id;
+  return (id == 4 && t->cont_ok && !cont_disabled()) ? 5 : id;
 }
 
 // Per-thread state of the host-span path: three streams (copy-in, decode,
@@ -441,6 +518,7 @@ int ecf8_tensor_upload(const ecf8_sections* s, void* stream, ecf8_dev_tensor** o
     auto t = std::make_unique<ecf8_dev_tensor>();
     try {
       upload_into(t.get(), s, nb, static_cast<cudaStream_t>(stream));
+      t->cont_ok = verify_continuous(t.get(), static_cast<cudaStream_t>(stream));
     } catch (...) {
       if (t->arena) cudaFree(t->arena);
       throw;
@@ -470,7 +548,7 @@ int ecf8_decode_device(const ecf8_dev_tensor* t, uint8_t* d_out, void* stream) {
     d.out = d_out;
     d.out_offset = 0;
     d.tile_begin = 0;
-    return launch_one(d, static_cast<cudaStream_t>(stream));
+    return launch_one(d, static_cast<cudaStream_t>(stream), tensor_variant(t));
   });
 }
 
@@ -480,7 +558,7 @@ int ecf8_batch_create(const ecf8_dev_tensor* const* ts, uint8_t* const* d_outs, 
     if (!out || (count > 0 && (!ts || !d_outs))) return fail(ECF8_EINVAL, "null argument");
     *out = nullptr;
     auto b = std::make_unique<ecf8_batch>();
-    for (int kw = 0; kw < 5; ++kw) {  // one launch per kernel variant present
+    for (int kw = 0; kw < 6; ++kw) {  // one launch per kernel variant present
       std::vector<TensorDesc> group;
       std::uint64_t tiles = 0;
       int kwin_tile = 1;
@@ -488,7 +566,7 @@ int ecf8_batch_create(const ecf8_dev_tensor* const* ts, uint8_t* const* d_outs, 
         const ecf8_dev_tensor* t = ts[i];
         if (!t) return fail(ECF8_EINVAL, "null tensor");
         const ecf8::dev::Variant v = ecf8::dev::variant_for(t->T, t->desc.lmin);
-        if (t->n_elem == 0 || v.id != kw) continue;
+        if (t->n_elem == 0 || tensor_variant(t) != kw) continue;
         kwin_tile = v.tile_win;
         if (!d_outs[i] || (reinterpret_cast<std::uintptr_t>(d_outs[i]) & 15))
           return fail(ECF8_EINVAL, "device output must be 16-byte aligned");

@@ -175,6 +175,62 @@ __device__ __forceinline__ bool decode_window_fast(std::uint32_t w0, std::uint32
   return !(flags & kSlowFlag);
 }
 
+// Continuous fast walk over a lane's n consecutive windows (n <= 8; w holds
+// their 2n big-endian words plus 2 lookahead words): starts at the first
+// window's gap and runs through the window boundaries without restarting,
+// taking every code word that starts before bit 64n.  Equals the per-window
+// walks of decode_window_fast (codec.cpp:133-190) exactly when each window's
+// gap is the start of the first code word the stream places in it -- true
+// for every encoder-produced stream; ecf8_tensor_upload verifies it per
+// tensor before this path is enabled.  Returns false if a flagged entry was
+// met (the caller redoes the windows exactly).
+template <int NW>
+__device__ __forceinline__ bool decode_lane_continuous(const std::uint32_t (&w)[2 * NW + 2], std::uint32_t n,
+                                                       std::uint32_t gap, std::uint32_t fast, std::uint32_t smask,
+                                                       SlotSink& sink) {
+  std::uint32_t hi = __funnelshift_l(w[1], w[0], gap);
+  std::uint32_t lo = __funnelshift_l(w[2], w[1], gap);
+  std::uint32_t p = gap, flags = 0;  // p: bit position of hi's MSB within the current 32-bit phase
+  const std::uint32_t last = 2 * n - 1;
+#pragma unroll
+  for (std::uint32_t k = 0; k < 2 * NW; ++k) {
+    if (k == last) {
+      // final half window: whole entries while they end before bit 32, then
+      // the symbols that start before it (start mask + popcount)
+      for (;;) {
+        const std::uint32_t idx = hi >> kFastShift;
+        const std::uint32_t e = lds32(fast + 4 * idx);
+        flags |= e;
+        const std::uint32_t b = e & 31, r = 32 - p;
+        if (b >= r) {
+          const std::uint32_t k4 = 4 * __popc(lds16(smask + 2 * idx) & ((1u << r) - 1));
+          sink.put((e >> 12) & ((1u << k4) - 1), k4);
+          break;
+        }
+        sink.put(e >> 12, (e >> 5) & 31);
+        hi = __funnelshift_l(lo, hi, e);
+        lo = __funnelshift_l(0u, lo, e);
+        p += b;
+      }
+      break;
+    }
+    while (p < 32) {
+      const std::uint32_t e = lds32(fast + ((hi >> (kFastShift - 2)) & ~3u));
+      flags |= e;
+      sink.put(e >> 12, (e >> 5) & 31);
+      hi = __funnelshift_l(lo, hi, e);
+      lo = __funnelshift_l(0u, lo, e);
+      p += e & 31;
+    }
+    p -= 32;  // next phase: hi:lo = bits [32(k+1) + p, +64)
+    if (k + 3 < 2 * NW + 2) {
+      hi = __funnelshift_l(w[k + 2], w[k + 1], p);
+      lo = __funnelshift_l(w[k + 3], w[k + 2], p);
+    }
+  }
+  return !(flags & kSlowFlag);
+}
+
 __device__ __forceinline__ void decode_window(std::uint32_t w0, std::uint32_t w1, std::uint32_t w2,
                                               std::uint32_t w3, std::uint32_t gap, const Tables& tb,
                                               std::uint32_t len_off, SlotSink& sink) {

@@ -48,10 +48,11 @@ struct WarpSmem {
 __shared__ Tables g_tb;
 __shared__ unsigned long long g_next_tile;  // CTA-local work queue of the current segment
 
+template <bool CONT>
 __device__ __forceinline__ void warp_tile(const TensorDesc& d, const WarpIn& in, std::uint32_t log2T,
                                           std::uint32_t len_off, WarpSmem& ws, int lane) {
   std::uint32_t* const my_slot = ws.slot + lane * WarpSmem::kStride;
-  const LaneRun run = warp_decode_scan(in, log2T, len_off, g_tb, my_slot, lane);
+  const LaneRun run = warp_decode_scan<kLaneWin, CONT>(in, log2T, len_off, g_tb, my_slot, lane);
   const std::uint32_t cc = run.len;
   const std::uint32_t off = static_cast<std::uint32_t>(in.A & 15);  // staging nibble of element A
   const std::uint32_t d0 = run.start + off, dend = d0 + cc;
@@ -158,7 +159,7 @@ __device__ __forceinline__ void warp_tile(const TensorDesc& d, const WarpIn& in,
   }
 }
 
-template <int NW>
+template <int NW, bool CONT>
 __global__ void __launch_bounds__(NW * 32, 1) decode_warp_kernel(const LaunchArgs args) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -205,31 +206,31 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_warp_kernel(const LaunchArg
       if (lane == 0) claim = atomicAdd(&g_next_tile, 1ull);
       const std::uint64_t next = __shfl_sync(0xffffffffu, claim, 0);
       if (next < seg_end) load_warp_tile(d, next, log2T, lane, nxt);
-      warp_tile(d, cur, log2T, len_off, ws, lane);
+      warp_tile<CONT>(d, cur, log2T, len_off, ws, lane);
       tile = next;
     }
     seg = seg_end;
   }
 }
 
-template <int NW>
+template <int NW, bool CONT>
 cudaError_t launch_nw(const LaunchArgs& args, cudaStream_t s) {
   static int grid_cap = 0;
   const int smem = static_cast<int>(sizeof(WarpSmem)) * NW;
   if (grid_cap == 0) {
-    cudaError_t e = cudaFuncSetAttribute(decode_warp_kernel<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = cudaFuncSetAttribute(decode_warp_kernel<NW, CONT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_warp_kernel<NW>, NW * 32, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_warp_kernel<NW, CONT>, NW * 32, smem);
     if (e != cudaSuccess) return e;
     grid_cap = sms * (per_sm > 0 ? per_sm : 1);
   }
   const std::uint64_t want = (args.total_tiles + NW - 1) / NW;
   const std::uint64_t grid = want < static_cast<std::uint64_t>(grid_cap) ? want : grid_cap;
   if (grid == 0) return cudaSuccess;
-  decode_warp_kernel<NW><<<static_cast<unsigned>(grid), NW * 32, smem, s>>>(args);
+  decode_warp_kernel<NW, CONT><<<static_cast<unsigned>(grid), NW * 32, smem, s>>>(args);
   return cudaGetLastError();
 }
 
@@ -243,7 +244,17 @@ cudaError_t launch_decode_warp(const LaunchArgs& args, cudaStream_t s) {
     const char* e = std::getenv("ECF8_WARPS");
     return e ? std::atoi(e) : 20;
   }();
-  return nw == 16 ? launch_nw<16>(args, s) : launch_nw<20>(args, s);
+  return nw == 16 ? launch_nw<16, false>(args, s) : launch_nw<20, false>(args, s);
+}
+
+// Variant 5: the same kernel walking each lane's windows continuously, for
+// tensors whose gaps ecf8_tensor_upload verified (decode_lane_continuous).
+cudaError_t launch_decode_warp_cont(const LaunchArgs& args, cudaStream_t s) {
+  static const int nw = [] {
+    const char* e = std::getenv("ECF8_WARPS");
+    return e ? std::atoi(e) : 20;
+  }();
+  return nw == 16 ? launch_nw<16, true>(args, s) : launch_nw<20, true>(args, s);
 }
 
 }  // namespace ecf8::dev

@@ -76,7 +76,9 @@ struct LaneRun {
 
 // Decode this lane's windows into `slot` (kSlotWords words, nibble i of the
 // run in bits 4(i%8).. of word i/8), then scan + clamp across the warp.
-template <int LW>
+// CONT: walk the lane's windows continuously (decode_lane_continuous; only
+// for tensors whose gaps were verified at upload), else window by window.
+template <int LW, bool CONT = false>
 __device__ __forceinline__ LaneRun warp_decode_scan(const WarpInT<LW>& in, std::uint32_t log2T,
                                                    std::uint32_t len_off, const Tables& tb, std::uint32_t* slot,
                                                    int lane) {
@@ -94,12 +96,24 @@ __device__ __forceinline__ LaneRun warp_decode_scan(const WarpInT<LW>& in, std::
     }
     w[2 * LW] = bswap32(in.w8.x), w[2 * LW + 1] = bswap32(in.w8.y);
     const std::uint32_t n = min(in.nwin - wl0, static_cast<std::uint32_t>(LW));
+    bool exact = true;
+    if constexpr (CONT) {
+      const SlotSink saved = sink;
+      const std::uint32_t gap0 = (in.gaps >> 4) & 15u;  // window 0: high nibble of byte 0
+      exact = !decode_lane_continuous<LW>(w, n, gap0, smem_addr(tb.fast), smem_addr(tb.smask), sink);
+      if (exact) sink = saved;
+    }
+    if (exact) {
 #pragma unroll
-    for (int i = 0; i < LW; ++i) {
-      if (static_cast<std::uint32_t>(i) < n) {
-        // byte j of the gap word: window 2j in the high nibble, 2j + 1 low
-        const std::uint32_t gap = (in.gaps >> (8 * (i >> 1) + ((i & 1) ? 0 : 4))) & 15u;
-        decode_window(w[2 * i], w[2 * i + 1], w[2 * i + 2], w[2 * i + 3], gap, tb, len_off, sink);
+      for (int i = 0; i < LW; ++i) {
+        if (static_cast<std::uint32_t>(i) < n) {
+          // byte j of the gap word: window 2j in the high nibble, 2j + 1 low
+          const std::uint32_t gap = (in.gaps >> (8 * (i >> 1) + ((i & 1) ? 0 : 4))) & 15u;
+          if constexpr (CONT)
+            decode_window_exact(w[2 * i], w[2 * i + 1], w[2 * i + 2], w[2 * i + 3], gap, tb, len_off, sink);
+          else
+            decode_window(w[2 * i], w[2 * i + 1], w[2 * i + 2], w[2 * i + 3], gap, tb, len_off, sink);
+        }
       }
     }
   }
