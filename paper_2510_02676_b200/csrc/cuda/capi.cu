@@ -535,6 +535,7 @@ void ecf8_tensor_free(ecf8_dev_tensor* t) {
 }
 
 uint64_t ecf8_tensor_n_elem(const ecf8_dev_tensor* t) { return t ? t->n_elem : 0; }
+int ecf8_tensor_kernel_variant(const ecf8_dev_tensor* t) { return t && t->n_elem ? tensor_variant(t) : -1; }
 uint64_t ecf8_tensor_algorithmic_bytes(const ecf8_dev_tensor* t) { return t ? t->algo_bytes : 0; }
 uint64_t ecf8_tensor_device_bytes(const ecf8_dev_tensor* t) { return t ? t->arena_bytes : 0; }
 

@@ -31,6 +31,7 @@ class DeviceTensor:
         self.handle = h
         self.algorithmic_bytes = int(lib.ecf8_tensor_algorithmic_bytes(h))
         self.device_bytes = int(lib.ecf8_tensor_device_bytes(h))
+        self.kernel_variant = int(lib.ecf8_tensor_kernel_variant(h))
 
     def decode_into(self, out: torch.Tensor, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
         if out.dtype not in (torch.uint8, torch.float8_e4m3fn, torch.float8_e5m2) or not out.is_cuda:

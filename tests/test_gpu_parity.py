@@ -179,3 +179,51 @@ def test_decode_many_validates_each_tensor():
     t = codec.encode_tensor(codec.synth(1.8, 0.05, 1000, 1), 256)
     with pytest.raises(InvalidArgument, match="output size mismatch"):
         codec.decode_many_into([t, t], [np.empty(1000, np.uint8), np.empty(999, np.uint8)])
+
+
+@pytest.mark.parametrize("n,T,seed", [(5_000_000, 256, 1), (777_777, 64, 2), (123_457, 8, 3), (3_000_001, 128, 4)])
+def test_device_path_continuous_variant(orc, n, T, seed):
+    # encoder output: the upload check enables the continuous-walk kernel
+    import torch
+
+    from paper_2510_02676_b200.device import DeviceTensor
+
+    x = codec.synth(1.8, 0.05, n, seed)
+    t = codec.encode_tensor(x, T)
+    d = DeviceTensor(t)
+    assert d.kernel_variant == 5
+    got = d.decode().cpu().numpy()
+    torch.cuda.synchronize()
+    assert np.array_equal(got, x)
+
+
+def test_inconsistent_gaps_fall_back_to_reference_semantics(orc):
+    # a parseable stream whose gap nibbles disagree with the code words: the
+    # reference still decodes it window by window (codec.cpp:201-253); the
+    # device path must detect it at upload and produce the same bytes.  Where
+    # a corrupted block's windows count fewer symbols than outpos says, the
+    # reference leaves that tail of the block to stale scratch contents
+    # (codec.cpp:253 copies the whole staging range) -- undefined, so only
+    # blocks whose counts cover them are compared.
+    from paper_2510_02676_b200.device import DeviceTensor
+
+    x = codec.synth(1.8, 0.05, 400_000, 9)
+    t = codec.encode_tensor(x, 256).copy()
+    g = np.asarray(t.gaps)
+    for j in (37, 1000, 5001):  # windows 2j (high nibble) get a shifted gap
+        g[j] = ((((g[j] >> 4) + 3) & 15) << 4) | (g[j] & 15)
+    d = tensor_dict(t)
+    want = orc.decode_parallel(d)  # the reference's parallel decoder on these gaps
+    assert not np.array_equal(want, x)
+    T, enc, op = 256, np.asarray(t.encoded), np.asarray(t.outpos)
+    defined = np.ones(t.n_elem, bool)
+    for b in range(len(op) - 1):
+        cnt = sum(orc.count_phase(enc[8 * w:8 * w + 10], t.gap_at(w), d["lengths"]) for w in range(b * T, (b + 1) * T))
+        if cnt < op[b + 1] - op[b]:
+            defined[op[b]:op[b + 1]] = False
+    dev = DeviceTensor(t)
+    assert dev.kernel_variant == 4  # the upload check rejected the continuous walk
+    got = dev.decode().cpu().numpy()
+    assert defined.sum() > 0.9 * t.n_elem
+    assert np.array_equal(got[defined], want[defined])
+    assert np.array_equal(codec.decode_parallel(t)[defined], want[defined])

@@ -38,10 +38,13 @@ def test_ecf8_linear_matches_fp8_gemm_on_reference_decoded_weights(orc, fmt, m):
     assert np.array_equal(lin.decode_weight().view(torch.uint8).cpu().numpy(), wd)
     # ... and the GEMM on them matches cuBLASLt on the reference bytes (cuBLASLt
     # may pick a different split per call: equal up to bf16 rounding)
-    torch.testing.assert_close(y.float(), want.float(), rtol=1e-2, atol=1e-2 * want.abs().max().item())
+    wf = want.float()
+    scale = wf[wf.isfinite()].abs().max().item()
+    torch.testing.assert_close(y.float(), wf, rtol=1e-2, atol=1e-2 * scale, equal_nan=True)
     # and against an fp32 dequantised reference within FP8-GEMM tolerance
     ref = (xq[:m].float() * sx) @ (wt.float() * 0.5).t()
-    torch.testing.assert_close(y.float(), ref, rtol=2e-2, atol=2e-2 * ref.abs().max().item())
+    fin = ref.isfinite()
+    torch.testing.assert_close(y.float()[fin], ref[fin], rtol=2e-2, atol=2e-2 * ref[fin].abs().max().item())
 
 
 def test_compress_linears_shares_one_arena():
