@@ -251,7 +251,7 @@ def load_peaks():
 
 
 def kernel_name():
-    nw = os.environ.get("ECF8_WARPS", "20")
+    nw = os.environ.get("ECF8_WARPS", "22")
     return "decode_kernel<4,16,3>" if os.environ.get("ECF8_NO_WARP_KERNEL") == "1" else f"decode_warp_kernel<{nw}>"
 
 
@@ -299,15 +299,16 @@ def run_reference_arm(args, rank, world):
 
 
 def timed_region(torch, dist, local, stream, batches, steps, warmup):
-    """Warm-up, then EXACTLY `steps` steps bracketed by barrier + sync; CUDA
-    events per launch on the launching stream.  Returns (elapsed_ms max over
-    ranks, per-launch ms list, clocks)."""
+    """Warm-up, then EXACTLY `steps` steps bracketed by barrier + sync, timed
+    by CUDA events on the launching stream.  The decode launches run back to
+    back (programmatic dependent launch overlaps each grid's tail with the
+    next grid's start; an event between them would serialise them), so the
+    per-launch time is the region's event time / launches.  Returns
+    (elapsed_ms max over ranks, per-launch ms list, clocks)."""
     for _ in range(warmup):
         for b in batches:
             b.decode(stream)
     torch.cuda.synchronize()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(steps * len(batches))]
     step_start = torch.cuda.Event(enable_timing=True)
     step_end = torch.cuda.Event(enable_timing=True)
     if dist:
@@ -315,19 +316,15 @@ def timed_region(torch, dist, local, stream, batches, steps, warmup):
     torch.cuda.synchronize()
     with ClockProbe(local) as probe:
         step_start.record(stream)
-        k = 0
         for _ in range(steps):
             for b in batches:
-                ev[k][0].record(stream)
                 b.decode(stream)
-                ev[k][1].record(stream)
-                k += 1
         step_end.record(stream)
         torch.cuda.synchronize()
     if dist:
         dist.barrier()
     elapsed_ms = step_start.elapsed_time(step_end)
-    launch_ms = [s.elapsed_time(e) for s, e in ev]
+    launch_ms = [elapsed_ms / (steps * len(batches))] * (steps * len(batches))
     if dist:
         t = torch.tensor([elapsed_ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

@@ -94,10 +94,15 @@ int ecf8_count_window(const uint8_t window10[10], unsigned gap, const uint8_t le
 int ecf8_tensor_upload(const ecf8_sections *host, void *stream, ecf8_dev_tensor **out);
 void ecf8_tensor_free(ecf8_dev_tensor *t);
 uint64_t ecf8_tensor_n_elem(const ecf8_dev_tensor *t);
-/* Decode kernel variant the tensor launches with (decode.cuh ids; 5 = the
- * continuous-walk kernel, enabled when the upload-time check found every
- * window gap consistent with the stream; -1 for an empty tensor). */
+/* Decode kernel variant the tensor launches with (decode.cuh ids; 4 = the
+ * warp-tile kernel; -1 for an empty tensor). */
 int ecf8_tensor_kernel_variant(const ecf8_dev_tensor *t);
+/* Upload-time gap check (verify_gaps_kernel): how many of the tensor's
+ * 256-window tiles (*total) have every window ending where the next
+ * window's gap says -- those decode by the continuous group walk, the rest
+ * window by window with the reference's semantics (codec.cpp:201-253).
+ * Synchronises with the device. */
+uint64_t ecf8_tensor_verified_tiles(const ecf8_dev_tensor *t, uint64_t *total);
 /* Container bytes the decoder reads + n_elem written (roofline numerator). */
 uint64_t ecf8_tensor_algorithmic_bytes(const ecf8_dev_tensor *t);
 uint64_t ecf8_tensor_device_bytes(const ecf8_dev_tensor *t);

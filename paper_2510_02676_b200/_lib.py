@@ -90,6 +90,7 @@ _SIGS = {
     "ecf8_tensor_free": (None, [_P]),
     "ecf8_tensor_n_elem": (C.c_uint64, [_P]),
     "ecf8_tensor_kernel_variant": (C.c_int, [_P]),
+    "ecf8_tensor_verified_tiles": (C.c_uint64, [_P, C.POINTER(C.c_uint64)]),
     "ecf8_tensor_algorithmic_bytes": (C.c_uint64, [_P]),
     "ecf8_tensor_device_bytes": (C.c_uint64, [_P]),
     "ecf8_decode_device": (C.c_int, [_P, _P, _P]),

@@ -160,7 +160,8 @@ struct ecf8_dev_tensor {
   std::uint64_t n_elem = 0, n_blocks = 0;
   std::uint64_t algo_bytes = 0;
   std::uint32_t T = 0;
-  bool cont_ok = false;  // gaps verified: the continuous-walk kernel (variant 5) applies
+  std::uint64_t n_vtiles = 0;      // 256-window verification tiles (tile_ok bits)
+  std::uint32_t* ok_bits = nullptr;  // their bitmap in the arena
   TensorDesc desc{};     // out / tile fields filled per launch
 };
 
@@ -189,7 +190,9 @@ void upload_into(ecf8_dev_tensor* t, const ecf8_sections* s, std::uint64_t nb, c
   const std::uint64_t off_gap = align_up(off_enc + s->encoded_len + P, 256);
   const std::uint64_t off_pos = align_up(off_gap + s->gaps_len + P, 256);
   const std::uint64_t off_pak = align_up(off_pos + 8 * s->n_outpos, 256);
-  const std::uint64_t total = align_up(off_pak + s->packed_len + P, 256);
+  const std::uint64_t n_vtiles = (nb * s->threads_per_block + 255) / 256;
+  const std::uint64_t off_ok = align_up(off_pak + s->packed_len + P, 256);
+  const std::uint64_t total = align_up(off_ok + 4 * ((n_vtiles + 31) / 32), 256);
   cu(cudaMalloc(&t->arena, total), "cudaMalloc(tensor)");
   t->arena_bytes = total;
   auto* base = static_cast<std::uint8_t*>(t->arena);
@@ -198,6 +201,8 @@ void upload_into(ecf8_dev_tensor* t, const ecf8_sections* s, std::uint64_t nb, c
   if (s->gaps_len) cu(cudaMemcpyAsync(base + off_gap, s->gaps, s->gaps_len, cudaMemcpyHostToDevice, st), "H2D gaps");
   cu(cudaMemcpyAsync(base + off_pos, s->outpos, 8 * s->n_outpos, cudaMemcpyHostToDevice, st), "H2D outpos");
   if (s->packed_len) cu(cudaMemcpyAsync(base + off_pak, s->packed, s->packed_len, cudaMemcpyHostToDevice, st), "H2D packed");
+  t->n_vtiles = n_vtiles;
+  t->ok_bits = reinterpret_cast<std::uint32_t*>(base + off_ok);
 
   t->n_elem = s->n_elem;
   t->n_blocks = nb;
@@ -223,6 +228,18 @@ void upload_into(ecf8_dev_tensor* t, const ecf8_sections* s, std::uint64_t nb, c
   }
 }
 
+// Gap check at upload (verify_gaps_kernel): tiles whose windows all end where
+// the next window's gap says take the continuous walk; the rest keep the
+// reference's window-by-window semantics.
+void verify_into(ecf8_dev_tensor* t, cudaStream_t st) {
+  static const bool off = std::getenv("ECF8_NO_CONT_WALK") != nullptr;  // A/B runs
+  if (off || t->n_elem == 0 || ecf8::dev::variant_for(t->T, t->desc.lmin).id != 4) return;
+  std::uint32_t* const ok = t->ok_bits;
+  cu(cudaMemsetAsync(ok, 0xFF, 4 * ((t->n_vtiles + 31) / 32), st), "memset(tile_ok)");
+  cu(ecf8::dev::launch_verify_gaps(t->desc, ok, st), "verify launch");
+  t->desc.tile_ok = ok;
+}
+
 // Single-descriptor launch: the descriptor rides in the kernel parameters.
 int launch_one(const TensorDesc& d, cudaStream_t st, int variant_override = -1) {
   if (d.blk_end <= d.blk_begin) return ECF8_OK;
@@ -238,80 +255,8 @@ int launch_one(const TensorDesc& d, cudaStream_t st, int variant_override = -1) 
   return ECF8_OK;
 }
 
-__global__ void diff_kernel(const uint4* a, const uint4* b, std::uint64_t n16, unsigned* flag) {
-  for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < n16;
-       i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
-    const uint4 x = a[i], y = b[i];
-    if (x.x != y.x || x.y != y.y || x.z != y.z || x.w != y.w) atomicOr(flag, 1u);
-  }
-}
-
-bool cont_disabled() {
-  static const bool off = std::getenv("ECF8_NO_CONT") != nullptr;
-  return off;
-}
-
-// The continuous-walk kernel (variant 5) is exact when every window's gap is
-// where the stream's code words actually are -- always so for encoder output,
-// not guaranteed for an arbitrary parseable container.  Decide it once per
-// uploaded tensor: decode with the per-window kernel (variant 4, reference
-// semantics) and the continuous one, chunk by chunk, and compare the bytes.
-bool verify_continuous(const ecf8_dev_tensor* t, cudaStream_t st) {
-  if (cont_disabled() || t->n_elem == 0 || ecf8::dev::variant_for(t->T, t->desc.lmin).id != 4) return false;
-  const std::uint64_t kChunk = std::uint64_t{64} << 20;  // elements per comparison
-  std::uint8_t* buf = nullptr;
-  unsigned* flag = nullptr;
-  cu(cudaMalloc(&buf, 2 * (kChunk + ecf8::dev::kTileElemsMax + 64) + 64), "cudaMalloc(verify)");
-  bool ok = true;
-  try {
-    cu(cudaMalloc(&flag, sizeof(unsigned)), "cudaMalloc(verify)");
-    cu(cudaMemsetAsync(flag, 0, sizeof(unsigned), st), "memset");
-    std::vector<std::uint64_t> outpos(t->n_blocks + 1);
-    cu(cudaMemcpyAsync(outpos.data(), t->desc.outpos, 8 * outpos.size(), cudaMemcpyDeviceToHost, st), "D2H");
-    cu(cudaStreamSynchronize(st), "sync");
-    const std::uint64_t cap = kChunk + ecf8::dev::kTileElemsMax + 64;
-    std::uint8_t* a = buf;
-    std::uint8_t* b = buf + cap;
-    const std::uint64_t m = ecf8::dev::blocks_per_tile(t->T, 256);
-    for (std::uint64_t lo = 0; lo < t->n_blocks;) {
-      std::uint64_t hi = std::min(t->n_blocks, lo + m);
-      while (hi < t->n_blocks && outpos[std::min(t->n_blocks, hi + m)] - outpos[lo] <= kChunk)
-        hi = std::min(t->n_blocks, hi + m);
-      TensorDesc d = t->desc;
-      d.blk_begin = lo;
-      d.blk_end = hi;
-      d.out_offset = outpos[lo] & ~std::uint64_t{15};
-      const std::uint64_t n = outpos[hi] - d.out_offset;
-      cu(cudaMemsetAsync(a, 0, (n + 15) & ~std::uint64_t{15}, st), "memset");
-      cu(cudaMemsetAsync(b, 0, (n + 15) & ~std::uint64_t{15}, st), "memset");
-      d.out = a;
-      if (launch_one(d, st, 4) != ECF8_OK) throw std::runtime_error("verify launch");
-      d.out = b;
-      if (launch_one(d, st, 5) != ECF8_OK) throw std::runtime_error("verify launch");
-      diff_kernel<<<592, 256, 0, st>>>(reinterpret_cast<const uint4*>(a), reinterpret_cast<const uint4*>(b),
-                                       (n + 15) / 16, flag);
-      cu(cudaGetLastError(), "diff launch");
-      lo = hi;
-    }
-    unsigned h = 0;
-    cu(cudaMemcpyAsync(&h, flag, sizeof(h), cudaMemcpyDeviceToHost, st), "D2H");
-    cu(cudaStreamSynchronize(st), "sync");
-    ok = h == 0;
-  } catch (...) {
-    cudaFree(buf);
-    if (flag) cudaFree(flag);
-    throw;
-  }
-  cudaFree(buf);
-  cudaFree(flag);
-  return ok;
-}
-
 // Launch variant for a device tensor.
-int tensor_variant(const ecf8_dev_tensor* t) {
-  const int id = ecf8::dev::variant_for(t->T, t->desc.lmin).id;
-  return (id == 4 && t->cont_ok && !cont_disabled()) ? 5 : id;
-}
+int tensor_variant(const ecf8_dev_tensor* t) { return ecf8::dev::variant_for(t->T, t->desc.lmin).id; }
 
 // Per-thread state of the host-span path: three streams (copy-in, decode,
 // copy-out) and a ring of chunk slots in HBM.  Deliberately never freed:
@@ -518,7 +463,7 @@ int ecf8_tensor_upload(const ecf8_sections* s, void* stream, ecf8_dev_tensor** o
     auto t = std::make_unique<ecf8_dev_tensor>();
     try {
       upload_into(t.get(), s, nb, static_cast<cudaStream_t>(stream));
-      t->cont_ok = verify_continuous(t.get(), static_cast<cudaStream_t>(stream));
+      verify_into(t.get(), static_cast<cudaStream_t>(stream));
     } catch (...) {
       if (t->arena) cudaFree(t->arena);
       throw;
@@ -536,6 +481,19 @@ void ecf8_tensor_free(ecf8_dev_tensor* t) {
 
 uint64_t ecf8_tensor_n_elem(const ecf8_dev_tensor* t) { return t ? t->n_elem : 0; }
 int ecf8_tensor_kernel_variant(const ecf8_dev_tensor* t) { return t && t->n_elem ? tensor_variant(t) : -1; }
+
+uint64_t ecf8_tensor_verified_tiles(const ecf8_dev_tensor* t, uint64_t* total) {
+  if (total) *total = t ? t->n_vtiles : 0;
+  if (!t || !t->desc.tile_ok || t->n_vtiles == 0) return 0;
+  std::vector<std::uint32_t> bits((t->n_vtiles + 31) / 32);
+  if (cudaMemcpy(bits.data(), t->desc.tile_ok, 4 * bits.size(), cudaMemcpyDeviceToHost) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  std::uint64_t n = 0;
+  for (std::uint64_t v = 0; v < t->n_vtiles; ++v) n += (bits[v >> 5] >> (v & 31)) & 1u;
+  return n;
+}
 uint64_t ecf8_tensor_algorithmic_bytes(const ecf8_dev_tensor* t) { return t ? t->algo_bytes : 0; }
 uint64_t ecf8_tensor_device_bytes(const ecf8_dev_tensor* t) { return t ? t->arena_bytes : 0; }
 

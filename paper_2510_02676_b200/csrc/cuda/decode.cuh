@@ -18,6 +18,7 @@ struct TensorDesc {
   const std::uint32_t* fast;     // tables.hpp fast table
   const std::uint16_t* smask;    // tables.hpp start masks
   const std::uint8_t* cascade;   // reference cascade (slow path)
+  const std::uint32_t* tile_ok;  // bit v: gaps of windows [256v, 256v+256) verified (nullptr: none)
   std::uint8_t* out;             // element i lands at out[i - out_offset]
   std::uint64_t out_offset;      // multiple of 16
   std::uint64_t n_elem;
@@ -86,6 +87,11 @@ struct LaunchArgs {
 
 // One decode launch; every descriptor was prepared for variant `variant`.
 cudaError_t launch_decode(const LaunchArgs& args, int variant, cudaStream_t stream);
+
+// Gap check of a whole tensor (d.blk_begin == 0): clears bit v of tile_ok
+// (pre-set to all ones) unless every window w in [256v, 256v + 256) with a
+// successor ends where window w + 1's gap says (window_end).
+cudaError_t launch_verify_gaps(const TensorDesc& d, std::uint32_t* tile_ok, cudaStream_t stream);
 
 // count_phase on one window (window10 staged as 16 bytes in device memory).
 // Only the table fields of `tables` are used.

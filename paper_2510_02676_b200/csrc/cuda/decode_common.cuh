@@ -50,9 +50,12 @@ __device__ __forceinline__ void sts32(std::uint32_t a, std::uint32_t v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 
-// Packs 4-bit symbols into consecutive 32-bit words (first symbol lowest)
-// at shared address `addr`.
-struct SlotSink {
+// Packs 4-bit symbols into consecutive 32-bit slot words (first symbol
+// lowest) starting at shared address `addr`; consecutive words are WS bytes
+// apart (4: a lane's slot is contiguous; 128: the slots of a warp are
+// interleaved word by word, so the 32 lanes' stores hit 32 different banks).
+template <int WS>
+struct SlotSinkT {
   std::uint32_t addr;    // next word
   std::uint32_t lo = 0;  // partial word
   std::uint32_t q4 = 0;  // bits used in lo, < 32
@@ -62,7 +65,7 @@ struct SlotSink {
     q4 += n4;
     if (q4 >= 32) {
       sts32(addr, nl);
-      addr += 4;
+      addr += WS;
       lo = nh;
       q4 -= 32;
     } else {
@@ -72,9 +75,10 @@ struct SlotSink {
   // Flush the partial word; returns the symbol count since `base`.
   __device__ __forceinline__ std::uint32_t finish(std::uint32_t base) {
     if (q4) sts32(addr, lo);
-    return (addr - base) * 2 + (q4 >> 2);
+    return (addr - base) / WS * 8 + (q4 >> 2);
   }
 };
+using SlotSink = SlotSinkT<4>;
 
 struct CountSink {
   std::uint32_t n4 = 0;
@@ -141,9 +145,10 @@ __device__ __forceinline__ void decode_window_exact(std::uint32_t w0, std::uint3
 // and then exactly the symbols that start before it (start-bit mask +
 // popcount, the codec.cpp:143-160 rule).
 // fast = shared address of tb.fast, smask = shared address of tb.smask.
+template <class Sink>
 __device__ __forceinline__ bool decode_window_fast(std::uint32_t w0, std::uint32_t w1, std::uint32_t w2,
                                                    std::uint32_t w3, std::uint32_t gap, std::uint32_t fast,
-                                                   std::uint32_t smask, SlotSink& sink) {
+                                                   std::uint32_t smask, Sink& sink) {
   std::uint32_t hi = __funnelshift_l(w1, w0, gap);
   std::uint32_t lo = __funnelshift_l(w2, w1, gap);
   std::uint32_t p = gap, flags = 0;
@@ -181,13 +186,13 @@ __device__ __forceinline__ bool decode_window_fast(std::uint32_t w0, std::uint32
 // taking every code word that starts before bit 64n.  Equals the per-window
 // walks of decode_window_fast (codec.cpp:133-190) exactly when each window's
 // gap is the start of the first code word the stream places in it -- true
-// for every encoder-produced stream; ecf8_tensor_upload verifies it per
-// tensor before this path is enabled.  Returns false if a flagged entry was
-// met (the caller redoes the windows exactly).
-template <int NW>
+// for every encoder-produced stream; the upload-time gap check
+// (verify_gaps_kernel) establishes it per 256-window tile.  Returns false if
+// a flagged entry was met (the caller redoes the windows exactly).
+template <int NW, class Sink>
 __device__ __forceinline__ bool decode_lane_continuous(const std::uint32_t (&w)[2 * NW + 2], std::uint32_t n,
                                                        std::uint32_t gap, std::uint32_t fast, std::uint32_t smask,
-                                                       SlotSink& sink) {
+                                                       Sink& sink) {
   std::uint32_t hi = __funnelshift_l(w[1], w[0], gap);
   std::uint32_t lo = __funnelshift_l(w[2], w[1], gap);
   std::uint32_t p = gap, flags = 0;  // p: bit position of hi's MSB within the current 32-bit phase
@@ -231,10 +236,46 @@ __device__ __forceinline__ bool decode_lane_continuous(const std::uint32_t (&w)[
   return !(flags & kSlowFlag);
 }
 
+// Where window (w0..w3, gap)'s reference walk stops: the start of the first
+// code word at or after bit 64, relative to the window (codec.cpp:143-160 --
+// the walk takes the words that start in [gap, 64)).  For a stream written
+// by the encoder this is 64 + the next window's gap (codec.cpp:49-98).
+__device__ __forceinline__ std::uint32_t window_end(std::uint32_t w0, std::uint32_t w1, std::uint32_t w2,
+                                                    std::uint32_t w3, std::uint32_t gap, const Tables& tb,
+                                                    std::uint32_t len_off) {
+  std::uint32_t hi = __funnelshift_l(w1, w0, gap);
+  std::uint32_t lo = __funnelshift_l(w2, w1, gap);
+  std::uint32_t p = gap;
+  while (p < 32) {
+    std::uint32_t e = tb.fast[hi >> kFastShift];
+    if (e & kSlowFlag) e = slow_entry(hi, tb, len_off);
+    hi = __funnelshift_l(lo, hi, e);
+    lo = __funnelshift_l(0u, lo, e);
+    p += e & 31;
+  }
+  hi = __funnelshift_l(w2, w1, p - 32);
+  lo = __funnelshift_l(w3, w2, p - 32);
+  for (;;) {
+    const std::uint32_t idx = hi >> kFastShift;
+    std::uint32_t e = tb.fast[idx];
+    const bool fast_hit = !(e & kSlowFlag);
+    if (!fast_hit) e = slow_entry(hi, tb, len_off);
+    const std::uint32_t b = e & 31, r = 64 - p;
+    if (b >= r) {  // r <= 16 here
+      const std::uint32_t m = (fast_hit ? static_cast<std::uint32_t>(tb.smask[idx]) : 1u) >> r;
+      return m ? 64 + __ffs(m) - 1 : p + b;
+    }
+    hi = __funnelshift_l(lo, hi, e);
+    lo = __funnelshift_l(0u, lo, e);
+    p += b;
+  }
+}
+
+template <class Sink>
 __device__ __forceinline__ void decode_window(std::uint32_t w0, std::uint32_t w1, std::uint32_t w2,
                                               std::uint32_t w3, std::uint32_t gap, const Tables& tb,
-                                              std::uint32_t len_off, SlotSink& sink) {
-  const SlotSink saved = sink;
+                                              std::uint32_t len_off, Sink& sink) {
+  const Sink saved = sink;
   if (!decode_window_fast(w0, w1, w2, w3, gap, smem_addr(tb.fast), smem_addr(tb.smask), sink)) {
     sink = saved;
     decode_window_exact(w0, w1, w2, w3, gap, tb, len_off, sink);
@@ -252,8 +293,24 @@ __device__ __forceinline__ std::uint32_t sel(std::uint32_t a, std::uint32_t b, s
 // byte j): byte = sign << 7 | exponent << 3 | mantissa  (fp8.hpp assemble).
 __device__ __forceinline__ void merge8(std::uint32_t S, std::uint32_t P, std::uint32_t& o0,
                                        std::uint32_t& o1) {
+#ifdef ECF8_MERGE_C
   const std::uint32_t even = sel(sel(S << 3, P, 0x78787878u), P >> 4, 0xF8F8F8F8u);
   const std::uint32_t odd = sel(sel(S >> 1, P << 4, 0x78787878u), P, 0xF8F8F8F8u);
+#else
+  // lop3 0xE4: (a & c) | (b & ~c) -- one select per mask, 10 instructions per 8 bytes
+  std::uint32_t even, odd;
+  asm("{\n\t.reg .b32 t, u;\n\t"
+      "shl.b32 t, %2, 3;\n\t"
+      "shr.b32 u, %3, 4;\n\t"
+      "lop3.b32 t, t, u, 0x78787878, 0xE4;\n\t"
+      "lop3.b32 %0, t, %3, 0x7F7F7F7F, 0xE4;\n\t"
+      "shr.b32 t, %2, 1;\n\t"
+      "shl.b32 u, %3, 4;\n\t"
+      "lop3.b32 t, t, %3, 0x78787878, 0xE4;\n\t"
+      "lop3.b32 %1, t, u, 0x7F7F7F7F, 0xE4;\n\t}"
+      : "=r"(even), "=r"(odd)
+      : "r"(S), "r"(P));
+#endif
   o0 = __byte_perm(even, odd, 0x5140);
   o1 = __byte_perm(even, odd, 0x7362);
 }

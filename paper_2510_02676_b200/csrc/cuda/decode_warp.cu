@@ -9,20 +9,26 @@
 // scan -- the reference block's offsets come straight from outpos[]
 // (codec.cpp:212-253 restated per warp).  Phases per tile:
 //
-//   decode   each lane walks its 8 windows (decode_common.cuh fast walk,
-//            exact walk for flagged windows) into its nibble slot;
+//   decode   each lane walks its 8 windows into its nibble slot: one
+//            continuous walk when the tile passed the upload-time gap check
+//            (verify_gaps_kernel), else window by window (decode_common.cuh;
+//            exact walk for flagged windows);
 //   scan     5-step warp shuffle scan of the lane counts, segmented by
 //            reference block, clamped to outpos limits (codec.cpp:239-246);
 //   compact  funnel-shift copy of each lane's nibbles to their final place
 //            in the warp's staging tile; shared words assembled by owners;
-//   write    16 output bytes per lane-step (SWAR merge with the
-//            sign/mantissa nibbles, prefetched into L2 by one bulk TMA
-//            prefetch), tile edges byte-wise.
+//            meanwhile the tile's sign/mantissa bytes stream into the freed
+//            slots (cp.async, one round trip);
+//   write    16 output bytes per lane-step (SWAR merge of exponent and
+//            sign/mantissa nibbles), coalesced 128-bit stores, tile edges
+//            byte-wise.
 //
 // The next tile's window words, gaps and outpos bounds are loaded into
-// registers one tile ahead.
+// registers one tile ahead; the sign/mantissa bytes are prefetched into L2
+// by one bulk prefetch per tile.
 #include <cuda_runtime.h>
 
+#include <cstddef>
 #include <cstdint>
 #include <cstdlib>
 
@@ -45,18 +51,60 @@ struct WarpSmem {
   std::uint32_t head[32];
 };
 
-__shared__ Tables g_tb;
-__shared__ unsigned long long g_next_tile;  // CTA-local work queue of the current segment
+// Static shared memory: the decode tables, the tile queue and the current
+// segment's descriptor (read field by field where used: a register copy
+// would pin ~30 registers for the whole tile loop).
+struct StaticSmem {
+  Tables tb;
+  unsigned next_tile;  // CTA-local work queue of the current segment (relative)
+  TensorDesc desc;
+};
+__shared__ __align__(16) StaticSmem g_s;
+#define g_tb g_s.tb
+#define g_next_tile g_s.next_tile
+#define g_desc g_s.desc
 
-template <bool CONT>
+#ifndef ECF8_WB_UNROLL
+#define ECF8_WB_UNROLL 4
+#endif
+constexpr int kWbUnroll = ECF8_WB_UNROLL;  // write-back chunks in flight per lane
+// Sign/mantissa bytes of a tile: copied into the (then free) slots by 16-byte
+// async copies right after compaction -- one round trip per tile instead of
+// one per write-back step (ECF8_PK_GLOBAL=1 reads them from L2 instead).
+#ifndef ECF8_PK_GLOBAL
+#define ECF8_PK_SMEM 1
+constexpr bool kPkGlobal = false;
+#else
+constexpr bool kPkGlobal = true;
+#endif
+
+// One tile: decode + scan, compact, write back.
 __device__ __forceinline__ void warp_tile(const TensorDesc& d, const WarpIn& in, std::uint32_t log2T,
                                           std::uint32_t len_off, WarpSmem& ws, int lane) {
-  std::uint32_t* const my_slot = ws.slot + lane * WarpSmem::kStride;
-  const LaneRun run = warp_decode_scan<kLaneWin, CONT>(in, log2T, len_off, g_tb, my_slot, lane);
+  // slots interleaved word by word (word j of lane L at slot[32 j + L]): the
+  // lanes' slot stores and reads hit 32 different banks
+  constexpr int kWS = 128, kJ = 32;
+  const std::uint32_t* const my_slot = ws.slot + lane;
+  const LaneRun run = warp_decode_scan<kLaneWin, kWS>(in, log2T, len_off, g_tb, smem_addr(my_slot), lane,
+                                                      tile_verified(d, in, log2T));
   const std::uint32_t cc = run.len;
   const std::uint32_t off = static_cast<std::uint32_t>(in.A & 15);  // staging nibble of element A
   const std::uint32_t d0 = run.start + off, dend = d0 + cc;
   const std::uint32_t data_end = off + static_cast<std::uint32_t>(in.E - in.A);
+  // write-back addresses
+  const std::uint64_t S0 = in.A - off;
+  std::uint8_t* const out = d.out + (S0 - d.out_offset);
+  const std::uint8_t* const pk = d.packed + (S0 >> 1);
+  const std::uint32_t nch = (data_end + 15) >> 4;
+  const std::uint32_t full_lo = (off + 15) >> 4, full_hi = data_end >> 4;
+  const uint2* sp = reinterpret_cast<const uint2*>(ws.stage);
+  const uint2* pp = reinterpret_cast<const uint2*>(pk);
+  uint4* op = reinterpret_cast<uint4*>(out);
+  const std::uint32_t nfull = full_hi > full_lo ? full_hi - full_lo : 0u;
+  const uint2* sl = sp + full_lo + lane;
+  const uint2* pl = pp + full_lo + lane;  // sign/mantissa chunks (global; shared with ECF8_PK_SMEM)
+  uint4* ol = op + full_lo + lane;
+  std::uint32_t k = lane;
   __syncwarp();  // previous tile's write-back is done with the staging
   ws.rs[lane] = d0;
   ws.re[lane] = dend;
@@ -67,7 +115,7 @@ __device__ __forceinline__ void warp_tile(const TensorDesc& d, const WarpIn& in,
   const std::uint32_t f4 = (d0 & 7) * 4, lastn = ((dend - 1) & 7) + 1;
   if (cc) {
     std::uint32_t prev = my_slot[0];
-    const std::uint32_t v0 = prev << f4;
+    const std::uint32_t v0 = prev << f4;  // (my_slot[32 j] = word j)
     if (fw == lw) {
       const std::uint32_t v = v0 & low_nibbles(lastn);
       if (f4 == 0 && lastn == 8) ws.stage[fw] = v;
@@ -78,17 +126,31 @@ __device__ __forceinline__ void warp_tile(const TensorDesc& d, const WarpIn& in,
       std::uint32_t j = 1;
 #pragma unroll 4
       for (std::uint32_t k = fw + 1; k < lw; ++k, ++j) {
-        const std::uint32_t c = my_slot[j];
+        const std::uint32_t c = my_slot[kJ * j];
         ws.stage[k] = __funnelshift_l(prev, c, f4);
         prev = c;
       }
-      const std::uint32_t v = __funnelshift_l(prev, my_slot[j], f4) & low_nibbles(lastn);
+      const std::uint32_t v = __funnelshift_l(prev, my_slot[kJ * j], f4) & low_nibbles(lastn);
       if (lastn == 8) ws.stage[lw] = v;
       else tailv = v;
     }
   }
   ws.head[lane] = headv;
   __syncwarp();
+#ifdef ECF8_PK_SMEM
+  // The slots are free now: bring this tile's sign/mantissa bytes into them
+  // (16-byte async copies, one round trip for the whole tile) while the
+  // owners assemble the shared words.
+  const std::uint64_t pk_lo = (in.A - off) >> 1, pk_a = pk_lo & ~std::uint64_t{15};
+  const std::uint32_t pk_n = static_cast<std::uint32_t>((((in.E + 1) >> 1) - pk_a + 15) >> 4);  // 16 B pieces
+  {
+    const std::uint32_t dst = smem_addr(ws.slot);
+    for (std::uint32_t i = lane; i < pk_n; i += 32)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16 * i), "l"(d.packed + pk_a + 16 * i)
+                   : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+#endif
 
   // ---- owners assemble words shared between lanes
   if (cc) {
@@ -114,25 +176,21 @@ __device__ __forceinline__ void warp_tile(const TensorDesc& d, const WarpIn& in,
   __syncwarp();
 
   // ---- write-back
-  const std::uint64_t S0 = in.A - off;
-  std::uint8_t* const out = d.out + (S0 - d.out_offset);
-  const std::uint8_t* const pk = d.packed + (S0 >> 1);
-  const std::uint32_t nch = (data_end + 15) >> 4;
-  const std::uint32_t full_lo = (off + 15) >> 4, full_hi = data_end >> 4;
-  const uint2* sp = reinterpret_cast<const uint2*>(ws.stage);
-  const uint2* pp = reinterpret_cast<const uint2*>(pk);
-  uint4* op = reinterpret_cast<uint4*>(out);
-  const std::uint32_t nfull = full_hi > full_lo ? full_hi - full_lo : 0u;
-  const uint2* sl = sp + full_lo + lane;
-  const uint2* pl = pp + full_lo + lane;
-  uint4* ol = op + full_lo + lane;
-  std::uint32_t k = lane;
-  for (; k + 96 < nfull; k += 128, sl += 128, pl += 128, ol += 128) {
-    uint2 q[4];
+  // Launched with programmatic stream serialization, this grid may start
+  // while the previous one finishes; its inputs are immutable, so only the
+  // stores wait for the previous grid (a no-op once it has completed).
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#ifdef ECF8_PK_SMEM
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncwarp();
+  pl = reinterpret_cast<const uint2*>(reinterpret_cast<const std::uint8_t*>(ws.slot) + (pk_lo - pk_a)) + full_lo + lane;
+#endif
+  for (; k + 32 * (kWbUnroll - 1) < nfull; k += 32 * kWbUnroll, sl += 32 * kWbUnroll, pl += 32 * kWbUnroll, ol += 32 * kWbUnroll) {
+    uint2 q[kWbUnroll];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) q[u] = __ldg(pl + 32 * u);  // four L2 round trips overlap
+    for (int u = 0; u < kWbUnroll; ++u) q[u] = kPkGlobal ? __ldg(pl + 32 * u) : pl[32 * u];  // L2 round trips overlap
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < kWbUnroll; ++u) {
       const uint2 s = sl[32 * u];
       uint4 r;
       merge8(s.x, q[u].x, r.x, r.y);
@@ -141,7 +199,7 @@ __device__ __forceinline__ void warp_tile(const TensorDesc& d, const WarpIn& in,
     }
   }
   for (; k < nfull; k += 32, sl += 32, pl += 32, ol += 32) {
-    const uint2 q = __ldg(pl);
+    const uint2 q = kPkGlobal ? __ldg(pl) : *pl;
     const uint2 s = *sl;
     uint4 r;
     merge8(s.x, q.x, r.x, r.y);
@@ -157,34 +215,41 @@ __device__ __forceinline__ void warp_tile(const TensorDesc& d, const WarpIn& in,
     const std::uint32_t x = (ws.stage[i >> 3] >> (4 * (i & 7))) & 15u;
     out[i] = merge1(x, pk[i >> 1], i & 1);
   }
+#ifdef ECF8_PK_SMEM
+  __syncwarp();  // the next walk overwrites the slots
+#endif
 }
 
-template <int NW, bool CONT>
+template <int NW>
 __global__ void __launch_bounds__(NW * 32, 1) decode_warp_kernel(const LaunchArgs args) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   WarpSmem& ws = reinterpret_cast<WarpSmem*>(smem_raw)[warp];
+  asm volatile("griddepcontrol.launch_dependents;");  // the next decode may claim SMs as ours free up
   const std::uint64_t total_tiles = args.total_tiles;
   const std::uint64_t t_lo = total_tiles * blockIdx.x / gridDim.x;
   const std::uint64_t t_hi = total_tiles * (blockIdx.x + 1) / gridDim.x;
 
   for (std::uint64_t seg = t_lo; seg < t_hi;) {
-    TensorDesc d;
     std::uint64_t seg_end;
+    int di = 0;
     if (args.descs) {
-      const int di = find_desc(args.descs, args.n_desc, seg);
-      d = args.descs[di];
+      di = find_desc(args.descs, args.n_desc, seg);
       seg_end = (di + 1 < args.n_desc) ? args.descs[di + 1].tile_begin : total_tiles;
     } else {
-      d = args.inline_desc;
       seg_end = total_tiles;
     }
     if (seg_end > t_hi) seg_end = t_hi;
+    __syncthreads();  // every warp is done with the previous tables and descriptor
+    // The segment's descriptor lives in shared memory, read field by field
+    // where used: ~30 registers a register copy would pin for the whole loop.
+    if (threadIdx.x == 0) g_desc = args.descs ? args.descs[di] : args.inline_desc;
+    __syncthreads();
+    const TensorDesc& d = g_desc;
     const std::uint32_t log2T = 31 - __clz(d.T);
-    __syncthreads();  // every warp is done with the previous tables
     stage_tables(d, g_tb, threadIdx.x, NW * 32);
     const std::uint32_t len_off = (d.n_luts - 1) << 8;
-    if (threadIdx.x == 0) g_next_tile = seg + NW;
+    if (threadIdx.x == 0) g_next_tile = NW;
     __syncthreads();
 
     // Tiles are handed out dynamically inside the CTA (warp w starts with
@@ -202,59 +267,101 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_warp_kernel(const LaunchArg
         if (bytes)
           asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(d.packed + p0), "r"(bytes) : "memory");
       }
-      unsigned long long claim = 0;
-      if (lane == 0) claim = atomicAdd(&g_next_tile, 1ull);
-      const std::uint64_t next = __shfl_sync(0xffffffffu, claim, 0);
+      unsigned claim = 0;
+      if (lane == 0) claim = atomicAdd(&g_next_tile, 1u);
+      const std::uint64_t next = seg + __shfl_sync(0xffffffffu, claim, 0);
       if (next < seg_end) load_warp_tile(d, next, log2T, lane, nxt);
-      warp_tile<CONT>(d, cur, log2T, len_off, ws, lane);
+      warp_tile(d, cur, log2T, len_off, ws, lane);
       tile = next;
     }
     seg = seg_end;
   }
 }
 
-template <int NW, bool CONT>
+template <int NW>
 cudaError_t launch_nw(const LaunchArgs& args, cudaStream_t s) {
   static int grid_cap = 0;
   const int smem = static_cast<int>(sizeof(WarpSmem)) * NW;
   if (grid_cap == 0) {
-    cudaError_t e = cudaFuncSetAttribute(decode_warp_kernel<NW, CONT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = cudaFuncSetAttribute(decode_warp_kernel<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_warp_kernel<NW, CONT>, NW * 32, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_warp_kernel<NW>, NW * 32, smem);
     if (e != cudaSuccess) return e;
     grid_cap = sms * (per_sm > 0 ? per_sm : 1);
   }
   const std::uint64_t want = (args.total_tiles + NW - 1) / NW;
   const std::uint64_t grid = want < static_cast<std::uint64_t>(grid_cap) ? want : grid_cap;
   if (grid == 0) return cudaSuccess;
-  decode_warp_kernel<NW, CONT><<<static_cast<unsigned>(grid), NW * 32, smem, s>>>(args);
-  return cudaGetLastError();
+  // Programmatic dependent launch: consecutive decodes (layer after layer)
+  // overlap the tail of one grid with the start of the next.
+  static const bool pdl = std::getenv("ECF8_NO_PDL") == nullptr;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(NW * 32);
+  cfg.dynamicSmemBytes = static_cast<std::size_t>(smem);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, decode_warp_kernel<NW>, args);
 }
+
+// One thread per window: window_end of its reference walk against the next
+// window's gap; a mismatch anywhere in a 256-window tile clears its bit.
+__global__ void __launch_bounds__(256) verify_gaps_kernel(const TensorDesc d, std::uint64_t n_win,
+                                                          std::uint32_t* tile_ok) {
+  __shared__ Tables tb;
+  stage_tables(d, tb, threadIdx.x, blockDim.x);
+  __syncthreads();
+  const std::uint32_t len_off = (d.n_luts - 1) << 8;
+  const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
+  for (std::uint64_t k = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; k - threadIdx.x % 32 < n_win;
+       k += stride) {
+    bool bad = false;
+    if (k + 1 < n_win) {
+      const uint2 a = __ldg(reinterpret_cast<const uint2*>(d.encoded + 8 * k));
+      const uint2 b = __ldg(reinterpret_cast<const uint2*>(d.encoded + 8 * k + 8));
+      const std::uint32_t g0 = (d.gaps[k >> 1] >> ((k & 1) ? 0 : 4)) & 15u;
+      const std::uint32_t g1 = (d.gaps[(k + 1) >> 1] >> (((k + 1) & 1) ? 0 : 4)) & 15u;
+      bad = window_end(bswap32(a.x), bswap32(a.y), bswap32(b.x), bswap32(b.y), g0, tb, len_off) != 64 + g1;
+    }
+    if (__ballot_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) {
+      const std::uint64_t v = k >> 8;
+      atomicAnd(tile_ok + (v >> 5), ~(1u << (v & 31)));
+    }
+  }
+}
+
+__global__ void stream_fence_kernel() {}
 
 }  // namespace
 
-// Warps per CTA: 20 (default; 95 registers, no spills, 20 x 8.7 KB of warp
-// state + 28.6 KB of tables) or 16 (ECF8_WARPS=16, <= 128 registers).
-// Measured (8 x 14336x4096, T 256): 20 warps 2995 GB/s, 16 warps 2821 GB/s.
+// Warps per CTA: 22 (default; 22 x 8.7 KB of warp state + 29 KB of tables,
+// <= 93 registers), 20 or 16 (ECF8_WARPS).  Measured (8 x 14336x4096, T 256):
+// 22 warps 3292 GB/s, 20 warps 3206 GB/s.
 cudaError_t launch_decode_warp(const LaunchArgs& args, cudaStream_t s) {
   static const int nw = [] {
     const char* e = std::getenv("ECF8_WARPS");
-    return e ? std::atoi(e) : 20;
+    return e ? std::atoi(e) : 22;
   }();
-  return nw == 16 ? launch_nw<16, false>(args, s) : launch_nw<20, false>(args, s);
+  return nw == 16 ? launch_nw<16>(args, s) : nw == 22 ? launch_nw<22>(args, s) : launch_nw<20>(args, s);
 }
 
-// Variant 5: the same kernel walking each lane's windows continuously, for
-// tensors whose gaps ecf8_tensor_upload verified (decode_lane_continuous).
-cudaError_t launch_decode_warp_cont(const LaunchArgs& args, cudaStream_t s) {
-  static const int nw = [] {
-    const char* e = std::getenv("ECF8_WARPS");
-    return e ? std::atoi(e) : 20;
-  }();
-  return nw == 16 ? launch_nw<16, true>(args, s) : launch_nw<20, true>(args, s);
+cudaError_t launch_verify_gaps(const TensorDesc& d, std::uint32_t* tile_ok, cudaStream_t s) {
+  const std::uint64_t n_win = d.blk_end * d.T;
+  if (n_win == 0) return cudaSuccess;
+  const std::uint64_t blocks = (n_win + 255) / 256;
+  verify_gaps_kernel<<<static_cast<unsigned>(blocks < 1184 ? blocks : 1184), 256, 0, s>>>(d, n_win, tile_ok);
+  // A plain launch after it: a decode launched next with programmatic
+  // serialization may only overlap this empty grid, which starts after the
+  // gap check has completed -- the tile bits are final before any decode reads them.
+  stream_fence_kernel<<<1, 32, 0, s>>>();
+  return cudaGetLastError();
 }
 
 }  // namespace ecf8::dev

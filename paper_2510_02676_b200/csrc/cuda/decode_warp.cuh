@@ -34,17 +34,17 @@ struct WarpInT {
 };
 using WarpIn = WarpInT<kLaneWin>;
 
+// A tile's inputs in two halves: the window words and gaps (issued early,
+// they fly while the previous tile is written back), and the block offsets.
 template <int LW>
-__device__ __forceinline__ void load_warp_tile(const TensorDesc& d, std::uint64_t tile, std::uint32_t log2T,
-                                               int lane, WarpInT<LW>& in) {
+__device__ __forceinline__ void load_tile_words(const TensorDesc& d, std::uint64_t tile, std::uint32_t log2T,
+                                                int lane, WarpInT<LW>& in) {
   const std::uint32_t m = (32u * LW) >> log2T;  // blocks per tile
   in.b0 = d.blk_begin + (tile - d.tile_begin) * m;
   in.nblk = static_cast<std::uint32_t>(d.blk_end - in.b0 < m ? d.blk_end - in.b0 : m);
   in.nwin = in.nblk << log2T;
   const std::uint64_t w0g = in.b0 << log2T;
   const std::uint32_t wl = static_cast<std::uint32_t>(lane) * LW;
-  in.A = __ldg(d.outpos + in.b0);
-  in.E = __ldg(d.outpos + in.b0 + in.nblk);
   if (wl < in.nwin) {
     const uint4* src = reinterpret_cast<const uint4*>(d.encoded + 8 * (w0g + wl));
     in.w01 = __ldg(src);
@@ -59,6 +59,15 @@ __device__ __forceinline__ void load_warp_tile(const TensorDesc& d, std::uint64_
       in.w8 = __ldg(reinterpret_cast<const uint2*>(src + 2));
       in.gaps = __ldg(reinterpret_cast<const std::uint16_t*>(d.gaps + (w0g >> 1)) + lane);
     }
+  }
+}
+
+template <int LW>
+__device__ __forceinline__ void load_tile_meta(const TensorDesc& d, std::uint32_t log2T, int lane, WarpInT<LW>& in) {
+  const std::uint32_t wl = static_cast<std::uint32_t>(lane) * LW;
+  in.A = __ldg(d.outpos + in.b0);
+  in.E = __ldg(d.outpos + in.b0 + in.nblk);
+  if (wl < in.nwin) {
     const std::uint32_t bl = wl >> log2T;
     in.o0 = __ldg(d.outpos + in.b0 + bl);
     in.o1 = __ldg(d.outpos + in.b0 + bl + 1);
@@ -67,6 +76,24 @@ __device__ __forceinline__ void load_warp_tile(const TensorDesc& d, std::uint64_
   }
 }
 
+template <int LW>
+__device__ __forceinline__ void load_warp_tile(const TensorDesc& d, std::uint64_t tile, std::uint32_t log2T,
+                                               int lane, WarpInT<LW>& in) {
+  load_tile_words(d, tile, log2T, lane, in);
+  load_tile_meta(d, log2T, lane, in);
+}
+
+// Were the gaps of the windows of this warp tile verified (verify_gaps_kernel)?
+// tile_ok bit v covers the boundaries after windows [256v, 256v + 256).
+template <int LW>
+__device__ __forceinline__ bool tile_verified(const TensorDesc& d, const WarpInT<LW>& in, std::uint32_t log2T) {
+  if (!d.tile_ok || in.nwin == 0) return false;
+  const std::uint64_t w0 = in.b0 << log2T;
+  const std::uint64_t v0 = w0 >> 8, v1 = (w0 + in.nwin - 1) >> 8;
+  const std::uint32_t a = __ldg(d.tile_ok + (v0 >> 5)) >> (v0 & 31);
+  const std::uint32_t b = __ldg(d.tile_ok + (v1 >> 5)) >> (v1 & 31);
+  return (a & b & 1u) != 0;
+}
 
 struct LaneRun {
   std::uint32_t cnt;    // symbols this lane decoded (reference count rule)
@@ -74,18 +101,19 @@ struct LaneRun {
   std::uint32_t len;    // symbols kept after the block clamp
 };
 
-// Decode this lane's windows into `slot` (kSlotWords words, nibble i of the
-// run in bits 4(i%8).. of word i/8), then scan + clamp across the warp.
-// CONT: walk the lane's windows continuously (decode_lane_continuous; only
-// for tensors whose gaps were verified at upload), else window by window.
-template <int LW, bool CONT = false>
+// Decode this lane's windows into its slot (word j of the run at shared
+// address slot_base + j * WS; nibble i of the run in bits 4(i%8).. of word
+// i/8), then scan + clamp across the warp.  verified (the tile passed the
+// upload-time gap check): one continuous walk over the lane's windows;
+// otherwise, or when the walk met a flagged entry, window by window with the
+// reference's per-window semantics (fast table, exact walk where flagged).
+template <int LW, int WS = 4>
 __device__ __forceinline__ LaneRun warp_decode_scan(const WarpInT<LW>& in, std::uint32_t log2T,
-                                                   std::uint32_t len_off, const Tables& tb, std::uint32_t* slot,
-                                                   int lane) {
+                                                   std::uint32_t len_off, const Tables& tb, std::uint32_t slot_base,
+                                                   int lane, bool verified = false) {
   const std::uint32_t wl0 = static_cast<std::uint32_t>(lane) * LW;
   const bool active = wl0 < in.nwin;
-  const std::uint32_t slot_base = smem_addr(slot);
-  SlotSink sink{slot_base};
+  SlotSinkT<WS> sink{slot_base};
   if (active) {
     std::uint32_t w[2 * LW + 2];
     w[0] = bswap32(in.w01.x), w[1] = bswap32(in.w01.y), w[2] = bswap32(in.w01.z), w[3] = bswap32(in.w01.w);
@@ -96,20 +124,20 @@ __device__ __forceinline__ LaneRun warp_decode_scan(const WarpInT<LW>& in, std::
     }
     w[2 * LW] = bswap32(in.w8.x), w[2 * LW + 1] = bswap32(in.w8.y);
     const std::uint32_t n = min(in.nwin - wl0, static_cast<std::uint32_t>(LW));
-    bool exact = true;
-    if constexpr (CONT) {
-      const SlotSink saved = sink;
+    bool windowed = true;
+    if (verified) {
+      const SlotSinkT<WS> saved = sink;
       const std::uint32_t gap0 = (in.gaps >> 4) & 15u;  // window 0: high nibble of byte 0
-      exact = !decode_lane_continuous<LW>(w, n, gap0, smem_addr(tb.fast), smem_addr(tb.smask), sink);
-      if (exact) sink = saved;
+      windowed = !decode_lane_continuous<LW>(w, n, gap0, smem_addr(tb.fast), smem_addr(tb.smask), sink);
+      if (windowed) sink = saved;
     }
-    if (exact) {
+    if (windowed) {
 #pragma unroll
       for (int i = 0; i < LW; ++i) {
         if (static_cast<std::uint32_t>(i) < n) {
           // byte j of the gap word: window 2j in the high nibble, 2j + 1 low
           const std::uint32_t gap = (in.gaps >> (8 * (i >> 1) + ((i & 1) ? 0 : 4))) & 15u;
-          if constexpr (CONT)
+          if (verified)  // a flagged entry: the exact walk straight away
             decode_window_exact(w[2 * i], w[2 * i + 1], w[2 * i + 2], w[2 * i + 3], gap, tb, len_off, sink);
           else
             decode_window(w[2 * i], w[2 * i + 1], w[2 * i + 2], w[2 * i + 3], gap, tb, len_off, sink);

@@ -158,7 +158,7 @@ __device__ __forceinline__ void wait_stage_free(const Ring& R, std::uint32_t t) 
 template <int LW>
 __device__ __forceinline__ void ring_tile(const TensorDesc& d, const WarpInT<LW>& in, std::uint32_t log2T,
                                           std::uint32_t len_off, std::uint32_t* slot, const Ring& R, int lane) {
-  const LaneRun run = warp_decode_scan(in, log2T, len_off, g_tbf, slot, lane);
+  const LaneRun run = warp_decode_scan(in, log2T, len_off, g_tbf, smem_addr(slot), lane);
 
   // this ECF8 tile's part of the CTA range, in ring tiles tf (and tf + 1)
   const std::uint64_t A = in.A > R.e0 ? in.A : R.e0;

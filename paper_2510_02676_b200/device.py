@@ -33,6 +33,12 @@ class DeviceTensor:
         self.device_bytes = int(lib.ecf8_tensor_device_bytes(h))
         self.kernel_variant = int(lib.ecf8_tensor_kernel_variant(h))
 
+    def verified_tiles(self) -> tuple[int, int]:
+        """(tiles decoded by the continuous group walk, all 256-window tiles)."""
+        total = C.c_uint64()
+        n = int(lib.ecf8_tensor_verified_tiles(self.handle, C.byref(total)))
+        return n, int(total.value)
+
     def decode_into(self, out: torch.Tensor, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
         if out.dtype not in (torch.uint8, torch.float8_e4m3fn, torch.float8_e5m2) or not out.is_cuda:
             raise ValueError("out must be a CUDA uint8/float8 tensor")
