@@ -686,7 +686,7 @@ int ecf8_fused_create(const ecf8_dev_tensor* t, uint64_t n, uint64_t k, int w_fm
     if (t->n_elem != n * k) return fail(ECF8_EINVAL, "output size mismatch");
     if (w_fmt != 0 && w_fmt != 1) return fail(ECF8_EINVAL, "weight format must be 0 (E4M3) or 1 (E5M2)");
     if (ecf8::dev::fused_lane_windows(t->T, t->desc.lmin) == 0)
-      return fail(ECF8_EINVAL, "fused GEMM needs T in [8, 256] (T <= 128 when a code word is 1 bit)");
+      return fail(ECF8_EINVAL, "fused GEMM needs T in [4, 128], or T = 256 (T <= 128 when a code word is 1 bit)");
     if (int rc = require_device()) return rc;
     std::vector<std::uint64_t> outpos(t->n_blocks + 1);
     cu(cudaMemcpy(outpos.data(), t->desc.outpos, 8 * outpos.size(), cudaMemcpyDeviceToHost), "D2H outpos");
@@ -758,7 +758,7 @@ int ecf8_fused_gemm(const ecf8_fused* f, const uint8_t* d_x, uint32_t m, float s
     a.n = static_cast<std::uint32_t>(f->n);
     a.k = static_cast<std::uint32_t>(f->k);
     a.split_k = f->split_k;
-    a.stages_a = ecf8::dev::fused_stages_a(a.m_pad);
+    a.stages_a = ecf8::dev::fused_stages_a(a.m_pad, ecf8::dev::fused_slot_stride(f->w->T, f->w->desc.lmin));
     a.stages_b = ecf8::dev::fused_stages_b(a.m_pad);
     if (a.stages_a < 2) return fail(ECF8_EINVAL, "fused GEMM: shared memory too small for this m");
     a.acc_cols = 32;

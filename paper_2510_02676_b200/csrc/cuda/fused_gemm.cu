@@ -53,10 +53,10 @@ constexpr int kDecodeWarps = 20;
 constexpr int kThreadsF = (kDecodeWarps + 1) * 32;
 constexpr int kCtrlWarp = kDecodeWarps;
 constexpr std::uint32_t kTileElems = 128 * 128;  // one K tile of A (bytes)
-constexpr int kSlotStride = kSlotWords + 1;
 
 __shared__ Tables g_tbf;
-__shared__ unsigned long long g_qnext;
+__shared__ TensorDesc g_wdesc;  // this CTA's weight descriptor (read where used: frees ~30 registers)
+__shared__ unsigned g_qnext;
 __shared__ alignas(8) unsigned long long g_full[kMaxStagesA];
 __shared__ alignas(8) unsigned long long g_empty[kMaxStagesA];
 __shared__ alignas(8) unsigned long long g_bfull[2];
@@ -84,6 +84,23 @@ __device__ __forceinline__ void mbar_wait(std::uint32_t bar, std::uint32_t parit
       "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
       "r"(parity)
       : "memory");
+}
+
+// Waits that back off: a spinning try_wait loop steals issue slots from the
+// decode warps sharing the scheduler.
+__device__ __forceinline__ void mbar_wait_sleep(std::uint32_t bar, std::uint32_t parity, unsigned ns) {
+  for (;;) {
+    std::uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    if (ok) return;
+    __nanosleep(ns);
+  }
 }
 
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
@@ -152,13 +169,18 @@ __device__ __forceinline__ void wait_stage_free(const Ring& R, std::uint32_t t) 
       __nanosleep(128);
     }
   }
-  mbar_wait(smem_addr(&g_empty[t % R.stages]), ((t / R.stages) - 1) & 1u);
+  mbar_wait_sleep(smem_addr(&g_empty[t % R.stages]), ((t / R.stages) - 1) & 1u, 128);
 }
 
 template <int LW>
 __device__ __forceinline__ void ring_tile(const TensorDesc& d, const WarpInT<LW>& in, std::uint32_t log2T,
                                           std::uint32_t len_off, std::uint32_t* slot, const Ring& R, int lane) {
-  const LaneRun run = warp_decode_scan(in, log2T, len_off, g_tbf, smem_addr(slot), lane);
+  const LaneRun run = warp_decode_scan(in, log2T, len_off, g_tbf, smem_addr(slot), lane, tile_verified(d, in, log2T));
+  {  // the tile's sign/mantissa bytes (in L2 by now) -> L1 for the merge below
+    const std::uint64_t p0 = (in.A >> 1) & ~std::uint64_t{127};
+    const std::uint64_t pl = p0 + 128 * static_cast<std::uint64_t>(lane);
+    if (pl < ((in.E + 1) >> 1)) asm volatile("prefetch.global.L1 [%0];" ::"l"(d.packed + pl));
+  }
 
   // this ECF8 tile's part of the CTA range, in ring tiles tf (and tf + 1)
   const std::uint64_t A = in.A > R.e0 ? in.A : R.e0;
@@ -247,7 +269,7 @@ __device__ __forceinline__ void ring_tile(const TensorDesc& d, const WarpInT<LW>
   }
 }
 
-template <int LW>
+template <int LW, int SLOT_STRIDE>
 __global__ void __launch_bounds__(kThreadsF, 1) fused_gemm_kernel(const FusedArgs args) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -264,10 +286,14 @@ __global__ void __launch_bounds__(kThreadsF, 1) fused_gemm_kernel(const FusedArg
   std::uint32_t* const slots =
       reinterpret_cast<std::uint32_t*>(smem_raw + (b_base + args.stages_b * b_bytes - raw));
 
-  TensorDesc d = args.w;
-  d.blk_begin = cta.blk_begin;
-  d.blk_end = cta.blk_end;
-  d.tile_begin = 0;
+  if (threadIdx.x == 0) {
+    g_wdesc = args.w;
+    g_wdesc.blk_begin = cta.blk_begin;
+    g_wdesc.blk_end = cta.blk_end;
+    g_wdesc.tile_begin = 0;
+  }
+  __syncthreads();
+  const TensorDesc& d = g_wdesc;
   const std::uint32_t log2T = 31 - __clz(d.T);
   const std::uint32_t m_blk = (32u * LW) >> log2T;
   const std::uint64_t n_tiles = (cta.blk_end - cta.blk_begin + m_blk - 1) / m_blk;
@@ -301,15 +327,15 @@ __global__ void __launch_bounds__(kThreadsF, 1) fused_gemm_kernel(const FusedArg
     // ---- decode warps: dynamic queue over the CTA's ECF8 tiles, in order
     const Ring R{a_base, args.stages_a, cta.e0, cta.e1};
     const std::uint32_t len_off = (d.n_luts - 1) << 8;
-    std::uint32_t* const slot = slots + (warp * 32 + lane) * kSlotStride;
+    std::uint32_t* const slot = slots + (warp * 32 + lane) * SLOT_STRIDE;
     WarpInT<LW> nxt;
     std::uint64_t tile = warp;
     if (tile < n_tiles) load_warp_tile(d, tile, log2T, lane, nxt);
     while (tile < n_tiles) {
       const WarpInT<LW> cur = nxt;
-      unsigned long long claim = 0;
+      unsigned claim = 0;
       if (lane == 0) {
-        claim = atomicAdd(&g_qnext, 1ull);
+        claim = atomicAdd(&g_qnext, 1u);
         // sign/mantissa bytes of this tile -> L2 while it decodes
         const std::uint64_t p0 = (cur.A >> 1) & ~std::uint64_t{15};
         const std::uint32_t bytes = static_cast<std::uint32_t>((((cur.E + 1) >> 1) - p0 + 15) & ~std::uint64_t{15});
@@ -353,9 +379,9 @@ __global__ void __launch_bounds__(kThreadsF, 1) fused_gemm_kernel(const FusedArg
       // reader, the MMAs of tile t-1, completed: waited on at the end of
       // iteration t-1); one stage (m_pad > 128): after this tile's MMAs
       if (lane == 0 && args.stages_b == 2 && t + 1 < n_kt) issue_x(t + 1);
-      mbar_wait(smem_addr(&g_bfull[bs]), (t / args.stages_b) & 1u);
+      mbar_wait_sleep(smem_addr(&g_bfull[bs]), (t / args.stages_b) & 1u, 32);
       const std::uint32_t s = t % args.stages_a;
-      mbar_wait(smem_addr(&g_full[s]), (t / args.stages_a) & 1u);
+      mbar_wait_sleep(smem_addr(&g_full[s]), (t / args.stages_a) & 1u, 32);
       tc_fence_after();
       if (lane == 0) {
         const std::uint32_t a_st = a_base + s * kTileElems;
@@ -427,33 +453,44 @@ __global__ void x_tiles_kernel(const std::uint8_t* __restrict__ x, std::uint8_t*
 
 std::uint32_t fused_stages_b(std::uint32_t m_pad) { return m_pad > 128 ? 1u : 2u; }
 
-std::uint32_t fused_stages_a(std::uint32_t m_pad) {
-  // 227 KB per CTA: tables 28.6 KB static, slots 20 x 32 x 33 x 4 B,
+// Windows per decode lane and slot stride (words) for a tiled weight:
+//   Lmin >= 2, T <= 128: 4 windows, 16 + 1 words -- half-size warp tiles, so
+//       the 20 decode warps span ~4 K tiles of the ring and rarely wait for
+//       a stage, and small slots leave room for 8 A stages;
+//   Lmin >= 2, T == 256: 8 windows, 32 + 1 words;
+//   Lmin == 1, T <= 128: 4 windows of up to 64 symbols, 32 + 1 words.
+int fused_lane_windows(std::uint32_t T, std::uint32_t lmin) {
+  if (lmin >= 2 && T >= 4 && T <= 128) return 4;
+  if (lmin >= 2 && T == 256) return 8;
+  if (lmin >= 1 && T >= 4 && T <= 128) return 4;
+  return 0;
+}
+
+std::uint32_t fused_slot_stride(std::uint32_t T, std::uint32_t lmin) {
+  return (lmin >= 2 && T <= 128) ? 17u : 33u;
+}
+
+std::uint32_t fused_stages_a(std::uint32_t m_pad, std::uint32_t slot_stride) {
+  // 227 KB per CTA: tables 29 KB static, slots 20 x 32 x stride x 4 B,
   // B ring 2 x m_pad x 128 B, A ring stages x 16 KB, 1 KB alignment slack
   const std::uint32_t budget = 232448 - 30 * 1024;
-  const std::uint32_t fixed = kDecodeWarps * 32 * kSlotStride * 4 + fused_stages_b(m_pad) * m_pad * 128 + 1024;
+  const std::uint32_t fixed = kDecodeWarps * 32 * slot_stride * 4 + fused_stages_b(m_pad) * m_pad * 128 + 1024;
   const std::uint32_t s = fixed < budget ? (budget - fixed) / kTileElems : 0;
   return s > kMaxStagesA ? kMaxStagesA : s;
 }
 
-std::uint32_t fused_smem_bytes(std::uint32_t m_pad, std::uint32_t stages_a) {
-  return 1024 + stages_a * kTileElems + fused_stages_b(m_pad) * m_pad * 128 + kDecodeWarps * 32 * kSlotStride * 4;
+std::uint32_t fused_smem_bytes(std::uint32_t m_pad, std::uint32_t stages_a, std::uint32_t slot_stride) {
+  return 1024 + stages_a * kTileElems + fused_stages_b(m_pad) * m_pad * 128 + kDecodeWarps * 32 * slot_stride * 4;
 }
 
-template <int LW>
+template <int LW, int SLOT_STRIDE>
 cudaError_t launch_lw(const FusedArgs& args, std::uint32_t n_cta, cudaStream_t s) {
-  const std::uint32_t smem = fused_smem_bytes(args.m_pad, args.stages_a);
-  cudaError_t e = cudaFuncSetAttribute(fused_gemm_kernel<LW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
+  const std::uint32_t smem = fused_smem_bytes(args.m_pad, args.stages_a, SLOT_STRIDE);
+  cudaError_t e = cudaFuncSetAttribute(fused_gemm_kernel<LW, SLOT_STRIDE>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  fused_gemm_kernel<LW><<<n_cta, kThreadsF, smem, s>>>(args);
+  fused_gemm_kernel<LW, SLOT_STRIDE><<<n_cta, kThreadsF, smem, s>>>(args);
   return cudaGetLastError();
-}
-
-int fused_lane_windows(std::uint32_t T, std::uint32_t lmin) {
-  if (lmin >= 2 && T >= 8 && T <= 256) return 8;
-  if (lmin >= 1 && T >= 4 && T <= 128) return 4;
-  return 0;
 }
 
 cudaError_t launch_fused_gemm(const FusedArgs& args, std::uint32_t n_cta, cudaStream_t s) {
@@ -461,7 +498,10 @@ cudaError_t launch_fused_gemm(const FusedArgs& args, std::uint32_t n_cta, cudaSt
   const unsigned blocks = static_cast<unsigned>(std::min<std::uint64_t>((chunks + 255) / 256, 4 * 148));
   x_tiles_kernel<<<blocks, 256, 0, s>>>(args.x, const_cast<std::uint8_t*>(args.xt), args.m, args.m_pad, args.k);
   if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) return e;
-  return fused_lane_windows(args.w.T, args.w.lmin) == 8 ? launch_lw<8>(args, n_cta, s) : launch_lw<4>(args, n_cta, s);
+  const int lw = fused_lane_windows(args.w.T, args.w.lmin);
+  if (lw == 8) return launch_lw<8, 33>(args, n_cta, s);
+  return fused_slot_stride(args.w.T, args.w.lmin) == 17 ? launch_lw<4, 17>(args, n_cta, s)
+                                                        : launch_lw<4, 33>(args, n_cta, s);
 }
 
 }  // namespace ecf8::dev

@@ -38,12 +38,13 @@ struct FusedArgs {
   float scale;
 };
 
-// Windows per decode lane for a tiled weight: 8 (Lmin >= 2, T in [8, 256]),
-// 4 (Lmin == 1, T in [4, 128]), 0 = unsupported.
+// Windows per decode lane for a tiled weight (4 or 8; 0 = unsupported) and
+// the decode slot stride in words (fused_gemm.cu).
 int fused_lane_windows(std::uint32_t T, std::uint32_t lmin);
+std::uint32_t fused_slot_stride(std::uint32_t T, std::uint32_t lmin);
 std::uint32_t fused_stages_b(std::uint32_t m_pad);
-std::uint32_t fused_stages_a(std::uint32_t m_pad);
-std::uint32_t fused_smem_bytes(std::uint32_t m_pad, std::uint32_t stages_a);
+std::uint32_t fused_stages_a(std::uint32_t m_pad, std::uint32_t slot_stride);
+std::uint32_t fused_smem_bytes(std::uint32_t m_pad, std::uint32_t stages_a, std::uint32_t slot_stride);
 cudaError_t launch_fused_gemm(const FusedArgs& args, std::uint32_t n_cta, cudaStream_t s);
 
 }  // namespace ecf8::dev

@@ -47,8 +47,9 @@ for name, n, k in SHAPES:
                              out_dtype=torch.float32)
 
         td = t_ms(dtg)
+        tdec = t_ms(lambda: batch.decode())
         tp = t_ms(lambda: torch._scaled_mm(xp, wt.t(), scale_a=one, scale_b=one, out_dtype=torch.float32))
         comp = lin.compressed_bytes
         print(f"{name:8s} {n}x{k} m={m:3d}: fused {tf * 1e3:8.1f} us ({m / tf * 1e3:9.0f} tok/s, "
               f"{comp / tf / 1e6:6.0f} GB/s compressed, split_k {lin.split_k}) | decode+gemm {td * 1e3:8.1f} us | "
-              f"plain fp8 gemm {tp * 1e3:7.1f} us", flush=True)
+              f"plain fp8 gemm {tp * 1e3:7.1f} us | decode only {tdec * 1e3:7.1f} us", flush=True)
