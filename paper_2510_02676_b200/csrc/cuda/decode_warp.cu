@@ -40,16 +40,9 @@ namespace ecf8::dev {
 
 namespace {
 
-struct WarpSmem {
-  static constexpr int kSlotW = kSlotWords;
-  static constexpr int kStride = kSlotW + 1;
-  static constexpr int kStageWords = 32 * kSlotW + 8;
-  std::uint32_t slot[32 * kStride];
-  alignas(16) std::uint32_t stage[kStageWords];
-  std::uint32_t rs[32];
-  std::uint32_t re[32];
-  std::uint32_t head[32];
-};
+// 33 slot rows: a lane's run is <= 256 nibbles (32 words); the staging tile
+// holds 8192 nibbles + the 16-byte alignment offset.
+using WarpSmem = WarpPipeSmem<33, 32 * kSlotWords + 8>;
 
 // Static shared memory: the decode tables, the tile queue and the current
 // segment's descriptor (read field by field where used: a register copy
@@ -67,157 +60,31 @@ __shared__ __align__(16) StaticSmem g_s;
 #ifndef ECF8_WB_UNROLL
 #define ECF8_WB_UNROLL 4
 #endif
-constexpr int kWbUnroll = ECF8_WB_UNROLL;  // write-back chunks in flight per lane
-// Sign/mantissa bytes of a tile: copied into the (then free) slots by 16-byte
-// async copies right after compaction -- one round trip per tile instead of
-// one per write-back step (ECF8_PK_GLOBAL=1 reads them from L2 instead).
-#ifndef ECF8_PK_GLOBAL
-#define ECF8_PK_SMEM 1
-constexpr bool kPkGlobal = false;
-#else
-constexpr bool kPkGlobal = true;
-#endif
+constexpr int kWbUnroll = ECF8_WB_UNROLL;  // write-back chunks per lane and loop step
+
+// Output to global memory (d.out).  Launched with programmatic stream
+// serialization, this grid may start while the previous one finishes; its
+// inputs are immutable, so only the stores wait for the previous grid (a
+// no-op once it has completed).
+struct GlobalOut {
+  std::uint8_t* base;  // element S0
+  __device__ __forceinline__ void wait() const { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+  __device__ __forceinline__ void chunk(std::uint32_t c, const uint4& r) const {
+    reinterpret_cast<uint4*>(base)[c] = r;
+  }
+  __device__ __forceinline__ void byte(std::uint32_t i, std::uint8_t b) const { base[i] = b; }
+  __device__ __forceinline__ void done() const {}
+};
 
 // One tile: decode + scan, compact, write back.
 __device__ __forceinline__ void warp_tile(const TensorDesc& d, const WarpIn& in, std::uint32_t log2T,
                                           std::uint32_t len_off, WarpSmem& ws, int lane) {
   // slots interleaved word by word (word j of lane L at slot[32 j + L]): the
   // lanes' slot stores and reads hit 32 different banks
-  constexpr int kWS = 128, kJ = 32;
-  const std::uint32_t* const my_slot = ws.slot + lane;
-  const LaneRun run = warp_decode_scan<kLaneWin, kWS>(in, log2T, len_off, g_tb, smem_addr(my_slot), lane,
+  const LaneRun run = warp_decode_scan<kLaneWin, 128>(in, log2T, len_off, g_tb, smem_addr(ws.slot + lane), lane,
                                                       tile_verified(d, in, log2T));
-  const std::uint32_t cc = run.len;
-  const std::uint32_t off = static_cast<std::uint32_t>(in.A & 15);  // staging nibble of element A
-  const std::uint32_t d0 = run.start + off, dend = d0 + cc;
-  const std::uint32_t data_end = off + static_cast<std::uint32_t>(in.E - in.A);
-  // write-back addresses
-  const std::uint64_t S0 = in.A - off;
-  std::uint8_t* const out = d.out + (S0 - d.out_offset);
-  const std::uint8_t* const pk = d.packed + (S0 >> 1);
-  const std::uint32_t nch = (data_end + 15) >> 4;
-  const std::uint32_t full_lo = (off + 15) >> 4, full_hi = data_end >> 4;
-  const uint2* sp = reinterpret_cast<const uint2*>(ws.stage);
-  const uint2* pp = reinterpret_cast<const uint2*>(pk);
-  uint4* op = reinterpret_cast<uint4*>(out);
-  const std::uint32_t nfull = full_hi > full_lo ? full_hi - full_lo : 0u;
-  const uint2* sl = sp + full_lo + lane;
-  const uint2* pl = pp + full_lo + lane;  // sign/mantissa chunks (global; shared with ECF8_PK_SMEM)
-  uint4* ol = op + full_lo + lane;
-  std::uint32_t k = lane;
-  __syncwarp();  // previous tile's write-back is done with the staging
-  ws.rs[lane] = d0;
-  ws.re[lane] = dend;
-
-  // ---- move my nibbles to their final place; publish partial words
-  std::uint32_t headv = 0, tailv = 0;
-  const std::uint32_t fw = d0 >> 3, lw = (dend - 1) >> 3;
-  const std::uint32_t f4 = (d0 & 7) * 4, lastn = ((dend - 1) & 7) + 1;
-  if (cc) {
-    std::uint32_t prev = my_slot[0];
-    const std::uint32_t v0 = prev << f4;  // (my_slot[32 j] = word j)
-    if (fw == lw) {
-      const std::uint32_t v = v0 & low_nibbles(lastn);
-      if (f4 == 0 && lastn == 8) ws.stage[fw] = v;
-      else headv = v;
-    } else {
-      if (f4 == 0) ws.stage[fw] = v0;
-      else headv = v0;
-      std::uint32_t j = 1;
-#pragma unroll 4
-      for (std::uint32_t k = fw + 1; k < lw; ++k, ++j) {
-        const std::uint32_t c = my_slot[kJ * j];
-        ws.stage[k] = __funnelshift_l(prev, c, f4);
-        prev = c;
-      }
-      const std::uint32_t v = __funnelshift_l(prev, my_slot[kJ * j], f4) & low_nibbles(lastn);
-      if (lastn == 8) ws.stage[lw] = v;
-      else tailv = v;
-    }
-  }
-  ws.head[lane] = headv;
-  __syncwarp();
-#ifdef ECF8_PK_SMEM
-  // The slots are free now: bring this tile's sign/mantissa bytes into them
-  // (16-byte async copies, one round trip for the whole tile) while the
-  // owners assemble the shared words.
-  const std::uint64_t pk_lo = (in.A - off) >> 1, pk_a = pk_lo & ~std::uint64_t{15};
-  const std::uint32_t pk_n = static_cast<std::uint32_t>((((in.E + 1) >> 1) - pk_a + 15) >> 4);  // 16 B pieces
-  {
-    const std::uint32_t dst = smem_addr(ws.slot);
-    for (std::uint32_t i = lane; i < pk_n; i += 32)
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16 * i), "l"(d.packed + pk_a + 16 * i)
-                   : "memory");
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  }
-#endif
-
-  // ---- owners assemble words shared between lanes
-  if (cc) {
-    const bool start_owner = (f4 == 0 || d0 == off) && !(f4 == 0 && (fw < lw || lastn == 8));
-    const bool tail_owner = fw != lw && lastn != 8;
-#pragma unroll
-    for (int pass = 0; pass < 2; ++pass) {
-      if (pass == 0 ? !start_owner : !tail_owner) continue;
-      const std::uint32_t k = pass == 0 ? fw : lw;
-      std::uint32_t v = pass == 0 ? headv : tailv;
-      const std::uint32_t wend = min(8 * k + 8, data_end);
-      std::uint32_t covered = dend;
-      for (int j = lane + 1; covered < wend && j < 32; ++j) {
-        const std::uint32_t rj = ws.rs[j], ej = ws.re[j];
-        if (ej > rj) {
-          v |= ws.head[j];
-          covered = ej;
-        }
-      }
-      ws.stage[k] = v;
-    }
-  }
-  __syncwarp();
-
-  // ---- write-back
-  // Launched with programmatic stream serialization, this grid may start
-  // while the previous one finishes; its inputs are immutable, so only the
-  // stores wait for the previous grid (a no-op once it has completed).
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-#ifdef ECF8_PK_SMEM
-  asm volatile("cp.async.wait_all;" ::: "memory");
-  __syncwarp();
-  pl = reinterpret_cast<const uint2*>(reinterpret_cast<const std::uint8_t*>(ws.slot) + (pk_lo - pk_a)) + full_lo + lane;
-#endif
-  for (; k + 32 * (kWbUnroll - 1) < nfull; k += 32 * kWbUnroll, sl += 32 * kWbUnroll, pl += 32 * kWbUnroll, ol += 32 * kWbUnroll) {
-    uint2 q[kWbUnroll];
-#pragma unroll
-    for (int u = 0; u < kWbUnroll; ++u) q[u] = kPkGlobal ? __ldg(pl + 32 * u) : pl[32 * u];  // L2 round trips overlap
-#pragma unroll
-    for (int u = 0; u < kWbUnroll; ++u) {
-      const uint2 s = sl[32 * u];
-      uint4 r;
-      merge8(s.x, q[u].x, r.x, r.y);
-      merge8(s.y, q[u].y, r.z, r.w);
-      ol[32 * u] = r;
-    }
-  }
-  for (; k < nfull; k += 32, sl += 32, pl += 32, ol += 32) {
-    const uint2 q = kPkGlobal ? __ldg(pl) : *pl;
-    const uint2 s = *sl;
-    uint4 r;
-    merge8(s.x, q.x, r.x, r.y);
-    merge8(s.y, q.y, r.z, r.w);
-    *ol = r;
-  }
-  // partial edge chunks, one byte per lane: lanes 0-15 the first chunk,
-  // lanes 16-31 the last one
-  const std::uint32_t i = lane < 16 ? static_cast<std::uint32_t>(lane) : 16 * (nch - 1) + (lane - 16);
-  const bool edge = lane < 16 ? (full_lo > 0 && i >= off && i < data_end)
-                              : (full_hi < nch && !(nch == 1 && full_lo > 0) && i < data_end);
-  if (edge) {
-    const std::uint32_t x = (ws.stage[i >> 3] >> (4 * (i & 7))) & 15u;
-    out[i] = merge1(x, pk[i >> 1], i & 1);
-  }
-#ifdef ECF8_PK_SMEM
-  __syncwarp();  // the next walk overwrites the slots
-#endif
+  GlobalOut out{d.out + ((in.A & ~std::uint64_t{15}) - d.out_offset)};
+  compact_write<kWbUnroll>(d, in.A, in.E, run, ws, lane, out);
 }
 
 template <int NW>

@@ -164,4 +164,150 @@ __device__ __forceinline__ LaneRun warp_decode_scan(const WarpInT<LW>& in, std::
   return LaneRun{cnt, start_rel, cc};
 }
 
+// ---- compaction + write-back (shared by the decode kernel and the fused GEMM)
+
+// Per-warp shared memory of the tile pipeline: the lanes' nibble slots
+// (interleaved word by word: word j of lane L at slot[32 j + L]), the staging
+// tile the runs are compacted into, and the lanes' run bounds / partial head
+// words.  After compaction the slots hold the tile's sign/mantissa bytes.
+template <int SLOT_ROWS, int STAGE_WORDS>
+struct WarpPipeSmem {
+  static constexpr int kSlotRows = SLOT_ROWS;
+  std::uint32_t slot[SLOT_ROWS * 32];
+  alignas(16) std::uint32_t stage[STAGE_WORDS];
+  std::uint32_t rs[32];
+  std::uint32_t re[32];
+  std::uint32_t head[32];
+};
+
+// Compact the lanes' runs (slot nibbles, LaneRun from warp_decode_scan) into
+// the staging tile, then write the tile's output elements [A, E) -- FP8
+// bytes = exponent nibble + sign/mantissa nibble (fp8.hpp:42-57) -- through
+// `out`:
+//   out.wait()               once, before the first store
+//   out.chunk(c, r)          16 bytes for elements [S0 + 16c, +16), S0 = A & ~15
+//   out.byte(i, b)           one byte for element S0 + i
+//   out.done()               after the last store
+// Full 16-element chunks go out as 16-byte stores, lane-interleaved
+// (coalesced); the ragged first and last chunks byte by byte.  The
+// sign/mantissa bytes of the full chunks come into the (then free) slots by
+// 16-byte async copies issued right after compaction: one round trip per tile
+// (the slots must hold 8 x full chunks + 16 bytes).
+template <int UNROLL, class WSm, class Out>
+__device__ __forceinline__ void compact_write(const TensorDesc& d, std::uint64_t A, std::uint64_t E,
+                                              const LaneRun& run, WSm& ws, int lane, Out& out) {
+  const std::uint32_t* const my_slot = ws.slot + lane;
+  const std::uint32_t cc = run.len;
+  const std::uint32_t off = static_cast<std::uint32_t>(A & 15);  // staging nibble of element A
+  const std::uint32_t d0 = run.start + off, dend = d0 + cc;
+  const std::uint32_t data_end = off + static_cast<std::uint32_t>(E - A);
+  const std::uint64_t S0 = A - off;
+  const std::uint32_t nch = (data_end + 15) >> 4;
+  const std::uint32_t full_lo = (off + 15) >> 4, full_hi = data_end >> 4;
+  const std::uint32_t nfull = full_hi > full_lo ? full_hi - full_lo : 0u;
+  __syncwarp();  // previous tile's write-back is done with the staging and the slots' packed bytes
+  ws.rs[lane] = d0;
+  ws.re[lane] = dend;
+
+  // ---- move my nibbles to their final place; publish partial words
+  std::uint32_t headv = 0, tailv = 0;
+  const std::uint32_t fw = d0 >> 3, lw = (dend - 1) >> 3;
+  const std::uint32_t f4 = (d0 & 7) * 4, lastn = ((dend - 1) & 7) + 1;
+  if (cc) {
+    std::uint32_t prev = my_slot[0];
+    const std::uint32_t v0 = prev << f4;
+    if (fw == lw) {
+      const std::uint32_t v = v0 & low_nibbles(lastn);
+      if (f4 == 0 && lastn == 8) ws.stage[fw] = v;
+      else headv = v;
+    } else {
+      if (f4 == 0) ws.stage[fw] = v0;
+      else headv = v0;
+      std::uint32_t j = 1;
+#pragma unroll 4
+      for (std::uint32_t k = fw + 1; k < lw; ++k, ++j) {
+        const std::uint32_t c = my_slot[32 * j];
+        ws.stage[k] = __funnelshift_l(prev, c, f4);
+        prev = c;
+      }
+      const std::uint32_t v = __funnelshift_l(prev, my_slot[32 * j], f4) & low_nibbles(lastn);
+      if (lastn == 8) ws.stage[lw] = v;
+      else tailv = v;
+    }
+  }
+  ws.head[lane] = headv;
+  __syncwarp();
+
+  // ---- the slots are free: sign/mantissa bytes of the full chunks into them
+  // (16-byte pieces from the 16-byte aligned address at or below the first
+  // full chunk's bytes: <= 8 nfull + 16 bytes)
+  const std::uint8_t* const pk = d.packed + (S0 >> 1);
+  const std::uint64_t pk_lo = (S0 >> 1) + 8 * full_lo, pk_a = pk_lo & ~std::uint64_t{15};
+  {
+    const std::uint32_t n16 = static_cast<std::uint32_t>((pk_lo + 8 * nfull - pk_a + 15) >> 4);
+    const std::uint32_t dst = smem_addr(ws.slot);
+    for (std::uint32_t i = lane; i < n16; i += 32)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16 * i), "l"(d.packed + pk_a + 16 * i)
+                   : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+
+  // ---- owners assemble words shared between lanes
+  if (cc) {
+    const bool start_owner = (f4 == 0 || d0 == off) && !(f4 == 0 && (fw < lw || lastn == 8));
+    const bool tail_owner = fw != lw && lastn != 8;
+#pragma unroll
+    for (int pass = 0; pass < 2; ++pass) {
+      if (pass == 0 ? !start_owner : !tail_owner) continue;
+      const std::uint32_t k = pass == 0 ? fw : lw;
+      std::uint32_t v = pass == 0 ? headv : tailv;
+      const std::uint32_t wend = min(8 * k + 8, data_end);
+      std::uint32_t covered = dend;
+      for (int j = lane + 1; covered < wend && j < 32; ++j) {
+        const std::uint32_t rj = ws.rs[j], ej = ws.re[j];
+        if (ej > rj) {
+          v |= ws.head[j];
+          covered = ej;
+        }
+      }
+      ws.stage[k] = v;
+    }
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncwarp();
+
+  // ---- write-back
+  out.wait();
+  const uint2* sl = reinterpret_cast<const uint2*>(ws.stage) + full_lo + lane;
+  const uint2* pl = reinterpret_cast<const uint2*>(reinterpret_cast<const std::uint8_t*>(ws.slot) + (pk_lo - pk_a)) + lane;
+  std::uint32_t k = lane;
+  for (; k + 32 * (UNROLL - 1) < nfull; k += 32 * UNROLL, sl += 32 * UNROLL, pl += 32 * UNROLL) {
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      const uint2 s = sl[32 * u], q = pl[32 * u];
+      uint4 r;
+      merge8(s.x, q.x, r.x, r.y);
+      merge8(s.y, q.y, r.z, r.w);
+      out.chunk(full_lo + k + 32 * u, r);
+    }
+  }
+  for (; k < nfull; k += 32, sl += 32, pl += 32) {
+    const uint2 s = *sl, q = *pl;
+    uint4 r;
+    merge8(s.x, q.x, r.x, r.y);
+    merge8(s.y, q.y, r.z, r.w);
+    out.chunk(full_lo + k, r);
+  }
+  // partial edge chunks, one byte per lane: lanes 0-15 the first chunk,
+  // lanes 16-31 the last one
+  const std::uint32_t i = lane < 16 ? static_cast<std::uint32_t>(lane) : 16 * (nch - 1) + (lane - 16);
+  const bool edge = lane < 16 ? (full_lo > 0 && i >= off && i < data_end)
+                              : (full_hi < nch && !(nch == 1 && full_lo > 0) && i < data_end);
+  if (edge) {
+    const std::uint32_t x = (ws.stage[i >> 3] >> (4 * (i & 7))) & 15u;
+    out.byte(i, merge1(x, pk[i >> 1], i & 1));
+  }
+  out.done();
+}
+
 }  // namespace ecf8::dev

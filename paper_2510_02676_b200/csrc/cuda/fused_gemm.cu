@@ -19,7 +19,7 @@
 // the launch (a whole number of waves of the 148 SMs, one CTA per SM); a run
 // spans at most two n-tiles, each accumulated in its own TMEM block, and the
 // partial rows are added into y with red.global.add.f32.  Warp roles:
-//   decode warps (kDecodeWarps)  claim ECF8 tiles (256 windows, decode_warp.cuh)
+//   decode warps (20; 12 for 1-bit codes)  claim ECF8 warp tiles (decode_warp.cuh)
 //       covering the CTA's element range in order, decode them into their
 //       nibble slots, then merge exponent + sign/mantissa nibbles and store
 //       the FP8 bytes straight into the A ring stage of their K tile; each
@@ -49,9 +49,10 @@ namespace ecf8::dev {
 
 namespace {
 
-constexpr int kDecodeWarps = 20;
-constexpr int kThreadsF = (kDecodeWarps + 1) * 32;
-constexpr int kCtrlWarp = kDecodeWarps;
+// Decode warps per CTA: 20, or 12 when a lane's run can hold 64-symbol
+// windows (1-bit codes) and its pipeline state doubles.
+template <int LW, int ROWS>
+constexpr int decode_warps() { return (LW == 4 && ROWS > 17) ? 12 : 20; }
 constexpr std::uint32_t kTileElems = 128 * 128;  // one K tile of A (bytes)
 
 __shared__ Tables g_tbf;
@@ -172,105 +173,100 @@ __device__ __forceinline__ void wait_stage_free(const Ring& R, std::uint32_t t) 
   mbar_wait_sleep(smem_addr(&g_empty[t % R.stages]), ((t / R.stages) - 1) & 1u, 128);
 }
 
-template <int LW>
-__device__ __forceinline__ void ring_tile(const TensorDesc& d, const WarpInT<LW>& in, std::uint32_t log2T,
-                                          std::uint32_t len_off, std::uint32_t* slot, const Ring& R, int lane) {
-  const LaneRun run = warp_decode_scan(in, log2T, len_off, g_tbf, smem_addr(slot), lane, tile_verified(d, in, log2T));
-  {  // the tile's sign/mantissa bytes (in L2 by now) -> L1 for the merge below
-    const std::uint64_t p0 = (in.A >> 1) & ~std::uint64_t{127};
-    const std::uint64_t pl = p0 + 128 * static_cast<std::uint64_t>(lane);
-    if (pl < ((in.E + 1) >> 1)) asm volatile("prefetch.global.L1 [%0];" ::"l"(d.packed + pl));
-  }
+// Output into the A ring: element g of the CTA range [e0, e1) lands in ring
+// tile (g - e0) >> 14 at offset g & 16383 (the tiled layout is the swizzled
+// shared-memory image).  A warp tile spans at most two ring tiles, tf and
+// tf + 1; elements outside [e0, e1) belong to the neighbouring CTA.
+struct RingOut {
+  std::uint64_t S0;              // element of chunk 0
+  std::uint64_t e0, e1;          // CTA range
+  std::uint32_t c_lo, c_hi;      // chunks inside [e0, e1) (chunks never straddle e0 / e1: multiples of 16384)
+  std::uint32_t c_split;         // first chunk in ring tile tf + 1
+  std::uint32_t base_f, base_l;  // shared address of chunk 0 if it were in ring tile tf / tf + 1
+  std::uint32_t tf;              // first ring tile of the warp tile
+  std::uint32_t bf, bl;          // bytes this warp writes into ring tiles tf, tf + 1
+  std::uint32_t bar_f, bar_l;    // their "full" barriers
+  const Ring* R;
+  int lane;
 
+  __device__ __forceinline__ void wait() const {
+    wait_stage_free(*R, tf);
+    if (bl) wait_stage_free(*R, tf + 1);
+  }
+  __device__ __forceinline__ void chunk(std::uint32_t c, const uint4& r) const {
+    if (c < c_lo || c >= c_hi) return;
+    const std::uint32_t a = (c < c_split ? base_f : base_l) + 16 * c;
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(r.x), "r"(r.y), "r"(r.z), "r"(r.w)
+                 : "memory");
+  }
+  __device__ __forceinline__ void byte(std::uint32_t i, std::uint8_t b) const {
+    const std::uint64_t g = S0 + i;
+    if (g < e0 || g >= e1) return;
+    const std::uint32_t a = ((i >> 4) < c_split ? base_f : base_l) + i;
+    asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(static_cast<std::uint32_t>(b)) : "memory");
+  }
+  // every writer fences its generic-proxy stores for the tensor core's async
+  // proxy, then lane 0 arrives with the warp's byte counts
+  __device__ __forceinline__ void done() const {
+    fence_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      if (bf) mbar_arrive(bar_f, bf);
+      if (bl) mbar_arrive(bar_l, bl);
+    }
+  }
+};
+
+template <int LW, class WSm>
+__device__ __forceinline__ void ring_tile(const TensorDesc& d, const WarpInT<LW>& in, std::uint32_t log2T,
+                                          std::uint32_t len_off, WSm& ws, const Ring& R, int lane) {
+  const LaneRun run = warp_decode_scan<LW, 128>(in, log2T, len_off, g_tbf, smem_addr(ws.slot + lane), lane,
+                                                tile_verified(d, in, log2T));
   // this ECF8 tile's part of the CTA range, in ring tiles tf (and tf + 1)
   const std::uint64_t A = in.A > R.e0 ? in.A : R.e0;
   const std::uint64_t E = in.E < R.e1 ? in.E : R.e1;
-  if (A >= E) return;
-  const std::uint32_t tf = static_cast<std::uint32_t>((A - R.e0) >> 14);
+  if (A >= E) {
+    __syncwarp();
+    return;
+  }
+  RingOut out;
+  out.S0 = in.A & ~std::uint64_t{15};
+  out.e0 = R.e0;
+  out.e1 = R.e1;
+  out.tf = static_cast<std::uint32_t>((A - R.e0) >> 14);
   const std::uint32_t tl = static_cast<std::uint32_t>((E - 1 - R.e0) >> 14);
-  wait_stage_free(R, tf);
-  if (tl != tf) wait_stage_free(R, tl);
-
-  // my run in CTA-relative element coordinates (a CTA run is < 2^31 elements)
-  const int rr0 = static_cast<int>(static_cast<long long>(in.A + run.start) - static_cast<long long>(R.e0));
-  const int span = static_cast<int>(R.e1 - R.e0);
-  const int lo_r = rr0 > 0 ? rr0 : 0;
-  const int hi_r = rr0 + static_cast<int>(run.len) < span ? rr0 + static_cast<int>(run.len) : span;
-  const std::uint32_t bnd = (tf + 1) << 14;  // first element of ring tile tf + 1
-  if (lo_r < hi_r) {
-    const std::uint32_t offA = R.a_base + (tf % R.stages) * kTileElems - (tf << 14);
-    const std::uint32_t offB = R.a_base + ((tf + 1) % R.stages) * kTileElems - bnd;
-    const std::uint32_t* pk = reinterpret_cast<const std::uint32_t*>(d.packed + (R.e0 >> 1));
-    const std::uint32_t sb = smem_addr(slot);
-    // a group of 8 elements starting at g (multiple of 8), bytes [b0, b1)
-    auto partial = [&](int g, int b0, int b1) {
-      const int ig = g - rr0;
-      std::uint32_t x;
-      if (ig >= 0) {
-        const std::uint32_t w = static_cast<std::uint32_t>(ig) >> 3, sh = (static_cast<std::uint32_t>(ig) & 7) * 4;
-        x = __funnelshift_r(lds32(sb + 4 * w), lds32(sb + 4 * w + 4), sh);
-      } else {
-        x = lds32(sb) << static_cast<std::uint32_t>(-ig * 4);
-      }
-      std::uint32_t r0, r1;
-      merge8(x, __ldg(pk + (g >> 3)), r0, r1);
-      const std::uint32_t dst = (static_cast<std::uint32_t>(g) < bnd ? offA : offB) + static_cast<std::uint32_t>(g);
-      for (int o = b0; o < b1; ++o) {
-        const int j = o - g;
-        const std::uint32_t byte = ((j < 4 ? r0 : r1) >> (8 * (j & 3))) & 0xFFu;
-        asm volatile("st.shared.u8 [%0], %1;" ::"r"(dst + j), "r"(byte) : "memory");
-      }
-    };
-    const int g1 = (lo_r + 7) & ~7, g2 = hi_r & ~7;
-    if (g1 > g2) {
-      partial(lo_r & ~7, lo_r, hi_r);
-    } else {
-      if (lo_r < g1) partial(g1 - 8, lo_r, g1);
-      if (g1 < g2) {
-        // full groups: the run's nibbles slide through one word at a time
-        const std::uint32_t ig = static_cast<std::uint32_t>(g1 - rr0);
-        const std::uint32_t sh = (ig & 7) * 4;
-        std::uint32_t sa = sb + 4 * (ig >> 3);
-        std::uint32_t prev = lds32(sa);
-        for (int g = g1; g < g2; g += 8) {
-          sa += 4;
-          const std::uint32_t nxt = lds32(sa);
-          const std::uint32_t x = __funnelshift_r(prev, nxt, sh);
-          prev = nxt;
-          std::uint32_t r0, r1;
-          merge8(x, __ldg(pk + (g >> 3)), r0, r1);
-          const std::uint32_t dst = (static_cast<std::uint32_t>(g) < bnd ? offA : offB) + static_cast<std::uint32_t>(g);
-          asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(dst), "r"(r0), "r"(r1) : "memory");
-        }
-      }
-      if (g2 < hi_r) partial(g2, g2, hi_r);
-    }
-  }
-  // publish: every writer fences its generic-proxy stores for the tensor
-  // core's async proxy, then lane 0 arrives with the warp's byte counts
-  const int t0 = static_cast<int>(tf << 14), t1 = static_cast<int>(bnd), t2 = t1 + static_cast<int>(kTileElems);
-  std::uint32_t bf = 0, bl = 0;
-  if (lo_r < hi_r) {
-    const int a0 = lo_r > t0 ? lo_r : t0, a1 = hi_r < t1 ? hi_r : t1;
-    const int c0 = lo_r > t1 ? lo_r : t1, c1 = hi_r < t2 ? hi_r : t2;
-    bf = a1 > a0 ? static_cast<std::uint32_t>(a1 - a0) : 0u;
-    bl = c1 > c0 ? static_cast<std::uint32_t>(c1 - c0) : 0u;
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    bf += __shfl_xor_sync(0xffffffffu, bf, o);
-    bl += __shfl_xor_sync(0xffffffffu, bl, o);
-  }
-  fence_async_smem();
-  __syncwarp();
-  if (lane == 0) {
-    if (bf) mbar_arrive(smem_addr(&g_full[tf % R.stages]), bf);
-    if (bl) mbar_arrive(smem_addr(&g_full[(tf + 1) % R.stages]), bl);
-  }
+  const std::uint64_t bnd = R.e0 + (static_cast<std::uint64_t>(out.tf + 1) << 14);
+  out.bf = static_cast<std::uint32_t>((E < bnd ? E : bnd) - A);
+  out.bl = tl != out.tf ? static_cast<std::uint32_t>(E - bnd) : 0u;
+  // chunk c holds elements S0 + 16c ..; CTA-relative element g - e0 of ring
+  // tile t lives at a_base + (t % stages) * 16384 + (g - e0 - 16384 t)
+  const std::int64_t s_rel = static_cast<std::int64_t>(out.S0) - static_cast<std::int64_t>(R.e0);
+  out.c_lo = s_rel >= 0 ? 0u : static_cast<std::uint32_t>((-s_rel) >> 4);
+  out.c_hi = static_cast<std::uint32_t>((static_cast<std::int64_t>(R.e1) - static_cast<std::int64_t>(out.S0)) >> 4);
+  out.c_split = static_cast<std::uint32_t>((static_cast<std::int64_t>(bnd) - static_cast<std::int64_t>(out.S0)) >> 4);
+  const std::int32_t s_rel32 = static_cast<std::int32_t>(s_rel);  // a CTA run is < 2^31 elements
+  out.base_f = static_cast<std::uint32_t>(static_cast<std::int32_t>(R.a_base + (out.tf % R.stages) * kTileElems) -
+                                          static_cast<std::int32_t>(out.tf << 14) + s_rel32);
+  out.base_l = static_cast<std::uint32_t>(static_cast<std::int32_t>(R.a_base + ((out.tf + 1) % R.stages) * kTileElems) -
+                                          static_cast<std::int32_t>((out.tf + 1) << 14) + s_rel32);
+  out.bar_f = smem_addr(&g_full[out.tf % R.stages]);
+  out.bar_l = smem_addr(&g_full[(out.tf + 1) % R.stages]);
+  out.R = &R;
+  out.lane = lane;
+  compact_write<2>(d, in.A, in.E, run, ws, lane, out);
 }
 
-template <int LW, int SLOT_STRIDE>
-__global__ void __launch_bounds__(kThreadsF, 1) fused_gemm_kernel(const FusedArgs args) {
+// Per decode warp: slots of SLOT_ROWS words per lane (a lane's run of LW
+// windows), the staging tile (32 LW windows x <= 32 or 64 symbols).
+template <int LW, int SLOT_ROWS>
+using FusedWarpSmem = WarpPipeSmem<SLOT_ROWS, 32 * LW * (SLOT_ROWS > 17 && LW == 4 ? 64 : 32) / 8 + 8>;
+
+template <int LW, int SLOT_ROWS>
+__global__ void __launch_bounds__((decode_warps<LW, SLOT_ROWS>() + 1) * 32, 1) fused_gemm_kernel(const FusedArgs args) {
+  using WSm = FusedWarpSmem<LW, SLOT_ROWS>;
+  constexpr int kDecodeWarps = decode_warps<LW, SLOT_ROWS>();
+  constexpr int kThreadsF = (kDecodeWarps + 1) * 32;
+  constexpr int kCtrlWarp = kDecodeWarps;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const FusedCta cta = args.plan[blockIdx.x];
@@ -283,8 +279,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) fused_gemm_kernel(const FusedArg
   const std::uint32_t a_base = (raw + 1023u) & ~1023u;
   const std::uint32_t b_base = a_base + args.stages_a * kTileElems;
   const std::uint32_t b_bytes = args.m_pad * 128u;
-  std::uint32_t* const slots =
-      reinterpret_cast<std::uint32_t*>(smem_raw + (b_base + args.stages_b * b_bytes - raw));
+  WSm* const wsm = reinterpret_cast<WSm*>(smem_raw + (b_base + args.stages_b * b_bytes - raw));
 
   if (threadIdx.x == 0) {
     g_wdesc = args.w;
@@ -327,7 +322,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) fused_gemm_kernel(const FusedArg
     // ---- decode warps: dynamic queue over the CTA's ECF8 tiles, in order
     const Ring R{a_base, args.stages_a, cta.e0, cta.e1};
     const std::uint32_t len_off = (d.n_luts - 1) << 8;
-    std::uint32_t* const slot = slots + (warp * 32 + lane) * SLOT_STRIDE;
+    WSm& ws = wsm[warp];
     WarpInT<LW> nxt;
     std::uint64_t tile = warp;
     if (tile < n_tiles) load_warp_tile(d, tile, log2T, lane, nxt);
@@ -344,7 +339,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) fused_gemm_kernel(const FusedArg
       }
       const std::uint64_t next = __shfl_sync(0xffffffffu, claim, 0);
       if (next < n_tiles) load_warp_tile(d, next, log2T, lane, nxt);
-      ring_tile(d, cur, log2T, len_off, slot, R, lane);
+      ring_tile(d, cur, log2T, len_off, ws, R, lane);
       tile = next;
     }
   } else {
@@ -453,12 +448,11 @@ __global__ void x_tiles_kernel(const std::uint8_t* __restrict__ x, std::uint8_t*
 
 std::uint32_t fused_stages_b(std::uint32_t m_pad) { return m_pad > 128 ? 1u : 2u; }
 
-// Windows per decode lane and slot stride (words) for a tiled weight:
-//   Lmin >= 2, T <= 128: 4 windows, 16 + 1 words -- half-size warp tiles, so
-//       the 20 decode warps span ~4 K tiles of the ring and rarely wait for
-//       a stage, and small slots leave room for 8 A stages;
-//   Lmin >= 2, T == 256: 8 windows, 32 + 1 words;
-//   Lmin == 1, T <= 128: 4 windows of up to 64 symbols, 32 + 1 words.
+// Decode-warp geometry for a tiled weight:
+//   Lmin >= 2, T <= 128: 4 windows per lane, 17 slot rows -- half-size warp
+//       tiles keep the 20 decode warps within ~4 K tiles of the MMA;
+//   Lmin >= 2, T == 256: 8 windows per lane, 33 slot rows;
+//   Lmin == 1, T <= 128: 4 windows of up to 64 symbols, 33 slot rows.
 int fused_lane_windows(std::uint32_t T, std::uint32_t lmin) {
   if (lmin >= 2 && T >= 4 && T <= 128) return 4;
   if (lmin >= 2 && T == 256) return 8;
@@ -466,30 +460,37 @@ int fused_lane_windows(std::uint32_t T, std::uint32_t lmin) {
   return 0;
 }
 
-std::uint32_t fused_slot_stride(std::uint32_t T, std::uint32_t lmin) {
-  return (lmin >= 2 && T <= 128) ? 17u : 33u;
+template <int LW, int ROWS>
+constexpr std::uint32_t warps_smem() {
+  return static_cast<std::uint32_t>(decode_warps<LW, ROWS>() * sizeof(FusedWarpSmem<LW, ROWS>));
 }
 
-std::uint32_t fused_stages_a(std::uint32_t m_pad, std::uint32_t slot_stride) {
-  // 227 KB per CTA: tables 29 KB static, slots 20 x 32 x stride x 4 B,
+// All decode warps' pipeline state.
+std::uint32_t fused_warp_smem(std::uint32_t T, std::uint32_t lmin) {
+  if (fused_lane_windows(T, lmin) == 8) return warps_smem<8, 33>();
+  return (lmin >= 2) ? warps_smem<4, 17>() : warps_smem<4, 33>();
+}
+
+std::uint32_t fused_stages_a(std::uint32_t m_pad, std::uint32_t warp_smem) {
+  // 227 KB per CTA: tables 29 KB static, the decode warps' pipeline state,
   // B ring 2 x m_pad x 128 B, A ring stages x 16 KB, 1 KB alignment slack
   const std::uint32_t budget = 232448 - 30 * 1024;
-  const std::uint32_t fixed = kDecodeWarps * 32 * slot_stride * 4 + fused_stages_b(m_pad) * m_pad * 128 + 1024;
+  const std::uint32_t fixed = warp_smem + fused_stages_b(m_pad) * m_pad * 128 + 1024;
   const std::uint32_t s = fixed < budget ? (budget - fixed) / kTileElems : 0;
   return s > kMaxStagesA ? kMaxStagesA : s;
 }
 
-std::uint32_t fused_smem_bytes(std::uint32_t m_pad, std::uint32_t stages_a, std::uint32_t slot_stride) {
-  return 1024 + stages_a * kTileElems + fused_stages_b(m_pad) * m_pad * 128 + kDecodeWarps * 32 * slot_stride * 4;
+std::uint32_t fused_smem_bytes(std::uint32_t m_pad, std::uint32_t stages_a, std::uint32_t warp_smem) {
+  return 1024 + stages_a * kTileElems + fused_stages_b(m_pad) * m_pad * 128 + warp_smem;
 }
 
-template <int LW, int SLOT_STRIDE>
+template <int LW, int ROWS>
 cudaError_t launch_lw(const FusedArgs& args, std::uint32_t n_cta, cudaStream_t s) {
-  const std::uint32_t smem = fused_smem_bytes(args.m_pad, args.stages_a, SLOT_STRIDE);
-  cudaError_t e = cudaFuncSetAttribute(fused_gemm_kernel<LW, SLOT_STRIDE>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  const std::uint32_t smem = fused_smem_bytes(args.m_pad, args.stages_a, warps_smem<LW, ROWS>());
+  cudaError_t e = cudaFuncSetAttribute(fused_gemm_kernel<LW, ROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  fused_gemm_kernel<LW, SLOT_STRIDE><<<n_cta, kThreadsF, smem, s>>>(args);
+  fused_gemm_kernel<LW, ROWS><<<n_cta, (decode_warps<LW, ROWS>() + 1) * 32, smem, s>>>(args);
   return cudaGetLastError();
 }
 
@@ -498,10 +499,8 @@ cudaError_t launch_fused_gemm(const FusedArgs& args, std::uint32_t n_cta, cudaSt
   const unsigned blocks = static_cast<unsigned>(std::min<std::uint64_t>((chunks + 255) / 256, 4 * 148));
   x_tiles_kernel<<<blocks, 256, 0, s>>>(args.x, const_cast<std::uint8_t*>(args.xt), args.m, args.m_pad, args.k);
   if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) return e;
-  const int lw = fused_lane_windows(args.w.T, args.w.lmin);
-  if (lw == 8) return launch_lw<8, 33>(args, n_cta, s);
-  return fused_slot_stride(args.w.T, args.w.lmin) == 17 ? launch_lw<4, 17>(args, n_cta, s)
-                                                        : launch_lw<4, 33>(args, n_cta, s);
+  if (fused_lane_windows(args.w.T, args.w.lmin) == 8) return launch_lw<8, 33>(args, n_cta, s);
+  return args.w.lmin >= 2 ? launch_lw<4, 17>(args, n_cta, s) : launch_lw<4, 33>(args, n_cta, s);
 }
 
 }  // namespace ecf8::dev

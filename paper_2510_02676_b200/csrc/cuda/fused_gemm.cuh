@@ -39,12 +39,12 @@ struct FusedArgs {
 };
 
 // Windows per decode lane for a tiled weight (4 or 8; 0 = unsupported) and
-// the decode slot stride in words (fused_gemm.cu).
+// the shared memory of one decode warp's pipeline (fused_gemm.cu).
 int fused_lane_windows(std::uint32_t T, std::uint32_t lmin);
-std::uint32_t fused_slot_stride(std::uint32_t T, std::uint32_t lmin);
+std::uint32_t fused_warp_smem(std::uint32_t T, std::uint32_t lmin);
 std::uint32_t fused_stages_b(std::uint32_t m_pad);
-std::uint32_t fused_stages_a(std::uint32_t m_pad, std::uint32_t slot_stride);
-std::uint32_t fused_smem_bytes(std::uint32_t m_pad, std::uint32_t stages_a, std::uint32_t slot_stride);
+std::uint32_t fused_stages_a(std::uint32_t m_pad, std::uint32_t warp_smem);
+std::uint32_t fused_smem_bytes(std::uint32_t m_pad, std::uint32_t stages_a, std::uint32_t warp_smem);
 cudaError_t launch_fused_gemm(const FusedArgs& args, std::uint32_t n_cta, cudaStream_t s);
 
 }  // namespace ecf8::dev
