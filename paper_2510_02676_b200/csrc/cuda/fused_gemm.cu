@@ -49,10 +49,14 @@ namespace ecf8::dev {
 
 namespace {
 
-// Decode warps per CTA: 20, or 12 when a lane's run can hold 64-symbol
+#ifndef ECF8_FUSED_WARPS
+#define ECF8_FUSED_WARPS 22
+#endif
+// Decode warps per CTA: 22 (measured: 16 -> 211, 20 -> 196, 22 -> 186, 24 -> 187 us
+// on a 28672x8192 weight at m = 1), or 12 when a lane's run can hold 64-symbol
 // windows (1-bit codes) and its pipeline state doubles.
 template <int LW, int ROWS>
-constexpr int decode_warps() { return (LW == 4 && ROWS > 17) ? 12 : 20; }
+constexpr int decode_warps() { return (LW == 4 && ROWS > 17) ? 12 : ECF8_FUSED_WARPS; }
 constexpr std::uint32_t kTileElems = 128 * 128;  // one K tile of A (bytes)
 
 __shared__ Tables g_tbf;
