@@ -251,7 +251,7 @@ def load_peaks():
 
 
 def kernel_name():
-    nw = os.environ.get("ECF8_WARPS", "22")
+    nw = os.environ.get("ECF8_WARPS", "24")
     return "decode_kernel<4,16,3>" if os.environ.get("ECF8_NO_WARP_KERNEL") == "1" else f"decode_warp_kernel<{nw}>"
 
 

@@ -208,15 +208,15 @@ __global__ void stream_fence_kernel() {}
 
 }  // namespace
 
-// Warps per CTA: 22 (default; 22 x 8.7 KB of warp state + 29 KB of tables,
-// <= 93 registers), 20 or 16 (ECF8_WARPS).  Measured (8 x 14336x4096, T 256):
-// 22 warps 3292 GB/s, 20 warps 3206 GB/s.
+// Warps per CTA: 24 (default; 24 x 8.2 KB of warp state + 29 KB of tables,
+// <= 85 registers), 22 or 20 (ECF8_WARPS).  Measured (8 x 14336x4096, T 256):
+// 24 warps 3532 GB/s, 22 warps 3448 GB/s, 20 warps 3206 GB/s.
 cudaError_t launch_decode_warp(const LaunchArgs& args, cudaStream_t s) {
   static const int nw = [] {
     const char* e = std::getenv("ECF8_WARPS");
-    return e ? std::atoi(e) : 22;
+    return e ? std::atoi(e) : 24;
   }();
-  return nw == 16 ? launch_nw<16>(args, s) : nw == 22 ? launch_nw<22>(args, s) : launch_nw<20>(args, s);
+  return nw == 20 ? launch_nw<20>(args, s) : nw == 22 ? launch_nw<22>(args, s) : launch_nw<24>(args, s);
 }
 
 cudaError_t launch_verify_gaps(const TensorDesc& d, std::uint32_t* tile_ok, cudaStream_t s) {

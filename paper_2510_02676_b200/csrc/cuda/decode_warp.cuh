@@ -167,17 +167,14 @@ __device__ __forceinline__ LaneRun warp_decode_scan(const WarpInT<LW>& in, std::
 // ---- compaction + write-back (shared by the decode kernel and the fused GEMM)
 
 // Per-warp shared memory of the tile pipeline: the lanes' nibble slots
-// (interleaved word by word: word j of lane L at slot[32 j + L]), the staging
-// tile the runs are compacted into, and the lanes' run bounds / partial head
-// words.  After compaction the slots hold the tile's sign/mantissa bytes.
+// (interleaved word by word: word j of lane L at slot[32 j + L]) and the
+// staging tile the runs are compacted into.  After compaction the slots hold
+// the tile's sign/mantissa bytes.
 template <int SLOT_ROWS, int STAGE_WORDS>
 struct WarpPipeSmem {
   static constexpr int kSlotRows = SLOT_ROWS;
   std::uint32_t slot[SLOT_ROWS * 32];
   alignas(16) std::uint32_t stage[STAGE_WORDS];
-  std::uint32_t rs[32];
-  std::uint32_t re[32];
-  std::uint32_t head[32];
 };
 
 // Compact the lanes' runs (slot nibbles, LaneRun from warp_decode_scan) into
@@ -206,8 +203,6 @@ __device__ __forceinline__ void compact_write(const TensorDesc& d, std::uint64_t
   const std::uint32_t full_lo = (off + 15) >> 4, full_hi = data_end >> 4;
   const std::uint32_t nfull = full_hi > full_lo ? full_hi - full_lo : 0u;
   __syncwarp();  // previous tile's write-back is done with the staging and the slots' packed bytes
-  ws.rs[lane] = d0;
-  ws.re[lane] = dend;
 
   // ---- move my nibbles to their final place; publish partial words
   std::uint32_t headv = 0, tailv = 0;
@@ -235,7 +230,6 @@ __device__ __forceinline__ void compact_write(const TensorDesc& d, std::uint64_t
       else tailv = v;
     }
   }
-  ws.head[lane] = headv;
   __syncwarp();
 
   // ---- the slots are free: sign/mantissa bytes of the full chunks into them
@@ -252,27 +246,27 @@ __device__ __forceinline__ void compact_write(const TensorDesc& d, std::uint64_t
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
 
-  // ---- owners assemble words shared between lanes
-  if (cc) {
-    const bool start_owner = (f4 == 0 || d0 == off) && !(f4 == 0 && (fw < lw || lastn == 8));
-    const bool tail_owner = fw != lw && lastn != 8;
-#pragma unroll
-    for (int pass = 0; pass < 2; ++pass) {
-      if (pass == 0 ? !start_owner : !tail_owner) continue;
-      const std::uint32_t k = pass == 0 ? fw : lw;
-      std::uint32_t v = pass == 0 ? headv : tailv;
-      const std::uint32_t wend = min(8 * k + 8, data_end);
-      std::uint32_t covered = dend;
-      for (int j = lane + 1; covered < wend && j < 32; ++j) {
-        const std::uint32_t rj = ws.rs[j], ej = ws.re[j];
-        if (ej > rj) {
-          v |= ws.head[j];
-          covered = ej;
-        }
-      }
-      ws.stage[k] = v;
+  // ---- owners assemble words shared between lanes: the start owner of my
+  // first word / my tail word OR in the partial head words of the following
+  // lanes until the word is covered (lane bounds and heads by shuffle; runs
+  // are contiguous, so this takes one or two steps)
+  const bool start_owner = cc && (f4 == 0 || d0 == off) && !(f4 == 0 && (fw < lw || lastn == 8));
+  const bool tail_owner = cc && fw != lw && lastn != 8;
+  std::uint32_t vs = headv, vt = tailv, cov_s = dend, cov_t = dend;
+  const std::uint32_t wend_s = min(8 * fw + 8, data_end), wend_t = min(8 * lw + 8, data_end);
+  for (std::uint32_t o = 1; o < 32; ++o) {
+    const bool need_s = start_owner && cov_s < wend_s, need_t = tail_owner && cov_t < wend_t;
+    if (!__any_sync(0xffffffffu, need_s || need_t)) break;
+    const std::uint32_t rj = __shfl_down_sync(0xffffffffu, d0, o);
+    const std::uint32_t ej = __shfl_down_sync(0xffffffffu, cc ? dend : d0, o);
+    const std::uint32_t hj = __shfl_down_sync(0xffffffffu, headv, o);
+    if (static_cast<std::uint32_t>(lane) + o < 32 && ej > rj) {
+      if (need_s) vs |= hj, cov_s = ej;
+      if (need_t) vt |= hj, cov_t = ej;
     }
   }
+  if (start_owner) ws.stage[fw] = vs;
+  if (tail_owner) ws.stage[lw] = vt;
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncwarp();
 

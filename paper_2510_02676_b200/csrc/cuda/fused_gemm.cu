@@ -50,9 +50,9 @@ namespace ecf8::dev {
 namespace {
 
 #ifndef ECF8_FUSED_WARPS
-#define ECF8_FUSED_WARPS 22
+#define ECF8_FUSED_WARPS 24
 #endif
-// Decode warps per CTA: 22 (measured: 16 -> 211, 20 -> 196, 22 -> 186, 24 -> 187 us
+// Decode warps per CTA: 24 (measured: 16 -> 211, 20 -> 196, 22 -> 190, 24 -> 184, 26 -> 197 us
 // on a 28672x8192 weight at m = 1), or 12 when a lane's run can hold 64-symbol
 // windows (1-bit codes) and its pipeline state doubles.
 template <int LW, int ROWS>
