@@ -52,11 +52,22 @@ namespace {
 #ifndef ECF8_FUSED_WARPS
 #define ECF8_FUSED_WARPS 24
 #endif
-// Decode warps per CTA: 24 (measured: 16 -> 211, 20 -> 196, 22 -> 190, 24 -> 184, 26 -> 197 us
-// on a 28672x8192 weight at m = 1), or 12 when a lane's run can hold 64-symbol
-// windows (1-bit codes) and its pipeline state doubles.
-template <int LW, int ROWS>
-constexpr int decode_warps() { return (LW == 4 && ROWS > 17) ? 12 : ECF8_FUSED_WARPS; }
+// Decode warps per CTA.  Half-size warp tiles (LW 4, 17 slot rows): 24
+// (measured on a 28672x8192 weight at m = 1: 16 -> 211, 20 -> 196, 22 -> 190,
+// 24 -> 184, 26 -> 197 us).  For m > 128 (WIDE) one 32 KB X stage keeps room
+// for three A stages: 24 warps / 1 X stage 236 us, 16 / 2 264 us, 22 / 2 287
+// us (two A stages) at m = 256.  Lanes holding 256 symbols (LW 8, or
+// 64-symbol windows): 12.
+#ifndef ECF8_FUSED_WIDE_WARPS
+#define ECF8_FUSED_WIDE_WARPS 24
+#endif
+#ifndef ECF8_FUSED_WIDE_XSTAGES
+#define ECF8_FUSED_WIDE_XSTAGES 1
+#endif
+template <int LW, int ROWS, bool WIDE>
+constexpr int decode_warps() {
+  return ROWS > 17 ? 12 : (WIDE ? ECF8_FUSED_WIDE_WARPS : ECF8_FUSED_WARPS);
+}
 constexpr std::uint32_t kTileElems = 128 * 128;  // one K tile of A (bytes)
 
 __shared__ Tables g_tbf;
@@ -265,10 +276,10 @@ __device__ __forceinline__ void ring_tile(const TensorDesc& d, const WarpInT<LW>
 template <int LW, int SLOT_ROWS>
 using FusedWarpSmem = WarpPipeSmem<SLOT_ROWS, 32 * LW * (SLOT_ROWS > 17 && LW == 4 ? 64 : 32) / 8 + 8>;
 
-template <int LW, int SLOT_ROWS>
-__global__ void __launch_bounds__((decode_warps<LW, SLOT_ROWS>() + 1) * 32, 1) fused_gemm_kernel(const FusedArgs args) {
+template <int LW, int SLOT_ROWS, bool WIDE>
+__global__ void __launch_bounds__((decode_warps<LW, SLOT_ROWS, WIDE>() + 1) * 32, 1) fused_gemm_kernel(const FusedArgs args) {
   using WSm = FusedWarpSmem<LW, SLOT_ROWS>;
-  constexpr int kDecodeWarps = decode_warps<LW, SLOT_ROWS>();
+  constexpr int kDecodeWarps = decode_warps<LW, SLOT_ROWS, WIDE>();
   constexpr int kThreadsF = (kDecodeWarps + 1) * 32;
   constexpr int kCtrlWarp = kDecodeWarps;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -450,11 +461,11 @@ __global__ void x_tiles_kernel(const std::uint8_t* __restrict__ x, std::uint8_t*
 
 }  // namespace
 
-std::uint32_t fused_stages_b(std::uint32_t m_pad) { return m_pad > 128 ? 1u : 2u; }
+std::uint32_t fused_stages_b(std::uint32_t m_pad) { return m_pad > 128 ? ECF8_FUSED_WIDE_XSTAGES : 2u; }
 
 // Decode-warp geometry for a tiled weight:
 //   Lmin >= 2, T <= 128: 4 windows per lane, 17 slot rows -- half-size warp
-//       tiles keep the 20 decode warps within ~4 K tiles of the MMA;
+//       tiles keep the decode warps within ~4 K tiles of the MMA;
 //   Lmin >= 2, T == 256: 8 windows per lane, 33 slot rows;
 //   Lmin == 1, T <= 128: 4 windows of up to 64 symbols, 33 slot rows.
 int fused_lane_windows(std::uint32_t T, std::uint32_t lmin) {
@@ -464,15 +475,17 @@ int fused_lane_windows(std::uint32_t T, std::uint32_t lmin) {
   return 0;
 }
 
-template <int LW, int ROWS>
+template <int LW, int ROWS, bool WIDE>
 constexpr std::uint32_t warps_smem() {
-  return static_cast<std::uint32_t>(decode_warps<LW, ROWS>() * sizeof(FusedWarpSmem<LW, ROWS>));
+  return static_cast<std::uint32_t>(decode_warps<LW, ROWS, WIDE>() * sizeof(FusedWarpSmem<LW, ROWS>));
 }
 
 // All decode warps' pipeline state.
-std::uint32_t fused_warp_smem(std::uint32_t T, std::uint32_t lmin) {
-  if (fused_lane_windows(T, lmin) == 8) return warps_smem<8, 33>();
-  return (lmin >= 2) ? warps_smem<4, 17>() : warps_smem<4, 33>();
+std::uint32_t fused_warp_smem(std::uint32_t T, std::uint32_t lmin, std::uint32_t m_pad) {
+  const bool wide = m_pad > 128;
+  if (fused_lane_windows(T, lmin) == 8) return wide ? warps_smem<8, 33, true>() : warps_smem<8, 33, false>();
+  if (lmin >= 2) return wide ? warps_smem<4, 17, true>() : warps_smem<4, 17, false>();
+  return wide ? warps_smem<4, 33, true>() : warps_smem<4, 33, false>();
 }
 
 std::uint32_t fused_stages_a(std::uint32_t m_pad, std::uint32_t warp_smem) {
@@ -488,14 +501,20 @@ std::uint32_t fused_smem_bytes(std::uint32_t m_pad, std::uint32_t stages_a, std:
   return 1024 + stages_a * kTileElems + fused_stages_b(m_pad) * m_pad * 128 + warp_smem;
 }
 
-template <int LW, int ROWS>
+template <int LW, int ROWS, bool WIDE>
 cudaError_t launch_lw(const FusedArgs& args, std::uint32_t n_cta, cudaStream_t s) {
-  const std::uint32_t smem = fused_smem_bytes(args.m_pad, args.stages_a, warps_smem<LW, ROWS>());
-  cudaError_t e = cudaFuncSetAttribute(fused_gemm_kernel<LW, ROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
+  const std::uint32_t smem = fused_smem_bytes(args.m_pad, args.stages_a, warps_smem<LW, ROWS, WIDE>());
+  cudaError_t e = cudaFuncSetAttribute(fused_gemm_kernel<LW, ROWS, WIDE>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  fused_gemm_kernel<LW, ROWS><<<n_cta, (decode_warps<LW, ROWS>() + 1) * 32, smem, s>>>(args);
+  fused_gemm_kernel<LW, ROWS, WIDE><<<n_cta, (decode_warps<LW, ROWS, WIDE>() + 1) * 32, smem, s>>>(args);
   return cudaGetLastError();
+}
+
+template <bool WIDE>
+cudaError_t launch_geometry(const FusedArgs& args, std::uint32_t n_cta, cudaStream_t s) {
+  if (fused_lane_windows(args.w.T, args.w.lmin) == 8) return launch_lw<8, 33, WIDE>(args, n_cta, s);
+  return args.w.lmin >= 2 ? launch_lw<4, 17, WIDE>(args, n_cta, s) : launch_lw<4, 33, WIDE>(args, n_cta, s);
 }
 
 cudaError_t launch_fused_gemm(const FusedArgs& args, std::uint32_t n_cta, cudaStream_t s) {
@@ -503,8 +522,7 @@ cudaError_t launch_fused_gemm(const FusedArgs& args, std::uint32_t n_cta, cudaSt
   const unsigned blocks = static_cast<unsigned>(std::min<std::uint64_t>((chunks + 255) / 256, 4 * 148));
   x_tiles_kernel<<<blocks, 256, 0, s>>>(args.x, const_cast<std::uint8_t*>(args.xt), args.m, args.m_pad, args.k);
   if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) return e;
-  if (fused_lane_windows(args.w.T, args.w.lmin) == 8) return launch_lw<8, 33>(args, n_cta, s);
-  return args.w.lmin >= 2 ? launch_lw<4, 17>(args, n_cta, s) : launch_lw<4, 33>(args, n_cta, s);
+  return args.m_pad > 128 ? launch_geometry<true>(args, n_cta, s) : launch_geometry<false>(args, n_cta, s);
 }
 
 }  // namespace ecf8::dev

@@ -31,7 +31,7 @@ struct FusedArgs {
   std::uint32_t n, k;
   std::uint32_t split_k;
   std::uint32_t stages_a;
-  std::uint32_t stages_b;   // X ring: 2, or 1 when m_pad > 128
+  std::uint32_t stages_b;   // X ring stages (2)
   std::uint32_t tmem_cols;  // allocation: 2 accumulators of acc_cols
   std::uint32_t acc_cols;   // power of two >= max(32, m_pad)
   std::uint32_t w_fmt;       // 0 E4M3, 1 E5M2
@@ -41,7 +41,7 @@ struct FusedArgs {
 // Windows per decode lane for a tiled weight (4 or 8; 0 = unsupported) and
 // the shared memory of one decode warp's pipeline (fused_gemm.cu).
 int fused_lane_windows(std::uint32_t T, std::uint32_t lmin);
-std::uint32_t fused_warp_smem(std::uint32_t T, std::uint32_t lmin);
+std::uint32_t fused_warp_smem(std::uint32_t T, std::uint32_t lmin, std::uint32_t m_pad);
 std::uint32_t fused_stages_b(std::uint32_t m_pad);
 std::uint32_t fused_stages_a(std::uint32_t m_pad, std::uint32_t warp_smem);
 std::uint32_t fused_smem_bytes(std::uint32_t m_pad, std::uint32_t stages_a, std::uint32_t warp_smem);

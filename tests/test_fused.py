@@ -60,3 +60,41 @@ def test_fused_gemm_matches_fp8_gemm_on_reference_decoded_weights(orc, fmt, m, n
     tol = 1e-3 * want.abs().max().item() + 1e-3
     err = (y - want).abs().max().item()
     assert err <= tol, f"max err {err} > {tol} (split_k={lin.split_k})"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("T", [8, 64, 256])
+@pytest.mark.parametrize("m", [1, 200])
+def test_fused_gemm_decode_geometries(orc, T, m):
+    # every decode-warp geometry of the fused kernel: 4-window lanes (T <= 128),
+    # 8-window lanes (T = 256), 24 or 16 decode warps (m <= 128 / m > 128)
+    from paper_2510_02676_b200.fused import FusedLinear
+
+    n, k = 512, 1024
+    w = codec.synth(1.8, 0.05, n * k, 900 + T, fmt="e4m3").reshape(n, k)
+    lin = FusedLinear(w, "e4m3", threads_per_block=T)
+    torch.manual_seed(T + m)
+    x8 = (torch.randn(m, k, device="cuda") * 4).to(torch.float8_e4m3fn)
+    y = lin(x8, scale=0.5)
+    torch.cuda.synchronize()
+    want, wd = ref_gemm(orc, lin, x8, 0.5, "e4m3")
+    assert np.array_equal(wd, w)
+    tol = 1e-3 * want.abs().max().item() + 1e-3
+    assert (y - want).abs().max().item() <= tol
+
+
+@pytest.mark.gpu
+def test_back_to_back_decodes_into_one_buffer():
+    # consecutive decodes overlap by programmatic dependent launch; the second
+    # one's stores must still land after the first one's
+    from paper_2510_02676_b200.device import Batch, DeviceTensor
+
+    xs = [codec.synth(1.8, 0.05, 3_000_000, 40 + i) for i in range(3)]
+    ds = [DeviceTensor(codec.encode_tensor(x, 256)) for x in xs]
+    out = torch.empty(3_000_000, dtype=torch.uint8, device="cuda")
+    bs = [Batch([d], [out]) for d in ds]
+    for _ in range(4):
+        for b in bs:
+            b.decode()
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), xs[-1])
