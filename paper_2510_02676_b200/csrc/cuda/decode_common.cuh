@@ -151,33 +151,32 @@ __device__ __forceinline__ bool decode_window_fast(std::uint32_t w0, std::uint32
                                                    std::uint32_t smask, Sink& sink) {
   std::uint32_t hi = __funnelshift_l(w1, w0, gap);
   std::uint32_t lo = __funnelshift_l(w2, w1, gap);
-  std::uint32_t p = gap, flags = 0;
+  std::uint32_t p = gap;  // + kSlowFlag once a flagged entry was met (ends the loops)
   while (p < 32) {
     const std::uint32_t e = lds32(fast + ((hi >> (kFastShift - 2)) & ~3u));
-    flags |= e;
     sink.put(e >> 12, (e >> 5) & 31);
     hi = __funnelshift_l(lo, hi, e);  // shift amount = e & 31 = bits consumed
     lo = __funnelshift_l(0u, lo, e);
-    p += e & 31;
+    p += e & (31u | kSlowFlag);
   }
+  if (p >= 64) return false;
   hi = __funnelshift_l(w2, w1, p - 32);  // p in [32, 44): window = bits [p, p + 64)
   lo = __funnelshift_l(w3, w2, p - 32);
   for (;;) {
     const std::uint32_t idx = hi >> kFastShift;
     const std::uint32_t e = lds32(fast + 4 * idx);
-    flags |= e;
+    if (e & kSlowFlag) return false;
     const std::uint32_t b = e & 31, r = 64 - p;
     if (b >= r) {
       const std::uint32_t k4 = 4 * __popc(lds16(smask + 2 * idx) & ((1u << r) - 1));
       sink.put((e >> 12) & ((1u << k4) - 1), k4);
-      break;
+      return true;
     }
     sink.put(e >> 12, (e >> 5) & 31);
     hi = __funnelshift_l(lo, hi, e);
     lo = __funnelshift_l(0u, lo, e);
     p += b;
   }
-  return !(flags & kSlowFlag);
 }
 
 // Continuous fast walk over a lane's n consecutive windows (n <= 8; w holds
@@ -195,37 +194,44 @@ __device__ __forceinline__ bool decode_lane_continuous(const std::uint32_t (&w)[
                                                        Sink& sink) {
   std::uint32_t hi = __funnelshift_l(w[1], w[0], gap);
   std::uint32_t lo = __funnelshift_l(w[2], w[1], gap);
-  std::uint32_t p = gap, flags = 0;  // p: bit position of hi's MSB within the current 32-bit phase
+  // p: bit position of hi's MSB within the current 32-bit phase.  A flagged
+  // entry adds kSlowFlag to it, which ends this and every later phase loop
+  // (p stays >= 32) -- no separate flag accumulator in the hot loop.
+  std::uint32_t p = gap;
   const std::uint32_t last = 2 * n - 1;
 #pragma unroll
   for (std::uint32_t k = 0; k < 2 * NW; ++k) {
     if (k == last) {
       // final half window: whole entries while they end before bit 32, then
       // the symbols that start before it (start mask + popcount)
-      for (;;) {
-        const std::uint32_t idx = hi >> kFastShift;
-        const std::uint32_t e = lds32(fast + 4 * idx);
-        flags |= e;
-        const std::uint32_t b = e & 31, r = 32 - p;
-        if (b >= r) {
-          const std::uint32_t k4 = 4 * __popc(lds16(smask + 2 * idx) & ((1u << r) - 1));
-          sink.put((e >> 12) & ((1u << k4) - 1), k4);
-          break;
+      if (p < 32) {
+        for (;;) {
+          const std::uint32_t idx = hi >> kFastShift;
+          const std::uint32_t e = lds32(fast + 4 * idx);
+          if (e & kSlowFlag) {
+            p = kSlowFlag;
+            break;
+          }
+          const std::uint32_t b = e & 31, r = 32 - p;
+          if (b >= r) {
+            const std::uint32_t k4 = 4 * __popc(lds16(smask + 2 * idx) & ((1u << r) - 1));
+            sink.put((e >> 12) & ((1u << k4) - 1), k4);
+            break;
+          }
+          sink.put(e >> 12, (e >> 5) & 31);
+          hi = __funnelshift_l(lo, hi, e);
+          lo = __funnelshift_l(0u, lo, e);
+          p += b;
         }
-        sink.put(e >> 12, (e >> 5) & 31);
-        hi = __funnelshift_l(lo, hi, e);
-        lo = __funnelshift_l(0u, lo, e);
-        p += b;
       }
       break;
     }
     while (p < 32) {
       const std::uint32_t e = lds32(fast + ((hi >> (kFastShift - 2)) & ~3u));
-      flags |= e;
       sink.put(e >> 12, (e >> 5) & 31);
       hi = __funnelshift_l(lo, hi, e);
       lo = __funnelshift_l(0u, lo, e);
-      p += e & 31;
+      p += e & (31u | kSlowFlag);
     }
     p -= 32;  // next phase: hi:lo = bits [32(k+1) + p, +64)
     if (k + 3 < 2 * NW + 2) {
@@ -233,7 +239,7 @@ __device__ __forceinline__ bool decode_lane_continuous(const std::uint32_t (&w)[
       lo = __funnelshift_l(w[k + 3], w[k + 2], p);
     }
   }
-  return !(flags & kSlowFlag);
+  return p < 32;
 }
 
 // Where window (w0..w3, gap)'s reference walk stops: the start of the first
