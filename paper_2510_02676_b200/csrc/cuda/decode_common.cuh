@@ -17,10 +17,19 @@ constexpr int kFastShift = 32 - kFastBits;
 // the fast table whose first word is not resolvable from kFastBits bits are
 // rewritten on staging to the "flagged" form below.
 struct Tables {
-  std::uint32_t fast[kFastEntries];
   std::uint16_t smask[kFastEntries];
   std::uint8_t cascade[18 * 256];
+  std::uint32_t fast[kFastEntries];  // last: decode_warp.cu places it at a 16 KB-aligned shared address
 };
+
+// Shared address of the fast-table entry for the next kFastBits bits of hi.
+// OR_BASE: the table sits at a 16 KB-aligned address, so base | offset
+// (one LOP3) replaces base + offset.
+template <bool OR_BASE>
+__device__ __forceinline__ std::uint32_t fast_entry_addr(std::uint32_t fast, std::uint32_t hi) {
+  const std::uint32_t off = (hi >> (kFastShift - 2)) & ~3u;
+  return OR_BASE ? (fast | off) : (fast + off);
+}
 
 // A fast entry with n == 0 is staged as: advance 1 bit, emit nothing, set
 // kSlowFlag.  The fast walk then runs branch-free; a window that met such an
@@ -145,7 +154,7 @@ __device__ __forceinline__ void decode_window_exact(std::uint32_t w0, std::uint3
 // and then exactly the symbols that start before it (start-bit mask +
 // popcount, the codec.cpp:143-160 rule).
 // fast = shared address of tb.fast, smask = shared address of tb.smask.
-template <class Sink>
+template <class Sink, bool OR_BASE = false>
 __device__ __forceinline__ bool decode_window_fast(std::uint32_t w0, std::uint32_t w1, std::uint32_t w2,
                                                    std::uint32_t w3, std::uint32_t gap, std::uint32_t fast,
                                                    std::uint32_t smask, Sink& sink) {
@@ -153,7 +162,7 @@ __device__ __forceinline__ bool decode_window_fast(std::uint32_t w0, std::uint32
   std::uint32_t lo = __funnelshift_l(w2, w1, gap);
   std::uint32_t p = gap;  // + kSlowFlag once a flagged entry was met (ends the loops)
   while (p < 32) {
-    const std::uint32_t e = lds32(fast + ((hi >> (kFastShift - 2)) & ~3u));
+    const std::uint32_t e = lds32(fast_entry_addr<OR_BASE>(fast, hi));
     sink.put(e >> 12, (e >> 5) & 31);
     hi = __funnelshift_l(lo, hi, e);  // shift amount = e & 31 = bits consumed
     lo = __funnelshift_l(0u, lo, e);
@@ -164,7 +173,7 @@ __device__ __forceinline__ bool decode_window_fast(std::uint32_t w0, std::uint32
   lo = __funnelshift_l(w3, w2, p - 32);
   for (;;) {
     const std::uint32_t idx = hi >> kFastShift;
-    const std::uint32_t e = lds32(fast + 4 * idx);
+    const std::uint32_t e = lds32(fast_entry_addr<OR_BASE>(fast, hi));
     if (e & kSlowFlag) return false;
     const std::uint32_t b = e & 31, r = 64 - p;
     if (b >= r) {
@@ -188,7 +197,7 @@ __device__ __forceinline__ bool decode_window_fast(std::uint32_t w0, std::uint32
 // for every encoder-produced stream; the upload-time gap check
 // (verify_gaps_kernel) establishes it per 256-window tile.  Returns false if
 // a flagged entry was met (the caller redoes the windows exactly).
-template <int NW, class Sink>
+template <int NW, class Sink, bool OR_BASE = false>
 __device__ __forceinline__ bool decode_lane_continuous(const std::uint32_t (&w)[2 * NW + 2], std::uint32_t n,
                                                        std::uint32_t gap, std::uint32_t fast, std::uint32_t smask,
                                                        Sink& sink) {
@@ -207,7 +216,7 @@ __device__ __forceinline__ bool decode_lane_continuous(const std::uint32_t (&w)[
       if (p < 32) {
         for (;;) {
           const std::uint32_t idx = hi >> kFastShift;
-          const std::uint32_t e = lds32(fast + 4 * idx);
+          const std::uint32_t e = lds32(fast_entry_addr<OR_BASE>(fast, hi));
           if (e & kSlowFlag) {
             p = kSlowFlag;
             break;
@@ -227,7 +236,7 @@ __device__ __forceinline__ bool decode_lane_continuous(const std::uint32_t (&w)[
       break;
     }
     while (p < 32) {
-      const std::uint32_t e = lds32(fast + ((hi >> (kFastShift - 2)) & ~3u));
+      const std::uint32_t e = lds32(fast_entry_addr<OR_BASE>(fast, hi));
       sink.put(e >> 12, (e >> 5) & 31);
       hi = __funnelshift_l(lo, hi, e);
       lo = __funnelshift_l(0u, lo, e);
@@ -277,12 +286,12 @@ __device__ __forceinline__ std::uint32_t window_end(std::uint32_t w0, std::uint3
   }
 }
 
-template <class Sink>
+template <bool OR_BASE = false, class Sink>
 __device__ __forceinline__ void decode_window(std::uint32_t w0, std::uint32_t w1, std::uint32_t w2,
                                               std::uint32_t w3, std::uint32_t gap, const Tables& tb,
                                               std::uint32_t len_off, Sink& sink) {
   const Sink saved = sink;
-  if (!decode_window_fast(w0, w1, w2, w3, gap, smem_addr(tb.fast), smem_addr(tb.smask), sink)) {
+  if (!decode_window_fast<Sink, OR_BASE>(w0, w1, w2, w3, gap, smem_addr(tb.fast), smem_addr(tb.smask), sink)) {
     sink = saved;
     decode_window_exact(w0, w1, w2, w3, gap, tb, len_off, sink);
   }

@@ -44,15 +44,20 @@ namespace {
 // holds 8192 nibbles + the 16-byte alignment offset.
 using WarpSmem = WarpPipeSmem<33, 32 * kSlotWords + 8>;
 
-// Static shared memory: the decode tables, the tile queue and the current
-// segment's descriptor (read field by field where used: a register copy
-// would pin ~30 registers for the whole tile loop).
+// Static shared memory: the tile queue, the current segment's descriptor
+// (read field by field where used: a register copy would pin ~30 registers
+// for the whole tile loop) and the decode tables, laid out so that the fast
+// table starts at shared address 0x4000 (the CTA window begins 1 KB in, after
+// the reserved area): a probe address is then base | offset.  The kernel
+// traps if the toolchain ever places it elsewhere.
 struct StaticSmem {
-  Tables tb;
   unsigned next_tile;  // CTA-local work queue of the current segment (relative)
-  TensorDesc desc;
+  TensorDesc desc;     // the current segment's tensor
+  unsigned char pad[0x4000 - 0x400 - offsetof(Tables, fast) - 8 - sizeof(TensorDesc)];
+  Tables tb;
 };
-__shared__ __align__(16) StaticSmem g_s;
+static_assert(offsetof(StaticSmem, tb) + offsetof(Tables, fast) == 0x4000 - 0x400, "fast table offset");
+__shared__ __align__(1024) StaticSmem g_s;
 #define g_tb g_s.tb
 #define g_next_tile g_s.next_tile
 #define g_desc g_s.desc
@@ -81,8 +86,8 @@ __device__ __forceinline__ void warp_tile(const TensorDesc& d, const WarpIn& in,
                                           std::uint32_t len_off, WarpSmem& ws, int lane) {
   // slots interleaved word by word (word j of lane L at slot[32 j + L]): the
   // lanes' slot stores and reads hit 32 different banks
-  const LaneRun run = warp_decode_scan<kLaneWin, 128>(in, log2T, len_off, g_tb, smem_addr(ws.slot + lane), lane,
-                                                      tile_verified(d, in, log2T));
+  const LaneRun run = warp_decode_scan<kLaneWin, 128, true>(in, log2T, len_off, g_tb, smem_addr(ws.slot + lane),
+                                                            lane, tile_verified(d, in, log2T));
   GlobalOut out{d.out + ((in.A & ~std::uint64_t{15}) - d.out_offset)};
   compact_write<kWbUnroll>(d, in.A, in.E, run, ws, lane, out);
 }
@@ -114,6 +119,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_warp_kernel(const LaunchArg
     __syncthreads();
     const TensorDesc& d = g_desc;
     const std::uint32_t log2T = 31 - __clz(d.T);
+    if (threadIdx.x == 0 && (smem_addr(g_tb.fast) & 0x3FFFu)) __trap();  // base | offset needs 16 KB alignment
     stage_tables(d, g_tb, threadIdx.x, NW * 32);
     const std::uint32_t len_off = (d.n_luts - 1) << 8;
     if (threadIdx.x == 0) g_next_tile = NW;

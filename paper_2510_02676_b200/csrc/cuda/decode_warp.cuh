@@ -107,7 +107,7 @@ struct LaneRun {
 // upload-time gap check): one continuous walk over the lane's windows;
 // otherwise, or when the walk met a flagged entry, window by window with the
 // reference's per-window semantics (fast table, exact walk where flagged).
-template <int LW, int WS = 4>
+template <int LW, int WS = 4, bool OR_BASE = false>
 __device__ __forceinline__ LaneRun warp_decode_scan(const WarpInT<LW>& in, std::uint32_t log2T,
                                                    std::uint32_t len_off, const Tables& tb, std::uint32_t slot_base,
                                                    int lane, bool verified = false) {
@@ -128,7 +128,8 @@ __device__ __forceinline__ LaneRun warp_decode_scan(const WarpInT<LW>& in, std::
     if (verified) {
       const SlotSinkT<WS> saved = sink;
       const std::uint32_t gap0 = (in.gaps >> 4) & 15u;  // window 0: high nibble of byte 0
-      windowed = !decode_lane_continuous<LW>(w, n, gap0, smem_addr(tb.fast), smem_addr(tb.smask), sink);
+      windowed = !decode_lane_continuous<LW, SlotSinkT<WS>, OR_BASE>(w, n, gap0, smem_addr(tb.fast),
+                                                                    smem_addr(tb.smask), sink);
       if (windowed) sink = saved;
     }
     if (windowed) {
@@ -140,7 +141,7 @@ __device__ __forceinline__ LaneRun warp_decode_scan(const WarpInT<LW>& in, std::
           if (verified)  // a flagged entry: the exact walk straight away
             decode_window_exact(w[2 * i], w[2 * i + 1], w[2 * i + 2], w[2 * i + 3], gap, tb, len_off, sink);
           else
-            decode_window(w[2 * i], w[2 * i + 1], w[2 * i + 2], w[2 * i + 3], gap, tb, len_off, sink);
+            decode_window<OR_BASE>(w[2 * i], w[2 * i + 1], w[2 * i + 2], w[2 * i + 3], gap, tb, len_off, sink);
         }
       }
     }
