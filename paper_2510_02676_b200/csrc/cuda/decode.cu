@@ -132,7 +132,7 @@ __device__ __forceinline__ void decode_tile(const TensorDesc& d, const TileGeo& 
     for (int i = 0; i < KWIN; ++i) {
       if (wl0 + i < g.nwin)
         decode_window(bswap32(cur.win[i].x), bswap32(cur.win[i].y), bswap32(cur.win[i + 1].x),
-                      bswap32(cur.win[i + 1].y), gap_of<KWIN>(cur.gaps, i, wl0 + i), tb, len_off, sink);
+                      bswap32(cur.win[i + 1].y), gap_of<KWIN>(cur.gaps, i, wl0 + i), SmemTables{tb}, len_off, sink);
     }
   }
   const std::uint32_t cnt = sink.finish(slot_base);
@@ -349,7 +349,7 @@ __global__ void count_window_kernel(const std::uint8_t* w16, unsigned gap, Tenso
       w[k] = v;
     }
     CountSink c;
-    decode_window_exact(w[0], w[1], w[2], w[3], gap & 15u, tb, (d.n_luts - 1) << 8, c);
+    decode_window_exact(w[0], w[1], w[2], w[3], gap & 15u, SmemTables{tb}, (d.n_luts - 1) << 8, c);
     *out = c.n4 >> 2;
   }
 }

@@ -94,29 +94,41 @@ struct CountSink {
   __device__ __forceinline__ void put(std::uint32_t, std::uint32_t k4) { n4 += k4; }
 };
 
+// Table access for the walks (a view, so a kernel may keep the start masks
+// and the cascade -- window ends and flagged entries only -- elsewhere than
+// shared memory; the fast table is always addressed in shared memory).
+struct SmemTables {
+  const Tables& tb;
+  __device__ __forceinline__ std::uint32_t fast_addr() const { return smem_addr(tb.fast); }
+  __device__ __forceinline__ std::uint32_t fast(std::uint32_t idx) const { return tb.fast[idx]; }
+  __device__ __forceinline__ std::uint32_t smask(std::uint32_t idx) const { return tb.smask[idx]; }
+  __device__ __forceinline__ std::uint32_t cascade(std::uint32_t i) const { return tb.cascade[i]; }
+};
+
+
 // The reference cascade (lut.hpp:43-49) on the 16-bit head of `hi`, as a
 // fast-format entry: one symbol, its length as b.
-__device__ __forceinline__ std::uint32_t slow_entry(std::uint32_t hi, const Tables& tb,
-                                                    std::uint32_t len_off) {
+template <class TV>
+__device__ __forceinline__ std::uint32_t slow_entry(std::uint32_t hi, const TV& tv, std::uint32_t len_off) {
   const std::uint32_t w16 = hi >> 16;
-  std::uint32_t v = tb.cascade[w16 >> 8];
-  if (v >= 240) v = tb.cascade[((256u - v) << 8) | (w16 & 255u)];
-  return (v << 12) | (4u << 5) | tb.cascade[len_off + v];
+  std::uint32_t v = tv.cascade(w16 >> 8);
+  if (v >= 240) v = tv.cascade(((256u - v) << 8) | (w16 & 255u));
+  return (v << 12) | (4u << 5) | tv.cascade(len_off + v);
 }
 
 // Exact walk of one 64-bit window: the code words that start in [gap, 64)
 // (codec.cpp:133-190 semantics); w0..w3 = window bits 0..127, big-endian.
 // Handles every entry kind; used for count_phase and for flagged windows.
-template <class Sink>
+template <class Sink, class TV>
 __device__ __forceinline__ void decode_window_exact(std::uint32_t w0, std::uint32_t w1,
                                                     std::uint32_t w2, std::uint32_t w3,
-                                                    std::uint32_t gap, const Tables& tb,
+                                                    std::uint32_t gap, const TV& tb,
                                                     std::uint32_t len_off, Sink& sink) {
   std::uint32_t hi = __funnelshift_l(w1, w0, gap);
   std::uint32_t lo = __funnelshift_l(w2, w1, gap);
   std::uint32_t p = gap;
   while (p < 32) {
-    std::uint32_t e = tb.fast[hi >> kFastShift];
+    std::uint32_t e = tb.fast(hi >> kFastShift);
     if (e & kSlowFlag) e = slow_entry(hi, tb, len_off);
     sink.put(e >> 12, (e >> 5) & 31);
     hi = __funnelshift_l(lo, hi, e);
@@ -127,12 +139,12 @@ __device__ __forceinline__ void decode_window_exact(std::uint32_t w0, std::uint3
   lo = __funnelshift_l(w3, w2, p - 32);
   for (;;) {
     const std::uint32_t idx = hi >> kFastShift;
-    std::uint32_t e = tb.fast[idx];
+    std::uint32_t e = tb.fast(idx);
     const bool fast_hit = !(e & kSlowFlag);
     if (!fast_hit) e = slow_entry(hi, tb, len_off);
     const std::uint32_t b = e & 31, r = 64 - p;
     if (b >= r) {
-      const std::uint32_t starts = fast_hit ? tb.smask[idx] : 1u;
+      const std::uint32_t starts = fast_hit ? tb.smask(idx) : 1u;
       const std::uint32_t k4 = 4 * __popc(starts & ((1u << r) - 1));
       sink.put((e >> 12) & ((1u << k4) - 1), k4);
       return;
@@ -154,10 +166,10 @@ __device__ __forceinline__ void decode_window_exact(std::uint32_t w0, std::uint3
 // and then exactly the symbols that start before it (start-bit mask +
 // popcount, the codec.cpp:143-160 rule).
 // fast = shared address of tb.fast, smask = shared address of tb.smask.
-template <class Sink, bool OR_BASE = false>
+template <class Sink, bool OR_BASE, class TV>
 __device__ __forceinline__ bool decode_window_fast(std::uint32_t w0, std::uint32_t w1, std::uint32_t w2,
                                                    std::uint32_t w3, std::uint32_t gap, std::uint32_t fast,
-                                                   std::uint32_t smask, Sink& sink) {
+                                                   const TV& tv, Sink& sink) {
   std::uint32_t hi = __funnelshift_l(w1, w0, gap);
   std::uint32_t lo = __funnelshift_l(w2, w1, gap);
   std::uint32_t p = gap;  // + kSlowFlag once a flagged entry was met (ends the loops)
@@ -177,7 +189,7 @@ __device__ __forceinline__ bool decode_window_fast(std::uint32_t w0, std::uint32
     if (e & kSlowFlag) return false;
     const std::uint32_t b = e & 31, r = 64 - p;
     if (b >= r) {
-      const std::uint32_t k4 = 4 * __popc(lds16(smask + 2 * idx) & ((1u << r) - 1));
+      const std::uint32_t k4 = 4 * __popc(tv.smask(idx) & ((1u << r) - 1));
       sink.put((e >> 12) & ((1u << k4) - 1), k4);
       return true;
     }
@@ -197,9 +209,9 @@ __device__ __forceinline__ bool decode_window_fast(std::uint32_t w0, std::uint32
 // for every encoder-produced stream; the upload-time gap check
 // (verify_gaps_kernel) establishes it per 256-window tile.  Returns false if
 // a flagged entry was met (the caller redoes the windows exactly).
-template <int NW, class Sink, bool OR_BASE = false>
+template <int NW, class Sink, bool OR_BASE, class TV>
 __device__ __forceinline__ bool decode_lane_continuous(const std::uint32_t (&w)[2 * NW + 2], std::uint32_t n,
-                                                       std::uint32_t gap, std::uint32_t fast, std::uint32_t smask,
+                                                       std::uint32_t gap, std::uint32_t fast, const TV& tv,
                                                        Sink& sink) {
   std::uint32_t hi = __funnelshift_l(w[1], w[0], gap);
   std::uint32_t lo = __funnelshift_l(w[2], w[1], gap);
@@ -223,7 +235,7 @@ __device__ __forceinline__ bool decode_lane_continuous(const std::uint32_t (&w)[
           }
           const std::uint32_t b = e & 31, r = 32 - p;
           if (b >= r) {
-            const std::uint32_t k4 = 4 * __popc(lds16(smask + 2 * idx) & ((1u << r) - 1));
+            const std::uint32_t k4 = 4 * __popc(tv.smask(idx) & ((1u << r) - 1));
             sink.put((e >> 12) & ((1u << k4) - 1), k4);
             break;
           }
@@ -255,14 +267,15 @@ __device__ __forceinline__ bool decode_lane_continuous(const std::uint32_t (&w)[
 // code word at or after bit 64, relative to the window (codec.cpp:143-160 --
 // the walk takes the words that start in [gap, 64)).  For a stream written
 // by the encoder this is 64 + the next window's gap (codec.cpp:49-98).
+template <class TV>
 __device__ __forceinline__ std::uint32_t window_end(std::uint32_t w0, std::uint32_t w1, std::uint32_t w2,
-                                                    std::uint32_t w3, std::uint32_t gap, const Tables& tb,
+                                                    std::uint32_t w3, std::uint32_t gap, const TV& tb,
                                                     std::uint32_t len_off) {
   std::uint32_t hi = __funnelshift_l(w1, w0, gap);
   std::uint32_t lo = __funnelshift_l(w2, w1, gap);
   std::uint32_t p = gap;
   while (p < 32) {
-    std::uint32_t e = tb.fast[hi >> kFastShift];
+    std::uint32_t e = tb.fast(hi >> kFastShift);
     if (e & kSlowFlag) e = slow_entry(hi, tb, len_off);
     hi = __funnelshift_l(lo, hi, e);
     lo = __funnelshift_l(0u, lo, e);
@@ -272,12 +285,12 @@ __device__ __forceinline__ std::uint32_t window_end(std::uint32_t w0, std::uint3
   lo = __funnelshift_l(w3, w2, p - 32);
   for (;;) {
     const std::uint32_t idx = hi >> kFastShift;
-    std::uint32_t e = tb.fast[idx];
+    std::uint32_t e = tb.fast(idx);
     const bool fast_hit = !(e & kSlowFlag);
     if (!fast_hit) e = slow_entry(hi, tb, len_off);
     const std::uint32_t b = e & 31, r = 64 - p;
     if (b >= r) {  // r <= 16 here
-      const std::uint32_t m = (fast_hit ? static_cast<std::uint32_t>(tb.smask[idx]) : 1u) >> r;
+      const std::uint32_t m = (fast_hit ? tb.smask(idx) : 1u) >> r;
       return m ? 64 + __ffs(m) - 1 : p + b;
     }
     hi = __funnelshift_l(lo, hi, e);
@@ -286,12 +299,12 @@ __device__ __forceinline__ std::uint32_t window_end(std::uint32_t w0, std::uint3
   }
 }
 
-template <bool OR_BASE = false, class Sink>
+template <bool OR_BASE = false, class Sink, class TV>
 __device__ __forceinline__ void decode_window(std::uint32_t w0, std::uint32_t w1, std::uint32_t w2,
-                                              std::uint32_t w3, std::uint32_t gap, const Tables& tb,
+                                              std::uint32_t w3, std::uint32_t gap, const TV& tb,
                                               std::uint32_t len_off, Sink& sink) {
   const Sink saved = sink;
-  if (!decode_window_fast<Sink, OR_BASE>(w0, w1, w2, w3, gap, smem_addr(tb.fast), smem_addr(tb.smask), sink)) {
+  if (!decode_window_fast<Sink, OR_BASE>(w0, w1, w2, w3, gap, tb.fast_addr(), tb, sink)) {
     sink = saved;
     decode_window_exact(w0, w1, w2, w3, gap, tb, len_off, sink);
   }

@@ -58,6 +58,7 @@ struct StaticSmem {
 };
 static_assert(offsetof(StaticSmem, tb) + offsetof(Tables, fast) == 0x4000 - 0x400, "fast table offset");
 __shared__ __align__(1024) StaticSmem g_s;
+
 #define g_tb g_s.tb
 #define g_next_tile g_s.next_tile
 #define g_desc g_s.desc
@@ -86,8 +87,10 @@ __device__ __forceinline__ void warp_tile(const TensorDesc& d, const WarpIn& in,
                                           std::uint32_t len_off, WarpSmem& ws, int lane) {
   // slots interleaved word by word (word j of lane L at slot[32 j + L]): the
   // lanes' slot stores and reads hit 32 different banks
-  const LaneRun run = warp_decode_scan<kLaneWin, 128, true>(in, log2T, len_off, g_tb, smem_addr(ws.slot + lane),
-                                                            lane, tile_verified(d, in, log2T));
+  const std::uint32_t slot = smem_addr(ws.slot + lane);
+  const bool verified = tile_verified(d, in, log2T);
+  const LaneRun run =
+      warp_decode_scan<kLaneWin, 128, true>(in, log2T, len_off, SmemTables{g_tb}, slot, lane, verified);
   GlobalOut out{d.out + ((in.A & ~std::uint64_t{15}) - d.out_offset)};
   compact_write<kWbUnroll>(d, in.A, in.E, run, ws, lane, out);
 }
@@ -97,6 +100,8 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_warp_kernel(const LaunchArg
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   WarpSmem& ws = reinterpret_cast<WarpSmem*>(smem_raw)[warp];
+  unsigned& next_tile = g_next_tile;
+  TensorDesc& desc = g_desc;
   asm volatile("griddepcontrol.launch_dependents;");  // the next decode may claim SMs as ours free up
   const std::uint64_t total_tiles = args.total_tiles;
   const std::uint64_t t_lo = total_tiles * blockIdx.x / gridDim.x;
@@ -115,14 +120,14 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_warp_kernel(const LaunchArg
     __syncthreads();  // every warp is done with the previous tables and descriptor
     // The segment's descriptor lives in shared memory, read field by field
     // where used: ~30 registers a register copy would pin for the whole loop.
-    if (threadIdx.x == 0) g_desc = args.descs ? args.descs[di] : args.inline_desc;
+    if (threadIdx.x == 0) desc = args.descs ? args.descs[di] : args.inline_desc;
     __syncthreads();
-    const TensorDesc& d = g_desc;
+    const TensorDesc& d = desc;
     const std::uint32_t log2T = 31 - __clz(d.T);
     if (threadIdx.x == 0 && (smem_addr(g_tb.fast) & 0x3FFFu)) __trap();  // base | offset needs 16 KB alignment
     stage_tables(d, g_tb, threadIdx.x, NW * 32);
     const std::uint32_t len_off = (d.n_luts - 1) << 8;
-    if (threadIdx.x == 0) g_next_tile = NW;
+    if (threadIdx.x == 0) next_tile = NW;
     __syncthreads();
 
     // Tiles are handed out dynamically inside the CTA (warp w starts with
@@ -141,7 +146,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_warp_kernel(const LaunchArg
           asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(d.packed + p0), "r"(bytes) : "memory");
       }
       unsigned claim = 0;
-      if (lane == 0) claim = atomicAdd(&g_next_tile, 1u);
+      if (lane == 0) claim = atomicAdd(&next_tile, 1u);
       const std::uint64_t next = seg + __shfl_sync(0xffffffffu, claim, 0);
       if (next < seg_end) load_warp_tile(d, next, log2T, lane, nxt);
       warp_tile(d, cur, log2T, len_off, ws, lane);
@@ -201,7 +206,7 @@ __global__ void __launch_bounds__(256) verify_gaps_kernel(const TensorDesc d, st
       const uint2 b = __ldg(reinterpret_cast<const uint2*>(d.encoded + 8 * k + 8));
       const std::uint32_t g0 = (d.gaps[k >> 1] >> ((k & 1) ? 0 : 4)) & 15u;
       const std::uint32_t g1 = (d.gaps[(k + 1) >> 1] >> (((k + 1) & 1) ? 0 : 4)) & 15u;
-      bad = window_end(bswap32(a.x), bswap32(a.y), bswap32(b.x), bswap32(b.y), g0, tb, len_off) != 64 + g1;
+      bad = window_end(bswap32(a.x), bswap32(a.y), bswap32(b.x), bswap32(b.y), g0, SmemTables{tb}, len_off) != 64 + g1;
     }
     if (__ballot_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) {
       const std::uint64_t v = k >> 8;

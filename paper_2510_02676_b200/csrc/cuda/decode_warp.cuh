@@ -107,9 +107,9 @@ struct LaneRun {
 // upload-time gap check): one continuous walk over the lane's windows;
 // otherwise, or when the walk met a flagged entry, window by window with the
 // reference's per-window semantics (fast table, exact walk where flagged).
-template <int LW, int WS = 4, bool OR_BASE = false>
+template <int LW, int WS = 4, bool OR_BASE = false, class TV>
 __device__ __forceinline__ LaneRun warp_decode_scan(const WarpInT<LW>& in, std::uint32_t log2T,
-                                                   std::uint32_t len_off, const Tables& tb, std::uint32_t slot_base,
+                                                   std::uint32_t len_off, const TV& tb, std::uint32_t slot_base,
                                                    int lane, bool verified = false) {
   const std::uint32_t wl0 = static_cast<std::uint32_t>(lane) * LW;
   const bool active = wl0 < in.nwin;
@@ -128,8 +128,7 @@ __device__ __forceinline__ LaneRun warp_decode_scan(const WarpInT<LW>& in, std::
     if (verified) {
       const SlotSinkT<WS> saved = sink;
       const std::uint32_t gap0 = (in.gaps >> 4) & 15u;  // window 0: high nibble of byte 0
-      windowed = !decode_lane_continuous<LW, SlotSinkT<WS>, OR_BASE>(w, n, gap0, smem_addr(tb.fast),
-                                                                    smem_addr(tb.smask), sink);
+      windowed = !decode_lane_continuous<LW, SlotSinkT<WS>, OR_BASE>(w, n, gap0, tb.fast_addr(), tb, sink);
       if (windowed) sink = saved;
     }
     if (windowed) {

@@ -235,7 +235,7 @@ struct RingOut {
 template <int LW, class WSm>
 __device__ __forceinline__ void ring_tile(const TensorDesc& d, const WarpInT<LW>& in, std::uint32_t log2T,
                                           std::uint32_t len_off, WSm& ws, const Ring& R, int lane) {
-  const LaneRun run = warp_decode_scan<LW, 128>(in, log2T, len_off, g_tbf, smem_addr(ws.slot + lane), lane,
+  const LaneRun run = warp_decode_scan<LW, 128>(in, log2T, len_off, SmemTables{g_tbf}, smem_addr(ws.slot + lane), lane,
                                                 tile_verified(d, in, log2T));
   // this ECF8 tile's part of the CTA range, in ring tiles tf (and tf + 1)
   const std::uint64_t A = in.A > R.e0 ? in.A : R.e0;
