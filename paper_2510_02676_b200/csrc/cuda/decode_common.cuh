@@ -209,7 +209,7 @@ __device__ __forceinline__ bool decode_window_fast(std::uint32_t w0, std::uint32
 // for every encoder-produced stream; the upload-time gap check
 // (verify_gaps_kernel) establishes it per 256-window tile.  Returns false if
 // a flagged entry was met (the caller redoes the windows exactly).
-template <int NW, class Sink, bool OR_BASE, class TV>
+template <int NW, class Sink, bool OR_BASE, class TV, bool FULL = false>
 __device__ __forceinline__ bool decode_lane_continuous(const std::uint32_t (&w)[2 * NW + 2], std::uint32_t n,
                                                        std::uint32_t gap, std::uint32_t fast, const TV& tv,
                                                        Sink& sink) {
@@ -219,7 +219,7 @@ __device__ __forceinline__ bool decode_lane_continuous(const std::uint32_t (&w)[
   // entry adds kSlowFlag to it, which ends this and every later phase loop
   // (p stays >= 32) -- no separate flag accumulator in the hot loop.
   std::uint32_t p = gap;
-  const std::uint32_t last = 2 * n - 1;
+  const std::uint32_t last = FULL ? 2 * NW - 1 : 2 * n - 1;  // FULL: n == NW known at compile time
 #pragma unroll
   for (std::uint32_t k = 0; k < 2 * NW; ++k) {
     if (k == last) {

@@ -128,7 +128,8 @@ __device__ __forceinline__ LaneRun warp_decode_scan(const WarpInT<LW>& in, std::
     if (verified) {
       const SlotSinkT<WS> saved = sink;
       const std::uint32_t gap0 = (in.gaps >> 4) & 15u;  // window 0: high nibble of byte 0
-      windowed = !decode_lane_continuous<LW, SlotSinkT<WS>, OR_BASE>(w, n, gap0, tb.fast_addr(), tb, sink);
+      // n == LW: tiles are whole blocks of T >= LW windows, so every active lane owns LW windows
+      windowed = !decode_lane_continuous<LW, SlotSinkT<WS>, OR_BASE, TV, true>(w, n, gap0, tb.fast_addr(), tb, sink);
       if (windowed) sink = saved;
     }
     if (windowed) {
