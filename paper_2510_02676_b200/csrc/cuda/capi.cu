@@ -233,7 +233,8 @@ void upload_into(ecf8_dev_tensor* t, const ecf8_sections* s, std::uint64_t nb, c
 // reference's window-by-window semantics.
 void verify_into(ecf8_dev_tensor* t, cudaStream_t st) {
   static const bool off = std::getenv("ECF8_NO_CONT_WALK") != nullptr;  // A/B runs
-  if (off || t->n_elem == 0 || ecf8::dev::variant_for(t->T, t->desc.lmin).id != 4) return;
+  const int vid = t->n_elem ? ecf8::dev::variant_for(t->T, t->desc.lmin).id : -1;
+  if (off || (vid != 4 && vid != 5)) return;
   std::uint32_t* const ok = t->ok_bits;
   cu(cudaMemsetAsync(ok, 0xFF, 4 * ((t->n_vtiles + 31) / 32), st), "memset(tile_ok)");
   cu(ecf8::dev::launch_verify_gaps(t->desc, ok, st), "verify launch");
@@ -517,7 +518,7 @@ int ecf8_batch_create(const ecf8_dev_tensor* const* ts, uint8_t* const* d_outs, 
     if (!out || (count > 0 && (!ts || !d_outs))) return fail(ECF8_EINVAL, "null argument");
     *out = nullptr;
     auto b = std::make_unique<ecf8_batch>();
-    for (int kw = 0; kw < 6; ++kw) {  // one launch per kernel variant present
+    for (int kw = 0; kw < 6; ++kw) {  // one launch per kernel variant present (ids 0..5)
       std::vector<TensorDesc> group;
       std::uint64_t tiles = 0;
       int kwin_tile = 1;

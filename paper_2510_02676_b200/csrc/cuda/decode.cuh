@@ -46,7 +46,9 @@ constexpr std::uint64_t kTileElemsMax = 1024 * 64;
 //
 // Variant 4 is the warp-autonomous kernel (decode_warp.cu): one warp owns a
 // 256-window tile, eight windows per lane; it needs T in [8, 256] (whole
-// blocks per tile, whole lanes per block) and Lmin >= 2.
+// blocks per tile, whole lanes per block) and Lmin >= 2.  Variant 5 is the
+// same kernel for 1-bit codes: 64-symbol windows double a lane's slot and
+// the staging tile, so 12 warps per SM.
 struct Variant {
   int kwin;
   int slotw;
@@ -58,6 +60,7 @@ bool warp_variant_enabled();  // false when ECF8_NO_WARP_KERNEL=1 (A/B runs)
 
 inline Variant variant_for(std::uint32_t T, std::uint32_t lmin) {
   if (lmin >= 2 && T >= 8 && T <= 256 && warp_variant_enabled()) return {8, 32, 4, 256};
+  if (lmin == 1 && T >= 8 && T <= 256 && warp_variant_enabled()) return {8, 64, 5, 256};
   if (T == 1) return {1, 8, 0, kThreads};
   if (T == 2) return {2, 16, 1, 2 * kThreads};
   if (lmin >= 2) return {4, 16, 2, 4 * kThreads};

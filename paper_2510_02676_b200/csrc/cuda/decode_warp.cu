@@ -41,8 +41,10 @@ namespace ecf8::dev {
 namespace {
 
 // 33 slot rows: a lane's run is <= 256 nibbles (32 words); the staging tile
-// holds 8192 nibbles + the 16-byte alignment offset.
-using WarpSmem = WarpPipeSmem<33, 32 * kSlotWords + 8>;
+// holds 8192 nibbles + the 16-byte alignment offset.  With 1-bit codes (WIDE)
+// both double: 512 nibbles per lane, 16384 per tile.
+template <bool WIDE>
+using WarpSmemT = WarpPipeSmem<WIDE ? 65 : 33, (WIDE ? 2 : 1) * 32 * kSlotWords + 8>;
 
 // Static shared memory: the tile queue, the current segment's descriptor
 // (read field by field where used: a register copy would pin ~30 registers
@@ -83,8 +85,9 @@ struct GlobalOut {
 };
 
 // One tile: decode + scan, compact, write back.
+template <class WSm>
 __device__ __forceinline__ void warp_tile(const TensorDesc& d, const WarpIn& in, std::uint32_t log2T,
-                                          std::uint32_t len_off, WarpSmem& ws, int lane) {
+                                          std::uint32_t len_off, WSm& ws, int lane) {
   // slots interleaved word by word (word j of lane L at slot[32 j + L]): the
   // lanes' slot stores and reads hit 32 different banks
   const std::uint32_t slot = smem_addr(ws.slot + lane);
@@ -95,8 +98,9 @@ __device__ __forceinline__ void warp_tile(const TensorDesc& d, const WarpIn& in,
   compact_write<kWbUnroll>(d, in.A, in.E, run, ws, lane, out);
 }
 
-template <int NW>
+template <int NW, bool WIDE>
 __global__ void __launch_bounds__(NW * 32, 1) decode_warp_kernel(const LaunchArgs args) {
+  using WarpSmem = WarpSmemT<WIDE>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   WarpSmem& ws = reinterpret_cast<WarpSmem*>(smem_raw)[warp];
@@ -156,17 +160,17 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_warp_kernel(const LaunchArg
   }
 }
 
-template <int NW>
+template <int NW, bool WIDE = false>
 cudaError_t launch_nw(const LaunchArgs& args, cudaStream_t s) {
   static int grid_cap = 0;
-  const int smem = static_cast<int>(sizeof(WarpSmem)) * NW;
+  const int smem = static_cast<int>(sizeof(WarpSmemT<WIDE>)) * NW;
   if (grid_cap == 0) {
-    cudaError_t e = cudaFuncSetAttribute(decode_warp_kernel<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = cudaFuncSetAttribute(decode_warp_kernel<NW, WIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_warp_kernel<NW>, NW * 32, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_warp_kernel<NW, WIDE>, NW * 32, smem);
     if (e != cudaSuccess) return e;
     grid_cap = sms * (per_sm > 0 ? per_sm : 1);
   }
@@ -186,7 +190,7 @@ cudaError_t launch_nw(const LaunchArgs& args, cudaStream_t s) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, decode_warp_kernel<NW>, args);
+  return cudaLaunchKernelEx(&cfg, decode_warp_kernel<NW, WIDE>, args);
 }
 
 // One thread per window: window_end of its reference walk against the next
@@ -229,6 +233,9 @@ cudaError_t launch_decode_warp(const LaunchArgs& args, cudaStream_t s) {
   }();
   return nw == 20 ? launch_nw<20>(args, s) : nw == 22 ? launch_nw<22>(args, s) : launch_nw<24>(args, s);
 }
+
+// Variant 5 (1-bit codes): 12 warps x 16.5 KB of warp state.
+cudaError_t launch_decode_warp_wide(const LaunchArgs& args, cudaStream_t s) { return launch_nw<12, true>(args, s); }
 
 cudaError_t launch_verify_gaps(const TensorDesc& d, std::uint32_t* tile_ok, cudaStream_t s) {
   const std::uint64_t n_win = d.blk_end * d.T;
