@@ -67,13 +67,11 @@ __device__ __forceinline__ void load_tile_meta(const TensorDesc& d, std::uint32_
   const std::uint32_t wl = static_cast<std::uint32_t>(lane) * LW;
   in.A = __ldg(d.outpos + in.b0);
   in.E = __ldg(d.outpos + in.b0 + in.nblk);
-  if (wl < in.nwin) {
-    const std::uint32_t bl = wl >> log2T;
-    in.o0 = __ldg(d.outpos + in.b0 + bl);
-    in.o1 = __ldg(d.outpos + in.b0 + bl + 1);
-  } else {
-    in.o0 = in.o1 = in.E;
-  }
+  // my block's bounds (lanes past the tile's windows read the last block's:
+  // unused, their run is empty) -- no select on E, which would wait for it here
+  const std::uint32_t bl = min(wl >> log2T, in.nblk - 1);
+  in.o0 = __ldg(d.outpos + in.b0 + bl);
+  in.o1 = __ldg(d.outpos + in.b0 + bl + 1);
 }
 
 template <int LW>
@@ -190,7 +188,8 @@ struct WarpPipeSmem {
 // (coalesced); the ragged first and last chunks byte by byte.  The
 // sign/mantissa bytes of the full chunks come into the (then free) slots by
 // 16-byte async copies issued right after compaction: one round trip per tile
-// (the slots must hold 8 x full chunks + 16 bytes).
+// (the slots must hold the tile's packed bytes + 16: (8192 + 30) / 2 + 16 <=
+// 33 x 128 bytes).
 template <int UNROLL, class WSm, class Out>
 __device__ __forceinline__ void compact_write(const TensorDesc& d, std::uint64_t A, std::uint64_t E,
                                               const LaneRun& run, WSm& ws, int lane, Out& out) {
@@ -236,10 +235,10 @@ __device__ __forceinline__ void compact_write(const TensorDesc& d, std::uint64_t
   // ---- the slots are free: sign/mantissa bytes of the full chunks into them
   // (16-byte pieces from the 16-byte aligned address at or below the first
   // full chunk's bytes: <= 8 nfull + 16 bytes)
-  const std::uint8_t* const pk = d.packed + (S0 >> 1);
-  const std::uint64_t pk_lo = (S0 >> 1) + 8 * full_lo, pk_a = pk_lo & ~std::uint64_t{15};
+  // all of the tile's packed bytes [S0 / 2, (S0 + data_end + 1) / 2), edge chunks included
+  const std::uint64_t pk_lo = (S0 >> 1) + 8 * full_lo, pk_a = (S0 >> 1) & ~std::uint64_t{15};
   {
-    const std::uint32_t n16 = static_cast<std::uint32_t>((pk_lo + 8 * nfull - pk_a + 15) >> 4);
+    const std::uint32_t n16 = static_cast<std::uint32_t>((((S0 + data_end + 1) >> 1) - pk_a + 15) >> 4);
     const std::uint32_t dst = smem_addr(ws.slot);
     for (std::uint32_t i = lane; i < n16; i += 32)
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16 * i), "l"(d.packed + pk_a + 16 * i)
@@ -300,7 +299,8 @@ __device__ __forceinline__ void compact_write(const TensorDesc& d, std::uint64_t
                               : (full_hi < nch && !(nch == 1 && full_lo > 0) && i < data_end);
   if (edge) {
     const std::uint32_t x = (ws.stage[i >> 3] >> (4 * (i & 7))) & 15u;
-    out.byte(i, merge1(x, pk[i >> 1], i & 1));
+    const std::uint8_t* const pks = reinterpret_cast<const std::uint8_t*>(ws.slot) + ((S0 >> 1) - pk_a);
+    out.byte(i, merge1(x, pks[i >> 1], i & 1));
   }
   out.done();
 }
