@@ -31,6 +31,7 @@ struct WarpInT {
   std::uint64_t o0, o1;      // my reference block's output range
   std::uint32_t nblk, nwin;
   std::uint64_t b0;
+  std::uint32_t ok_a, ok_b;  // tile_ok words of the tile's first / last window (loaded one tile ahead)
 };
 using WarpIn = WarpInT<kLaneWin>;
 
@@ -72,6 +73,12 @@ __device__ __forceinline__ void load_tile_meta(const TensorDesc& d, std::uint32_
   const std::uint32_t bl = min(wl >> log2T, in.nblk - 1);
   in.o0 = __ldg(d.outpos + in.b0 + bl);
   in.o1 = __ldg(d.outpos + in.b0 + bl + 1);
+  in.ok_a = in.ok_b = 0;
+  if (d.tile_ok && in.nwin) {
+    const std::uint64_t w0 = in.b0 << log2T;
+    in.ok_a = __ldg(d.tile_ok + (w0 >> 13));
+    in.ok_b = __ldg(d.tile_ok + ((w0 + in.nwin - 1) >> 13));
+  }
 }
 
 template <int LW>
@@ -84,13 +91,10 @@ __device__ __forceinline__ void load_warp_tile(const TensorDesc& d, std::uint64_
 // Were the gaps of the windows of this warp tile verified (verify_gaps_kernel)?
 // tile_ok bit v covers the boundaries after windows [256v, 256v + 256).
 template <int LW>
-__device__ __forceinline__ bool tile_verified(const TensorDesc& d, const WarpInT<LW>& in, std::uint32_t log2T) {
-  if (!d.tile_ok || in.nwin == 0) return false;
+__device__ __forceinline__ bool tile_verified(const TensorDesc&, const WarpInT<LW>& in, std::uint32_t log2T) {
   const std::uint64_t w0 = in.b0 << log2T;
-  const std::uint64_t v0 = w0 >> 8, v1 = (w0 + in.nwin - 1) >> 8;
-  const std::uint32_t a = __ldg(d.tile_ok + (v0 >> 5)) >> (v0 & 31);
-  const std::uint32_t b = __ldg(d.tile_ok + (v1 >> 5)) >> (v1 & 31);
-  return (a & b & 1u) != 0;
+  const std::uint32_t v0 = static_cast<std::uint32_t>(w0 >> 8), v1 = static_cast<std::uint32_t>((w0 + in.nwin - 1) >> 8);
+  return ((in.ok_a >> (v0 & 31)) & (in.ok_b >> (v1 & 31)) & 1u) != 0;  // ok words are 0 when unverified
 }
 
 struct LaneRun {
