@@ -167,8 +167,12 @@ struct ecf8_dev_tensor {
 
 struct ecf8_fused {
   const ecf8_dev_tensor* w = nullptr;
-  ecf8::dev::FusedCta* d_plan = nullptr;
-  std::uint32_t n_cta = 0, split_k = 1;
+  // Two CTA plans: [0] for up to 2 n-tile segments per CTA (any m), [1] for
+  // up to 4 (m <= 128: four accumulators fit the 512 TMEM columns), which
+  // lets the big weights run in one wave of the SMs.
+  ecf8::dev::FusedCta* d_plan[2] = {nullptr, nullptr};
+  std::uint32_t n_cta[2] = {0, 0}, max_seg[2] = {0, 0};
+  std::uint32_t split_k = 1;
   std::uint8_t* xt = nullptr;  // swizzled-X workspace (grow-only)
   std::uint64_t xt_cap = 0;
   std::uint64_t n = 0, k = 0;
@@ -691,39 +695,54 @@ int ecf8_fused_create(const ecf8_dev_tensor* t, uint64_t n, uint64_t k, int w_fm
     if (int rc = require_device()) return rc;
     std::vector<std::uint64_t> outpos(t->n_blocks + 1);
     cu(cudaMemcpy(outpos.data(), t->desc.outpos, 8 * outpos.size(), cudaMemcpyDeviceToHost), "D2H outpos");
-    // whole waves of the SMs (one CTA per SM); enough waves that a CTA's run
-    // of tiles spans at most two n-tiles (two TMEM accumulators)
+    // whole waves of the SMs (one CTA per SM); as few waves as keep every
+    // CTA's run of tiles within max_seg n-tiles (one TMEM accumulator each)
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const std::uint64_t KT = k / 128, total = (n / 128) * KT;
-    std::uint64_t waves = (total + static_cast<std::uint64_t>(sms) * KT - 1) / (static_cast<std::uint64_t>(sms) * KT);
-    if (waves == 0) waves = 1;
-    std::uint64_t ctas = std::min<std::uint64_t>(total, waves * static_cast<std::uint64_t>(sms));
     auto f = std::make_unique<ecf8_fused>();
     f->w = t;
     f->n = n;
     f->k = k;
     f->w_fmt = static_cast<std::uint32_t>(w_fmt);
-    f->split_k = static_cast<std::uint32_t>((ctas + n / 128 - 1) / (n / 128));
-    std::vector<ecf8::dev::FusedCta> plan;
-    for (std::uint64_t c = 0; c < ctas; ++c) {
-      ecf8::dev::FusedCta p{};
-      p.tile0 = static_cast<std::uint32_t>(total * c / ctas);
-      p.tile1 = static_cast<std::uint32_t>(total * (c + 1) / ctas);
-      p.e0 = std::uint64_t{p.tile0} * 16384;
-      p.e1 = std::uint64_t{p.tile1} * 16384;
-      // blocks overlapping [e0, e1): the block holding element e0 .. first block starting >= e1
-      auto ub = std::upper_bound(outpos.begin(), outpos.end() - 1, p.e0);
-      p.blk_begin = static_cast<std::uint64_t>(ub - outpos.begin()) - 1;
-      auto lb = std::lower_bound(outpos.begin(), outpos.end(), p.e1);
-      p.blk_end = std::min<std::uint64_t>(static_cast<std::uint64_t>(lb - outpos.begin()), t->n_blocks);
-      plan.push_back(p);
+    auto make_plan = [&](std::uint64_t ctas) {
+      std::vector<ecf8::dev::FusedCta> plan;
+      for (std::uint64_t c = 0; c < ctas; ++c) {
+        ecf8::dev::FusedCta p{};
+        p.tile0 = static_cast<std::uint32_t>(total * c / ctas);
+        p.tile1 = static_cast<std::uint32_t>(total * (c + 1) / ctas);
+        p.e0 = std::uint64_t{p.tile0} * 16384;
+        p.e1 = std::uint64_t{p.tile1} * 16384;
+        // blocks overlapping [e0, e1): the block holding element e0 .. first block starting >= e1
+        auto ub = std::upper_bound(outpos.begin(), outpos.end() - 1, p.e0);
+        p.blk_begin = static_cast<std::uint64_t>(ub - outpos.begin()) - 1;
+        auto lb = std::lower_bound(outpos.begin(), outpos.end(), p.e1);
+        p.blk_end = std::min<std::uint64_t>(static_cast<std::uint64_t>(lb - outpos.begin()), t->n_blocks);
+        plan.push_back(p);
+      }
+      return plan;
+    };
+    auto segs = [&](const std::vector<ecf8::dev::FusedCta>& plan) {
+      std::uint32_t m = 1;
+      for (const auto& p : plan)
+        if (p.tile1 > p.tile0) m = std::max<std::uint32_t>(m, static_cast<std::uint32_t>((p.tile1 - 1) / KT - p.tile0 / KT + 1));
+      return m;
+    };
+    const std::uint32_t caps[2] = {2, 4};
+    for (int i = 0; i < 2; ++i) {
+      std::vector<ecf8::dev::FusedCta> plan;
+      for (std::uint64_t waves = 1;; ++waves) {
+        plan = make_plan(std::min<std::uint64_t>(total, waves * static_cast<std::uint64_t>(sms)));
+        if (segs(plan) <= caps[i] || plan.size() == total) break;
+      }
+      f->n_cta[i] = static_cast<std::uint32_t>(plan.size());
+      f->max_seg[i] = segs(plan);
+      cu(cudaMalloc(&f->d_plan[i], sizeof(ecf8::dev::FusedCta) * plan.size()), "cudaMalloc(plan)");
+      cu(cudaMemcpy(f->d_plan[i], plan.data(), sizeof(ecf8::dev::FusedCta) * plan.size(), cudaMemcpyHostToDevice),
+         "H2D plan");
     }
-    f->n_cta = static_cast<std::uint32_t>(plan.size());
-    cu(cudaMalloc(&f->d_plan, sizeof(ecf8::dev::FusedCta) * plan.size()), "cudaMalloc(plan)");
-    cu(cudaMemcpy(f->d_plan, plan.data(), sizeof(ecf8::dev::FusedCta) * plan.size(), cudaMemcpyHostToDevice),
-       "H2D plan");
+    f->split_k = static_cast<std::uint32_t>((f->n_cta[1] + n / 128 - 1) / (n / 128));
     *out = f.release();
     return ECF8_OK;
   });
@@ -740,7 +759,8 @@ int ecf8_fused_gemm(const ecf8_fused* f, const uint8_t* d_x, uint32_t m, float s
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
     ecf8::dev::FusedArgs a{};
     a.w = f->w->desc;
-    a.plan = f->d_plan;
+    const int pi = m <= 128 ? 1 : 0;  // accumulator columns <= 128: up to four n-tile segments per CTA
+    a.plan = f->d_plan[pi];
     a.x = d_x;
     a.y = d_y;
     auto* mf = const_cast<ecf8_fused*>(f);
@@ -764,18 +784,20 @@ int ecf8_fused_gemm(const ecf8_fused* f, const uint8_t* d_x, uint32_t m, float s
     if (a.stages_a < 2) return fail(ECF8_EINVAL, "fused GEMM: shared memory too small for this m");
     a.acc_cols = 32;
     while (a.acc_cols < a.m_pad) a.acc_cols <<= 1;
-    a.tmem_cols = 2 * a.acc_cols;
+    a.tmem_cols = 32;
+    while (a.tmem_cols < f->max_seg[pi] * a.acc_cols) a.tmem_cols <<= 1;
     a.w_fmt = f->w_fmt;
     a.scale = scale;
     cu(cudaMemsetAsync(d_y, 0, sizeof(float) * m * f->n, st), "memset y");
-    cu(ecf8::dev::launch_fused_gemm(a, f->n_cta, st), "fused GEMM launch");
+    cu(ecf8::dev::launch_fused_gemm(a, f->n_cta[pi], st), "fused GEMM launch");
     return ECF8_OK;
   });
 }
 
 void ecf8_fused_free(ecf8_fused* f) {
   if (!f) return;
-  if (f->d_plan) cudaFree(f->d_plan);
+  for (auto* p : f->d_plan)
+    if (p) cudaFree(p);
   if (f->xt) cudaFree(f->xt);
   delete f;
 }

@@ -32,7 +32,7 @@ struct FusedArgs {
   std::uint32_t split_k;
   std::uint32_t stages_a;
   std::uint32_t stages_b;   // X ring stages (2)
-  std::uint32_t tmem_cols;  // allocation: 2 accumulators of acc_cols
+  std::uint32_t tmem_cols;  // allocation: one accumulator of acc_cols per n-tile segment (power of two)
   std::uint32_t acc_cols;   // power of two >= max(32, m_pad)
   std::uint32_t w_fmt;       // 0 E4M3, 1 E5M2
   float scale;
