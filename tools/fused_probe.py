@@ -27,7 +27,7 @@ def t_ms(fn, reps=20):
 
 for name, n, k in SHAPES:
     w = codec.synth(1.8, 0.05, n * k, 5).reshape(n, k)
-    lin = FusedLinear(w)
+    lin = FusedLinear(w, threads_per_block=int(__import__("os").environ.get("FUSED_T", "128")))
     enc = codec.encode_tensor(w.reshape(-1), 256)
     dev = DeviceTensor(enc)
     wbuf = torch.empty(n * k, dtype=torch.uint8, device="cuda")
