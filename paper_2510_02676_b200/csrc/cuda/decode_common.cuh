@@ -22,14 +22,6 @@ struct Tables {
   std::uint32_t fast[kFastEntries];  // last: decode_warp.cu places it at a 16 KB-aligned shared address
 };
 
-// Shared address of the fast-table entry for the next kFastBits bits of hi.
-// OR_BASE: the table sits at a 16 KB-aligned address, so base | offset
-// (one LOP3) replaces base + offset.
-template <bool OR_BASE>
-__device__ __forceinline__ std::uint32_t fast_entry_addr(std::uint32_t fast, std::uint32_t hi) {
-  const std::uint32_t off = (hi >> (kFastShift - 2)) & ~3u;
-  return OR_BASE ? (fast | off) : (fast + off);
-}
 
 // A fast entry with n == 0 is staged as: advance 1 bit, emit nothing, set
 // kSlowFlag.  The fast walk then runs branch-free; a window that met such an
@@ -57,6 +49,24 @@ __device__ __forceinline__ std::uint32_t lds16(std::uint32_t a) {
 }
 __device__ __forceinline__ void sts32(std::uint32_t a, std::uint32_t v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
+// The fast-table entry for the next kFastBits bits of hi.
+// FIXED: the kernel pins the table at shared address kFastAt (decode_warp.cu
+// checks it), so the address is offset + constant -- the constant folds into
+// the load's immediate and no base register has to live across the walk.
+constexpr std::uint32_t kFastAt = 0x4000;
+template <bool FIXED>
+__device__ __forceinline__ std::uint32_t fast_entry(std::uint32_t fast, std::uint32_t hi) {
+  const std::uint32_t off = (hi >> (kFastShift - 2)) & ~3u;
+  if constexpr (FIXED) {
+    std::uint32_t v;  // constant in the load's immediate (ptxas would otherwise OR it in)
+    asm volatile("ld.shared.u32 %0, [%1+16384];" : "=r"(v) : "r"(off));
+    static_assert(kFastAt == 16384, "immediate above");
+    return v;
+  } else {
+    return lds32(fast + off);
+  }
 }
 
 // Packs 4-bit symbols into consecutive 32-bit slot words (first symbol
@@ -174,7 +184,7 @@ __device__ __forceinline__ bool decode_window_fast(std::uint32_t w0, std::uint32
   std::uint32_t lo = __funnelshift_l(w2, w1, gap);
   std::uint32_t p = gap;  // + kSlowFlag once a flagged entry was met (ends the loops)
   while (p < 32) {
-    const std::uint32_t e = lds32(fast_entry_addr<OR_BASE>(fast, hi));
+    const std::uint32_t e = fast_entry<OR_BASE>(fast, hi);
     sink.put(e >> 12, (e >> 5) & 31);
     hi = __funnelshift_l(lo, hi, e);  // shift amount = e & 31 = bits consumed
     lo = __funnelshift_l(0u, lo, e);
@@ -185,7 +195,7 @@ __device__ __forceinline__ bool decode_window_fast(std::uint32_t w0, std::uint32
   lo = __funnelshift_l(w3, w2, p - 32);
   for (;;) {
     const std::uint32_t idx = hi >> kFastShift;
-    const std::uint32_t e = lds32(fast_entry_addr<OR_BASE>(fast, hi));
+    const std::uint32_t e = fast_entry<OR_BASE>(fast, hi);
     if (e & kSlowFlag) return false;
     const std::uint32_t b = e & 31, r = 64 - p;
     if (b >= r) {
@@ -228,7 +238,7 @@ __device__ __forceinline__ bool decode_lane_continuous(const std::uint32_t (&w)[
       if (p < 32) {
         for (;;) {
           const std::uint32_t idx = hi >> kFastShift;
-          const std::uint32_t e = lds32(fast_entry_addr<OR_BASE>(fast, hi));
+          const std::uint32_t e = fast_entry<OR_BASE>(fast, hi);
           if (e & kSlowFlag) {
             p = kSlowFlag;
             break;
@@ -248,7 +258,7 @@ __device__ __forceinline__ bool decode_lane_continuous(const std::uint32_t (&w)[
       break;
     }
     while (p < 32) {
-      const std::uint32_t e = lds32(fast_entry_addr<OR_BASE>(fast, hi));
+      const std::uint32_t e = fast_entry<OR_BASE>(fast, hi);
       sink.put(e >> 12, (e >> 5) & 31);
       hi = __funnelshift_l(lo, hi, e);
       lo = __funnelshift_l(0u, lo, e);

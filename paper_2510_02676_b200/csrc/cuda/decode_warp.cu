@@ -49,9 +49,9 @@ using WarpSmemT = WarpPipeSmem<WIDE ? 65 : 33, (WIDE ? 2 : 1) * 32 * kSlotWords 
 // Static shared memory: the tile queue, the current segment's descriptor
 // (read field by field where used: a register copy would pin ~30 registers
 // for the whole tile loop) and the decode tables, laid out so that the fast
-// table starts at shared address 0x4000 (the CTA window begins 1 KB in, after
-// the reserved area): a probe address is then base | offset.  The kernel
-// traps if the toolchain ever places it elsewhere.
+// table starts at shared address kFastAt = 0x4000 (the CTA window begins 1 KB
+// in, after the reserved area): a probe address is offset + constant.  The
+// kernel traps if the toolchain ever places it elsewhere.
 struct StaticSmem {
   unsigned next_tile;  // CTA-local work queue of the current segment (relative)
   TensorDesc desc;     // the current segment's tensor
@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_warp_kernel(const LaunchArg
     __syncthreads();
     const TensorDesc& d = desc;
     const std::uint32_t log2T = 31 - __clz(d.T);
-    if (threadIdx.x == 0 && (smem_addr(g_tb.fast) & 0x3FFFu)) __trap();  // base | offset needs 16 KB alignment
+    if (threadIdx.x == 0 && smem_addr(g_tb.fast) != kFastAt) __trap();  // the walk addresses the table at kFastAt
     stage_tables(d, g_tb, threadIdx.x, NW * 32);
     const std::uint32_t len_off = (d.n_luts - 1) << 8;
     if (threadIdx.x == 0) next_tile = NW;
