@@ -23,14 +23,24 @@ struct Tables {
 };
 
 
-// A fast entry with n == 0 is staged as: advance 1 bit, emit nothing, set
-// kSlowFlag.  The fast walk then runs branch-free; a window that met such an
-// entry is decoded again exactly by the slow walk (rare: code words longer
-// than kFastBits bits, or garbage windows of incomplete codes).
-constexpr std::uint32_t kSlowFlag = 1u << 11;
+// Staged (shared-memory) fast entries, rearranged from the host layout
+// (tables.hpp: b 0..4, n4 5..9, symbols 12..31):
+//   bits  0..4   b   bits consumed (the funnel-shift amount)
+//   bit   5      0
+//   bit   6      kSlowFlag: first code word not resolvable from kFastBits
+//                bits (then b = 0, nothing emitted; the window is redone by
+//                the exact walk -- rare: long code words, garbage windows)
+//   bits  7..11  n4  4 x symbols
+//   bits 12..31  up to five 4-bit symbols, first lowest
+// Bits 0..6 of a walk position that adds whole entries are therefore exact
+// (at most 43 + 64 < 128, no carry into bit 7); higher bits collect garbage
+// that nothing reads -- one IADD per step instead of mask + add.
+constexpr std::uint32_t kSlowFlag = 1u << 6;
+constexpr std::uint32_t kPhaseDone = 0x60u;  // position bits 5..6: past bit 32 of the phase, or flagged
 __host__ __device__ constexpr std::uint32_t stage_entry(std::uint32_t e) {
-  return ((e >> 5) & 31) ? e : (kSlowFlag | 1u);
+  return ((e >> 5) & 31) ? ((e & 0xFFFFF01Fu) | (((e >> 5) & 31u) << 7)) : kSlowFlag;
 }
+__host__ __device__ constexpr std::uint32_t entry_n4(std::uint32_t e) { return (e >> 7) & 31u; }
 
 // Shared-memory accesses by 32-bit shared-window address: one register per
 // address and no generic-to-shared conversion in the hot loops.
@@ -123,7 +133,7 @@ __device__ __forceinline__ std::uint32_t slow_entry(std::uint32_t hi, const TV& 
   const std::uint32_t w16 = hi >> 16;
   std::uint32_t v = tv.cascade(w16 >> 8);
   if (v >= 240) v = tv.cascade(((256u - v) << 8) | (w16 & 255u));
-  return (v << 12) | (4u << 5) | tv.cascade(len_off + v);
+  return (v << 12) | (4u << 7) | tv.cascade(len_off + v);
 }
 
 // Exact walk of one 64-bit window: the code words that start in [gap, 64)
@@ -140,7 +150,7 @@ __device__ __forceinline__ void decode_window_exact(std::uint32_t w0, std::uint3
   while (p < 32) {
     std::uint32_t e = tb.fast(hi >> kFastShift);
     if (e & kSlowFlag) e = slow_entry(hi, tb, len_off);
-    sink.put(e >> 12, (e >> 5) & 31);
+    sink.put(e >> 12, entry_n4(e));
     hi = __funnelshift_l(lo, hi, e);
     lo = __funnelshift_l(0u, lo, e);
     p += e & 31;
@@ -159,7 +169,7 @@ __device__ __forceinline__ void decode_window_exact(std::uint32_t w0, std::uint3
       sink.put((e >> 12) & ((1u << k4) - 1), k4);
       return;
     }
-    sink.put(e >> 12, (e >> 5) & 31);
+    sink.put(e >> 12, entry_n4(e));
     hi = __funnelshift_l(lo, hi, e);
     lo = __funnelshift_l(0u, lo, e);
     p += b;
@@ -182,15 +192,16 @@ __device__ __forceinline__ bool decode_window_fast(std::uint32_t w0, std::uint32
                                                    const TV& tv, Sink& sink) {
   std::uint32_t hi = __funnelshift_l(w1, w0, gap);
   std::uint32_t lo = __funnelshift_l(w2, w1, gap);
-  std::uint32_t p = gap;  // + kSlowFlag once a flagged entry was met (ends the loops)
-  while (p < 32) {
+  std::uint32_t p = gap;  // adds whole staged entries: bits 0..6 exact, kSlowFlag ends the loop
+  while (!(p & kPhaseDone)) {
     const std::uint32_t e = fast_entry<OR_BASE>(fast, hi);
-    sink.put(e >> 12, (e >> 5) & 31);
+    sink.put(e >> 12, entry_n4(e));
     hi = __funnelshift_l(lo, hi, e);  // shift amount = e & 31 = bits consumed
     lo = __funnelshift_l(0u, lo, e);
-    p += e & (31u | kSlowFlag);
+    p += e;
   }
-  if (p >= 64) return false;
+  if (p & kSlowFlag) return false;
+  p &= 63;
   hi = __funnelshift_l(w2, w1, p - 32);  // p in [32, 44): window = bits [p, p + 64)
   lo = __funnelshift_l(w3, w2, p - 32);
   for (;;) {
@@ -203,7 +214,7 @@ __device__ __forceinline__ bool decode_window_fast(std::uint32_t w0, std::uint32
       sink.put((e >> 12) & ((1u << k4) - 1), k4);
       return true;
     }
-    sink.put(e >> 12, (e >> 5) & 31);
+    sink.put(e >> 12, entry_n4(e));
     hi = __funnelshift_l(lo, hi, e);
     lo = __funnelshift_l(0u, lo, e);
     p += b;
@@ -225,9 +236,10 @@ __device__ __forceinline__ bool decode_lane_continuous(const std::uint32_t (&w)[
                                                        Sink& sink) {
   std::uint32_t hi = __funnelshift_l(w[1], w[0], gap);
   std::uint32_t lo = __funnelshift_l(w[2], w[1], gap);
-  // p: bit position of hi's MSB within the current 32-bit phase.  A flagged
-  // entry adds kSlowFlag to it, which ends this and every later phase loop
-  // (p stays >= 32) -- no separate flag accumulator in the hot loop.
+  // p: bit position of hi's MSB within the current 32-bit phase (bits 0..6,
+  // the walk adds whole staged entries).  A flagged entry sets kSlowFlag,
+  // which ends this and -- kept through the phase steps -- every later phase
+  // loop: no separate flag accumulator in the hot loop.
   std::uint32_t p = gap;
   const std::uint32_t last = FULL ? 2 * NW - 1 : 2 * n - 1;  // FULL: n == NW known at compile time
 #pragma unroll
@@ -235,7 +247,8 @@ __device__ __forceinline__ bool decode_lane_continuous(const std::uint32_t (&w)[
     if (k == last) {
       // final half window: whole entries while they end before bit 32, then
       // the symbols that start before it (start mask + popcount)
-      if (p < 32) {
+      if (!(p & kPhaseDone)) {
+        p &= 31;
         for (;;) {
           const std::uint32_t idx = hi >> kFastShift;
           const std::uint32_t e = fast_entry<OR_BASE>(fast, hi);
@@ -249,7 +262,7 @@ __device__ __forceinline__ bool decode_lane_continuous(const std::uint32_t (&w)[
             sink.put((e >> 12) & ((1u << k4) - 1), k4);
             break;
           }
-          sink.put(e >> 12, (e >> 5) & 31);
+          sink.put(e >> 12, entry_n4(e));
           hi = __funnelshift_l(lo, hi, e);
           lo = __funnelshift_l(0u, lo, e);
           p += b;
@@ -257,20 +270,20 @@ __device__ __forceinline__ bool decode_lane_continuous(const std::uint32_t (&w)[
       }
       break;
     }
-    while (p < 32) {
+    while (!(p & kPhaseDone)) {
       const std::uint32_t e = fast_entry<OR_BASE>(fast, hi);
-      sink.put(e >> 12, (e >> 5) & 31);
+      sink.put(e >> 12, entry_n4(e));
       hi = __funnelshift_l(lo, hi, e);
       lo = __funnelshift_l(0u, lo, e);
-      p += e & (31u | kSlowFlag);
+      p += e;
     }
-    p -= 32;  // next phase: hi:lo = bits [32(k+1) + p, +64)
+    p = (p & kSlowFlag) ? kSlowFlag : (p & 63) - 32;  // next phase: hi:lo = bits [32(k+1) + p, +64)
     if (k + 3 < 2 * NW + 2) {
       hi = __funnelshift_l(w[k + 2], w[k + 1], p);
       lo = __funnelshift_l(w[k + 3], w[k + 2], p);
     }
   }
-  return p < 32;
+  return !(p & kSlowFlag);
 }
 
 // Where window (w0..w3, gap)'s reference walk stops: the start of the first
