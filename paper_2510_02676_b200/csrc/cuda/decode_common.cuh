@@ -16,7 +16,7 @@ constexpr int kFastShift = 32 - kFastBits;
 // Decode tables as staged in shared memory (see tables.hpp).  Entries of
 // the fast table whose first word is not resolvable from kFastBits bits are
 // rewritten on staging to the "flagged" form below.
-struct Tables {
+struct alignas(16) Tables {
   std::uint16_t smask[kFastEntries];
   std::uint8_t cascade[18 * 256];
   std::uint32_t fast[kFastEntries];  // last: decode_warp.cu places it at a 16 KB-aligned shared address
@@ -400,7 +400,9 @@ __device__ __forceinline__ void stage_tables(const TensorDesc& d, Tables& tb, in
   const uint4* m4 = reinterpret_cast<const uint4*>(d.smask);
   uint4* sm4 = reinterpret_cast<uint4*>(tb.smask);
   for (int i = tid; i < kFastEntries / 8; i += nthreads) sm4[i] = __ldg(m4 + i);
-  for (int i = tid; i < static_cast<int>(d.n_luts) * 256; i += nthreads) tb.cascade[i] = d.cascade[i];
+  const uint4* c4 = reinterpret_cast<const uint4*>(d.cascade);  // n_luts x 256 bytes, 16-byte aligned
+  uint4* sc4 = reinterpret_cast<uint4*>(tb.cascade);
+  for (int i = tid; i < static_cast<int>(d.n_luts) * 16; i += nthreads) sc4[i] = __ldg(c4 + i);
 }
 
 // Byte-wise write of output elements [lo, hi) (staging nibble coordinates)

@@ -115,7 +115,12 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_warp_kernel(const LaunchArg
     std::uint64_t seg_end;
     int di = 0;
     if (args.descs) {
-      di = find_desc(args.descs, args.n_desc, seg);
+      if (args.n_desc <= 32) {  // one parallel probe instead of a dependent binary search
+        const bool le = lane < args.n_desc && args.descs[lane].tile_begin <= seg;
+        di = 31 - __clz(__ballot_sync(0xffffffffu, le) | 1u);
+      } else {
+        di = find_desc(args.descs, args.n_desc, seg);
+      }
       seg_end = (di + 1 < args.n_desc) ? args.descs[di + 1].tile_begin : total_tiles;
     } else {
       seg_end = total_tiles;
@@ -124,7 +129,12 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_warp_kernel(const LaunchArg
     __syncthreads();  // every warp is done with the previous tables and descriptor
     // The segment's descriptor lives in shared memory, read field by field
     // where used: ~30 registers a register copy would pin for the whole loop.
-    if (threadIdx.x == 0) desc = args.descs ? args.descs[di] : args.inline_desc;
+    // Warp 0 copies it 8 bytes per lane.
+    if (warp == 0) {
+      static_assert(sizeof(TensorDesc) % 8 == 0 && sizeof(TensorDesc) <= 32 * 8, "descriptor copy");
+      const auto* src = reinterpret_cast<const unsigned long long*>(args.descs ? &args.descs[di] : &args.inline_desc);
+      if (lane < static_cast<int>(sizeof(TensorDesc) / 8)) reinterpret_cast<unsigned long long*>(&desc)[lane] = src[lane];
+    }
     __syncthreads();
     const TensorDesc& d = desc;
     const std::uint32_t log2T = 31 - __clz(d.T);
