@@ -153,12 +153,14 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_warp_kernel(const LaunchArg
     if (tile < seg_end) load_warp_tile(d, tile, log2T, lane, nxt);
     while (tile < seg_end) {
       const WarpIn cur = nxt;
+#ifndef ECF8_NO_PK_PREFETCH
       if (lane == 0) {  // sign/mantissa bytes of this tile -> L2 (one bulk TMA prefetch)
         const std::uint64_t p0 = (cur.A >> 1) & ~std::uint64_t{15};
         const std::uint32_t bytes = static_cast<std::uint32_t>((((cur.E + 1) >> 1) - p0 + 15) & ~std::uint64_t{15});
         if (bytes)
           asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(d.packed + p0), "r"(bytes) : "memory");
       }
+#endif
       unsigned claim = 0;
       if (lane == 0) claim = atomicAdd(&next_tile, 1u);
       const std::uint64_t next = seg + __shfl_sync(0xffffffffu, claim, 0);
