@@ -236,3 +236,33 @@ def test_inconsistent_gaps_fall_back_to_reference_semantics(orc):
     assert defined.sum() > 0.9 * t.n_elem
     assert np.array_equal(got[defined], want[defined])
     assert np.array_equal(codec.decode_parallel(t)[defined], want[defined])
+
+
+@pytest.mark.gpu
+def test_batch_decode_in_cuda_graph():
+    # the per-layer decode as a captured CUDA graph (programmatic dependent
+    # launches inside the graph), replayed: bit-exact every time
+    import torch
+
+    from paper_2510_02676_b200.device import Batch, DeviceTensor
+
+    xs = [codec.synth(1.8, 0.05, n, 60 + i) for i, n in enumerate((2_000_000, 750_001, 3_100_000))]
+    ds = [DeviceTensor(codec.encode_tensor(x, 256)) for x in xs]
+    outs = [torch.empty(x.size, dtype=torch.uint8, device="cuda") for x in xs]
+    b = Batch(ds, outs)
+    s = torch.cuda.Stream()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s):
+        b.decode(s)  # warm-up outside the capture (lazy attribute setup)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        b.decode(s)
+        b.decode(s)
+    for _ in range(3):
+        for o in outs:
+            o.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        for o, x in zip(outs, xs):
+            assert np.array_equal(o.cpu().numpy(), x)
