@@ -54,8 +54,8 @@ print(f"h2d {n_in / 1e6:.0f} MB: {n_in / t_in / 1e9:.1f} GB/s; d2h {n_out / 1e6:
       f"both: {t_both * 1e3:.2f} ms -> copy bound {algo / t_both / 1e9:.1f} GB/s (algorithmic)", flush=True)
 
 # chunked, with the host pipeline's coupling (4 slots: H2D of chunk k+4 waits
-# for the D2H of chunk k)
-for mb in (4, 8, 16, 32, 64):
+# for the D2H of chunk k) or without (a staging buffer per chunk)
+for mb, slots in ((8, 4), (16, 4), (32, 4), (4, 0), (8, 0), (16, 0), (32, 0)):
     c_out = mb << 20
     c_in = c_out * n_in // n_out
     nch = (n_out + c_out - 1) // c_out
@@ -67,8 +67,8 @@ for mb in (4, 8, 16, 32, 64):
         s2.wait_stream(torch.cuda.current_stream())
         for k in range(nch):
             with torch.cuda.stream(s1):
-                if k >= 4:
-                    s1.wait_event(ev_out[k - 4])
+                if slots and k >= slots:
+                    s1.wait_event(ev_out[k - slots])
                 a, b = k * c_in, min(n_in, (k + 1) * c_in)
                 if b > a:
                     d_in[a:b].copy_(h_in[a:b], non_blocking=True)
@@ -80,4 +80,4 @@ for mb in (4, 8, 16, 32, 64):
                 ev_out[k].record(s2)
 
     t = timed(chunked)
-    print(f"chunks of {mb} MB out ({nch}): {t * 1e3:.2f} ms -> {algo / t / 1e9:.1f} GB/s", flush=True)
+    print(f"chunks of {mb} MB out ({nch}), {slots or 'unbounded'} slots: {t * 1e3:.2f} ms -> {algo / t / 1e9:.1f} GB/s", flush=True)
