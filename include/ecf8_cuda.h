@@ -107,6 +107,26 @@ uint64_t ecf8_tensor_verified_tiles(const ecf8_dev_tensor *t, uint64_t *total);
 uint64_t ecf8_tensor_algorithmic_bytes(const ecf8_dev_tensor *t);
 uint64_t ecf8_tensor_device_bytes(const ecf8_dev_tensor *t);
 
+/* ---- device encoder -------------------------------- */
+
+/* make_stats' exponent histogram (container.cpp:386-413, ExponentHistogram::
+ * of_bytes) of n FP8 bytes in device memory; counts[16] on the host.
+ * Synchronises `stream`. */
+int ecf8_exponent_histogram(const uint8_t *d_fp8, uint64_t n, uint64_t counts[16], void *stream);
+/* encode_tensor (codec.cpp:49-98 + the nibble split, fp8.hpp:24-57) of n FP8
+ * bytes in device memory with the canonical code of `lengths`, straight into
+ * a device-resident tensor (same sections, byte for byte, as the host
+ * encoder + ecf8_tensor_upload).  Errors as the reference: "invalid length
+ * vector", "symbol absent from code table", bad T (ECF8_EINVAL).
+ * Synchronises `stream` (the code-bit total sizes the arena). */
+int ecf8_encode_device(const uint8_t *d_fp8, uint64_t n, uint32_t T, const uint8_t lengths[16], void *stream,
+                       ecf8_dev_tensor **out);
+/* The tensor's sections: sizes, T, lengths, and DEVICE pointers. */
+int ecf8_tensor_sections(const ecf8_dev_tensor *t, ecf8_sections *out);
+/* Copy sections to host buffers sized by ecf8_tensor_sections (NULL skips). */
+int ecf8_tensor_download(const ecf8_dev_tensor *t, uint8_t *encoded, uint8_t *gaps, uint64_t *outpos,
+                         uint8_t *packed);
+
 /* Decode into device memory d_out (n_elem bytes, 16-byte aligned). */
 int ecf8_decode_device(const ecf8_dev_tensor *t, uint8_t *d_out, void *stream);
 

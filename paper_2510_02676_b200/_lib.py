@@ -88,6 +88,10 @@ _SIGS = {
     "ecf8_count_window": (C.c_int, [_P, C.c_uint, _P, _U32P]),
     "ecf8_tensor_upload": (C.c_int, [C.POINTER(Sections), _P, C.POINTER(_P)]),
     "ecf8_tensor_free": (None, [_P]),
+    "ecf8_exponent_histogram": (C.c_int, [_P, C.c_uint64, _U64P, _P]),
+    "ecf8_encode_device": (C.c_int, [_P, C.c_uint64, C.c_uint32, _P, _P, C.POINTER(_P)]),
+    "ecf8_tensor_sections": (C.c_int, [_P, C.POINTER(Sections)]),
+    "ecf8_tensor_download": (C.c_int, [_P, _P, _P, _P, _P]),
     "ecf8_tensor_n_elem": (C.c_uint64, [_P]),
     "ecf8_tensor_kernel_variant": (C.c_int, [_P]),
     "ecf8_tensor_verified_tiles": (C.c_uint64, [_P, C.POINTER(C.c_uint64)]),

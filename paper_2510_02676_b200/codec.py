@@ -141,7 +141,7 @@ class _HostTensor:
         self.handle = handle
 
     def __del__(self):
-        if self.handle:
+        if self.handle and lib is not None:  # lib is None during interpreter teardown
             lib.ecf8_host_tensor_free(self.handle)
             self.handle = None
 

@@ -20,6 +20,8 @@
 #include <vector>
 
 #include "decode.cuh"
+#include "encode.cuh"
+#include "ecf8/huffman.hpp"
 #include "fused_gemm.cuh"
 #include "ecf8_cuda.h"
 #include "tables.hpp"
@@ -163,7 +165,20 @@ struct ecf8_dev_tensor {
   std::uint64_t n_vtiles = 0;      // 256-window verification tiles (tile_ok bits)
   std::uint32_t* ok_bits = nullptr;  // their bitmap in the arena
   TensorDesc desc{};     // out / tile fields filled per launch
+  std::uint64_t encoded_len = 0, gaps_len = 0, n_outpos = 0, packed_len = 0;
+  std::uint8_t lengths[16] = {};
+  bool pooled = false;  // arena from the stream-ordered pool (device encoder)
 };
+
+void free_arena(ecf8_dev_tensor* t) {
+  if (!t->arena) return;
+  if (t->pooled) {
+    cudaDeviceSynchronize();  // like cudaFree: no launch on any stream may still read it
+    cudaFreeAsync(t->arena, nullptr);  // back to the pool (kept mapped)
+  } else
+    cudaFree(t->arena);
+  t->arena = nullptr;
+}
 
 struct ecf8_fused {
   const ecf8_dev_tensor* w = nullptr;
@@ -188,7 +203,11 @@ struct ecf8_batch {
 
 namespace {
 
-void upload_into(ecf8_dev_tensor* t, const ecf8_sections* s, std::uint64_t nb, cudaStream_t st) {
+// The tensor's HBM arena for sections of the sizes in *s (pointers unused):
+// allocated, zeroed on `st`, descriptor filled.  The caller fills the
+// sections (H2D copies, or the device encoder).
+void alloc_arena(ecf8_dev_tensor* t, const ecf8_sections* s, std::uint64_t nb, cudaStream_t st,
+                 bool pooled = false) {
   const std::uint64_t P = ecf8::dev::kPad;
   const std::uint64_t off_enc = 0;
   const std::uint64_t off_gap = align_up(off_enc + s->encoded_len + P, 256);
@@ -197,16 +216,35 @@ void upload_into(ecf8_dev_tensor* t, const ecf8_sections* s, std::uint64_t nb, c
   const std::uint64_t n_vtiles = (nb * s->threads_per_block + 255) / 256;
   const std::uint64_t off_ok = align_up(off_pak + s->packed_len + P, 256);
   const std::uint64_t total = align_up(off_ok + 4 * ((n_vtiles + 31) / 32), 256);
-  cu(cudaMalloc(&t->arena, total), "cudaMalloc(tensor)");
+  if (pooled) {
+    // stream-ordered pool (the device encoder: many tensors created and
+    // dropped in a row; cudaMalloc/cudaFree cost ~1 ms each at 50 MB)
+    static const bool keep = [] {
+      int dev = 0;
+      cudaMemPool_t pool;
+      if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        std::uint64_t thr = ~std::uint64_t{0};
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      }
+      cudaGetLastError();
+      return true;
+    }();
+    (void)keep;
+    cu(cudaMallocAsync(&t->arena, total, st), "cudaMallocAsync(tensor)");
+    t->pooled = true;
+  } else {
+    cu(cudaMalloc(&t->arena, total), "cudaMalloc(tensor)");
+  }
   t->arena_bytes = total;
   auto* base = static_cast<std::uint8_t*>(t->arena);
   cu(cudaMemsetAsync(base, 0, total, st), "cudaMemset");
-  cu(cudaMemcpyAsync(base + off_enc, s->encoded, s->encoded_len, cudaMemcpyHostToDevice, st), "H2D encoded");
-  if (s->gaps_len) cu(cudaMemcpyAsync(base + off_gap, s->gaps, s->gaps_len, cudaMemcpyHostToDevice, st), "H2D gaps");
-  cu(cudaMemcpyAsync(base + off_pos, s->outpos, 8 * s->n_outpos, cudaMemcpyHostToDevice, st), "H2D outpos");
-  if (s->packed_len) cu(cudaMemcpyAsync(base + off_pak, s->packed, s->packed_len, cudaMemcpyHostToDevice, st), "H2D packed");
   t->n_vtiles = n_vtiles;
   t->ok_bits = reinterpret_cast<std::uint32_t*>(base + off_ok);
+  t->encoded_len = s->encoded_len;
+  t->gaps_len = s->gaps_len;
+  t->n_outpos = s->n_outpos;
+  t->packed_len = s->packed_len;
+  std::memcpy(t->lengths, s->lengths, 16);
 
   t->n_elem = s->n_elem;
   t->n_blocks = nb;
@@ -230,6 +268,21 @@ void upload_into(ecf8_dev_tensor* t, const ecf8_sections* s, std::uint64_t nb, c
     d.n_luts = tb.n_luts;
     d.lenpack = tb.lenpack;
   }
+}
+
+void upload_into(ecf8_dev_tensor* t, const ecf8_sections* s, std::uint64_t nb, cudaStream_t st) {
+  alloc_arena(t, s, nb, st);
+  const TensorDesc& d = t->desc;
+  cu(cudaMemcpyAsync(const_cast<std::uint8_t*>(d.encoded), s->encoded, s->encoded_len, cudaMemcpyHostToDevice, st),
+     "H2D encoded");
+  if (s->gaps_len)
+    cu(cudaMemcpyAsync(const_cast<std::uint8_t*>(d.gaps), s->gaps, s->gaps_len, cudaMemcpyHostToDevice, st),
+       "H2D gaps");
+  cu(cudaMemcpyAsync(const_cast<std::uint64_t*>(d.outpos), s->outpos, 8 * s->n_outpos, cudaMemcpyHostToDevice, st),
+     "H2D outpos");
+  if (s->packed_len)
+    cu(cudaMemcpyAsync(const_cast<std::uint8_t*>(d.packed), s->packed, s->packed_len, cudaMemcpyHostToDevice, st),
+       "H2D packed");
 }
 
 // Gap check at upload (verify_gaps_kernel): tiles whose windows all end where
@@ -470,7 +523,7 @@ int ecf8_tensor_upload(const ecf8_sections* s, void* stream, ecf8_dev_tensor** o
       upload_into(t.get(), s, nb, static_cast<cudaStream_t>(stream));
       verify_into(t.get(), static_cast<cudaStream_t>(stream));
     } catch (...) {
-      if (t->arena) cudaFree(t->arena);
+      free_arena(t.get());
       throw;
     }
     *out = t.release();
@@ -478,9 +531,176 @@ int ecf8_tensor_upload(const ecf8_sections* s, void* stream, ecf8_dev_tensor** o
   });
 }
 
+namespace {
+// Per-thread device scratch of the encoder (grow-only, never freed: see
+// HostCtx) and a pinned readback word block.
+struct EncScratch {
+  int dev = -1;
+  std::uint8_t* buf = nullptr;
+  std::uint64_t cap = 0;
+  unsigned long long* host = nullptr;  // pinned, 32 words
+  cudaEvent_t free_at = nullptr;       // recorded after the last reader of buf
+};
+// `st` waits until the previous user of the scratch (any stream) is done.
+EncScratch& enc_scratch(std::uint64_t need, cudaStream_t st) {
+  thread_local EncScratch e;
+  int dev = 0;
+  cu(cudaGetDevice(&dev), "cudaGetDevice");
+  if (e.dev != dev) {
+    e = EncScratch{};
+    cu(cudaMallocHost(reinterpret_cast<void**>(&e.host), 32 * sizeof(unsigned long long)), "cudaMallocHost");
+    cu(cudaEventCreateWithFlags(&e.free_at, cudaEventDisableTiming), "event");
+    cu(cudaEventRecord(e.free_at, st), "record");
+    e.dev = dev;
+  }
+  cu(cudaStreamWaitEvent(st, e.free_at, 0), "wait");
+  if (need > e.cap) {
+    if (e.buf) {
+      cu(cudaDeviceSynchronize(), "sync");
+      cudaFree(e.buf);
+      e.buf = nullptr;
+      e.cap = 0;
+    }
+    const std::uint64_t cap = std::max<std::uint64_t>(need + (need >> 1), 1 << 20);
+    cu(cudaMalloc(&e.buf, cap), "cudaMalloc(encode scratch)");
+    e.cap = cap;
+  }
+  return e;
+}
+}  // namespace
+
+int ecf8_exponent_histogram(const uint8_t* d_fp8, uint64_t n, uint64_t counts[16], void* stream) {
+  return guarded([&]() -> int {
+    if (!counts || (n && !d_fp8)) return fail(ECF8_EINVAL, "null argument");
+    if (int rc = require_device()) return rc;
+    const auto st = static_cast<cudaStream_t>(stream);
+    EncScratch& sc = enc_scratch(256, st);
+    auto* d_counts = reinterpret_cast<unsigned long long*>(sc.buf);
+    cu(cudaMemsetAsync(d_counts, 0, 16 * sizeof(unsigned long long), st), "cudaMemset");
+    cu(ecf8::dev::launch_exponent_histogram(d_fp8, n, d_counts, st), "histogram launch");
+    cu(cudaMemcpyAsync(sc.host, d_counts, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st), "D2H");
+    cu(cudaEventRecord(sc.free_at, st), "record");
+    cu(cudaStreamSynchronize(st), "sync");
+    for (int i = 0; i < 16; ++i) counts[i] = sc.host[i];
+    return ECF8_OK;
+  });
+}
+
+int ecf8_encode_device(const uint8_t* d_fp8, uint64_t n, uint32_t T, const uint8_t lengths[16], void* stream,
+                       ecf8_dev_tensor** out) {
+  return guarded([&]() -> int {
+    if (!out || !lengths || (n && !d_fp8)) return fail(ECF8_EINVAL, "null argument");
+    *out = nullptr;
+    if (T < 1 || T > 1024 || (T & (T - 1)))
+      return fail(ECF8_EINVAL, "threads per block must be a power of two in [1, 1024]");
+    std::array<std::uint8_t, 16> lv{};
+    std::memcpy(lv.data(), lengths, 16);
+    const ecf8::CodeTable code = ecf8::canonical_codes(lv);  // "invalid length vector" (huffman.cpp:137-142)
+    if (int rc = require_device()) return rc;
+    const auto st = static_cast<cudaStream_t>(stream);
+    const std::uint64_t n_chunks = (n + ecf8::dev::kEncChunkElems - 1) / ecf8::dev::kEncChunkElems;
+
+    // passes 1-2: code bits per chunk, their scan, the total (one sync: it sizes the arena)
+    const std::uint64_t off_start = align_up(4 * n_chunks, 256), off_tot = off_start + align_up(8 * n_chunks, 256);
+    EncScratch& sc = enc_scratch(off_tot + 256, st);
+    std::uint8_t* const work = sc.buf;
+    auto* chunk_bits = reinterpret_cast<std::uint32_t*>(work);
+    auto* chunk_start = reinterpret_cast<std::uint64_t*>(work + off_start);
+    auto* d_total = reinterpret_cast<unsigned long long*>(work + off_tot);
+    auto* d_bad = reinterpret_cast<std::uint32_t*>(work + off_tot + 8);
+    std::uint8_t* d_len = work + off_tot + 16;
+    cu(cudaMemsetAsync(work + off_tot, 0, 16, st), "cudaMemset");
+    cu(cudaMemcpyAsync(d_len, lengths, 16, cudaMemcpyHostToDevice, st), "H2D lengths");
+    cu(ecf8::dev::launch_encode_sizes(d_fp8, n, d_len, chunk_bits, chunk_start, d_total, d_bad, st), "encode sizes");
+    cu(cudaMemcpyAsync(sc.host, d_total, 16, cudaMemcpyDeviceToHost, st), "D2H total");
+    cu(cudaStreamSynchronize(st), "sync");
+    const unsigned long long tot_bad[2] = {sc.host[0], sc.host[1]};
+    if (tot_bad[1] & 0xFFFFFFFFu) {
+      cu(cudaEventRecord(sc.free_at, st), "record");
+      return fail(ECF8_EINVAL, "symbol absent from code table");  // codec.cpp:53
+    }
+
+    // geometry (make_geometry, codec.cpp:39-47) and the arena
+    const std::uint64_t bits = tot_bad[0];
+    const std::uint64_t bytes = (bits + 7) / 8, bb = std::uint64_t{T} * 8;
+    const std::uint64_t nb = bytes / bb + (bytes % bb != 0);
+    ecf8_sections sz{};
+    sz.n_elem = n;
+    sz.threads_per_block = T;
+    std::memcpy(sz.lengths, lengths, 16);
+    sz.encoded_len = nb * bb + 2;
+    sz.gaps_len = (nb * T + 1) / 2;
+    sz.n_outpos = nb + 1;
+    sz.packed_len = (n + 1) / 2;
+    auto t = std::make_unique<ecf8_dev_tensor>();
+    try {
+      alloc_arena(t.get(), &sz, nb, st, true);
+      t->n_elem = n;
+      t->n_blocks = nb;
+      t->T = T;
+      t->algo_bytes = sz.encoded_len + sz.gaps_len + 8 * sz.n_outpos + sz.packed_len + n;
+      if (n) {
+        ecf8::dev::EncodeArgs a{};
+        a.fp8 = d_fp8;
+        a.n = n;
+        a.chunk_start = chunk_start;
+        a.encoded = reinterpret_cast<std::uint32_t*>(const_cast<std::uint8_t*>(t->desc.encoded));
+        a.gaps = reinterpret_cast<std::uint32_t*>(const_cast<std::uint8_t*>(t->desc.gaps));
+        a.outpos = const_cast<std::uint64_t*>(t->desc.outpos);
+        a.packed = const_cast<std::uint8_t*>(t->desc.packed);
+        a.n_blocks = nb;
+        a.log2T = static_cast<std::uint32_t>(31 - __builtin_clz(T));
+        for (int i = 0; i < 16; ++i) {
+          a.lengths[i] = lengths[i];
+          a.codes[i] = code.codes[i];
+        }
+        cu(ecf8::dev::launch_encode_emit(a, st), "encode emit");
+      }
+      cu(cudaEventRecord(sc.free_at, st), "record");  // chunk_start read
+      verify_into(t.get(), st);
+    } catch (...) {
+      free_arena(t.get());
+      throw;
+    }
+    *out = t.release();
+    return ECF8_OK;
+  });
+}
+
+int ecf8_tensor_sections(const ecf8_dev_tensor* t, ecf8_sections* out) {
+  if (!t || !out) return fail(ECF8_EINVAL, "null argument");
+  ecf8_sections s{};
+  s.n_elem = t->n_elem;
+  s.threads_per_block = t->T;
+  std::memcpy(s.lengths, t->lengths, 16);
+  s.encoded = t->desc.encoded;
+  s.encoded_len = t->encoded_len;
+  s.gaps = t->desc.gaps;
+  s.gaps_len = t->gaps_len;
+  s.outpos = t->desc.outpos;
+  s.n_outpos = t->n_outpos;
+  s.packed = t->desc.packed;
+  s.packed_len = t->packed_len;
+  *out = s;
+  return ECF8_OK;
+}
+
+int ecf8_tensor_download(const ecf8_dev_tensor* t, uint8_t* encoded, uint8_t* gaps, uint64_t* outpos,
+                         uint8_t* packed) {
+  return guarded([&]() -> int {
+    if (!t) return fail(ECF8_EINVAL, "null tensor");
+    const TensorDesc& d = t->desc;
+    if (encoded) cu(cudaMemcpy(encoded, d.encoded, t->encoded_len, cudaMemcpyDeviceToHost), "D2H encoded");
+    if (gaps && t->gaps_len) cu(cudaMemcpy(gaps, d.gaps, t->gaps_len, cudaMemcpyDeviceToHost), "D2H gaps");
+    if (outpos) cu(cudaMemcpy(outpos, d.outpos, 8 * t->n_outpos, cudaMemcpyDeviceToHost), "D2H outpos");
+    if (packed && t->packed_len) cu(cudaMemcpy(packed, d.packed, t->packed_len, cudaMemcpyDeviceToHost), "D2H packed");
+    return ECF8_OK;
+  });
+}
+
 void ecf8_tensor_free(ecf8_dev_tensor* t) {
   if (!t) return;
-  if (t->arena) cudaFree(t->arena);
+  free_arena(t);
   delete t;
 }
 

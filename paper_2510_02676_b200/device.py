@@ -8,10 +8,31 @@ from __future__ import annotations
 
 import ctypes as C
 
+import numpy as np
 import torch
 
-from ._lib import check, lib
-from .codec import EncodedTensor
+from ._lib import Sections, check, lib
+from .codec import EncodedTensor, build_code
+
+
+def _fp8_bytes(x: torch.Tensor) -> torch.Tensor:
+    if not x.is_cuda:
+        raise ValueError("expected a CUDA tensor")
+    if x.dtype in (torch.float8_e4m3fn, torch.float8_e5m2):
+        x = x.view(torch.uint8)
+    if x.dtype != torch.uint8:
+        raise ValueError("expected FP8 or uint8 bytes")
+    return x.contiguous().reshape(-1)
+
+
+def exponent_histogram(x: torch.Tensor, stream: torch.cuda.Stream | None = None) -> np.ndarray:
+    """ecf8_exponent_histogram: counts of the 16 exponent-field values
+    (ExponentHistogram::of_bytes, the first step of make_stats) on the GPU."""
+    x = _fp8_bytes(x)
+    counts = np.zeros(16, np.uint64)
+    check(lib.ecf8_exponent_histogram(C.c_void_p(x.data_ptr() if x.numel() else None), x.numel(),
+                                      counts.ctypes.data_as(C.POINTER(C.c_uint64)), _stream_ptr(stream)))
+    return counts
 
 
 def _stream_ptr(stream: torch.cuda.Stream | None) -> int | None:
@@ -23,15 +44,51 @@ class DeviceTensor:
     """ecf8_tensor_upload: container sections + decode tables in HBM."""
 
     def __init__(self, t: EncodedTensor, stream: torch.cuda.Stream | None = None):
-        self.n_elem = t.n_elem
         self._sections = t.sections()
         self._src = t  # keep host arrays alive until the async copy completes
         h = C.c_void_p()
         check(lib.ecf8_tensor_upload(C.byref(self._sections), _stream_ptr(stream), C.byref(h)))
+        self._adopt(h)
+
+    def _adopt(self, h: C.c_void_p) -> None:
         self.handle = h
+        self.n_elem = int(lib.ecf8_tensor_n_elem(h))
         self.algorithmic_bytes = int(lib.ecf8_tensor_algorithmic_bytes(h))
         self.device_bytes = int(lib.ecf8_tensor_device_bytes(h))
         self.kernel_variant = int(lib.ecf8_tensor_kernel_variant(h))
+
+    @classmethod
+    def encode(cls, x: torch.Tensor, lengths=None, threads_per_block: int = 256,
+               stream: torch.cuda.Stream | None = None) -> "DeviceTensor":
+        """ecf8_encode_device: encode_tensor (codec.cpp:49-98) of a CUDA FP8 /
+        uint8 tensor on the GPU, straight into HBM.  lengths=None builds the
+        code from the GPU exponent histogram (host build_code, huffman.cpp)."""
+        x = _fp8_bytes(x)
+        if lengths is None:
+            lengths = build_code(exponent_histogram(x, stream))
+        lv = np.ascontiguousarray(np.asarray(lengths, dtype=np.uint8))
+        if lv.size != 16:
+            raise ValueError("invalid length vector")
+        h = C.c_void_p()
+        check(lib.ecf8_encode_device(C.c_void_p(x.data_ptr() if x.numel() else None), x.numel(), threads_per_block,
+                                     lv.ctypes.data_as(C.c_void_p), _stream_ptr(stream), C.byref(h)))
+        self = cls.__new__(cls)
+        self._src = None
+        self._adopt(h)
+        return self
+
+    def to_host(self) -> EncodedTensor:
+        """The tensor's container sections, copied back to host memory."""
+        s = Sections()
+        check(lib.ecf8_tensor_sections(self.handle, C.byref(s)))
+        enc = np.empty(s.encoded_len, np.uint8)
+        gaps = np.empty(s.gaps_len, np.uint8)
+        outpos = np.empty(s.n_outpos, np.uint64)
+        packed = np.empty(s.packed_len, np.uint8)
+        check(lib.ecf8_tensor_download(self.handle, enc.ctypes.data_as(C.c_void_p), gaps.ctypes.data_as(C.c_void_p),
+                                       outpos.ctypes.data_as(C.c_void_p), packed.ctypes.data_as(C.c_void_p)))
+        return EncodedTensor(int(s.n_elem), int(s.threads_per_block), np.array(list(s.lengths), np.uint8), enc, gaps,
+                             outpos, packed)
 
     def verified_tiles(self) -> tuple[int, int]:
         """(tiles decoded by the continuous group walk, all 256-window tiles)."""
