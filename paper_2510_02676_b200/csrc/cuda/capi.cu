@@ -650,10 +650,8 @@ int ecf8_encode_device(const uint8_t* d_fp8, uint64_t n, uint32_t T, const uint8
         a.packed = const_cast<std::uint8_t*>(t->desc.packed);
         a.n_blocks = nb;
         a.log2T = static_cast<std::uint32_t>(31 - __builtin_clz(T));
-        for (int i = 0; i < 16; ++i) {
-          a.lengths[i] = lengths[i];
-          a.codes[i] = code.codes[i];
-        }
+        for (int i = 0; i < 16; ++i)
+          a.lc[i] = lengths[i] ? (static_cast<std::uint32_t>(code.codes[i]) << (32 - lengths[i])) | lengths[i] : 0u;
         cu(ecf8::dev::launch_encode_emit(a, st), "encode emit");
       }
       cu(cudaEventRecord(sc.free_at, st), "record");  // chunk_start read

@@ -150,10 +150,16 @@ __global__ void __launch_bounds__(1024) chunk_scan_kernel(const std::uint32_t* _
 __global__ void __launch_bounds__(256) encode_emit_kernel(const EncodeArgs a) {
   constexpr int kWords = (kEncChunkElems * 16 + 31) / 32 + 2;  // the chunk's bit run + misalignment
   __shared__ std::uint32_t run[kWords];
-  __shared__ std::uint32_t s_lc[16];  // code | length << 16
+  __shared__ std::uint32_t s_lc[16];  // code MSB-aligned | length (low 5 bits: the code is <= 16 bits)
   __shared__ std::uint32_t wsum[8];
   const std::uint32_t t = threadIdx.x;
-  if (t < 16) s_lc[t] = a.codes[t] | (static_cast<std::uint32_t>(a.lengths[t]) << 16);
+  if (t < 16) {
+    std::uint32_t v = 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i)  // static indices: the parameter array stays in param space
+      if (static_cast<int>(t) == i) v = a.lc[i];
+    s_lc[t] = v;
+  }
   for (int i = t; i < kWords; i += kEncThreads) run[i] = 0;
   const std::uint64_t e_begin = blockIdx.x * static_cast<std::uint64_t>(kEncChunkElems);
   const std::uint64_t e0 = e_begin + kPerThread * t;
@@ -186,52 +192,55 @@ __global__ void __launch_bounds__(256) encode_emit_kernel(const EncodeArgs a) {
   std::uint32_t my_bits = 0;
 #pragma unroll
   for (int j = 0; j < 16; ++j)
-    if (j < static_cast<int>(cnt)) my_bits += s_lc[exp_of(x[j])] >> 16;
+    if (j < static_cast<int>(cnt)) my_bits += s_lc[exp_of(x[j])] & 31u;
   std::uint32_t chunk_total;
   const std::uint32_t excl = block_excl_scan(my_bits, wsum, &chunk_total);
   const std::uint64_t gw0 = cs >> 5;  // first global word of the chunk's run
-  std::uint64_t p = cs + excl;        // my first code's start bit
 
   if (cnt) {
+    // 32-bit positions relative to B = the chunk start rounded down to a
+    // window: window and block changes are bit changes of lp ^ prev.
+    const std::uint64_t B = cs & ~std::uint64_t{63};
     const std::uint32_t blk_shift = 6 + a.log2T;
-    std::uint32_t len_prev = e0 ? (s_lc[exp_of(x_prev)] >> 16) : 0;
-    const std::uint64_t lb = p - (gw0 << 5);
-    std::uint32_t word = static_cast<std::uint32_t>(lb >> 5);
-    std::uint32_t fill = static_cast<std::uint32_t>(lb & 31);
-    std::uint64_t acc = 0;
-    std::uint64_t last_start = p;
+    const std::uint32_t boff = static_cast<std::uint32_t>(B & ((std::uint64_t{1} << blk_shift) - 1));
+    std::uint32_t lp = static_cast<std::uint32_t>(cs - B) + excl;  // my first code's start
+    // previous code's length (element 0: a fake 64 marks its window as new)
+    std::uint32_t len_prev = e0 ? (s_lc[exp_of(x_prev)] & 31u) : 64u;
+    const std::uint32_t lb = static_cast<std::uint32_t>(cs & 31) + excl;  // bit offset in run[]
+    std::uint32_t word = lb >> 5, fill = lb & 31, cur = 0;
+    std::uint32_t lp_last = lp;
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       if (j < static_cast<int>(cnt)) {
         const std::uint32_t lc = s_lc[exp_of(x[j])];
-        const std::uint32_t len = lc >> 16;
-        const std::uint64_t idx = e0 + j;
-        const std::uint64_t w = p >> 6;
-        const std::uint64_t prev = p - len_prev;  // previous code's start (idx > 0)
-        if (idx == 0 || (prev >> 6) != w) {
-          // first code starting in window w: its gap nibble
+        const std::uint32_t len = lc & 31u, val = lc & ~31u;  // code MSB-aligned
+        const std::uint32_t prev = lp - len_prev;             // previous code's start (mod 2^32)
+        if ((lp ^ prev) >> 6) {
+          // first code starting in window B/64 + lp/64: its gap nibble
+          const std::uint64_t w = (B >> 6) + (lp >> 6);
           const std::uint64_t gb = w >> 1;
-          const std::uint32_t v = static_cast<std::uint32_t>(p & 63) << ((w & 1) ? 0 : 4);
+          const std::uint32_t v = (lp & 63) << ((w & 1) ? 0 : 4);
           if (v) atomicOr(a.gaps + (gb >> 2), v << (8 * (gb & 3)));
         }
-        if (idx != 0 && (prev >> blk_shift) != (p >> blk_shift)) a.outpos[p >> blk_shift] = idx;
-        acc |= static_cast<std::uint64_t>(lc & 0xFFFFu) << (64 - fill - len);
+        if (((lp + boff) ^ (prev + boff)) >> blk_shift) a.outpos[(B + lp) >> blk_shift] = e0 + j;
+        cur |= val >> fill;
+        const std::uint32_t spill = fill ? val << (32 - fill) : 0u;
         fill += len;
         if (fill >= 32) {
-          atomicOr(&run[word], static_cast<std::uint32_t>(acc >> 32));
-          acc <<= 32;
+          atomicOr(&run[word], cur);
+          cur = spill;
           fill -= 32;
           ++word;
         }
-        last_start = p;
-        p += len;
+        lp_last = lp;
+        lp += len;
         len_prev = len;
       }
     }
-    if (fill) atomicOr(&run[word], static_cast<std::uint32_t>(acc >> 32));
+    if (fill) atomicOr(&run[word], cur);
     if (e0 + cnt == a.n) {
       // blocks after the last code's: no code starts there
-      for (std::uint64_t b = (last_start >> blk_shift) + 1; b <= a.n_blocks; ++b) a.outpos[b] = a.n;
+      for (std::uint64_t b = ((B + lp_last) >> blk_shift) + 1; b <= a.n_blocks; ++b) a.outpos[b] = a.n;
     }
   }
   __syncthreads();

@@ -30,8 +30,7 @@ struct EncodeArgs {
   std::uint8_t* packed;    // 8-byte aligned
   std::uint64_t n_blocks;
   std::uint32_t log2T;
-  std::uint8_t lengths[16];
-  std::uint16_t codes[16];
+  std::uint32_t lc[16];  // code << (32 - length) | length (0 for absent symbols)
 };
 // Pass 3: bitstream, gaps, outpos and packed nibbles.
 cudaError_t launch_encode_emit(const EncodeArgs& a, cudaStream_t s);
