@@ -40,7 +40,28 @@ constexpr std::uint32_t kPhaseDone = 0x60u;  // position bits 5..6: past bit 32 
 __host__ __device__ constexpr std::uint32_t stage_entry(std::uint32_t e) {
   return ((e >> 5) & 31) ? ((e & 0xFFFFF01Fu) | (((e >> 5) & 31u) << 7)) : kSlowFlag;
 }
-__host__ __device__ constexpr std::uint32_t entry_n4(std::uint32_t e) { return (e >> 7) & 31u; }
+__host__ __device__ constexpr std::uint32_t entry_n4_ref(std::uint32_t e) { return (e >> 7) & 31u; }
+
+// Integer multiplies the compiler must keep: IMAD runs on the FMA pipe, so a
+// shift-left by multiply (plus the right shift or LEA.HI that follows)
+// replaces a shift + LOP3 mask pair on the ALU pipe, which the walk keeps
+// ~70 % busy.  ECF8_ALU_MASKS=1 restores the plain expressions (A/B).
+#ifndef ECF8_ALU_MASKS
+#define ECF8_ALU_MASKS 0
+#endif
+template <std::uint32_t M>
+__device__ __forceinline__ std::uint32_t imul(std::uint32_t x) {
+  std::uint32_t r;
+  asm("mul.lo.u32 %0, %1, %2;" : "=r"(r) : "r"(x), "n"(M));
+  return r;
+}
+__device__ __forceinline__ std::uint32_t entry_n4(std::uint32_t e) {
+#if ECF8_ALU_MASKS
+  return entry_n4_ref(e);
+#else
+  return imul<1u << 20>(e) >> 27;  // bits 7..11
+#endif
+}
 
 // Shared-memory accesses by 32-bit shared-window address: one register per
 // address and no generic-to-shared conversion in the hot loops.
@@ -68,7 +89,11 @@ __device__ __forceinline__ void sts32(std::uint32_t a, std::uint32_t v) {
 constexpr std::uint32_t kFastAt = 0x4000;
 template <bool FIXED>
 __device__ __forceinline__ std::uint32_t fast_entry(std::uint32_t fast, std::uint32_t hi) {
+#if ECF8_ALU_MASKS
   const std::uint32_t off = (hi >> (kFastShift - 2)) & ~3u;
+#else
+  const std::uint32_t off = imul<4>(hi >> kFastShift);
+#endif
   if constexpr (FIXED) {
     std::uint32_t v;  // constant in the load's immediate (ptxas would otherwise OR it in)
     asm volatile("ld.shared.u32 %0, [%1+16384];" : "=r"(v) : "r"(off));
