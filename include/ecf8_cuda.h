@@ -121,6 +121,21 @@ int ecf8_exponent_histogram(const uint8_t *d_fp8, uint64_t n, uint64_t counts[16
  * Synchronises `stream` (the code-bit total sizes the arena). */
 int ecf8_encode_device(const uint8_t *d_fp8, uint64_t n, uint32_t T, const uint8_t lengths[16], void *stream,
                        ecf8_dev_tensor **out);
+/* One tensor's make_stats report (EntropyReport, entropy.hpp; the name is
+ * the caller's). */
+typedef struct ecf8_entropy_report {
+  uint64_t n_elem;
+  double entropy_bits, bits_per_symbol, bits_per_weight;
+  double bound_lower, bound_upper; /* entropy_bounds(2.0) */
+  double projected_savings, actual_savings;
+} ecf8_entropy_report;
+/* make_stats (container.cpp:386-413) for one tensor whose FP8 bytes are in
+ * device memory: histogram and encode on the GPU, the code and the entropy
+ * arithmetic on the host.  name_len and rank (>= 1) give the container
+ * overhead that actual_savings counts (tensor_section_bytes).  Same numbers
+ * as ecf8_host_make_stats.  Synchronises `stream`. */
+int ecf8_make_stats_device(const uint8_t *d_fp8, uint64_t n, uint32_t T, uint32_t name_len, uint32_t rank,
+                           void *stream, ecf8_entropy_report *out);
 /* The tensor's sections: sizes, T, lengths, and DEVICE pointers. */
 int ecf8_tensor_sections(const ecf8_dev_tensor *t, ecf8_sections *out);
 /* Copy sections to host buffers sized by ecf8_tensor_sections (NULL skips). */

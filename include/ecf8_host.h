@@ -64,6 +64,10 @@ int ecf8_host_synth(double alpha, double gamma, uint64_t n, uint64_t seed, int f
                     int nthreads);
 
 int ecf8_host_max_threads(void);
+/* make_stats (container.cpp:386-413) of one raw tensor with a name of
+ * name_len bytes and `rank` dims (the container overhead in actual_savings). */
+int ecf8_host_make_stats(const uint8_t *fp8, uint64_t n, uint32_t T, uint32_t name_len, uint32_t rank,
+                         ecf8_entropy_report *out);
 
 /* Weight layout for the decode-fused GEMM (ecf8_cuda.h ecf8_fused_*): an
  * n x k row-major FP8 matrix -> 128 x 128 tiles in row-major tile order,

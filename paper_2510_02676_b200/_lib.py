@@ -64,6 +64,19 @@ class Sections(C.Structure):
     ]
 
 
+class EntropyReport(C.Structure):
+    """ecf8_entropy_report: make_stats' EntropyReport for one tensor."""
+
+    _fields_ = [("n_elem", C.c_uint64)] + [
+        (f, C.c_double)
+        for f in ("entropy_bits", "bits_per_symbol", "bits_per_weight", "bound_lower", "bound_upper",
+                  "projected_savings", "actual_savings")
+    ]
+
+    def as_dict(self) -> dict:
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
 if not os.path.exists(LIB_PATH):
     raise ImportError(
         f"{LIB_PATH} is missing: build it with `make` (or __graft_entry__.build()); "
@@ -91,6 +104,8 @@ _SIGS = {
     "ecf8_exponent_histogram": (C.c_int, [_P, C.c_uint64, _U64P, _P]),
     "ecf8_encode_device": (C.c_int, [_P, C.c_uint64, C.c_uint32, _P, _P, C.POINTER(_P)]),
     "ecf8_tensor_sections": (C.c_int, [_P, C.POINTER(Sections)]),
+    "ecf8_make_stats_device": (C.c_int, [_P, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, _P,
+                                         C.POINTER(EntropyReport)]),
     "ecf8_tensor_download": (C.c_int, [_P, _P, _P, _P, _P]),
     "ecf8_tensor_n_elem": (C.c_uint64, [_P]),
     "ecf8_tensor_kernel_variant": (C.c_int, [_P]),
@@ -128,6 +143,7 @@ _SIGS = {
     ),
     "ecf8_host_synth": (C.c_int, [C.c_double, C.c_double, C.c_uint64, C.c_uint64, C.c_int, _P, C.c_int]),
     "ecf8_host_max_threads": (C.c_int, []),
+    "ecf8_host_make_stats": (C.c_int, [_P, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(EntropyReport)]),
 }
 
 for _name, (_res, _args) in _SIGS.items():

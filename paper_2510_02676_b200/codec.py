@@ -175,6 +175,18 @@ def encode_tensor(fp8, threads_per_block: int = 256, lengths=None) -> EncodedTen
     return _from_handle(h)
 
 
+def make_stats(fp8, threads_per_block: int = 256, name_len: int = 1, rank: int = 1) -> dict:
+    """make_stats (container.cpp:386-413) of one raw tensor: entropy, code
+    length, projected and actual savings (name_len / rank: its container
+    overhead)."""
+    from ._lib import EntropyReport
+
+    a = _u8(fp8).reshape(-1)
+    r = EntropyReport()
+    check(lib.ecf8_host_make_stats(_ptr(a), a.size, threads_per_block, name_len, rank, C.byref(r)))
+    return r.as_dict()
+
+
 def encode_many(arrays, threads_per_block: int = 256, nthreads: int = 0) -> list[EncodedTensor]:
     arrs = [_u8(a).reshape(-1) for a in arrays]
     n = len(arrs)

@@ -21,6 +21,7 @@
 
 #include "decode.cuh"
 #include "encode.cuh"
+#include "ecf8/entropy.hpp"
 #include "ecf8/huffman.hpp"
 #include "fused_gemm.cuh"
 #include "ecf8_cuda.h"
@@ -661,6 +662,37 @@ int ecf8_encode_device(const uint8_t* d_fp8, uint64_t n, uint32_t T, const uint8
       throw;
     }
     *out = t.release();
+    return ECF8_OK;
+  });
+}
+
+int ecf8_make_stats_device(const uint8_t* d_fp8, uint64_t n, uint32_t T, uint32_t name_len, uint32_t rank,
+                           void* stream, ecf8_entropy_report* out) {
+  return guarded([&]() -> int {
+    if (!out || (n && !d_fp8) || rank == 0) return fail(ECF8_EINVAL, "null argument");
+    // container.cpp:386-413 (make_stats), the histogram and the encode on the GPU
+    const ecf8::EntropyBounds gauss = ecf8::entropy_bounds(2.0);
+    ecf8_entropy_report r{};
+    r.n_elem = n;
+    r.bound_lower = gauss.lower;
+    r.bound_upper = gauss.upper;
+    if (n) {
+      ecf8::ExponentHistogram h;
+      if (int rc = ecf8_exponent_histogram(d_fp8, n, h.counts.data(), stream)) return rc;
+      const ecf8::CodeTable code = ecf8::build_code(h);
+      r.entropy_bits = ecf8::shannon_entropy(h);
+      r.bits_per_symbol = ecf8::expected_length(code, h);
+      r.bits_per_weight = 4.0 + r.bits_per_symbol;
+      r.projected_savings = (4.0 - r.bits_per_symbol) / 8.0;
+      ecf8_dev_tensor* t = nullptr;
+      if (int rc = ecf8_encode_device(d_fp8, n, T, code.lengths.data(), stream, &t)) return rc;
+      // tensor_section_bytes (container.cpp): shape, fixed fields, sections
+      const std::uint64_t bytes = 2 + std::uint64_t{name_len} + 1 + 8 * std::uint64_t{rank} + (8 + 4 + 16 + 8 + 8 + 8) +
+                                  t->encoded_len + t->gaps_len + 8 * t->n_outpos + t->packed_len;
+      ecf8_tensor_free(t);
+      r.actual_savings = 1.0 - static_cast<double>(bytes) / static_cast<double>(n);
+    }
+    *out = r;
     return ECF8_OK;
   });
 }

@@ -83,6 +83,23 @@ void ecf8_host_free(void* p) { std::free(p); }
 
 int ecf8_host_max_threads(void) { return omp_get_max_threads(); }
 
+int ecf8_host_make_stats(const uint8_t* fp8, uint64_t n, uint32_t T, uint32_t name_len, uint32_t rank,
+                         ecf8_entropy_report* out) {
+  return guarded([&] {
+    if (!out || (n && !fp8) || rank == 0) throw std::invalid_argument("invalid argument");
+    ecf8::RawTensorFile raw;
+    ecf8::RawTensor rt;
+    rt.shape.name.assign(name_len, 't');
+    rt.shape.dims.assign(rank, 1);
+    rt.shape.dims[0] = n;
+    rt.data.assign(fp8, fp8 + n);
+    raw.tensors.push_back(std::move(rt));
+    const ecf8::EntropyReport r = ecf8::make_stats(raw, T).at(0);
+    *out = ecf8_entropy_report{r.n_elem,      r.entropy_bits, r.bits_per_symbol,   r.bits_per_weight,
+                               r.bound_lower, r.bound_upper,  r.projected_savings, r.actual_savings};
+  });
+}
+
 int ecf8_host_build_code(const uint64_t counts[16], uint8_t lengths[16]) {
   return guarded([&] {
     ecf8::ExponentHistogram h;

@@ -35,6 +35,19 @@ def exponent_histogram(x: torch.Tensor, stream: torch.cuda.Stream | None = None)
     return counts
 
 
+def make_stats_device(x: torch.Tensor, threads_per_block: int = 256, name_len: int = 1, rank: int = 1,
+                      stream: torch.cuda.Stream | None = None) -> dict:
+    """ecf8_make_stats_device: make_stats (container.cpp:386-413) with the
+    histogram and the encode on the GPU; same numbers as codec.make_stats."""
+    from ._lib import EntropyReport
+
+    x = _fp8_bytes(x)
+    r = EntropyReport()
+    check(lib.ecf8_make_stats_device(C.c_void_p(x.data_ptr() if x.numel() else None), x.numel(), threads_per_block,
+                                     name_len, rank, _stream_ptr(stream), C.byref(r)))
+    return r.as_dict()
+
+
 def _stream_ptr(stream: torch.cuda.Stream | None) -> int | None:
     s = stream if stream is not None else torch.cuda.current_stream()
     return s.cuda_stream or None
