@@ -1038,7 +1038,6 @@ int ecf8_fused_gemm(const ecf8_fused* f, const uint8_t* d_x, uint32_t m, float s
     while (a.tmem_cols < f->max_seg[pi] * a.acc_cols) a.tmem_cols <<= 1;
     a.w_fmt = f->w_fmt;
     a.scale = scale;
-    cu(cudaMemsetAsync(d_y, 0, sizeof(float) * m * f->n, st), "memset y");
     cu(ecf8::dev::launch_fused_gemm(a, f->n_cta[pi], st), "fused GEMM launch");
     return ECF8_OK;
   });

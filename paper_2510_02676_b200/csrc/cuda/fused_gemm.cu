@@ -378,6 +378,7 @@ __global__ void __launch_bounds__((decode_warps<LW, SLOT_ROWS, WIDE>() + 1) * 32
                    "l"(args.xt + static_cast<std::uint64_t>(kt) * b_bytes), "r"(b_bytes), "r"(bar)
                    : "memory");
     };
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // x_tiles_kernel: X tiles written, y zeroed
     if (lane == 0 && n_kt) issue_x(0);
     for (std::uint32_t t = 0; t < n_kt; ++t) {
       const std::uint32_t bs = t % args.stages_b;
@@ -415,6 +416,7 @@ __global__ void __launch_bounds__((decode_warps<LW, SLOT_ROWS, WIDE>() + 1) * 32
   //      accumulator block per n-tile segment, partial sums added into y
   if (warp < 4) {
     mbar_wait(smem_addr(&g_done), 0);
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // y zeroed (returns at once: the MMAs waited)
     tc_fence_after();
     const std::uint32_t row = warp * 32 + lane;
     const std::uint32_t nseg = (cta.tile1 - 1) / KT - nt0 + 1;
@@ -443,8 +445,21 @@ __global__ void __launch_bounds__((decode_warps<LW, SLOT_ROWS, WIDE>() + 1) * 32
 
 // x [m, k] row-major -> xt [k/128][m_pad][128 B] in the 128B-swizzled
 // K-major image (rows >= m zero), so every B tile is one contiguous copy.
+// Also zeroes y (the split-K partial sums are added into it).  The fused
+// kernel is launched as its programmatic dependent: its decode warps start
+// while this runs; its X loads and y updates wait for it (griddepcontrol).
 __global__ void x_tiles_kernel(const std::uint8_t* __restrict__ x, std::uint8_t* __restrict__ xt, std::uint32_t m,
-                               std::uint32_t m_pad, std::uint32_t k) {
+                               std::uint32_t m_pad, std::uint32_t k, float* __restrict__ y, std::uint64_t y_elems) {
+  asm volatile("griddepcontrol.launch_dependents;");
+  const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
+  const std::uint64_t tid = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
+  if ((reinterpret_cast<std::uintptr_t>(y) & 15) == 0) {
+    for (std::uint64_t i = tid; i < y_elems / 4; i += stride)
+      reinterpret_cast<float4*>(y)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (tid < (y_elems & 3)) y[(y_elems & ~std::uint64_t{3}) + tid] = 0.f;
+  } else {
+    for (std::uint64_t i = tid; i < y_elems; i += stride) y[i] = 0.f;
+  }
   const std::uint64_t chunks = static_cast<std::uint64_t>(k / 128) * m_pad * 8;
   for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < chunks;
        i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
@@ -507,8 +522,18 @@ cudaError_t launch_lw(const FusedArgs& args, std::uint32_t n_cta, cudaStream_t s
   cudaError_t e = cudaFuncSetAttribute(fused_gemm_kernel<LW, ROWS, WIDE>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  fused_gemm_kernel<LW, ROWS, WIDE><<<n_cta, (decode_warps<LW, ROWS, WIDE>() + 1) * 32, smem, s>>>(args);
-  return cudaGetLastError();
+  static const bool pdl = std::getenv("ECF8_NO_PDL") == nullptr;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(n_cta);
+  cfg.blockDim = dim3((decode_warps<LW, ROWS, WIDE>() + 1) * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, fused_gemm_kernel<LW, ROWS, WIDE>, args);
 }
 
 template <bool WIDE>
@@ -520,7 +545,8 @@ cudaError_t launch_geometry(const FusedArgs& args, std::uint32_t n_cta, cudaStre
 cudaError_t launch_fused_gemm(const FusedArgs& args, std::uint32_t n_cta, cudaStream_t s) {
   const std::uint64_t chunks = static_cast<std::uint64_t>(args.k / 128) * args.m_pad * 8;
   const unsigned blocks = static_cast<unsigned>(std::min<std::uint64_t>((chunks + 255) / 256, 4 * 148));
-  x_tiles_kernel<<<blocks, 256, 0, s>>>(args.x, const_cast<std::uint8_t*>(args.xt), args.m, args.m_pad, args.k);
+  x_tiles_kernel<<<blocks, 256, 0, s>>>(args.x, const_cast<std::uint8_t*>(args.xt), args.m, args.m_pad, args.k, args.y,
+                                       static_cast<std::uint64_t>(args.m) * args.n);
   if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) return e;
   return args.m_pad > 128 ? launch_geometry<true>(args, n_cta, s) : launch_geometry<false>(args, n_cta, s);
 }
