@@ -98,3 +98,41 @@ def test_back_to_back_decodes_into_one_buffer():
             b.decode()
     torch.cuda.synchronize()
     assert np.array_equal(out.cpu().numpy(), xs[-1])
+
+
+@pytest.mark.gpu
+def test_fused_gemm_back_to_back_and_graph(orc):
+    # the GEMM is the programmatic dependent of its X-swizzle kernel, which
+    # also zeroes y: back-to-back calls into one y (no host sync) and a CUDA
+    # graph replay must give the single-call result
+    from paper_2510_02676_b200.fused import FusedLinear
+
+    n, k, m = 512, 1024, 16
+    w = codec.synth(1.8, 0.05, n * k, 77).reshape(n, k)
+    lin = FusedLinear(w)
+    xs = [(torch.randn(m, k, device="cuda") * 4).to(torch.float8_e4m3fn) for _ in range(3)]
+    want = []
+    for x in xs:
+        y = torch.empty(m, n, device="cuda")
+        lin(x, 1.0, y)
+        torch.cuda.synchronize()
+        want.append(y.clone())
+    y = torch.full((m, n), 7.0, device="cuda")
+    for _ in range(3):
+        for x in xs:
+            lin(x, 1.0, y)
+    torch.cuda.synchronize()
+    # split-K partial sums are added atomically: equal up to fp32 reassociation
+    torch.testing.assert_close(y, want[-1], rtol=1e-5, atol=1e-3)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        lin(xs[0], 1.0, y)  # warm-up on the capture stream
+        with torch.cuda.graph(g, stream=s):
+            lin(xs[1], 1.0, y)
+    torch.cuda.synchronize()
+    y.fill_(3.0)
+    g.replay()
+    torch.cuda.synchronize()
+    torch.testing.assert_close(y, want[1], rtol=1e-5, atol=1e-3)
