@@ -164,6 +164,36 @@ void* ecf8ref_tensor_new(std::uint64_t n_elem, std::uint32_t T, const std::uint8
 
 void ecf8ref_tensor_free(void* h) { delete static_cast<RefTensor*>(h); }
 
+// Every tensor of a container parsed once by the reference's parse_container
+// (container.cpp:182-250), each with its LUT built (the per-tensor work of
+// decompress_streaming, container.cpp:334-339), as handles for
+// ecf8ref_tensor_decode.  The bench reference arm builds its inputs with
+// ecf8ref_synth_raw + ecf8ref_compress_raw and this, never with the product.
+int ecf8ref_container_tensors(const std::uint8_t* c, std::size_t len, void** handles,
+                              std::uint32_t cap, std::uint32_t* count) {
+  return guarded([&] {
+    auto f = ecf8::parse_container({c, len});
+    if (f.tensors.size() > cap) throw std::invalid_argument("too many tensors for the handle array");
+    *count = static_cast<std::uint32_t>(f.tensors.size());
+    for (std::size_t i = 0; i < f.tensors.size(); ++i) {
+      auto* x = new RefTensor;
+      x->t = std::move(f.tensors[i].tensor);
+      if (x->t.stream.n_elem) x->lut = ecf8::build_lut(ecf8::canonical_codes(x->t.stream.lengths));
+      handles[i] = x;
+    }
+  });
+}
+
+std::uint64_t ecf8ref_tensor_n_elem(void* h) { return static_cast<RefTensor*>(h)->t.stream.n_elem; }
+
+// Algorithmic bytes of one decode: container sections read
+// (encoded + gaps + 8 (n_blocks + 1) + packed) + n_elem FP8 bytes written.
+std::uint64_t ecf8ref_tensor_algorithmic_bytes(void* h) {
+  const auto& t = static_cast<RefTensor*>(h)->t;
+  return t.stream.encoded.size() + t.stream.gaps.size() + 8 * t.stream.outpos.size() + t.packed.size() +
+         t.stream.n_elem;
+}
+
 // Decode with `nthreads` OpenMP threads (<= 0: all); returns seconds.
 double ecf8ref_tensor_decode(void* h, std::uint8_t* out, int nthreads) {
   auto* r = static_cast<RefTensor*>(h);

@@ -90,7 +90,16 @@ int validate(const ecf8_sections* s, std::uint64_t* n_blocks_out) {
   const std::uint64_t nb = (s->encoded_len - 2) / bb;
   if (s->n_outpos != nb + 1 || !s->outpos || s->outpos[nb] != s->n_elem || s->outpos[0] != 0)
     return fail(ECF8_EINVAL, "inconsistent block offsets");
-  const std::uint64_t cap = std::uint64_t{T} * 64;
+  // The reference allows a block up to T * 64 elements (container.cpp:231-239),
+  // but a block's windows can hold at most T * ceil(64 / Lmin) code words
+  // (every code word, garbage fallbacks included, is >= Lmin bits): elements
+  // past that are never emitted, and the reference copies stale scratch for
+  // them (codec.cpp:242-253).  Such a container is not encoder output; it is
+  // rejected, since the kernels size their slots and staging tiles by Lmin.
+  std::uint32_t lmin = 16;
+  for (int i = 0; i < 16; ++i)
+    if (s->lengths[i] && s->lengths[i] < lmin) lmin = s->lengths[i];
+  const std::uint64_t cap = std::uint64_t{T} * ((64 + lmin - 1) / lmin);
   for (std::uint64_t b = 0; b < nb; ++b)
     if (s->outpos[b + 1] < s->outpos[b] || s->outpos[b + 1] - s->outpos[b] > cap)
       return fail(ECF8_EINVAL, "inconsistent block offsets");

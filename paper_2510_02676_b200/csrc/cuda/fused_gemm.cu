@@ -74,7 +74,8 @@ __shared__ Tables g_tbf;
 __shared__ TensorDesc g_wdesc;  // this CTA's weight descriptor (read where used: frees ~30 registers)
 __shared__ unsigned g_qnext;
 __shared__ alignas(8) unsigned long long g_full[kMaxStagesA];
-__shared__ alignas(8) unsigned long long g_empty[kMaxStagesA];
+__shared__ alignas(8) unsigned long long g_empty[kMaxStagesA];  // arrived by tcgen05.commit (MMAs done)
+__shared__ alignas(8) unsigned long long g_free[kMaxStagesA];   // arrived by the MMA lane once it saw g_empty
 __shared__ alignas(8) unsigned long long g_bfull[2];
 __shared__ alignas(8) unsigned long long g_done;
 __shared__ std::uint32_t g_tmem;
@@ -168,11 +169,15 @@ struct Ring {
 };
 
 // Writers of K tile t need stage t % S back from the MMAs of tile t - S
-// (completion u - 1 of that stage's "empty" barrier, u = t / S).  Decode
+// (completion u - 1 of that stage's "free" barrier, u = t / S).  The MMA
+// lane arrives on "free" after it has waited for the stage's "empty"
+// barrier (tcgen05.commit): a thread-to-thread release/acquire chain
+// (writer -> full -> MMA lane -> free -> next writer) that compute-sanitizer
+// racecheck can follow, which a hardware-arrived barrier is not.  Decode
 // warps run up to ~8 K tiles ahead of the MMA, so a bare parity wait could
 // alias a completion two phases back; the control warp's monotonic count of
 // consumed K tiles first guarantees the barrier is at most one phase behind
-// (tile t - 2S consumed), then the hardware parity wait does the rest.
+// (tile t - 2S consumed), then the parity wait does the rest.
 __device__ __forceinline__ void wait_stage_free(const Ring& R, std::uint32_t t) {
   if (t < R.stages) return;
   if (t >= 2 * R.stages) {
@@ -185,7 +190,7 @@ __device__ __forceinline__ void wait_stage_free(const Ring& R, std::uint32_t t) 
       __nanosleep(128);
     }
   }
-  mbar_wait_sleep(smem_addr(&g_empty[t % R.stages]), ((t / R.stages) - 1) & 1u, 128);
+  mbar_wait_sleep(smem_addr(&g_free[t % R.stages]), ((t / R.stages) - 1) & 1u, 128);
 }
 
 // Output into the A ring: element g of the CTA range [e0, e1) lands in ring
@@ -318,6 +323,7 @@ __global__ void __launch_bounds__((decode_warps<LW, SLOT_ROWS, WIDE>() + 1) * 32
       for (std::uint32_t s = 0; s < args.stages_a; ++s) {
         mbar_init(smem_addr(&g_full[s]), kTileElems);
         mbar_init(smem_addr(&g_empty[s]), 1);
+        mbar_init(smem_addr(&g_free[s]), 1);
       }
       mbar_init(smem_addr(&g_bfull[0]), 1);
       mbar_init(smem_addr(&g_bfull[1]), 1);
@@ -404,6 +410,7 @@ __global__ void __launch_bounds__((decode_warps<LW, SLOT_ROWS, WIDE>() + 1) * 32
         if (t + 1 == n_kt) tc_commit(smem_addr(&g_done));
         // the MMAs of tile t have read stage s: publish it to the decode warps
         mbar_wait(smem_addr(&g_empty[s]), (t / args.stages_a) & 1u);
+        mbar_arrive(smem_addr(&g_free[s]), 1);
         asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_addr(&g_consumed)), "r"(t + 1)
                      : "memory");
         if (args.stages_b == 1 && t + 1 < n_kt) issue_x(t + 1);

@@ -60,6 +60,10 @@ class FusedLinear:
         m = x.shape[0]
         if out is None:
             out = torch.empty(m, self.n, dtype=torch.float32, device=x.device)
+        elif (out.dtype != torch.float32 or out.device != x.device or tuple(out.shape) != (m, self.n)
+              or not out.is_contiguous()):
+            # the kernel zeroes and atomically adds m * n fp32 values at out.data_ptr()
+            raise ValueError(f"out must be a contiguous float32 tensor [{m}, {self.n}] on {x.device}")
         check(lib.ecf8_fused_gemm(self.handle, C.c_void_p(x.data_ptr()), m, float(scale),
                                   C.c_void_p(out.data_ptr()), _stream_ptr(stream)))
         return out

@@ -144,6 +144,11 @@ class Reference:
         L.ecf8ref_tensor_free.argtypes = [_P]
         L.ecf8ref_tensor_decode.restype = C.c_double
         L.ecf8ref_tensor_decode.argtypes = [_P, _P, C.c_int]
+        L.ecf8ref_container_tensors.argtypes = [_P, C.c_size_t, C.POINTER(_P), C.c_uint32, C.POINTER(C.c_uint32)]
+        L.ecf8ref_tensor_n_elem.restype = C.c_uint64
+        L.ecf8ref_tensor_n_elem.argtypes = [_P]
+        L.ecf8ref_tensor_algorithmic_bytes.restype = C.c_uint64
+        L.ecf8ref_tensor_algorithmic_bytes.argtypes = [_P]
 
     def _err(self):
         return self.lib.ecf8ref_last_error().decode()
@@ -211,6 +216,20 @@ class Reference:
 
     def free(self, h):
         self.lib.ecf8ref_tensor_free(h)
+
+    def container_tensors(self, data: bytes) -> list:
+        """Handles of every tensor of a container (reference parse_container + build_lut)."""
+        buf = np.frombuffer(data, np.uint8)
+        hs, n = (_P * 4096)(), C.c_uint32()
+        if self.lib.ecf8ref_container_tensors(_p(buf), buf.size, hs, 4096, C.byref(n)):
+            raise ValueError(self._err())
+        return [hs[i] for i in range(n.value)]
+
+    def n_elem(self, h) -> int:
+        return int(self.lib.ecf8ref_tensor_n_elem(h))
+
+    def algorithmic_bytes(self, h) -> int:
+        return int(self.lib.ecf8ref_tensor_algorithmic_bytes(h))
 
 
 def oracle() -> Oracle:

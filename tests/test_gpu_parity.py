@@ -158,6 +158,33 @@ def test_invalid_lengths_rejected_by_device_path():
         codec.decode_parallel(bad)
 
 
+@pytest.mark.parametrize("T", [8, 64, 256, 1024])
+def test_block_range_beyond_window_capacity_rejected(T):
+    # outpos steps up to T * 64 pass the reference's container check, but with
+    # Lmin >= 2 a block's windows hold at most T * 32 code words; such a block
+    # (never encoder output) must be rejected, not decoded past the kernels'
+    # Lmin-sized slots and staging tiles
+    from paper_2510_02676_b200._lib import InvalidArgument
+
+    x = codec.synth(1.8, 0.05, 40 * T * 32, 11)
+    t = codec.encode_tensor(x, T)
+    assert int(np.flatnonzero(t.lengths).size) and min(l for l in t.lengths if l) >= 2
+    bad = t.copy()
+    op = bad.outpos
+    assert len(op) >= 4
+    op[1] = op[0] + 1  # block 1 now spans (nearly) two blocks' symbols
+    assert op[2] - op[1] > T * 32 and op[2] - op[1] <= T * 64
+    with pytest.raises(InvalidArgument, match="inconsistent block offsets"):
+        codec.decode_parallel(bad)
+    import torch  # noqa: F401
+
+    from paper_2510_02676_b200.device import DeviceTensor
+
+    with pytest.raises(InvalidArgument, match="inconsistent block offsets"):
+        DeviceTensor(bad)
+    assert np.array_equal(codec.decode_parallel(t), x)
+
+
 def test_decode_many_pipeline_across_tensors(orc):
     # mixed T / sizes / an empty tensor; the 12 M-element tensor spans several
     # 2 MB chunks, so chunk slots are reused within and across tensors
