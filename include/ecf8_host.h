@@ -32,6 +32,10 @@ int ecf8_host_build_lut(const uint8_t lengths[16], uint8_t *entries, uint32_t *n
  * smask 1 << 16 u16, cascade 18*256 bytes (first 1 << fast_bits used). */
 int ecf8_host_device_tables(const uint8_t lengths[16], uint32_t *fast, uint16_t *smask,
                             uint8_t *cascade, uint32_t *n_luts, uint32_t *fast_bits);
+/* The byte-step decoder for `lengths` (tables.hpp fsm / fsm_cm): fsm needs
+ * 16*256 u32, cm 16*256 bytes; *ok = 0 when the code has none (incomplete
+ * code, or a 1-bit word). */
+int ecf8_host_fsm_tables(const uint8_t lengths[16], uint32_t *fsm, uint8_t *cm, int *ok);
 
 /* encode_tensor (codec.cpp:100-109) with the tensor's own build_code;
  * lengths may be NULL (histogram code) or a caller-chosen code. */

@@ -127,6 +127,7 @@ _SIGS = {
     "ecf8_host_build_code": (C.c_int, [_P, _P]),
     "ecf8_host_build_lut": (C.c_int, [_P, _P, _U32P]),
     "ecf8_host_device_tables": (C.c_int, [_P, _P, _P, _P, _U32P, _U32P]),
+    "ecf8_host_fsm_tables": (C.c_int, [_P, _P, _P, C.POINTER(C.c_int)]),
     "ecf8_host_encode": (C.c_int, [_P, C.c_uint64, C.c_uint32, _P, C.POINTER(_P)]),
     "ecf8_host_encode_many": (C.c_int, [C.POINTER(_P), _U64P, C.c_int, C.c_uint32, C.POINTER(_P), C.c_int]),
     "ecf8_host_tensor_sections": (C.c_int, [_P, C.POINTER(Sections)]),

@@ -72,6 +72,17 @@ def device_tables(lengths) -> tuple[np.ndarray, np.ndarray, np.ndarray, int, int
     return fast[:k].copy(), smask[:k].copy(), casc[: 256 * n.value].copy(), n.value, fb.value
 
 
+def fsm_tables(lengths) -> tuple[np.ndarray, np.ndarray, bool]:
+    """(fsm u32 [16, 256], completion masks u8 [16, 256], available) -- the
+    byte-step decoder the B200 kernel stages for verified tiles."""
+    l = _u8(lengths)
+    fsm = np.zeros(16 * 256, np.uint32)
+    cm = np.zeros(16 * 256, np.uint8)
+    ok = C.c_int()
+    check(lib.ecf8_host_fsm_tables(_ptr(l), _ptr(fsm), _ptr(cm), C.byref(ok)))
+    return fsm.reshape(16, 256), cm.reshape(16, 256), bool(ok.value)
+
+
 # --------------------------------------------------------------- tensors
 
 

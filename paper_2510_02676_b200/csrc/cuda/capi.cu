@@ -135,6 +135,8 @@ struct DevTables {
   std::uint8_t* cascade = nullptr;
   std::uint32_t n_luts = 0;
   std::uint64_t lenpack = 0;
+  std::uint32_t* fsm = nullptr;  // byte-step decoder (tables.hpp), nullptr when the code has none
+  std::uint8_t* fsm_cm = nullptr;
 };
 
 const DevTables& device_tables(const std::uint8_t lengths[16]) {
@@ -159,6 +161,14 @@ const DevTables& device_tables(const std::uint8_t lengths[16]) {
   cu(cudaMemcpy(d.fast, t->fast.data(), t->fast.size() * 4, cudaMemcpyHostToDevice), "upload tables");
   cu(cudaMemcpy(d.smask, t->smask.data(), t->smask.size() * 2, cudaMemcpyHostToDevice), "upload tables");
   cu(cudaMemcpy(d.cascade, t->cascade.data(), t->cascade.size(), cudaMemcpyHostToDevice), "upload tables");
+  if (t->fsm_ok) {
+    void* q = nullptr;
+    cu(cudaMalloc(&q, t->fsm.size() * 4 + t->fsm_cm.size()), "cudaMalloc(tables)");
+    d.fsm = static_cast<std::uint32_t*>(q);
+    d.fsm_cm = static_cast<std::uint8_t*>(q) + t->fsm.size() * 4;
+    cu(cudaMemcpy(d.fsm, t->fsm.data(), t->fsm.size() * 4, cudaMemcpyHostToDevice), "upload tables");
+    cu(cudaMemcpy(d.fsm_cm, t->fsm_cm.data(), t->fsm_cm.size(), cudaMemcpyHostToDevice), "upload tables");
+  }
   return cache.emplace(std::make_pair(dev, key), d).first->second;
 }
 
@@ -277,6 +287,8 @@ void alloc_arena(ecf8_dev_tensor* t, const ecf8_sections* s, std::uint64_t nb, c
     d.cascade = tb.cascade;
     d.n_luts = tb.n_luts;
     d.lenpack = tb.lenpack;
+    d.fsm = tb.fsm;
+    d.fsm_cm = tb.fsm_cm;
   }
 }
 
@@ -431,6 +443,8 @@ int host_pipeline(const ecf8_sections* const* ss, const std::uint64_t* nbs, std:
     d.cascade = tb.cascade;
     d.n_luts = tb.n_luts;
     d.lenpack = tb.lenpack;
+    d.fsm = tb.fsm;
+    d.fsm_cm = tb.fsm_cm;
     d.lmin = lmin_of(s->lengths);
 
     HostCtx::Meta& mt = c.meta[parity];

@@ -19,6 +19,8 @@ struct TensorDesc {
   const std::uint16_t* smask;    // tables.hpp start masks
   const std::uint8_t* cascade;   // reference cascade (slow path)
   const std::uint32_t* tile_ok;  // bit v: gaps of windows [256v, 256v+256) verified (nullptr: none)
+  const std::uint32_t* fsm;      // tables.hpp byte-step decoder (nullptr: the code has none)
+  const std::uint8_t* fsm_cm;    // its completion masks
   std::uint8_t* out;             // element i lands at out[i - out_offset]
   std::uint64_t out_offset;      // multiple of 16
   std::uint64_t n_elem;

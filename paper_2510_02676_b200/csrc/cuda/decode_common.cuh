@@ -143,6 +143,7 @@ struct CountSink {
 // and the cascade -- window ends and flagged entries only -- elsewhere than
 // shared memory; the fast table is always addressed in shared memory).
 struct SmemTables {
+  static constexpr bool kGlobal = false;
   const Tables& tb;
   __device__ __forceinline__ std::uint32_t fast_addr() const { return smem_addr(tb.fast); }
   __device__ __forceinline__ std::uint32_t fast(std::uint32_t idx) const { return tb.fast[idx]; }
@@ -150,6 +151,26 @@ struct SmemTables {
   __device__ __forceinline__ std::uint32_t cascade(std::uint32_t i) const { return tb.cascade[i]; }
 };
 
+
+// The same tables read from global memory (L1-cached) -- for the kernels
+// whose shared memory holds the byte-step decoder instead (decode_warp.cu);
+// only windows off the verified fast path get here.
+struct GlobalTables {
+  static constexpr bool kGlobal = true;
+  const TensorDesc& d;
+  __device__ __forceinline__ std::uint32_t fast_addr() const { return 0; }
+  __device__ __forceinline__ std::uint32_t fast(std::uint32_t idx) const { return stage_entry(__ldg(d.fast + idx)); }
+  __device__ __forceinline__ std::uint32_t smask(std::uint32_t idx) const { return __ldg(d.smask + idx); }
+  __device__ __forceinline__ std::uint32_t cascade(std::uint32_t i) const { return __ldg(d.cascade + i); }
+};
+
+// The staged fast-table entry for the next kFastBits bits of hi, from
+// shared memory (address `fast`) or through the global view.
+template <bool OR_BASE, class TV>
+__device__ __forceinline__ std::uint32_t tv_fast(const TV& tv, std::uint32_t fast, std::uint32_t hi) {
+  if constexpr (TV::kGlobal) return tv.fast(hi >> kFastShift);
+  else return fast_entry<OR_BASE>(fast, hi);
+}
 
 // The reference cascade (lut.hpp:43-49) on the 16-bit head of `hi`, as a
 // fast-format entry: one symbol, its length as b.
@@ -219,7 +240,7 @@ __device__ __forceinline__ bool decode_window_fast(std::uint32_t w0, std::uint32
   std::uint32_t lo = __funnelshift_l(w2, w1, gap);
   std::uint32_t p = gap;  // adds whole staged entries: bits 0..6 exact, kSlowFlag ends the loop
   while (!(p & kPhaseDone)) {
-    const std::uint32_t e = fast_entry<OR_BASE>(fast, hi);
+    const std::uint32_t e = tv_fast<OR_BASE>(tv, fast, hi);
     sink.put(e >> 12, entry_n4(e));
     hi = __funnelshift_l(lo, hi, e);  // shift amount = e & 31 = bits consumed
     lo = __funnelshift_l(0u, lo, e);
@@ -231,7 +252,7 @@ __device__ __forceinline__ bool decode_window_fast(std::uint32_t w0, std::uint32
   lo = __funnelshift_l(w3, w2, p - 32);
   for (;;) {
     const std::uint32_t idx = hi >> kFastShift;
-    const std::uint32_t e = fast_entry<OR_BASE>(fast, hi);
+    const std::uint32_t e = tv_fast<OR_BASE>(tv, fast, hi);
     if (e & kSlowFlag) return false;
     const std::uint32_t b = e & 31, r = 64 - p;
     if (b >= r) {
@@ -309,6 +330,115 @@ __device__ __forceinline__ bool decode_lane_continuous(const std::uint32_t (&w)[
     }
   }
   return !(p & kSlowFlag);
+}
+
+// ---- byte-step decoder (tables.hpp fsm / fsm_cm) --------------------------
+
+__device__ __forceinline__ std::uint32_t prmt(std::uint32_t a, std::uint32_t b, std::uint32_t sel) {
+  std::uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
+}
+
+// Shared address of the staged byte-step table: the kernels that use it pin
+// it there, so a probe is [index * 4 + constant] (decode_warp.cu checks).
+constexpr std::uint32_t kFsmAt = 0x800;
+constexpr std::uint32_t kFsmCmAt = kFsmAt + 4 * 256 * kFsmStates;
+
+// One byte step: the entry for (state of `prev`, byte j of the pre-shifted
+// lane stream s[]).  The index is state * 256 + byte, built by one byte
+// permute: byte 0 from the stream word (big-endian: byte j is byte 3 - j % 4
+// of s[j / 4]), byte 1 = prev's state byte, bytes 2-3 = that byte's sign
+// (0: states are < 16).
+__device__ __forceinline__ std::uint32_t fsm_index(std::uint32_t word, std::uint32_t prev, int j) {
+  return prmt(word, prev, 0xDD50u | static_cast<std::uint32_t>(3 - (j & 3)));
+}
+__device__ __forceinline__ std::uint32_t fsm_entry(std::uint32_t idx) {
+  std::uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1+2048];" : "=r"(v) : "r"(imul<4>(idx)));
+  static_assert(kFsmAt == 2048, "immediate above");
+  return v;
+}
+__device__ __forceinline__ std::uint32_t fsm_cm(std::uint32_t idx) {
+  std::uint16_t v;
+  asm volatile("ld.shared.u8 %0, [%1+18432];" : "=h"(v) : "r"(idx));
+  static_assert(kFsmCmAt == 18432, "immediate above");
+  return v;
+}
+
+// Nibble sink for two byte steps at once: their symbol fields (<= 4 + 4
+// symbols) are joined into one 32-bit run c, then appended at nibble q4 of
+// the partial word lo; a full word goes to the slot.  q4 adds the whole
+// entries (n4 in bits 0..4, bit 5 clear): bits 0..4 stay exact, bit 5
+// toggles when a word fills (the pair adds <= 32 bits: at most one word),
+// the state / symbol bits above collect garbage nothing reads.
+template <int WS>
+struct PairSink {
+  std::uint32_t addr;  // next slot word
+  std::uint32_t lo = 0, q4 = 0;
+  __device__ __forceinline__ void put2(std::uint32_t e1, std::uint32_t e2) {
+    const std::uint32_t c = (e1 >> 16) | __funnelshift_l(0u, e2 >> 16, e1);  // f2 << n4(e1)
+    const std::uint32_t q = q4 + e1 + e2;
+    const std::uint32_t nl = lo | __funnelshift_l(0u, c, q4);  // c << (q4 % 32)
+    const std::uint32_t nh = __funnelshift_l(c, 0u, q4);       // c >> (32 - q4 % 32)
+    const bool full = ((q ^ q4) & 32u) != 0;
+    if (full) sts32(addr, nl);
+    addr += full ? WS : 0u;
+    lo = full ? nh : nl;
+    q4 = q;
+  }
+  __device__ __forceinline__ std::uint32_t finish(std::uint32_t base) {
+    if (q4 & 31u) sts32(addr, lo);
+    return (addr - base) / WS * 8 + ((q4 & 31u) >> 2);
+  }
+};
+
+// A lane's LW windows (verified tile) decoded by byte steps: the code words
+// from bit gap0 of its first window up to bit 64 LW + gnext, gnext = the gap
+// of the window after its last one.  On a verified tile that end is exactly
+// where the reference's walk of the last window stops (the first word
+// starting at or after the window boundary, codec.cpp:143-160 / 49-98), so
+// the words are those the reference's per-window walks take, in order.
+// w: the 2 LW window words + 2 lookahead words, big-endian.  Writes the
+// symbols to the slot at `slot` (word stride WS); returns their count.
+template <int LW, int WS>
+__device__ __forceinline__ std::uint32_t decode_lane_fsm(const std::uint32_t (&w)[2 * LW + 2], std::uint32_t gap0,
+                                                         std::uint32_t gnext, std::uint32_t slot) {
+  constexpr int NB = 8 * LW;     // bytes of the lane's windows
+  constexpr int NS = 2 * LW + 1;  // stream words from bit gap0: bytes 0 .. 4 NS - 1 >= NB + 2
+  std::uint32_t st[NS];
+#pragma unroll
+  for (int i = 0; i < NS; ++i) st[i] = __funnelshift_l(w[i + 1], w[i], gap0);
+  // end of the lane's words, relative to gap0: byte Bp, bit r of it
+  const std::uint32_t Lp = 64u * LW + gnext - gap0;  // in [64 LW - 15, 64 LW + 15]
+  const std::uint32_t Bp = Lp >> 3, rmask = (1u << (Lp & 7)) - 1;
+  PairSink<WS> sink{slot};
+  std::uint32_t e = 0;  // root
+#pragma unroll
+  for (int j = 0; j < NB - 2; j += 2) {  // bytes before NB - 2 <= Bp: all words complete inside the lane
+    const std::uint32_t e1 = fsm_entry(fsm_index(st[j >> 2], e, j));
+    const std::uint32_t e2 = fsm_entry(fsm_index(st[(j + 1) >> 2], e1, j + 1));
+    sink.put2(e1, e2);
+    e = e2;
+  }
+  // bytes NB - 2 .. NB + 1: whole before Bp; at Bp the words completing in
+  // its first r bits (they end by Lp); after Bp none
+  auto clip = [&](std::uint32_t ej, std::uint32_t idx, int j) -> std::uint32_t {
+    const std::uint32_t lm = static_cast<std::uint32_t>(j) == Bp ? rmask : 0u;
+    const std::uint32_t kept4 = 4u * __popc(fsm_cm(idx) & lm);
+    const std::uint32_t clipped = (ej & ((0x10000u << kept4) - 0x10000u)) | kept4;
+    return static_cast<std::uint32_t>(j) < Bp ? ej : clipped;
+  };
+#pragma unroll
+  for (int j = NB - 2; j < NB + 2; j += 2) {
+    const std::uint32_t i1 = fsm_index(st[j >> 2], e, j);
+    const std::uint32_t e1 = clip(fsm_entry(i1), i1, j);
+    const std::uint32_t i2 = fsm_index(st[(j + 1) >> 2], e1, j + 1);
+    const std::uint32_t e2 = clip(fsm_entry(i2), i2, j + 1);
+    sink.put2(e1, e2);
+    e = e2;
+  }
+  return sink.finish(slot);
 }
 
 // Where window (w0..w3, gap)'s reference walk stops: the start of the first

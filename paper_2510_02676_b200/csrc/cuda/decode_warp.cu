@@ -62,8 +62,30 @@ static_assert(offsetof(StaticSmem, tb) + offsetof(Tables, fast) == 0x4000 - 0x40
 __shared__ __align__(1024) StaticSmem g_s;
 
 #define g_tb g_s.tb
-#define g_next_tile g_s.next_tile
-#define g_desc g_s.desc
+
+// The byte-step variant (Lmin >= 2): the staged tables are the byte-step
+// decoder (16 KB + 4 KB of completion masks), pinned at kFsmAt; windows off
+// the verified path read the fast / cascade tables through L1.
+struct StaticSmemFsm {
+  unsigned next_tile;
+  TensorDesc desc;
+  unsigned char pad[kFsmAt - 0x400 - 8 - sizeof(TensorDesc)];
+  std::uint32_t fsm[256 * kFsmStates];
+  std::uint8_t cm[256 * kFsmStates];
+};
+static_assert(offsetof(StaticSmemFsm, fsm) == kFsmAt - 0x400, "fsm table offset");
+static_assert(offsetof(StaticSmemFsm, cm) == kFsmCmAt - 0x400, "fsm mask offset");
+__shared__ __align__(1024) StaticSmemFsm g_f;
+
+__device__ __forceinline__ void stage_fsm(const TensorDesc& d, int tid, int nthreads) {
+  if (!d.fsm) return;
+  const uint4* f4 = reinterpret_cast<const uint4*>(d.fsm);
+  uint4* sf4 = reinterpret_cast<uint4*>(g_f.fsm);
+  for (int i = tid; i < 256 * kFsmStates / 4; i += nthreads) sf4[i] = __ldg(f4 + i);
+  const uint4* c4 = reinterpret_cast<const uint4*>(d.fsm_cm);
+  uint4* sc4 = reinterpret_cast<uint4*>(g_f.cm);
+  for (int i = tid; i < 256 * kFsmStates / 16; i += nthreads) sc4[i] = __ldg(c4 + i);
+}
 
 #ifndef ECF8_WB_UNROLL
 #define ECF8_WB_UNROLL 4
@@ -85,15 +107,21 @@ struct GlobalOut {
 };
 
 // One tile: decode + scan, compact, write back.
-template <class WSm>
+template <bool WIDE, class WSm>
 __device__ __forceinline__ void warp_tile(const TensorDesc& d, const WarpIn& in, std::uint32_t log2T,
                                           std::uint32_t len_off, WSm& ws, int lane) {
   // slots interleaved word by word (word j of lane L at slot[32 j + L]): the
   // lanes' slot stores and reads hit 32 different banks
   const std::uint32_t slot = smem_addr(ws.slot + lane);
-  const bool verified = tile_verified(d, in, log2T);
-  const LaneRun run =
-      warp_decode_scan<kLaneWin, 128, true>(in, log2T, len_off, SmemTables{g_tb}, slot, lane, verified);
+  LaneRun run;
+  if constexpr (WIDE) {
+    run = warp_decode_scan<kLaneWin, 128, true>(in, log2T, len_off, SmemTables{g_tb}, slot, lane,
+                                                tile_verified(d, in, log2T));
+  } else {
+    const bool verified = tile_verified(d, in, log2T) && d.fsm != nullptr;
+    run = warp_decode_scan<kLaneWin, 128, false, GlobalTables, true>(in, log2T, len_off, GlobalTables{d}, slot, lane,
+                                                                     verified);
+  }
   GlobalOut out{d.out + ((in.A & ~std::uint64_t{15}) - d.out_offset)};
   compact_write<kWbUnroll>(d, in.A, in.E, run, ws, lane, out);
 }
@@ -104,8 +132,8 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_warp_kernel(const LaunchArg
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   WarpSmem& ws = reinterpret_cast<WarpSmem*>(smem_raw)[warp];
-  unsigned& next_tile = g_next_tile;
-  TensorDesc& desc = g_desc;
+  unsigned& next_tile = WIDE ? g_s.next_tile : g_f.next_tile;
+  TensorDesc& desc = WIDE ? g_s.desc : g_f.desc;
   asm volatile("griddepcontrol.launch_dependents;");  // the next decode may claim SMs as ours free up
   const std::uint64_t total_tiles = args.total_tiles;
   const std::uint64_t t_lo = total_tiles * blockIdx.x / gridDim.x;
@@ -138,8 +166,13 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_warp_kernel(const LaunchArg
     __syncthreads();
     const TensorDesc& d = desc;
     const std::uint32_t log2T = 31 - __clz(d.T);
-    if (threadIdx.x == 0 && smem_addr(g_tb.fast) != kFastAt) __trap();  // the walk addresses the table at kFastAt
-    stage_tables(d, g_tb, threadIdx.x, NW * 32);
+    if constexpr (WIDE) {
+      if (threadIdx.x == 0 && smem_addr(g_tb.fast) != kFastAt) __trap();  // the walk addresses the table at kFastAt
+      stage_tables(d, g_tb, threadIdx.x, NW * 32);
+    } else {
+      if (threadIdx.x == 0 && smem_addr(g_f.fsm) != kFsmAt) __trap();  // the byte steps address the table at kFsmAt
+      stage_fsm(d, threadIdx.x, NW * 32);
+    }
     const std::uint32_t len_off = (d.n_luts - 1) << 8;
     if (threadIdx.x == 0) next_tile = NW;
     __syncthreads();
@@ -150,7 +183,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_warp_kernel(const LaunchArg
     // cost.  The next tile is claimed and its inputs loaded one tile ahead.
     WarpIn nxt;
     std::uint64_t tile = seg + warp;
-    if (tile < seg_end) load_warp_tile(d, tile, log2T, lane, nxt);
+    if (tile < seg_end) load_warp_tile<kLaneWin, !WIDE>(d, tile, log2T, lane, nxt);
     while (tile < seg_end) {
       const WarpIn cur = nxt;
 #ifndef ECF8_NO_PK_PREFETCH
@@ -164,8 +197,8 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_warp_kernel(const LaunchArg
       unsigned claim = 0;
       if (lane == 0) claim = atomicAdd(&next_tile, 1u);
       const std::uint64_t next = seg + __shfl_sync(0xffffffffu, claim, 0);
-      if (next < seg_end) load_warp_tile(d, next, log2T, lane, nxt);
-      warp_tile(d, cur, log2T, len_off, ws, lane);
+      if (next < seg_end) load_warp_tile<kLaneWin, !WIDE>(d, next, log2T, lane, nxt);
+      warp_tile<WIDE>(d, cur, log2T, len_off, ws, lane);
       tile = next;
     }
     seg = seg_end;
@@ -216,7 +249,10 @@ __global__ void __launch_bounds__(256) verify_gaps_kernel(const TensorDesc d, st
   const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
   for (std::uint64_t k = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; k - threadIdx.x % 32 < n_win;
        k += stride) {
-    bool bad = false;
+    // the tensor's last window has no successor to check against: its tile
+    // keeps the window-by-window walk (the byte-step decoder ends a lane at
+    // the next window's gap)
+    bool bad = k + 1 == n_win;
     if (k + 1 < n_win) {
       const uint2 a = __ldg(reinterpret_cast<const uint2*>(d.encoded + 8 * k));
       const uint2 b = __ldg(reinterpret_cast<const uint2*>(d.encoded + 8 * k + 8));

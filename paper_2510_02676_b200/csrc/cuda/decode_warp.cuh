@@ -32,12 +32,13 @@ struct WarpInT {
   std::uint32_t nblk, nwin;
   std::uint64_t b0;
   std::uint32_t ok_a, ok_b;  // tile_ok words of the tile's first / last window (loaded one tile ahead)
+  std::uint32_t gnext;       // the next lane's gap word (its first window: bits 4..7) -- byte-step decoder only
 };
 using WarpIn = WarpInT<kLaneWin>;
 
 // A tile's inputs in two halves: the window words and gaps (issued early,
 // they fly while the previous tile is written back), and the block offsets.
-template <int LW>
+template <int LW, bool NEXT = false>
 __device__ __forceinline__ void load_tile_words(const TensorDesc& d, std::uint64_t tile, std::uint32_t log2T,
                                                 int lane, WarpInT<LW>& in) {
   const std::uint32_t m = (32u * LW) >> log2T;  // blocks per tile
@@ -55,10 +56,13 @@ __device__ __forceinline__ void load_tile_words(const TensorDesc& d, std::uint64
       in.w67 = __ldg(src + 3);
       in.w8 = __ldg(reinterpret_cast<const uint2*>(src + 4));
       in.gaps = __ldg(reinterpret_cast<const std::uint32_t*>(d.gaps + (w0g >> 1)) + lane);
+      // lane 31: the next tile's first window (gaps carry >= 64 bytes of padding)
+      if constexpr (NEXT) in.gnext = __ldg(reinterpret_cast<const std::uint32_t*>(d.gaps + (w0g >> 1)) + lane + 1);
     } else {
       static_assert(LW == 4, "4 or 8 windows per lane");
       in.w8 = __ldg(reinterpret_cast<const uint2*>(src + 2));
       in.gaps = __ldg(reinterpret_cast<const std::uint16_t*>(d.gaps + (w0g >> 1)) + lane);
+      if constexpr (NEXT) in.gnext = __ldg(reinterpret_cast<const std::uint16_t*>(d.gaps + (w0g >> 1)) + lane + 1);
     }
   }
 }
@@ -81,10 +85,10 @@ __device__ __forceinline__ void load_tile_meta(const TensorDesc& d, std::uint32_
   }
 }
 
-template <int LW>
+template <int LW, bool NEXT = false>
 __device__ __forceinline__ void load_warp_tile(const TensorDesc& d, std::uint64_t tile, std::uint32_t log2T,
                                                int lane, WarpInT<LW>& in) {
-  load_tile_words(d, tile, log2T, lane, in);
+  load_tile_words<LW, NEXT>(d, tile, log2T, lane, in);
   load_tile_meta(d, log2T, lane, in);
 }
 
@@ -109,13 +113,16 @@ struct LaneRun {
 // upload-time gap check): one continuous walk over the lane's windows;
 // otherwise, or when the walk met a flagged entry, window by window with the
 // reference's per-window semantics (fast table, exact walk where flagged).
-template <int LW, int WS = 4, bool OR_BASE = false, class TV>
+// FSM: verified tiles take the byte-step decoder (staged at kFsmAt;
+// decode_lane_fsm) instead of the continuous fast-table walk.
+template <int LW, int WS = 4, bool OR_BASE = false, class TV, bool FSM = false>
 __device__ __forceinline__ LaneRun warp_decode_scan(const WarpInT<LW>& in, std::uint32_t log2T,
                                                    std::uint32_t len_off, const TV& tb, std::uint32_t slot_base,
                                                    int lane, bool verified = false) {
   const std::uint32_t wl0 = static_cast<std::uint32_t>(lane) * LW;
   const bool active = wl0 < in.nwin;
   SlotSinkT<WS> sink{slot_base};
+  std::uint32_t cnt_fsm = 0;  // byte-step path: its count (the sink then stays empty)
   if (active) {
     std::uint32_t w[2 * LW + 2];
     w[0] = bswap32(in.w01.x), w[1] = bswap32(in.w01.y), w[2] = bswap32(in.w01.z), w[3] = bswap32(in.w01.w);
@@ -127,7 +134,10 @@ __device__ __forceinline__ LaneRun warp_decode_scan(const WarpInT<LW>& in, std::
     w[2 * LW] = bswap32(in.w8.x), w[2 * LW + 1] = bswap32(in.w8.y);
     const std::uint32_t n = min(in.nwin - wl0, static_cast<std::uint32_t>(LW));
     bool windowed = true;
-    if (verified) {
+    if (FSM && verified) {
+      cnt_fsm = decode_lane_fsm<LW, WS>(w, (in.gaps >> 4) & 15u, (in.gnext >> 4) & 15u, slot_base);
+      windowed = false;
+    } else if (verified) {
       const SlotSinkT<WS> saved = sink;
       const std::uint32_t gap0 = (in.gaps >> 4) & 15u;  // window 0: high nibble of byte 0
       // n == LW: tiles are whole blocks of T >= LW windows, so every active lane owns LW windows
@@ -148,7 +158,7 @@ __device__ __forceinline__ LaneRun warp_decode_scan(const WarpInT<LW>& in, std::
       }
     }
   }
-  const std::uint32_t cnt = sink.finish(slot_base);
+  const std::uint32_t cnt = sink.finish(slot_base) + cnt_fsm;
 
   // warp scan, segmented by reference block (2^(log2T-3) lanes each)
   std::uint32_t incl = cnt;

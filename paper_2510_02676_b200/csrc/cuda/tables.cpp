@@ -1,6 +1,8 @@
 // tables.cpp -- host builder for the device decode tables (see tables.hpp).
 #include "tables.hpp"
 
+#include <algorithm>
+#include <cmath>
 #include <map>
 #include <mutex>
 #include <stdexcept>
@@ -15,6 +17,62 @@ constexpr std::uint16_t kUndetermined = 0xFFFF;
 
 inline std::uint16_t pack_step(unsigned sym, unsigned len) {
   return static_cast<std::uint16_t>(sym | (len << 4));
+}
+// The byte-step state machine of tables.hpp: walk the code tree bit by bit
+// (MSB first), emitting a symbol at every leaf.  The tree is the canonical
+// code's (huffman.cpp:131-157 word assignment), so a complete code parses
+// any bit string exactly as the reference's decode_one chain does
+// (lut.hpp:43-49; every 16-bit window then starts with a whole code word).
+void build_fsm(const CodeTable& code, DecodeTables& t) {
+  t.fsm.assign(kFsmStates * 256, 0);
+  t.fsm_cm.assign(kFsmStates * 256, 0);
+  t.fsm_ok = false;
+  // leaf[(len, word)] = symbol; node ids for proper prefixes of words
+  std::map<std::pair<int, std::uint32_t>, int> leaf, node;
+  double kraft = 0;
+  int lmin = 17, present = 0;
+  for (int s = 0; s < 16; ++s) {
+    const int l = code.lengths[s];
+    if (!l) continue;
+    ++present;
+    lmin = std::min(lmin, l);
+    kraft += std::ldexp(1.0, -l);
+    leaf[{l, code.codes[s]}] = s;
+  }
+  if (present < 2 || lmin < 2 || kraft != 1.0) return;
+  node[{0, 0}] = 0;
+  for (int l = 1; l <= 16; ++l)  // breadth-first ids
+    for (const auto& [k, s] : leaf)
+      if (k.first > l) {
+        const std::pair<int, std::uint32_t> pre{l, k.second >> (k.first - l)};
+        if (!node.count(pre)) node.emplace(pre, static_cast<int>(node.size()));
+      }
+  if (node.size() > static_cast<std::size_t>(kFsmStates)) return;
+  for (const auto& [pre, id] : node) {
+    for (std::uint32_t b = 0; b < 256; ++b) {
+      int l = pre.first;
+      std::uint32_t v = pre.second, syms = 0, cm = 0, n = 0;
+      for (int i = 0; i < 8; ++i) {
+        ++l;
+        v = (v << 1) | ((b >> (7 - i)) & 1u);
+        auto f = leaf.find({l, v});
+        if (f != leaf.end()) {
+          if (n == 4) return;  // cannot happen with words >= 2 bits
+          syms |= static_cast<std::uint32_t>(f->second) << (4 * n);
+          cm |= 1u << i;
+          ++n;
+          l = 0;
+          v = 0;
+        } else if (!node.count({l, v})) {
+          return;  // not a prefix of any word: the code is incomplete
+        }
+      }
+      const std::uint32_t next = static_cast<std::uint32_t>(node.at({l, v}));
+      t.fsm[id * 256 + b] = (4 * n) | (next << 8) | (syms << 16);
+      t.fsm_cm[id * 256 + b] = static_cast<std::uint8_t>(cm);
+    }
+  }
+  t.fsm_ok = true;
 }
 }  // namespace
 
@@ -47,6 +105,8 @@ DecodeTables build_tables(const std::uint8_t lengths[16]) {
       same[r][v] = (a == b) ? a : kUndetermined;
     }
   }
+
+  build_fsm(code, t);
 
   t.fast.resize(kFastEntries);
   t.smask.resize(kFastEntries);

@@ -30,6 +30,7 @@
 namespace ecf8::dev {
 
 inline constexpr int kFastBits = 12;
+inline constexpr int kFsmStates = 16;  // internal nodes of a complete 16-symbol code tree: <= 15
 inline constexpr int kFastEntries = 1 << kFastBits;
 inline constexpr int kMaxPerEntry = 5;
 
@@ -40,6 +41,19 @@ struct DecodeTables {
   std::vector<std::uint8_t> cascade;   // n_luts * 256, reference layout
   std::uint32_t n_luts = 0;
   std::uint64_t lenpack = 0;           // 4 bits per symbol: length & 15 (16 -> 0)
+  // Byte-step decoder (finite-state machine over the code tree), available
+  // when the code is complete (Kraft sum 1: every bit string parses) and
+  // every word is >= 2 bits (<= 4 words complete per input byte).  A state is
+  // an internal node of the code tree (the pending prefix; 0 = root, i.e. at
+  // a code boundary).  fsm[state * 256 + byte] (uint32):
+  //   bits  0..4   n4 = 4 * (code words completed by the byte, MSB first), <= 16
+  //   bits  8..11  next state
+  //   bits 16..31  the completed words' symbols, first lowest (4 bits each)
+  // fsm_cm[state * 256 + byte]: bit i set iff a word completes at bit i of
+  // the byte (bit 0 = the byte's most significant bit).
+  bool fsm_ok = false;
+  std::vector<std::uint32_t> fsm;     // kFsmStates * 256 (zeros when !fsm_ok)
+  std::vector<std::uint8_t> fsm_cm;   // kFsmStates * 256
 };
 
 // Throws std::invalid_argument("invalid length vector") like the reference.

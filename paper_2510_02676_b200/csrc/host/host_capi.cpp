@@ -129,6 +129,15 @@ int ecf8_host_device_tables(const uint8_t lengths[16], uint32_t* fast, uint16_t*
   });
 }
 
+int ecf8_host_fsm_tables(const uint8_t lengths[16], uint32_t* fsm, uint8_t* cm, int* ok) {
+  return guarded([&] {
+    const ecf8::dev::DecodeTables t = ecf8::dev::build_tables(lengths);
+    std::memcpy(fsm, t.fsm.data(), t.fsm.size() * 4);
+    std::memcpy(cm, t.fsm_cm.data(), t.fsm_cm.size());
+    *ok = t.fsm_ok ? 1 : 0;
+  });
+}
+
 int ecf8_host_encode(const uint8_t* fp8, uint64_t n, uint32_t T, const uint8_t* lengths,
                      ecf8_host_tensor** out) {
   return guarded([&] {
