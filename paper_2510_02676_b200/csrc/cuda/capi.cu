@@ -184,6 +184,7 @@ struct ecf8_dev_tensor {
   std::uint32_t T = 0;
   std::uint64_t n_vtiles = 0;      // 256-window verification tiles (tile_ok bits)
   std::uint32_t* ok_bits = nullptr;  // their bitmap in the arena
+  std::uint8_t* endgap = nullptr;    // per-window end nibbles (verify_gaps_kernel)
   TensorDesc desc{};     // out / tile fields filled per launch
   std::uint64_t encoded_len = 0, gaps_len = 0, n_outpos = 0, packed_len = 0;
   std::uint8_t lengths[16] = {};
@@ -235,7 +236,8 @@ void alloc_arena(ecf8_dev_tensor* t, const ecf8_sections* s, std::uint64_t nb, c
   const std::uint64_t off_pak = align_up(off_pos + 8 * s->n_outpos, 256);
   const std::uint64_t n_vtiles = (nb * s->threads_per_block + 255) / 256;
   const std::uint64_t off_ok = align_up(off_pak + s->packed_len + P, 256);
-  const std::uint64_t total = align_up(off_ok + 4 * ((n_vtiles + 31) / 32), 256);
+  const std::uint64_t off_eg = align_up(off_ok + 4 * ((n_vtiles + 31) / 32), 256);
+  const std::uint64_t total = align_up(off_eg + (nb * s->threads_per_block + 1) / 2 + P, 256);
   if (pooled) {
     // stream-ordered pool (the device encoder: many tensors created and
     // dropped in a row; cudaMalloc/cudaFree cost ~1 ms each at 50 MB)
@@ -260,6 +262,7 @@ void alloc_arena(ecf8_dev_tensor* t, const ecf8_sections* s, std::uint64_t nb, c
   cu(cudaMemsetAsync(base, 0, total, st), "cudaMemset");
   t->n_vtiles = n_vtiles;
   t->ok_bits = reinterpret_cast<std::uint32_t*>(base + off_ok);
+  t->endgap = base + off_eg;
   t->encoded_len = s->encoded_len;
   t->gaps_len = s->gaps_len;
   t->n_outpos = s->n_outpos;
@@ -307,17 +310,19 @@ void upload_into(ecf8_dev_tensor* t, const ecf8_sections* s, std::uint64_t nb, c
        "H2D packed");
 }
 
-// Gap check at upload (verify_gaps_kernel): tiles whose windows all end where
-// the next window's gap says take the continuous walk; the rest keep the
-// reference's window-by-window semantics.
+// Gap check at upload (verify_gaps_kernel): every window's end (endgap) is
+// recorded; tiles whose 8-window lanes are internally consistent (each window
+// ends where the next one's gap says) take the continuous walk, the rest
+// keep the reference's window-by-window semantics.
 void verify_into(ecf8_dev_tensor* t, cudaStream_t st) {
   static const bool off = std::getenv("ECF8_NO_CONT_WALK") != nullptr;  // A/B runs
   const int vid = t->n_elem ? ecf8::dev::variant_for(t->T, t->desc.lmin).id : -1;
   if (off || (vid != 4 && vid != 5)) return;
   std::uint32_t* const ok = t->ok_bits;
   cu(cudaMemsetAsync(ok, 0xFF, 4 * ((t->n_vtiles + 31) / 32), st), "memset(tile_ok)");
-  cu(ecf8::dev::launch_verify_gaps(t->desc, ok, st), "verify launch");
+  cu(ecf8::dev::launch_verify_gaps(t->desc, ok, t->endgap, st), "verify launch");
   t->desc.tile_ok = ok;
+  t->desc.endgap = t->endgap;
 }
 
 // Single-descriptor launch: the descriptor rides in the kernel parameters.

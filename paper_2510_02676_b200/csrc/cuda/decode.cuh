@@ -21,6 +21,7 @@ struct TensorDesc {
   const std::uint32_t* tile_ok;  // bit v: gaps of windows [256v, 256v+256) verified (nullptr: none)
   const std::uint32_t* fsm;      // tables.hpp byte-step decoder (nullptr: the code has none)
   const std::uint8_t* fsm_cm;    // its completion masks
+  const std::uint8_t* endgap;    // per window, gap layout: where its reference walk stops, minus 64 (upload check)
   std::uint8_t* out;             // element i lands at out[i - out_offset]
   std::uint64_t out_offset;      // multiple of 16
   std::uint64_t n_elem;
@@ -93,10 +94,12 @@ struct LaunchArgs {
 // One decode launch; every descriptor was prepared for variant `variant`.
 cudaError_t launch_decode(const LaunchArgs& args, int variant, cudaStream_t stream);
 
-// Gap check of a whole tensor (d.blk_begin == 0): clears bit v of tile_ok
-// (pre-set to all ones) unless every window w in [256v, 256v + 256) with a
-// successor ends where window w + 1's gap says (window_end).
-cudaError_t launch_verify_gaps(const TensorDesc& d, std::uint32_t* tile_ok, cudaStream_t stream);
+// Gap check of a whole tensor (d.blk_begin == 0): writes every window's
+// end nibble (window_end - 64, endgap) and clears bit v of tile_ok (pre-set
+// to all ones) unless every window w in [256v, 256v + 256) that is not the
+// last of an 8-window group (w % 8 != 7) ends where window w + 1's gap says.
+cudaError_t launch_verify_gaps(const TensorDesc& d, std::uint32_t* tile_ok, std::uint8_t* endgap,
+                               cudaStream_t stream);
 
 // count_phase on one window (window10 staged as 16 bytes in device memory).
 // Only the table fields of `tables` are used.

@@ -393,29 +393,29 @@ struct PairSink {
   }
 };
 
-// A lane's LW windows (verified tile) decoded by byte steps: the code words
-// from bit gap0 of its first window up to bit 64 LW + gnext, gnext = the gap
-// of the window after its last one.  On a verified tile that end is exactly
-// where the reference's walk of the last window stops (the first word
-// starting at or after the window boundary, codec.cpp:143-160 / 49-98), so
-// the words are those the reference's per-window walks take, in order.
-// w: the 2 LW window words + 2 lookahead words, big-endian.  Writes the
-// symbols to the slot at `slot` (word stride WS); returns their count.
-template <int LW, int WS>
-__device__ __forceinline__ std::uint32_t decode_lane_fsm(const std::uint32_t (&w)[2 * LW + 2], std::uint32_t gap0,
-                                                         std::uint32_t gnext, std::uint32_t slot) {
-  constexpr int NB = 8 * LW;     // bytes of the lane's windows
-  constexpr int NS = 2 * LW + 1;  // stream words from bit gap0: bytes 0 .. 4 NS - 1 >= NB + 2
+// The code words of n consecutive windows (w: their 2n big-endian words + 2
+// lookahead words) from bit gap0 of the first up to bit 64 n + end, decoded
+// by byte steps and appended to the sink.  With end = the last window's
+// endgap (its reference walk stops at bit 64 + end: the first word starting
+// at or after the window boundary, codec.cpp:143-160) this is exactly the
+// words the reference's walks of the n windows take -- for n = 1 always,
+// for n > 1 when every inner window ends where the next one's gap says
+// (the upload check).  A complete code parses every bit string the way the
+// reference's decode_one chain does, so no fallback is needed.
+template <int NWIN, int WS>
+__device__ __forceinline__ void decode_windows_fsm(const std::uint32_t* w, std::uint32_t gap0, std::uint32_t end,
+                                                   PairSink<WS>& sink) {
+  constexpr int NB = 8 * NWIN;      // bytes of the windows
+  constexpr int NS = 2 * NWIN + 1;  // stream words from bit gap0: bytes 0 .. 4 NS - 1 >= NB + 2
   std::uint32_t st[NS];
 #pragma unroll
   for (int i = 0; i < NS; ++i) st[i] = __funnelshift_l(w[i + 1], w[i], gap0);
-  // end of the lane's words, relative to gap0: byte Bp, bit r of it
-  const std::uint32_t Lp = 64u * LW + gnext - gap0;  // in [64 LW - 15, 64 LW + 15]
+  // end of the words, relative to gap0: byte Bp, bit r of it
+  const std::uint32_t Lp = 64u * NWIN + end - gap0;  // in [64 n - 15, 64 n + 15]
   const std::uint32_t Bp = Lp >> 3, rmask = (1u << (Lp & 7)) - 1;
-  PairSink<WS> sink{slot};
   std::uint32_t e = 0;  // root
 #pragma unroll
-  for (int j = 0; j < NB - 2; j += 2) {  // bytes before NB - 2 <= Bp: all words complete inside the lane
+  for (int j = 0; j < NB - 2; j += 2) {  // bytes before NB - 2 <= Bp: every word they complete is taken
     const std::uint32_t e1 = fsm_entry(fsm_index(st[j >> 2], e, j));
     const std::uint32_t e2 = fsm_entry(fsm_index(st[(j + 1) >> 2], e1, j + 1));
     sink.put2(e1, e2);
@@ -438,7 +438,6 @@ __device__ __forceinline__ std::uint32_t decode_lane_fsm(const std::uint32_t (&w
     sink.put2(e1, e2);
     e = e2;
   }
-  return sink.finish(slot);
 }
 
 // Where window (w0..w3, gap)'s reference walk stops: the start of the first

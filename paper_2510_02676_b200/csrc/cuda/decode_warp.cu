@@ -117,10 +117,12 @@ __device__ __forceinline__ void warp_tile(const TensorDesc& d, const WarpIn& in,
   if constexpr (WIDE) {
     run = warp_decode_scan<kLaneWin, 128, true>(in, log2T, len_off, SmemTables{g_tb}, slot, lane,
                                                 tile_verified(d, in, log2T));
-  } else {
-    const bool verified = tile_verified(d, in, log2T) && d.fsm != nullptr;
+  } else if (d.fsm) {  // byte steps: whole lanes on verified tiles, else window by window
     run = warp_decode_scan<kLaneWin, 128, false, GlobalTables, true>(in, log2T, len_off, GlobalTables{d}, slot, lane,
-                                                                     verified);
+                                                                     tile_verified(d, in, log2T));
+  } else {  // an incomplete code (no encoder writes one): the reference walk per window, tables through L1
+    run = warp_decode_scan<kLaneWin, 128, false, GlobalTables, false>(in, log2T, len_off, GlobalTables{d}, slot, lane,
+                                                                      false);
   }
   GlobalOut out{d.out + ((in.A & ~std::uint64_t{15}) - d.out_offset)};
   compact_write<kWbUnroll>(d, in.A, in.E, run, ws, lane, out);
@@ -238,10 +240,11 @@ cudaError_t launch_nw(const LaunchArgs& args, cudaStream_t s) {
   return cudaLaunchKernelEx(&cfg, decode_warp_kernel<NW, WIDE>, args);
 }
 
-// One thread per window: window_end of its reference walk against the next
-// window's gap; a mismatch anywhere in a 256-window tile clears its bit.
+// One thread per window: its reference walk's end (window_end, codec.cpp:
+// 143-160) -> endgap nibble; a window inside an 8-window group that does not
+// end where the next window's gap says clears its 256-window tile's bit.
 __global__ void __launch_bounds__(256) verify_gaps_kernel(const TensorDesc d, std::uint64_t n_win,
-                                                          std::uint32_t* tile_ok) {
+                                                          std::uint32_t* tile_ok, std::uint8_t* endgap) {
   __shared__ Tables tb;
   stage_tables(d, tb, threadIdx.x, blockDim.x);
   __syncthreads();
@@ -249,17 +252,21 @@ __global__ void __launch_bounds__(256) verify_gaps_kernel(const TensorDesc d, st
   const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
   for (std::uint64_t k = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; k - threadIdx.x % 32 < n_win;
        k += stride) {
-    // the tensor's last window has no successor to check against: its tile
-    // keeps the window-by-window walk (the byte-step decoder ends a lane at
-    // the next window's gap)
-    bool bad = k + 1 == n_win;
-    if (k + 1 < n_win) {
+    bool bad = false;
+    std::uint32_t eg = 0;
+    if (k < n_win) {
       const uint2 a = __ldg(reinterpret_cast<const uint2*>(d.encoded + 8 * k));
       const uint2 b = __ldg(reinterpret_cast<const uint2*>(d.encoded + 8 * k + 8));
       const std::uint32_t g0 = (d.gaps[k >> 1] >> ((k & 1) ? 0 : 4)) & 15u;
-      const std::uint32_t g1 = (d.gaps[(k + 1) >> 1] >> (((k + 1) & 1) ? 0 : 4)) & 15u;
-      bad = window_end(bswap32(a.x), bswap32(a.y), bswap32(b.x), bswap32(b.y), g0, SmemTables{tb}, len_off) != 64 + g1;
+      eg = window_end(bswap32(a.x), bswap32(a.y), bswap32(b.x), bswap32(b.y), g0, SmemTables{tb}, len_off) - 64;
+      if ((k & 7) != 7 && k + 1 < n_win) {
+        const std::uint32_t g1 = (d.gaps[(k + 1) >> 1] >> (((k + 1) & 1) ? 0 : 4)) & 15u;
+        bad = eg != g1;
+      }
     }
+    // two windows per byte, the even one in the high nibble (gap layout)
+    const std::uint32_t pair = __shfl_xor_sync(0xffffffffu, eg, 1);
+    if (k < n_win && !(k & 1)) endgap[k >> 1] = static_cast<std::uint8_t>((eg << 4) | (k + 1 < n_win ? pair : 0u));
     if (__ballot_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) {
       const std::uint64_t v = k >> 8;
       atomicAnd(tile_ok + (v >> 5), ~(1u << (v & 31)));
@@ -285,11 +292,11 @@ cudaError_t launch_decode_warp(const LaunchArgs& args, cudaStream_t s) {
 // Variant 5 (1-bit codes): 12 warps x 16.5 KB of warp state.
 cudaError_t launch_decode_warp_wide(const LaunchArgs& args, cudaStream_t s) { return launch_nw<12, true>(args, s); }
 
-cudaError_t launch_verify_gaps(const TensorDesc& d, std::uint32_t* tile_ok, cudaStream_t s) {
+cudaError_t launch_verify_gaps(const TensorDesc& d, std::uint32_t* tile_ok, std::uint8_t* endgap, cudaStream_t s) {
   const std::uint64_t n_win = d.blk_end * d.T;
   if (n_win == 0) return cudaSuccess;
   const std::uint64_t blocks = (n_win + 255) / 256;
-  verify_gaps_kernel<<<static_cast<unsigned>(blocks < 1184 ? blocks : 1184), 256, 0, s>>>(d, n_win, tile_ok);
+  verify_gaps_kernel<<<static_cast<unsigned>(blocks < 1184 ? blocks : 1184), 256, 0, s>>>(d, n_win, tile_ok, endgap);
   // A plain launch after it: a decode launched next with programmatic
   // serialization may only overlap this empty grid, which starts after the
   // gap check has completed -- the tile bits are final before any decode reads them.

@@ -32,7 +32,7 @@ struct WarpInT {
   std::uint32_t nblk, nwin;
   std::uint64_t b0;
   std::uint32_t ok_a, ok_b;  // tile_ok words of the tile's first / last window (loaded one tile ahead)
-  std::uint32_t gnext;       // the next lane's gap word (its first window: bits 4..7) -- byte-step decoder only
+  std::uint32_t gnext;       // the lane's endgap word (gap layout) -- byte-step decoder only
 };
 using WarpIn = WarpInT<kLaneWin>;
 
@@ -56,13 +56,12 @@ __device__ __forceinline__ void load_tile_words(const TensorDesc& d, std::uint64
       in.w67 = __ldg(src + 3);
       in.w8 = __ldg(reinterpret_cast<const uint2*>(src + 4));
       in.gaps = __ldg(reinterpret_cast<const std::uint32_t*>(d.gaps + (w0g >> 1)) + lane);
-      // lane 31: the next tile's first window (gaps carry >= 64 bytes of padding)
-      if constexpr (NEXT) in.gnext = __ldg(reinterpret_cast<const std::uint32_t*>(d.gaps + (w0g >> 1)) + lane + 1);
+      if constexpr (NEXT) in.gnext = __ldg(reinterpret_cast<const std::uint32_t*>(d.endgap + (w0g >> 1)) + lane);
     } else {
       static_assert(LW == 4, "4 or 8 windows per lane");
       in.w8 = __ldg(reinterpret_cast<const uint2*>(src + 2));
       in.gaps = __ldg(reinterpret_cast<const std::uint16_t*>(d.gaps + (w0g >> 1)) + lane);
-      if constexpr (NEXT) in.gnext = __ldg(reinterpret_cast<const std::uint16_t*>(d.gaps + (w0g >> 1)) + lane + 1);
+      if constexpr (NEXT) in.gnext = __ldg(reinterpret_cast<const std::uint16_t*>(d.endgap + (w0g >> 1)) + lane);
     }
   }
 }
@@ -113,8 +112,9 @@ struct LaneRun {
 // upload-time gap check): one continuous walk over the lane's windows;
 // otherwise, or when the walk met a flagged entry, window by window with the
 // reference's per-window semantics (fast table, exact walk where flagged).
-// FSM: verified tiles take the byte-step decoder (staged at kFsmAt;
-// decode_lane_fsm) instead of the continuous fast-table walk.
+// FSM (the tensor's code has a byte-step decoder, staged at kFsmAt): a
+// verified tile's lanes decode their LW windows in one pass, the others
+// window by window, each up to its recorded end (decode_windows_fsm).
 template <int LW, int WS = 4, bool OR_BASE = false, class TV, bool FSM = false>
 __device__ __forceinline__ LaneRun warp_decode_scan(const WarpInT<LW>& in, std::uint32_t log2T,
                                                    std::uint32_t len_off, const TV& tb, std::uint32_t slot_base,
@@ -122,7 +122,7 @@ __device__ __forceinline__ LaneRun warp_decode_scan(const WarpInT<LW>& in, std::
   const std::uint32_t wl0 = static_cast<std::uint32_t>(lane) * LW;
   const bool active = wl0 < in.nwin;
   SlotSinkT<WS> sink{slot_base};
-  std::uint32_t cnt_fsm = 0;  // byte-step path: its count (the sink then stays empty)
+  PairSink<WS> psink{slot_base};  // byte-step path (the other sink then stays empty)
   if (active) {
     std::uint32_t w[2 * LW + 2];
     w[0] = bswap32(in.w01.x), w[1] = bswap32(in.w01.y), w[2] = bswap32(in.w01.z), w[3] = bswap32(in.w01.w);
@@ -134,10 +134,18 @@ __device__ __forceinline__ LaneRun warp_decode_scan(const WarpInT<LW>& in, std::
     w[2 * LW] = bswap32(in.w8.x), w[2 * LW + 1] = bswap32(in.w8.y);
     const std::uint32_t n = min(in.nwin - wl0, static_cast<std::uint32_t>(LW));
     bool windowed = true;
-    if (FSM && verified) {
-      cnt_fsm = decode_lane_fsm<LW, WS>(w, (in.gaps >> 4) & 15u, (in.gnext >> 4) & 15u, slot_base);
+    if constexpr (FSM) {
       windowed = false;
-    } else if (verified) {
+      if (verified) {
+        decode_windows_fsm<LW, WS>(w, (in.gaps >> 4) & 15u, (in.gnext >> (8 * ((LW - 1) >> 1))) & 15u, psink);
+      } else {
+#pragma unroll
+        for (int i = 0; i < LW; ++i) {
+          const int sh = 8 * (i >> 1) + ((i & 1) ? 0 : 4);  // window 2j: high nibble of byte j
+          decode_windows_fsm<1, WS>(w + 2 * i, (in.gaps >> sh) & 15u, (in.gnext >> sh) & 15u, psink);
+        }
+      }
+    } else if (!TV::kGlobal && verified) {
       const SlotSinkT<WS> saved = sink;
       const std::uint32_t gap0 = (in.gaps >> 4) & 15u;  // window 0: high nibble of byte 0
       // n == LW: tiles are whole blocks of T >= LW windows, so every active lane owns LW windows
@@ -158,7 +166,7 @@ __device__ __forceinline__ LaneRun warp_decode_scan(const WarpInT<LW>& in, std::
       }
     }
   }
-  const std::uint32_t cnt = sink.finish(slot_base) + cnt_fsm;
+  const std::uint32_t cnt = FSM ? psink.finish(slot_base) : sink.finish(slot_base);
 
   // warp scan, segmented by reference block (2^(log2T-3) lanes each)
   std::uint32_t incl = cnt;
