@@ -362,6 +362,8 @@ struct HostCtx {
   cudaStream_t s_in = nullptr, s_run = nullptr, s_out = nullptr;
   struct Slot {
     std::uint8_t *enc, *pak, *out;
+    std::uint8_t* eg;     // the chunk's window ends (verify_gaps_kernel)
+    std::uint32_t* ok;    // and its tile_ok words
     cudaEvent_t in, run, out_done;
     bool used;
   } slot[kSlots]{};
@@ -391,14 +393,19 @@ HostCtx& host_ctx() {
     const std::uint64_t b_enc = align_up(c.enc_chunk + ecf8::dev::kTileBytesMax + S, 256);
     const std::uint64_t b_pak = align_up(c.elem_chunk / 2 + ecf8::dev::kTileElemsMax + S, 256);
     const std::uint64_t b_out = align_up(c.elem_chunk + 2 * ecf8::dev::kTileElemsMax + S, 256);
+    const std::uint64_t b_eg = align_up(b_enc / 16 + S, 256);              // a nibble per 8-byte window
+    const std::uint64_t b_ok = align_up(4 * (b_enc / 8 / 8192 + 2), 256);  // a bit per 256 windows (+ a straddled word)
     for (auto& sl : c.slot) {
       void* p = nullptr;
-      cu(cudaMalloc(&p, b_enc + b_pak + b_out), "cudaMalloc(staging)");
-      cu(cudaMemset(p, 0, b_enc + b_pak + b_out), "cudaMemset(staging)");
+      const std::uint64_t all = b_enc + b_pak + b_out + b_eg + b_ok;
+      cu(cudaMalloc(&p, all), "cudaMalloc(staging)");
+      cu(cudaMemset(p, 0, all), "cudaMemset(staging)");
       auto* base = static_cast<std::uint8_t*>(p);
       sl.enc = base;
       sl.pak = base + b_enc;
       sl.out = base + b_enc + b_pak;
+      sl.eg = base + b_enc + b_pak + b_out;
+      sl.ok = reinterpret_cast<std::uint32_t*>(base + b_enc + b_pak + b_out + b_eg);
       cu(cudaEventCreateWithFlags(&sl.in, cudaEventDisableTiming), "event");
       cu(cudaEventCreateWithFlags(&sl.run, cudaEventDisableTiming), "event");
       cu(cudaEventCreateWithFlags(&sl.out_done, cudaEventDisableTiming), "event");
@@ -423,17 +430,23 @@ P rebase(P slot, std::uint64_t lo_bytes) {
 // on s_run and chunk k-2's bytes come back on s_out, across tensor
 // boundaries.  With pinned host memory both PCIe directions and the
 // decode overlap; the call returns when every byte is in `outs`.
-int host_pipeline(const ecf8_sections* const* ss, const std::uint64_t* nbs, std::uint8_t* const* outs, int count) {
+//
+// blk_lo / blk_hi (optional): decode only blocks [blk_lo[i], blk_hi[i]) of
+// tensor i -- its elements [outpos[lo], outpos[hi]) land at the same offsets
+// of outs[i] (decode_block); only those blocks' sections cross PCIe.
+int host_pipeline(const ecf8_sections* const* ss, const std::uint64_t* nbs, std::uint8_t* const* outs, int count,
+                  const std::uint64_t* blk_lo = nullptr, const std::uint64_t* blk_hi = nullptr) {
   HostCtx& c = host_ctx();
   std::uint64_t k = 0, remaining = 0;
-  for (int i = 0; i < count; ++i) remaining += ss[i]->n_elem;
+  for (int i = 0; i < count; ++i)
+    remaining += blk_lo ? ss[i]->outpos[blk_hi[i]] - ss[i]->outpos[blk_lo[i]] : ss[i]->n_elem;
   std::uint64_t target = c.elem_min;
   int parity = 0;
   static const bool skip_kernel = std::getenv("ECF8_DIAG_NO_KERNEL") != nullptr;  // PCIe-only diagnostics
   for (int i = 0; i < count; ++i) {
     const ecf8_sections* s = ss[i];
-    const std::uint64_t nb = nbs[i];
-    if (s->n_elem == 0) continue;
+    const std::uint64_t b_begin = blk_lo ? blk_lo[i] : 0, nb = blk_lo ? blk_hi[i] : nbs[i];
+    if (s->n_elem == 0 || s->outpos[nb] == s->outpos[b_begin]) continue;
     std::uint8_t* const out = outs[i];
     const std::uint32_t T = s->threads_per_block;
     const ecf8::dev::Variant v = ecf8::dev::variant_for(T, lmin_of(s->lengths));
@@ -454,8 +467,10 @@ int host_pipeline(const ecf8_sections* const* ss, const std::uint64_t* nbs, std:
 
     HostCtx::Meta& mt = c.meta[parity];
     parity ^= 1;
-    const std::uint64_t off_pos = align_up(s->gaps_len + ecf8::dev::kPad, 256);
-    const std::uint64_t need = off_pos + 8 * s->n_outpos;
+    // the blocks' gaps (window nibbles [b_begin T, nb T)) and outpos [b_begin, nb]
+    const std::uint64_t g0 = (b_begin * T) >> 1, g1 = std::min(s->gaps_len, (nb * T + 1) / 2 + 1);
+    const std::uint64_t off_pos = align_up(g1 - g0 + ecf8::dev::kPad, 256);
+    const std::uint64_t need = off_pos + 8 * (nb - b_begin + 1);
     if (need > mt.cap) {
       if (mt.used) cu(cudaEventSynchronize(mt.done), "sync");
       if (mt.buf) cudaFree(mt.buf);
@@ -467,11 +482,12 @@ int host_pipeline(const ecf8_sections* const* ss, const std::uint64_t* nbs, std:
       cu(cudaStreamWaitEvent(c.s_in, mt.done, 0), "wait");
     }
     mt.used = true;
-    cu(cudaMemcpyAsync(mt.buf, s->gaps, s->gaps_len, cudaMemcpyHostToDevice, c.s_in), "H2D gaps");
-    cu(cudaMemcpyAsync(mt.buf + off_pos, s->outpos, 8 * s->n_outpos, cudaMemcpyHostToDevice, c.s_in), "H2D outpos");
-    d.gaps = mt.buf;
-    d.outpos = reinterpret_cast<const std::uint64_t*>(mt.buf + off_pos);
-    for (std::uint64_t lo = 0; lo < nb; ++k) {
+    if (g1 > g0) cu(cudaMemcpyAsync(mt.buf, s->gaps + g0, g1 - g0, cudaMemcpyHostToDevice, c.s_in), "H2D gaps");
+    cu(cudaMemcpyAsync(mt.buf + off_pos, s->outpos + b_begin, 8 * (nb - b_begin + 1), cudaMemcpyHostToDevice, c.s_in),
+       "H2D outpos");
+    d.gaps = rebase(static_cast<const std::uint8_t*>(mt.buf), g0);
+    d.outpos = rebase(reinterpret_cast<const std::uint64_t*>(mt.buf + off_pos), 8 * b_begin);
+    for (std::uint64_t lo = b_begin; lo < nb; ++k) {
       // grow the chunk tile by tile up to the ramped target and slot limits
       const std::uint64_t want =
           std::max(c.elem_min, std::min({target, c.elem_chunk, remaining / 3}));
@@ -502,6 +518,17 @@ int host_pipeline(const ecf8_sections* const* ss, const std::uint64_t* nbs, std:
       dk.out_offset = o0 & ~std::uint64_t{15};
       dk.blk_begin = lo;
       dk.blk_end = hi;
+      if (v.id == 4 && dk.fsm && !skip_kernel) {
+        // the byte-step decoder needs every window's end: the upload check on
+        // this chunk (its windows only) into the slot's scratch
+        const std::uint64_t w0 = lo * T;
+        dk.endgap = rebase(sl.eg, w0 >> 1);
+        dk.tile_ok = rebase(sl.ok, 4 * (w0 >> 13));
+        cu(cudaMemsetAsync(sl.ok, 0xFF, 4 * (((hi * T) >> 13) - (w0 >> 13) + 1), c.s_run), "memset(tile_ok)");
+        cu(ecf8::dev::launch_verify_gaps(dk, const_cast<std::uint32_t*>(dk.tile_ok),
+                                         const_cast<std::uint8_t*>(dk.endgap), c.s_run),
+           "verify launch");
+      }
       if (!skip_kernel)
         if (int rc = launch_one(dk, c.s_run)) return rc;
       cu(cudaEventRecord(sl.run, c.s_run), "record");
@@ -892,35 +919,11 @@ int ecf8_decode_block_host(const ecf8_sections* s, uint64_t block, uint8_t* out,
     if (int rc = validate(s, &nb)) return rc;
     if (block >= nb) return fail(ECF8_EINVAL, "block index out of range");
     if (out_len < s->outpos[block + 1]) return fail(ECF8_EINVAL, "output size mismatch");
-    const std::uint64_t lo = s->outpos[block], hi = s->outpos[block + 1];
-    if (hi == lo) return ECF8_OK;
+    if (s->outpos[block + 1] == s->outpos[block]) return ECF8_OK;
     if (int rc = require_device()) return rc;
-    ecf8_dev_tensor t;
-    upload_into(&t, s, nb, nullptr);
-    const std::uint64_t off = lo & ~std::uint64_t{15};
-    std::uint8_t* d_out = nullptr;
-    const cudaError_t ae = cudaMalloc(&d_out, align_up(hi - off, 16) + 16);
-    if (ae != cudaSuccess) {
-      cudaFree(t.arena);
-      cu(ae, "cudaMalloc(out)");
-    }
-    int rc = ECF8_OK;
-    try {
-      TensorDesc d = t.desc;
-      d.out = d_out;
-      d.out_offset = off;
-      d.blk_begin = block;
-      d.blk_end = block + 1;
-      rc = launch_one(d, nullptr);
-      if (rc == ECF8_OK) cu(cudaMemcpy(out + lo, d_out + (lo - off), hi - lo, cudaMemcpyDeviceToHost), "D2H block");
-    } catch (...) {
-      cudaFree(d_out);
-      cudaFree(t.arena);
-      throw;
-    }
-    cudaFree(d_out);
-    cudaFree(t.arena);
-    return rc;
+    // only this block's sections go to the device (decode_block, codec.cpp:201-254)
+    const std::uint64_t hi = block + 1;
+    return host_pipeline(&s, &nb, &out, 1, &block, &hi);
   });
 }
 

@@ -94,7 +94,8 @@ struct LaunchArgs {
 // One decode launch; every descriptor was prepared for variant `variant`.
 cudaError_t launch_decode(const LaunchArgs& args, int variant, cudaStream_t stream);
 
-// Gap check of a whole tensor (d.blk_begin == 0): writes every window's
+// Gap check of blocks [d.blk_begin, d.blk_end) (whole 256-window tiles;
+// tile_ok / endgap indexed by global window number): writes every window's
 // end nibble (window_end - 64, endgap) and clears bit v of tile_ok (pre-set
 // to all ones) unless every window w in [256v, 256v + 256) that is not the
 // last of an 8-window group (w % 8 != 7) ends where window w + 1's gap says.

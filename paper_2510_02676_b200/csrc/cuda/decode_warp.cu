@@ -243,15 +243,17 @@ cudaError_t launch_nw(const LaunchArgs& args, cudaStream_t s) {
 // One thread per window: its reference walk's end (window_end, codec.cpp:
 // 143-160) -> endgap nibble; a window inside an 8-window group that does not
 // end where the next window's gap says clears its 256-window tile's bit.
-__global__ void __launch_bounds__(256) verify_gaps_kernel(const TensorDesc d, std::uint64_t n_win,
-                                                          std::uint32_t* tile_ok, std::uint8_t* endgap) {
+__global__ void __launch_bounds__(256) verify_gaps_kernel(const TensorDesc d, std::uint64_t w_begin,
+                                                          std::uint64_t n_win, std::uint32_t* tile_ok,
+                                                          std::uint8_t* endgap) {
   __shared__ Tables tb;
   stage_tables(d, tb, threadIdx.x, blockDim.x);
   __syncthreads();
   const std::uint32_t len_off = (d.n_luts - 1) << 8;
   const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
-  for (std::uint64_t k = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; k - threadIdx.x % 32 < n_win;
-       k += stride) {
+  // windows [w_begin, n_win) (w_begin a multiple of 256: whole tiles)
+  for (std::uint64_t k = w_begin + blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
+       k - threadIdx.x % 32 < n_win; k += stride) {
     bool bad = false;
     std::uint32_t eg = 0;
     if (k < n_win) {
@@ -293,10 +295,11 @@ cudaError_t launch_decode_warp(const LaunchArgs& args, cudaStream_t s) {
 cudaError_t launch_decode_warp_wide(const LaunchArgs& args, cudaStream_t s) { return launch_nw<12, true>(args, s); }
 
 cudaError_t launch_verify_gaps(const TensorDesc& d, std::uint32_t* tile_ok, std::uint8_t* endgap, cudaStream_t s) {
-  const std::uint64_t n_win = d.blk_end * d.T;
-  if (n_win == 0) return cudaSuccess;
-  const std::uint64_t blocks = (n_win + 255) / 256;
-  verify_gaps_kernel<<<static_cast<unsigned>(blocks < 1184 ? blocks : 1184), 256, 0, s>>>(d, n_win, tile_ok, endgap);
+  const std::uint64_t w_begin = d.blk_begin * d.T, n_win = d.blk_end * d.T;
+  if (n_win <= w_begin) return cudaSuccess;
+  const std::uint64_t blocks = (n_win - w_begin + 255) / 256;
+  verify_gaps_kernel<<<static_cast<unsigned>(blocks < 1184 ? blocks : 1184), 256, 0, s>>>(d, w_begin, n_win, tile_ok,
+                                                                                        endgap);
   // A plain launch after it: a decode launched next with programmatic
   // serialization may only overlap this empty grid, which starts after the
   // gap check has completed -- the tile bits are final before any decode reads them.
