@@ -117,7 +117,7 @@ __device__ __forceinline__ void warp_tile(const TensorDesc& d, const WarpIn& in,
   if constexpr (WIDE) {
     run = warp_decode_scan<kLaneWin, 128, true>(in, log2T, len_off, SmemTables{g_tb}, slot, lane,
                                                 tile_verified(d, in, log2T));
-  } else if (d.fsm) {  // byte steps: whole lanes on verified tiles, else window by window
+  } else if (d.fsm && d.endgap) {  // byte steps: whole lanes on verified tiles, else window by window
     run = warp_decode_scan<kLaneWin, 128, false, GlobalTables, true>(in, log2T, len_off, GlobalTables{d}, slot, lane,
                                                                      tile_verified(d, in, log2T));
   } else {  // an incomplete code (no encoder writes one): the reference walk per window, tables through L1

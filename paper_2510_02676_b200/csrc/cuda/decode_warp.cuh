@@ -56,12 +56,14 @@ __device__ __forceinline__ void load_tile_words(const TensorDesc& d, std::uint64
       in.w67 = __ldg(src + 3);
       in.w8 = __ldg(reinterpret_cast<const uint2*>(src + 4));
       in.gaps = __ldg(reinterpret_cast<const std::uint32_t*>(d.gaps + (w0g >> 1)) + lane);
-      if constexpr (NEXT) in.gnext = __ldg(reinterpret_cast<const std::uint32_t*>(d.endgap + (w0g >> 1)) + lane);
+      if constexpr (NEXT)  // (no byte-step decoder -> no recorded ends)
+        in.gnext = d.endgap ? __ldg(reinterpret_cast<const std::uint32_t*>(d.endgap + (w0g >> 1)) + lane) : 0u;
     } else {
       static_assert(LW == 4, "4 or 8 windows per lane");
       in.w8 = __ldg(reinterpret_cast<const uint2*>(src + 2));
       in.gaps = __ldg(reinterpret_cast<const std::uint16_t*>(d.gaps + (w0g >> 1)) + lane);
-      if constexpr (NEXT) in.gnext = __ldg(reinterpret_cast<const std::uint16_t*>(d.endgap + (w0g >> 1)) + lane);
+      if constexpr (NEXT)
+        in.gnext = d.endgap ? __ldg(reinterpret_cast<const std::uint16_t*>(d.endgap + (w0g >> 1)) + lane) : 0u;
     }
   }
 }
