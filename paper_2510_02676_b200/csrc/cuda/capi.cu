@@ -316,7 +316,7 @@ void upload_into(ecf8_dev_tensor* t, const ecf8_sections* s, std::uint64_t nb, c
 // keep the reference's window-by-window semantics.
 void verify_into(ecf8_dev_tensor* t, cudaStream_t st) {
   static const bool off = std::getenv("ECF8_NO_CONT_WALK") != nullptr;  // A/B runs
-  const int vid = t->n_elem ? ecf8::dev::variant_for(t->T, t->desc.lmin).id : -1;
+  const int vid = t->n_elem ? ecf8::dev::variant_for(t->T, t->desc.lmin, t->desc.fsm != nullptr).id : -1;
   if (off || (vid != 4 && vid != 5)) return;
   std::uint32_t* const ok = t->ok_bits;
   cu(cudaMemsetAsync(ok, 0xFF, 4 * ((t->n_vtiles + 31) / 32), st), "memset(tile_ok)");
@@ -328,7 +328,7 @@ void verify_into(ecf8_dev_tensor* t, cudaStream_t st) {
 // Single-descriptor launch: the descriptor rides in the kernel parameters.
 int launch_one(const TensorDesc& d, cudaStream_t st, int variant_override = -1) {
   if (d.blk_end <= d.blk_begin) return ECF8_OK;
-  ecf8::dev::Variant v = ecf8::dev::variant_for(d.T, d.lmin);
+  ecf8::dev::Variant v = ecf8::dev::variant_for(d.T, d.lmin, d.fsm != nullptr);
   if (variant_override >= 0) v.id = variant_override;
   ecf8::dev::LaunchArgs a{};
   a.descs = nullptr;
@@ -341,7 +341,9 @@ int launch_one(const TensorDesc& d, cudaStream_t st, int variant_override = -1) 
 }
 
 // Launch variant for a device tensor.
-int tensor_variant(const ecf8_dev_tensor* t) { return ecf8::dev::variant_for(t->T, t->desc.lmin).id; }
+int tensor_variant(const ecf8_dev_tensor* t) {
+  return ecf8::dev::variant_for(t->T, t->desc.lmin, t->desc.fsm != nullptr).id;
+}
 
 // Per-thread state of the host-span path: three streams (copy-in, decode,
 // copy-out) and a ring of chunk slots in HBM.  Deliberately never freed:
@@ -449,10 +451,10 @@ int host_pipeline(const ecf8_sections* const* ss, const std::uint64_t* nbs, std:
     if (s->n_elem == 0 || s->outpos[nb] == s->outpos[b_begin]) continue;
     std::uint8_t* const out = outs[i];
     const std::uint32_t T = s->threads_per_block;
-    const ecf8::dev::Variant v = ecf8::dev::variant_for(T, lmin_of(s->lengths));
+    const DevTables& tb = device_tables(s->lengths);
+    const ecf8::dev::Variant v = ecf8::dev::variant_for(T, lmin_of(s->lengths), tb.fsm != nullptr);
     const std::uint64_t m = ecf8::dev::blocks_per_tile(T, v.tile_win);
     const std::uint64_t tile_enc = m * T * 8;
-    const DevTables& tb = device_tables(s->lengths);
     TensorDesc d{};
     d.n_elem = s->n_elem;
     d.T = T;
@@ -834,7 +836,7 @@ int ecf8_batch_create(const ecf8_dev_tensor* const* ts, uint8_t* const* d_outs, 
       for (int i = 0; i < count; ++i) {
         const ecf8_dev_tensor* t = ts[i];
         if (!t) return fail(ECF8_EINVAL, "null tensor");
-        const ecf8::dev::Variant v = ecf8::dev::variant_for(t->T, t->desc.lmin);
+        const ecf8::dev::Variant v = ecf8::dev::variant_for(t->T, t->desc.lmin, t->desc.fsm != nullptr);
         if (t->n_elem == 0 || tensor_variant(t) != kw) continue;
         kwin_tile = v.tile_win;
         if (!d_outs[i] || (reinterpret_cast<std::uintptr_t>(d_outs[i]) & 15))

@@ -61,9 +61,11 @@ struct Variant {
 
 bool warp_variant_enabled();  // false when ECF8_NO_WARP_KERNEL=1 (A/B runs)
 
-inline Variant variant_for(std::uint32_t T, std::uint32_t lmin) {
-  if (lmin >= 2 && T >= 8 && T <= 256 && warp_variant_enabled()) return {8, 32, 4, 256};
-  if (lmin == 1 && T >= 8 && T <= 256 && warp_variant_enabled()) return {8, 64, 5, 256};
+// fsm: the code has a byte-step decoder (tables.hpp; complete, Lmin >= 2),
+// which variant 4 needs; other codes with T in [8, 256] take variant 5.
+inline Variant variant_for(std::uint32_t T, std::uint32_t lmin, bool fsm = true) {
+  if (lmin >= 2 && fsm && T >= 8 && T <= 256 && warp_variant_enabled()) return {8, 32, 4, 256};
+  if (lmin >= 1 && T >= 8 && T <= 256 && warp_variant_enabled()) return {8, 64, 5, 256};
   if (T == 1) return {1, 8, 0, kThreads};
   if (T == 2) return {2, 16, 1, 2 * kThreads};
   if (lmin >= 2) return {4, 16, 2, 4 * kThreads};

@@ -31,6 +31,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <cstdlib>
+#include <type_traits>
 
 #include "decode.cuh"
 #include "decode_common.cuh"
@@ -106,26 +107,28 @@ struct GlobalOut {
   __device__ __forceinline__ void done() const {}
 };
 
-// One tile: decode + scan, compact, write back.
+// One tile: decode + scan, compact, write back.  WIDE (1-bit codes, or a
+// code without a byte-step decoder): one 8-window walk per lane with the
+// staged fast / cascade tables; otherwise two interleaved 4-window byte-step
+// chains per lane (warp_decode_scan2).
 template <bool WIDE, class WSm>
-__device__ __forceinline__ void warp_tile(const TensorDesc& d, const WarpIn& in, std::uint32_t log2T,
-                                          std::uint32_t len_off, WSm& ws, int lane) {
+__device__ __forceinline__ void warp_tile(const TensorDesc& d, const std::conditional_t<WIDE, WarpIn, WarpIn2>& in,
+                                          std::uint32_t log2T, std::uint32_t len_off, WSm& ws, int lane) {
   // slots interleaved word by word (word j of lane L at slot[32 j + L]): the
   // lanes' slot stores and reads hit 32 different banks
   const std::uint32_t slot = smem_addr(ws.slot + lane);
-  LaneRun run;
-  if constexpr (WIDE) {
-    run = warp_decode_scan<kLaneWin, 128, true>(in, log2T, len_off, SmemTables{g_tb}, slot, lane,
-                                                tile_verified(d, in, log2T));
-  } else if (d.fsm && d.endgap) {  // byte steps: whole lanes on verified tiles, else window by window
-    run = warp_decode_scan<kLaneWin, 128, false, GlobalTables, true>(in, log2T, len_off, GlobalTables{d}, slot, lane,
-                                                                     tile_verified(d, in, log2T));
-  } else {  // an incomplete code (no encoder writes one): the reference walk per window, tables through L1
-    run = warp_decode_scan<kLaneWin, 128, false, GlobalTables, false>(in, log2T, len_off, GlobalTables{d}, slot, lane,
-                                                                      false);
-  }
   GlobalOut out{d.out + ((in.A & ~std::uint64_t{15}) - d.out_offset)};
-  compact_write<kWbUnroll>(d, in.A, in.E, run, ws, lane, out);
+  if constexpr (WIDE) {
+    const LaneRun run = warp_decode_scan<kLaneWin, 128, true>(in, log2T, len_off, SmemTables{g_tb}, slot, lane,
+                                                              tile_verified(d, in, log2T));
+    compact_write<kWbUnroll>(d, in.A, in.E, run, ws, lane, out);
+  } else {
+    const std::uint64_t w0 = in.b0 << log2T;
+    const std::uint32_t v0 = static_cast<std::uint32_t>(w0 >> 8), v1 = static_cast<std::uint32_t>((w0 + in.nwin - 1) >> 8);
+    const bool verified = ((in.ok_a >> (v0 & 31)) & (in.ok_b >> (v1 & 31)) & 1u) != 0;
+    const LaneRun2 run = warp_decode_scan2<128>(in, log2T, slot, lane, verified);
+    compact_write2<kWbUnroll>(d, in.A, in.E, run, ws, lane, out);
+  }
 }
 
 template <int NW, bool WIDE>
@@ -183,11 +186,16 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_warp_kernel(const LaunchArg
     // tile seg + w, then takes the next unclaimed one), so the warps of a
     // segment finish within one tile of each other whatever the per-tile
     // cost.  The next tile is claimed and its inputs loaded one tile ahead.
-    WarpIn nxt;
+    using In = std::conditional_t<WIDE, WarpIn, WarpIn2>;
+    auto load = [&](std::uint64_t t, In& in) {
+      if constexpr (WIDE) load_warp_tile(d, t, log2T, lane, in);
+      else load_warp_tile2(d, t, log2T, lane, in);
+    };
+    In nxt;
     std::uint64_t tile = seg + warp;
-    if (tile < seg_end) load_warp_tile<kLaneWin, !WIDE>(d, tile, log2T, lane, nxt);
+    if (tile < seg_end) load(tile, nxt);
     while (tile < seg_end) {
-      const WarpIn cur = nxt;
+      const In cur = nxt;
 #ifndef ECF8_NO_PK_PREFETCH
       if (lane == 0) {  // sign/mantissa bytes of this tile -> L2 (one bulk TMA prefetch)
         const std::uint64_t p0 = (cur.A >> 1) & ~std::uint64_t{15};
@@ -199,7 +207,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_warp_kernel(const LaunchArg
       unsigned claim = 0;
       if (lane == 0) claim = atomicAdd(&next_tile, 1u);
       const std::uint64_t next = seg + __shfl_sync(0xffffffffu, claim, 0);
-      if (next < seg_end) load_warp_tile<kLaneWin, !WIDE>(d, next, log2T, lane, nxt);
+      if (next < seg_end) load(next, nxt);
       warp_tile<WIDE>(d, cur, log2T, len_off, ws, lane);
       tile = next;
     }
