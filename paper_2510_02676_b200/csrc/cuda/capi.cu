@@ -189,15 +189,31 @@ struct ecf8_dev_tensor {
   std::uint64_t encoded_len = 0, gaps_len = 0, n_outpos = 0, packed_len = 0;
   std::uint8_t lengths[16] = {};
   bool pooled = false;  // arena from the stream-ordered pool (device encoder)
+  cudaStream_t home = nullptr;      // pooled: the stream it was allocated (and is freed) on
+  cudaEvent_t last_use = nullptr;   // pooled: recorded after every launch that reads it
 };
+
+// A launch on `st` reads t: a pooled arena is freed stream-ordered after it.
+void note_use(const ecf8_dev_tensor* t, cudaStream_t st) {
+  if (!t || !t->pooled) return;
+  auto* m = const_cast<ecf8_dev_tensor*>(t);
+  if (!m->last_use) cu(cudaEventCreateWithFlags(&m->last_use, cudaEventDisableTiming), "event");
+  cu(cudaEventRecord(m->last_use, st), "record");
+}
 
 void free_arena(ecf8_dev_tensor* t) {
   if (!t->arena) return;
   if (t->pooled) {
-    cudaDeviceSynchronize();  // like cudaFree: no launch on any stream may still read it
-    cudaFreeAsync(t->arena, nullptr);  // back to the pool (kept mapped)
-  } else
+    // stream-ordered: back to the pool once the last launch reading it (on
+    // any stream) and the work on its own stream are done -- no device-wide
+    // sync (which would also break a CUDA graph capture elsewhere)
+    if (t->last_use) cudaStreamWaitEvent(t->home, t->last_use, 0);
+    cudaFreeAsync(t->arena, t->home);
+    if (t->last_use) cudaEventDestroy(t->last_use);
+    t->last_use = nullptr;
+  } else {
     cudaFree(t->arena);
+  }
   t->arena = nullptr;
 }
 
@@ -216,6 +232,7 @@ struct ecf8_fused {
 };
 
 struct ecf8_batch {
+  std::vector<const ecf8_dev_tensor*> pooled;  // members whose arenas are freed stream-ordered
   std::vector<TensorDesc*> d_descs;  // one device array per kwin group
   std::vector<int> counts;
   std::vector<int> kwins;
@@ -254,6 +271,7 @@ void alloc_arena(ecf8_dev_tensor* t, const ecf8_sections* s, std::uint64_t nb, c
     (void)keep;
     cu(cudaMallocAsync(&t->arena, total, st), "cudaMallocAsync(tensor)");
     t->pooled = true;
+    t->home = st;
   } else {
     cu(cudaMalloc(&t->arena, total), "cudaMalloc(tensor)");
   }
@@ -390,6 +408,9 @@ HostCtx& host_ctx() {
     cu(cudaStreamCreateWithFlags(&c.s_out, cudaStreamNonBlocking), "stream");
     if (const char* e = std::getenv("ECF8_CHUNK_M")) c.elem_chunk = std::min<std::uint64_t>(std::atoi(e), 128) << 20;
     if (const char* e = std::getenv("ECF8_CHUNK_MIN_M")) c.elem_min = std::min<std::uint64_t>(std::atoi(e), 16) << 20;
+    // a chunk is >= one tile and the ramp never exceeds the slot size
+    c.elem_chunk = std::max<std::uint64_t>(c.elem_chunk, ecf8::dev::kTileElemsMax);
+    c.elem_min = std::clamp<std::uint64_t>(c.elem_min, ecf8::dev::kTileElemsMax, c.elem_chunk);
     const std::uint64_t S = HostCtx::kSlack;
     c.enc_chunk = std::max(HostCtx::kEncChunk, c.elem_chunk / 2);
     const std::uint64_t b_enc = align_up(c.enc_chunk + ecf8::dev::kTileBytesMax + S, 256);
@@ -500,7 +521,7 @@ int host_pipeline(const ecf8_sections* const* ss, const std::uint64_t* nbs, std:
         hi = nh;
       }
       (void)tile_enc;
-      target *= 2;
+      target = std::min(2 * target, c.elem_chunk);  // ramp up (saturating)
       remaining -= s->outpos[hi] - s->outpos[lo];
       HostCtx::Slot& sl = c.slot[k % HostCtx::kSlots];
       if (sl.used) cu(cudaStreamWaitEvent(c.s_in, sl.out_done, 0), "wait");
@@ -819,7 +840,9 @@ int ecf8_decode_device(const ecf8_dev_tensor* t, uint8_t* d_out, void* stream) {
     d.out = d_out;
     d.out_offset = 0;
     d.tile_begin = 0;
-    return launch_one(d, static_cast<cudaStream_t>(stream), tensor_variant(t));
+    const int rc = launch_one(d, static_cast<cudaStream_t>(stream), tensor_variant(t));
+    note_use(t, static_cast<cudaStream_t>(stream));
+    return rc;
   });
 }
 
@@ -829,6 +852,8 @@ int ecf8_batch_create(const ecf8_dev_tensor* const* ts, uint8_t* const* d_outs, 
     if (!out || (count > 0 && (!ts || !d_outs))) return fail(ECF8_EINVAL, "null argument");
     *out = nullptr;
     auto b = std::make_unique<ecf8_batch>();
+    for (int i = 0; i < count; ++i)
+      if (ts[i] && ts[i]->pooled) b->pooled.push_back(ts[i]);
     for (int kw = 0; kw < 6; ++kw) {  // one launch per kernel variant present (ids 0..5)
       std::vector<TensorDesc> group;
       std::uint64_t tiles = 0;
@@ -872,6 +897,7 @@ int ecf8_batch_decode(const ecf8_batch* b, void* stream) {
       a.total_tiles = b->tiles[g];
       cu(ecf8::dev::launch_decode(a, b->kwins[g], static_cast<cudaStream_t>(stream)), "decode launch");
     }
+    for (const ecf8_dev_tensor* t : b->pooled) note_use(t, static_cast<cudaStream_t>(stream));
     return ECF8_OK;
   });
 }
@@ -1072,6 +1098,7 @@ int ecf8_fused_gemm(const ecf8_fused* f, const uint8_t* d_x, uint32_t m, float s
     a.w_fmt = f->w_fmt;
     a.scale = scale;
     cu(ecf8::dev::launch_fused_gemm(a, f->n_cta[pi], st), "fused GEMM launch");
+    note_use(f->w, st);
     return ECF8_OK;
   });
 }
