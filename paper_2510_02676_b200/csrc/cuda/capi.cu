@@ -185,6 +185,8 @@ struct ecf8_dev_tensor {
   std::uint64_t n_vtiles = 0;      // 256-window verification tiles (tile_ok bits)
   std::uint32_t* ok_bits = nullptr;  // their bitmap in the arena
   std::uint8_t* endgap = nullptr;    // per-window end nibbles (verify_gaps_kernel)
+  std::uint32_t* direct_bits = nullptr;  // tile_direct bitmap
+  std::uint16_t* lane_start = nullptr;   // per 8-window group output offsets
   TensorDesc desc{};     // out / tile fields filled per launch
   std::uint64_t encoded_len = 0, gaps_len = 0, n_outpos = 0, packed_len = 0;
   std::uint8_t lengths[16] = {};
@@ -253,8 +255,11 @@ void alloc_arena(ecf8_dev_tensor* t, const ecf8_sections* s, std::uint64_t nb, c
   const std::uint64_t off_pak = align_up(off_pos + 8 * s->n_outpos, 256);
   const std::uint64_t n_vtiles = (nb * s->threads_per_block + 255) / 256;
   const std::uint64_t off_ok = align_up(off_pak + s->packed_len + P, 256);
-  const std::uint64_t off_eg = align_up(off_ok + 4 * ((n_vtiles + 31) / 32), 256);
-  const std::uint64_t total = align_up(off_eg + (nb * s->threads_per_block + 1) / 2 + P, 256);
+  const std::uint64_t n_win = nb * s->threads_per_block;
+  const std::uint64_t off_dir = align_up(off_ok + 4 * ((n_vtiles + 31) / 32), 256);
+  const std::uint64_t off_eg = align_up(off_dir + 4 * ((n_vtiles + 31) / 32), 256);
+  const std::uint64_t off_ls = align_up(off_eg + (n_win + 1) / 2 + P, 256);
+  const std::uint64_t total = align_up(off_ls + 2 * ((n_win + 7) / 8) + P, 256);
   if (pooled) {
     // stream-ordered pool (the device encoder: many tensors created and
     // dropped in a row; cudaMalloc/cudaFree cost ~1 ms each at 50 MB)
@@ -281,6 +286,8 @@ void alloc_arena(ecf8_dev_tensor* t, const ecf8_sections* s, std::uint64_t nb, c
   t->n_vtiles = n_vtiles;
   t->ok_bits = reinterpret_cast<std::uint32_t*>(base + off_ok);
   t->endgap = base + off_eg;
+  t->direct_bits = reinterpret_cast<std::uint32_t*>(base + off_dir);
+  t->lane_start = reinterpret_cast<std::uint16_t*>(base + off_ls);
   t->encoded_len = s->encoded_len;
   t->gaps_len = s->gaps_len;
   t->n_outpos = s->n_outpos;
@@ -338,9 +345,15 @@ void verify_into(ecf8_dev_tensor* t, cudaStream_t st) {
   if (off || (vid != 4 && vid != 5)) return;
   std::uint32_t* const ok = t->ok_bits;
   cu(cudaMemsetAsync(ok, 0xFF, 4 * ((t->n_vtiles + 31) / 32), st), "memset(tile_ok)");
-  cu(ecf8::dev::launch_verify_gaps(t->desc, ok, t->endgap, st), "verify launch");
+  cu(cudaMemsetAsync(t->direct_bits, 0xFF, 4 * ((t->n_vtiles + 31) / 32), st), "memset(tile_direct)");
+  cu(ecf8::dev::launch_verify_gaps(t->desc, t->n_blocks, ok, t->endgap, t->lane_start, t->direct_bits, st),
+     "verify launch");
   t->desc.tile_ok = ok;
   t->desc.endgap = t->endgap;
+  if (vid == 4) {
+    t->desc.lane_start = t->lane_start;
+    t->desc.tile_direct = t->direct_bits;
+  }
 }
 
 // Single-descriptor launch: the descriptor rides in the kernel parameters.
@@ -384,6 +397,8 @@ struct HostCtx {
     std::uint8_t *enc, *pak, *out;
     std::uint8_t* eg;     // the chunk's window ends (verify_gaps_kernel)
     std::uint32_t* ok;    // and its tile_ok words
+    std::uint32_t* dir;   // tile_direct words
+    std::uint16_t* ls;    // 8-window group offsets
     cudaEvent_t in, run, out_done;
     bool used;
   } slot[kSlots]{};
@@ -418,9 +433,10 @@ HostCtx& host_ctx() {
     const std::uint64_t b_out = align_up(c.elem_chunk + 2 * ecf8::dev::kTileElemsMax + S, 256);
     const std::uint64_t b_eg = align_up(b_enc / 16 + S, 256);              // a nibble per 8-byte window
     const std::uint64_t b_ok = align_up(4 * (b_enc / 8 / 8192 + 2), 256);  // a bit per 256 windows (+ a straddled word)
+    const std::uint64_t b_ls = align_up(2 * (b_enc / 64 + 1) + S, 256);    // a u16 per 8 windows
     for (auto& sl : c.slot) {
       void* p = nullptr;
-      const std::uint64_t all = b_enc + b_pak + b_out + b_eg + b_ok;
+      const std::uint64_t all = b_enc + b_pak + b_out + b_eg + 2 * b_ok + b_ls;
       cu(cudaMalloc(&p, all), "cudaMalloc(staging)");
       cu(cudaMemset(p, 0, all), "cudaMemset(staging)");
       auto* base = static_cast<std::uint8_t*>(p);
@@ -429,6 +445,8 @@ HostCtx& host_ctx() {
       sl.out = base + b_enc + b_pak;
       sl.eg = base + b_enc + b_pak + b_out;
       sl.ok = reinterpret_cast<std::uint32_t*>(base + b_enc + b_pak + b_out + b_eg);
+      sl.dir = reinterpret_cast<std::uint32_t*>(base + b_enc + b_pak + b_out + b_eg + b_ok);
+      sl.ls = reinterpret_cast<std::uint16_t*>(base + b_enc + b_pak + b_out + b_eg + 2 * b_ok);
       cu(cudaEventCreateWithFlags(&sl.in, cudaEventDisableTiming), "event");
       cu(cudaEventCreateWithFlags(&sl.run, cudaEventDisableTiming), "event");
       cu(cudaEventCreateWithFlags(&sl.out_done, cudaEventDisableTiming), "event");
@@ -547,9 +565,14 @@ int host_pipeline(const ecf8_sections* const* ss, const std::uint64_t* nbs, std:
         const std::uint64_t w0 = lo * T;
         dk.endgap = rebase(sl.eg, w0 >> 1);
         dk.tile_ok = rebase(sl.ok, 4 * (w0 >> 13));
-        cu(cudaMemsetAsync(sl.ok, 0xFF, 4 * (((hi * T) >> 13) - (w0 >> 13) + 1), c.s_run), "memset(tile_ok)");
-        cu(ecf8::dev::launch_verify_gaps(dk, const_cast<std::uint32_t*>(dk.tile_ok),
-                                         const_cast<std::uint8_t*>(dk.endgap), c.s_run),
+        dk.tile_direct = rebase(sl.dir, 4 * (w0 >> 13));
+        dk.lane_start = rebase(sl.ls, 2 * (w0 >> 3));
+        const std::uint64_t words = ((hi * T) >> 13) - (w0 >> 13) + 1;
+        cu(cudaMemsetAsync(sl.ok, 0xFF, 4 * words, c.s_run), "memset(tile_ok)");
+        cu(cudaMemsetAsync(sl.dir, 0xFF, 4 * words, c.s_run), "memset(tile_direct)");
+        cu(ecf8::dev::launch_verify_gaps(dk, nbs[i], const_cast<std::uint32_t*>(dk.tile_ok),
+                                         const_cast<std::uint8_t*>(dk.endgap), const_cast<std::uint16_t*>(dk.lane_start),
+                                         const_cast<std::uint32_t*>(dk.tile_direct), c.s_run),
            "verify launch");
       }
       if (!skip_kernel)

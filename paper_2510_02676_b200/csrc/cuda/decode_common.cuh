@@ -444,16 +444,18 @@ __device__ __forceinline__ void decode_windows_fsm(const std::uint32_t* w, std::
 // code word at or after bit 64, relative to the window (codec.cpp:143-160 --
 // the walk takes the words that start in [gap, 64)).  For a stream written
 // by the encoder this is 64 + the next window's gap (codec.cpp:49-98).
+// *count (optional): the words the walk takes (count_phase, codec.cpp:133-161).
 template <class TV>
 __device__ __forceinline__ std::uint32_t window_end(std::uint32_t w0, std::uint32_t w1, std::uint32_t w2,
                                                     std::uint32_t w3, std::uint32_t gap, const TV& tb,
-                                                    std::uint32_t len_off) {
+                                                    std::uint32_t len_off, std::uint32_t* count = nullptr) {
   std::uint32_t hi = __funnelshift_l(w1, w0, gap);
   std::uint32_t lo = __funnelshift_l(w2, w1, gap);
-  std::uint32_t p = gap;
+  std::uint32_t p = gap, n4 = 0;
   while (p < 32) {
     std::uint32_t e = tb.fast(hi >> kFastShift);
     if (e & kSlowFlag) e = slow_entry(hi, tb, len_off);
+    n4 += entry_n4(e);
     hi = __funnelshift_l(lo, hi, e);
     lo = __funnelshift_l(0u, lo, e);
     p += e & 31;
@@ -467,9 +469,12 @@ __device__ __forceinline__ std::uint32_t window_end(std::uint32_t w0, std::uint3
     if (!fast_hit) e = slow_entry(hi, tb, len_off);
     const std::uint32_t b = e & 31, r = 64 - p;
     if (b >= r) {  // r <= 16 here
-      const std::uint32_t m = (fast_hit ? tb.smask(idx) : 1u) >> r;
+      const std::uint32_t st = fast_hit ? tb.smask(idx) : 1u;
+      if (count) *count = (n4 >> 2) + __popc(st & ((1u << r) - 1));
+      const std::uint32_t m = st >> r;
       return m ? 64 + __ffs(m) - 1 : p + b;
     }
+    n4 += entry_n4(e);
     hi = __funnelshift_l(lo, hi, e);
     lo = __funnelshift_l(0u, lo, e);
     p += b;

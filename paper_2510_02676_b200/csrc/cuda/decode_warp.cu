@@ -31,7 +31,6 @@
 #include <cstddef>
 #include <cstdint>
 #include <cstdlib>
-#include <type_traits>
 
 #include "decode.cuh"
 #include "decode_common.cuh"
@@ -107,28 +106,33 @@ struct GlobalOut {
   __device__ __forceinline__ void done() const {}
 };
 
-// One tile: decode + scan, compact, write back.  WIDE (1-bit codes, or a
-// code without a byte-step decoder): one 8-window walk per lane with the
-// staged fast / cascade tables; otherwise two interleaved 4-window byte-step
-// chains per lane (warp_decode_scan2).
+// One tile: decode + scan, compact, write back.
 template <bool WIDE, class WSm>
-__device__ __forceinline__ void warp_tile(const TensorDesc& d, const std::conditional_t<WIDE, WarpIn, WarpIn2>& in,
-                                          std::uint32_t log2T, std::uint32_t len_off, WSm& ws, int lane) {
+__device__ __forceinline__ void warp_tile(const TensorDesc& d, const WarpIn& in, std::uint32_t log2T,
+                                          std::uint32_t len_off, WSm& ws, int lane) {
   // slots interleaved word by word (word j of lane L at slot[32 j + L]): the
   // lanes' slot stores and reads hit 32 different banks
   const std::uint32_t slot = smem_addr(ws.slot + lane);
-  GlobalOut out{d.out + ((in.A & ~std::uint64_t{15}) - d.out_offset)};
+  LaneRun run;
   if constexpr (WIDE) {
-    const LaneRun run = warp_decode_scan<kLaneWin, 128, true>(in, log2T, len_off, SmemTables{g_tb}, slot, lane,
-                                                              tile_verified(d, in, log2T));
-    compact_write<kWbUnroll>(d, in.A, in.E, run, ws, lane, out);
-  } else {
-    const std::uint64_t w0 = in.b0 << log2T;
-    const std::uint32_t v0 = static_cast<std::uint32_t>(w0 >> 8), v1 = static_cast<std::uint32_t>((w0 + in.nwin - 1) >> 8);
-    const bool verified = ((in.ok_a >> (v0 & 31)) & (in.ok_b >> (v1 & 31)) & 1u) != 0;
-    const LaneRun2 run = warp_decode_scan2<128>(in, log2T, slot, lane, verified);
-    compact_write2<kWbUnroll>(d, in.A, in.E, run, ws, lane, out);
+    run = warp_decode_scan<kLaneWin, 128, true>(in, log2T, len_off, SmemTables{g_tb}, slot, lane,
+                                                tile_verified(d, in, log2T));
+  } else if (d.fsm && d.endgap) {  // byte steps: whole lanes on verified tiles, else window by window
+    const bool verified = tile_verified(d, in, log2T);
+    const std::uint32_t v = static_cast<std::uint32_t>((in.b0 << log2T) >> 8);  // the tile's verification tile
+    if ((in.dir >> (v & 31)) & 1u) {  // every lane's output offset known: decode in place
+      GlobalOut out{d.out + ((in.A & ~std::uint64_t{15}) - d.out_offset)};
+      direct_tile<kWbUnroll>(d, in, ws, lane, out, verified);
+      return;
+    }
+    run = warp_decode_scan<kLaneWin, 128, false, GlobalTables, true>(in, log2T, len_off, GlobalTables{d}, slot, lane,
+                                                                     verified);
+  } else {  // an incomplete code (no encoder writes one): the reference walk per window, tables through L1
+    run = warp_decode_scan<kLaneWin, 128, false, GlobalTables, false>(in, log2T, len_off, GlobalTables{d}, slot, lane,
+                                                                      false);
   }
+  GlobalOut out{d.out + ((in.A & ~std::uint64_t{15}) - d.out_offset)};
+  compact_write<kWbUnroll>(d, in.A, in.E, run, ws, lane, out);
 }
 
 template <int NW, bool WIDE>
@@ -186,16 +190,11 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_warp_kernel(const LaunchArg
     // tile seg + w, then takes the next unclaimed one), so the warps of a
     // segment finish within one tile of each other whatever the per-tile
     // cost.  The next tile is claimed and its inputs loaded one tile ahead.
-    using In = std::conditional_t<WIDE, WarpIn, WarpIn2>;
-    auto load = [&](std::uint64_t t, In& in) {
-      if constexpr (WIDE) load_warp_tile(d, t, log2T, lane, in);
-      else load_warp_tile2(d, t, log2T, lane, in);
-    };
-    In nxt;
+    WarpIn nxt;
     std::uint64_t tile = seg + warp;
-    if (tile < seg_end) load(tile, nxt);
+    if (tile < seg_end) load_warp_tile<kLaneWin, !WIDE>(d, tile, log2T, lane, nxt);
     while (tile < seg_end) {
-      const In cur = nxt;
+      const WarpIn cur = nxt;
 #ifndef ECF8_NO_PK_PREFETCH
       if (lane == 0) {  // sign/mantissa bytes of this tile -> L2 (one bulk TMA prefetch)
         const std::uint64_t p0 = (cur.A >> 1) & ~std::uint64_t{15};
@@ -207,7 +206,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_warp_kernel(const LaunchArg
       unsigned claim = 0;
       if (lane == 0) claim = atomicAdd(&next_tile, 1u);
       const std::uint64_t next = seg + __shfl_sync(0xffffffffu, claim, 0);
-      if (next < seg_end) load(next, nxt);
+      if (next < seg_end) load_warp_tile<kLaneWin, !WIDE>(d, next, log2T, lane, nxt);
       warp_tile<WIDE>(d, cur, log2T, len_off, ws, lane);
       tile = next;
     }
@@ -248,27 +247,34 @@ cudaError_t launch_nw(const LaunchArgs& args, cudaStream_t s) {
   return cudaLaunchKernelEx(&cfg, decode_warp_kernel<NW, WIDE>, args);
 }
 
-// One thread per window: its reference walk's end (window_end, codec.cpp:
-// 143-160) -> endgap nibble; a window inside an 8-window group that does not
-// end where the next window's gap says clears its 256-window tile's bit.
+// One CTA iteration per 256-window tile, one thread per window: the
+// reference walk of the window (window_end, codec.cpp:143-160) gives its end
+// nibble (endgap) and its word count.  A window inside an 8-window group that
+// does not end where the next window's gap says clears its tile's tile_ok
+// bit.  The counts are summed per group and scanned per block (lane_start);
+// a block that decodes to more words than its outpos range (not the tensor's
+// last block) clears tile_direct.
 __global__ void __launch_bounds__(256) verify_gaps_kernel(const TensorDesc d, std::uint64_t w_begin,
-                                                          std::uint64_t n_win, std::uint32_t* tile_ok,
-                                                          std::uint8_t* endgap) {
+                                                          std::uint64_t n_win, std::uint64_t nb_total,
+                                                          std::uint32_t* tile_ok, std::uint8_t* endgap,
+                                                          std::uint16_t* lane_start, std::uint32_t* tile_direct) {
   __shared__ Tables tb;
+  __shared__ std::uint32_t gsum[32];
+  __shared__ unsigned over;
   stage_tables(d, tb, threadIdx.x, blockDim.x);
   __syncthreads();
   const std::uint32_t len_off = (d.n_luts - 1) << 8;
-  const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
-  // windows [w_begin, n_win) (w_begin a multiple of 256: whole tiles)
-  for (std::uint64_t k = w_begin + blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
-       k - threadIdx.x % 32 < n_win; k += stride) {
+  const std::uint32_t log2T = 31 - __clz(d.T);
+  const std::uint64_t n_tiles = (n_win - w_begin + 255) / 256;  // w_begin: a multiple of 256
+  for (std::uint64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    const std::uint64_t w_tile = w_begin + 256 * t, k = w_tile + threadIdx.x;
     bool bad = false;
-    std::uint32_t eg = 0;
+    std::uint32_t eg = 0, cnt = 0;
     if (k < n_win) {
       const uint2 a = __ldg(reinterpret_cast<const uint2*>(d.encoded + 8 * k));
       const uint2 b = __ldg(reinterpret_cast<const uint2*>(d.encoded + 8 * k + 8));
       const std::uint32_t g0 = (d.gaps[k >> 1] >> ((k & 1) ? 0 : 4)) & 15u;
-      eg = window_end(bswap32(a.x), bswap32(a.y), bswap32(b.x), bswap32(b.y), g0, SmemTables{tb}, len_off) - 64;
+      eg = window_end(bswap32(a.x), bswap32(a.y), bswap32(b.x), bswap32(b.y), g0, SmemTables{tb}, len_off, &cnt) - 64;
       if ((k & 7) != 7 && k + 1 < n_win) {
         const std::uint32_t g1 = (d.gaps[(k + 1) >> 1] >> (((k + 1) & 1) ? 0 : 4)) & 15u;
         bad = eg != g1;
@@ -280,6 +286,40 @@ __global__ void __launch_bounds__(256) verify_gaps_kernel(const TensorDesc d, st
     if (__ballot_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) {
       const std::uint64_t v = k >> 8;
       atomicAnd(tile_ok + (v >> 5), ~(1u << (v & 31)));
+    }
+    if (lane_start) {
+      std::uint32_t g = cnt;  // the 8-window group's words
+      g += __shfl_xor_sync(0xffffffffu, g, 1);
+      g += __shfl_xor_sync(0xffffffffu, g, 2);
+      g += __shfl_xor_sync(0xffffffffu, g, 4);
+      if ((threadIdx.x & 7) == 0) gsum[threadIdx.x >> 3] = g;
+      if (threadIdx.x == 0) over = 0;
+      __syncthreads();
+      if (threadIdx.x < 32) {
+        const std::uint32_t i = threadIdx.x, v = gsum[i];
+        std::uint32_t incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const std::uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (i >= static_cast<std::uint32_t>(o)) incl += y;
+        }
+        const std::uint32_t gpb = log2T >= 8 ? 32u : (1u << (log2T - 3));  // groups per block
+        const std::uint32_t excl = incl - v - __shfl_sync(0xffffffffu, incl - v, i & ~(gpb - 1));
+        const std::uint64_t wg = w_tile + 8 * i;
+        if (wg < n_win) {
+          lane_start[wg >> 3] = static_cast<std::uint16_t>(excl);
+          if ((i & (gpb - 1)) == gpb - 1 || wg + 8 >= n_win) {  // the block's last group
+            const std::uint64_t blk = wg >> log2T;
+            if (blk + 1 < nb_total && excl + v > d.outpos[blk + 1] - d.outpos[blk]) atomicOr(&over, 1u);
+          }
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x == 0 && over) {
+        const std::uint64_t v = w_tile >> 8;
+        atomicAnd(tile_direct + (v >> 5), ~(1u << (v & 31)));
+      }
+      __syncthreads();  // gsum / over are reused by the next tile
     }
   }
 }
@@ -302,12 +342,15 @@ cudaError_t launch_decode_warp(const LaunchArgs& args, cudaStream_t s) {
 // Variant 5 (1-bit codes): 12 warps x 16.5 KB of warp state.
 cudaError_t launch_decode_warp_wide(const LaunchArgs& args, cudaStream_t s) { return launch_nw<12, true>(args, s); }
 
-cudaError_t launch_verify_gaps(const TensorDesc& d, std::uint32_t* tile_ok, std::uint8_t* endgap, cudaStream_t s) {
+cudaError_t launch_verify_gaps(const TensorDesc& d, std::uint64_t nb_total, std::uint32_t* tile_ok,
+                               std::uint8_t* endgap, std::uint16_t* lane_start, std::uint32_t* tile_direct,
+                               cudaStream_t s) {
   const std::uint64_t w_begin = d.blk_begin * d.T, n_win = d.blk_end * d.T;
   if (n_win <= w_begin) return cudaSuccess;
   const std::uint64_t blocks = (n_win - w_begin + 255) / 256;
-  verify_gaps_kernel<<<static_cast<unsigned>(blocks < 1184 ? blocks : 1184), 256, 0, s>>>(d, w_begin, n_win, tile_ok,
-                                                                                        endgap);
+  if (d.T < 8 || d.T > 256) lane_start = nullptr;  // groups of 8 windows inside one block
+  verify_gaps_kernel<<<static_cast<unsigned>(blocks < 1184 ? blocks : 1184), 256, 0, s>>>(
+      d, w_begin, n_win, nb_total, tile_ok, endgap, lane_start, tile_direct);
   // A plain launch after it: a decode launched next with programmatic
   // serialization may only overlap this empty grid, which starts after the
   // gap check has completed -- the tile bits are final before any decode reads them.

@@ -33,6 +33,8 @@ struct WarpInT {
   std::uint64_t b0;
   std::uint32_t ok_a, ok_b;  // tile_ok words of the tile's first / last window (loaded one tile ahead)
   std::uint32_t gnext;       // the lane's endgap word (gap layout) -- byte-step decoder only
+  std::uint32_t ls;          // the lane's output offset in its block (lane_start) -- byte-step decoder only
+  std::uint32_t dir;         // the tile's tile_direct word -- byte-step decoder only
 };
 using WarpIn = WarpInT<kLaneWin>;
 
@@ -68,7 +70,7 @@ __device__ __forceinline__ void load_tile_words(const TensorDesc& d, std::uint64
   }
 }
 
-template <int LW>
+template <int LW, bool NEXT = false>
 __device__ __forceinline__ void load_tile_meta(const TensorDesc& d, std::uint32_t log2T, int lane, WarpInT<LW>& in) {
   const std::uint32_t wl = static_cast<std::uint32_t>(lane) * LW;
   in.A = __ldg(d.outpos + in.b0);
@@ -84,13 +86,21 @@ __device__ __forceinline__ void load_tile_meta(const TensorDesc& d, std::uint32_
     in.ok_a = __ldg(d.tile_ok + (w0 >> 13));
     in.ok_b = __ldg(d.tile_ok + ((w0 + in.nwin - 1) >> 13));
   }
+  if constexpr (NEXT) {
+    in.ls = in.dir = 0;
+    if (d.lane_start && in.nwin) {
+      const std::uint64_t w0 = in.b0 << log2T;
+      in.dir = __ldg(d.tile_direct + (w0 >> 13));
+      if (wl < in.nwin) in.ls = __ldg(d.lane_start + (w0 >> 3) + lane);
+    }
+  }
 }
 
 template <int LW, bool NEXT = false>
 __device__ __forceinline__ void load_warp_tile(const TensorDesc& d, std::uint64_t tile, std::uint32_t log2T,
                                                int lane, WarpInT<LW>& in) {
   load_tile_words<LW, NEXT>(d, tile, log2T, lane, in);
-  load_tile_meta(d, log2T, lane, in);
+  load_tile_meta<LW, NEXT>(d, log2T, lane, in);
 }
 
 // Were the gaps of the windows of this warp tile verified (verify_gaps_kernel)?
@@ -200,101 +210,17 @@ struct WarpPipeSmem {
   alignas(16) std::uint32_t stage[STAGE_WORDS];
 };
 
-// Compact the lanes' runs (slot nibbles, LaneRun from warp_decode_scan) into
-// the staging tile, then write the tile's output elements [A, E) -- FP8
-// bytes = exponent nibble + sign/mantissa nibble (fp8.hpp:42-57) -- through
-// `out`:
-//   out.wait()               once, before the first store
-//   out.chunk(c, r)          16 bytes for elements [S0 + 16c, +16), S0 = A & ~15
-//   out.byte(i, b)           one byte for element S0 + i
-//   out.done()               after the last store
-// Full 16-element chunks go out as 16-byte stores, lane-interleaved
-// (coalesced); the ragged first and last chunks byte by byte.  The
-// sign/mantissa bytes of the full chunks come into the (then free) slots by
-// 16-byte async copies issued right after compaction: one round trip per tile
-// (the slots must hold the tile's packed bytes + 16: (8192 + 30) / 2 + 16 <=
-// 33 x 128 bytes).
+// Write the tile's output elements [A, E) from the staging tile (exponent
+// nibbles at nibble off + i for element A + i) and the packed bytes copied
+// to the slots (from the 16-byte aligned pk_a): full 16-element chunks as
+// lane-interleaved 16-byte stores, the ragged first / last chunk byte-wise.
 template <int UNROLL, class WSm, class Out>
-__device__ __forceinline__ void compact_write(const TensorDesc& d, std::uint64_t A, std::uint64_t E,
-                                              const LaneRun& run, WSm& ws, int lane, Out& out) {
-  const std::uint32_t* const my_slot = ws.slot + lane;
-  const std::uint32_t cc = run.len;
-  const std::uint32_t off = static_cast<std::uint32_t>(A & 15);  // staging nibble of element A
-  const std::uint32_t d0 = run.start + off, dend = d0 + cc;
-  const std::uint32_t data_end = off + static_cast<std::uint32_t>(E - A);
-  const std::uint64_t S0 = A - off;
+__device__ __forceinline__ void write_back(std::uint64_t S0, std::uint32_t off, std::uint32_t data_end,
+                                           std::uint64_t pk_a, const WSm& ws, int lane, Out& out) {
   const std::uint32_t nch = (data_end + 15) >> 4;
   const std::uint32_t full_lo = (off + 15) >> 4, full_hi = data_end >> 4;
   const std::uint32_t nfull = full_hi > full_lo ? full_hi - full_lo : 0u;
-  __syncwarp();  // previous tile's write-back is done with the staging and the slots' packed bytes
-
-  // ---- move my nibbles to their final place; publish partial words
-  std::uint32_t headv = 0, tailv = 0;
-  const std::uint32_t fw = d0 >> 3, lw = (dend - 1) >> 3;
-  const std::uint32_t f4 = (d0 & 7) * 4, lastn = ((dend - 1) & 7) + 1;
-  if (cc) {
-    std::uint32_t prev = my_slot[0];
-    const std::uint32_t v0 = prev << f4;
-    if (fw == lw) {
-      const std::uint32_t v = v0 & low_nibbles(lastn);
-      if (f4 == 0 && lastn == 8) ws.stage[fw] = v;
-      else headv = v;
-    } else {
-      if (f4 == 0) ws.stage[fw] = v0;
-      else headv = v0;
-      std::uint32_t j = 1;
-#pragma unroll 4
-      for (std::uint32_t k = fw + 1; k < lw; ++k, ++j) {
-        const std::uint32_t c = my_slot[32 * j];
-        ws.stage[k] = __funnelshift_l(prev, c, f4);
-        prev = c;
-      }
-      const std::uint32_t v = __funnelshift_l(prev, my_slot[32 * j], f4) & low_nibbles(lastn);
-      if (lastn == 8) ws.stage[lw] = v;
-      else tailv = v;
-    }
-  }
-  __syncwarp();
-
-  // ---- the slots are free: sign/mantissa bytes of the full chunks into them
-  // (16-byte pieces from the 16-byte aligned address at or below the first
-  // full chunk's bytes: <= 8 nfull + 16 bytes)
-  // all of the tile's packed bytes [S0 / 2, (S0 + data_end + 1) / 2), edge chunks included
-  const std::uint64_t pk_lo = (S0 >> 1) + 8 * full_lo, pk_a = (S0 >> 1) & ~std::uint64_t{15};
-  {
-    const std::uint32_t n16 = static_cast<std::uint32_t>((((S0 + data_end + 1) >> 1) - pk_a + 15) >> 4);
-    const std::uint32_t dst = smem_addr(ws.slot);
-    for (std::uint32_t i = lane; i < n16; i += 32)
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16 * i), "l"(d.packed + pk_a + 16 * i)
-                   : "memory");
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  }
-
-  // ---- owners assemble words shared between lanes: the start owner of my
-  // first word / my tail word OR in the partial head words of the following
-  // lanes until the word is covered (lane bounds and heads by shuffle; runs
-  // are contiguous, so this takes one or two steps)
-  const bool start_owner = cc && (f4 == 0 || d0 == off) && !(f4 == 0 && (fw < lw || lastn == 8));
-  const bool tail_owner = cc && fw != lw && lastn != 8;
-  std::uint32_t vs = headv, vt = tailv, cov_s = dend, cov_t = dend;
-  const std::uint32_t wend_s = min(8 * fw + 8, data_end), wend_t = min(8 * lw + 8, data_end);
-  for (std::uint32_t o = 1; o < 32; ++o) {
-    const bool need_s = start_owner && cov_s < wend_s, need_t = tail_owner && cov_t < wend_t;
-    if (!__any_sync(0xffffffffu, need_s || need_t)) break;
-    const std::uint32_t rj = __shfl_down_sync(0xffffffffu, d0, o);
-    const std::uint32_t ej = __shfl_down_sync(0xffffffffu, cc ? dend : d0, o);
-    const std::uint32_t hj = __shfl_down_sync(0xffffffffu, headv, o);
-    if (static_cast<std::uint32_t>(lane) + o < 32 && ej > rj) {
-      if (need_s) vs |= hj, cov_s = ej;
-      if (need_t) vt |= hj, cov_t = ej;
-    }
-  }
-  if (start_owner) ws.stage[fw] = vs;
-  if (tail_owner) ws.stage[lw] = vt;
-  asm volatile("cp.async.wait_all;" ::: "memory");
-  __syncwarp();
-
-  // ---- write-back
+  const std::uint64_t pk_lo = (S0 >> 1) + 8 * full_lo;
   out.wait();
   const uint2* sl = reinterpret_cast<const uint2*>(ws.stage) + full_lo + lane;
   const uint2* pl = reinterpret_cast<const uint2*>(reinterpret_cast<const std::uint8_t*>(ws.slot) + (pk_lo - pk_a)) + lane;
@@ -329,321 +255,160 @@ __device__ __forceinline__ void compact_write(const TensorDesc& d, std::uint64_t
   out.done();
 }
 
-// ---- two-chain byte-step tile (decode_warp.cu, codes with a byte-step
-// decoder).  A warp tile is still 256 windows = 256 / T reference blocks, but
-// lane L decodes two 4-window groups, [4L, 4L + 4) (chain A) and
-// [128 + 4L, 128 + 4L + 4) (chain B), interleaved: two independent table-
-// probe chains per lane hide the shared-memory latency of the byte steps.
-// The warp's 64 runs are the tile's 4-window groups in order: A-runs 0..31
-// cover windows [0, 128), B-runs [128, 256).
-
-struct WarpIn2 {
-  uint4 a01, a23;            // chain A: windows 4L .. 4L+3 (little-endian words)
-  uint2 a4;                  //          + the next 8 bytes (lookahead)
-  uint4 b01, b23;            // chain B: windows 128 + 4L ..
-  uint2 b4;
-  std::uint32_t gaps;        // A's 4 gap nibbles (gap layout) | B's << 16
-  std::uint32_t ends;        // their endgap nibbles, likewise
-  std::uint64_t A, E;        // tile output range
-  std::uint64_t oA0, oA1;    // chain A's reference block range
-  std::uint64_t oB0, oB1;    // chain B's
-  std::uint32_t nblk, nwin;
-  std::uint64_t b0;
-  std::uint32_t ok_a, ok_b;  // tile_ok words of the tile's first / last window
-};
-
-__device__ __forceinline__ void load_warp_tile2(const TensorDesc& d, std::uint64_t tile, std::uint32_t log2T, int lane,
-                                                WarpIn2& in) {
-  const std::uint32_t m = 256u >> log2T;  // blocks per tile
-  in.b0 = d.blk_begin + (tile - d.tile_begin) * m;
-  in.nblk = static_cast<std::uint32_t>(d.blk_end - in.b0 < m ? d.blk_end - in.b0 : m);
-  in.nwin = in.nblk << log2T;
-  const std::uint64_t w0g = in.b0 << log2T;
-  const std::uint32_t wa = 4u * lane, wb = 128u + 4u * lane;
-  in.gaps = in.ends = 0;
-  if (wa < in.nwin) {
-    const uint4* src = reinterpret_cast<const uint4*>(d.encoded + 8 * (w0g + wa));
-    in.a01 = __ldg(src);
-    in.a23 = __ldg(src + 1);
-    in.a4 = __ldg(reinterpret_cast<const uint2*>(src + 2));
-    in.gaps = __ldg(reinterpret_cast<const std::uint16_t*>(d.gaps + (w0g >> 1)) + lane);
-    in.ends = __ldg(reinterpret_cast<const std::uint16_t*>(d.endgap + (w0g >> 1)) + lane);
-  }
-  if (wb < in.nwin) {
-    const uint4* src = reinterpret_cast<const uint4*>(d.encoded + 8 * (w0g + wb));
-    in.b01 = __ldg(src);
-    in.b23 = __ldg(src + 1);
-    in.b4 = __ldg(reinterpret_cast<const uint2*>(src + 2));
-    in.gaps |= static_cast<std::uint32_t>(__ldg(reinterpret_cast<const std::uint16_t*>(d.gaps + (w0g >> 1)) + 32 + lane))
-               << 16;
-    in.ends |= static_cast<std::uint32_t>(__ldg(reinterpret_cast<const std::uint16_t*>(d.endgap + (w0g >> 1)) + 32 + lane))
-               << 16;
-  }
-  in.A = __ldg(d.outpos + in.b0);
-  in.E = __ldg(d.outpos + in.b0 + in.nblk);
-  // the chains' blocks (lanes past the tile's windows read the last block's: unused)
-  const std::uint32_t ba = min(wa >> log2T, in.nblk - 1), bb = min(wb >> log2T, in.nblk - 1);
-  in.oA0 = __ldg(d.outpos + in.b0 + ba);
-  in.oA1 = __ldg(d.outpos + in.b0 + ba + 1);
-  in.oB0 = __ldg(d.outpos + in.b0 + bb);
-  in.oB1 = __ldg(d.outpos + in.b0 + bb + 1);
-  in.ok_a = in.ok_b = 0;
-  if (d.tile_ok && in.nwin) {
-    in.ok_a = __ldg(d.tile_ok + (w0g >> 13));
-    in.ok_b = __ldg(d.tile_ok + ((w0g + in.nwin - 1) >> 13));
-  }
-}
-
-// Both chains' 4-window groups from gap0 to the last window's recorded end,
-// byte steps interleaved (decode_windows_fsm, two at a time).
-template <int WS>
-__device__ __forceinline__ void decode_two_fsm(const std::uint32_t (&wa)[10], std::uint32_t ga, std::uint32_t ea,
-                                               PairSink<WS>& sa, const std::uint32_t (&wb)[10], std::uint32_t gb,
-                                               std::uint32_t eb, PairSink<WS>& sb) {
-  constexpr int NB = 32, NS = 9;
-  std::uint32_t sta[NS], stb[NS];
-#pragma unroll
-  for (int i = 0; i < NS; ++i) {
-    sta[i] = __funnelshift_l(wa[i + 1], wa[i], ga);
-    stb[i] = __funnelshift_l(wb[i + 1], wb[i], gb);
-  }
-  const std::uint32_t LA = 256u + ea - ga, LB = 256u + eb - gb;
-  const std::uint32_t BA = LA >> 3, rA = (1u << (LA & 7)) - 1, BB = LB >> 3, rB = (1u << (LB & 7)) - 1;
-  std::uint32_t xa = 0, xb = 0;
-#pragma unroll
-  for (int j = 0; j < NB - 2; j += 2) {
-    const std::uint32_t a1 = fsm_entry(fsm_index(sta[j >> 2], xa, j));
-    const std::uint32_t b1 = fsm_entry(fsm_index(stb[j >> 2], xb, j));
-    const std::uint32_t a2 = fsm_entry(fsm_index(sta[(j + 1) >> 2], a1, j + 1));
-    const std::uint32_t b2 = fsm_entry(fsm_index(stb[(j + 1) >> 2], b1, j + 1));
-    sa.put2(a1, a2);
-    sb.put2(b1, b2);
-    xa = a2;
-    xb = b2;
-  }
-  auto clip = [](std::uint32_t ej, std::uint32_t idx, int j, std::uint32_t Bp, std::uint32_t rmask) {
-    const std::uint32_t lm = static_cast<std::uint32_t>(j) == Bp ? rmask : 0u;
-    const std::uint32_t kept4 = 4u * __popc(fsm_cm(idx) & lm);
-    const std::uint32_t clipped = (ej & ((0x10000u << kept4) - 0x10000u)) | kept4;
-    return static_cast<std::uint32_t>(j) < Bp ? ej : clipped;
-  };
-#pragma unroll
-  for (int j = NB - 2; j < NB + 2; j += 2) {
-    const std::uint32_t ia1 = fsm_index(sta[j >> 2], xa, j), ib1 = fsm_index(stb[j >> 2], xb, j);
-    const std::uint32_t a1 = clip(fsm_entry(ia1), ia1, j, BA, rA), b1 = clip(fsm_entry(ib1), ib1, j, BB, rB);
-    const std::uint32_t ia2 = fsm_index(sta[(j + 1) >> 2], a1, j + 1), ib2 = fsm_index(stb[(j + 1) >> 2], b1, j + 1);
-    const std::uint32_t a2 = clip(fsm_entry(ia2), ia2, j + 1, BA, rA), b2 = clip(fsm_entry(ib2), ib2, j + 1, BB, rB);
-    sa.put2(a1, a2);
-    sb.put2(b1, b2);
-    xa = a2;
-    xb = b2;
-  }
-}
-
-struct LaneRun2 {
-  std::uint32_t startA, lenA;  // chain A's output run, relative to the tile's first element
-  std::uint32_t startB, lenB;
-};
-
-// Decode both chains into the lane's slot (A at rows 0.., B at rows 16..),
-// then scan the 64 run lengths (packed A | B << 16, segmented by reference
-// block) and clamp to the block limits -- codec.cpp:212-253 per warp.
-template <int WS>
-__device__ __forceinline__ LaneRun2 warp_decode_scan2(const WarpIn2& in, std::uint32_t log2T, std::uint32_t slot_base,
-                                                      int lane, bool verified) {
-  const bool actA = 4u * lane < in.nwin, actB = 128u + 4u * lane < in.nwin;
-  PairSink<WS> sa{slot_base}, sb{slot_base + 16 * WS};
-  std::uint32_t wa[10], wb[10];
-  wa[0] = bswap32(in.a01.x), wa[1] = bswap32(in.a01.y), wa[2] = bswap32(in.a01.z), wa[3] = bswap32(in.a01.w);
-  wa[4] = bswap32(in.a23.x), wa[5] = bswap32(in.a23.y), wa[6] = bswap32(in.a23.z), wa[7] = bswap32(in.a23.w);
-  wa[8] = bswap32(in.a4.x), wa[9] = bswap32(in.a4.y);
-  wb[0] = bswap32(in.b01.x), wb[1] = bswap32(in.b01.y), wb[2] = bswap32(in.b01.z), wb[3] = bswap32(in.b01.w);
-  wb[4] = bswap32(in.b23.x), wb[5] = bswap32(in.b23.y), wb[6] = bswap32(in.b23.z), wb[7] = bswap32(in.b23.w);
-  wb[8] = bswap32(in.b4.x), wb[9] = bswap32(in.b4.y);
-  if (verified) {
-    // inactive chains (past the tile's windows) decode harmlessly: counts are discarded
-    decode_two_fsm<WS>(wa, (in.gaps >> 4) & 15u, (in.ends >> 8) & 15u, sa, wb, (in.gaps >> 20) & 15u,
-                       (in.ends >> 24) & 15u, sb);
-  } else {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int sh = 8 * (i >> 1) + ((i & 1) ? 0 : 4);  // window 2j: high nibble of byte j
-      if (actA) decode_windows_fsm<1, WS>(wa + 2 * i, (in.gaps >> sh) & 15u, (in.ends >> sh) & 15u, sa);
-      if (actB) decode_windows_fsm<1, WS>(wb + 2 * i, (in.gaps >> (16 + sh)) & 15u, (in.ends >> (16 + sh)) & 15u, sb);
-    }
-  }
-  const std::uint32_t cA = actA ? sa.finish(slot_base) : 0u;
-  const std::uint32_t cB = actB ? sb.finish(slot_base + 16 * WS) : 0u;
-
-  const std::uint32_t x = cA | (cB << 16);
-  std::uint32_t incl = x;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const std::uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += y;
-  }
-  const std::uint32_t excl = incl - x;
-  // 4-window runs per block: T / 4 lanes' A-runs (and as many B-runs); T = 256:
-  // one block, its B-runs after all A-runs
-  const std::uint32_t lpb_mask = log2T >= 7 ? 31u : (1u << (log2T - 2)) - 1;
-  const std::uint32_t rel = excl - __shfl_sync(0xffffffffu, excl, static_cast<std::uint32_t>(lane) & ~lpb_mask);
-  const std::uint32_t totA = log2T == 8 ? (__shfl_sync(0xffffffffu, incl, 31) & 0xFFFFu) : 0u;
-  LaneRun2 r;
-  r.startA = static_cast<std::uint32_t>(in.oA0 - in.A) + (rel & 0xFFFFu);
-  r.startB = static_cast<std::uint32_t>(in.oB0 - in.A) + (rel >> 16) + totA;
-  const std::uint32_t limA = static_cast<std::uint32_t>(in.oA1 - in.A), limB = static_cast<std::uint32_t>(in.oB1 - in.A);
-  r.lenA = (actA && r.startA < limA) ? min(cA, limA - r.startA) : 0u;
-  r.lenB = (actB && r.startB < limB) ? min(cB, limB - r.startB) : 0u;
-  return r;
-}
-
-// One run's nibbles from the lane's slot words (src, stride 32 words) to
-// their final place in the staging tile: full words stored, the partial
-// first / last words returned (head / tail) for the owners to assemble.
-struct RunMove {
-  std::uint32_t d0, dend, fw, lw, f4, lastn, headv, tailv;
-  bool start_owner, tail_owner;
-};
-
+// The tile's packed sign/mantissa bytes [S0 / 2, (S0 + data_end + 1) / 2) into
+// the slots by 16-byte async copies from the 16-byte aligned address pk_a
+// (the slots must hold the tile's packed bytes + 16: (8192 + 30) / 2 + 16 <=
+// 33 x 128 bytes).  Returns pk_a.
 template <class WSm>
-__device__ __forceinline__ RunMove move_run(const std::uint32_t* src, std::uint32_t d0, std::uint32_t cc,
-                                            std::uint32_t off, WSm& ws) {
-  RunMove m;
-  m.d0 = d0;
-  m.dend = d0 + cc;
-  m.fw = d0 >> 3;
-  m.lw = (m.dend - 1) >> 3;
-  m.f4 = (d0 & 7) * 4;
-  m.lastn = ((m.dend - 1) & 7) + 1;
-  m.headv = m.tailv = 0;
+__device__ __forceinline__ std::uint64_t fetch_packed(const TensorDesc& d, std::uint64_t S0, std::uint32_t data_end,
+                                                      WSm& ws, int lane) {
+  const std::uint64_t pk_a = (S0 >> 1) & ~std::uint64_t{15};
+  const std::uint32_t n16 = static_cast<std::uint32_t>((((S0 + data_end + 1) >> 1) - pk_a + 15) >> 4);
+  const std::uint32_t dst = smem_addr(ws.slot);
+  for (std::uint32_t i = lane; i < n16; i += 32)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16 * i), "l"(d.packed + pk_a + 16 * i)
+                 : "memory");
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  return pk_a;
+}
+
+// Compact the lanes' runs (slot nibbles, LaneRun from warp_decode_scan) into
+// the staging tile, then write the tile's output elements [A, E) -- FP8
+// bytes = exponent nibble + sign/mantissa nibble (fp8.hpp:42-57) -- through
+// `out`:
+//   out.wait()               once, before the first store
+//   out.chunk(c, r)          16 bytes for elements [S0 + 16c, +16), S0 = A & ~15
+//   out.byte(i, b)           one byte for element S0 + i
+//   out.done()               after the last store
+// Full 16-element chunks go out as 16-byte stores, lane-interleaved
+// (coalesced); the ragged first and last chunks byte by byte.  The
+// sign/mantissa bytes of the full chunks come into the (then free) slots by
+// 16-byte async copies issued right after compaction: one round trip per tile
+// (the slots must hold the tile's packed bytes + 16: (8192 + 30) / 2 + 16 <=
+// 33 x 128 bytes).
+template <int UNROLL, class WSm, class Out>
+__device__ __forceinline__ void compact_write(const TensorDesc& d, std::uint64_t A, std::uint64_t E,
+                                              const LaneRun& run, WSm& ws, int lane, Out& out) {
+  const std::uint32_t* const my_slot = ws.slot + lane;
+  const std::uint32_t cc = run.len;
+  const std::uint32_t off = static_cast<std::uint32_t>(A & 15);  // staging nibble of element A
+  const std::uint32_t d0 = run.start + off, dend = d0 + cc;
+  const std::uint32_t data_end = off + static_cast<std::uint32_t>(E - A);
+  const std::uint64_t S0 = A - off;
+  __syncwarp();  // previous tile's write-back is done with the staging and the slots' packed bytes
+
+  // ---- move my nibbles to their final place; publish partial words
+  std::uint32_t headv = 0, tailv = 0;
+  const std::uint32_t fw = d0 >> 3, lw = (dend - 1) >> 3;
+  const std::uint32_t f4 = (d0 & 7) * 4, lastn = ((dend - 1) & 7) + 1;
   if (cc) {
-    std::uint32_t prev = src[0];
-    const std::uint32_t v0 = prev << m.f4;
-    if (m.fw == m.lw) {
-      const std::uint32_t v = v0 & low_nibbles(m.lastn);
-      if (m.f4 == 0 && m.lastn == 8) ws.stage[m.fw] = v;
-      else m.headv = v;
+    std::uint32_t prev = my_slot[0];
+    const std::uint32_t v0 = prev << f4;
+    if (fw == lw) {
+      const std::uint32_t v = v0 & low_nibbles(lastn);
+      if (f4 == 0 && lastn == 8) ws.stage[fw] = v;
+      else headv = v;
     } else {
-      if (m.f4 == 0) ws.stage[m.fw] = v0;
-      else m.headv = v0;
+      if (f4 == 0) ws.stage[fw] = v0;
+      else headv = v0;
       std::uint32_t j = 1;
 #pragma unroll 4
-      for (std::uint32_t k = m.fw + 1; k < m.lw; ++k, ++j) {
-        const std::uint32_t c = src[32 * j];
-        ws.stage[k] = __funnelshift_l(prev, c, m.f4);
+      for (std::uint32_t k = fw + 1; k < lw; ++k, ++j) {
+        const std::uint32_t c = my_slot[32 * j];
+        ws.stage[k] = __funnelshift_l(prev, c, f4);
         prev = c;
       }
-      const std::uint32_t v = __funnelshift_l(prev, src[32 * j], m.f4) & low_nibbles(m.lastn);
-      if (m.lastn == 8) ws.stage[m.lw] = v;
-      else m.tailv = v;
+      const std::uint32_t v = __funnelshift_l(prev, my_slot[32 * j], f4) & low_nibbles(lastn);
+      if (lastn == 8) ws.stage[lw] = v;
+      else tailv = v;
     }
   }
-  m.start_owner = cc && (m.f4 == 0 || d0 == off) && !(m.f4 == 0 && (m.fw < m.lw || m.lastn == 8));
-  m.tail_owner = cc && m.fw != m.lw && m.lastn != 8;
-  return m;
-}
+  __syncwarp();
 
-// Owners complete the partial words shared by consecutive runs (one run per
-// lane, in lane order): the start owner of a word / a tail owner ORs in the
-// head words of the following runs until the word is covered.  rmw: the
-// start owner's word already holds nibbles of the runs before this set
-// (written by the previous set's owners).
-// set_end: where the set's runs end (words are covered up to there).
-template <class WSm>
-__device__ __forceinline__ void assemble_owners(const RunMove& m, std::uint32_t cc, std::uint32_t set_end, int lane,
-                                                WSm& ws, bool rmw) {
-  const bool start_owner = m.start_owner || rmw;
-  std::uint32_t vs = m.headv, vt = m.tailv, cov_s = m.dend, cov_t = m.dend;
-  const std::uint32_t wend_s = min(8 * m.fw + 8, set_end), wend_t = min(8 * m.lw + 8, set_end);
+  // ---- the slots are free: sign/mantissa bytes of the full chunks into them
+  // (16-byte pieces from the 16-byte aligned address at or below the first
+  // full chunk's bytes: <= 8 nfull + 16 bytes)
+  // all of the tile's packed bytes [S0 / 2, (S0 + data_end + 1) / 2), edge chunks included
+  const std::uint64_t pk_a = fetch_packed(d, S0, data_end, ws, lane);
+
+  // ---- owners assemble words shared between lanes: the start owner of my
+  // first word / my tail word OR in the partial head words of the following
+  // lanes until the word is covered (lane bounds and heads by shuffle; runs
+  // are contiguous, so this takes one or two steps)
+  const bool start_owner = cc && (f4 == 0 || d0 == off) && !(f4 == 0 && (fw < lw || lastn == 8));
+  const bool tail_owner = cc && fw != lw && lastn != 8;
+  std::uint32_t vs = headv, vt = tailv, cov_s = dend, cov_t = dend;
+  const std::uint32_t wend_s = min(8 * fw + 8, data_end), wend_t = min(8 * lw + 8, data_end);
   for (std::uint32_t o = 1; o < 32; ++o) {
-    const bool need_s = start_owner && cov_s < wend_s, need_t = m.tail_owner && cov_t < wend_t;
+    const bool need_s = start_owner && cov_s < wend_s, need_t = tail_owner && cov_t < wend_t;
     if (!__any_sync(0xffffffffu, need_s || need_t)) break;
-    const std::uint32_t rj = __shfl_down_sync(0xffffffffu, m.d0, o);
-    const std::uint32_t ej = __shfl_down_sync(0xffffffffu, cc ? m.dend : m.d0, o);
-    const std::uint32_t hj = __shfl_down_sync(0xffffffffu, m.headv, o);
+    const std::uint32_t rj = __shfl_down_sync(0xffffffffu, d0, o);
+    const std::uint32_t ej = __shfl_down_sync(0xffffffffu, cc ? dend : d0, o);
+    const std::uint32_t hj = __shfl_down_sync(0xffffffffu, headv, o);
     if (static_cast<std::uint32_t>(lane) + o < 32 && ej > rj) {
       if (need_s) vs |= hj, cov_s = ej;
       if (need_t) vt |= hj, cov_t = ej;
     }
   }
-  if (rmw) vs |= ws.stage[m.fw];
-  if (start_owner) ws.stage[m.fw] = vs;
-  if (m.tail_owner) ws.stage[m.lw] = vt;
-}
-
-// compact_write for the two-chain tile: A-runs (lanes' chain A, tile windows
-// [0, 128)) then B-runs ([128, 256)), each set compacted and assembled like
-// the one-run tile; the word joining the last A-run and the first B-run is
-// completed by the first non-empty B-run (read-modify-write).  Then the same
-// packed-byte copy and write-back as compact_write.
-template <int UNROLL, class WSm, class Out>
-__device__ __forceinline__ void compact_write2(const TensorDesc& d, std::uint64_t A, std::uint64_t E,
-                                               const LaneRun2& run, WSm& ws, int lane, Out& out) {
-  const std::uint32_t off = static_cast<std::uint32_t>(A & 15);  // staging nibble of element A
-  const std::uint32_t data_end = off + static_cast<std::uint32_t>(E - A);
-  const std::uint64_t S0 = A - off;
-  const std::uint32_t nch = (data_end + 15) >> 4;
-  const std::uint32_t full_lo = (off + 15) >> 4, full_hi = data_end >> 4;
-  const std::uint32_t nfull = full_hi > full_lo ? full_hi - full_lo : 0u;
-  __syncwarp();  // previous tile's write-back is done with the staging and the slots' packed bytes
-
-  const RunMove ma = move_run(ws.slot + lane, run.startA + off, run.lenA, off, ws);
-  const RunMove mb = move_run(ws.slot + 16 * 32 + lane, run.startB + off, run.lenB, off, ws);
-  __syncwarp();
-
-  // ---- the slots are free: the tile's packed bytes into them (compact_write)
-  const std::uint64_t pk_lo = (S0 >> 1) + 8 * full_lo, pk_a = (S0 >> 1) & ~std::uint64_t{15};
-  {
-    const std::uint32_t n16 = static_cast<std::uint32_t>((((S0 + data_end + 1) >> 1) - pk_a + 15) >> 4);
-    const std::uint32_t dst = smem_addr(ws.slot);
-    for (std::uint32_t i = lane; i < n16; i += 32)
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16 * i), "l"(d.packed + pk_a + 16 * i)
-                   : "memory");
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  }
-
-  const std::uint32_t endA = __reduce_max_sync(0xffffffffu, run.lenA ? ma.dend : 0u);  // A-runs end, B-runs start
-  assemble_owners(ma, run.lenA, endA, lane, ws, false);
-  __syncwarp();
-  // the first non-empty B-run completes the word it shares with the A-runs
-  const unsigned nzb = __ballot_sync(0xffffffffu, run.lenB != 0);
-  const bool anyA = __any_sync(0xffffffffu, run.lenA != 0);
-  const bool rmw = anyA && nzb && lane == __ffs(nzb) - 1 && mb.f4 != 0;
-  assemble_owners(mb, run.lenB, data_end, lane, ws, rmw);
+  if (start_owner) ws.stage[fw] = vs;
+  if (tail_owner) ws.stage[lw] = vt;
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncwarp();
 
-  // ---- write-back (as compact_write)
-  out.wait();
-  const uint2* sl = reinterpret_cast<const uint2*>(ws.stage) + full_lo + lane;
-  const uint2* pl = reinterpret_cast<const uint2*>(reinterpret_cast<const std::uint8_t*>(ws.slot) + (pk_lo - pk_a)) + lane;
-  std::uint32_t k = lane;
-  for (; k + 32 * (UNROLL - 1) < nfull; k += 32 * UNROLL, sl += 32 * UNROLL, pl += 32 * UNROLL) {
+  // ---- write-back
+  write_back<UNROLL>(S0, off, data_end, pk_a, ws, lane, out);
+}
+
+// ---- direct tile (byte-step decoder, tile_direct set): every lane's output
+// offset is known before decoding (lane_start, from the upload check), so
+// the byte steps append straight into the zeroed staging tile at the lane's
+// final place -- no slot, no scan, no compaction.  Full words are plain
+// stores (each belongs to one lane); a lane's partial last word is OR-ed in
+// after all lanes' first words (which may share it) have been stored.  The
+// tile's packed bytes stream into the slots while the lanes decode.
+template <int UNROLL, class WSm, class Out>
+__device__ __forceinline__ void direct_tile(const TensorDesc& d, const WarpInT<8>& in, WSm& ws, int lane, Out& out,
+                                            bool verified) {
+  const std::uint32_t off = static_cast<std::uint32_t>(in.A & 15);  // staging nibble of element A
+  const std::uint32_t data_end = off + static_cast<std::uint32_t>(in.E - in.A);
+  const std::uint64_t S0 = in.A - off;
+  __syncwarp();  // previous tile's write-back is done with the staging and the slots' packed bytes
+  {
+    const std::uint32_t st = smem_addr(ws.stage);
+    constexpr std::uint32_t n16 = sizeof(ws.stage) / 16;
+    for (std::uint32_t i = lane; i < n16; i += 32)
+      asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(st + 16 * i), "r"(0u) : "memory");
+  }
+  const std::uint64_t pk_a = fetch_packed(d, S0, data_end, ws, lane);
+  __syncwarp();  // the zeroes are in place
+  std::uint32_t tail_addr = 0, tail = 0;
+  if (static_cast<std::uint32_t>(lane) * kLaneWin < in.nwin) {
+    const std::uint32_t d0 = static_cast<std::uint32_t>(in.o0 - in.A) + in.ls + off;  // my first element's nibble
+    PairSink<4> sink{smem_addr(ws.stage) + 4 * (d0 >> 3)};
+    sink.q4 = 4 * (d0 & 7);
+    std::uint32_t w[18];
+    w[0] = bswap32(in.w01.x), w[1] = bswap32(in.w01.y), w[2] = bswap32(in.w01.z), w[3] = bswap32(in.w01.w);
+    w[4] = bswap32(in.w23.x), w[5] = bswap32(in.w23.y), w[6] = bswap32(in.w23.z), w[7] = bswap32(in.w23.w);
+    w[8] = bswap32(in.w45.x), w[9] = bswap32(in.w45.y), w[10] = bswap32(in.w45.z), w[11] = bswap32(in.w45.w);
+    w[12] = bswap32(in.w67.x), w[13] = bswap32(in.w67.y), w[14] = bswap32(in.w67.z), w[15] = bswap32(in.w67.w);
+    w[16] = bswap32(in.w8.x), w[17] = bswap32(in.w8.y);
+    if (verified) {
+      decode_windows_fsm<8, 4>(w, (in.gaps >> 4) & 15u, (in.gnext >> 24) & 15u, sink);
+    } else {
 #pragma unroll
-    for (int u = 0; u < UNROLL; ++u) {
-      const uint2 s = sl[32 * u], q = pl[32 * u];
-      uint4 r;
-      merge8(s.x, q.x, r.x, r.y);
-      merge8(s.y, q.y, r.z, r.w);
-      out.chunk(full_lo + k + 32 * u, r);
+      for (int i = 0; i < 8; ++i) {
+        const int sh = 8 * (i >> 1) + ((i & 1) ? 0 : 4);  // window 2j: high nibble of byte j
+        decode_windows_fsm<1, 4>(w + 2 * i, (in.gaps >> sh) & 15u, (in.gnext >> sh) & 15u, sink);
+      }
     }
+    tail_addr = sink.addr;
+    tail = (sink.q4 & 31u) ? sink.lo : 0u;
   }
-  for (; k < nfull; k += 32, sl += 32, pl += 32) {
-    const uint2 s = *sl, q = *pl;
-    uint4 r;
-    merge8(s.x, q.x, r.x, r.y);
-    merge8(s.y, q.y, r.z, r.w);
-    out.chunk(full_lo + k, r);
-  }
-  const std::uint32_t i = lane < 16 ? static_cast<std::uint32_t>(lane) : 16 * (nch - 1) + (lane - 16);
-  const bool edge = lane < 16 ? (full_lo > 0 && i >= off && i < data_end)
-                              : (full_hi < nch && !(nch == 1 && full_lo > 0) && i < data_end);
-  if (edge) {
-    const std::uint32_t x = (ws.stage[i >> 3] >> (4 * (i & 7))) & 15u;
-    const std::uint8_t* const pks = reinterpret_cast<const std::uint8_t*>(ws.slot) + ((S0 >> 1) - pk_a);
-    out.byte(i, merge1(x, pks[i >> 1], i & 1));
-  }
-  out.done();
+  __syncwarp();  // every full word and every lane's first word is stored
+  if (tail) asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(tail_addr), "r"(tail) : "memory");
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncwarp();
+  write_back<UNROLL>(S0, off, data_end, pk_a, ws, lane, out);
 }
 
 }  // namespace ecf8::dev
