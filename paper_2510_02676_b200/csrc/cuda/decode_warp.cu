@@ -106,6 +106,26 @@ struct GlobalOut {
   __device__ __forceinline__ void done() const {}
 };
 
+// A warp tile's input sections -> L2 (bulk prefetches, lane 0): its
+// windows, gap and end nibbles, group offsets and block offsets.  The packed
+// bytes are fetched by the tile itself (cp.async during the decode).
+__device__ __forceinline__ void prefetch_l2(const void* p, std::uint64_t bytes) {
+  const std::uintptr_t a = reinterpret_cast<std::uintptr_t>(p) & ~std::uintptr_t{15};
+  const std::uint32_t n = static_cast<std::uint32_t>((reinterpret_cast<std::uintptr_t>(p) + bytes - a + 15) & ~std::uint64_t{15});
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(n) : "memory");
+}
+__device__ __forceinline__ void prefetch_tile_l2(const TensorDesc& d, std::uint64_t tile, std::uint32_t log2T) {
+  const std::uint32_t m = 256u >> log2T;
+  const std::uint64_t b0 = d.blk_begin + (tile - d.tile_begin) * m;
+  const std::uint64_t nb = d.blk_end - b0 < m ? d.blk_end - b0 : m;
+  const std::uint64_t w0 = b0 << log2T, nw = nb << log2T;
+  prefetch_l2(d.encoded + 8 * w0, 8 * nw + 8);
+  prefetch_l2(d.gaps + (w0 >> 1), nw >> 1);
+  prefetch_l2(d.outpos + b0, 8 * (nb + 1));
+  if (d.endgap) prefetch_l2(d.endgap + (w0 >> 1), nw >> 1);
+  if (d.lane_start) prefetch_l2(d.lane_start + (w0 >> 3), nw >> 2);
+}
+
 // One tile: decode + scan, compact, write back.
 template <bool WIDE, class WSm>
 __device__ __forceinline__ void warp_tile(const TensorDesc& d, const WarpIn& in, std::uint32_t log2T,
@@ -189,26 +209,43 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_warp_kernel(const LaunchArg
     // Tiles are handed out dynamically inside the CTA (warp w starts with
     // tile seg + w, then takes the next unclaimed one), so the warps of a
     // segment finish within one tile of each other whatever the per-tile
-    // cost.  The next tile is claimed and its inputs loaded one tile ahead.
-    WarpIn nxt;
+    // cost.  WIDE: the next tile is claimed and its inputs loaded into
+    // registers one tile ahead.  Byte-step variant: the registers go to the
+    // two decode paths instead; the next tile's inputs are prefetched into L2
+    // (bulk prefetches, one tile ahead) and loaded at the tile's start.
     std::uint64_t tile = seg + warp;
-    if (tile < seg_end) load_warp_tile<kLaneWin, !WIDE>(d, tile, log2T, lane, nxt);
-    while (tile < seg_end) {
-      const WarpIn cur = nxt;
-#ifndef ECF8_NO_PK_PREFETCH
-      if (lane == 0) {  // sign/mantissa bytes of this tile -> L2 (one bulk TMA prefetch)
-        const std::uint64_t p0 = (cur.A >> 1) & ~std::uint64_t{15};
-        const std::uint32_t bytes = static_cast<std::uint32_t>((((cur.E + 1) >> 1) - p0 + 15) & ~std::uint64_t{15});
-        if (bytes)
-          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(d.packed + p0), "r"(bytes) : "memory");
+    if constexpr (WIDE) {
+      WarpIn nxt;
+      if (tile < seg_end) load_warp_tile(d, tile, log2T, lane, nxt);
+      while (tile < seg_end) {
+        const WarpIn cur = nxt;
+        if (lane == 0) {  // sign/mantissa bytes of this tile -> L2 (one bulk TMA prefetch)
+          const std::uint64_t p0 = (cur.A >> 1) & ~std::uint64_t{15};
+          const std::uint32_t bytes = static_cast<std::uint32_t>((((cur.E + 1) >> 1) - p0 + 15) & ~std::uint64_t{15});
+          if (bytes)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(d.packed + p0), "r"(bytes) : "memory");
+        }
+        unsigned claim = 0;
+        if (lane == 0) claim = atomicAdd(&next_tile, 1u);
+        const std::uint64_t next = seg + __shfl_sync(0xffffffffu, claim, 0);
+        if (next < seg_end) load_warp_tile(d, next, log2T, lane, nxt);
+        warp_tile<WIDE>(d, cur, log2T, len_off, ws, lane);
+        tile = next;
       }
-#endif
-      unsigned claim = 0;
-      if (lane == 0) claim = atomicAdd(&next_tile, 1u);
-      const std::uint64_t next = seg + __shfl_sync(0xffffffffu, claim, 0);
-      if (next < seg_end) load_warp_tile<kLaneWin, !WIDE>(d, next, log2T, lane, nxt);
-      warp_tile<WIDE>(d, cur, log2T, len_off, ws, lane);
-      tile = next;
+    } else {
+      if (tile < seg_end && lane == 0) prefetch_tile_l2(d, tile, log2T);
+      while (tile < seg_end) {
+        WarpIn cur;
+        load_warp_tile<kLaneWin, true>(d, tile, log2T, lane, cur);
+        unsigned claim = 0;
+        if (lane == 0) {
+          claim = atomicAdd(&next_tile, 1u);
+          if (seg + claim < seg_end) prefetch_tile_l2(d, seg + claim, log2T);
+        }
+        const std::uint64_t next = seg + __shfl_sync(0xffffffffu, claim, 0);
+        warp_tile<WIDE>(d, cur, log2T, len_off, ws, lane);
+        tile = next;
+      }
     }
     seg = seg_end;
   }
