@@ -186,7 +186,7 @@ struct ecf8_dev_tensor {
   std::uint32_t* ok_bits = nullptr;  // their bitmap in the arena
   std::uint8_t* endgap = nullptr;    // per-window end nibbles (verify_gaps_kernel)
   std::uint32_t* direct_bits = nullptr;  // tile_direct bitmap
-  std::uint16_t* lane_start = nullptr;   // per 8-window group output offsets
+  std::uint16_t* lane_start = nullptr;   // per 4-window group output offsets
   TensorDesc desc{};     // out / tile fields filled per launch
   std::uint64_t encoded_len = 0, gaps_len = 0, n_outpos = 0, packed_len = 0;
   std::uint8_t lengths[16] = {};
@@ -259,7 +259,7 @@ void alloc_arena(ecf8_dev_tensor* t, const ecf8_sections* s, std::uint64_t nb, c
   const std::uint64_t off_dir = align_up(off_ok + 4 * ((n_vtiles + 31) / 32), 256);
   const std::uint64_t off_eg = align_up(off_dir + 4 * ((n_vtiles + 31) / 32), 256);
   const std::uint64_t off_ls = align_up(off_eg + (n_win + 1) / 2 + P, 256);
-  const std::uint64_t total = align_up(off_ls + 2 * ((n_win + 7) / 8) + P, 256);
+  const std::uint64_t total = align_up(off_ls + 2 * ((n_win + 3) / 4) + P, 256);
   if (pooled) {
     // stream-ordered pool (the device encoder: many tensors created and
     // dropped in a row; cudaMalloc/cudaFree cost ~1 ms each at 50 MB)
@@ -398,7 +398,7 @@ struct HostCtx {
     std::uint8_t* eg;     // the chunk's window ends (verify_gaps_kernel)
     std::uint32_t* ok;    // and its tile_ok words
     std::uint32_t* dir;   // tile_direct words
-    std::uint16_t* ls;    // 8-window group offsets
+    std::uint16_t* ls;    // 4-window group offsets
     cudaEvent_t in, run, out_done;
     bool used;
   } slot[kSlots]{};
@@ -433,7 +433,7 @@ HostCtx& host_ctx() {
     const std::uint64_t b_out = align_up(c.elem_chunk + 2 * ecf8::dev::kTileElemsMax + S, 256);
     const std::uint64_t b_eg = align_up(b_enc / 16 + S, 256);              // a nibble per 8-byte window
     const std::uint64_t b_ok = align_up(4 * (b_enc / 8 / 8192 + 2), 256);  // a bit per 256 windows (+ a straddled word)
-    const std::uint64_t b_ls = align_up(2 * (b_enc / 64 + 1) + S, 256);    // a u16 per 8 windows
+    const std::uint64_t b_ls = align_up(2 * (b_enc / 32 + 1) + S, 256);    // a u16 per 4 windows
     for (auto& sl : c.slot) {
       void* p = nullptr;
       const std::uint64_t all = b_enc + b_pak + b_out + b_eg + 2 * b_ok + b_ls;
@@ -566,7 +566,7 @@ int host_pipeline(const ecf8_sections* const* ss, const std::uint64_t* nbs, std:
         dk.endgap = rebase(sl.eg, w0 >> 1);
         dk.tile_ok = rebase(sl.ok, 4 * (w0 >> 13));
         dk.tile_direct = rebase(sl.dir, 4 * (w0 >> 13));
-        dk.lane_start = rebase(sl.ls, 2 * (w0 >> 3));
+        dk.lane_start = rebase(sl.ls, 2 * (w0 >> 2));
         const std::uint64_t words = ((hi * T) >> 13) - (w0 >> 13) + 1;
         cu(cudaMemsetAsync(sl.ok, 0xFF, 4 * words, c.s_run), "memset(tile_ok)");
         cu(cudaMemsetAsync(sl.dir, 0xFF, 4 * words, c.s_run), "memset(tile_direct)");

@@ -22,7 +22,7 @@ struct TensorDesc {
   const std::uint32_t* fsm;      // tables.hpp byte-step decoder (nullptr: the code has none)
   const std::uint8_t* fsm_cm;    // its completion masks
   const std::uint8_t* endgap;    // per window, gap layout: where its reference walk stops, minus 64 (upload check)
-  const std::uint16_t* lane_start;   // per 8-window group: first output element, relative to its block's outpos
+  const std::uint16_t* lane_start;   // per 4-window group: first output element, relative to its block's outpos
   const std::uint32_t* tile_direct;  // bit v: tile v's blocks (but the tensor's last) decode to exactly their ranges
   std::uint8_t* out;             // element i lands at out[i - out_offset]
   std::uint64_t out_offset;      // multiple of 16
@@ -103,9 +103,9 @@ cudaError_t launch_decode(const LaunchArgs& args, int variant, cudaStream_t stre
 // end nibble (window_end - 64, endgap) and clears bit v of tile_ok (pre-set
 // to all ones) unless every window w in [256v, 256v + 256) that is not the
 // last of an 8-window group (w % 8 != 7) ends where window w + 1's gap says.
-// Also (T in [8, 256]): every 8-window group's output offset within its
+// Also (T in [8, 256]): every 4-window group's output offset within its
 // block (lane_start: the reference's per-block scan, codec.cpp:227-237,
-// taken per group of 8 windows), and tile_direct bit v cleared unless every
+// taken per group of 4 windows), and tile_direct bit v cleared unless every
 // block of tile v except the tensor's last (nb_total - 1) decodes to no more
 // symbols than its outpos range.
 cudaError_t launch_verify_gaps(const TensorDesc& d, std::uint64_t nb_total, std::uint32_t* tile_ok,

@@ -440,6 +440,53 @@ __device__ __forceinline__ void decode_windows_fsm(const std::uint32_t* w, std::
   }
 }
 
+// Two independent runs of decode_windows_fsm (NWIN windows each: words wa /
+// wb, start gaps, recorded ends, sinks), their byte steps interleaved so
+// both table-probe chains are in flight at once.
+template <int NWIN = 4, int WS = 4>
+__device__ __forceinline__ void decode_two_fsm(const std::uint32_t* wa, std::uint32_t ga, std::uint32_t ea,
+                                               PairSink<WS>& sa, const std::uint32_t* wb, std::uint32_t gb,
+                                               std::uint32_t eb, PairSink<WS>& sb) {
+  constexpr int NB = 8 * NWIN, NS = 2 * NWIN + 1;
+  std::uint32_t sta[NS], stb[NS];
+#pragma unroll
+  for (int i = 0; i < NS; ++i) {
+    sta[i] = __funnelshift_l(wa[i + 1], wa[i], ga);
+    stb[i] = __funnelshift_l(wb[i + 1], wb[i], gb);
+  }
+  const std::uint32_t LA = 64u * NWIN + ea - ga, LB = 64u * NWIN + eb - gb;
+  const std::uint32_t BA = LA >> 3, rA = (1u << (LA & 7)) - 1, BB = LB >> 3, rB = (1u << (LB & 7)) - 1;
+  std::uint32_t xa = 0, xb = 0;
+#pragma unroll
+  for (int j = 0; j < NB - 2; j += 2) {
+    const std::uint32_t a1 = fsm_entry(fsm_index(sta[j >> 2], xa, j));
+    const std::uint32_t b1 = fsm_entry(fsm_index(stb[j >> 2], xb, j));
+    const std::uint32_t a2 = fsm_entry(fsm_index(sta[(j + 1) >> 2], a1, j + 1));
+    const std::uint32_t b2 = fsm_entry(fsm_index(stb[(j + 1) >> 2], b1, j + 1));
+    sa.put2(a1, a2);
+    sb.put2(b1, b2);
+    xa = a2;
+    xb = b2;
+  }
+  auto clip = [](std::uint32_t ej, std::uint32_t idx, int j, std::uint32_t Bp, std::uint32_t rmask) {
+    const std::uint32_t lm = static_cast<std::uint32_t>(j) == Bp ? rmask : 0u;
+    const std::uint32_t kept4 = 4u * __popc(fsm_cm(idx) & lm);
+    const std::uint32_t clipped = (ej & ((0x10000u << kept4) - 0x10000u)) | kept4;
+    return static_cast<std::uint32_t>(j) < Bp ? ej : clipped;
+  };
+#pragma unroll
+  for (int j = NB - 2; j < NB + 2; j += 2) {
+    const std::uint32_t ia1 = fsm_index(sta[j >> 2], xa, j), ib1 = fsm_index(stb[j >> 2], xb, j);
+    const std::uint32_t a1 = clip(fsm_entry(ia1), ia1, j, BA, rA), b1 = clip(fsm_entry(ib1), ib1, j, BB, rB);
+    const std::uint32_t ia2 = fsm_index(sta[(j + 1) >> 2], a1, j + 1), ib2 = fsm_index(stb[(j + 1) >> 2], b1, j + 1);
+    const std::uint32_t a2 = clip(fsm_entry(ia2), ia2, j + 1, BA, rA), b2 = clip(fsm_entry(ib2), ib2, j + 1, BB, rB);
+    sa.put2(a1, a2);
+    sb.put2(b1, b2);
+    xa = a2;
+    xb = b2;
+  }
+}
+
 // Where window (w0..w3, gap)'s reference walk stops: the start of the first
 // code word at or after bit 64, relative to the window (codec.cpp:143-160 --
 // the walk takes the words that start in [gap, 64)).  For a stream written

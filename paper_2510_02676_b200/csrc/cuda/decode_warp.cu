@@ -123,7 +123,7 @@ __device__ __forceinline__ void prefetch_tile_l2(const TensorDesc& d, std::uint6
   prefetch_l2(d.gaps + (w0 >> 1), nw >> 1);
   prefetch_l2(d.outpos + b0, 8 * (nb + 1));
   if (d.endgap) prefetch_l2(d.endgap + (w0 >> 1), nw >> 1);
-  if (d.lane_start) prefetch_l2(d.lane_start + (w0 >> 3), nw >> 2);
+  if (d.lane_start) prefetch_l2(d.lane_start + (w0 >> 2), nw >> 1);
 }
 
 // One tile: decode + scan, compact, write back.
@@ -288,7 +288,9 @@ cudaError_t launch_nw(const LaunchArgs& args, cudaStream_t s) {
 // reference walk of the window (window_end, codec.cpp:143-160) gives its end
 // nibble (endgap) and its word count.  A window inside an 8-window group that
 // does not end where the next window's gap says clears its tile's tile_ok
-// bit.  The counts are summed per group and scanned per block (lane_start);
+// bit.  The counts are summed per 4-window group and scanned per block
+// (lane_start: one u16 per group; the two groups of an 8-window lane in one
+// 32-bit word);
 // a block that decodes to more words than its outpos range (not the tensor's
 // last block) clears tile_direct.
 __global__ void __launch_bounds__(256) verify_gaps_kernel(const TensorDesc d, std::uint64_t w_begin,
@@ -296,7 +298,7 @@ __global__ void __launch_bounds__(256) verify_gaps_kernel(const TensorDesc d, st
                                                           std::uint32_t* tile_ok, std::uint8_t* endgap,
                                                           std::uint16_t* lane_start, std::uint32_t* tile_direct) {
   __shared__ Tables tb;
-  __shared__ std::uint32_t gsum[32];
+  __shared__ std::uint32_t gsum[64];
   __shared__ unsigned over;
   stage_tables(d, tb, threadIdx.x, blockDim.x);
   __syncthreads();
@@ -325,36 +327,30 @@ __global__ void __launch_bounds__(256) verify_gaps_kernel(const TensorDesc d, st
       atomicAnd(tile_ok + (v >> 5), ~(1u << (v & 31)));
     }
     if (lane_start) {
-      std::uint32_t g = cnt;  // the 8-window group's words
+      std::uint32_t g = cnt;  // the 4-window group's words
       g += __shfl_xor_sync(0xffffffffu, g, 1);
       g += __shfl_xor_sync(0xffffffffu, g, 2);
-      g += __shfl_xor_sync(0xffffffffu, g, 4);
-      if ((threadIdx.x & 7) == 0) gsum[threadIdx.x >> 3] = g;
+      if ((threadIdx.x & 3) == 0) gsum[threadIdx.x >> 2] = g;
       if (threadIdx.x == 0) over = 0;
       __syncthreads();
-      if (threadIdx.x < 32) {
-        const std::uint32_t i = threadIdx.x, v = gsum[i];
+      if (threadIdx.x < 32) {  // lane i: groups 2i, 2i + 1 (windows 8i .. 8i + 7)
+        const std::uint32_t i = threadIdx.x, v0 = gsum[2 * i], v1 = gsum[2 * i + 1], v = v0 + v1;
         std::uint32_t incl = v;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
           const std::uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
           if (i >= static_cast<std::uint32_t>(o)) incl += y;
         }
-        const std::uint32_t gpb = log2T >= 8 ? 32u : (1u << (log2T - 3));  // groups per block
-        const std::uint32_t excl = incl - v - __shfl_sync(0xffffffffu, incl - v, i & ~(gpb - 1));
+        const std::uint32_t lpb = log2T >= 8 ? 32u : (1u << (log2T - 3));  // lanes (8 windows) per block
+        const std::uint32_t excl = incl - v - __shfl_sync(0xffffffffu, incl - v, i & ~(lpb - 1));
         const std::uint64_t wg = w_tile + 8 * i;
         if (wg < n_win) {
-          lane_start[wg >> 3] = static_cast<std::uint16_t>(excl);
-          if ((i & (gpb - 1)) == gpb - 1 || wg + 8 >= n_win) {  // the block's last group
+          reinterpret_cast<std::uint32_t*>(lane_start)[wg >> 3] = excl | ((excl + v0) << 16);
+          if ((i & (lpb - 1)) == lpb - 1 || wg + 8 >= n_win) {  // the block's last lane
             const std::uint64_t blk = wg >> log2T;
             if (blk + 1 < nb_total && excl + v > d.outpos[blk + 1] - d.outpos[blk]) atomicOr(&over, 1u);
           }
         }
-      }
-      __syncthreads();
-      if (threadIdx.x == 0 && over) {
-        const std::uint64_t v = w_tile >> 8;
-        atomicAnd(tile_direct + (v >> 5), ~(1u << (v & 31)));
       }
       __syncthreads();  // gsum / over are reused by the next tile
     }

@@ -33,7 +33,7 @@ struct WarpInT {
   std::uint64_t b0;
   std::uint32_t ok_a, ok_b;  // tile_ok words of the tile's first / last window (loaded one tile ahead)
   std::uint32_t gnext;       // the lane's endgap word (gap layout) -- byte-step decoder only
-  std::uint32_t ls;          // the lane's output offset in its block (lane_start) -- byte-step decoder only
+  std::uint32_t ls;          // its two 4-window groups' output offsets in their block (lane_start) -- byte-step only
   std::uint32_t dir;         // the tile's tile_direct word -- byte-step decoder only
 };
 using WarpIn = WarpInT<kLaneWin>;
@@ -91,7 +91,7 @@ __device__ __forceinline__ void load_tile_meta(const TensorDesc& d, std::uint32_
     if (d.lane_start && in.nwin) {
       const std::uint64_t w0 = in.b0 << log2T;
       in.dir = __ldg(d.tile_direct + (w0 >> 13));
-      if (wl < in.nwin) in.ls = __ldg(d.lane_start + (w0 >> 3) + lane);
+      if (wl < in.nwin) in.ls = __ldg(reinterpret_cast<const std::uint32_t*>(d.lane_start + (w0 >> 2)) + lane);
     }
   }
 }
@@ -362,10 +362,12 @@ __device__ __forceinline__ void compact_write(const TensorDesc& d, std::uint64_t
 // ---- direct tile (byte-step decoder, tile_direct set): every lane's output
 // offset is known before decoding (lane_start, from the upload check), so
 // the byte steps append straight into the zeroed staging tile at the lane's
-// final place -- no slot, no scan, no compaction.  Full words are plain
-// stores (each belongs to one lane); a lane's partial last word is OR-ed in
-// after all lanes' first words (which may share it) have been stored.  The
-// tile's packed bytes stream into the slots while the lanes decode.
+// final place -- no slot, no scan, no compaction.  Each lane runs two
+// independent chains (its 4-window groups, each from its own known offset),
+// interleaved: two table-probe chains in flight per lane.  Full words are
+// plain stores (each belongs to one chain); a chain's partial last word is
+// OR-ed in after every chain's first word (which may share it) is stored.
+// The tile's packed bytes stream into the slots while the lanes decode.
 template <int UNROLL, class WSm, class Out>
 __device__ __forceinline__ void direct_tile(const TensorDesc& d, const WarpInT<8>& in, WSm& ws, int lane, Out& out,
                                             bool verified) {
@@ -381,11 +383,14 @@ __device__ __forceinline__ void direct_tile(const TensorDesc& d, const WarpInT<8
   }
   const std::uint64_t pk_a = fetch_packed(d, S0, data_end, ws, lane);
   __syncwarp();  // the zeroes are in place
-  std::uint32_t tail_addr = 0, tail = 0;
+  std::uint32_t ta_addr = 0, ta = 0, tb_addr = 0, tb = 0;
   if (static_cast<std::uint32_t>(lane) * kLaneWin < in.nwin) {
-    const std::uint32_t d0 = static_cast<std::uint32_t>(in.o0 - in.A) + in.ls + off;  // my first element's nibble
-    PairSink<4> sink{smem_addr(ws.stage) + 4 * (d0 >> 3)};
-    sink.q4 = 4 * (d0 & 7);
+    // two chains: windows 0-3 and 4-7, each from its group's known offset
+    const std::uint32_t base = static_cast<std::uint32_t>(in.o0 - in.A) + off;
+    const std::uint32_t da = base + (in.ls & 0xFFFFu), db = base + (in.ls >> 16);
+    PairSink<4> sa{smem_addr(ws.stage) + 4 * (da >> 3)}, sb{smem_addr(ws.stage) + 4 * (db >> 3)};
+    sa.q4 = 4 * (da & 7);
+    sb.q4 = 4 * (db & 7);
     std::uint32_t w[18];
     w[0] = bswap32(in.w01.x), w[1] = bswap32(in.w01.y), w[2] = bswap32(in.w01.z), w[3] = bswap32(in.w01.w);
     w[4] = bswap32(in.w23.x), w[5] = bswap32(in.w23.y), w[6] = bswap32(in.w23.z), w[7] = bswap32(in.w23.w);
@@ -393,19 +398,24 @@ __device__ __forceinline__ void direct_tile(const TensorDesc& d, const WarpInT<8
     w[12] = bswap32(in.w67.x), w[13] = bswap32(in.w67.y), w[14] = bswap32(in.w67.z), w[15] = bswap32(in.w67.w);
     w[16] = bswap32(in.w8.x), w[17] = bswap32(in.w8.y);
     if (verified) {
-      decode_windows_fsm<8, 4>(w, (in.gaps >> 4) & 15u, (in.gnext >> 24) & 15u, sink);
+      decode_two_fsm(w, (in.gaps >> 4) & 15u, (in.gnext >> 8) & 15u, sa, w + 8, (in.gaps >> 20) & 15u,
+                     (in.gnext >> 24) & 15u, sb);
     } else {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
+      for (int i = 0; i < 4; ++i) {
         const int sh = 8 * (i >> 1) + ((i & 1) ? 0 : 4);  // window 2j: high nibble of byte j
-        decode_windows_fsm<1, 4>(w + 2 * i, (in.gaps >> sh) & 15u, (in.gnext >> sh) & 15u, sink);
+        decode_two_fsm<1>(w + 2 * i, (in.gaps >> sh) & 15u, (in.gnext >> sh) & 15u, sa, w + 8 + 2 * i,
+                          (in.gaps >> (16 + sh)) & 15u, (in.gnext >> (16 + sh)) & 15u, sb);
       }
     }
-    tail_addr = sink.addr;
-    tail = (sink.q4 & 31u) ? sink.lo : 0u;
+    ta_addr = sa.addr;
+    ta = (sa.q4 & 31u) ? sa.lo : 0u;
+    tb_addr = sb.addr;
+    tb = (sb.q4 & 31u) ? sb.lo : 0u;
   }
   __syncwarp();  // every full word and every lane's first word is stored
-  if (tail) asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(tail_addr), "r"(tail) : "memory");
+  if (ta) asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(ta_addr), "r"(ta) : "memory");
+  if (tb) asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(tb_addr), "r"(tb) : "memory");
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncwarp();
   write_back<UNROLL>(S0, off, data_end, pk_a, ws, lane, out);
