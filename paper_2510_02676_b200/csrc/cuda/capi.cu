@@ -231,6 +231,7 @@ struct ecf8_fused {
   std::uint64_t xt_cap = 0;
   std::uint64_t n = 0, k = 0;
   std::uint32_t w_fmt = 0;
+  bool fsm = false;  // byte-step direct decode: the code has a byte-step decoder and every tile is direct
 };
 
 struct ecf8_batch {
@@ -1075,6 +1076,16 @@ int ecf8_fused_create(const ecf8_dev_tensor* t, uint64_t n, uint64_t k, int w_fm
          "H2D plan");
     }
     f->split_k = static_cast<std::uint32_t>((f->n_cta[1] + n / 128 - 1) / (n / 128));
+    // byte-step direct decode when every verification tile is direct (the
+    // upload check's tile_direct bits) -- always, for encoder-written weights
+    static const bool no_fsm = std::getenv("ECF8_FUSED_NO_FSM") != nullptr;  // A/B runs
+    if (!no_fsm && t->desc.fsm && t->desc.lane_start && ecf8::dev::fused_lane_windows(t->T, t->desc.lmin) == 4) {
+      std::vector<std::uint32_t> bits((t->n_vtiles + 31) / 32);
+      cu(cudaMemcpy(bits.data(), t->desc.tile_direct, 4 * bits.size(), cudaMemcpyDeviceToHost), "D2H tile_direct");
+      bool all = true;
+      for (std::uint64_t v = 0; v < t->n_vtiles; ++v) all &= ((bits[v >> 5] >> (v & 31)) & 1u) != 0;
+      f->fsm = all;
+    }
     *out = f.release();
     return ECF8_OK;
   });
@@ -1111,7 +1122,9 @@ int ecf8_fused_gemm(const ecf8_fused* f, const uint8_t* d_x, uint32_t m, float s
     a.n = static_cast<std::uint32_t>(f->n);
     a.k = static_cast<std::uint32_t>(f->k);
     a.split_k = f->split_k;
-    a.stages_a = ecf8::dev::fused_stages_a(a.m_pad, ecf8::dev::fused_warp_smem(f->w->T, f->w->desc.lmin, a.m_pad));
+    a.fsm = f->fsm ? 1u : 0u;
+    a.stages_a = ecf8::dev::fused_stages_a(a.m_pad, ecf8::dev::fused_warp_smem(f->w->T, f->w->desc.lmin, a.m_pad),
+                                           f->fsm);
     a.stages_b = ecf8::dev::fused_stages_b(a.m_pad);
     if (a.stages_a < 2) return fail(ECF8_EINVAL, "fused GEMM: shared memory too small for this m");
     a.acc_cols = 32;

@@ -366,6 +366,29 @@ __device__ __forceinline__ std::uint32_t fsm_cm(std::uint32_t idx) {
   return v;
 }
 
+// Where the byte-step tables are: pinned at kFsmAt (FsmPinned, the probe
+// address in the load's immediate), or at shared addresses held in registers
+// (FsmAt: the kernels whose static shared layout is not pinned; index * 4 +
+// base is one IMAD, like index * 4).
+struct FsmPinned {
+  __device__ __forceinline__ std::uint32_t entry(std::uint32_t idx) const { return fsm_entry(idx); }
+  __device__ __forceinline__ std::uint32_t cm(std::uint32_t idx) const { return fsm_cm(idx); }
+};
+struct FsmAt {
+  std::uint32_t tab, cmb;  // shared addresses of the entries and the completion masks
+  __device__ __forceinline__ std::uint32_t entry(std::uint32_t idx) const {
+    std::uint32_t a, v;
+    asm("mad.lo.u32 %0, %1, 4, %2;" : "=r"(a) : "r"(idx), "r"(tab));
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+  }
+  __device__ __forceinline__ std::uint32_t cm(std::uint32_t idx) const {
+    std::uint16_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=h"(v) : "r"(idx + cmb));
+    return v;
+  }
+};
+
 // Nibble sink for two byte steps at once: their symbol fields (<= 4 + 4
 // symbols) are joined into one 32-bit run c, then appended at nibble q4 of
 // the partial word lo; a full word goes to the slot.  q4 adds the whole
@@ -402,9 +425,9 @@ struct PairSink {
 // for n > 1 when every inner window ends where the next one's gap says
 // (the upload check).  A complete code parses every bit string the way the
 // reference's decode_one chain does, so no fallback is needed.
-template <int NWIN, int WS>
+template <int NWIN, int WS, class FT = FsmPinned>
 __device__ __forceinline__ void decode_windows_fsm(const std::uint32_t* w, std::uint32_t gap0, std::uint32_t end,
-                                                   PairSink<WS>& sink) {
+                                                   PairSink<WS>& sink, const FT& ft = FT{}) {
   constexpr int NB = 8 * NWIN;      // bytes of the windows
   constexpr int NS = 2 * NWIN + 1;  // stream words from bit gap0: bytes 0 .. 4 NS - 1 >= NB + 2
   std::uint32_t st[NS];
@@ -416,8 +439,8 @@ __device__ __forceinline__ void decode_windows_fsm(const std::uint32_t* w, std::
   std::uint32_t e = 0;  // root
 #pragma unroll
   for (int j = 0; j < NB - 2; j += 2) {  // bytes before NB - 2 <= Bp: every word they complete is taken
-    const std::uint32_t e1 = fsm_entry(fsm_index(st[j >> 2], e, j));
-    const std::uint32_t e2 = fsm_entry(fsm_index(st[(j + 1) >> 2], e1, j + 1));
+    const std::uint32_t e1 = ft.entry(fsm_index(st[j >> 2], e, j));
+    const std::uint32_t e2 = ft.entry(fsm_index(st[(j + 1) >> 2], e1, j + 1));
     sink.put2(e1, e2);
     e = e2;
   }
@@ -425,16 +448,16 @@ __device__ __forceinline__ void decode_windows_fsm(const std::uint32_t* w, std::
   // its first r bits (they end by Lp); after Bp none
   auto clip = [&](std::uint32_t ej, std::uint32_t idx, int j) -> std::uint32_t {
     const std::uint32_t lm = static_cast<std::uint32_t>(j) == Bp ? rmask : 0u;
-    const std::uint32_t kept4 = 4u * __popc(fsm_cm(idx) & lm);
+    const std::uint32_t kept4 = 4u * __popc(ft.cm(idx) & lm);
     const std::uint32_t clipped = (ej & ((0x10000u << kept4) - 0x10000u)) | kept4;
     return static_cast<std::uint32_t>(j) < Bp ? ej : clipped;
   };
 #pragma unroll
   for (int j = NB - 2; j < NB + 2; j += 2) {
     const std::uint32_t i1 = fsm_index(st[j >> 2], e, j);
-    const std::uint32_t e1 = clip(fsm_entry(i1), i1, j);
+    const std::uint32_t e1 = clip(ft.entry(i1), i1, j);
     const std::uint32_t i2 = fsm_index(st[(j + 1) >> 2], e1, j + 1);
-    const std::uint32_t e2 = clip(fsm_entry(i2), i2, j + 1);
+    const std::uint32_t e2 = clip(ft.entry(i2), i2, j + 1);
     sink.put2(e1, e2);
     e = e2;
   }
@@ -443,10 +466,10 @@ __device__ __forceinline__ void decode_windows_fsm(const std::uint32_t* w, std::
 // Two independent runs of decode_windows_fsm (NWIN windows each: words wa /
 // wb, start gaps, recorded ends, sinks), their byte steps interleaved so
 // both table-probe chains are in flight at once.
-template <int NWIN = 4, int WS = 4>
+template <int NWIN = 4, int WS = 4, class FT = FsmPinned>
 __device__ __forceinline__ void decode_two_fsm(const std::uint32_t* wa, std::uint32_t ga, std::uint32_t ea,
                                                PairSink<WS>& sa, const std::uint32_t* wb, std::uint32_t gb,
-                                               std::uint32_t eb, PairSink<WS>& sb) {
+                                               std::uint32_t eb, PairSink<WS>& sb, const FT& ft = FT{}) {
   constexpr int NB = 8 * NWIN, NS = 2 * NWIN + 1;
   std::uint32_t sta[NS], stb[NS];
 #pragma unroll
@@ -459,27 +482,27 @@ __device__ __forceinline__ void decode_two_fsm(const std::uint32_t* wa, std::uin
   std::uint32_t xa = 0, xb = 0;
 #pragma unroll
   for (int j = 0; j < NB - 2; j += 2) {
-    const std::uint32_t a1 = fsm_entry(fsm_index(sta[j >> 2], xa, j));
-    const std::uint32_t b1 = fsm_entry(fsm_index(stb[j >> 2], xb, j));
-    const std::uint32_t a2 = fsm_entry(fsm_index(sta[(j + 1) >> 2], a1, j + 1));
-    const std::uint32_t b2 = fsm_entry(fsm_index(stb[(j + 1) >> 2], b1, j + 1));
+    const std::uint32_t a1 = ft.entry(fsm_index(sta[j >> 2], xa, j));
+    const std::uint32_t b1 = ft.entry(fsm_index(stb[j >> 2], xb, j));
+    const std::uint32_t a2 = ft.entry(fsm_index(sta[(j + 1) >> 2], a1, j + 1));
+    const std::uint32_t b2 = ft.entry(fsm_index(stb[(j + 1) >> 2], b1, j + 1));
     sa.put2(a1, a2);
     sb.put2(b1, b2);
     xa = a2;
     xb = b2;
   }
-  auto clip = [](std::uint32_t ej, std::uint32_t idx, int j, std::uint32_t Bp, std::uint32_t rmask) {
+  auto clip = [&](std::uint32_t ej, std::uint32_t idx, int j, std::uint32_t Bp, std::uint32_t rmask) {
     const std::uint32_t lm = static_cast<std::uint32_t>(j) == Bp ? rmask : 0u;
-    const std::uint32_t kept4 = 4u * __popc(fsm_cm(idx) & lm);
+    const std::uint32_t kept4 = 4u * __popc(ft.cm(idx) & lm);
     const std::uint32_t clipped = (ej & ((0x10000u << kept4) - 0x10000u)) | kept4;
     return static_cast<std::uint32_t>(j) < Bp ? ej : clipped;
   };
 #pragma unroll
   for (int j = NB - 2; j < NB + 2; j += 2) {
     const std::uint32_t ia1 = fsm_index(sta[j >> 2], xa, j), ib1 = fsm_index(stb[j >> 2], xb, j);
-    const std::uint32_t a1 = clip(fsm_entry(ia1), ia1, j, BA, rA), b1 = clip(fsm_entry(ib1), ib1, j, BB, rB);
+    const std::uint32_t a1 = clip(ft.entry(ia1), ia1, j, BA, rA), b1 = clip(ft.entry(ib1), ib1, j, BB, rB);
     const std::uint32_t ia2 = fsm_index(sta[(j + 1) >> 2], a1, j + 1), ib2 = fsm_index(stb[(j + 1) >> 2], b1, j + 1);
-    const std::uint32_t a2 = clip(fsm_entry(ia2), ia2, j + 1, BA, rA), b2 = clip(fsm_entry(ib2), ib2, j + 1, BB, rB);
+    const std::uint32_t a2 = clip(ft.entry(ia2), ia2, j + 1, BA, rA), b2 = clip(ft.entry(ib2), ib2, j + 1, BB, rB);
     sa.put2(a1, a2);
     sb.put2(b1, b2);
     xa = a2;

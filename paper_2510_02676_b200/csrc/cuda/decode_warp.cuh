@@ -91,7 +91,10 @@ __device__ __forceinline__ void load_tile_meta(const TensorDesc& d, std::uint32_
     if (d.lane_start && in.nwin) {
       const std::uint64_t w0 = in.b0 << log2T;
       in.dir = __ldg(d.tile_direct + (w0 >> 13));
-      if (wl < in.nwin) in.ls = __ldg(reinterpret_cast<const std::uint32_t*>(d.lane_start + (w0 >> 2)) + lane);
+      if (wl < in.nwin) {
+        if constexpr (LW == 8) in.ls = __ldg(reinterpret_cast<const std::uint32_t*>(d.lane_start + (w0 >> 2)) + lane);
+        else in.ls = __ldg(d.lane_start + (w0 >> 2) + lane);
+      }
     }
   }
 }
@@ -368,9 +371,9 @@ __device__ __forceinline__ void compact_write(const TensorDesc& d, std::uint64_t
 // plain stores (each belongs to one chain); a chain's partial last word is
 // OR-ed in after every chain's first word (which may share it) is stored.
 // The tile's packed bytes stream into the slots while the lanes decode.
-template <int UNROLL, class WSm, class Out>
-__device__ __forceinline__ void direct_tile(const TensorDesc& d, const WarpInT<8>& in, WSm& ws, int lane, Out& out,
-                                            bool verified) {
+template <int UNROLL, int LW, class WSm, class Out, class FT = FsmPinned>
+__device__ __forceinline__ void direct_tile(const TensorDesc& d, const WarpInT<LW>& in, WSm& ws, int lane, Out& out,
+                                            bool verified, const FT& ft = FT{}) {
   const std::uint32_t off = static_cast<std::uint32_t>(in.A & 15);  // staging nibble of element A
   const std::uint32_t data_end = off + static_cast<std::uint32_t>(in.E - in.A);
   const std::uint64_t S0 = in.A - off;
@@ -384,34 +387,54 @@ __device__ __forceinline__ void direct_tile(const TensorDesc& d, const WarpInT<8
   const std::uint64_t pk_a = fetch_packed(d, S0, data_end, ws, lane);
   __syncwarp();  // the zeroes are in place
   std::uint32_t ta_addr = 0, ta = 0, tb_addr = 0, tb = 0;
-  if (static_cast<std::uint32_t>(lane) * kLaneWin < in.nwin) {
-    // two chains: windows 0-3 and 4-7, each from its group's known offset
+  if (static_cast<std::uint32_t>(lane) * LW < in.nwin) {
     const std::uint32_t base = static_cast<std::uint32_t>(in.o0 - in.A) + off;
-    const std::uint32_t da = base + (in.ls & 0xFFFFu), db = base + (in.ls >> 16);
-    PairSink<4> sa{smem_addr(ws.stage) + 4 * (da >> 3)}, sb{smem_addr(ws.stage) + 4 * (db >> 3)};
-    sa.q4 = 4 * (da & 7);
-    sb.q4 = 4 * (db & 7);
-    std::uint32_t w[18];
+    std::uint32_t w[2 * LW + 2];
     w[0] = bswap32(in.w01.x), w[1] = bswap32(in.w01.y), w[2] = bswap32(in.w01.z), w[3] = bswap32(in.w01.w);
     w[4] = bswap32(in.w23.x), w[5] = bswap32(in.w23.y), w[6] = bswap32(in.w23.z), w[7] = bswap32(in.w23.w);
-    w[8] = bswap32(in.w45.x), w[9] = bswap32(in.w45.y), w[10] = bswap32(in.w45.z), w[11] = bswap32(in.w45.w);
-    w[12] = bswap32(in.w67.x), w[13] = bswap32(in.w67.y), w[14] = bswap32(in.w67.z), w[15] = bswap32(in.w67.w);
-    w[16] = bswap32(in.w8.x), w[17] = bswap32(in.w8.y);
-    if (verified) {
-      decode_two_fsm(w, (in.gaps >> 4) & 15u, (in.gnext >> 8) & 15u, sa, w + 8, (in.gaps >> 20) & 15u,
-                     (in.gnext >> 24) & 15u, sb);
-    } else {
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int sh = 8 * (i >> 1) + ((i & 1) ? 0 : 4);  // window 2j: high nibble of byte j
-        decode_two_fsm<1>(w + 2 * i, (in.gaps >> sh) & 15u, (in.gnext >> sh) & 15u, sa, w + 8 + 2 * i,
-                          (in.gaps >> (16 + sh)) & 15u, (in.gnext >> (16 + sh)) & 15u, sb);
-      }
+    if constexpr (LW == 8) {
+      w[8] = bswap32(in.w45.x), w[9] = bswap32(in.w45.y), w[10] = bswap32(in.w45.z), w[11] = bswap32(in.w45.w);
+      w[12] = bswap32(in.w67.x), w[13] = bswap32(in.w67.y), w[14] = bswap32(in.w67.z), w[15] = bswap32(in.w67.w);
     }
-    ta_addr = sa.addr;
-    ta = (sa.q4 & 31u) ? sa.lo : 0u;
-    tb_addr = sb.addr;
-    tb = (sb.q4 & 31u) ? sb.lo : 0u;
+    w[2 * LW] = bswap32(in.w8.x), w[2 * LW + 1] = bswap32(in.w8.y);
+    if constexpr (LW == 8) {
+      // two chains: windows 0-3 and 4-7, each from its group's known offset
+      const std::uint32_t da = base + (in.ls & 0xFFFFu), db = base + (in.ls >> 16);
+      PairSink<4> sa{smem_addr(ws.stage) + 4 * (da >> 3)}, sb{smem_addr(ws.stage) + 4 * (db >> 3)};
+      sa.q4 = 4 * (da & 7);
+      sb.q4 = 4 * (db & 7);
+      if (verified) {
+        decode_two_fsm<4, 4, FT>(w, (in.gaps >> 4) & 15u, (in.gnext >> 8) & 15u, sa, w + 8, (in.gaps >> 20) & 15u,
+                                 (in.gnext >> 24) & 15u, sb, ft);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int sh = 8 * (i >> 1) + ((i & 1) ? 0 : 4);  // window 2j: high nibble of byte j
+          decode_two_fsm<1, 4, FT>(w + 2 * i, (in.gaps >> sh) & 15u, (in.gnext >> sh) & 15u, sa, w + 8 + 2 * i,
+                                   (in.gaps >> (16 + sh)) & 15u, (in.gnext >> (16 + sh)) & 15u, sb, ft);
+        }
+      }
+      tb_addr = sb.addr;
+      tb = (sb.q4 & 31u) ? sb.lo : 0u;
+      ta_addr = sa.addr;
+      ta = (sa.q4 & 31u) ? sa.lo : 0u;
+    } else {
+      // one chain: the lane's 4-window group
+      const std::uint32_t da = base + in.ls;
+      PairSink<4> sa{smem_addr(ws.stage) + 4 * (da >> 3)};
+      sa.q4 = 4 * (da & 7);
+      if (verified) {
+        decode_windows_fsm<4, 4, FT>(w, (in.gaps >> 4) & 15u, (in.gnext >> 8) & 15u, sa, ft);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int sh = 8 * (i >> 1) + ((i & 1) ? 0 : 4);
+          decode_windows_fsm<1, 4, FT>(w + 2 * i, (in.gaps >> sh) & 15u, (in.gnext >> sh) & 15u, sa, ft);
+        }
+      }
+      ta_addr = sa.addr;
+      ta = (sa.q4 & 31u) ? sa.lo : 0u;
+    }
   }
   __syncwarp();  // every full word and every lane's first word is stored
   if (ta) asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(ta_addr), "r"(ta) : "memory");

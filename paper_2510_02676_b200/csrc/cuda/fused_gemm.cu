@@ -71,6 +71,8 @@ constexpr int decode_warps() {
 constexpr std::uint32_t kTileElems = 128 * 128;  // one K tile of A (bytes)
 
 __shared__ Tables g_tbf;
+__shared__ alignas(16) std::uint32_t g_fsmf[256 * kFsmStates];  // byte-step variant: its tables
+__shared__ alignas(16) std::uint8_t g_cmf[256 * kFsmStates];
 __shared__ TensorDesc g_wdesc;  // this CTA's weight descriptor (read where used: frees ~30 registers)
 __shared__ unsigned g_qnext;
 __shared__ alignas(8) unsigned long long g_full[kMaxStagesA];
@@ -237,20 +239,11 @@ struct RingOut {
   }
 };
 
-template <int LW, class WSm>
-__device__ __forceinline__ void ring_tile(const TensorDesc& d, const WarpInT<LW>& in, std::uint32_t log2T,
-                                          std::uint32_t len_off, WSm& ws, const Ring& R, int lane) {
-  const LaneRun run = warp_decode_scan<LW, 128>(in, log2T, len_off, SmemTables{g_tbf}, smem_addr(ws.slot + lane), lane,
-                                                tile_verified(d, in, log2T));
-  // this ECF8 tile's part of the CTA range, in ring tiles tf (and tf + 1)
-  const std::uint64_t A = in.A > R.e0 ? in.A : R.e0;
-  const std::uint64_t E = in.E < R.e1 ? in.E : R.e1;
-  if (A >= E) {
-    __syncwarp();
-    return;
-  }
+// The ring output of an ECF8 tile whose elements [tA, tE) meet the CTA range
+// (A < E after clipping).
+__device__ __forceinline__ RingOut ring_out(std::uint64_t tA, std::uint64_t A, std::uint64_t E, const Ring& R, int lane) {
   RingOut out;
-  out.S0 = in.A & ~std::uint64_t{15};
+  out.S0 = tA & ~std::uint64_t{15};
   out.e0 = R.e0;
   out.e1 = R.e1;
   out.tf = static_cast<std::uint32_t>((A - R.e0) >> 14);
@@ -273,7 +266,36 @@ __device__ __forceinline__ void ring_tile(const TensorDesc& d, const WarpInT<LW>
   out.bar_l = smem_addr(&g_full[(out.tf + 1) % R.stages]);
   out.R = &R;
   out.lane = lane;
+  return out;
+}
+
+template <int LW, class WSm>
+__device__ __forceinline__ void ring_tile(const TensorDesc& d, const WarpInT<LW>& in, std::uint32_t log2T,
+                                          std::uint32_t len_off, WSm& ws, const Ring& R, int lane) {
+  const LaneRun run = warp_decode_scan<LW, 128>(in, log2T, len_off, SmemTables{g_tbf}, smem_addr(ws.slot + lane), lane,
+                                                tile_verified(d, in, log2T));
+  // this ECF8 tile's part of the CTA range, in ring tiles tf (and tf + 1)
+  const std::uint64_t A = in.A > R.e0 ? in.A : R.e0;
+  const std::uint64_t E = in.E < R.e1 ? in.E : R.e1;
+  if (A >= E) {
+    __syncwarp();
+    return;
+  }
+  RingOut out = ring_out(in.A, A, E, R, lane);
   compact_write<2>(d, in.A, in.E, run, ws, lane, out);
+}
+
+// Byte-step variant: every lane's output offset is known (lane_start), the
+// lanes decode straight into the warp's staging tile (direct_tile) and the
+// merged FP8 bytes go to the A ring.
+template <int LW, class WSm>
+__device__ __forceinline__ void ring_tile_fsm(const TensorDesc& d, const WarpInT<LW>& in, std::uint32_t log2T, WSm& ws,
+                                              const Ring& R, int lane, const FsmAt& ft) {
+  const std::uint64_t A = in.A > R.e0 ? in.A : R.e0;
+  const std::uint64_t E = in.E < R.e1 ? in.E : R.e1;
+  if (A >= E) return;
+  RingOut out = ring_out(in.A, A, E, R, lane);
+  direct_tile<2>(d, in, ws, lane, out, tile_verified(d, in, log2T), ft);
 }
 
 // Per decode warp: slots of SLOT_ROWS words per lane (a lane's run of LW
@@ -281,7 +303,7 @@ __device__ __forceinline__ void ring_tile(const TensorDesc& d, const WarpInT<LW>
 template <int LW, int SLOT_ROWS>
 using FusedWarpSmem = WarpPipeSmem<SLOT_ROWS, 32 * LW * (SLOT_ROWS > 17 && LW == 4 ? 64 : 32) / 8 + 8>;
 
-template <int LW, int SLOT_ROWS, bool WIDE>
+template <int LW, int SLOT_ROWS, bool WIDE, bool FSM = false>
 __global__ void __launch_bounds__((decode_warps<LW, SLOT_ROWS, WIDE>() + 1) * 32, 1) fused_gemm_kernel(const FusedArgs args) {
   using WSm = FusedWarpSmem<LW, SLOT_ROWS>;
   constexpr int kDecodeWarps = decode_warps<LW, SLOT_ROWS, WIDE>();
@@ -333,7 +355,14 @@ __global__ void __launch_bounds__((decode_warps<LW, SLOT_ROWS, WIDE>() + 1) * 32
       g_consumed = 0;
     }
   }
-  stage_tables(d, g_tbf, threadIdx.x, kThreadsF);
+  if constexpr (FSM) {
+    const uint4* f4 = reinterpret_cast<const uint4*>(d.fsm);
+    const uint4* c4 = reinterpret_cast<const uint4*>(d.fsm_cm);
+    for (int i = threadIdx.x; i < 256 * kFsmStates / 4; i += kThreadsF) reinterpret_cast<uint4*>(g_fsmf)[i] = __ldg(f4 + i);
+    for (int i = threadIdx.x; i < 256 * kFsmStates / 16; i += kThreadsF) reinterpret_cast<uint4*>(g_cmf)[i] = __ldg(c4 + i);
+  } else {
+    stage_tables(d, g_tbf, threadIdx.x, kThreadsF);
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -346,7 +375,7 @@ __global__ void __launch_bounds__((decode_warps<LW, SLOT_ROWS, WIDE>() + 1) * 32
     WSm& ws = wsm[warp];
     WarpInT<LW> nxt;
     std::uint64_t tile = warp;
-    if (tile < n_tiles) load_warp_tile(d, tile, log2T, lane, nxt);
+    if (tile < n_tiles) load_warp_tile<LW, FSM>(d, tile, log2T, lane, nxt);
     while (tile < n_tiles) {
       const WarpInT<LW> cur = nxt;
       unsigned claim = 0;
@@ -359,8 +388,9 @@ __global__ void __launch_bounds__((decode_warps<LW, SLOT_ROWS, WIDE>() + 1) * 32
           asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(d.packed + p0), "r"(bytes) : "memory");
       }
       const std::uint64_t next = __shfl_sync(0xffffffffu, claim, 0);
-      if (next < n_tiles) load_warp_tile(d, next, log2T, lane, nxt);
-      ring_tile(d, cur, log2T, len_off, ws, R, lane);
+      if (next < n_tiles) load_warp_tile<LW, FSM>(d, next, log2T, lane, nxt);
+      if constexpr (FSM) ring_tile_fsm(d, cur, log2T, ws, R, lane, FsmAt{smem_addr(g_fsmf), smem_addr(g_cmf)});
+      else ring_tile(d, cur, log2T, len_off, ws, R, lane);
       tile = next;
     }
   } else {
@@ -510,10 +540,11 @@ std::uint32_t fused_warp_smem(std::uint32_t T, std::uint32_t lmin, std::uint32_t
   return wide ? warps_smem<4, 33, true>() : warps_smem<4, 33, false>();
 }
 
-std::uint32_t fused_stages_a(std::uint32_t m_pad, std::uint32_t warp_smem) {
-  // 227 KB per CTA: tables 29 KB static, the decode warps' pipeline state,
-  // B ring 2 x m_pad x 128 B, A ring stages x 16 KB, 1 KB alignment slack
-  const std::uint32_t budget = 232448 - 30 * 1024;
+std::uint32_t fused_stages_a(std::uint32_t m_pad, std::uint32_t warp_smem, bool fsm) {
+  // 227 KB per CTA: tables 29 KB static (byte-step tables: 20 KB), the
+  // decode warps' pipeline state, B ring 2 x m_pad x 128 B, A ring stages x
+  // 16 KB, 1 KB alignment slack
+  const std::uint32_t budget = 232448 - (fsm ? 21 : 30) * 1024;
   const std::uint32_t fixed = warp_smem + fused_stages_b(m_pad) * m_pad * 128 + 1024;
   const std::uint32_t s = fixed < budget ? (budget - fixed) / kTileElems : 0;
   return s > kMaxStagesA ? kMaxStagesA : s;
@@ -523,10 +554,10 @@ std::uint32_t fused_smem_bytes(std::uint32_t m_pad, std::uint32_t stages_a, std:
   return 1024 + stages_a * kTileElems + fused_stages_b(m_pad) * m_pad * 128 + warp_smem;
 }
 
-template <int LW, int ROWS, bool WIDE>
+template <int LW, int ROWS, bool WIDE, bool FSM = false>
 cudaError_t launch_lw(const FusedArgs& args, std::uint32_t n_cta, cudaStream_t s) {
   const std::uint32_t smem = fused_smem_bytes(args.m_pad, args.stages_a, warps_smem<LW, ROWS, WIDE>());
-  cudaError_t e = cudaFuncSetAttribute(fused_gemm_kernel<LW, ROWS, WIDE>,
+  cudaError_t e = cudaFuncSetAttribute(fused_gemm_kernel<LW, ROWS, WIDE, FSM>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   static const bool pdl = std::getenv("ECF8_NO_PDL") == nullptr;
@@ -540,12 +571,13 @@ cudaError_t launch_lw(const FusedArgs& args, std::uint32_t n_cta, cudaStream_t s
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, fused_gemm_kernel<LW, ROWS, WIDE>, args);
+  return cudaLaunchKernelEx(&cfg, fused_gemm_kernel<LW, ROWS, WIDE, FSM>, args);
 }
 
 template <bool WIDE>
 cudaError_t launch_geometry(const FusedArgs& args, std::uint32_t n_cta, cudaStream_t s) {
   if (fused_lane_windows(args.w.T, args.w.lmin) == 8) return launch_lw<8, 33, WIDE>(args, n_cta, s);
+  if (args.w.lmin >= 2 && args.fsm) return launch_lw<4, 17, WIDE, true>(args, n_cta, s);
   return args.w.lmin >= 2 ? launch_lw<4, 17, WIDE>(args, n_cta, s) : launch_lw<4, 33, WIDE>(args, n_cta, s);
 }
 

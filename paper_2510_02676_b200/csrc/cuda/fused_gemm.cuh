@@ -35,6 +35,7 @@ struct FusedArgs {
   std::uint32_t tmem_cols;  // allocation: one accumulator of acc_cols per n-tile segment (power of two)
   std::uint32_t acc_cols;   // power of two >= max(32, m_pad)
   std::uint32_t w_fmt;       // 0 E4M3, 1 E5M2
+  std::uint32_t fsm;         // 1: byte-step direct decode (lane offsets known for every tile; 4-window lanes)
   float scale;
 };
 
@@ -43,7 +44,7 @@ struct FusedArgs {
 int fused_lane_windows(std::uint32_t T, std::uint32_t lmin);
 std::uint32_t fused_warp_smem(std::uint32_t T, std::uint32_t lmin, std::uint32_t m_pad);
 std::uint32_t fused_stages_b(std::uint32_t m_pad);
-std::uint32_t fused_stages_a(std::uint32_t m_pad, std::uint32_t warp_smem);
+std::uint32_t fused_stages_a(std::uint32_t m_pad, std::uint32_t warp_smem, bool fsm);
 std::uint32_t fused_smem_bytes(std::uint32_t m_pad, std::uint32_t stages_a, std::uint32_t warp_smem);
 cudaError_t launch_fused_gemm(const FusedArgs& args, std::uint32_t n_cta, cudaStream_t s);
 
