@@ -173,6 +173,12 @@ int ecf8_fused_gemm(const ecf8_fused *f, const uint8_t *d_x, uint32_t m, float s
  * added into y. */
 int ecf8_fused_split_k(const ecf8_fused *f);
 void ecf8_fused_free(ecf8_fused *f);
+/* ecf8_host_fused_layout on device memory, stream-ordered: row-major n x k
+ * FP8 bytes <-> the tiled, swizzled sequence (inverse != 0: back).  With the
+ * device decoder and encoder this re-tiles a weight from a reference-format
+ * container (row-major, any T) for the fused GEMM without a host round trip:
+ * decode -> ecf8_fused_layout_device -> ecf8_encode_device (T = 128). */
+int ecf8_fused_layout_device(const uint8_t *d_in, uint64_t n, uint64_t k, uint8_t *d_out, int inverse, void *stream);
 
 #ifdef __cplusplus
 }

@@ -57,6 +57,8 @@ int ecf8_host_compress_raw(const uint8_t *raw, size_t len, uint32_t T, uint8_t *
 int ecf8_host_parse(const uint8_t *bytes, size_t len, ecf8_host_file **out);
 int ecf8_host_file_count(const ecf8_host_file *f);
 int ecf8_host_file_tensor(const ecf8_host_file *f, int i, ecf8_sections *out, const char **name);
+/* Tensor i's shape (container.hpp TensorShape): rank, then up to max_rank dims. */
+int ecf8_host_file_shape(const ecf8_host_file *f, int i, uint64_t *dims, int max_rank, int *rank);
 void ecf8_host_file_free(ecf8_host_file *f);
 /* decompress_streaming: container bytes -> raw file bytes (B200 decode). */
 int ecf8_host_decompress(const uint8_t *bytes, size_t len, uint8_t **out, size_t *out_len,

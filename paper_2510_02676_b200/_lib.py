@@ -121,6 +121,7 @@ _SIGS = {
     "ecf8_fused_gemm": (C.c_int, [_P, _P, C.c_uint32, C.c_float, _P, _P]),
     "ecf8_fused_split_k": (C.c_int, [_P]),
     "ecf8_fused_free": (None, [_P]),
+    "ecf8_fused_layout_device": (C.c_int, [_P, C.c_uint64, C.c_uint64, _P, C.c_int, _P]),
     # ecf8_host.h
     "ecf8_host_free": (None, [_P]),
     "ecf8_host_fused_layout": (C.c_int, [_P, C.c_uint64, C.c_uint64, _P, C.c_int]),
@@ -137,6 +138,7 @@ _SIGS = {
     "ecf8_host_parse": (C.c_int, [_P, C.c_size_t, C.POINTER(_P)]),
     "ecf8_host_file_count": (C.c_int, [_P]),
     "ecf8_host_file_tensor": (C.c_int, [_P, C.c_int, C.POINTER(Sections), C.POINTER(C.c_char_p)]),
+    "ecf8_host_file_shape": (C.c_int, [_P, C.c_int, C.POINTER(C.c_uint64), C.c_int, C.POINTER(C.c_int)]),
     "ecf8_host_file_free": (None, [_P]),
     "ecf8_host_decompress": (
         C.c_int,

@@ -292,10 +292,14 @@ class Ecf8File:
         check(lib.ecf8_host_parse(_ptr(buf), buf.size, C.byref(h)))
         self._h = h
         self.tensors: list[tuple[str, EncodedTensor]] = []
+        self.shapes: list[list[int]] = []
         for i in range(lib.ecf8_host_file_count(h)):
             s, name = Sections(), C.c_char_p()
             check(lib.ecf8_host_file_tensor(h, i, C.byref(s), C.byref(name)))
             self.tensors.append((name.value.decode("utf-8", "replace"), _from_sections(s, self)))
+            dims, rank = (C.c_uint64 * 255)(), C.c_int()
+            check(lib.ecf8_host_file_shape(h, i, dims, 255, C.byref(rank)))
+            self.shapes.append([int(dims[j]) for j in range(rank.value)])
 
     def __del__(self):
         if getattr(self, "_h", None):

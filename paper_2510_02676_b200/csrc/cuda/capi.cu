@@ -1147,4 +1147,17 @@ void ecf8_fused_free(ecf8_fused* f) {
   delete f;
 }
 
+int ecf8_fused_layout_device(const uint8_t* d_in, uint64_t n, uint64_t k, uint8_t* d_out, int inverse, void* stream) {
+  return guarded([&]() -> int {
+    if (!d_in || !d_out) return fail(ECF8_EINVAL, "null argument");
+    if (n % 128 || k % 128) return fail(ECF8_EINVAL, "fused layout needs n, k multiples of 128");
+    if ((reinterpret_cast<std::uintptr_t>(d_in) | reinterpret_cast<std::uintptr_t>(d_out)) & 15)
+      return fail(ECF8_EINVAL, "device buffers must be 16-byte aligned");
+    if (int rc = require_device()) return rc;
+    cu(ecf8::dev::launch_fused_layout(d_in, n, k, d_out, inverse != 0, static_cast<cudaStream_t>(stream)),
+       "fused layout launch");
+    return ECF8_OK;
+  });
+}
+
 }  // extern "C"

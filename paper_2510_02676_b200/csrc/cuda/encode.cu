@@ -13,6 +13,8 @@
 // the neighbouring chunks).
 #include "encode.cuh"
 
+#include <algorithm>
+
 namespace ecf8::dev {
 namespace {
 
@@ -287,6 +289,33 @@ cudaError_t launch_encode_emit(const EncodeArgs& a, cudaStream_t s) {
   const std::uint64_t n_chunks = (a.n + kEncChunkElems - 1) / kEncChunkElems;
   if (n_chunks == 0) return cudaSuccess;
   encode_emit_kernel<<<static_cast<unsigned>(n_chunks), kEncThreads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+// One thread per 16-byte chunk: tile (nt, kt) in row-major tile order, each
+// tile the 128B-swizzled K-major image (chunk c of row r at r * 128 +
+// ((c ^ (r & 7)) << 4)) -- the host layout of ecf8_host_fused_layout.
+__global__ void fused_layout_kernel(const uint4* __restrict__ in, std::uint64_t n, std::uint64_t k,
+                                    uint4* __restrict__ out, bool inverse) {
+  const std::uint64_t KT = k / 128, chunks = n * k / 16;
+  for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < chunks;
+       i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+    // i: chunk of the row-major matrix (coalesced on that side)
+    const std::uint64_t row = i / (k / 16), cc = i % (k / 16);
+    const std::uint64_t nt = row / 128, r = row % 128, kt = cc / 8, c = cc % 8;
+    const std::uint64_t t = (nt * KT + kt) * 1024 + r * 8 + (c ^ (r & 7));
+    if (inverse) out[i] = in[t];
+    else out[t] = in[i];
+  }
+}
+
+cudaError_t launch_fused_layout(const std::uint8_t* in, std::uint64_t n, std::uint64_t k, std::uint8_t* out,
+                                bool inverse, cudaStream_t s) {
+  const std::uint64_t chunks = n * k / 16;
+  if (!chunks) return cudaSuccess;
+  const std::uint64_t blocks = std::min<std::uint64_t>((chunks + 255) / 256, 148 * 16);
+  fused_layout_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(reinterpret_cast<const uint4*>(in), n, k,
+                                                                    reinterpret_cast<uint4*>(out), inverse);
   return cudaGetLastError();
 }
 

@@ -35,4 +35,8 @@ struct EncodeArgs {
 // Pass 3: bitstream, gaps, outpos and packed nibbles.
 cudaError_t launch_encode_emit(const EncodeArgs& a, cudaStream_t s);
 
+// Row-major [n, k] FP8 bytes <-> the fused GEMM's tiled, swizzled layout.
+cudaError_t launch_fused_layout(const std::uint8_t* in, std::uint64_t n, std::uint64_t k, std::uint8_t* out,
+                                bool inverse, cudaStream_t s);
+
 }  // namespace ecf8::dev

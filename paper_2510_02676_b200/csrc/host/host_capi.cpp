@@ -227,6 +227,15 @@ int ecf8_host_file_tensor(const ecf8_host_file* f, int i, ecf8_sections* out, co
   return ECF8_OK;
 }
 
+int ecf8_host_file_shape(const ecf8_host_file* f, int i, uint64_t* dims, int max_rank, int* rank) {
+  if (!f || i < 0 || static_cast<std::size_t>(i) >= f->f.tensors.size() || !rank)
+    return set_error(ECF8_EINVAL, "tensor index out of range");
+  const auto& d = f->f.tensors[i].shape.dims;
+  *rank = static_cast<int>(d.size());
+  for (int j = 0; j < *rank && j < max_rank; ++j) dims[j] = d[j];
+  return ECF8_OK;
+}
+
 void ecf8_host_file_free(ecf8_host_file* f) { delete f; }
 
 int ecf8_host_decompress(const uint8_t* bytes, size_t len, uint8_t** out, size_t* out_len,

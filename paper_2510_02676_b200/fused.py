@@ -38,19 +38,78 @@ def fused_layout_inverse(seq: np.ndarray, n: int, k: int) -> np.ndarray:
     return out
 
 
-class FusedLinear:
-    """An ECF8-compressed FP8 weight [n, k] served by the decode-fused GEMM."""
+def fused_layout_device(w: torch.Tensor, n: int, k: int, inverse: bool = False,
+                        stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+    """ecf8_fused_layout_device: the tiled layout on the GPU (row-major <->
+    tiled FP8 bytes, n * k uint8 in and out)."""
+    if not w.is_cuda or w.numel() != n * k:
+        raise ValueError(f"expected {n * k} CUDA bytes")
+    src = w.contiguous().view(torch.uint8).reshape(-1)
+    out = torch.empty(n * k, dtype=torch.uint8, device=w.device)
+    check(lib.ecf8_fused_layout_device(C.c_void_p(src.data_ptr()), n, k, C.c_void_p(out.data_ptr()), int(inverse),
+                                       _stream_ptr(stream)))
+    return out
 
-    def __init__(self, w_fp8: np.ndarray, fmt: str = "e4m3", threads_per_block: int = 128):
-        self.n, self.k = map(int, w_fp8.shape)
+
+class FusedLinear:
+    """An ECF8-compressed FP8 weight [n, k] served by the decode-fused GEMM.
+
+    FusedLinear(w_fp8)                  host bytes, tiled and encoded on the host
+    FusedLinear.from_encoded(t, n, k)   a row-major ECF8 tensor (e.g. one tensor
+                                        of a reference-written .ecf8 container,
+                                        any T) re-tiled on the GPU: decode ->
+                                        tiled layout -> device encoder (T = 128)
+    """
+
+    def __init__(self, w_fp8: np.ndarray | None, fmt: str = "e4m3", threads_per_block: int = 128,
+                 _dev: DeviceTensor | None = None, _nk: tuple[int, int] | None = None):
+        if fmt not in ("e4m3", "e5m2"):
+            raise ValueError("fmt must be e4m3 or e5m2")
         self.fmt = fmt
-        # T = 128 serves both decode-lane widths (1-bit codes need T <= 128)
-        self.encoded = codec.encode_tensor(fused_layout(w_fp8), threads_per_block)
-        self.dev = DeviceTensor(self.encoded)
+        if _dev is None:
+            self.n, self.k = map(int, w_fp8.shape)
+            # T = 128 serves both decode-lane widths (1-bit codes need T <= 128)
+            self.encoded = codec.encode_tensor(fused_layout(w_fp8), threads_per_block)
+            self.dev = DeviceTensor(self.encoded)
+        else:
+            self.n, self.k = _nk
+            self.encoded = None
+            self.dev = _dev
         h = C.c_void_p()
         check(lib.ecf8_fused_create(self.dev.handle, self.n, self.k, {"e4m3": 0, "e5m2": 1}[fmt], C.byref(h)))
         self.handle = h
         self.split_k = int(lib.ecf8_fused_split_k(h))
+
+    @classmethod
+    def from_encoded(cls, t: codec.EncodedTensor, n: int, k: int, fmt: str = "e4m3",
+                     stream: torch.cuda.Stream | None = None) -> "FusedLinear":
+        """Serve a row-major ECF8 weight (reference container layout) through
+        the fused GEMM: decoded, re-tiled and re-encoded on the GPU -- no host
+        round trip of the weight."""
+        if t.n_elem != n * k or n % 128 or k % 128:
+            raise ValueError("fused GEMM needs an n x k weight with n, k multiples of 128")
+        rowmajor = DeviceTensor(t, stream)
+        w = rowmajor.decode(stream)
+        tiled = fused_layout_device(w, n, k, stream=stream)
+        del w
+        rowmajor.free()
+        dev = DeviceTensor.encode(tiled, threads_per_block=128, stream=stream)
+        return cls(None, fmt, _dev=dev, _nk=(n, k))
+
+    @classmethod
+    def from_container(cls, data: bytes, name: str, fmt: str = "e4m3") -> "FusedLinear":
+        """One 2-D tensor of an .ecf8 container (container.hpp:18-30) by name."""
+        f = codec.parse_container(data)
+        for (tname, t), dims in zip(f.tensors, f.shapes):
+            if tname == name:
+                if len(dims) != 2:
+                    raise ValueError(f"{name}: expected a 2-D weight, got shape {dims}")
+                return cls.from_encoded(t, int(dims[0]), int(dims[1]), fmt)
+        raise KeyError(name)
+
+    @property
+    def compressed_bytes(self) -> int:
+        return int(lib.ecf8_tensor_algorithmic_bytes(self.dev.handle)) - self.n * self.k
 
     def __call__(self, x: torch.Tensor, scale: float = 1.0, out: torch.Tensor | None = None,
                  stream: torch.cuda.Stream | None = None) -> torch.Tensor:
@@ -68,10 +127,6 @@ class FusedLinear:
                                   C.c_void_p(out.data_ptr()), _stream_ptr(stream)))
         return out
 
-    @property
-    def compressed_bytes(self) -> int:
-        return self.encoded.compressed_bytes()
-
     def free(self):
         if getattr(self, "handle", None):
             lib.ecf8_fused_free(self.handle)
@@ -79,3 +134,24 @@ class FusedLinear:
 
     def __del__(self):
         self.free()
+
+
+# ---- torch.library op: the fused GEMM as a PyTorch operator (shape-inferable,
+# usable from torch.compile'd graphs and CUDA graphs; the handle is the
+# FusedLinear's ecf8_fused*)
+
+@torch.library.custom_op("ecf8::fused_gemm", mutates_args=())
+def fused_gemm_op(x: torch.Tensor, handle: int, n: int, scale: float) -> torch.Tensor:
+    """y[m, n] (fp32) = scale * x[m, k] . W^T for the ECF8 weight behind `handle`."""
+    if x.dtype != torch.float8_e4m3fn or not x.is_cuda or x.dim() != 2:
+        raise ValueError("x must be a CUDA float8_e4m3fn tensor [m, k]")
+    x = x.contiguous()
+    out = torch.empty(x.shape[0], n, dtype=torch.float32, device=x.device)
+    check(lib.ecf8_fused_gemm(C.c_void_p(handle), C.c_void_p(x.data_ptr()), x.shape[0], float(scale),
+                              C.c_void_p(out.data_ptr()), _stream_ptr(None)))
+    return out
+
+
+@fused_gemm_op.register_fake
+def _fused_gemm_fake(x: torch.Tensor, handle: int, n: int, scale: float) -> torch.Tensor:
+    return x.new_empty(x.shape[0], n, dtype=torch.float32)

@@ -9,9 +9,13 @@ lists framework hooks as out of its scope).  Here:
     every layer decodes into (the device-side ``ReusableBuffer``,
     container.hpp:80-95): grow-only, counts its allocations.
   * ``ECF8Linear``   -- an ``nn.Module`` holding ECF8-compressed FP8 weights
-    ([out_features, in_features] E4M3 or E5M2 bytes) resident in HBM; forward
-    decodes them with one batched launch into the arena and runs the FP8 GEMM
-    (``torch._scaled_mm``, cuBLASLt) on the decoded view.
+    ([out_features, in_features] E4M3 or E5M2 bytes) resident in HBM.  When
+    both feature sizes are multiples of 128 (and m <= 256 tokens), forward is
+    the decode-fused tcgen05 GEMM (``torch.ops.ecf8.fused_gemm``: the weight
+    is decoded tile by tile into shared memory and never written to HBM; its
+    tiled copy is made on the GPU from the row-major ECF8 tensor, fused.py);
+    otherwise it decodes the weight with one batched launch into the arena
+    and runs the FP8 GEMM (``torch._scaled_mm``, cuBLASLt) on it.
   * ``compress_linears`` -- replaces the ``nn.Linear`` layers of a model with
     ``ECF8Linear`` built from FP8-quantised copies of their weights.
 
@@ -70,7 +74,8 @@ class ECF8Linear(nn.Module):
     is supported."""
 
     def __init__(self, weight_fp8: np.ndarray, bias: torch.Tensor | None = None, scale_w: float = 1.0,
-                 fmt: str = "e4m3", threads_per_block: int = 256, arena: DecodeArena | None = None):
+                 fmt: str = "e4m3", threads_per_block: int = 256, arena: DecodeArena | None = None,
+                 fused: bool | None = None):
         super().__init__()
         if weight_fp8.ndim != 2:
             raise ValueError("weight must be [out_features, in_features]")
@@ -85,6 +90,14 @@ class ECF8Linear(nn.Module):
         self.arena = arena or default_arena()
         self._batch_key = None
         self._batch = None
+        if fused is None:
+            fused = self.out_features % 128 == 0 and self.in_features % 128 == 0
+        self.fused = None
+        if fused:
+            from .fused import FusedLinear
+
+            # the tiled copy is made on the GPU from the row-major ECF8 tensor
+            self.fused = FusedLinear.from_encoded(self.encoded, self.out_features, self.in_features, fmt)
 
     @property
     def compressed_bytes(self) -> int:
@@ -103,7 +116,6 @@ class ECF8Linear(nn.Module):
         return buf[:n].view(_FP8[self.fmt]).view(self.out_features, self.in_features)
 
     def forward(self, x: torch.Tensor, scale_x: torch.Tensor | None = None) -> torch.Tensor:
-        w = self.decode_weight()
         lead = x.shape[:-1]
         x2 = x.reshape(-1, self.in_features)
         act = torch.float8_e4m3fn
@@ -115,6 +127,13 @@ class ECF8Linear(nn.Module):
         elif scale_x is None:
             scale_x = torch.tensor(1.0, device=x.device)
         m = x2.shape[0]
+        if self.fused is not None and 1 <= m <= 256:
+            y = torch.ops.ecf8.fused_gemm(x2, self.fused.handle.value, self.out_features, 1.0)
+            y = y * (scale_x.float().reshape(()) * self.scale_w)
+            if self.bias is not None:
+                y = y + self.bias.float()
+            return y.to(torch.bfloat16).reshape(*lead, self.out_features)
+        w = self.decode_weight()
         pad = (-m) % 16
         if pad:
             x2 = torch.cat([x2, x2.new_zeros(pad, self.in_features)])

@@ -79,6 +79,24 @@ def main():
         json.dump({"generator": "tests/golden/make_golden.py (reference compiled from /root/reference/proj/src)",
                    "cases": manifest}, f, indent=1)
     print(f"wrote {len(manifest)} cases, {sum(m['container_bytes'] for m in manifest)} container bytes")
+    weights(ref)
+
+
+def weights(ref):
+    """A reference-written container of 2-D weights (row-major [out, in] FP8
+    E4M3, reference synth_raw draws) for the container -> fused GEMM path."""
+    tensors = [("layers.0.mlp.up_proj.weight", [256, 384], ref.synth(1.8, 0.05, 256 * 384, 21)),
+               ("layers.0.self_attn.o_proj.weight", [128, 1024], ref.synth(1.8, 0.05, 128 * 1024, 22))]
+    raw = codec.raw_file([(n, d, x) for n, d, x in tensors])
+    data = ref.compress_raw(raw, 256)
+    out, _ = ref.decompress(data)
+    assert out == raw
+    with open(os.path.join(HERE, "weights_T256.ecf8"), "wb") as f:
+        f.write(data)
+    with open(os.path.join(HERE, "weights.json"), "w") as f:
+        json.dump({"container": "weights_T256.ecf8", "T": 256, "container_sha256": hashlib.sha256(data).hexdigest(),
+                   "tensors": [{"name": n, "shape": d, "sha256": hashlib.sha256(x.tobytes()).hexdigest()}
+                               for n, d, x in tensors]}, f, indent=1)
 
 
 if __name__ == "__main__":
