@@ -1079,7 +1079,7 @@ int ecf8_fused_create(const ecf8_dev_tensor* t, uint64_t n, uint64_t k, int w_fm
     // byte-step direct decode when every verification tile is direct (the
     // upload check's tile_direct bits) -- always, for encoder-written weights
     static const bool no_fsm = std::getenv("ECF8_FUSED_NO_FSM") != nullptr;  // A/B runs
-    if (!no_fsm && t->desc.fsm && t->desc.lane_start && ecf8::dev::fused_lane_windows(t->T, t->desc.lmin) == 4) {
+    if (!no_fsm && t->desc.fsm && t->desc.lane_start && t->T >= 8 && t->T <= 256) {
       std::vector<std::uint32_t> bits((t->n_vtiles + 31) / 32);
       cu(cudaMemcpy(bits.data(), t->desc.tile_direct, 4 * bits.size(), cudaMemcpyDeviceToHost), "D2H tile_direct");
       bool all = true;
@@ -1123,8 +1123,8 @@ int ecf8_fused_gemm(const ecf8_fused* f, const uint8_t* d_x, uint32_t m, float s
     a.k = static_cast<std::uint32_t>(f->k);
     a.split_k = f->split_k;
     a.fsm = f->fsm ? 1u : 0u;
-    a.stages_a = ecf8::dev::fused_stages_a(a.m_pad, ecf8::dev::fused_warp_smem(f->w->T, f->w->desc.lmin, a.m_pad),
-                                           f->fsm);
+    a.stages_a = ecf8::dev::fused_stages_a(
+        a.m_pad, ecf8::dev::fused_warp_smem(f->w->T, f->w->desc.lmin, a.m_pad, f->fsm), f->fsm);
     a.stages_b = ecf8::dev::fused_stages_b(a.m_pad);
     if (a.stages_a < 2) return fail(ECF8_EINVAL, "fused GEMM: shared memory too small for this m");
     a.acc_cols = 32;

@@ -64,9 +64,14 @@ namespace {
 #ifndef ECF8_FUSED_WIDE_XSTAGES
 #define ECF8_FUSED_WIDE_XSTAGES 1
 #endif
-template <int LW, int ROWS, bool WIDE>
+#ifndef ECF8_FUSED_FSM_WARPS
+#define ECF8_FUSED_FSM_WARPS 12
+#endif
+// Byte-step variant: 8-window lanes, two chains each (direct_tile), 8.2 KB of
+// warp state: ECF8_FUSED_FSM_WARPS decode warps.
+template <int LW, int ROWS, bool WIDE, bool FSM = false>
 constexpr int decode_warps() {
-  return ROWS > 17 ? 12 : (WIDE ? ECF8_FUSED_WIDE_WARPS : ECF8_FUSED_WARPS);
+  return FSM ? ECF8_FUSED_FSM_WARPS : ROWS > 17 ? 12 : (WIDE ? ECF8_FUSED_WIDE_WARPS : ECF8_FUSED_WARPS);
 }
 constexpr std::uint32_t kTileElems = 128 * 128;  // one K tile of A (bytes)
 
@@ -304,9 +309,9 @@ template <int LW, int SLOT_ROWS>
 using FusedWarpSmem = WarpPipeSmem<SLOT_ROWS, 32 * LW * (SLOT_ROWS > 17 && LW == 4 ? 64 : 32) / 8 + 8>;
 
 template <int LW, int SLOT_ROWS, bool WIDE, bool FSM = false>
-__global__ void __launch_bounds__((decode_warps<LW, SLOT_ROWS, WIDE>() + 1) * 32, 1) fused_gemm_kernel(const FusedArgs args) {
+__global__ void __launch_bounds__((decode_warps<LW, SLOT_ROWS, WIDE, FSM>() + 1) * 32, 1) fused_gemm_kernel(const FusedArgs args) {
   using WSm = FusedWarpSmem<LW, SLOT_ROWS>;
-  constexpr int kDecodeWarps = decode_warps<LW, SLOT_ROWS, WIDE>();
+  constexpr int kDecodeWarps = decode_warps<LW, SLOT_ROWS, WIDE, FSM>();
   constexpr int kThreadsF = (kDecodeWarps + 1) * 32;
   constexpr int kCtrlWarp = kDecodeWarps;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -527,14 +532,15 @@ int fused_lane_windows(std::uint32_t T, std::uint32_t lmin) {
   return 0;
 }
 
-template <int LW, int ROWS, bool WIDE>
+template <int LW, int ROWS, bool WIDE, bool FSM = false>
 constexpr std::uint32_t warps_smem() {
-  return static_cast<std::uint32_t>(decode_warps<LW, ROWS, WIDE>() * sizeof(FusedWarpSmem<LW, ROWS>));
+  return static_cast<std::uint32_t>(decode_warps<LW, ROWS, WIDE, FSM>() * sizeof(FusedWarpSmem<LW, ROWS>));
 }
 
 // All decode warps' pipeline state.
-std::uint32_t fused_warp_smem(std::uint32_t T, std::uint32_t lmin, std::uint32_t m_pad) {
+std::uint32_t fused_warp_smem(std::uint32_t T, std::uint32_t lmin, std::uint32_t m_pad, bool fsm) {
   const bool wide = m_pad > 128;
+  if (fsm) return wide ? warps_smem<8, 33, true, true>() : warps_smem<8, 33, false, true>();
   if (fused_lane_windows(T, lmin) == 8) return wide ? warps_smem<8, 33, true>() : warps_smem<8, 33, false>();
   if (lmin >= 2) return wide ? warps_smem<4, 17, true>() : warps_smem<4, 17, false>();
   return wide ? warps_smem<4, 33, true>() : warps_smem<4, 33, false>();
@@ -556,14 +562,14 @@ std::uint32_t fused_smem_bytes(std::uint32_t m_pad, std::uint32_t stages_a, std:
 
 template <int LW, int ROWS, bool WIDE, bool FSM = false>
 cudaError_t launch_lw(const FusedArgs& args, std::uint32_t n_cta, cudaStream_t s) {
-  const std::uint32_t smem = fused_smem_bytes(args.m_pad, args.stages_a, warps_smem<LW, ROWS, WIDE>());
+  const std::uint32_t smem = fused_smem_bytes(args.m_pad, args.stages_a, warps_smem<LW, ROWS, WIDE, FSM>());
   cudaError_t e = cudaFuncSetAttribute(fused_gemm_kernel<LW, ROWS, WIDE, FSM>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   static const bool pdl = std::getenv("ECF8_NO_PDL") == nullptr;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(n_cta);
-  cfg.blockDim = dim3((decode_warps<LW, ROWS, WIDE>() + 1) * 32);
+  cfg.blockDim = dim3((decode_warps<LW, ROWS, WIDE, FSM>() + 1) * 32);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -577,7 +583,7 @@ cudaError_t launch_lw(const FusedArgs& args, std::uint32_t n_cta, cudaStream_t s
 template <bool WIDE>
 cudaError_t launch_geometry(const FusedArgs& args, std::uint32_t n_cta, cudaStream_t s) {
   if (fused_lane_windows(args.w.T, args.w.lmin) == 8) return launch_lw<8, 33, WIDE>(args, n_cta, s);
-  if (args.w.lmin >= 2 && args.fsm) return launch_lw<4, 17, WIDE, true>(args, n_cta, s);
+  if (args.fsm) return launch_lw<8, 33, WIDE, true>(args, n_cta, s);
   return args.w.lmin >= 2 ? launch_lw<4, 17, WIDE>(args, n_cta, s) : launch_lw<4, 33, WIDE>(args, n_cta, s);
 }
 

@@ -35,14 +35,14 @@ struct FusedArgs {
   std::uint32_t tmem_cols;  // allocation: one accumulator of acc_cols per n-tile segment (power of two)
   std::uint32_t acc_cols;   // power of two >= max(32, m_pad)
   std::uint32_t w_fmt;       // 0 E4M3, 1 E5M2
-  std::uint32_t fsm;         // 1: byte-step direct decode (lane offsets known for every tile; 4-window lanes)
+  std::uint32_t fsm;         // 1: byte-step direct decode (lane offsets known for every tile; 8-window lanes)
   float scale;
 };
 
 // Windows per decode lane for a tiled weight (4 or 8; 0 = unsupported) and
 // the shared memory of one decode warp's pipeline (fused_gemm.cu).
 int fused_lane_windows(std::uint32_t T, std::uint32_t lmin);
-std::uint32_t fused_warp_smem(std::uint32_t T, std::uint32_t lmin, std::uint32_t m_pad);
+std::uint32_t fused_warp_smem(std::uint32_t T, std::uint32_t lmin, std::uint32_t m_pad, bool fsm);
 std::uint32_t fused_stages_b(std::uint32_t m_pad);
 std::uint32_t fused_stages_a(std::uint32_t m_pad, std::uint32_t warp_smem, bool fsm);
 std::uint32_t fused_smem_bytes(std::uint32_t m_pad, std::uint32_t stages_a, std::uint32_t warp_smem);

@@ -152,16 +152,17 @@ def quantize_fp8(w: torch.Tensor, fmt: str = "e4m3") -> tuple[np.ndarray, float]
 
 
 def compress_linears(model: nn.Module, fmt: str = "e4m3", arena: DecodeArena | None = None,
-                     threads_per_block: int = 256) -> dict[str, ECF8Linear]:
+                     threads_per_block: int = 256, fused: bool | None = None) -> dict[str, ECF8Linear]:
     """Replace every nn.Linear (feature sizes multiple of 16) by an ECF8Linear
-    sharing one decode arena.  Returns {qualified name: module}."""
+    sharing one decode arena (fused: see ECF8Linear; None = where the shapes
+    allow).  Returns {qualified name: module}."""
     arena = arena or DecodeArena()
     done = {}
     for name, mod in list(model.named_modules()):
         for cname, child in list(mod.named_children()):
             if isinstance(child, nn.Linear) and child.in_features % 16 == 0 and child.out_features % 16 == 0:
                 q, s = quantize_fp8(child.weight, fmt)
-                new = ECF8Linear(q, child.bias, s, fmt, threads_per_block, arena)
+                new = ECF8Linear(q, child.bias, s, fmt, threads_per_block, arena, fused)
                 setattr(mod, cname, new)
                 done[f"{name}.{cname}" if name else cname] = new
     return done

@@ -56,7 +56,7 @@ def test_compress_linears_shares_one_arena():
     x = torch.randn(8, 512, device="cuda")
     with torch.no_grad():
         ref = model(x)
-        mods = compress_linears(model)
+        mods = compress_linears(model, fused=False)  # the just-in-time decode path
         assert len(mods) == 3 and all(isinstance(m, ECF8Linear) for m in mods.values())
         y = model(x)
         y2 = model(x)
@@ -66,3 +66,21 @@ def test_compress_linears_shares_one_arena():
     assert torch.equal(y, y2)  # re-decoding is deterministic
     rel = (y.float() - ref).norm() / ref.norm()
     assert rel < 0.1  # FP8 weight + activation quantisation error only
+
+
+def test_compress_linears_fused_matches_decode_then_gemm():
+    from paper_2510_02676_b200.hooks import compress_linears
+
+    torch.manual_seed(1)
+    make = lambda: torch.nn.Sequential(torch.nn.Linear(512, 1024), torch.nn.GELU(),  # noqa: E731
+                                       torch.nn.Linear(1024, 256)).cuda()
+    a = make()
+    b = make()
+    b.load_state_dict(a.state_dict())
+    x = torch.randn(8, 512, device="cuda")
+    with torch.no_grad():
+        ma = compress_linears(a, fused=True)
+        mb = compress_linears(b, fused=False)
+        assert all(m.fused is not None for m in ma.values()) and all(m.fused is None for m in mb.values())
+        ya, yb = a(x), b(x)
+    torch.testing.assert_close(ya.float(), yb.float(), rtol=2e-2, atol=2e-2 * yb.float().abs().max().item())
