@@ -1125,7 +1125,7 @@ int ecf8_fused_gemm(const ecf8_fused* f, const uint8_t* d_x, uint32_t m, float s
     a.fsm = f->fsm ? 1u : 0u;
     a.stages_a = ecf8::dev::fused_stages_a(
         a.m_pad, ecf8::dev::fused_warp_smem(f->w->T, f->w->desc.lmin, a.m_pad, f->fsm), f->fsm);
-    a.stages_b = ecf8::dev::fused_stages_b(a.m_pad);
+    a.stages_b = ecf8::dev::fused_stages_b(a.m_pad, f->fsm);
     if (a.stages_a < 2) return fail(ECF8_EINVAL, "fused GEMM: shared memory too small for this m");
     a.acc_cols = 32;
     while (a.acc_cols < a.m_pad) a.acc_cols <<= 1;

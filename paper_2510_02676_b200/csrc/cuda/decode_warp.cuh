@@ -217,21 +217,26 @@ struct WarpPipeSmem {
 // nibbles at nibble off + i for element A + i) and the packed bytes copied
 // to the slots (from the 16-byte aligned pk_a): full 16-element chunks as
 // lane-interleaved 16-byte stores, the ragged first / last chunk byte-wise.
-template <int UNROLL, class WSm, class Out>
+// GPK: the packed bytes are read from global memory (gpk = d.packed; L2
+// after the tile's bulk prefetch) instead of the slots -- the fused GEMM,
+// whose shared memory goes to the A ring.
+template <int UNROLL, bool GPK = false, class WSm, class Out>
 __device__ __forceinline__ void write_back(std::uint64_t S0, std::uint32_t off, std::uint32_t data_end,
-                                           std::uint64_t pk_a, const WSm& ws, int lane, Out& out) {
+                                           std::uint64_t pk_a, const WSm& ws, int lane, Out& out,
+                                           const std::uint8_t* gpk = nullptr) {
   const std::uint32_t nch = (data_end + 15) >> 4;
   const std::uint32_t full_lo = (off + 15) >> 4, full_hi = data_end >> 4;
   const std::uint32_t nfull = full_hi > full_lo ? full_hi - full_lo : 0u;
   const std::uint64_t pk_lo = (S0 >> 1) + 8 * full_lo;
   out.wait();
   const uint2* sl = reinterpret_cast<const uint2*>(ws.stage) + full_lo + lane;
-  const uint2* pl = reinterpret_cast<const uint2*>(reinterpret_cast<const std::uint8_t*>(ws.slot) + (pk_lo - pk_a)) + lane;
+  const uint2* pl = GPK ? reinterpret_cast<const uint2*>(gpk + pk_lo) + lane
+                        : reinterpret_cast<const uint2*>(reinterpret_cast<const std::uint8_t*>(ws.slot) + (pk_lo - pk_a)) + lane;
   std::uint32_t k = lane;
   for (; k + 32 * (UNROLL - 1) < nfull; k += 32 * UNROLL, sl += 32 * UNROLL, pl += 32 * UNROLL) {
 #pragma unroll
     for (int u = 0; u < UNROLL; ++u) {
-      const uint2 s = sl[32 * u], q = pl[32 * u];
+      const uint2 s = sl[32 * u], q = GPK ? __ldg(pl + 32 * u) : pl[32 * u];
       uint4 r;
       merge8(s.x, q.x, r.x, r.y);
       merge8(s.y, q.y, r.z, r.w);
@@ -239,7 +244,7 @@ __device__ __forceinline__ void write_back(std::uint64_t S0, std::uint32_t off, 
     }
   }
   for (; k < nfull; k += 32, sl += 32, pl += 32) {
-    const uint2 s = *sl, q = *pl;
+    const uint2 s = *sl, q = GPK ? __ldg(pl) : *pl;
     uint4 r;
     merge8(s.x, q.x, r.x, r.y);
     merge8(s.y, q.y, r.z, r.w);
@@ -252,8 +257,9 @@ __device__ __forceinline__ void write_back(std::uint64_t S0, std::uint32_t off, 
                               : (full_hi < nch && !(nch == 1 && full_lo > 0) && i < data_end);
   if (edge) {
     const std::uint32_t x = (ws.stage[i >> 3] >> (4 * (i & 7))) & 15u;
-    const std::uint8_t* const pks = reinterpret_cast<const std::uint8_t*>(ws.slot) + ((S0 >> 1) - pk_a);
-    out.byte(i, merge1(x, pks[i >> 1], i & 1));
+    const std::uint8_t qb = GPK ? __ldg(gpk + (S0 >> 1) + (i >> 1))
+                                : (reinterpret_cast<const std::uint8_t*>(ws.slot) + ((S0 >> 1) - pk_a))[i >> 1];
+    out.byte(i, merge1(x, qb, i & 1));
   }
   out.done();
 }
@@ -371,7 +377,7 @@ __device__ __forceinline__ void compact_write(const TensorDesc& d, std::uint64_t
 // plain stores (each belongs to one chain); a chain's partial last word is
 // OR-ed in after every chain's first word (which may share it) is stored.
 // The tile's packed bytes stream into the slots while the lanes decode.
-template <int UNROLL, int LW, class WSm, class Out, class FT = FsmPinned>
+template <int UNROLL, int LW, bool GPK = false, class WSm, class Out, class FT = FsmPinned>
 __device__ __forceinline__ void direct_tile(const TensorDesc& d, const WarpInT<LW>& in, WSm& ws, int lane, Out& out,
                                             bool verified, const FT& ft = FT{}) {
   const std::uint32_t off = static_cast<std::uint32_t>(in.A & 15);  // staging nibble of element A
@@ -384,7 +390,7 @@ __device__ __forceinline__ void direct_tile(const TensorDesc& d, const WarpInT<L
     for (std::uint32_t i = lane; i < n16; i += 32)
       asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(st + 16 * i), "r"(0u) : "memory");
   }
-  const std::uint64_t pk_a = fetch_packed(d, S0, data_end, ws, lane);
+  const std::uint64_t pk_a = GPK ? 0 : fetch_packed(d, S0, data_end, ws, lane);
   __syncwarp();  // the zeroes are in place
   std::uint32_t ta_addr = 0, ta = 0, tb_addr = 0, tb = 0;
   if (static_cast<std::uint32_t>(lane) * LW < in.nwin) {
@@ -439,9 +445,9 @@ __device__ __forceinline__ void direct_tile(const TensorDesc& d, const WarpInT<L
   __syncwarp();  // every full word and every lane's first word is stored
   if (ta) asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(ta_addr), "r"(ta) : "memory");
   if (tb) asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(tb_addr), "r"(tb) : "memory");
-  asm volatile("cp.async.wait_all;" ::: "memory");
+  if constexpr (!GPK) asm volatile("cp.async.wait_all;" ::: "memory");
   __syncwarp();
-  write_back<UNROLL>(S0, off, data_end, pk_a, ws, lane, out);
+  write_back<UNROLL, GPK>(S0, off, data_end, pk_a, ws, lane, out, d.packed);
 }
 
 }  // namespace ecf8::dev

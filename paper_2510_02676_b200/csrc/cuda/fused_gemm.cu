@@ -39,6 +39,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
+#include <type_traits>
 
 #include "decode.cuh"
 #include "decode_common.cuh"
@@ -65,10 +66,10 @@ namespace {
 #define ECF8_FUSED_WIDE_XSTAGES 1
 #endif
 #ifndef ECF8_FUSED_FSM_WARPS
-#define ECF8_FUSED_FSM_WARPS 12
+#define ECF8_FUSED_FSM_WARPS 16
 #endif
-// Byte-step variant: 8-window lanes, two chains each (direct_tile), 8.2 KB of
-// warp state: ECF8_FUSED_FSM_WARPS decode warps.
+// Byte-step variant: 8-window lanes, two chains each (direct_tile), 4.2 KB of
+// warp state (the staging tile): ECF8_FUSED_FSM_WARPS decode warps.
 template <int LW, int ROWS, bool WIDE, bool FSM = false>
 constexpr int decode_warps() {
   return FSM ? ECF8_FUSED_FSM_WARPS : ROWS > 17 ? 12 : (WIDE ? ECF8_FUSED_WIDE_WARPS : ECF8_FUSED_WARPS);
@@ -300,19 +301,30 @@ __device__ __forceinline__ void ring_tile_fsm(const TensorDesc& d, const WarpInT
   const std::uint64_t E = in.E < R.e1 ? in.E : R.e1;
   if (A >= E) return;
   RingOut out = ring_out(in.A, A, E, R, lane);
-  direct_tile<2>(d, in, ws, lane, out, tile_verified(d, in, log2T), ft);
+  direct_tile<2, LW, true>(d, in, ws, lane, out, tile_verified(d, in, log2T), ft);
 }
 
 // Per decode warp: slots of SLOT_ROWS words per lane (a lane's run of LW
 // windows), the staging tile (32 LW windows x <= 32 or 64 symbols).
 template <int LW, int SLOT_ROWS>
 using FusedWarpSmem = WarpPipeSmem<SLOT_ROWS, 32 * LW * (SLOT_ROWS > 17 && LW == 4 ? 64 : 32) / 8 + 8>;
+// Byte-step variant: the staging tile only (the packed bytes are read from
+// L2 at write-back): SLOT_ROWS = 1.
+template <int LW, int SLOT_ROWS, bool FSM>
+using FusedWarpSmemF = std::conditional_t<FSM, WarpPipeSmem<1, 32 * LW * 32 / 8 + 8>, FusedWarpSmem<LW, SLOT_ROWS>>;
+
+// Warps after the decode warps: the MMA (control) warp and, in the byte-step
+// variant, a watcher warp that publishes A stages as their MMAs complete, so
+// the MMA lane never waits for its own MMAs (back-to-back K tiles).
+template <bool FSM>
+constexpr int extra_warps() { return FSM ? 2 : 1; }
 
 template <int LW, int SLOT_ROWS, bool WIDE, bool FSM = false>
-__global__ void __launch_bounds__((decode_warps<LW, SLOT_ROWS, WIDE, FSM>() + 1) * 32, 1) fused_gemm_kernel(const FusedArgs args) {
-  using WSm = FusedWarpSmem<LW, SLOT_ROWS>;
+__global__ void __launch_bounds__((decode_warps<LW, SLOT_ROWS, WIDE, FSM>() + extra_warps<FSM>()) * 32, 1)
+    fused_gemm_kernel(const FusedArgs args) {
+  using WSm = FusedWarpSmemF<LW, SLOT_ROWS, FSM>;
   constexpr int kDecodeWarps = decode_warps<LW, SLOT_ROWS, WIDE, FSM>();
-  constexpr int kThreadsF = (kDecodeWarps + 1) * 32;
+  constexpr int kThreadsF = (kDecodeWarps + extra_warps<FSM>()) * 32;
   constexpr int kCtrlWarp = kDecodeWarps;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -397,6 +409,59 @@ __global__ void __launch_bounds__((decode_warps<LW, SLOT_ROWS, WIDE, FSM>() + 1)
       if constexpr (FSM) ring_tile_fsm(d, cur, log2T, ws, R, lane, FsmAt{smem_addr(g_fsmf), smem_addr(g_cmf)});
       else ring_tile(d, cur, log2T, len_off, ws, R, lane);
       tile = next;
+    }
+  } else if (FSM && warp == kCtrlWarp + 1) {
+    // ---- watcher: A stage of tile t free once its MMAs completed (tcgen05.commit -> empty)
+    if (lane == 0) {
+      for (std::uint32_t t = 0; t < n_kt; ++t) {
+        const std::uint32_t s = t % args.stages_a;
+        mbar_wait_sleep(smem_addr(&g_empty[s]), (t / args.stages_a) & 1u, 64);
+        mbar_arrive(smem_addr(&g_free[s]), 1);
+        asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_addr(&g_consumed)), "r"(t + 1) : "memory");
+      }
+    }
+    __syncwarp();
+  } else if (FSM) {
+    // ---- control warp (byte-step variant): X tiles -> 2-stage B ring, MMAs back to back
+    const std::uint32_t idesc = (1u << 4) | (args.w_fmt << 7) | (0u << 10) | ((args.m_pad >> 3) << 17) | ((128u >> 4) << 24);
+    auto issue_x = [&](std::uint32_t t) {
+      const std::uint32_t bsl = t & 1u;
+      const std::uint32_t kt = (cta.tile0 + t) % KT;
+      const std::uint32_t bar = smem_addr(&g_bfull[bsl]);
+      asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(bar),
+                   "r"(b_bytes)
+                   : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       b_base + bsl * b_bytes),
+                   "l"(args.xt + static_cast<std::uint64_t>(kt) * b_bytes), "r"(b_bytes), "r"(bar)
+                   : "memory");
+    };
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // x_tiles_kernel: X tiles written, y zeroed
+    if (lane == 0 && n_kt) issue_x(0);
+    for (std::uint32_t t = 0; t < n_kt; ++t) {
+      const std::uint32_t bs = t & 1u;
+      const std::uint32_t g = cta.tile0 + t;
+      const std::uint32_t seg = g / KT - nt0;
+      const bool first_of_seg = t == 0 || g % KT == 0;
+      if (lane == 0 && t + 1 < n_kt) {
+        // X stage (t + 1) % 2 was last read by the MMAs of tile t - 1
+        if (t >= 1) mbar_wait(smem_addr(&g_empty[(t - 1) % args.stages_a]), ((t - 1) / args.stages_a) & 1u);
+        issue_x(t + 1);
+      }
+      mbar_wait_sleep(smem_addr(&g_bfull[bs]), (t >> 1) & 1u, 32);
+      const std::uint32_t s = t % args.stages_a;
+      mbar_wait_sleep(smem_addr(&g_full[s]), (t / args.stages_a) & 1u, 32);
+      tc_fence_after();
+      if (lane == 0) {
+        const std::uint32_t a_st = a_base + s * kTileElems, bdst = b_base + bs * b_bytes;
+#pragma unroll
+        for (std::uint32_t k = 0; k < 4; ++k)
+          mma_f8(tmem_d + seg * args.acc_cols, smem_desc(a_st + 32 * k), smem_desc(bdst + 32 * k), idesc,
+                 !(first_of_seg && k == 0));
+        tc_commit(smem_addr(&g_empty[s]));
+        if (t + 1 == n_kt) tc_commit(smem_addr(&g_done));
+      }
+      __syncwarp();
     }
   } else {
     // ---- control warp: X tiles -> B ring, one lane issues the MMAs
@@ -518,7 +583,9 @@ __global__ void x_tiles_kernel(const std::uint8_t* __restrict__ x, std::uint8_t*
 
 }  // namespace
 
-std::uint32_t fused_stages_b(std::uint32_t m_pad) { return m_pad > 128 ? ECF8_FUSED_WIDE_XSTAGES : 2u; }
+// X ring stages: two, except m > 128 with the round-1 decode warps (their
+// shared memory leaves room for one 32 KB X stage beside 3+ A stages)
+std::uint32_t fused_stages_b(std::uint32_t m_pad, bool fsm) { return m_pad > 128 && !fsm ? ECF8_FUSED_WIDE_XSTAGES : 2u; }
 
 // Decode-warp geometry for a tiled weight:
 //   Lmin >= 2, T <= 128: 4 windows per lane, 17 slot rows -- half-size warp
@@ -534,7 +601,7 @@ int fused_lane_windows(std::uint32_t T, std::uint32_t lmin) {
 
 template <int LW, int ROWS, bool WIDE, bool FSM = false>
 constexpr std::uint32_t warps_smem() {
-  return static_cast<std::uint32_t>(decode_warps<LW, ROWS, WIDE, FSM>() * sizeof(FusedWarpSmem<LW, ROWS>));
+  return static_cast<std::uint32_t>(decode_warps<LW, ROWS, WIDE, FSM>() * sizeof(FusedWarpSmemF<LW, ROWS, FSM>));
 }
 
 // All decode warps' pipeline state.
@@ -551,25 +618,25 @@ std::uint32_t fused_stages_a(std::uint32_t m_pad, std::uint32_t warp_smem, bool 
   // decode warps' pipeline state, B ring 2 x m_pad x 128 B, A ring stages x
   // 16 KB, 1 KB alignment slack
   const std::uint32_t budget = 232448 - (fsm ? 21 : 30) * 1024;
-  const std::uint32_t fixed = warp_smem + fused_stages_b(m_pad) * m_pad * 128 + 1024;
+  const std::uint32_t fixed = warp_smem + fused_stages_b(m_pad, fsm) * m_pad * 128 + 1024;
   const std::uint32_t s = fixed < budget ? (budget - fixed) / kTileElems : 0;
   return s > kMaxStagesA ? kMaxStagesA : s;
 }
 
-std::uint32_t fused_smem_bytes(std::uint32_t m_pad, std::uint32_t stages_a, std::uint32_t warp_smem) {
-  return 1024 + stages_a * kTileElems + fused_stages_b(m_pad) * m_pad * 128 + warp_smem;
+std::uint32_t fused_smem_bytes(std::uint32_t m_pad, std::uint32_t stages_a, std::uint32_t warp_smem, bool fsm) {
+  return 1024 + stages_a * kTileElems + fused_stages_b(m_pad, fsm) * m_pad * 128 + warp_smem;
 }
 
 template <int LW, int ROWS, bool WIDE, bool FSM = false>
 cudaError_t launch_lw(const FusedArgs& args, std::uint32_t n_cta, cudaStream_t s) {
-  const std::uint32_t smem = fused_smem_bytes(args.m_pad, args.stages_a, warps_smem<LW, ROWS, WIDE, FSM>());
+  const std::uint32_t smem = fused_smem_bytes(args.m_pad, args.stages_a, warps_smem<LW, ROWS, WIDE, FSM>(), FSM);
   cudaError_t e = cudaFuncSetAttribute(fused_gemm_kernel<LW, ROWS, WIDE, FSM>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   static const bool pdl = std::getenv("ECF8_NO_PDL") == nullptr;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(n_cta);
-  cfg.blockDim = dim3((decode_warps<LW, ROWS, WIDE, FSM>() + 1) * 32);
+  cfg.blockDim = dim3((decode_warps<LW, ROWS, WIDE, FSM>() + extra_warps<FSM>()) * 32);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -582,8 +649,8 @@ cudaError_t launch_lw(const FusedArgs& args, std::uint32_t n_cta, cudaStream_t s
 
 template <bool WIDE>
 cudaError_t launch_geometry(const FusedArgs& args, std::uint32_t n_cta, cudaStream_t s) {
-  if (fused_lane_windows(args.w.T, args.w.lmin) == 8) return launch_lw<8, 33, WIDE>(args, n_cta, s);
   if (args.fsm) return launch_lw<8, 33, WIDE, true>(args, n_cta, s);
+  if (fused_lane_windows(args.w.T, args.w.lmin) == 8) return launch_lw<8, 33, WIDE>(args, n_cta, s);
   return args.w.lmin >= 2 ? launch_lw<4, 17, WIDE>(args, n_cta, s) : launch_lw<4, 33, WIDE>(args, n_cta, s);
 }
 

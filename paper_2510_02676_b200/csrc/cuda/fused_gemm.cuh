@@ -43,9 +43,9 @@ struct FusedArgs {
 // the shared memory of one decode warp's pipeline (fused_gemm.cu).
 int fused_lane_windows(std::uint32_t T, std::uint32_t lmin);
 std::uint32_t fused_warp_smem(std::uint32_t T, std::uint32_t lmin, std::uint32_t m_pad, bool fsm);
-std::uint32_t fused_stages_b(std::uint32_t m_pad);
+std::uint32_t fused_stages_b(std::uint32_t m_pad, bool fsm);
 std::uint32_t fused_stages_a(std::uint32_t m_pad, std::uint32_t warp_smem, bool fsm);
-std::uint32_t fused_smem_bytes(std::uint32_t m_pad, std::uint32_t stages_a, std::uint32_t warp_smem);
+std::uint32_t fused_smem_bytes(std::uint32_t m_pad, std::uint32_t stages_a, std::uint32_t warp_smem, bool fsm);
 cudaError_t launch_fused_gemm(const FusedArgs& args, std::uint32_t n_cta, cudaStream_t s);
 
 }  // namespace ecf8::dev
