@@ -77,6 +77,13 @@ int ecf8_decode_host(const ecf8_sections *host, uint8_t *out, uint64_t out_len);
 int ecf8_decode_host_many(const ecf8_sections *const *host, uint8_t *const *outs, const uint64_t *out_lens,
                           int count);
 
+/* Page-lock / unlock a host buffer the host-span calls write into (the
+ * ReusableBuffer of decompress_streaming): device-to-host copies into it run
+ * at full PCIe rate instead of through a pageable bounce buffer.  Returns
+ * ECF8_OK also when the memory was already registered. */
+int ecf8_host_pin(void *p, uint64_t bytes);
+int ecf8_host_unpin(void *p);
+
 /* Replaces ecf8::decode_block (codec.cpp:201-254): decodes block `block`
  * into out[outpos[block], outpos[block+1]). out_len must be n_elem. */
 int ecf8_decode_block_host(const ecf8_sections *host, uint64_t block, uint8_t *out,

@@ -63,6 +63,12 @@ void ecf8_host_file_free(ecf8_host_file *f);
 /* decompress_streaming: container bytes -> raw file bytes (B200 decode). */
 int ecf8_host_decompress(const uint8_t *bytes, size_t len, uint8_t **out, size_t *out_len,
                          uint64_t *allocations, uint64_t *capacity);
+/* decompress_streaming into a caller sink: write(ctx, data, n) receives the
+ * raw file in order (a file descriptor, a socket, a counter).  Returns the
+ * first nonzero write() result as ECF8_EIO. */
+typedef int (*ecf8_write_fn)(void *ctx, const uint8_t *data, size_t n);
+int ecf8_host_decompress_to(const uint8_t *bytes, size_t len, ecf8_write_fn write, void *ctx,
+                            uint64_t *allocations, uint64_t *capacity);
 
 /* synth_raw data (container.cpp:482-495), bit-identical, on nthreads host
  * threads (SplitMix64 jump-ahead). fmt 0 = E4M3, 1 = E5M2. */

@@ -144,6 +144,9 @@ _SIGS = {
         C.c_int,
         [_P, C.c_size_t, C.POINTER(_P), C.POINTER(C.c_size_t), _U64P, _U64P],
     ),
+    "ecf8_host_decompress_to": (C.c_int, [_P, C.c_size_t, _P, _P, _U64P, _U64P]),
+    "ecf8_host_pin": (C.c_int, [_P, C.c_uint64]),
+    "ecf8_host_unpin": (C.c_int, [_P]),
     "ecf8_host_synth": (C.c_int, [C.c_double, C.c_double, C.c_uint64, C.c_uint64, C.c_int, _P, C.c_int]),
     "ecf8_host_max_threads": (C.c_int, []),
     "ecf8_host_make_stats": (C.c_int, [_P, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(EntropyReport)]),

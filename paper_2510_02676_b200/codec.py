@@ -311,6 +311,27 @@ def parse_container(data: bytes) -> Ecf8File:
     return Ecf8File(data)
 
 
+WRITE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t)
+
+
+def decompress_to(data: bytes, write) -> tuple[int, int]:
+    """decompress_streaming into a sink: write(memoryview) gets the raw file
+    in order (ecf8_host_decompress_to).  Returns (buffer_allocations, capacity)."""
+    buf = np.frombuffer(data, np.uint8)
+
+    def _w(_ctx, p, n):
+        try:
+            write(memoryview((C.c_uint8 * n).from_address(p)).cast("B"))
+            return 0
+        except Exception:  # surfaced as ECF8_EIO "sink write failed"
+            return 1
+
+    fn = WRITE_FN(_w)
+    a, cap = C.c_uint64(), C.c_uint64()
+    check(lib.ecf8_host_decompress_to(_ptr(buf), buf.size, C.cast(fn, C.c_void_p), None, C.byref(a), C.byref(cap)))
+    return a.value, cap.value
+
+
 def decompress(data: bytes) -> tuple[bytes, int, int]:
     """decompress_streaming: (raw file bytes, buffer_allocations, capacity)."""
     buf = np.frombuffer(data, np.uint8)

@@ -1160,4 +1160,31 @@ int ecf8_fused_layout_device(const uint8_t* d_in, uint64_t n, uint64_t k, uint8_
   });
 }
 
+int ecf8_host_pin(void* p, uint64_t bytes) {
+  return guarded([&]() -> int {
+    if (!p || !bytes) return ECF8_OK;
+    if (int rc = require_device()) return rc;
+    const cudaError_t e = cudaHostRegister(p, bytes, cudaHostRegisterDefault);
+    if (e == cudaErrorHostMemoryAlreadyRegistered) {
+      cudaGetLastError();
+      return ECF8_OK;
+    }
+    cu(e, "cudaHostRegister");
+    return ECF8_OK;
+  });
+}
+
+int ecf8_host_unpin(void* p) {
+  return guarded([&]() -> int {
+    if (!p) return ECF8_OK;
+    const cudaError_t e = cudaHostUnregister(p);
+    if (e == cudaErrorHostMemoryNotRegistered) {
+      cudaGetLastError();
+      return ECF8_OK;
+    }
+    cu(e, "cudaHostUnregister");
+    return ECF8_OK;
+  });
+}
+
 }  // extern "C"

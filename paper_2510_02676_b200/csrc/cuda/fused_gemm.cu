@@ -66,7 +66,13 @@ namespace {
 #define ECF8_FUSED_WIDE_XSTAGES 1
 #endif
 #ifndef ECF8_FUSED_FSM_WARPS
-#define ECF8_FUSED_FSM_WARPS 16
+#define ECF8_FUSED_FSM_WARPS 12
+#endif
+#ifndef ECF8_FUSED_GPK
+#define ECF8_FUSED_GPK 0  // 1: packed bytes read from L2 at write-back instead of staged (A/B: slower)
+#endif
+#ifndef ECF8_FUSED_WATCH
+#define ECF8_FUSED_WATCH 0  // 1: watcher warp + back-to-back MMAs + 2 X stages (A/B: slower at m = 256, fewer A stages)
 #endif
 // Byte-step variant: 8-window lanes, two chains each (direct_tile), 4.2 KB of
 // warp state (the staging tile): ECF8_FUSED_FSM_WARPS decode warps.
@@ -301,7 +307,7 @@ __device__ __forceinline__ void ring_tile_fsm(const TensorDesc& d, const WarpInT
   const std::uint64_t E = in.E < R.e1 ? in.E : R.e1;
   if (A >= E) return;
   RingOut out = ring_out(in.A, A, E, R, lane);
-  direct_tile<2, LW, true>(d, in, ws, lane, out, tile_verified(d, in, log2T), ft);
+  direct_tile<2, LW, ECF8_FUSED_GPK != 0>(d, in, ws, lane, out, tile_verified(d, in, log2T), ft);
 }
 
 // Per decode warp: slots of SLOT_ROWS words per lane (a lane's run of LW
@@ -311,13 +317,14 @@ using FusedWarpSmem = WarpPipeSmem<SLOT_ROWS, 32 * LW * (SLOT_ROWS > 17 && LW ==
 // Byte-step variant: the staging tile only (the packed bytes are read from
 // L2 at write-back): SLOT_ROWS = 1.
 template <int LW, int SLOT_ROWS, bool FSM>
-using FusedWarpSmemF = std::conditional_t<FSM, WarpPipeSmem<1, 32 * LW * 32 / 8 + 8>, FusedWarpSmem<LW, SLOT_ROWS>>;
+using FusedWarpSmemF =
+    std::conditional_t<FSM && ECF8_FUSED_GPK, WarpPipeSmem<1, 32 * LW * 32 / 8 + 8>, FusedWarpSmem<LW, SLOT_ROWS>>;
 
 // Warps after the decode warps: the MMA (control) warp and, in the byte-step
 // variant, a watcher warp that publishes A stages as their MMAs complete, so
 // the MMA lane never waits for its own MMAs (back-to-back K tiles).
 template <bool FSM>
-constexpr int extra_warps() { return FSM ? 2 : 1; }
+constexpr int extra_warps() { return FSM && ECF8_FUSED_WATCH ? 2 : 1; }
 
 template <int LW, int SLOT_ROWS, bool WIDE, bool FSM = false>
 __global__ void __launch_bounds__((decode_warps<LW, SLOT_ROWS, WIDE, FSM>() + extra_warps<FSM>()) * 32, 1)
@@ -410,7 +417,7 @@ __global__ void __launch_bounds__((decode_warps<LW, SLOT_ROWS, WIDE, FSM>() + ex
       else ring_tile(d, cur, log2T, len_off, ws, R, lane);
       tile = next;
     }
-  } else if (FSM && warp == kCtrlWarp + 1) {
+  } else if (FSM && ECF8_FUSED_WATCH && warp == kCtrlWarp + 1) {
     // ---- watcher: A stage of tile t free once its MMAs completed (tcgen05.commit -> empty)
     if (lane == 0) {
       for (std::uint32_t t = 0; t < n_kt; ++t) {
@@ -421,7 +428,7 @@ __global__ void __launch_bounds__((decode_warps<LW, SLOT_ROWS, WIDE, FSM>() + ex
       }
     }
     __syncwarp();
-  } else if (FSM) {
+  } else if (FSM && ECF8_FUSED_WATCH) {
     // ---- control warp (byte-step variant): X tiles -> 2-stage B ring, MMAs back to back
     const std::uint32_t idesc = (1u << 4) | (args.w_fmt << 7) | (0u << 10) | ((args.m_pad >> 3) << 17) | ((128u >> 4) << 24);
     auto issue_x = [&](std::uint32_t t) {
@@ -585,7 +592,9 @@ __global__ void x_tiles_kernel(const std::uint8_t* __restrict__ x, std::uint8_t*
 
 // X ring stages: two, except m > 128 with the round-1 decode warps (their
 // shared memory leaves room for one 32 KB X stage beside 3+ A stages)
-std::uint32_t fused_stages_b(std::uint32_t m_pad, bool fsm) { return m_pad > 128 && !fsm ? ECF8_FUSED_WIDE_XSTAGES : 2u; }
+std::uint32_t fused_stages_b(std::uint32_t m_pad, bool fsm) {
+  return m_pad > 128 && !(fsm && ECF8_FUSED_WATCH) ? ECF8_FUSED_WIDE_XSTAGES : 2u;
+}
 
 // Decode-warp geometry for a tiled weight:
 //   Lmin >= 2, T <= 128: 4 windows per lane, 17 slot rows -- half-size warp

@@ -275,6 +275,46 @@ int ecf8_host_fused_layout(const uint8_t* w, uint64_t n, uint64_t k, uint8_t* ou
   });
 }
 
+namespace {
+// std::streambuf forwarding to an ecf8_write_fn (decompress_streaming's ostream)
+class SinkBuf : public std::streambuf {
+ public:
+  SinkBuf(ecf8_write_fn w, void* ctx) : w_(w), ctx_(ctx) {}
+  int status() const { return rc_; }
+
+ protected:
+  std::streamsize xsputn(const char* s, std::streamsize n) override {
+    if (rc_ == 0 && n > 0) rc_ = w_(ctx_, reinterpret_cast<const uint8_t*>(s), static_cast<size_t>(n));
+    return rc_ == 0 ? n : 0;
+  }
+  int_type overflow(int_type c) override {
+    if (c == traits_type::eof()) return traits_type::not_eof(c);
+    const char ch = static_cast<char>(c);
+    return xsputn(&ch, 1) == 1 ? c : traits_type::eof();
+  }
+
+ private:
+  ecf8_write_fn w_;
+  void* ctx_;
+  int rc_ = 0;
+};
+}  // namespace
+
+int ecf8_host_decompress_to(const uint8_t* bytes, size_t len, ecf8_write_fn write, void* ctx, uint64_t* allocations,
+                            uint64_t* capacity) {
+  if (!write) return set_error(ECF8_EINVAL, "null sink");
+  SinkBuf buf(write, ctx);
+  int rc = guarded([&] {
+    const ecf8::Ecf8File f = ecf8::parse_container({bytes, len});
+    std::ostream os(&buf);
+    const ecf8::DecompressStats st = ecf8::decompress_streaming(f, os);
+    if (allocations) *allocations = st.buffer_allocations;
+    if (capacity) *capacity = st.buffer_capacity_bytes;
+  });
+  if (rc == ECF8_OK && buf.status() != 0) return set_error(ECF8_EIO, "sink write failed");
+  return rc;
+}
+
 int ecf8_host_synth(double alpha, double gamma, uint64_t n, uint64_t seed, int fmt, uint8_t* out,
                     int nthreads) {
   return guarded([&] {

@@ -294,3 +294,23 @@ def test_batch_decode_in_cuda_graph():
         torch.cuda.synchronize()
         for o, x in zip(outs, xs):
             assert np.array_equal(o.cpu().numpy(), x)
+
+
+def test_decompress_to_sink_matches_decompress():
+    # decompress_streaming into a caller sink (ecf8_host_decompress_to): same
+    # raw bytes, one buffer (pinned for the call), capacity = largest tensor
+    rng = np.random.default_rng(57)
+    tensors = [(f"t{i}", [n], codec.synth(1.8, 0.05, n, 70 + i)) for i, n in enumerate([5000, 0, 1_200_000, 77])]
+    raw = codec.raw_file(tensors)
+    blob = codec.compress_raw(raw, 256)
+    parts = []
+    allocs, cap = codec.decompress_to(blob, lambda mv: parts.append(bytes(mv)))
+    assert b"".join(parts) == raw and allocs == 1 and cap == 1_200_000
+    from paper_2510_02676_b200._lib import Ecf8Error
+
+    def bad(mv):
+        raise OSError("disk full")
+
+    with pytest.raises(Ecf8Error, match="sink write failed"):
+        codec.decompress_to(blob, bad)
+    assert rng is not None
