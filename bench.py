@@ -77,7 +77,7 @@ WORKLOADS = {
                              desc="llama3-70b fp8 linears (one layer), decode-fused tcgen05 FP8 GEMM, "
                                   "column TP over the ranks + NCCL all-gather"),
 }
-FUSED_MS = [1, 16, 64, 256]
+FUSED_MS = [int(v) for v in os.environ.get("ECF8_BENCH_FUSED_MS", "1,16,64,256").split(",")]
 
 
 def log(*a):
@@ -255,14 +255,14 @@ def kernel_name():
     return "decode_kernel<4,16,3>" if os.environ.get("ECF8_NO_WARP_KERNEL") == "1" else f"decode_warp_kernel<{nw}>"
 
 
-def load_traffic():
-    """Per-launch DRAM bytes of the decode kernel from the committed ncu capture."""
+def load_traffic(workload):
+    """Per-launch DRAM bytes of the decode kernel from the committed ncu capture of this workload."""
     p = os.path.join(ROOT, "profiles", "ncu_decode_summary.json")
     if not os.path.exists(p):
         return None
     with open(p) as f:
         d = json.load(f)
-    return d.get("dram_bytes_per_launch")
+    return d.get(workload, {}).get("dram_bytes_per_launch")
 
 
 def base_line(args, world, value, ms_per_step, workload_cfg):
@@ -655,7 +655,7 @@ def main():
     value = world * step_bytes * args.steps / (elapsed_ms * 1e-3) / 1e9
     per_launch_bytes = step_bytes / len(batches)
     achieved = per_launch_bytes / (statistics.mean(launch_ms) * 1e-3) / 1e9
-    traffic = load_traffic() if args.workload == "llama3.1-8b" else None
+    traffic = load_traffic(args.workload)
 
     # ---- e2e: host buffers through the drop-in C ABI call
     e2e = None

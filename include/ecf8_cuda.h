@@ -171,13 +171,12 @@ int ecf8_batch_launches(const ecf8_batch *b);
  *   y[m, n] = scale * sum_k x[m, k] * W[n, k]     (fp32 accumulate / out)
  * decodes W tile by tile into shared memory; decoded weights never reach
  * HBM.  x: m x k E4M3 row-major on the device (16-byte aligned), 1 <= m <=
- * 256; y: m x n fp32 row-major.  w_fmt: 0 = E4M3, 1 = E5M2 weights.  The
+ * 256; y: m x n fp32 row-major (16-byte aligned).  w_fmt: 0 = E4M3, 1 = E5M2 weights.  The
  * fused handle keeps a pointer to `t`, which must outlive it. */
 int ecf8_fused_create(const ecf8_dev_tensor *t, uint64_t n, uint64_t k, int w_fmt, ecf8_fused **out);
 int ecf8_fused_gemm(const ecf8_fused *f, const uint8_t *d_x, uint32_t m, float scale, float *d_y, void *stream);
 /* CTAs sharing one 128-row tile of W (rounded up): the launch is cut into
- * balanced runs of weight tiles for whole waves of the SMs; partial sums are
- * added into y. */
+ * balanced runs of weight tiles, one per SM; partial sums are added into y. */
 int ecf8_fused_split_k(const ecf8_fused *f);
 void ecf8_fused_free(ecf8_fused *f);
 /* ecf8_host_fused_layout on device memory, stream-ordered: row-major n x k

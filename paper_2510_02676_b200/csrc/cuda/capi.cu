@@ -1062,10 +1062,20 @@ int ecf8_fused_create(const ecf8_dev_tensor* t, uint64_t n, uint64_t k, int w_fm
         if (p.tile1 > p.tile0) m = std::max<std::uint32_t>(m, static_cast<std::uint32_t>((p.tile1 - 1) / KT - p.tile0 / KT + 1));
       return m;
     };
-    const std::uint32_t caps[2] = {2, 4};
+    // accumulators are reused round-robin within a CTA, so every plan is one
+    // wave (ECF8_FUSED_SEG_CAP: A/B runs with a segment cap instead)
+    static const std::uint32_t seg_cap = [] {
+      const char* e = std::getenv("ECF8_FUSED_SEG_CAP");
+      return e ? static_cast<std::uint32_t>(std::strtoul(e, nullptr, 10)) : 0u;
+    }();
+    const std::uint32_t caps[2] = {seg_cap ? seg_cap : ~0u, seg_cap ? seg_cap : ~0u};
     for (int i = 0; i < 2; ++i) {
       std::vector<ecf8::dev::FusedCta> plan;
-      for (std::uint64_t waves = 1;; ++waves) {
+      static const std::uint64_t min_waves = [] {  // A/B runs only
+        const char* e = std::getenv("ECF8_FUSED_MIN_WAVES");
+        return e ? std::max<std::uint64_t>(1, std::strtoull(e, nullptr, 10)) : std::uint64_t{1};
+      }();
+      for (std::uint64_t waves = min_waves;; ++waves) {
         plan = make_plan(std::min<std::uint64_t>(total, waves * static_cast<std::uint64_t>(sms)));
         if (segs(plan) <= caps[i] || plan.size() == total) break;
       }
@@ -1097,8 +1107,8 @@ int ecf8_fused_gemm(const ecf8_fused* f, const uint8_t* d_x, uint32_t m, float s
   return guarded([&]() -> int {
     if (!f || !d_x || !d_y) return fail(ECF8_EINVAL, "null argument");
     if (m == 0 || m > 256) return fail(ECF8_EINVAL, "fused GEMM supports 1 <= m <= 256 tokens");
-    if ((reinterpret_cast<std::uintptr_t>(d_x) & 15) || (reinterpret_cast<std::uintptr_t>(d_y) & 3))
-      return fail(ECF8_EINVAL, "x must be 16-byte aligned");
+    if ((reinterpret_cast<std::uintptr_t>(d_x) & 15) || (reinterpret_cast<std::uintptr_t>(d_y) & 15))
+      return fail(ECF8_EINVAL, "x and y must be 16-byte aligned");
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
     ecf8::dev::FusedArgs a{};
     a.w = f->w->desc;
@@ -1129,8 +1139,11 @@ int ecf8_fused_gemm(const ecf8_fused* f, const uint8_t* d_x, uint32_t m, float s
     if (a.stages_a < 2) return fail(ECF8_EINVAL, "fused GEMM: shared memory too small for this m");
     a.acc_cols = 32;
     while (a.acc_cols < a.m_pad) a.acc_cols <<= 1;
+    // one accumulator per n-tile segment of a CTA while they fit the 512
+    // TMEM columns; beyond that they are reused round-robin (flushed first)
     a.tmem_cols = 32;
-    while (a.tmem_cols < f->max_seg[pi] * a.acc_cols) a.tmem_cols <<= 1;
+    while (a.tmem_cols < f->max_seg[pi] * a.acc_cols && a.tmem_cols < 512) a.tmem_cols <<= 1;
+    a.acc_bufs = std::min<std::uint32_t>(a.tmem_cols / a.acc_cols, ecf8::dev::kMaxAccBufs);
     a.w_fmt = f->w_fmt;
     a.scale = scale;
     cu(ecf8::dev::launch_fused_gemm(a, f->n_cta[pi], st), "fused GEMM launch");

@@ -395,6 +395,9 @@ struct FsmAt {
 // entries (n4 in bits 0..4, bit 5 clear): bits 0..4 stay exact, bit 5
 // toggles when a word fills (the pair adds <= 32 bits: at most one word),
 // the state / symbol bits above collect garbage nothing reads.
+#ifndef ECF8_PUT2_PRED
+#define ECF8_PUT2_PRED 1
+#endif
 template <int WS>
 struct PairSink {
   std::uint32_t addr;  // next slot word
@@ -404,10 +407,26 @@ struct PairSink {
     const std::uint32_t q = q4 + e1 + e2;
     const std::uint32_t nl = lo | __funnelshift_l(0u, c, q4);  // c << (q4 % 32)
     const std::uint32_t nh = __funnelshift_l(c, 0u, q4);       // c >> (32 - q4 % 32)
+#if ECF8_PUT2_PRED
+    // one predicate for the store, the address step and the select (no
+    // 0 / WS materialisation)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t"
+        "xor.b32 t, %3, %4;\n\t"
+        "and.b32 t, t, 32;\n\t"
+        "setp.ne.u32 p, t, 0;\n\t"
+        "@p st.shared.u32 [%0], %5;\n\t"
+        "@p add.u32 %0, %0, %6;\n\t"
+        "selp.b32 %1, %2, %5, p;\n\t}"
+        : "+r"(addr), "=r"(lo)
+        : "r"(nh), "r"(q), "r"(q4), "r"(nl), "n"(WS)
+        : "memory");
+#else
     const bool full = ((q ^ q4) & 32u) != 0;
     if (full) sts32(addr, nl);
     addr += full ? WS : 0u;
     lo = full ? nh : nl;
+#endif
     q4 = q;
   }
   __device__ __forceinline__ std::uint32_t finish(std::uint32_t base) {

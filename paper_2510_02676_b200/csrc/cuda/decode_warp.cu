@@ -90,17 +90,30 @@ __device__ __forceinline__ void stage_fsm(const TensorDesc& d, int tid, int nthr
 #ifndef ECF8_WB_UNROLL
 #define ECF8_WB_UNROLL 4
 #endif
-constexpr int kWbUnroll = ECF8_WB_UNROLL;  // write-back chunks per lane and loop step
+constexpr int kWbUnroll = ECF8_WB_UNROLL;
+#ifndef ECF8_CLAIM_AHEAD
+#define ECF8_CLAIM_AHEAD 0  // 1: claim the next tile one tile early (A/B: slower)
+#endif  // write-back chunks per lane and loop step
 
 // Output to global memory (d.out).  Launched with programmatic stream
 // serialization, this grid may start while the previous one finishes; its
 // inputs are immutable, so only the stores wait for the previous grid (a
 // no-op once it has completed).
+#ifndef ECF8_STG
+#define ECF8_STG 1  // 0: generic stores (ptxas then keeps the write-back's shared loads behind them)
+#endif
 struct GlobalOut {
   std::uint8_t* base;  // element S0
   __device__ __forceinline__ void wait() const { asm volatile("griddepcontrol.wait;" ::: "memory"); }
   __device__ __forceinline__ void chunk(std::uint32_t c, const uint4& r) const {
+#if ECF8_STG
+    // st.global: a store ptxas knows cannot alias shared memory, so the next
+    // chunks' stage / packed loads may be issued ahead of it
+    asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(reinterpret_cast<uint4*>(base) + c), "r"(r.x),
+                 "r"(r.y), "r"(r.z), "r"(r.w));
+#else
     reinterpret_cast<uint4*>(base)[c] = r;
+#endif
   }
   __device__ __forceinline__ void byte(std::uint32_t i, std::uint8_t b) const { base[i] = b; }
   __device__ __forceinline__ void done() const {}
@@ -114,16 +127,25 @@ __device__ __forceinline__ void prefetch_l2(const void* p, std::uint64_t bytes) 
   const std::uint32_t n = static_cast<std::uint32_t>((reinterpret_cast<std::uintptr_t>(p) + bytes - a + 15) & ~std::uint64_t{15});
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(n) : "memory");
 }
-__device__ __forceinline__ void prefetch_tile_l2(const TensorDesc& d, std::uint64_t tile, std::uint32_t log2T) {
+// Lanes 0-4 issue one section each (the descriptor reads and the address
+// math run side by side instead of one after another).
+__device__ __forceinline__ void prefetch_tile_l2(const TensorDesc& d, std::uint64_t tile, std::uint32_t log2T,
+                                                 int lane) {
   const std::uint32_t m = 256u >> log2T;
   const std::uint64_t b0 = d.blk_begin + (tile - d.tile_begin) * m;
   const std::uint64_t nb = d.blk_end - b0 < m ? d.blk_end - b0 : m;
   const std::uint64_t w0 = b0 << log2T, nw = nb << log2T;
-  prefetch_l2(d.encoded + 8 * w0, 8 * nw + 8);
-  prefetch_l2(d.gaps + (w0 >> 1), nw >> 1);
-  prefetch_l2(d.outpos + b0, 8 * (nb + 1));
-  if (d.endgap) prefetch_l2(d.endgap + (w0 >> 1), nw >> 1);
-  if (d.lane_start) prefetch_l2(d.lane_start + (w0 >> 2), nw >> 1);
+  const void* p = nullptr;
+  std::uint64_t n = 0;
+  switch (lane) {
+    case 0: p = d.encoded + 8 * w0, n = 8 * nw + 8; break;
+    case 1: p = d.gaps + (w0 >> 1), n = nw >> 1; break;
+    case 2: p = d.outpos + b0, n = 8 * (nb + 1); break;
+    case 3: p = d.endgap ? d.endgap + (w0 >> 1) : nullptr, n = nw >> 1; break;
+    case 4: p = d.lane_start ? reinterpret_cast<const void*>(d.lane_start + (w0 >> 2)) : nullptr, n = nw >> 1; break;
+    default: break;
+  }
+  if (p && n) prefetch_l2(p, n);
 }
 
 // One tile: decode + scan, compact, write back.
@@ -233,19 +255,41 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_warp_kernel(const LaunchArg
         tile = next;
       }
     } else {
-      if (tile < seg_end && lane == 0) prefetch_tile_l2(d, tile, log2T);
+#if ECF8_CLAIM_AHEAD
+      // The tile after `tile` is claimed one tile early, so the claim's
+      // shared atomic completes while a tile decodes; its sections go to L2
+      // at the end of the tile before it (a tile of lead).  Claims are held
+      // as 32-bit offsets from seg (one register).
+      const std::uint32_t n_rel = static_cast<std::uint32_t>(seg_end - seg);
+      if (tile < seg_end && lane < 5) prefetch_tile_l2(d, tile, log2T, lane);
+      unsigned claim = 0;
+      if (lane == 0) claim = atomicAdd(&next_tile, 1u);
+      std::uint32_t next = __shfl_sync(0xffffffffu, claim, 0);
+      if (next < n_rel && lane < 5) prefetch_tile_l2(d, seg + next, log2T, lane);
+      while (tile < seg_end) {
+        WarpIn cur;
+        load_warp_tile<kLaneWin, true>(d, tile, log2T, lane, cur);
+        unsigned claim2 = 0;
+        if (lane == 0 && next < n_rel) claim2 = atomicAdd(&next_tile, 1u);
+        warp_tile<WIDE>(d, cur, log2T, len_off, ws, lane);
+        const std::uint32_t next2 = next < n_rel ? __shfl_sync(0xffffffffu, claim2, 0) : n_rel;
+        if (next2 < n_rel && lane < 5) prefetch_tile_l2(d, seg + next2, log2T, lane);
+        tile = seg + next;
+        next = next2;
+      }
+#else
+      if (tile < seg_end && lane < 5) prefetch_tile_l2(d, tile, log2T, lane);
       while (tile < seg_end) {
         WarpIn cur;
         load_warp_tile<kLaneWin, true>(d, tile, log2T, lane, cur);
         unsigned claim = 0;
-        if (lane == 0) {
-          claim = atomicAdd(&next_tile, 1u);
-          if (seg + claim < seg_end) prefetch_tile_l2(d, seg + claim, log2T);
-        }
+        if (lane == 0) claim = atomicAdd(&next_tile, 1u);
         const std::uint64_t next = seg + __shfl_sync(0xffffffffu, claim, 0);
+        if (next < seg_end && lane < 5) prefetch_tile_l2(d, next, log2T, lane);
         warp_tile<WIDE>(d, cur, log2T, len_off, ws, lane);
         tile = next;
       }
+#endif
     }
     seg = seg_end;
   }

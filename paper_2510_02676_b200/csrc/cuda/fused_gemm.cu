@@ -65,22 +65,39 @@ namespace {
 #ifndef ECF8_FUSED_WIDE_XSTAGES
 #define ECF8_FUSED_WIDE_XSTAGES 1
 #endif
+#ifndef ECF8_FUSED_FSM_WIDE_WARPS
+#define ECF8_FUSED_FSM_WIDE_WARPS 12  // m > 128
+#endif
+#ifndef ECF8_FUSED_FSM_WIDE_XSTAGES
+#define ECF8_FUSED_FSM_WIDE_XSTAGES 1
+#endif
 #ifndef ECF8_FUSED_FSM_WARPS
 #define ECF8_FUSED_FSM_WARPS 12
 #endif
 #ifndef ECF8_FUSED_GPK
 #define ECF8_FUSED_GPK 0  // 1: packed bytes read from L2 at write-back instead of staged (A/B: slower)
 #endif
-#ifndef ECF8_FUSED_WATCH
-#define ECF8_FUSED_WATCH 0  // 1: watcher warp + back-to-back MMAs + 2 X stages (A/B: slower at m = 256, fewer A stages)
+#ifndef ECF8_FUSED_CHAIN
+#define ECF8_FUSED_CHAIN 1  // consecutive fused GEMMs overlap (x_tiles_kernel as a programmatic dependent)
+#endif
+#ifndef ECF8_FUSED_XPROBE
+#define ECF8_FUSED_XPROBE 0
+#endif
+#ifndef ECF8_FUSED_MMAPROBE
+#define ECF8_FUSED_MMAPROBE 0
+#endif
+#ifndef ECF8_FUSED_EPI
+#define ECF8_FUSED_EPI 1  // 0: timing experiment without the epilogue's y updates (wrong results)
 #endif
 // Byte-step variant: 8-window lanes, two chains each (direct_tile), 4.2 KB of
 // warp state (the staging tile): ECF8_FUSED_FSM_WARPS decode warps.
 template <int LW, int ROWS, bool WIDE, bool FSM = false>
 constexpr int decode_warps() {
-  return FSM ? ECF8_FUSED_FSM_WARPS : ROWS > 17 ? 12 : (WIDE ? ECF8_FUSED_WIDE_WARPS : ECF8_FUSED_WARPS);
+  return FSM ? (WIDE ? ECF8_FUSED_FSM_WIDE_WARPS : ECF8_FUSED_FSM_WARPS)
+             : ROWS > 17 ? 12 : (WIDE ? ECF8_FUSED_WIDE_WARPS : ECF8_FUSED_WARPS);
 }
 constexpr std::uint32_t kTileElems = 128 * 128;  // one K tile of A (bytes)
+
 
 __shared__ Tables g_tbf;
 __shared__ alignas(16) std::uint32_t g_fsmf[256 * kFsmStates];  // byte-step variant: its tables
@@ -91,7 +108,9 @@ __shared__ alignas(8) unsigned long long g_full[kMaxStagesA];
 __shared__ alignas(8) unsigned long long g_empty[kMaxStagesA];  // arrived by tcgen05.commit (MMAs done)
 __shared__ alignas(8) unsigned long long g_free[kMaxStagesA];   // arrived by the MMA lane once it saw g_empty
 __shared__ alignas(8) unsigned long long g_bfull[2];
-__shared__ alignas(8) unsigned long long g_done;
+__shared__ alignas(8) unsigned long long g_segdone[kMaxAccBufs];  // arrived by tcgen05.commit after a segment's last MMA
+__shared__ alignas(8) unsigned long long g_accfree[kMaxAccBufs];  // arrived by the 4 flushing warps once they read it
+__shared__ std::uint32_t g_nflush[4];  // per flushing warp: the next segment it flushes
 __shared__ std::uint32_t g_tmem;
 __shared__ std::uint32_t g_consumed;  // K tiles whose MMAs have completed (stage reusable)
 
@@ -132,6 +151,31 @@ __device__ __forceinline__ void mbar_wait_sleep(std::uint32_t bar, std::uint32_t
     if (ok) return;
     __nanosleep(ns);
   }
+}
+
+__device__ __forceinline__ std::uint32_t mbar_try(std::uint32_t bar, std::uint32_t parity) {
+  std::uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok;
+}
+
+// Non-blocking probe (test_wait; try_wait may suspend the thread for a while).
+__device__ __forceinline__ std::uint32_t mbar_test(std::uint32_t bar, std::uint32_t parity) {
+  std::uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok;
 }
 
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
@@ -176,10 +220,12 @@ __device__ __forceinline__ void tmem_ld8(std::uint32_t taddr, float (&v)[8]) {
 
 // ---- decode warps: one ECF8 tile -> FP8 bytes in the A ring ---------------
 
+struct Flush;
 struct Ring {
   std::uint32_t a_base;  // shared address of A stage 0 (1024-aligned)
   std::uint32_t stages;  // A stages
   std::uint64_t e0, e1;  // CTA element range (tile-major), multiples of 16384
+  const Flush* fl;       // this warp's accumulator flushes (polled while waiting)
 };
 
 // Writers of K tile t need stage t % S back from the MMAs of tile t - S
@@ -192,8 +238,76 @@ struct Ring {
 // alias a completion two phases back; the control warp's monotonic count of
 // consumed K tiles first guarantees the barrier is at most one phase behind
 // (tile t - 2S consumed), then the parity wait does the rest.
-__device__ __forceinline__ void wait_stage_free(const Ring& R, std::uint32_t t) {
+// ---- accumulator flushes: partial rows of finished n-tile segments -> y
+//
+// A CTA's run covers segments s = 0 .. nseg-1 (n-tiles), accumulated in
+// TMEM buffer s % nb (nb = accumulator buffers that fit the 512 columns).
+// The MMA lane commits g_segdone[b] after a segment's last MMA; warps 0-3
+// (one TMEM lane quadrant each) read the buffer with tcgen05.ld, add the
+// partial rows into y, and arrive on g_accfree[b], which the MMA lane waits
+// for before it starts segment s + nb in the same buffer.  Warps 0-3 flush
+// between their decode tiles and while they wait for ring stages, so a
+// segment's epilogue overlaps the decode of the next ones; only the last
+// segment is flushed after the CTA's decode work.
+struct Flush {
+  float* y;
+  std::uint32_t n, m, nb, acc_cols, tmem_d, nt0, nseg;
+  float scale;
+  int warp, lane;
+
+  __device__ __forceinline__ void segment(std::uint32_t sg) const {
+    const std::uint32_t b = sg % nb;
+    const std::uint32_t row = static_cast<std::uint32_t>(warp) * 32 + static_cast<std::uint32_t>(lane);
+    const std::uint64_t col = static_cast<std::uint64_t>(nt0 + sg) * 128 + row;
+    const std::uint32_t tq = tmem_d + b * acc_cols + (static_cast<std::uint32_t>(warp * 32) << 16);
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // y zeroed by x_tiles_kernel (returns at once after)
+    for (std::uint32_t c0 = 0; c0 < m; c0 += 8) {
+      float v[8];
+      tmem_ld8(tq + c0, v);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const std::uint32_t mcol = c0 + j;
+#if ECF8_FUSED_EPI
+        if (mcol < m) atomicAdd(y + static_cast<std::uint64_t>(mcol) * n + col, v[j] * scale);
+#else
+        if (mcol < m && v[j] == 12345.f) y[0] = 0.f;  // timing experiment only: no y updates
+#endif
+      }
+    }
+  }
+  // Flush every finished segment (block: wait for each until all are done).
+  __device__ __forceinline__ void run(bool block) const {
+    if (warp >= 4) return;
+    for (;;) {
+      const std::uint32_t f = g_nflush[warp];
+      if (f >= nseg) return;
+      const std::uint32_t bar = smem_addr(&g_segdone[f % nb]), par = (f / nb) & 1u;
+      if (block) mbar_wait(bar, par);
+      else if (!__all_sync(0xffffffffu, mbar_test(bar, par))) return;
+      tc_fence_after();
+      segment(f);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(smem_addr(&g_accfree[f % nb]), 1);
+        g_nflush[warp] = f + 1;
+      }
+      __syncwarp();
+    }
+  }
+  __device__ __forceinline__ void operator()() const { run(false); }
+};
+
+#ifndef ECF8_FUSED_MIDFLUSH
+#define ECF8_FUSED_MIDFLUSH 1
+#endif
+#ifndef ECF8_FUSED_POLL
+#define ECF8_FUSED_POLL 1  // 0: A/B only (no flushes while waiting: deadlocks when accumulators are reused)
+#endif
+template <class Poll>
+__device__ __forceinline__ void wait_stage_free(const Ring& R, std::uint32_t t, const Poll& poll) {
   if (t < R.stages) return;
+#if !ECF8_FUSED_POLL
   if (t >= 2 * R.stages) {
     const std::uint32_t need = t - 2 * R.stages + 1;
     const std::uint32_t addr = smem_addr(&g_consumed);
@@ -205,6 +319,24 @@ __device__ __forceinline__ void wait_stage_free(const Ring& R, std::uint32_t t) 
     }
   }
   mbar_wait_sleep(smem_addr(&g_free[t % R.stages]), ((t / R.stages) - 1) & 1u, 128);
+  return;
+#endif
+  if (t >= 2 * R.stages) {
+    const std::uint32_t need = t - 2 * R.stages + 1;
+    const std::uint32_t addr = smem_addr(&g_consumed);
+    while (true) {
+      std::uint32_t v;
+      asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+      if (__all_sync(0xffffffffu, v >= need)) break;
+      poll();
+      __nanosleep(128);
+    }
+  }
+  const std::uint32_t bar = smem_addr(&g_free[t % R.stages]), par = ((t / R.stages) - 1) & 1u;
+  while (!__all_sync(0xffffffffu, mbar_try(bar, par))) {
+    poll();
+    __nanosleep(128);
+  }
 }
 
 // Output into the A ring: element g of the CTA range [e0, e1) lands in ring
@@ -224,8 +356,8 @@ struct RingOut {
   int lane;
 
   __device__ __forceinline__ void wait() const {
-    wait_stage_free(*R, tf);
-    if (bl) wait_stage_free(*R, tf + 1);
+    wait_stage_free(*R, tf, *R->fl);
+    if (bl) wait_stage_free(*R, tf + 1, *R->fl);
   }
   __device__ __forceinline__ void chunk(std::uint32_t c, const uint4& r) const {
     if (c < c_lo || c >= c_hi) return;
@@ -320,11 +452,9 @@ template <int LW, int SLOT_ROWS, bool FSM>
 using FusedWarpSmemF =
     std::conditional_t<FSM && ECF8_FUSED_GPK, WarpPipeSmem<1, 32 * LW * 32 / 8 + 8>, FusedWarpSmem<LW, SLOT_ROWS>>;
 
-// Warps after the decode warps: the MMA (control) warp and, in the byte-step
-// variant, a watcher warp that publishes A stages as their MMAs complete, so
-// the MMA lane never waits for its own MMAs (back-to-back K tiles).
+// Warps after the decode warps: the MMA (control) warp.
 template <bool FSM>
-constexpr int extra_warps() { return FSM && ECF8_FUSED_WATCH ? 2 : 1; }
+constexpr int extra_warps() { return 1; }
 
 template <int LW, int SLOT_ROWS, bool WIDE, bool FSM = false>
 __global__ void __launch_bounds__((decode_warps<LW, SLOT_ROWS, WIDE, FSM>() + extra_warps<FSM>()) * 32, 1)
@@ -335,6 +465,9 @@ __global__ void __launch_bounds__((decode_warps<LW, SLOT_ROWS, WIDE, FSM>() + ex
   constexpr int kCtrlWarp = kDecodeWarps;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#if ECF8_FUSED_CHAIN
+  asm volatile("griddepcontrol.launch_dependents;");  // the next call's x_tiles_kernel may queue now
+#endif
   const FusedCta cta = args.plan[blockIdx.x];
   const std::uint32_t n_kt = cta.tile1 - cta.tile0;
   const std::uint32_t KT = args.k / 128;
@@ -373,10 +506,14 @@ __global__ void __launch_bounds__((decode_warps<LW, SLOT_ROWS, WIDE, FSM>() + ex
       }
       mbar_init(smem_addr(&g_bfull[0]), 1);
       mbar_init(smem_addr(&g_bfull[1]), 1);
-      mbar_init(smem_addr(&g_done), 1);
+      for (std::uint32_t b = 0; b < args.acc_bufs; ++b) {
+        mbar_init(smem_addr(&g_segdone[b]), 1);
+        mbar_init(smem_addr(&g_accfree[b]), 4);
+      }
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       g_qnext = kDecodeWarps;
       g_consumed = 0;
+      for (int w = 0; w < 4; ++w) g_nflush[w] = 0;
     }
   }
   if constexpr (FSM) {
@@ -392,9 +529,12 @@ __global__ void __launch_bounds__((decode_warps<LW, SLOT_ROWS, WIDE, FSM>() + ex
   tc_fence_after();
   const std::uint32_t tmem_d = g_tmem;
 
+  const std::uint32_t nseg = n_kt ? (cta.tile1 - 1) / KT - nt0 + 1 : 0;
+  const Flush fl{args.y, args.n, args.m, args.acc_bufs, args.acc_cols, tmem_d, nt0, nseg, args.scale, warp, lane};
+
   if (warp < kDecodeWarps) {
     // ---- decode warps: dynamic queue over the CTA's ECF8 tiles, in order
-    const Ring R{a_base, args.stages_a, cta.e0, cta.e1};
+    const Ring R{a_base, args.stages_a, cta.e0, cta.e1, &fl};
     const std::uint32_t len_off = (d.n_luts - 1) << 8;
     WSm& ws = wsm[warp];
     WarpInT<LW> nxt;
@@ -415,61 +555,12 @@ __global__ void __launch_bounds__((decode_warps<LW, SLOT_ROWS, WIDE, FSM>() + ex
       if (next < n_tiles) load_warp_tile<LW, FSM>(d, next, log2T, lane, nxt);
       if constexpr (FSM) ring_tile_fsm(d, cur, log2T, ws, R, lane, FsmAt{smem_addr(g_fsmf), smem_addr(g_cmf)});
       else ring_tile(d, cur, log2T, len_off, ws, R, lane);
+#if ECF8_FUSED_MIDFLUSH
+      fl.run(false);  // warps 0-3: flush the segments the MMAs have finished
+#endif
       tile = next;
     }
-  } else if (FSM && ECF8_FUSED_WATCH && warp == kCtrlWarp + 1) {
-    // ---- watcher: A stage of tile t free once its MMAs completed (tcgen05.commit -> empty)
-    if (lane == 0) {
-      for (std::uint32_t t = 0; t < n_kt; ++t) {
-        const std::uint32_t s = t % args.stages_a;
-        mbar_wait_sleep(smem_addr(&g_empty[s]), (t / args.stages_a) & 1u, 64);
-        mbar_arrive(smem_addr(&g_free[s]), 1);
-        asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_addr(&g_consumed)), "r"(t + 1) : "memory");
-      }
-    }
-    __syncwarp();
-  } else if (FSM && ECF8_FUSED_WATCH) {
-    // ---- control warp (byte-step variant): X tiles -> 2-stage B ring, MMAs back to back
-    const std::uint32_t idesc = (1u << 4) | (args.w_fmt << 7) | (0u << 10) | ((args.m_pad >> 3) << 17) | ((128u >> 4) << 24);
-    auto issue_x = [&](std::uint32_t t) {
-      const std::uint32_t bsl = t & 1u;
-      const std::uint32_t kt = (cta.tile0 + t) % KT;
-      const std::uint32_t bar = smem_addr(&g_bfull[bsl]);
-      asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(bar),
-                   "r"(b_bytes)
-                   : "memory");
-      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                       b_base + bsl * b_bytes),
-                   "l"(args.xt + static_cast<std::uint64_t>(kt) * b_bytes), "r"(b_bytes), "r"(bar)
-                   : "memory");
-    };
-    asm volatile("griddepcontrol.wait;" ::: "memory");  // x_tiles_kernel: X tiles written, y zeroed
-    if (lane == 0 && n_kt) issue_x(0);
-    for (std::uint32_t t = 0; t < n_kt; ++t) {
-      const std::uint32_t bs = t & 1u;
-      const std::uint32_t g = cta.tile0 + t;
-      const std::uint32_t seg = g / KT - nt0;
-      const bool first_of_seg = t == 0 || g % KT == 0;
-      if (lane == 0 && t + 1 < n_kt) {
-        // X stage (t + 1) % 2 was last read by the MMAs of tile t - 1
-        if (t >= 1) mbar_wait(smem_addr(&g_empty[(t - 1) % args.stages_a]), ((t - 1) / args.stages_a) & 1u);
-        issue_x(t + 1);
-      }
-      mbar_wait_sleep(smem_addr(&g_bfull[bs]), (t >> 1) & 1u, 32);
-      const std::uint32_t s = t % args.stages_a;
-      mbar_wait_sleep(smem_addr(&g_full[s]), (t / args.stages_a) & 1u, 32);
-      tc_fence_after();
-      if (lane == 0) {
-        const std::uint32_t a_st = a_base + s * kTileElems, bdst = b_base + bs * b_bytes;
-#pragma unroll
-        for (std::uint32_t k = 0; k < 4; ++k)
-          mma_f8(tmem_d + seg * args.acc_cols, smem_desc(a_st + 32 * k), smem_desc(bdst + 32 * k), idesc,
-                 !(first_of_seg && k == 0));
-        tc_commit(smem_addr(&g_empty[s]));
-        if (t + 1 == n_kt) tc_commit(smem_addr(&g_done));
-      }
-      __syncwarp();
-    }
+    fl.run(true);  // warps 0-3: the remaining segments
   } else {
     // ---- control warp: X tiles -> B ring, one lane issues the MMAs
     const std::uint32_t idesc = (1u << 4)                       // D = f32
@@ -483,6 +574,10 @@ __global__ void __launch_bounds__((decode_warps<LW, SLOT_ROWS, WIDE, FSM>() + ex
       const std::uint32_t bsl = t % args.stages_b;
       const std::uint32_t kt = (cta.tile0 + t) % KT;
       const std::uint32_t bar = smem_addr(&g_bfull[bsl]);
+#if ECF8_FUSED_XPROBE  // timing experiment: X tiles not loaded (wrong results)
+      (void)kt;
+      mbar_arrive(bar, 1);
+#else
       asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(bar),
                    "r"(b_bytes)
                    : "memory");
@@ -490,6 +585,7 @@ __global__ void __launch_bounds__((decode_warps<LW, SLOT_ROWS, WIDE, FSM>() + ex
                        b_base + bsl * b_bytes),
                    "l"(args.xt + static_cast<std::uint64_t>(kt) * b_bytes), "r"(b_bytes), "r"(bar)
                    : "memory");
+#endif
     };
     asm volatile("griddepcontrol.wait;" ::: "memory");  // x_tiles_kernel: X tiles written, y zeroed
     if (lane == 0 && n_kt) issue_x(0);
@@ -498,11 +594,17 @@ __global__ void __launch_bounds__((decode_warps<LW, SLOT_ROWS, WIDE, FSM>() + ex
       const std::uint32_t bdst = b_base + bs * b_bytes;
       const std::uint32_t g = cta.tile0 + t;
       const std::uint32_t seg = g / KT - nt0;
+      const std::uint32_t buf = seg % args.acc_bufs;
       const bool first_of_seg = t == 0 || g % KT == 0;
+      const bool last_of_seg = t + 1 == n_kt || (g + 1) % KT == 0;
       // two B stages: next K tile's X into the other stage now (its previous
       // reader, the MMAs of tile t-1, completed: waited on at the end of
       // iteration t-1); one stage (m_pad > 128): after this tile's MMAs
       if (lane == 0 && args.stages_b == 2 && t + 1 < n_kt) issue_x(t + 1);
+      // segment seg reuses the accumulator of segment seg - acc_bufs: wait
+      // until warps 0-3 have read it out
+      if (first_of_seg && seg >= args.acc_bufs)
+        mbar_wait_sleep(smem_addr(&g_accfree[buf]), ((seg / args.acc_bufs) - 1) & 1u, 32);
       mbar_wait_sleep(smem_addr(&g_bfull[bs]), (t / args.stages_b) & 1u, 32);
       const std::uint32_t s = t % args.stages_a;
       mbar_wait_sleep(smem_addr(&g_full[s]), (t / args.stages_a) & 1u, 32);
@@ -511,10 +613,13 @@ __global__ void __launch_bounds__((decode_warps<LW, SLOT_ROWS, WIDE, FSM>() + ex
         const std::uint32_t a_st = a_base + s * kTileElems;
 #pragma unroll
         for (std::uint32_t k = 0; k < 4; ++k)
-          mma_f8(tmem_d + seg * args.acc_cols, smem_desc(a_st + 32 * k), smem_desc(bdst + 32 * k), idesc,
+#if ECF8_FUSED_MMAPROBE  // timing experiment: one K = 32 MMA per tile (wrong results)
+          if (k == 0)
+#endif
+          mma_f8(tmem_d + buf * args.acc_cols, smem_desc(a_st + 32 * k), smem_desc(bdst + 32 * k), idesc,
                  !(first_of_seg && k == 0));
         tc_commit(smem_addr(&g_empty[s]));
-        if (t + 1 == n_kt) tc_commit(smem_addr(&g_done));
+        if (last_of_seg) tc_commit(smem_addr(&g_segdone[buf]));
         // the MMAs of tile t have read stage s: publish it to the decode warps
         mbar_wait(smem_addr(&g_empty[s]), (t / args.stages_a) & 1u);
         mbar_arrive(smem_addr(&g_free[s]), 1);
@@ -526,28 +631,6 @@ __global__ void __launch_bounds__((decode_warps<LW, SLOT_ROWS, WIDE, FSM>() + ex
     }
   }
 
-  // ---- epilogue: warps 0-3 own TMEM lanes 32w .. 32w+31 (= W rows); one
-  //      accumulator block per n-tile segment, partial sums added into y
-  if (warp < 4) {
-    mbar_wait(smem_addr(&g_done), 0);
-    asm volatile("griddepcontrol.wait;" ::: "memory");  // y zeroed (returns at once: the MMAs waited)
-    tc_fence_after();
-    const std::uint32_t row = warp * 32 + lane;
-    const std::uint32_t nseg = (cta.tile1 - 1) / KT - nt0 + 1;
-    for (std::uint32_t sg = 0; sg < nseg; ++sg) {
-      const std::uint64_t n = static_cast<std::uint64_t>(nt0 + sg) * 128 + row;
-      const std::uint32_t tq = tmem_d + sg * args.acc_cols + (static_cast<std::uint32_t>(warp * 32) << 16);
-      for (std::uint32_t c0 = 0; c0 < args.m; c0 += 8) {
-        float v[8];
-        tmem_ld8(tq + c0, v);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const std::uint32_t mcol = c0 + j;
-          if (mcol < args.m) atomicAdd(args.y + static_cast<std::uint64_t>(mcol) * args.n + n, v[j] * args.scale);
-        }
-      }
-    }
-  }
   tc_fence_before();
   __syncthreads();
   if (warp == kCtrlWarp) {
@@ -565,6 +648,11 @@ __global__ void __launch_bounds__((decode_warps<LW, SLOT_ROWS, WIDE, FSM>() + ex
 __global__ void x_tiles_kernel(const std::uint8_t* __restrict__ x, std::uint8_t* __restrict__ xt, std::uint32_t m,
                                std::uint32_t m_pad, std::uint32_t k, float* __restrict__ y, std::uint64_t y_elems) {
   asm volatile("griddepcontrol.launch_dependents;");
+  // Launched as a programmatic dependent of whatever precedes it (typically
+  // the previous fused GEMM, whose tail -- last flushes, pipeline drain --
+  // then overlaps this call's start and the next GEMM's decode warps): x and
+  // y may be the previous kernel's output / input, so wait for it first.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * blockDim.x;
   const std::uint64_t tid = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
   if ((reinterpret_cast<std::uintptr_t>(y) & 15) == 0) {
@@ -593,7 +681,8 @@ __global__ void x_tiles_kernel(const std::uint8_t* __restrict__ x, std::uint8_t*
 // X ring stages: two, except m > 128 with the round-1 decode warps (their
 // shared memory leaves room for one 32 KB X stage beside 3+ A stages)
 std::uint32_t fused_stages_b(std::uint32_t m_pad, bool fsm) {
-  return m_pad > 128 && !(fsm && ECF8_FUSED_WATCH) ? ECF8_FUSED_WIDE_XSTAGES : 2u;
+  if (m_pad <= 128) return 2u;
+  return fsm ? ECF8_FUSED_FSM_WIDE_XSTAGES : ECF8_FUSED_WIDE_XSTAGES;
 }
 
 // Decode-warp geometry for a tiled weight:
@@ -666,9 +755,22 @@ cudaError_t launch_geometry(const FusedArgs& args, std::uint32_t n_cta, cudaStre
 cudaError_t launch_fused_gemm(const FusedArgs& args, std::uint32_t n_cta, cudaStream_t s) {
   const std::uint64_t chunks = static_cast<std::uint64_t>(args.k / 128) * args.m_pad * 8;
   const unsigned blocks = static_cast<unsigned>(std::min<std::uint64_t>((chunks + 255) / 256, 4 * 148));
-  x_tiles_kernel<<<blocks, 256, 0, s>>>(args.x, const_cast<std::uint8_t*>(args.xt), args.m, args.m_pad, args.k, args.y,
-                                       static_cast<std::uint64_t>(args.m) * args.n);
-  if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) return e;
+  {
+    static const bool pdl = std::getenv("ECF8_NO_PDL") == nullptr;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(blocks);
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl && ECF8_FUSED_CHAIN ? 1 : 0;
+    if (cudaError_t e = cudaLaunchKernelEx(&cfg, x_tiles_kernel, args.x, const_cast<std::uint8_t*>(args.xt), args.m,
+                                           args.m_pad, args.k, args.y, static_cast<std::uint64_t>(args.m) * args.n);
+        e != cudaSuccess)
+      return e;
+  }
   return args.m_pad > 128 ? launch_geometry<true>(args, n_cta, s) : launch_geometry<false>(args, n_cta, s);
 }
 

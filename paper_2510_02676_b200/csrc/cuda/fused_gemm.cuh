@@ -10,10 +10,11 @@
 namespace ecf8::dev {
 
 constexpr std::uint32_t kMaxStagesA = 8;
+constexpr std::uint32_t kMaxAccBufs = 16;  // TMEM accumulator buffers (512 columns / 32)
 
 // One CTA's work: the contiguous run of 128x128 weight tiles [tile0, tile1)
-// in tile-major (nt, kt) order -- at most two n-tiles ("segments"), each
-// accumulated in its own TMEM column block.  Its elements [e0, e1) of the
+// in tile-major (nt, kt) order; each n-tile of it (a "segment") is
+// accumulated in TMEM buffer (segment % acc_bufs).  Its elements [e0, e1) of the
 // tiled tensor live in ECF8 blocks [blk_begin, blk_end).
 struct FusedCta {
   std::uint64_t blk_begin, blk_end;
@@ -32,8 +33,9 @@ struct FusedArgs {
   std::uint32_t split_k;
   std::uint32_t stages_a;
   std::uint32_t stages_b;   // X ring stages (2)
-  std::uint32_t tmem_cols;  // allocation: one accumulator of acc_cols per n-tile segment (power of two)
+  std::uint32_t tmem_cols;  // allocation: acc_bufs x acc_cols (power of two <= 512)
   std::uint32_t acc_cols;   // power of two >= max(32, m_pad)
+  std::uint32_t acc_bufs;   // accumulator buffers, reused round-robin by the CTA's segments
   std::uint32_t w_fmt;       // 0 E4M3, 1 E5M2
   std::uint32_t fsm;         // 1: byte-step direct decode (lane offsets known for every tile; 8-window lanes)
   float scale;

@@ -311,7 +311,8 @@ int ecf8_host_decompress_to(const uint8_t* bytes, size_t len, ecf8_write_fn writ
     if (allocations) *allocations = st.buffer_allocations;
     if (capacity) *capacity = st.buffer_capacity_bytes;
   });
-  if (rc == ECF8_OK && buf.status() != 0) return set_error(ECF8_EIO, "sink write failed");
+  // a failed sink makes the stream throw IoError("write failed"): report the sink
+  if (buf.status() != 0) return set_error(ECF8_EIO, "sink write failed");
   return rc;
 }
 

@@ -120,11 +120,20 @@ def test_fused_T256_lanes_4096x8192(m):
 @pytest.mark.parametrize("k", [128, 256])
 def test_fused_many_segments_per_cta(m, k):
     # K = 1 or 2 tiles per output n-tile: a CTA's run of ~3.5 tiles spans up to
-    # four n-tiles (four TMEM accumulator blocks, four partial-row epilogues);
-    # m > 128 caps the plan at two segments (more waves of CTAs)
+    # five n-tiles; at m > 128 only two 256-column accumulators fit TMEM, so
+    # segments reuse them round-robin (flushed by warps 0-3 first)
     n = 128 * 518
     lin, w8 = _weight(n, k, "e4m3", 128)
     _check(lin, w8, m, 1.0, 500 + m + k)
+
+
+@pytest.mark.parametrize("m", [100, 256])
+def test_fused_accumulator_reuse_long_runs(m):
+    # 2000 n-tiles of one K tile: every CTA's run of ~13.5 tiles is ~14
+    # segments, more than the 4 (m <= 128) or 2 (m > 128) accumulator
+    # buffers -- each buffer is flushed and reused several times per CTA
+    lin, w8 = _weight(128 * 2000, 128, "e4m3", 128)
+    _check(lin, w8, m, 0.5, 600 + m)
 
 
 def test_fused_out_is_validated():

@@ -8,7 +8,9 @@ import statistics
 import sys
 from collections import defaultdict
 
-ALGO_PER_LAYER = 397023034  # bench.py layer launch, algorithmic bytes
+import os
+# bench.py layer launch, algorithmic bytes: Llama-3-70B (default workload); ECF8_ALGO_BYTES overrides
+ALGO_PER_LAYER = int(os.environ.get("ECF8_ALGO_BYTES", "1557522886"))
 
 
 def main():
