@@ -509,12 +509,36 @@ def run_fused(args, torch, dist, local, rank, world):
             tf = timed(fused_layer)
             td = timed(decode_gemm_layer)
             tpl = timed(plain_layer)
+            # verification (outside the timed regions): each linear's fused y
+            # against the exact fp64 product of the same FP8 x and the
+            # reference-format decode of W (decode kernel -> bytes), held to the
+            # fp32-accumulation bound |y - y64| <= (gamma_K + u) |x| @ |w|^T
+            # (tests/test_fused_large.py); max error relative to max |y64|.
+            worst, rel = 0.0, 0.0
+            if not args.no_verify:
+                fused_layer()
+                for (dt, buf, bt, nn, kk), x, o in zip(decs, xs, outs):
+                    bt.decode(stream)
+                    w64 = buf.view(torch.float8_e4m3fn).view(nn, kk).double()
+                    x64 = x.double()
+                    y64 = x64 @ w64.t()
+                    u = 2.0 ** -24
+                    gam = kk * u / (1 - kk * u)
+                    bound = (gam + u) * (x64.abs() @ w64.abs().t()) + 1e-30
+                    err = (o.double() - y64).abs()
+                    worst = max(worst, float((err / bound).max()))
+                    rel = max(rel, float(err.max()) / max(float(y64.abs().max()), 1e-30))
+                    del w64, y64, bound, err
             launches += args.steps * len(lins) * 2  # x tiles + fused GEMM per linear
             sweep.append({"m": m, "fused_ms": round(tf, 4), "tokens_per_s": round(m / (tf * 1e-3), 1),
                           "decode_then_gemm_ms": round(td, 4), "plain_fp8_gemm_ms": round(tpl, 4),
                           "compressed_gbs": round(world * comp / (tf * 1e-3) / 1e9, 1),
-                          "tensor_tflops": round(world * flops_per_token * m / (tf * 1e-3) / 1e12, 2)})
-            log(f"[bench] fused m={m}: {tf:.3f} ms/layer ({m / tf * 1e3:.0f} tok/s), decode+gemm {td:.3f}, plain {tpl:.3f}")
+                          "tensor_tflops": round(world * flops_per_token * m / (tf * 1e-3) / 1e12, 2),
+                          "max_err_over_bound": None if args.no_verify else round(worst, 4),
+                          "max_rel_err": None if args.no_verify else float(f"{rel:.3e}"),
+                          "verified": None if args.no_verify else worst <= 1.0})
+            log(f"[bench] fused m={m}: {tf:.3f} ms/layer ({m / tf * 1e3:.0f} tok/s), decode+gemm {td:.3f}, plain {tpl:.3f}"
+                f", err/bound {worst:.3f}")
     if rank == 0:
         top = sweep[-1]
         line = base_line(args, world, top["tokens_per_s"], top["fused_ms"], {
@@ -526,10 +550,11 @@ def run_fused(args, torch, dist, local, rank, world):
         line["dtype"] = "fp8-e4m3 x fp8-e4m3 -> fp32"
         line["scaling"] = "strong"
         line["sweep"] = sweep
+        line["verified"] = None if args.no_verify else all(r["verified"] for r in sweep)
         line["roofline"] = {"bound": "hbm", "achieved": top["compressed_gbs"] / world, "peak": peak, "unit": "GB/s",
                             "frac": round(top["compressed_gbs"] / world / peak, 4), "traffic": None,
                             "tensor_tflops": top["tensor_tflops"] / world, "tensor_peak_tflops": fp8_peak,
-                            "kernel": "fused_gemm_kernel<4,17>"}
+                            "kernel": "fused_gemm_kernel<8,33,*,1>"}
         line["clocks"] = probe.summary()
         line["gpu_launches"] = launches
         print(json.dumps(line), flush=True)

@@ -119,35 +119,6 @@ struct GlobalOut {
   __device__ __forceinline__ void done() const {}
 };
 
-// A warp tile's input sections -> L2 (bulk prefetches, lane 0): its
-// windows, gap and end nibbles, group offsets and block offsets.  The packed
-// bytes are fetched by the tile itself (cp.async during the decode).
-__device__ __forceinline__ void prefetch_l2(const void* p, std::uint64_t bytes) {
-  const std::uintptr_t a = reinterpret_cast<std::uintptr_t>(p) & ~std::uintptr_t{15};
-  const std::uint32_t n = static_cast<std::uint32_t>((reinterpret_cast<std::uintptr_t>(p) + bytes - a + 15) & ~std::uint64_t{15});
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(n) : "memory");
-}
-// Lanes 0-4 issue one section each (the descriptor reads and the address
-// math run side by side instead of one after another).
-__device__ __forceinline__ void prefetch_tile_l2(const TensorDesc& d, std::uint64_t tile, std::uint32_t log2T,
-                                                 int lane) {
-  const std::uint32_t m = 256u >> log2T;
-  const std::uint64_t b0 = d.blk_begin + (tile - d.tile_begin) * m;
-  const std::uint64_t nb = d.blk_end - b0 < m ? d.blk_end - b0 : m;
-  const std::uint64_t w0 = b0 << log2T, nw = nb << log2T;
-  const void* p = nullptr;
-  std::uint64_t n = 0;
-  switch (lane) {
-    case 0: p = d.encoded + 8 * w0, n = 8 * nw + 8; break;
-    case 1: p = d.gaps + (w0 >> 1), n = nw >> 1; break;
-    case 2: p = d.outpos + b0, n = 8 * (nb + 1); break;
-    case 3: p = d.endgap ? d.endgap + (w0 >> 1) : nullptr, n = nw >> 1; break;
-    case 4: p = d.lane_start ? reinterpret_cast<const void*>(d.lane_start + (w0 >> 2)) : nullptr, n = nw >> 1; break;
-    default: break;
-  }
-  if (p && n) prefetch_l2(p, n);
-}
-
 // One tile: decode + scan, compact, write back.
 template <bool WIDE, class WSm>
 __device__ __forceinline__ void warp_tile(const TensorDesc& d, const WarpIn& in, std::uint32_t log2T,
@@ -163,8 +134,8 @@ __device__ __forceinline__ void warp_tile(const TensorDesc& d, const WarpIn& in,
     const bool verified = tile_verified(d, in, log2T);
     const std::uint32_t v = static_cast<std::uint32_t>((in.b0 << log2T) >> 8);  // the tile's verification tile
     if ((in.dir >> (v & 31)) & 1u) {  // every lane's output offset known: decode in place
-      GlobalOut out{d.out + ((in.A & ~std::uint64_t{15}) - d.out_offset)};
-      direct_tile<kWbUnroll>(d, in, ws, lane, out, verified);
+      direct_tile<kWbUnroll>(
+          d, in, ws, lane, [&] { return GlobalOut{d.out + ((in.A & ~std::uint64_t{15}) - d.out_offset)}; }, verified);
       return;
     }
     run = warp_decode_scan<kLaneWin, 128, false, GlobalTables, true>(in, log2T, len_off, GlobalTables{d}, slot, lane,

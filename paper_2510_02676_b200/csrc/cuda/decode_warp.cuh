@@ -106,6 +106,35 @@ __device__ __forceinline__ void load_warp_tile(const TensorDesc& d, std::uint64_
   load_tile_meta<LW, NEXT>(d, log2T, lane, in);
 }
 
+// A warp tile's input sections -> L2 (bulk prefetches, lanes 0-4): its
+// windows, gap and end nibbles, group offsets and block offsets.  The packed
+// bytes are fetched by the tile itself (cp.async during the decode).
+__device__ __forceinline__ void prefetch_l2(const void* p, std::uint64_t bytes) {
+  const std::uintptr_t a = reinterpret_cast<std::uintptr_t>(p) & ~std::uintptr_t{15};
+  const std::uint32_t n = static_cast<std::uint32_t>((reinterpret_cast<std::uintptr_t>(p) + bytes - a + 15) & ~std::uint64_t{15});
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(n) : "memory");
+}
+// Lanes 0-4 issue one section each (the descriptor reads and the address
+// math run side by side instead of one after another).
+__device__ __forceinline__ void prefetch_tile_l2(const TensorDesc& d, std::uint64_t tile, std::uint32_t log2T,
+                                                 int lane) {
+  const std::uint32_t m = 256u >> log2T;
+  const std::uint64_t b0 = d.blk_begin + (tile - d.tile_begin) * m;
+  const std::uint64_t nb = d.blk_end - b0 < m ? d.blk_end - b0 : m;
+  const std::uint64_t w0 = b0 << log2T, nw = nb << log2T;
+  const void* p = nullptr;
+  std::uint64_t n = 0;
+  switch (lane) {
+    case 0: p = d.encoded + 8 * w0, n = 8 * nw + 8; break;
+    case 1: p = d.gaps + (w0 >> 1), n = nw >> 1; break;
+    case 2: p = d.outpos + b0, n = 8 * (nb + 1); break;
+    case 3: p = d.endgap ? d.endgap + (w0 >> 1) : nullptr, n = nw >> 1; break;
+    case 4: p = d.lane_start ? reinterpret_cast<const void*>(d.lane_start + (w0 >> 2)) : nullptr, n = nw >> 1; break;
+    default: break;
+  }
+  if (p && n) prefetch_l2(p, n);
+}
+
 // Were the gaps of the windows of this warp tile verified (verify_gaps_kernel)?
 // tile_ok bit v covers the boundaries after windows [256v, 256v + 256).
 template <int LW>
@@ -377,9 +406,11 @@ __device__ __forceinline__ void compact_write(const TensorDesc& d, std::uint64_t
 // plain stores (each belongs to one chain); a chain's partial last word is
 // OR-ed in after every chain's first word (which may share it) is stored.
 // The tile's packed bytes stream into the slots while the lanes decode.
-template <int UNROLL, int LW, bool GPK = false, class WSm, class Out, class FT = FsmPinned>
-__device__ __forceinline__ void direct_tile(const TensorDesc& d, const WarpInT<LW>& in, WSm& ws, int lane, Out& out,
-                                            bool verified, const FT& ft = FT{}) {
+// mk_out() builds the output sink (out.wait / chunk / byte / done, see
+// compact_write) after the decode: its state is not live across the byte steps.
+template <int UNROLL, int LW, bool GPK = false, class WSm, class MkOut, class FT = FsmPinned>
+__device__ __forceinline__ void direct_tile(const TensorDesc& d, const WarpInT<LW>& in, WSm& ws, int lane,
+                                            const MkOut& mk_out, bool verified, const FT& ft = FT{}) {
   const std::uint32_t off = static_cast<std::uint32_t>(in.A & 15);  // staging nibble of element A
   const std::uint32_t data_end = off + static_cast<std::uint32_t>(in.E - in.A);
   const std::uint64_t S0 = in.A - off;
@@ -447,6 +478,7 @@ __device__ __forceinline__ void direct_tile(const TensorDesc& d, const WarpInT<L
   if (tb) asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(tb_addr), "r"(tb) : "memory");
   if constexpr (!GPK) asm volatile("cp.async.wait_all;" ::: "memory");
   __syncwarp();
+  auto out = mk_out();
   write_back<UNROLL, GPK>(S0, off, data_end, pk_a, ws, lane, out, d.packed);
 }
 

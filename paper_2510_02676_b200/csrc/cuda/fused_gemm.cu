@@ -250,17 +250,17 @@ struct Ring {
 // segment's epilogue overlaps the decode of the next ones; only the last
 // segment is flushed after the CTA's decode work.
 struct Flush {
-  float* y;
-  std::uint32_t n, m, nb, acc_cols, tmem_d, nt0, nseg;
-  float scale;
-  int warp, lane;
+  const FusedArgs* a;  // the kernel's parameters (__grid_constant__: read in place)
+  std::uint32_t tmem_d, nt0, nseg;
 
   __device__ __forceinline__ void segment(std::uint32_t sg) const {
-    const std::uint32_t b = sg % nb;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const std::uint32_t b = sg % a->acc_bufs;
     const std::uint32_t row = static_cast<std::uint32_t>(warp) * 32 + static_cast<std::uint32_t>(lane);
     const std::uint64_t col = static_cast<std::uint64_t>(nt0 + sg) * 128 + row;
-    const std::uint32_t tq = tmem_d + b * acc_cols + (static_cast<std::uint32_t>(warp * 32) << 16);
+    const std::uint32_t tq = tmem_d + b * a->acc_cols + (static_cast<std::uint32_t>(warp * 32) << 16);
     asm volatile("griddepcontrol.wait;" ::: "memory");  // y zeroed by x_tiles_kernel (returns at once after)
+    const std::uint32_t m = a->m;
     for (std::uint32_t c0 = 0; c0 < m; c0 += 8) {
       float v[8];
       tmem_ld8(tq + c0, v);
@@ -268,16 +268,18 @@ struct Flush {
       for (int j = 0; j < 8; ++j) {
         const std::uint32_t mcol = c0 + j;
 #if ECF8_FUSED_EPI
-        if (mcol < m) atomicAdd(y + static_cast<std::uint64_t>(mcol) * n + col, v[j] * scale);
+        if (mcol < m) atomicAdd(a->y + static_cast<std::uint64_t>(mcol) * a->n + col, v[j] * a->scale);
 #else
-        if (mcol < m && v[j] == 12345.f) y[0] = 0.f;  // timing experiment only: no y updates
+        if (mcol < m && v[j] == 12345.f) a->y[0] = 0.f;  // timing experiment only: no y updates
 #endif
       }
     }
   }
   // Flush every finished segment (block: wait for each until all are done).
   __device__ __forceinline__ void run(bool block) const {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (warp >= 4) return;
+    const std::uint32_t nb = a->acc_bufs;
     for (;;) {
       const std::uint32_t f = g_nflush[warp];
       if (f >= nseg) return;
@@ -438,8 +440,8 @@ __device__ __forceinline__ void ring_tile_fsm(const TensorDesc& d, const WarpInT
   const std::uint64_t A = in.A > R.e0 ? in.A : R.e0;
   const std::uint64_t E = in.E < R.e1 ? in.E : R.e1;
   if (A >= E) return;
-  RingOut out = ring_out(in.A, A, E, R, lane);
-  direct_tile<2, LW, ECF8_FUSED_GPK != 0>(d, in, ws, lane, out, tile_verified(d, in, log2T), ft);
+  direct_tile<2, LW, ECF8_FUSED_GPK != 0>(
+      d, in, ws, lane, [&] { return ring_out(in.A, A, E, R, lane); }, tile_verified(d, in, log2T), ft);
 }
 
 // Per decode warp: slots of SLOT_ROWS words per lane (a lane's run of LW
@@ -458,7 +460,7 @@ constexpr int extra_warps() { return 1; }
 
 template <int LW, int SLOT_ROWS, bool WIDE, bool FSM = false>
 __global__ void __launch_bounds__((decode_warps<LW, SLOT_ROWS, WIDE, FSM>() + extra_warps<FSM>()) * 32, 1)
-    fused_gemm_kernel(const FusedArgs args) {
+    fused_gemm_kernel(const __grid_constant__ FusedArgs args) {
   using WSm = FusedWarpSmemF<LW, SLOT_ROWS, FSM>;
   constexpr int kDecodeWarps = decode_warps<LW, SLOT_ROWS, WIDE, FSM>();
   constexpr int kThreadsF = (kDecodeWarps + extra_warps<FSM>()) * 32;
@@ -530,7 +532,7 @@ __global__ void __launch_bounds__((decode_warps<LW, SLOT_ROWS, WIDE, FSM>() + ex
   const std::uint32_t tmem_d = g_tmem;
 
   const std::uint32_t nseg = n_kt ? (cta.tile1 - 1) / KT - nt0 + 1 : 0;
-  const Flush fl{args.y, args.n, args.m, args.acc_bufs, args.acc_cols, tmem_d, nt0, nseg, args.scale, warp, lane};
+  const Flush fl{&args, tmem_d, nt0, nseg};
 
   if (warp < kDecodeWarps) {
     // ---- decode warps: dynamic queue over the CTA's ECF8 tiles, in order

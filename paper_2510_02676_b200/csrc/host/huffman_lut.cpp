@@ -14,6 +14,7 @@
 
 #include "ecf8/huffman.hpp"
 #include "ecf8/lut.hpp"
+#include "package_merge.hpp"
 
 namespace ecf8 {
 
@@ -26,47 +27,10 @@ int CodeTable::max_length() const { return *std::max_element(lengths.begin(), le
 
 namespace {
 
-struct Coin {
-  std::uint64_t weight = 0;
-  std::array<std::uint8_t, kNumSymbols> mult{};  // leaf multiplicity per symbol
-};
-
 std::array<std::uint8_t, kNumSymbols> coin_collector_lengths(const ExponentHistogram& h) {
-  std::vector<std::pair<std::uint64_t, int>> live;
-  for (int s = 0; s < kNumSymbols; ++s)
-    if (h.counts[s]) live.emplace_back(h.counts[s], s);
-  std::sort(live.begin(), live.end());
-
-  std::vector<Coin> leaves(live.size());
-  for (std::size_t i = 0; i < live.size(); ++i) {
-    leaves[i].weight = live[i].first;
-    leaves[i].mult[live[i].second] = 1;
-  }
-
-  const auto lighter = [](const Coin& a, const Coin& b) { return a.weight < b.weight; };
-  std::vector<Coin> row = leaves, pairs, merged;
-  for (int pass = 1; pass < kMaxCodeLength; ++pass) {
-    pairs.clear();
-    for (std::size_t i = 1; i < row.size(); i += 2) {
-      Coin c;
-      c.weight = row[i - 1].weight + row[i].weight;
-      for (int s = 0; s < kNumSymbols; ++s)
-        c.mult[s] = static_cast<std::uint8_t>(row[i - 1].mult[s] + row[i].mult[s]);
-      pairs.push_back(c);
-    }
-    // std::merge keeps the first range ahead on ties: packages win.
-    merged.clear();
-    std::merge(pairs.begin(), pairs.end(), leaves.begin(), leaves.end(),
-               std::back_inserter(merged), lighter);
-    row.swap(merged);
-  }
-
-  std::array<std::uint8_t, kNumSymbols> len{};
-  const std::size_t keep = 2 * (live.size() - 1);
-  if (row.size() < keep) throw std::logic_error("package-merge list too short");
-  for (std::size_t i = 0; i < keep; ++i)
-    for (int s = 0; s < kNumSymbols; ++s) len[s] = static_cast<std::uint8_t>(len[s] + row[i].mult[s]);
-  return len;
+  std::array<std::uint64_t, kNumSymbols> c{};
+  for (int s = 0; s < kNumSymbols; ++s) c[s] = h.counts[s];
+  return host::package_merge_lengths<kNumSymbols, kMaxCodeLength>(c);
 }
 
 }  // namespace
