@@ -1,4 +1,5 @@
-"""ctypes binding of the product library (include/ecf8_cuda.h, include/ecf8_host.h).
+"""ctypes binding of the product library (include/ecf8_cuda.h, include/ecf8_host.h,
+include/ecf8_e5m2.h).
 
 The shared object is built in-tree by ``make`` (see __graft_entry__.build) at
 paper_2510_02676_b200/lib/libecf8_b200.so.  Importing this module never
@@ -61,6 +62,24 @@ class Sections(C.Structure):
         ("n_outpos", C.c_uint64),
         ("packed", C.c_void_p),
         ("packed_len", C.c_uint64),
+    ]
+
+
+class E5Sections(C.Structure):
+    """ecf8_e5_sections: one tensor of the native E5M2 variant (include/ecf8_e5m2.h)."""
+
+    _fields_ = [
+        ("n_elem", C.c_uint64),
+        ("threads_per_block", C.c_uint32),
+        ("lengths", C.c_uint8 * 32),
+        ("encoded", C.c_void_p),
+        ("encoded_len", C.c_uint64),
+        ("gaps", C.c_void_p),
+        ("gaps_len", C.c_uint64),
+        ("outpos", C.c_void_p),
+        ("n_outpos", C.c_uint64),
+        ("raw", C.c_void_p),
+        ("raw_len", C.c_uint64),
     ]
 
 
@@ -150,6 +169,23 @@ _SIGS = {
     "ecf8_host_synth": (C.c_int, [C.c_double, C.c_double, C.c_uint64, C.c_uint64, C.c_int, _P, C.c_int]),
     "ecf8_host_max_threads": (C.c_int, []),
     "ecf8_host_make_stats": (C.c_int, [_P, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(EntropyReport)]),
+    # ecf8_e5m2.h
+    "ecf8_e5_build_code": (C.c_int, [_P, _P]),
+    "ecf8_e5_encode": (C.c_int, [_P, C.c_uint64, C.c_uint32, C.POINTER(_P)]),
+    "ecf8_e5_tensor_sections": (C.c_int, [_P, C.POINTER(E5Sections)]),
+    "ecf8_e5_tensor_free": (None, [_P]),
+    "ecf8_e5_compress_raw": (C.c_int, [_P, C.c_size_t, C.c_uint32, C.POINTER(_P), C.POINTER(C.c_size_t)]),
+    "ecf8_e5_parse": (C.c_int, [_P, C.c_size_t, C.POINTER(_P)]),
+    "ecf8_e5_file_count": (C.c_int, [_P]),
+    "ecf8_e5_file_tensor": (C.c_int, [_P, C.c_int, C.POINTER(E5Sections), C.POINTER(C.c_char_p)]),
+    "ecf8_e5_file_shape": (C.c_int, [_P, C.c_int, C.POINTER(C.c_uint64), C.c_int, C.POINTER(C.c_int)]),
+    "ecf8_e5_file_free": (None, [_P]),
+    "ecf8_e5_decompress": (C.c_int, [_P, C.c_size_t, C.POINTER(_P), C.POINTER(C.c_size_t)]),
+    "ecf8_e5_upload": (C.c_int, [C.POINTER(E5Sections), C.POINTER(_P)]),
+    "ecf8_e5_decode_device": (C.c_int, [_P, _P, _P]),
+    "ecf8_e5_dev_n_elem": (C.c_uint64, [_P]),
+    "ecf8_e5_free": (None, [_P]),
+    "ecf8_e5_decode_host": (C.c_int, [C.POINTER(E5Sections), _P, C.c_uint64]),
 }
 
 for _name, (_res, _args) in _SIGS.items():

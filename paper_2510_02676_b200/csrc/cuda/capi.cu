@@ -1201,3 +1201,5 @@ int ecf8_host_unpin(void* p) {
 }
 
 }  // extern "C"
+
+extern "C" int ecf8_internal_require_device(void) { return require_device(); }

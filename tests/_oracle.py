@@ -118,6 +118,66 @@ class Oracle:
         return int(self.lib.orc_max_threads())
 
 
+class E5Oracle:
+    """numpy-facing wrapper of oracle/e5_oracle.c (the native E5M2 variant)."""
+
+    def __init__(self, path: str = ORACLE_SO):
+        self.lib = L = C.CDLL(path)
+        U64P = C.POINTER(C.c_uint64)
+        for name, args in {
+            "orc5_build_code": [_P, _P],
+            "orc5_canonical_codes": [_P, _P],
+            "orc5_sizes": [_P, C.c_uint64, _P, C.c_uint32, U64P, U64P, U64P, U64P],
+            "orc5_encode": [_P, C.c_uint64, _P, C.c_uint32, _P, _P, _P, _P],
+            "orc5_decode": [_P, C.c_uint32, _P, C.c_uint64, _P, C.c_uint64, _P, C.c_uint64, _P, C.c_uint64, _P,
+                            C.c_uint64],
+        }.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = C.c_int
+
+    def build_code(self, counts):
+        c = np.ascontiguousarray(counts, np.uint64)
+        l = np.zeros(32, np.uint8)
+        if self.lib.orc5_build_code(_p(c), _p(l)):
+            raise ValueError("empty input")
+        return l
+
+    def encode(self, e5, lengths, T):
+        a = np.ascontiguousarray(e5, np.uint8).reshape(-1)
+        l = np.ascontiguousarray(lengths, np.uint8)
+        nb, el, gl, rl = (C.c_uint64() for _ in range(4))
+        if self.lib.orc5_sizes(_p(a), a.size, _p(l), T, C.byref(nb), C.byref(el), C.byref(gl), C.byref(rl)):
+            raise ValueError("symbol absent from code table or bad T")
+        enc, gaps = np.zeros(el.value, np.uint8), np.zeros(gl.value, np.uint8)
+        outpos, raw = np.zeros(nb.value + 1, np.uint64), np.zeros(rl.value, np.uint8)
+        assert self.lib.orc5_encode(_p(a), a.size, _p(l), T, _p(enc), _p(gaps), _p(outpos), _p(raw)) == 0
+        return dict(n_elem=a.size, T=T, lengths=l.copy(), encoded=enc, gaps=gaps, outpos=outpos, raw=raw)
+
+    def encode_auto(self, e5, T):
+        a = np.ascontiguousarray(e5, np.uint8).reshape(-1)
+        if not a.size:
+            return dict(n_elem=0, T=T, lengths=np.zeros(32, np.uint8), encoded=np.zeros(2, np.uint8),
+                        gaps=np.zeros(0, np.uint8), outpos=np.zeros(1, np.uint64), raw=np.zeros(0, np.uint8))
+        counts = np.bincount((a >> 2) & 31, minlength=32).astype(np.uint64)
+        return self.encode(a, self.build_code(counts), T)
+
+    def decode(self, t):
+        out = np.zeros(t["n_elem"], np.uint8)
+        rc = self.lib.orc5_decode(_p(t["lengths"]), t["T"], _p(t["encoded"]), t["encoded"].size, _p(t["gaps"]),
+                                  t["gaps"].size, _p(np.ascontiguousarray(t["outpos"], np.uint64)),
+                                  t["outpos"].size - 1, _p(t["raw"]), t["raw"].size, _p(out), out.size)
+        assert rc == 0, rc
+        return out
+
+
+def e5_dict(t) -> dict:
+    """Product E5Tensor -> the oracle's dict form."""
+    return dict(n_elem=t.n_elem, T=t.threads_per_block, lengths=np.asarray(t.lengths, np.uint8),
+                encoded=np.asarray(t.encoded), gaps=np.asarray(t.gaps), outpos=np.asarray(t.outpos, np.uint64),
+                raw=np.asarray(t.raw))
+
+
 def tensor_dict(t) -> dict:
     """Product EncodedTensor -> the oracle's dict form."""
     return dict(n_elem=t.n_elem, T=t.threads_per_block, lengths=np.asarray(t.lengths, np.uint8),

@@ -1,0 +1,238 @@
+"""Native E5M2 variant (include/ecf8_e5m2.h).
+
+No reference implementation exists (the reference is E4M3-only,
+/root/reference/SPEC.md:83), so parity is pinned by (1) the product encoder
+matching the independent C statement oracle/e5_oracle.c section for section,
+(2) round trips through the oracle's decoder to the original bytes, and (3)
+the B200 decoder matching the oracle bit for bit, including clamped blocks,
+incomplete codes and garbage windows.  CPU tests cover (1), (2) and the
+container; the GPU tests (3).
+"""
+import numpy as np
+import pytest
+
+from paper_2510_02676_b200 import codec, e5m2
+from paper_2510_02676_b200._lib import Ecf8Error, FormatError, InvalidArgument, device_count
+
+from _oracle import E5Oracle, e5_dict
+
+SIZES = [0, 1, 7, 31, 32, 33, 1000, 65537]
+TS = [1, 2, 8, 32, 256, 1024]
+
+
+@pytest.fixture(scope="module")
+def orc():
+    return E5Oracle()
+
+
+def _data(n, seed, kind="stable"):
+    if kind == "stable":
+        return codec.synth(1.8, 0.05, n, seed, fmt="e5m2")
+    rng = np.random.default_rng(seed)
+    if kind == "uniform":
+        return rng.integers(0, 256, n, dtype=np.uint8)
+    if kind == "skewed":  # geometric exponents: long codes (length limit 16)
+        e = np.minimum(rng.geometric(0.55, n) - 1, 31).astype(np.uint8)
+        return ((e << 2) | rng.integers(0, 4, n, dtype=np.uint8) | (rng.integers(0, 2, n, dtype=np.uint8) << 7))
+    raise ValueError(kind)
+
+
+def _same(t, ref):
+    d = e5_dict(t)
+    for k in ("lengths", "encoded", "gaps", "outpos", "raw"):
+        assert np.array_equal(np.asarray(d[k]), np.asarray(ref[k])), k
+    assert d["n_elem"] == ref["n_elem"] and d["T"] == ref["T"]
+
+
+@pytest.mark.parametrize("kind", ["stable", "uniform", "skewed"])
+def test_code_matches_oracle_and_is_complete(orc, kind):
+    x = _data(200_000, 3, kind)
+    counts = np.bincount((x >> 2) & 31, minlength=32).astype(np.uint64)
+    l = e5m2.build_code(counts)
+    assert np.array_equal(l, orc.build_code(counts))
+    assert l.max() <= 16
+    present = counts > 0
+    assert np.array_equal(l > 0, present)
+    assert sum(2.0 ** -int(v) for v in l if v) == pytest.approx(1.0)
+
+
+def test_code_length_limit_and_single_symbol(orc):
+    fib = [1, 1]
+    while len(fib) < 32:
+        fib.append(fib[-1] + fib[-2])
+    counts = np.array(fib, np.uint64)  # unlimited Huffman would need 31-bit codes
+    l = e5m2.build_code(counts)
+    assert l.max() == 16 and np.array_equal(l, orc.build_code(counts))
+    one = np.zeros(32, np.uint64)
+    one[9] = 5
+    assert e5m2.build_code(one)[9] == 1
+    with pytest.raises(InvalidArgument):
+        e5m2.build_code(np.zeros(32, np.uint64))
+
+
+@pytest.mark.parametrize("n", SIZES)
+@pytest.mark.parametrize("T", TS)
+def test_encoder_matches_oracle_and_round_trips(orc, n, T):
+    x = _data(n, 100 + n + T)
+    t = e5m2.encode(x, T)
+    _same(t, orc.encode_auto(x, T))
+    assert np.array_equal(orc.decode(e5_dict(t)), x)
+
+
+@pytest.mark.parametrize("kind", ["uniform", "skewed"])
+def test_all_byte_values_round_trip(orc, kind):
+    x = np.concatenate([np.arange(256, dtype=np.uint8), _data(5000, 11, kind)])
+    for T in (4, 64):
+        t = e5m2.encode(x, T)
+        _same(t, orc.encode_auto(x, T))
+        assert np.array_equal(orc.decode(e5_dict(t)), x)
+
+
+def test_saves_more_than_the_byte_split_on_e5m2_weights():
+    x = _data(1 << 20, 42)
+    native = e5m2.encode(x, 256).compressed_bytes()
+    split = codec.encode_tensor(x, 256).compressed_bytes()
+    assert native < split < x.size
+    # bits per element: the native variant codes 5 exponent bits + 3 raw bits
+    assert native / x.size < 0.95
+
+
+def test_bad_T():
+    with pytest.raises(InvalidArgument, match="power of two"):
+        e5m2.encode(np.zeros(10, np.uint8), 3)
+
+
+def _container():
+    ts = [("a", [3, 5], _data(15, 1)), ("empty", [0], np.zeros(0, np.uint8)), ("w", [1000, 33], _data(33000, 2))]
+    raw = codec.raw_file(ts)
+    return ts, raw, e5m2.compress_raw(raw, 32)
+
+
+def test_container_round_trip_structure(orc):
+    ts, raw, blob = _container()
+    assert blob[:4] == b"EC5M"
+    f = e5m2.E5File(blob)
+    assert len(f) == len(ts)
+    for i, (name, dims, data) in enumerate(ts):
+        nm, d, t = f.tensor(i)
+        assert nm == name and d == dims
+        _same(t, orc.encode_auto(data, 32))
+        assert np.array_equal(orc.decode(e5_dict(t)), data)
+
+
+@pytest.mark.parametrize("cut,msg", [
+    (lambda b: b"XXXX" + b[4:], "bad magic"),
+    (lambda b: b[:4] + (2).to_bytes(4, "little") + b[8:], "unsupported version"),
+    (lambda b: b[:-1], "truncated"),
+    (lambda b: b + b"\0", "trailing bytes"),
+])
+def test_container_validation(cut, msg):
+    _, _, blob = _container()
+    with pytest.raises(FormatError, match=msg):
+        e5m2.E5File(cut(blob))
+
+
+def _single(data, T=32):
+    raw = codec.raw_file([("t", [data.size], data)])
+    return bytearray(e5m2.compress_raw(raw, T))
+
+
+def test_container_rejects_bad_sections():
+    data = _data(5000, 8)
+    b = _single(data)
+    hdr = 4 + 4 + 4 + 2 + 1 + 1 + 8  # magic, version, count, name_len, "t", rank, dims
+    # n_elem, T, lengths
+    bad = bytearray(b)
+    bad[hdr + 8:hdr + 12] = (3).to_bytes(4, "little")
+    with pytest.raises(FormatError, match="invalid thread count"):
+        e5m2.E5File(bytes(bad))
+    bad = bytearray(b)
+    bad[hdr + 12] = 17
+    with pytest.raises(FormatError, match="invalid length vector"):
+        e5m2.E5File(bytes(bad))
+    bad = bytearray(b)
+    el = int.from_bytes(b[hdr + 44:hdr + 52], "little")
+    bad[hdr + 44:hdr + 52] = (el + 1).to_bytes(8, "little")
+    with pytest.raises(FormatError):
+        e5m2.E5File(bytes(bad))
+
+
+def test_decode_without_gpu_fails_loudly():
+    if device_count() > 0:
+        pytest.skip("a device is present")
+    t = e5m2.encode(_data(100, 1), 32)
+    with pytest.raises(Ecf8Error, match="no CUDA device"):
+        e5m2.decode(t)
+
+
+# ---------------------------------------------------------------- GPU
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", ["stable", "uniform", "skewed"])
+@pytest.mark.parametrize("n", [1, 33, 4099, 1_000_003])
+@pytest.mark.parametrize("T", TS + [4, 128, 512])
+def test_gpu_decode_matches_oracle(orc, kind, n, T):
+    x = _data(n, 7 * n + T, kind)
+    t = e5m2.encode(x, T)
+    got = e5m2.decode(t)
+    assert np.array_equal(got, x)
+    assert np.array_equal(got, orc.decode(e5_dict(t)))
+
+
+@pytest.mark.gpu
+def test_gpu_device_resident_decode_and_large_tensor(orc):
+    import torch
+
+    x = _data(16 << 20, 5)
+    t = e5m2.encode(x, 256)
+    dt = e5m2.E5DeviceTensor(t)
+    out = torch.full((x.size + 64,), 0xAB, dtype=torch.uint8, device="cuda")
+    dt.decode_into(out[: x.size])
+    torch.cuda.synchronize()
+    got = out.cpu().numpy()
+    assert np.array_equal(got[: x.size], x)
+    assert (got[x.size:] == 0xAB).all(), "decode wrote past the tensor"
+
+
+def _crafted(orc, lengths, stream_bytes, T, n):
+    """A section set whose stream is arbitrary bits under `lengths` (incomplete
+    codes, garbage windows), with outpos from the oracle's own counts."""
+    nb = max(1, (len(stream_bytes) + 8 * T - 1) // (8 * T))
+    enc = np.zeros(nb * T * 8 + 2, np.uint8)
+    enc[:len(stream_bytes)] = np.frombuffer(bytes(stream_bytes), np.uint8)
+    gaps = np.zeros((nb * T + 1) // 2, np.uint8)
+    rng = np.random.default_rng(len(stream_bytes))
+    gaps[:] = rng.integers(0, 256, gaps.size, dtype=np.uint8)
+    outpos = np.linspace(0, n, nb + 1).astype(np.uint64)
+    raw = rng.integers(0, 256, 12 * ((n + 31) // 32), dtype=np.uint8)
+    return dict(n_elem=n, T=T, lengths=np.asarray(lengths, np.uint8), encoded=enc, gaps=gaps, outpos=outpos, raw=raw)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("T", [1, 8, 256, 1024])
+def test_gpu_incomplete_code_garbage_windows_and_clamps(orc, T):
+    lengths = np.zeros(32, np.uint8)
+    lengths[[3, 7, 20, 31]] = [2, 3, 5, 9]  # Kraft 0.25 + 0.125 + 1/32 + 1/512 < 1
+    rng = np.random.default_rng(T)
+    stream = rng.integers(0, 256, 8 * T * 3, dtype=np.uint8).tobytes()
+    d = _crafted(orc, lengths, stream, T, n=min(T * 3 * 20, 3 * 64 * T))
+    want = orc.decode(d)
+    t = e5m2.E5Tensor(d["n_elem"], T, d["lengths"], d["encoded"], d["gaps"], d["outpos"], d["raw"])
+    assert np.array_equal(e5m2.decode(t), want)
+
+
+@pytest.mark.gpu
+def test_gpu_container_decompress_matches_raw():
+    ts, raw, blob = _container()
+    assert e5m2.decompress(blob) == raw
+
+
+@pytest.mark.gpu
+def test_gpu_rejects_inconsistent_offsets():
+    t = e5m2.encode(_data(5000, 3), 32)
+    op = np.array(t.outpos, np.uint64)
+    op[-1] += 1
+    bad = e5m2.E5Tensor(t.n_elem, 32, t.lengths, t.encoded, t.gaps, op, t.raw)
+    with pytest.raises(InvalidArgument, match="inconsistent block offsets"):
+        e5m2.decode(bad)
