@@ -396,10 +396,20 @@ def timed_region(torch, dist, local, stream, batches, steps, warmup):
 
 def run_dit_sweep(args, torch, dist, local, world):
     """Config 5: E5M2 tensors of 1 MB .. 1 GB (rows of 3072 / 5120), one
-    launch per tensor, rotating over replicas so every size streams >= 2 GB
-    through HBM per measurement (defeats L2)."""
-    from paper_2510_02676_b200 import codec
+    launch per tensor, rotating over replicas so every measurement streams
+    >= 512 MB of distinct inputs (4x the 126 MB L2: no size is served from
+    L2).  Two encodings of the same bytes: the reference format's byte split
+    (4-bit symbols, decode_warp variant 5 for the 1-bit codes E5M2 gives) and
+    the native E5M2 variant (5-bit symbols + 3 raw bits, e5_decode.cu)."""
+    from paper_2510_02676_b200 import codec, e5m2
     from paper_2510_02676_b200.device import Batch, DeviceTensor
+
+    class E5Launch:  # timed_region's decode(stream) over an E5 device tensor
+        def __init__(self, dt, out):
+            self.dt, self.out = dt, out
+
+        def decode(self, stream):
+            self.dt.decode_into(self.out, stream)
 
     stream = torch.cuda.current_stream()
     sweep, total_launches = [], 0
@@ -408,23 +418,40 @@ def run_dit_sweep(args, torch, dist, local, world):
         rows = max(1, (mb << 20) // width)
         n = rows * width
         raw = codec.synth(ALPHA, GAMMA, n, 7000 + mb, fmt="e5m2")
-        enc = codec.encode_tensor(raw, T_BLOCK)
-        reps = max(2, min(64, (2 << 30) // max(1, enc.algorithmic_bytes())))
-        devs = [DeviceTensor(enc) for _ in range(reps)]
+        want = torch.from_numpy(raw).cuda()
         outs = [torch.empty(n, dtype=torch.uint8, device="cuda") for _ in range(2)]
-        batches = [Batch([d], [outs[i % 2]]) for i, d in enumerate(devs)]
-        batches[0].decode(stream)
-        torch.cuda.synchronize()
-        ok = bool(torch.equal(outs[0], torch.from_numpy(raw).cuda()))
-        elapsed, launch_ms, clocks = timed_region(torch, dist, local, stream, batches, args.steps, args.warmup)
-        algo = enc.algorithmic_bytes()
-        gbs = world * algo * len(batches) * args.steps / (elapsed * 1e-3) / 1e9
-        sweep.append({"size_mb": mb, "shape": [rows, width], "gbs": round(gbs, 1),
-                      "us_per_launch": round(statistics.median(launch_ms) * 1e3, 2),
-                      "bytes_per_elem": round(algo / n, 4), "verified_bit_exact": ok})
-        total_launches += len(batches) * args.steps
-        log(f"[bench] dit-e5m2 {mb} MB: {gbs:.1f} GB/s")
-        del devs, batches, outs
+        row = {"size_mb": mb, "shape": [rows, width]}
+        for fmt in ("split", "native"):
+            if fmt == "split":
+                enc = codec.encode_tensor(raw, T_BLOCK)
+                algo = enc.algorithmic_bytes()
+            else:
+                enc = e5m2.encode(raw, T_BLOCK)
+                algo = enc.algorithmic_bytes()
+            reps = max(2, min(512, -(-(512 << 20) // max(1, algo))))
+            if fmt == "split":
+                devs = [DeviceTensor(enc) for _ in range(reps)]
+                batches = [Batch([d], [outs[i % 2]]) for i, d in enumerate(devs)]
+            else:
+                devs = [e5m2.E5DeviceTensor(enc) for _ in range(reps)]
+                batches = [E5Launch(d, outs[i % 2]) for i, d in enumerate(devs)]
+            batches[0].decode(stream)
+            torch.cuda.synchronize()
+            ok = bool(torch.equal(outs[0], want))
+            elapsed, launch_ms, clocks = timed_region(torch, dist, local, stream, batches, args.steps, args.warmup)
+            gbs = world * algo * len(batches) * args.steps / (elapsed * 1e-3) / 1e9
+            r = {"gbs": round(gbs, 1), "us_per_launch": round(statistics.median(launch_ms) * 1e3, 2),
+                 "bytes_per_elem": round(algo / n, 4), "replicas": reps, "verified_bit_exact": ok}
+            if fmt == "split":
+                row.update(r)
+            else:
+                row["native"] = r
+            total_launches += len(batches) * args.steps
+            log(f"[bench] dit-e5m2 {mb} MB {fmt}: {gbs:.1f} GB/s ({r['us_per_launch']} us/launch, "
+                f"{r['bytes_per_elem']} B/elem)")
+            del devs, batches
+        sweep.append(row)
+        del outs
     return sweep, total_launches
 
 

@@ -433,6 +433,23 @@ struct PairSink {
     if (q4 & 31u) sts32(addr, lo);
     return (addr - base) / WS * 8 + ((q4 & 31u) >> 2);
   }
+  // put2 for a run that ends at a known place: words before `ew` (the word
+  // holding the run's end nibble) are stored, the end word's bits go to
+  // `tail` (OR-ed in by the caller, masked to the run), words after it are
+  // dropped -- the symbols a parse produces past the run's end.
+  __device__ __forceinline__ void put2_bounded(std::uint32_t e1, std::uint32_t e2, std::uint32_t ew,
+                                               std::uint32_t& tail) {
+    const std::uint32_t c = (e1 >> 16) | __funnelshift_l(0u, e2 >> 16, e1);
+    const std::uint32_t q = q4 + e1 + e2;
+    const std::uint32_t nl = lo | __funnelshift_l(0u, c, q4);
+    const std::uint32_t nh = __funnelshift_l(c, 0u, q4);
+    const bool full = ((q ^ q4) & 32u) != 0;
+    if (full && addr < ew) sts32(addr, nl);
+    if (full && addr == ew) tail = nl;
+    addr += full ? WS : 0u;
+    lo = full ? nh : nl;
+    q4 = q;
+  }
 };
 
 // The code words of n consecutive windows (w: their 2n big-endian words + 2
@@ -527,6 +544,56 @@ __device__ __forceinline__ void decode_two_fsm(const std::uint32_t* wa, std::uin
     xa = a2;
     xb = b2;
   }
+}
+
+// decode_two_fsm for two runs whose symbol counts are known (the upload
+// check's lane_start offsets): each run's stage nibbles [start, end) with
+// end = ea / eb (absolute nibble positions, start = the sink's).  The byte
+// steps run through all NWIN windows + the 2 lookahead bytes; the symbols
+// the last 4 bytes complete past a run's end are dropped by position instead
+// of by the completion masks (no fsm_cm probes, no popcounts).  Returns the
+// end words' contents in ta / tb (the caller ORs them in, masked to the run).
+template <int NWIN = 4, int WS = 4, class FT = FsmPinned>
+__device__ __forceinline__ void decode_two_fsm_counted(const std::uint32_t* wa, std::uint32_t ga, std::uint32_t ea,
+                                                       PairSink<WS>& sa, std::uint32_t& ta, const std::uint32_t* wb,
+                                                       std::uint32_t gb, std::uint32_t eb, PairSink<WS>& sb,
+                                                       std::uint32_t& tb, std::uint32_t stage, const FT& ft = FT{}) {
+  constexpr int NB = 8 * NWIN, NS = 2 * NWIN + 1;
+  std::uint32_t sta[NS], stb[NS];
+#pragma unroll
+  for (int i = 0; i < NS; ++i) {
+    sta[i] = __funnelshift_l(wa[i + 1], wa[i], ga);
+    stb[i] = __funnelshift_l(wb[i + 1], wb[i], gb);
+  }
+  std::uint32_t xa = 0, xb = 0;
+#pragma unroll
+  for (int j = 0; j < NB - 2; j += 2) {  // every word these bytes complete belongs to the run
+    const std::uint32_t a1 = ft.entry(fsm_index(sta[j >> 2], xa, j));
+    const std::uint32_t b1 = ft.entry(fsm_index(stb[j >> 2], xb, j));
+    const std::uint32_t a2 = ft.entry(fsm_index(sta[(j + 1) >> 2], a1, j + 1));
+    const std::uint32_t b2 = ft.entry(fsm_index(stb[(j + 1) >> 2], b1, j + 1));
+    sa.put2(a1, a2);
+    sb.put2(b1, b2);
+    xa = a2;
+    xb = b2;
+  }
+  const std::uint32_t ewa = stage + 4 * (ea >> 3), ewb = stage + 4 * (eb >> 3);
+  ta = tb = 0;
+#pragma unroll
+  for (int j = NB - 2; j < NB + 2; j += 2) {
+    const std::uint32_t a1 = ft.entry(fsm_index(sta[j >> 2], xa, j));
+    const std::uint32_t b1 = ft.entry(fsm_index(stb[j >> 2], xb, j));
+    const std::uint32_t a2 = ft.entry(fsm_index(sta[(j + 1) >> 2], a1, j + 1));
+    const std::uint32_t b2 = ft.entry(fsm_index(stb[(j + 1) >> 2], b1, j + 1));
+    sa.put2_bounded(a1, a2, ewa, ta);
+    sb.put2_bounded(b1, b2, ewb, tb);
+    xa = a2;
+    xb = b2;
+  }
+  if (sa.addr == ewa) ta = sa.lo;
+  if (sb.addr == ewb) tb = sb.lo;
+  ta &= (1u << (4 * (ea & 7))) - 1;  // the run's nibbles of its end word (none when it ends on a boundary)
+  tb &= (1u << (4 * (eb & 7))) - 1;
 }
 
 // Where window (w0..w3, gap)'s reference walk stops: the start of the first

@@ -20,6 +20,9 @@
 namespace ecf8::dev {
 
 constexpr int kLaneWin = 8;     // windows per lane (Lmin >= 2)
+#ifndef ECF8_COUNTED
+#define ECF8_COUNTED 1  // verified direct tiles: runs end by the group offsets (0: by the completion masks)
+#endif
 constexpr int kSlotWords = 32;  // 256 nibbles: 8 windows x 32 or 4 x 64 symbols
 
 template <int LW>
@@ -424,8 +427,27 @@ __device__ __forceinline__ void direct_tile(const TensorDesc& d, const WarpInT<L
   const std::uint64_t pk_a = GPK ? 0 : fetch_packed(d, S0, data_end, ws, lane);
   __syncwarp();  // the zeroes are in place
   std::uint32_t ta_addr = 0, ta = 0, tb_addr = 0, tb = 0;
+  const std::uint32_t base = static_cast<std::uint32_t>(in.o0 - in.A) + off;
+#if ECF8_COUNTED
+  // run ends from the group offsets: group A ends where group B starts, group
+  // B where the next lane's group A starts (same reference block), else at
+  // the block's end; every run clamped to its block's outpos range
+  // (codec.cpp:239-246: only the tensor's last block can decode past it)
+  std::uint32_t end_a = 0, end_b = 0;
+  if constexpr (LW == 8) {
+    const std::uint32_t blk_end = static_cast<std::uint32_t>(in.o1 - in.A) + off;
+    const std::uint32_t da = base + (in.ls & 0xFFFFu), db = base + (in.ls >> 16);
+    const std::uint32_t next_da = __shfl_down_sync(0xffffffffu, da, 1);
+    const std::uint32_t lpb = static_cast<std::uint32_t>(in.nblk ? (in.nwin / in.nblk) / 8 : 1);  // lanes per block
+    const std::uint32_t nl = static_cast<std::uint32_t>(lane) + 1;
+    const bool next_same = nl < 32 && (nl % lpb) != 0 && nl * 8 < in.nwin;
+    end_a = min(max(db, da), blk_end);
+    end_b = min(max(next_same ? next_da : blk_end, db), blk_end);
+    end_a = max(end_a, min(da, blk_end));
+    end_b = max(end_b, min(db, blk_end));
+  }
+#endif
   if (static_cast<std::uint32_t>(lane) * LW < in.nwin) {
-    const std::uint32_t base = static_cast<std::uint32_t>(in.o0 - in.A) + off;
     std::uint32_t w[2 * LW + 2];
     w[0] = bswap32(in.w01.x), w[1] = bswap32(in.w01.y), w[2] = bswap32(in.w01.z), w[3] = bswap32(in.w01.w);
     w[4] = bswap32(in.w23.x), w[5] = bswap32(in.w23.y), w[6] = bswap32(in.w23.z), w[7] = bswap32(in.w23.w);
@@ -441,8 +463,21 @@ __device__ __forceinline__ void direct_tile(const TensorDesc& d, const WarpInT<L
       sa.q4 = 4 * (da & 7);
       sb.q4 = 4 * (db & 7);
       if (verified) {
+#if ECF8_COUNTED
+        const std::uint32_t st = smem_addr(ws.stage);
+        std::uint32_t xa, xb;
+        decode_two_fsm_counted<4, 4, FT>(w, (in.gaps >> 4) & 15u, end_a, sa, xa, w + 8, (in.gaps >> 20) & 15u, end_b,
+                                         sb, xb, st, ft);
+        // the end words (OR-ed in below, after every run's plain stores)
+        ta_addr = st + 4 * (end_a >> 3);
+        ta = xa;
+        tb_addr = st + 4 * (end_b >> 3);
+        tb = xb;
+        goto stored;
+#else
         decode_two_fsm<4, 4, FT>(w, (in.gaps >> 4) & 15u, (in.gnext >> 8) & 15u, sa, w + 8, (in.gaps >> 20) & 15u,
                                  (in.gnext >> 24) & 15u, sb, ft);
+#endif
       } else {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -455,6 +490,9 @@ __device__ __forceinline__ void direct_tile(const TensorDesc& d, const WarpInT<L
       tb = (sb.q4 & 31u) ? sb.lo : 0u;
       ta_addr = sa.addr;
       ta = (sa.q4 & 31u) ? sa.lo : 0u;
+#if ECF8_COUNTED
+    stored:;
+#endif
     } else {
       // one chain: the lane's 4-window group
       const std::uint32_t da = base + in.ls;
