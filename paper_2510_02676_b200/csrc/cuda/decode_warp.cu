@@ -306,8 +306,8 @@ cudaError_t launch_nw(const LaunchArgs& args, cudaStream_t s) {
 // bit.  The counts are summed per 4-window group and scanned per block
 // (lane_start: one u16 per group; the two groups of an 8-window lane in one
 // 32-bit word);
-// a block that decodes to more words than its outpos range (not the tensor's
-// last block) clears tile_direct.
+// a block that decodes to fewer words than its outpos range, or to more (but
+// the tensor's last block), clears tile_direct.
 __global__ void __launch_bounds__(256) verify_gaps_kernel(const TensorDesc d, std::uint64_t w_begin,
                                                           std::uint64_t n_win, std::uint64_t nb_total,
                                                           std::uint32_t* tile_ok, std::uint8_t* endgap,
@@ -363,9 +363,17 @@ __global__ void __launch_bounds__(256) verify_gaps_kernel(const TensorDesc d, st
           reinterpret_cast<std::uint32_t*>(lane_start)[wg >> 3] = excl | ((excl + v0) << 16);
           if ((i & (lpb - 1)) == lpb - 1 || wg + 8 >= n_win) {  // the block's last lane
             const std::uint64_t blk = wg >> log2T;
-            if (blk + 1 < nb_total && excl + v > d.outpos[blk + 1] - d.outpos[blk]) atomicOr(&over, 1u);
+            // direct placement needs every block to decode to exactly its
+            // range (the tensor's last block may decode past it: padding)
+            const std::uint64_t range = d.outpos[blk + 1] - d.outpos[blk];
+            if (excl + v < range || (blk + 1 < nb_total && excl + v > range)) atomicOr(&over, 1u);
           }
         }
+      }
+      __syncthreads();
+      if (threadIdx.x == 0 && over) {  // a block decodes past its range: no direct placement for this tile
+        const std::uint64_t v = w_tile >> 8;
+        atomicAnd(tile_direct + (v >> 5), ~(1u << (v & 31)));
       }
       __syncthreads();  // gsum / over are reused by the next tile
     }

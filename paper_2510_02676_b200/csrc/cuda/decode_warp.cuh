@@ -125,16 +125,15 @@ __device__ __forceinline__ void prefetch_tile_l2(const TensorDesc& d, std::uint6
   const std::uint64_t b0 = d.blk_begin + (tile - d.tile_begin) * m;
   const std::uint64_t nb = d.blk_end - b0 < m ? d.blk_end - b0 : m;
   const std::uint64_t w0 = b0 << log2T, nw = nb << log2T;
-  const void* p = nullptr;
-  std::uint64_t n = 0;
-  switch (lane) {
-    case 0: p = d.encoded + 8 * w0, n = 8 * nw + 8; break;
-    case 1: p = d.gaps + (w0 >> 1), n = nw >> 1; break;
-    case 2: p = d.outpos + b0, n = 8 * (nb + 1); break;
-    case 3: p = d.endgap ? d.endgap + (w0 >> 1) : nullptr, n = nw >> 1; break;
-    case 4: p = d.lane_start ? reinterpret_cast<const void*>(d.lane_start + (w0 >> 2)) : nullptr, n = nw >> 1; break;
-    default: break;
-  }
+  // branch-free: lane i picks section i (0 windows, 1 gaps, 2 block offsets,
+  // 3 end nibbles, 4 group offsets)
+  const std::uint8_t* p = d.encoded + 8 * w0;
+  std::uint64_t n = 8 * nw + 8;
+  p = lane == 1 ? d.gaps + (w0 >> 1) : p;
+  p = lane == 2 ? reinterpret_cast<const std::uint8_t*>(d.outpos + b0) : p;
+  p = lane == 3 ? (d.endgap ? d.endgap + (w0 >> 1) : nullptr) : p;
+  p = lane == 4 ? (d.lane_start ? reinterpret_cast<const std::uint8_t*>(d.lane_start + (w0 >> 2)) : nullptr) : p;
+  n = lane == 2 ? 8 * (nb + 1) : lane >= 1 ? nw >> 1 : n;
   if (p && n) prefetch_l2(p, n);
 }
 
@@ -418,14 +417,6 @@ __device__ __forceinline__ void direct_tile(const TensorDesc& d, const WarpInT<L
   const std::uint32_t data_end = off + static_cast<std::uint32_t>(in.E - in.A);
   const std::uint64_t S0 = in.A - off;
   __syncwarp();  // previous tile's write-back is done with the staging and the slots' packed bytes
-  {
-    const std::uint32_t st = smem_addr(ws.stage);
-    constexpr std::uint32_t n16 = sizeof(ws.stage) / 16;
-    for (std::uint32_t i = lane; i < n16; i += 32)
-      asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(st + 16 * i), "r"(0u) : "memory");
-  }
-  const std::uint64_t pk_a = GPK ? 0 : fetch_packed(d, S0, data_end, ws, lane);
-  __syncwarp();  // the zeroes are in place
   std::uint32_t ta_addr = 0, ta = 0, tb_addr = 0, tb = 0;
   const std::uint32_t base = static_cast<std::uint32_t>(in.o0 - in.A) + off;
 #if ECF8_COUNTED
@@ -438,15 +429,37 @@ __device__ __forceinline__ void direct_tile(const TensorDesc& d, const WarpInT<L
     const std::uint32_t blk_end = static_cast<std::uint32_t>(in.o1 - in.A) + off;
     const std::uint32_t da = base + (in.ls & 0xFFFFu), db = base + (in.ls >> 16);
     const std::uint32_t next_da = __shfl_down_sync(0xffffffffu, da, 1);
-    const std::uint32_t lpb = static_cast<std::uint32_t>(in.nblk ? (in.nwin / in.nblk) / 8 : 1);  // lanes per block
+    const std::uint32_t lpb_mask = (d.T >> 3) - 1;  // lanes per reference block - 1 (T >= 8)
     const std::uint32_t nl = static_cast<std::uint32_t>(lane) + 1;
-    const bool next_same = nl < 32 && (nl % lpb) != 0 && nl * 8 < in.nwin;
+    const bool next_same = nl < 32 && (nl & lpb_mask) != 0 && nl * 8 < in.nwin;
     end_a = min(max(db, da), blk_end);
     end_b = min(max(next_same ? next_da : blk_end, db), blk_end);
     end_a = max(end_a, min(da, blk_end));
     end_b = max(end_b, min(db, blk_end));
   }
 #endif
+  {
+    const std::uint32_t st = smem_addr(ws.stage);
+#if ECF8_COUNTED
+    if constexpr (LW == 8) {
+      // direct tiles cover [A, E) with the lanes' runs, back to back (every
+      // block decodes to exactly its range, the upload check): a word is
+      // either plain-stored by a run that fills it, or it holds a run's end
+      // and gets OR-ed -- only those end words need zeroes
+      if (static_cast<std::uint32_t>(lane) * LW < in.nwin) {
+        sts32(st + 4 * (end_a >> 3), 0u);
+        sts32(st + 4 * (end_b >> 3), 0u);
+      }
+    } else
+#endif
+    {
+      constexpr std::uint32_t n16 = sizeof(ws.stage) / 16;
+      for (std::uint32_t i = lane; i < n16; i += 32)
+        asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(st + 16 * i), "r"(0u) : "memory");
+    }
+  }
+  const std::uint64_t pk_a = GPK ? 0 : fetch_packed(d, S0, data_end, ws, lane);
+  __syncwarp();  // the zeroes are in place
   if (static_cast<std::uint32_t>(lane) * LW < in.nwin) {
     std::uint32_t w[2 * LW + 2];
     w[0] = bswap32(in.w01.x), w[1] = bswap32(in.w01.y), w[2] = bswap32(in.w01.z), w[3] = bswap32(in.w01.w);

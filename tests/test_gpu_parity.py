@@ -266,6 +266,32 @@ def test_inconsistent_gaps_fall_back_to_reference_semantics(orc):
     assert np.array_equal(codec.decode_parallel(t)[defined], want[defined])
 
 
+@pytest.mark.parametrize("T", [8, 64, 256])
+def test_block_decoding_past_its_range_is_clamped(orc, T):
+    # one block boundary moved down by one symbol (never encoder output):
+    # block b decodes one word more than its range (the reference clamps it,
+    # codec.cpp:239-251), block b + 1 one fewer (its last element is stale
+    # scratch in the reference: undefined, not compared).  The upload check
+    # must take such a tile off the direct-placement path, or block b's extra
+    # word would land on block b + 1's first element.
+    from paper_2510_02676_b200.device import DeviceTensor
+
+    x = codec.synth(1.8, 0.05, 300_000, 21 + T)
+    t = codec.encode_tensor(x, T).copy()
+    op = t.outpos
+    nb = len(op) - 1
+    b = nb // 2
+    op[b + 1] -= 1
+    d = tensor_dict(t)
+    want = orc.decode_parallel(d)
+    defined = np.ones(t.n_elem, bool)
+    defined[op[b + 2] - 1] = False
+    assert not np.array_equal(want[defined], x[defined])
+    got = DeviceTensor(t).decode().cpu().numpy()
+    assert np.array_equal(got[defined], want[defined])
+    assert np.array_equal(codec.decode_parallel(t)[defined], want[defined])
+
+
 @pytest.mark.gpu
 def test_batch_decode_in_cuda_graph():
     # the per-layer decode as a captured CUDA graph (programmatic dependent
