@@ -123,6 +123,7 @@ struct GlobalOut {
 template <bool WIDE, class WSm>
 __device__ __forceinline__ void warp_tile(const TensorDesc& d, const WarpIn& in, std::uint32_t log2T,
                                           std::uint32_t len_off, WSm& ws, int lane) {
+
   // slots interleaved word by word (word j of lane L at slot[32 j + L]): the
   // lanes' slot stores and reads hit 32 different banks
   const std::uint32_t slot = smem_addr(ws.slot + lane);
@@ -134,7 +135,8 @@ __device__ __forceinline__ void warp_tile(const TensorDesc& d, const WarpIn& in,
     const bool verified = tile_verified(d, in, log2T);
     const std::uint32_t v = static_cast<std::uint32_t>((in.b0 << log2T) >> 8);  // the tile's verification tile
     if ((in.dir >> (v & 31)) & 1u) {  // every lane's output offset known: decode in place
-      direct_tile<kWbUnroll>(
+      // the packed sign/mantissa bytes come from L2 at write-back (prefetched at the tile's start)
+      direct_tile<kWbUnroll, kLaneWin, true>(
           d, in, ws, lane, [&] { return GlobalOut{d.out + ((in.A & ~std::uint64_t{15}) - d.out_offset)}; }, verified);
       return;
     }
@@ -257,6 +259,11 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_warp_kernel(const LaunchArg
         if (lane == 0) claim = atomicAdd(&next_tile, 1u);
         const std::uint64_t next = seg + __shfl_sync(0xffffffffu, claim, 0);
         if (next < seg_end && lane < 5) prefetch_tile_l2(d, next, log2T, lane);
+        if (lane == 0) {  // this tile's sign/mantissa bytes -> L2 (direct tiles read them at write-back)
+          const std::uint64_t p0 = (cur.A >> 1) & ~std::uint64_t{15};
+          const std::uint32_t bytes = static_cast<std::uint32_t>((((cur.E + 1) >> 1) - p0 + 15) & ~std::uint64_t{15});
+          if (bytes) prefetch_l2(d.packed + p0, bytes);
+        }
         warp_tile<WIDE>(d, cur, log2T, len_off, ws, lane);
         tile = next;
       }

@@ -1,0 +1,9 @@
+#!/bin/bash
+timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/r2ah_pytest.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/r2ah_pytest.log
+for rep in 1 2; do
+for v in main clip; do
+  if [ $v = main ]; then unset ECF8_LIB; else export ECF8_LIB=build/var/$v/libecf8_b200.so; fi
+  echo -n "$v: "; timeout 300 python bench.py --steps 20 --warmup 3 --e2e-steps 0 --cpu-seconds 0 --no-verify 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.readline()); print(d['value'], d['clocks']['sm_mhz'], d['clocks']['reasons'])"
+done; done
+unset ECF8_LIB
+timeout 300 python bench.py --workload llama3-70b-fused --steps 10 --warmup 3 2>&1 >/dev/null | grep "fused m="
