@@ -12,7 +12,8 @@ enough for the sanitizers' replay:
   * the decode-fused GEMM with multi-K-tile CTA runs (A-ring wrap, stage
     release, TMEM accumulation across K tiles, multi-segment epilogues),
     m <= 128 and m > 128 (single X stage), E4M3 and E5M2;
-  * the device encoder (histogram, chunk scan, emit).
+  * the device encoder (histogram, chunk scan, emit);
+  * the native E5M2 decoder (e5_decode_kernel, T 8 / 256 / 1024).
 Each output is checked bit-exact against the original bytes (the encoder's
 input), so a sanitizer-clean run is also a correct one.  The reference
 schedule argument (blocks write disjoint output ranges) is
@@ -82,6 +83,16 @@ def fused_cases(n, k, ms, fmt):
         print(f"fused {n}x{k} {fmt} m={m} split_k={lin.split_k} rel err {err:.2e} ok", flush=True)
 
 
+def e5_cases():
+    from paper_2510_02676_b200 import e5m2
+
+    for n, T, seed in [(200_003, 256, 51), (33_000, 8, 52), (70_000, 1024, 53), (1, 32, 54)]:
+        x = codec.synth(1.8, 0.05, n, seed, fmt="e5m2")
+        got = e5m2.E5DeviceTensor(e5m2.encode(x, T)).decode().cpu().numpy()
+        assert np.array_equal(got, x), (n, T)
+        print(f"e5m2 native n={n} T={T} ok", flush=True)
+
+
 def encode_cases():
     x = codec.synth(1.8, 0.05, 300_000, 41)
     xt = torch.from_numpy(x).cuda()
@@ -100,9 +111,11 @@ if __name__ == "__main__":
         # the 5-stage A ring wraps); k = 128 at n = 128 * 518: 3-4 segments per CTA
         fused_cases(1024, 4096, [16, 200], "e4m3")
         fused_cases(2048, 8192, [1, 130], "e4m3")
-        fused_cases(128 * 518, 128, [16], "e4m3")
+        fused_cases(128 * 518, 128, [16, 200], "e4m3")  # m = 200: 2 accumulator buffers reused round-robin
         fused_cases(1024, 2048, [64], "e5m2")
     if which in ("all", "encode"):
         encode_cases()
+    if which in ("all", "e5"):
+        e5_cases()
     torch.cuda.synchronize()
     print("sanitize cases done")
