@@ -137,6 +137,7 @@ struct DevTables {
   std::uint64_t lenpack = 0;
   std::uint32_t* fsm = nullptr;  // byte-step decoder (tables.hpp), nullptr when the code has none
   std::uint8_t* fsm_cm = nullptr;
+  std::uint64_t* fsm64 = nullptr;  // its 64-bit form for codes with a 1-bit word
 };
 
 const DevTables& device_tables(const std::uint8_t lengths[16]) {
@@ -168,6 +169,12 @@ const DevTables& device_tables(const std::uint8_t lengths[16]) {
     d.fsm_cm = static_cast<std::uint8_t*>(q) + t->fsm.size() * 4;
     cu(cudaMemcpy(d.fsm, t->fsm.data(), t->fsm.size() * 4, cudaMemcpyHostToDevice), "upload tables");
     cu(cudaMemcpy(d.fsm_cm, t->fsm_cm.data(), t->fsm_cm.size(), cudaMemcpyHostToDevice), "upload tables");
+  }
+  if (t->fsm64_ok) {
+    void* q = nullptr;
+    cu(cudaMalloc(&q, t->fsm64.size() * 8), "cudaMalloc(tables)");
+    d.fsm64 = static_cast<std::uint64_t*>(q);
+    cu(cudaMemcpy(d.fsm64, t->fsm64.data(), t->fsm64.size() * 8, cudaMemcpyHostToDevice), "upload tables");
   }
   return cache.emplace(std::make_pair(dev, key), d).first->second;
 }
@@ -342,7 +349,7 @@ void upload_into(ecf8_dev_tensor* t, const ecf8_sections* s, std::uint64_t nb, c
 // keep the reference's window-by-window semantics.
 void verify_into(ecf8_dev_tensor* t, cudaStream_t st) {
   static const bool off = std::getenv("ECF8_NO_CONT_WALK") != nullptr;  // A/B runs
-  const int vid = t->n_elem ? ecf8::dev::variant_for(t->T, t->desc.lmin, t->desc.fsm != nullptr).id : -1;
+  const int vid = t->n_elem ? ecf8::dev::variant_for(t->T, t->desc.lmin, t->desc.fsm != nullptr, t->desc.fsm64 != nullptr).id : -1;
   if (off || (vid != 4 && vid != 5)) return;
   std::uint32_t* const ok = t->ok_bits;
   cu(cudaMemsetAsync(ok, 0xFF, 4 * ((t->n_vtiles + 31) / 32), st), "memset(tile_ok)");
@@ -355,12 +362,32 @@ void verify_into(ecf8_dev_tensor* t, cudaStream_t st) {
     t->desc.lane_start = t->lane_start;
     t->desc.tile_direct = t->direct_bits;
   }
+  // Variant 6 (1-bit codes by byte steps) places every tile directly and has
+  // no per-window fallback: it is chosen only when every tile passed (one
+  // read-back of the two tile bitmaps; tensors of crafted streams keep
+  // variant 5).
+  static const bool no64 = std::getenv("ECF8_NO_FSM64") != nullptr;  // A/B runs
+  const DevTables& tb = device_tables(t->lengths);
+  if (vid == 5 && tb.fsm64 && !no64 && t->T >= 8 && t->T <= 256) {
+    const std::size_t words = (t->n_vtiles + 31) / 32;
+    std::vector<std::uint32_t> okb(words), dirb(words);
+    cu(cudaMemcpyAsync(okb.data(), ok, 4 * words, cudaMemcpyDeviceToHost, st), "D2H tile_ok");
+    cu(cudaMemcpyAsync(dirb.data(), t->direct_bits, 4 * words, cudaMemcpyDeviceToHost, st), "D2H tile_direct");
+    cu(cudaStreamSynchronize(st), "sync");
+    bool all = true;
+    for (std::uint64_t v = 0; v < t->n_vtiles; ++v) all &= ((okb[v >> 5] & dirb[v >> 5]) >> (v & 31)) & 1u;
+    if (all) {
+      t->desc.lane_start = t->lane_start;
+      t->desc.tile_direct = t->direct_bits;
+      t->desc.fsm64 = tb.fsm64;
+    }
+  }
 }
 
 // Single-descriptor launch: the descriptor rides in the kernel parameters.
 int launch_one(const TensorDesc& d, cudaStream_t st, int variant_override = -1) {
   if (d.blk_end <= d.blk_begin) return ECF8_OK;
-  ecf8::dev::Variant v = ecf8::dev::variant_for(d.T, d.lmin, d.fsm != nullptr);
+  ecf8::dev::Variant v = ecf8::dev::variant_for(d.T, d.lmin, d.fsm != nullptr, d.fsm64 != nullptr);
   if (variant_override >= 0) v.id = variant_override;
   ecf8::dev::LaunchArgs a{};
   a.descs = nullptr;
@@ -374,7 +401,7 @@ int launch_one(const TensorDesc& d, cudaStream_t st, int variant_override = -1) 
 
 // Launch variant for a device tensor.
 int tensor_variant(const ecf8_dev_tensor* t) {
-  return ecf8::dev::variant_for(t->T, t->desc.lmin, t->desc.fsm != nullptr).id;
+  return ecf8::dev::variant_for(t->T, t->desc.lmin, t->desc.fsm != nullptr, t->desc.fsm64 != nullptr).id;
 }
 
 // Per-thread state of the host-span path: three streams (copy-in, decode,
@@ -878,14 +905,14 @@ int ecf8_batch_create(const ecf8_dev_tensor* const* ts, uint8_t* const* d_outs, 
     auto b = std::make_unique<ecf8_batch>();
     for (int i = 0; i < count; ++i)
       if (ts[i] && ts[i]->pooled) b->pooled.push_back(ts[i]);
-    for (int kw = 0; kw < 6; ++kw) {  // one launch per kernel variant present (ids 0..5)
+    for (int kw = 0; kw < 7; ++kw) {  // one launch per kernel variant present (ids 0..6)
       std::vector<TensorDesc> group;
       std::uint64_t tiles = 0;
       int kwin_tile = 1;
       for (int i = 0; i < count; ++i) {
         const ecf8_dev_tensor* t = ts[i];
         if (!t) return fail(ECF8_EINVAL, "null tensor");
-        const ecf8::dev::Variant v = ecf8::dev::variant_for(t->T, t->desc.lmin, t->desc.fsm != nullptr);
+        const ecf8::dev::Variant v = ecf8::dev::variant_for(t->T, t->desc.lmin, t->desc.fsm != nullptr, t->desc.fsm64 != nullptr);
         if (t->n_elem == 0 || tensor_variant(t) != kw) continue;
         kwin_tile = v.tile_win;
         if (!d_outs[i] || (reinterpret_cast<std::uintptr_t>(d_outs[i]) & 15))

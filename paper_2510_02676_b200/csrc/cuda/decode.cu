@@ -38,6 +38,7 @@ bool warp_variant_enabled() {
 }
 
 cudaError_t launch_decode_warp(const LaunchArgs& args, cudaStream_t s);       // decode_warp.cu
+cudaError_t launch_decode_fsm64(const LaunchArgs& args, cudaStream_t s);      // decode_warp.cu
 cudaError_t launch_decode_warp_wide(const LaunchArgs& args, cudaStream_t s);  // decode_warp.cu (1-bit codes)
 
 namespace {
@@ -388,6 +389,7 @@ cudaError_t launch_decode(const LaunchArgs& args, int variant, cudaStream_t stre
     case 3: return launch_k<4, 32, 2>(args, stream);
     case 4: return launch_decode_warp(args, stream);
     case 5: return launch_decode_warp_wide(args, stream);
+    case 6: return launch_decode_fsm64(args, stream);
     default: return cudaErrorInvalidValue;
   }
 }

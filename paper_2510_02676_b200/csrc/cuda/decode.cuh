@@ -21,6 +21,7 @@ struct TensorDesc {
   const std::uint32_t* tile_ok;  // bit v: gaps of windows [256v, 256v+256) verified (nullptr: none)
   const std::uint32_t* fsm;      // tables.hpp byte-step decoder (nullptr: the code has none)
   const std::uint8_t* fsm_cm;    // its completion masks
+  const std::uint64_t* fsm64;    // 64-bit byte-step decoder for 1-bit codes; set only when every tile is direct (variant 6)
   const std::uint8_t* endgap;    // per window, gap layout: where its reference walk stops, minus 64 (upload check)
   const std::uint16_t* lane_start;   // per 4-window group: first output element, relative to its block's outpos
   const std::uint32_t* tile_direct;  // bit v: tile v's blocks (but the tensor's last) decode to exactly their ranges
@@ -64,9 +65,12 @@ struct Variant {
 bool warp_variant_enabled();  // false when ECF8_NO_WARP_KERNEL=1 (A/B runs)
 
 // fsm: the code has a byte-step decoder (tables.hpp; complete, Lmin >= 2),
-// which variant 4 needs; other codes with T in [8, 256] take variant 5.
-inline Variant variant_for(std::uint32_t T, std::uint32_t lmin, bool fsm = true) {
+// which variant 4 needs; fsm64: a complete code with a 1-bit word whose
+// tensor passed the upload check on every tile (variant 6, byte steps with
+// 64-bit entries); other codes with T in [8, 256] take variant 5.
+inline Variant variant_for(std::uint32_t T, std::uint32_t lmin, bool fsm = true, bool fsm64 = false) {
   if (lmin >= 2 && fsm && T >= 8 && T <= 256 && warp_variant_enabled()) return {8, 32, 4, 256};
+  if (lmin == 1 && fsm64 && T >= 8 && T <= 256 && warp_variant_enabled()) return {8, 64, 6, 256};
   if (lmin >= 1 && T >= 8 && T <= 256 && warp_variant_enabled()) return {8, 64, 5, 256};
   if (T == 1) return {1, 8, 0, kThreads};
   if (T == 2) return {2, 16, 1, 2 * kThreads};

@@ -546,6 +546,88 @@ __device__ __forceinline__ void decode_two_fsm(const std::uint32_t* wa, std::uin
   }
 }
 
+// One byte step of the 64-bit table (1-bit codes): up to 8 symbols (32
+// bits) per byte; h = the entry's high word, n4 in bits 0..5 (<= 32), the
+// state in bits 8..11.  q4 adds h whole: bits 0..4 stay exact and bit 5
+// toggles when a word fills (n4 = 32 fills exactly one).
+template <int WS>
+__device__ __forceinline__ void put1(PairSink<WS>& k, std::uint32_t c, std::uint32_t h) {
+  const std::uint32_t q = k.q4 + h;
+  const std::uint32_t nl = k.lo | __funnelshift_l(0u, c, k.q4);
+  const std::uint32_t nh = __funnelshift_l(c, 0u, k.q4);
+  const bool full = ((q ^ k.q4) & 32u) != 0;
+  if (full) sts32(k.addr, nl);
+  k.addr += full ? WS : 0u;
+  k.lo = full ? nh : nl;
+  k.q4 = q;
+}
+template <int WS>
+__device__ __forceinline__ void put1_bounded(PairSink<WS>& k, std::uint32_t c, std::uint32_t h, std::uint32_t ew,
+                                             std::uint32_t& tail) {
+  const std::uint32_t q = k.q4 + h;
+  const std::uint32_t nl = k.lo | __funnelshift_l(0u, c, k.q4);
+  const std::uint32_t nh = __funnelshift_l(c, 0u, k.q4);
+  const bool full = ((q ^ k.q4) & 32u) != 0;
+  if (full && k.addr < ew) sts32(k.addr, nl);
+  if (full && k.addr == ew) tail = nl;
+  k.addr += full ? WS : 0u;
+  k.lo = full ? nh : nl;
+  k.q4 = q;
+}
+
+// The 64-bit table staged in shared memory (address in a register).
+struct Fsm64At {
+  std::uint32_t tab;
+  __device__ __forceinline__ uint2 entry(std::uint32_t idx) const {
+    std::uint32_t a;
+    uint2 v;
+    asm("mad.lo.u32 %0, %1, 8, %2;" : "=r"(a) : "r"(idx), "r"(tab));
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+    return v;
+  }
+};
+
+// decode_two_fsm_counted with the 64-bit table: one byte per step (a byte
+// can complete 8 one-bit words, 32 bits of symbols).
+template <int NWIN = 4, int WS = 4>
+__device__ __forceinline__ void decode_two_fsm64_counted(const std::uint32_t* wa, std::uint32_t ga, std::uint32_t ea,
+                                                         PairSink<WS>& sa, std::uint32_t& ta, const std::uint32_t* wb,
+                                                         std::uint32_t gb, std::uint32_t eb, PairSink<WS>& sb,
+                                                         std::uint32_t& tb, std::uint32_t stage, const Fsm64At& ft) {
+  constexpr int NB = 8 * NWIN, NS = 2 * NWIN + 1;
+  std::uint32_t sta[NS], stb[NS];
+#pragma unroll
+  for (int i = 0; i < NS; ++i) {
+    sta[i] = __funnelshift_l(wa[i + 1], wa[i], ga);
+    stb[i] = __funnelshift_l(wb[i + 1], wb[i], gb);
+  }
+  std::uint32_t ha = 0, hb = 0;  // previous entries' high words (state in byte 1; root = 0)
+#pragma unroll
+  for (int j = 0; j < NB - 2; ++j) {
+    const uint2 a = ft.entry(fsm_index(sta[j >> 2], ha, j));
+    const uint2 b = ft.entry(fsm_index(stb[j >> 2], hb, j));
+    put1(sa, a.x, a.y);
+    put1(sb, b.x, b.y);
+    ha = a.y;
+    hb = b.y;
+  }
+  const std::uint32_t ewa = stage + 4 * (ea >> 3), ewb = stage + 4 * (eb >> 3);
+  ta = tb = 0;
+#pragma unroll
+  for (int j = NB - 2; j < NB + 2; ++j) {
+    const uint2 a = ft.entry(fsm_index(sta[j >> 2], ha, j));
+    const uint2 b = ft.entry(fsm_index(stb[j >> 2], hb, j));
+    put1_bounded(sa, a.x, a.y, ewa, ta);
+    put1_bounded(sb, b.x, b.y, ewb, tb);
+    ha = a.y;
+    hb = b.y;
+  }
+  if (sa.addr == ewa) ta = sa.lo;
+  if (sb.addr == ewb) tb = sb.lo;
+  ta &= (1u << (4 * (ea & 7))) - 1;
+  tb &= (1u << (4 * (eb & 7))) - 1;
+}
+
 // decode_two_fsm for two runs whose symbol counts are known (the upload
 // check's lane_start offsets): each run's stage nibbles [start, end) with
 // end = ea / eb (absolute nibble positions, start = the sink's).  The byte

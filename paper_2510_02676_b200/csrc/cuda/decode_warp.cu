@@ -273,6 +273,81 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_warp_kernel(const LaunchArg
   }
 }
 
+// ---- variant 6: codes with a 1-bit word by 64-bit byte steps (E5M2 bytes
+// through the reference format, small-gamma E4M3).  Same structure as the
+// byte-step loop above; every tile is direct (checked at upload), the
+// packed bytes come from L2, the 32 KB table is staged per segment.
+using Fsm64WarpSmem = WarpPipeSmem<1, 2 * 32 * kSlotWords + 8>;  // 16384 nibbles + alignment
+__shared__ __align__(16) std::uint64_t g_fsm64[256 * kFsmStates];
+__shared__ unsigned g6_next_tile;
+__shared__ TensorDesc g6_desc;
+
+template <int NW>
+__global__ void __launch_bounds__(NW * 32, 1) decode_fsm64_kernel(const LaunchArgs args) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  Fsm64WarpSmem& ws = reinterpret_cast<Fsm64WarpSmem*>(smem_raw)[warp];
+  asm volatile("griddepcontrol.launch_dependents;");
+  const std::uint64_t total_tiles = args.total_tiles;
+  const std::uint64_t t_lo = total_tiles * blockIdx.x / gridDim.x;
+  const std::uint64_t t_hi = total_tiles * (blockIdx.x + 1) / gridDim.x;
+  const Fsm64At ft{smem_addr(g_fsm64)};
+  for (std::uint64_t seg = t_lo; seg < t_hi;) {
+    std::uint64_t seg_end;
+    int di = 0;
+    if (args.descs) {
+      if (args.n_desc <= 32) {
+        const bool le = lane < args.n_desc && args.descs[lane].tile_begin <= seg;
+        di = 31 - __clz(__ballot_sync(0xffffffffu, le) | 1u);
+      } else {
+        di = find_desc(args.descs, args.n_desc, seg);
+      }
+      seg_end = (di + 1 < args.n_desc) ? args.descs[di + 1].tile_begin : total_tiles;
+    } else {
+      seg_end = total_tiles;
+    }
+    if (seg_end > t_hi) seg_end = t_hi;
+    __syncthreads();
+    if (warp == 0) {
+      const auto* src = reinterpret_cast<const unsigned long long*>(args.descs ? &args.descs[di] : &args.inline_desc);
+      if (lane < static_cast<int>(sizeof(TensorDesc) / 8)) reinterpret_cast<unsigned long long*>(&g6_desc)[lane] = src[lane];
+    }
+    __syncthreads();
+    const TensorDesc& d = g6_desc;
+    const std::uint32_t log2T = 31 - __clz(d.T);
+    {
+      const uint4* f4 = reinterpret_cast<const uint4*>(d.fsm64);
+      uint4* s4 = reinterpret_cast<uint4*>(g_fsm64);
+      for (int i = threadIdx.x; i < 256 * kFsmStates / 2; i += NW * 32) s4[i] = __ldg(f4 + i);
+    }
+    if (threadIdx.x == 0) g6_next_tile = NW;
+    __syncthreads();
+    std::uint64_t tile = seg + warp;
+    if (tile < seg_end && lane < 5) prefetch_tile_l2(d, tile, log2T, lane);
+    while (tile < seg_end) {
+      WarpIn cur;
+      load_warp_tile<kLaneWin, true>(d, tile, log2T, lane, cur);
+      unsigned claim = 0;
+      if (lane == 0) claim = atomicAdd(&g6_next_tile, 1u);
+      const std::uint64_t next = seg + __shfl_sync(0xffffffffu, claim, 0);
+      if (next < seg_end && lane < 5) prefetch_tile_l2(d, next, log2T, lane);
+      if (lane == 0) {  // this tile's sign/mantissa bytes -> L2 (read at write-back)
+        const std::uint64_t p0 = (cur.A >> 1) & ~std::uint64_t{15};
+        const std::uint32_t bytes = static_cast<std::uint32_t>((((cur.E + 1) >> 1) - p0 + 15) & ~std::uint64_t{15});
+        if (bytes) prefetch_l2(d.packed + p0, bytes);
+      }
+      direct_tile64<kWbUnroll>(
+          d, cur, ws, lane, [&] { return GlobalOut{d.out + ((cur.A & ~std::uint64_t{15}) - d.out_offset)}; }, ft);
+      tile = next;
+    }
+    seg = seg_end;
+  }
+}
+
+#ifndef ECF8_FSM64_WARPS
+#define ECF8_FSM64_WARPS 22  // 22 x 8.2 KB of staging + the 32 KB table
+#endif
+
 template <int NW, bool WIDE = false>
 cudaError_t launch_nw(const LaunchArgs& args, cudaStream_t s) {
   static int grid_cap = 0;
@@ -404,6 +479,38 @@ cudaError_t launch_decode_warp(const LaunchArgs& args, cudaStream_t s) {
 
 // Variant 5 (1-bit codes): 12 warps x 16.5 KB of warp state.
 cudaError_t launch_decode_warp_wide(const LaunchArgs& args, cudaStream_t s) { return launch_nw<12, true>(args, s); }
+
+// Variant 6 (1-bit codes, every tile direct): 64-bit byte steps.
+cudaError_t launch_decode_fsm64(const LaunchArgs& args, cudaStream_t s) {
+  constexpr int NW = ECF8_FSM64_WARPS;
+  static int grid_cap = 0;
+  const int smem = static_cast<int>(sizeof(Fsm64WarpSmem)) * NW;
+  if (grid_cap == 0) {
+    cudaError_t e = cudaFuncSetAttribute(decode_fsm64_kernel<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_fsm64_kernel<NW>, NW * 32, smem);
+    if (e != cudaSuccess) return e;
+    grid_cap = sms * (per_sm > 0 ? per_sm : 1);
+  }
+  const std::uint64_t want = (args.total_tiles + NW - 1) / NW;
+  const std::uint64_t grid = want < static_cast<std::uint64_t>(grid_cap) ? want : grid_cap;
+  if (grid == 0) return cudaSuccess;
+  static const bool pdl = std::getenv("ECF8_NO_PDL") == nullptr;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(NW * 32);
+  cfg.dynamicSmemBytes = static_cast<std::size_t>(smem);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, decode_fsm64_kernel<NW>, args);
+}
 
 cudaError_t launch_verify_gaps(const TensorDesc& d, std::uint64_t nb_total, std::uint32_t* tile_ok,
                                std::uint8_t* endgap, std::uint16_t* lane_start, std::uint32_t* tile_direct,

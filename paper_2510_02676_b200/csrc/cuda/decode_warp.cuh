@@ -533,4 +533,52 @@ __device__ __forceinline__ void direct_tile(const TensorDesc& d, const WarpInT<L
   write_back<UNROLL, GPK>(S0, off, data_end, pk_a, ws, lane, out, d.packed);
 }
 
+// ---- direct tile, 64-bit byte steps (variant 6: codes with a 1-bit word;
+// every tile of the tensor passed the upload check, so every lane's run is
+// placed directly and ends by its group offsets).  Windows hold up to 64
+// symbols: the staging tile holds 16384 nibbles.
+template <int UNROLL, class WSm, class MkOut>
+__device__ __forceinline__ void direct_tile64(const TensorDesc& d, const WarpInT<8>& in, WSm& ws, int lane,
+                                              const MkOut& mk_out, const Fsm64At& ft) {
+  const std::uint32_t off = static_cast<std::uint32_t>(in.A & 15);
+  const std::uint32_t data_end = off + static_cast<std::uint32_t>(in.E - in.A);
+  const std::uint64_t S0 = in.A - off;
+  __syncwarp();  // previous tile's write-back is done with the staging tile
+  const std::uint32_t st = smem_addr(ws.stage);
+  const std::uint32_t base = static_cast<std::uint32_t>(in.o0 - in.A) + off;
+  const std::uint32_t blk_end = static_cast<std::uint32_t>(in.o1 - in.A) + off;
+  const std::uint32_t da = base + (in.ls & 0xFFFFu), db = base + (in.ls >> 16);
+  const std::uint32_t next_da = __shfl_down_sync(0xffffffffu, da, 1);
+  const std::uint32_t nl = static_cast<std::uint32_t>(lane) + 1;
+  const bool next_same = nl < 32 && (nl & ((d.T >> 3) - 1)) != 0 && nl * 8 < in.nwin;
+  const std::uint32_t end_a = max(min(max(db, da), blk_end), min(da, blk_end));
+  const std::uint32_t end_b = max(min(max(next_same ? next_da : blk_end, db), blk_end), min(db, blk_end));
+  const bool active = static_cast<std::uint32_t>(lane) * 8 < in.nwin;
+  if (active) {  // only the runs' end words need zeroes (see direct_tile)
+    sts32(st + 4 * (end_a >> 3), 0u);
+    sts32(st + 4 * (end_b >> 3), 0u);
+  }
+  __syncwarp();
+  std::uint32_t ta = 0, tb = 0;
+  if (active) {
+    std::uint32_t w[18];
+    w[0] = bswap32(in.w01.x), w[1] = bswap32(in.w01.y), w[2] = bswap32(in.w01.z), w[3] = bswap32(in.w01.w);
+    w[4] = bswap32(in.w23.x), w[5] = bswap32(in.w23.y), w[6] = bswap32(in.w23.z), w[7] = bswap32(in.w23.w);
+    w[8] = bswap32(in.w45.x), w[9] = bswap32(in.w45.y), w[10] = bswap32(in.w45.z), w[11] = bswap32(in.w45.w);
+    w[12] = bswap32(in.w67.x), w[13] = bswap32(in.w67.y), w[14] = bswap32(in.w67.z), w[15] = bswap32(in.w67.w);
+    w[16] = bswap32(in.w8.x), w[17] = bswap32(in.w8.y);
+    PairSink<4> sa{st + 4 * (da >> 3)}, sb{st + 4 * (db >> 3)};
+    sa.q4 = 4 * (da & 7);
+    sb.q4 = 4 * (db & 7);
+    decode_two_fsm64_counted<4, 4>(w, (in.gaps >> 4) & 15u, end_a, sa, ta, w + 8, (in.gaps >> 20) & 15u, end_b, sb, tb,
+                                   st, ft);
+  }
+  __syncwarp();  // every run's plain stores are in place
+  if (ta) asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(st + 4 * (end_a >> 3)), "r"(ta) : "memory");
+  if (tb) asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(st + 4 * (end_b >> 3)), "r"(tb) : "memory");
+  __syncwarp();
+  auto out = mk_out();
+  write_back<UNROLL, true>(S0, off, data_end, 0, ws, lane, out, d.packed);
+}
+
 }  // namespace ecf8::dev

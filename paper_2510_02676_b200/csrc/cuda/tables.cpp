@@ -27,6 +27,8 @@ void build_fsm(const CodeTable& code, DecodeTables& t) {
   t.fsm.assign(kFsmStates * 256, 0);
   t.fsm_cm.assign(kFsmStates * 256, 0);
   t.fsm_ok = false;
+  t.fsm64_ok = false;
+  t.fsm64.clear();
   // leaf[(len, word)] = symbol; node ids for proper prefixes of words
   std::map<std::pair<int, std::uint32_t>, int> leaf, node;
   double kraft = 0;
@@ -39,7 +41,9 @@ void build_fsm(const CodeTable& code, DecodeTables& t) {
     kraft += std::ldexp(1.0, -l);
     leaf[{l, code.codes[s]}] = s;
   }
-  if (present < 2 || lmin < 2 || kraft != 1.0) return;
+  if (present < 2 || kraft != 1.0) return;
+  const bool wide = lmin < 2;  // a 1-bit word: up to 8 words per byte -> 64-bit entries
+  if (wide) t.fsm64.assign(kFsmStates * 256, 0);
   node[{0, 0}] = 0;
   for (int l = 1; l <= 16; ++l)  // breadth-first ids
     for (const auto& [k, s] : leaf)
@@ -57,7 +61,7 @@ void build_fsm(const CodeTable& code, DecodeTables& t) {
         v = (v << 1) | ((b >> (7 - i)) & 1u);
         auto f = leaf.find({l, v});
         if (f != leaf.end()) {
-          if (n == 4) return;  // cannot happen with words >= 2 bits
+          if (!wide && n == 4) return;  // cannot happen with words >= 2 bits
           syms |= static_cast<std::uint32_t>(f->second) << (4 * n);
           cm |= 1u << i;
           ++n;
@@ -68,11 +72,15 @@ void build_fsm(const CodeTable& code, DecodeTables& t) {
         }
       }
       const std::uint32_t next = static_cast<std::uint32_t>(node.at({l, v}));
-      t.fsm[id * 256 + b] = (4 * n) | (next << 8) | (syms << 16);
+      if (wide)
+        t.fsm64[id * 256 + b] = syms | (std::uint64_t{4 * n} << 32) | (std::uint64_t{next} << 40);
+      else
+        t.fsm[id * 256 + b] = (4 * n) | (next << 8) | (syms << 16);
       t.fsm_cm[id * 256 + b] = static_cast<std::uint8_t>(cm);
     }
   }
-  t.fsm_ok = true;
+  if (wide) t.fsm64_ok = true;
+  else t.fsm_ok = true;
 }
 }  // namespace
 

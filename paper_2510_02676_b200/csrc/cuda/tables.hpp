@@ -54,6 +54,13 @@ struct DecodeTables {
   bool fsm_ok = false;
   std::vector<std::uint32_t> fsm;     // kFsmStates * 256 (zeros when !fsm_ok)
   std::vector<std::uint8_t> fsm_cm;   // kFsmStates * 256
+  // The same state machine for complete codes with a 1-bit word (up to 8
+  // words per byte): fsm64[state * 256 + byte] (uint64)
+  //   bits  0..31  the completed words' symbols, first lowest (4 bits each)
+  //   bits 32..37  n4 = 4 * words completed (<= 32)
+  //   bits 40..43  next state
+  bool fsm64_ok = false;
+  std::vector<std::uint64_t> fsm64;   // kFsmStates * 256 (empty when !fsm64_ok)
 };
 
 // Throws std::invalid_argument("invalid length vector") like the reference.

@@ -340,3 +340,62 @@ def test_decompress_to_sink_matches_decompress():
     with pytest.raises(Ecf8Error, match="sink write failed"):
         codec.decompress_to(blob, bad)
     assert rng is not None
+
+
+@pytest.mark.parametrize("T", [8, 32, 128, 256])
+@pytest.mark.parametrize("n,fmt,gamma", [(3_000_001, "e5m2", 0.05), (777_777, "e5m2", 1.0), (500_000, "e4m3", 0.002),
+                                         (1, "e5m2", 0.05), (4099, "e5m2", 0.05)])
+def test_one_bit_codes_take_the_64bit_byte_steps(orc, T, n, fmt, gamma):
+    # codes with a 1-bit word (E5M2 bytes through the reference format,
+    # small-gamma E4M3): variant 6 when every tile passes the upload check
+    from paper_2510_02676_b200.device import DeviceTensor
+
+    x = codec.synth(1.8, gamma, n, 70 + T, fmt=fmt)
+    t = codec.encode_tensor(x, T)
+    lengths = [l for l in t.lengths if l]
+    if len(lengths) < 2 or min(lengths) != 1:
+        pytest.skip("no 1-bit word in this code")
+    d = DeviceTensor(t)
+    assert d.kernel_variant == 6
+    got = d.decode().cpu().numpy()
+    assert np.array_equal(got, x)
+    assert np.array_equal(got, orc.decode_parallel(tensor_dict(t)))
+
+
+def test_one_bit_code_with_corrupt_gaps_keeps_variant_5(orc):
+    from paper_2510_02676_b200.device import DeviceTensor
+
+    x = codec.synth(1.8, 0.05, 400_000, 77, fmt="e5m2")
+    t = codec.encode_tensor(x, 256).copy()
+    assert min(l for l in t.lengths if l) == 1
+    g = np.asarray(t.gaps)
+    g[333] = ((((g[333] >> 4) + 5) & 15) << 4) | (g[333] & 15)
+    d = DeviceTensor(t)
+    assert d.kernel_variant == 5
+    want = orc.decode_parallel(tensor_dict(t))
+    T, enc, op, dd = 256, np.asarray(t.encoded), np.asarray(t.outpos), tensor_dict(t)
+    defined = np.ones(t.n_elem, bool)
+    for b in range(len(op) - 1):
+        cnt = sum(orc.count_phase(enc[8 * w:8 * w + 10], t.gap_at(w), dd["lengths"]) for w in range(b * T, (b + 1) * T))
+        if cnt < op[b + 1] - op[b]:
+            defined[op[b]:op[b + 1]] = False
+    got = d.decode().cpu().numpy()
+    assert np.array_equal(got[defined], want[defined])
+
+
+def test_batch_mixes_variants_4_and_6(orc):
+    import torch
+
+    from paper_2510_02676_b200.device import Batch, DeviceTensor
+
+    xs = [codec.synth(1.8, 0.05, 1_000_003, 81, fmt="e5m2"), codec.synth(1.8, 0.05, 2_000_000, 82),
+          codec.synth(1.8, 0.05, 70_000, 83, fmt="e5m2")]
+    ds = [DeviceTensor(codec.encode_tensor(x, 256)) for x in xs]
+    assert sorted(d.kernel_variant for d in ds) == [4, 6, 6]
+    outs = [torch.empty(x.size, dtype=torch.uint8, device="cuda") for x in xs]
+    b = Batch(ds, outs)
+    for _ in range(2):
+        b.decode()
+        torch.cuda.synchronize()
+        for o, x in zip(outs, xs):
+            assert np.array_equal(o.cpu().numpy(), x)
