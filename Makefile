@@ -15,7 +15,7 @@ OBJ     := build/obj
 LIB     := $(LIBDIR)/libecf8_b200.so
 
 CXXFLAGS  := -std=c++20 -O3 -fPIC -fopenmp -Wall -Wextra -Iinclude -I$(CUDA)/include
-NVCCFLAGS := -std=c++20 -O3 $(ARCH) -lineinfo -Xcompiler -fPIC -Xptxas -v \
+NVCCFLAGS := -std=c++20 -O3 $(ARCH) -lineinfo -Xcompiler -fPIC,-fopenmp -Xptxas -v \
              -Iinclude -I$(PKG)/csrc/cuda --expt-relaxed-constexpr $(EXTRA)
 
 HOST_SRCS := $(wildcard $(PKG)/csrc/host/*.cpp) $(PKG)/csrc/cuda/tables.cpp

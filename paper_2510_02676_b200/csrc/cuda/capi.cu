@@ -429,7 +429,15 @@ struct HostCtx {
     std::uint16_t* ls;    // 4-window group offsets
     cudaEvent_t in, run, out_done;
     bool used;
+    // Pageable host spans: pinned staging (allocated on first need).  The
+    // inputs are copied in by the host threads before the slot's H2D, the
+    // output copied out after its D2H completed (when the slot is reused,
+    // or at the end of the call).
+    std::uint8_t *h_in = nullptr, *h_out = nullptr;
+    std::uint8_t* pend_dst = nullptr;  // pageable destination of the slot's last D2H
+    std::uint64_t pend_bytes = 0;
   } slot[kSlots]{};
+  std::uint64_t h_in_bytes = 0, h_out_bytes = 0;
   // Per-tensor gaps + outpos (one copy each per tensor, not per chunk),
   // double-buffered by tensor parity.
   struct Meta {
@@ -481,9 +489,46 @@ HostCtx& host_ctx() {
       sl.used = false;
     }
     for (auto& mt : c.meta) cu(cudaEventCreateWithFlags(&mt.done, cudaEventDisableTiming), "event");
+    c.h_in_bytes = b_enc + b_pak;
+    c.h_out_bytes = b_out;
     c.dev = dev;
   }
   return c;
+}
+
+// Host memory the DMA engines can read / write directly (cudaMallocHost,
+// cudaHostRegister); anything else is pageable and goes through staging.
+bool is_pinned(const void* p) {
+  if (!p) return true;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeManaged;
+}
+
+// memcpy by all host threads (pinned staging <-> pageable spans).
+void par_copy(void* dst, const void* src, std::uint64_t n) {
+  constexpr std::uint64_t kPiece = std::uint64_t{1} << 20;
+  const std::int64_t pieces = static_cast<std::int64_t>((n + kPiece - 1) / kPiece);
+  if (pieces <= 1) {
+    std::memcpy(dst, src, n);
+    return;
+  }
+#pragma omp parallel for schedule(static)
+  for (std::int64_t i = 0; i < pieces; ++i) {
+    const std::uint64_t o = static_cast<std::uint64_t>(i) * kPiece;
+    std::memcpy(static_cast<std::uint8_t*>(dst) + o, static_cast<const std::uint8_t*>(src) + o, std::min(kPiece, n - o));
+  }
+}
+
+// The slot's staged output, once its D2H has completed, to its pageable destination.
+void drain_out(HostCtx::Slot& sl) {
+  if (!sl.pend_bytes) return;
+  cu(cudaEventSynchronize(sl.out_done), "sync");
+  par_copy(sl.pend_dst, sl.h_out, sl.pend_bytes);
+  sl.pend_bytes = 0;
 }
 
 // Pointer whose element `lo` is `slot` (the kernels index sections with
@@ -517,6 +562,7 @@ int host_pipeline(const ecf8_sections* const* ss, const std::uint64_t* nbs, std:
     const std::uint64_t b_begin = blk_lo ? blk_lo[i] : 0, nb = blk_lo ? blk_hi[i] : nbs[i];
     if (s->n_elem == 0 || s->outpos[nb] == s->outpos[b_begin]) continue;
     std::uint8_t* const out = outs[i];
+    const bool in_pinned = is_pinned(s->encoded) && is_pinned(s->packed), out_pinned = is_pinned(out);
     const std::uint32_t T = s->threads_per_block;
     const DevTables& tb = device_tables(s->lengths);
     const ecf8::dev::Variant v = ecf8::dev::variant_for(T, lmin_of(s->lengths), tb.fsm != nullptr);
@@ -571,12 +617,31 @@ int host_pipeline(const ecf8_sections* const* ss, const std::uint64_t* nbs, std:
       remaining -= s->outpos[hi] - s->outpos[lo];
       HostCtx::Slot& sl = c.slot[k % HostCtx::kSlots];
       if (sl.used) cu(cudaStreamWaitEvent(c.s_in, sl.out_done, 0), "wait");
-      sl.used = true;
       const std::uint64_t e0 = lo * T * 8, e1 = hi * T * 8 + 2;
-      cu(cudaMemcpyAsync(sl.enc, s->encoded + e0, e1 - e0, cudaMemcpyHostToDevice, c.s_in), "H2D encoded");
       const std::uint64_t o0 = s->outpos[lo], o1 = s->outpos[hi];
       const std::uint64_t p0 = (o0 / 2) & ~std::uint64_t{15}, p1 = std::min(s->packed_len, (o1 + 1) / 2);
-      if (p1 > p0) cu(cudaMemcpyAsync(sl.pak, s->packed + p0, p1 - p0, cudaMemcpyHostToDevice, c.s_in), "H2D packed");
+      if (in_pinned) {
+        cu(cudaMemcpyAsync(sl.enc, s->encoded + e0, e1 - e0, cudaMemcpyHostToDevice, c.s_in), "H2D encoded");
+        if (p1 > p0)
+          cu(cudaMemcpyAsync(sl.pak, s->packed + p0, p1 - p0, cudaMemcpyHostToDevice, c.s_in), "H2D packed");
+      } else {
+        // pageable sections: the host threads copy the chunk into the slot's
+        // pinned staging (free once its previous H2D completed), the DMA
+        // engine takes it from there
+        if (!sl.h_in) {
+          void* h = nullptr;
+          cu(cudaMallocHost(&h, c.h_in_bytes), "cudaMallocHost(staging)");
+          sl.h_in = static_cast<std::uint8_t*>(h);
+        }
+        if (sl.used) cu(cudaEventSynchronize(sl.in), "sync");
+        const std::uint64_t enc_bytes = align_up(e1 - e0, 256);
+        par_copy(sl.h_in, s->encoded + e0, e1 - e0);
+        if (p1 > p0) par_copy(sl.h_in + enc_bytes, s->packed + p0, p1 - p0);
+        cu(cudaMemcpyAsync(sl.enc, sl.h_in, e1 - e0, cudaMemcpyHostToDevice, c.s_in), "H2D encoded");
+        if (p1 > p0)
+          cu(cudaMemcpyAsync(sl.pak, sl.h_in + enc_bytes, p1 - p0, cudaMemcpyHostToDevice, c.s_in), "H2D packed");
+      }
+      sl.used = true;
       cu(cudaEventRecord(sl.in, c.s_in), "record");
 
       cu(cudaStreamWaitEvent(c.s_run, sl.in, 0), "wait");
@@ -608,15 +673,33 @@ int host_pipeline(const ecf8_sections* const* ss, const std::uint64_t* nbs, std:
       cu(cudaEventRecord(sl.run, c.s_run), "record");
 
       cu(cudaStreamWaitEvent(c.s_out, sl.run, 0), "wait");
-      if (o1 > o0)
-        cu(cudaMemcpyAsync(out + o0, sl.out + (o0 - dk.out_offset), o1 - o0, cudaMemcpyDeviceToHost, c.s_out),
-           "D2H out");
+      if (out_pinned) {
+        if (o1 > o0)
+          cu(cudaMemcpyAsync(out + o0, sl.out + (o0 - dk.out_offset), o1 - o0, cudaMemcpyDeviceToHost, c.s_out),
+             "D2H out");
+      } else {
+        // pageable destination: D2H into the slot's pinned staging, copied out
+        // by the host threads once it completed (slot reuse or call end)
+        if (!sl.h_out) {
+          void* h = nullptr;
+          cu(cudaMallocHost(&h, c.h_out_bytes), "cudaMallocHost(staging)");
+          sl.h_out = static_cast<std::uint8_t*>(h);
+        }
+        drain_out(sl);
+        if (o1 > o0) {
+          cu(cudaMemcpyAsync(sl.h_out, sl.out + (o0 - dk.out_offset), o1 - o0, cudaMemcpyDeviceToHost, c.s_out),
+             "D2H out");
+          sl.pend_dst = out + o0;
+          sl.pend_bytes = o1 - o0;
+        }
+      }
       cu(cudaEventRecord(sl.out_done, c.s_out), "record");
       lo = hi;
     }
     cu(cudaEventRecord(mt.done, c.s_run), "record");
   }
   cu(cudaStreamSynchronize(c.s_out), "sync");
+  for (auto& sl : c.slot) drain_out(sl);
   return ECF8_OK;
 }
 

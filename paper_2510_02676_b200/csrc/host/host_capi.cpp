@@ -241,9 +241,8 @@ void ecf8_host_file_free(ecf8_host_file* f) { delete f; }
 int ecf8_host_decompress(const uint8_t* bytes, size_t len, uint8_t** out, size_t* out_len,
                          uint64_t* allocations, uint64_t* capacity) {
   return guarded([&] {
-    const ecf8::Ecf8File f = ecf8::parse_container({bytes, len});
     std::ostringstream os;
-    const ecf8::DecompressStats st = ecf8::decompress_streaming(f, os);
+    const ecf8::DecompressStats st = ecf8::host::decompress_bytes({bytes, len}, os);
     const std::string s = os.str();
     give(s.data(), s.size(), out, out_len);
     if (allocations) *allocations = st.buffer_allocations;
@@ -305,9 +304,8 @@ int ecf8_host_decompress_to(const uint8_t* bytes, size_t len, ecf8_write_fn writ
   if (!write) return set_error(ECF8_EINVAL, "null sink");
   SinkBuf buf(write, ctx);
   int rc = guarded([&] {
-    const ecf8::Ecf8File f = ecf8::parse_container({bytes, len});
     std::ostream os(&buf);
-    const ecf8::DecompressStats st = ecf8::decompress_streaming(f, os);
+    const ecf8::DecompressStats st = ecf8::host::decompress_bytes({bytes, len}, os);
     if (allocations) *allocations = st.buffer_allocations;
     if (capacity) *capacity = st.buffer_capacity_bytes;
   });

@@ -5,6 +5,7 @@
 #include <string>
 
 #include "ecf8/codec.hpp"
+#include "ecf8/container.hpp"
 #include "ecf8/errors.hpp"
 #include "ecf8_cuda.h"
 
@@ -45,5 +46,8 @@ inline void lengths_from_lut(const CascadedLut& lut, std::uint8_t lengths[16]) {
   const std::uint8_t* m = lut.entries.data() + std::size_t{256} * (lut.n_luts - 1);
   for (int s = 0; s < 16; ++s) lengths[s] = m[s];
 }
+
+// decompress_streaming straight from container bytes (no parse copies).
+DecompressStats decompress_bytes(std::span<const std::uint8_t> bytes, std::ostream& out);
 
 }  // namespace ecf8::host
