@@ -1,13 +1,13 @@
 """ECF8 decode benchmark (driver contract: one JSON line on rank 0).
 
-Default workload (BASELINE.json configs[1]): Llama-3.1-8B-shaped FP8 E4M3
-linear weights, all 32 layers (q/o 4096x4096, k/v 1024x4096, gate/up
-14336x4096, down 4096x14336 = 218.1 M elements per layer, 6.98 G per step),
-synthetic alpha-stable (alpha 1.8, gamma 0.05, seed 1000*layer + matrix),
+Default workload (BASELINE.json configs[2] shapes, the target's): Llama-3-70B
+FP8 E4M3 linear weights, all 80 layers (q/o 8192x8192, k/v 1024x8192, gate/up
+28672x8192, down 8192x28672 = 855.6 M elements per layer, 68.5 G per step;
+--workload llama3.1-8b: configs[1], 32 layers of 218.1 M), synthetic alpha-stable (alpha 1.8, gamma 0.05, seed 1000*layer + matrix),
 ECF8-encoded on the host with T = 256, decoded layer by layer (one batched
 launch per layer) into two alternating layer-sized HBM buffers.  A step =
-decoding all 32 layers.  Inputs (5.7 GB compressed per step) are far larger
-than L2.
+decoding all layers of the workload (default Llama-3-70B: 80 layers, 56 GB of
+compressed inputs per step, far larger than L2).
 
   value  device-resident: compressed sections already in HBM; GB/s of
          algorithmic bytes (container sections read + FP8 bytes written).
@@ -20,6 +20,7 @@ Other workloads (--workload), same line format:
   deepseek-v3-experts  MoE expert FP8 weights, experts e -> rank e mod world
                        (EP), one step = every local expert of --layers MoE layers
   dit-e5m2             FLUX/Wan DiT-shaped E5M2 tensors, size sweep 1 MB - 1 GB
+  t-sweep              one Llama-3-70B layer at every T in 1 .. 1024 (every kernel variant)
 
 --impl reference: the unmodified reference decoder (oracle/_ref, built from
 /root/reference/proj/src) -- or the C oracle port if _ref is absent -- on the
@@ -73,6 +74,8 @@ WORKLOADS = {
                                 desc="deepseek-v3 routed-expert fp8 weights, EP (expert e on rank e mod world), "
                                      "one batched launch per MoE layer"),
     "dit-e5m2": dict(layers=1, distinct=1, desc="FLUX/Wan DiT-shaped E5M2 tensors, size sweep"),
+    "t-sweep": dict(layers=1, distinct=1, desc="one llama3-70b layer encoded at every threads-per-block T, "
+                                                 "decode GB/s per T (every kernel variant)"),
     "llama3-70b-fused": dict(layers=1, distinct=1,
                              desc="llama3-70b fp8 linears (one layer), decode-fused tcgen05 FP8 GEMM, "
                                   "column TP over the ranks + NCCL all-gather"),
@@ -455,6 +458,44 @@ def run_dit_sweep(args, torch, dist, local, world):
     return sweep, total_launches
 
 
+# ------------------------------------------------------------------ T sweep
+
+
+T_SWEEP = [1, 2, 4, 8, 16, 32, 64, 128, 256, 512, 1024]
+
+
+def run_t_sweep(args, torch, dist, local, world):
+    """One Llama-3-70B layer (7 tensors, 855.6 M elements) encoded on the GPU
+    at every T the format allows (1 .. 1024): each T's kernel variant timed
+    like the default bench (batched launch, two replicas rotating, inputs
+    >> L2), bit-exact against the synthesized bytes."""
+    from paper_2510_02676_b200 import codec
+    from paper_2510_02676_b200.device import Batch, DeviceTensor
+
+    stream = torch.cuda.current_stream()
+    raws = [torch.from_numpy(codec.synth(ALPHA, GAMMA, n * k, 1000 * 0 + j)).cuda()
+            for j, (_, n, k) in enumerate(LLAMA70B)]
+    outs = [[torch.empty(r.numel(), dtype=torch.uint8, device="cuda") for r in raws] for _ in range(2)]
+    sweep, total_launches = [], 0
+    for T in T_SWEEP:
+        reps = [[DeviceTensor.encode(r, threads_per_block=T) for r in raws] for _ in range(2)]
+        batches = [Batch(reps[i], outs[i]) for i in range(2)]
+        batches[0].decode(stream)
+        torch.cuda.synchronize()
+        ok = all(bool(torch.equal(o, r)) for o, r in zip(outs[0], raws))
+        algo = sum(d.algorithmic_bytes for d in reps[0])
+        elapsed, launch_ms, clocks = timed_region(torch, dist, local, stream, batches, args.steps, args.warmup)
+        gbs = world * algo * len(batches) * args.steps / (elapsed * 1e-3) / 1e9
+        variants = sorted({d.kernel_variant for d in reps[0]})
+        sweep.append({"T": T, "gbs": round(gbs, 1), "kernel_variants": variants,
+                      "us_per_layer": round(statistics.median(launch_ms) * 1e3, 1),
+                      "bytes_per_elem": round(algo / sum(r.numel() for r in raws), 4), "verified_bit_exact": ok})
+        total_launches += sum(b.launches for b in batches) * args.steps
+        log(f"[bench] t-sweep T={T}: {gbs:.1f} GB/s (variants {variants}, {algo / 1e9:.3f} GB algorithmic)")
+        del reps, batches
+    return sweep, total_launches
+
+
 # ------------------------------------------------------------------ fused GEMM
 
 
@@ -637,6 +678,23 @@ def main():
 
     if args.workload == "llama3-70b-fused":
         run_fused(args, torch, dist, local, rank, world)
+        if dist:
+            dist.destroy_process_group()
+        return
+
+    if args.workload == "t-sweep":
+        sweep, launches = run_t_sweep(args, torch, dist, local, world)
+        if rank == 0:
+            best = max(sweep, key=lambda r: r["gbs"])
+            line = base_line(args, world, best["gbs"], best["us_per_layer"] / 1e3, {
+                "workload": wl["desc"], "T": T_SWEEP, "fmt": "e4m3", "alpha": ALPHA, "gamma": GAMMA,
+                "parallelism": f"shard{world} (replicas per rank, no collective)"})
+            line["sweep"] = sweep
+            line["roofline"] = {"bound": "hbm", "achieved": best["gbs"] / world, "peak": peak, "unit": "GB/s",
+                                "frac": round(best["gbs"] / world / peak, 4), "traffic": None, "peak_kind": peak_kind,
+                                "kernel": "per T: see sweep[].kernel_variants"}
+            line["gpu_launches"] = launches
+            print(json.dumps(line), flush=True)
         if dist:
             dist.destroy_process_group()
         return

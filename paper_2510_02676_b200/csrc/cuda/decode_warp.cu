@@ -91,6 +91,9 @@ __device__ __forceinline__ void stage_fsm(const TensorDesc& d, int tid, int nthr
 #define ECF8_WB_UNROLL 4
 #endif
 constexpr int kWbUnroll = ECF8_WB_UNROLL;
+#ifndef ECF8_STATIC_TILES
+#define ECF8_STATIC_TILES 0
+#endif
 #ifndef ECF8_CLAIM_AHEAD
 #define ECF8_CLAIM_AHEAD 0  // 1: claim the next tile one tile early (A/B: slower)
 #endif  // write-back chunks per lane and loop step
@@ -255,9 +258,13 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_warp_kernel(const LaunchArg
       while (tile < seg_end) {
         WarpIn cur;
         load_warp_tile<kLaneWin, true>(d, tile, log2T, lane, cur);
+#if ECF8_STATIC_TILES  // A/B: round-robin tiles (no shared atomic)
+        const std::uint64_t next = tile + NW;
+#else
         unsigned claim = 0;
         if (lane == 0) claim = atomicAdd(&next_tile, 1u);
         const std::uint64_t next = seg + __shfl_sync(0xffffffffu, claim, 0);
+#endif
         if (next < seg_end && lane < 5) prefetch_tile_l2(d, next, log2T, lane);
         if (lane == 0) {  // this tile's sign/mantissa bytes -> L2 (direct tiles read them at write-back)
           const std::uint64_t p0 = (cur.A >> 1) & ~std::uint64_t{15};

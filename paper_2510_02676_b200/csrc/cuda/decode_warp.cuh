@@ -20,6 +20,9 @@
 namespace ecf8::dev {
 
 constexpr int kLaneWin = 8;     // windows per lane (Lmin >= 2)
+#ifndef ECF8_PF_WINDOWS_ONLY
+#define ECF8_PF_WINDOWS_ONLY 0
+#endif
 #ifndef ECF8_COUNTED
 #define ECF8_COUNTED 1  // verified direct tiles: runs end by the group offsets (0: by the completion masks)
 #endif
@@ -129,6 +132,10 @@ __device__ __forceinline__ void prefetch_tile_l2(const TensorDesc& d, std::uint6
   // 3 end nibbles, 4 group offsets)
   const std::uint8_t* p = d.encoded + 8 * w0;
   std::uint64_t n = 8 * nw + 8;
+#if ECF8_PF_WINDOWS_ONLY  // A/B: only the windows (the small sections load from HBM at the tile's start)
+  if (lane == 0) prefetch_l2(p, n);
+  return;
+#endif
   p = lane == 1 ? d.gaps + (w0 >> 1) : p;
   p = lane == 2 ? reinterpret_cast<const std::uint8_t*>(d.outpos + b0) : p;
   p = lane == 3 ? (d.endgap ? d.endgap + (w0 >> 1) : nullptr) : p;
