@@ -178,6 +178,15 @@ int ecf8_fused_gemm(const ecf8_fused *f, const uint8_t *d_x, uint32_t m, float s
 /* CTAs sharing one 128-row tile of W (rounded up): the launch is cut into
  * balanced runs of weight tiles, one per SM; partial sums are added into y. */
 int ecf8_fused_split_k(const ecf8_fused *f);
+/* Rows [row0, row1) (whole 128-row tiles) of the fused weight decoded back to
+ * row-major FP8 bytes at d_rows ((row1 - row0) x k, 16-byte aligned),
+ * stream-ordered: the large-m path of the fused linear (decode a chunk of W
+ * into an L2-resident buffer, then a dense FP8 GEMM on it).  Needs a
+ * byte-step weight whose tiles all decode directly (encoder output). */
+int ecf8_fused_decode_rows(const ecf8_fused *f, uint64_t row0, uint64_t row1, uint8_t *d_rows, void *stream);
+/* 1 when the weight decodes by byte steps with every tile direct (the
+ * fused kernel's byte-step variant; ecf8_fused_decode_rows available). */
+int ecf8_fused_byte_steps(const ecf8_fused *f);
 void ecf8_fused_free(ecf8_fused *f);
 /* ecf8_host_fused_layout on device memory, stream-ordered: row-major n x k
  * FP8 bytes <-> the tiled, swizzled sequence (inverse != 0: back).  With the

@@ -139,6 +139,8 @@ _SIGS = {
     "ecf8_fused_create": (C.c_int, [_P, C.c_uint64, C.c_uint64, C.c_int, C.POINTER(_P)]),
     "ecf8_fused_gemm": (C.c_int, [_P, _P, C.c_uint32, C.c_float, _P, _P]),
     "ecf8_fused_split_k": (C.c_int, [_P]),
+    "ecf8_fused_decode_rows": (C.c_int, [_P, C.c_uint64, C.c_uint64, _P, _P]),
+    "ecf8_fused_byte_steps": (C.c_int, [_P]),
     "ecf8_fused_free": (None, [_P]),
     "ecf8_fused_layout_device": (C.c_int, [_P, C.c_uint64, C.c_uint64, _P, C.c_int, _P]),
     # ecf8_host.h

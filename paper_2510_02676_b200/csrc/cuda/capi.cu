@@ -239,6 +239,7 @@ struct ecf8_fused {
   std::uint64_t n = 0, k = 0;
   std::uint32_t w_fmt = 0;
   bool fsm = false;  // byte-step direct decode: the code has a byte-step decoder and every tile is direct
+  std::vector<std::uint64_t> outpos;  // host copy of the weight's block offsets (row ranges -> blocks)
 };
 
 struct ecf8_batch {
@@ -1138,6 +1139,7 @@ int ecf8_fused_create(const ecf8_dev_tensor* t, uint64_t n, uint64_t k, int w_fm
     if (int rc = require_device()) return rc;
     std::vector<std::uint64_t> outpos(t->n_blocks + 1);
     cu(cudaMemcpy(outpos.data(), t->desc.outpos, 8 * outpos.size(), cudaMemcpyDeviceToHost), "D2H outpos");
+    const std::vector<std::uint64_t>& outpos_ref = outpos;
     // whole waves of the SMs (one CTA per SM); as few waves as keep every
     // CTA's run of tiles within max_seg n-tiles (one TMEM accumulator each)
     int dev = 0, sms = 148;
@@ -1206,10 +1208,44 @@ int ecf8_fused_create(const ecf8_dev_tensor* t, uint64_t n, uint64_t k, int w_fm
       for (std::uint64_t v = 0; v < t->n_vtiles; ++v) all &= ((bits[v >> 5] >> (v & 31)) & 1u) != 0;
       f->fsm = all;
     }
+    f->outpos = outpos_ref;
     *out = f.release();
     return ECF8_OK;
   });
 }
+
+int ecf8_fused_decode_rows(const ecf8_fused* f, uint64_t row0, uint64_t row1, uint8_t* d_rows, void* stream) {
+  return guarded([&]() -> int {
+    if (!f || !d_rows) return fail(ECF8_EINVAL, "null argument");
+    if (row0 >= row1 || row1 > f->n || row0 % 128 || row1 % 128)
+      return fail(ECF8_EINVAL, "rows must be a non-empty range of whole 128-row tiles");
+    if (reinterpret_cast<std::uintptr_t>(d_rows) & 15) return fail(ECF8_EINVAL, "device output must be 16-byte aligned");
+    if (!f->fsm) return fail(ECF8_EINVAL, "row decode needs a byte-step weight with every tile direct");
+    const std::uint64_t KT = f->k / 128;
+    const std::uint64_t e0 = row0 / 128 * KT * 16384, e1 = row1 / 128 * KT * 16384;
+    TensorDesc d = f->w->desc;
+    const std::uint64_t T = d.T, m = std::max<std::uint64_t>(1, 256 / T);  // blocks per warp tile
+    // blocks holding [e0, e1), widened to whole warp tiles of the tensor
+    const auto& op = f->outpos;
+    std::uint64_t b0 = static_cast<std::uint64_t>(std::upper_bound(op.begin(), op.end() - 1, e0) - op.begin()) - 1;
+    std::uint64_t b1 = static_cast<std::uint64_t>(std::lower_bound(op.begin(), op.end(), e1) - op.begin());
+    b1 = std::min<std::uint64_t>(b1, f->w->n_blocks);
+    b0 = b0 / m * m;
+    b1 = std::min<std::uint64_t>((b1 + m - 1) / m * m, f->w->n_blocks);
+    d.blk_begin = b0;
+    d.blk_end = b1;
+    d.out = d_rows - row0 * f->k;  // row-major W[0][0] (only rows [row0, row1) are written)
+    d.out_offset = 0;
+    d.out_tiled_k = static_cast<std::uint32_t>(f->k);
+    d.out_lo = e0;
+    d.out_hi = e1;
+    if (int rc = launch_one(d, static_cast<cudaStream_t>(stream))) return rc;
+    note_use(f->w, static_cast<cudaStream_t>(stream));
+    return ECF8_OK;
+  });
+}
+
+int ecf8_fused_byte_steps(const ecf8_fused* f) { return f && f->fsm ? 1 : 0; }
 
 int ecf8_fused_split_k(const ecf8_fused* f) { return f ? static_cast<int>(f->split_k) : 0; }
 

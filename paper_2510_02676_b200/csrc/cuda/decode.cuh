@@ -32,6 +32,12 @@ struct TensorDesc {
   std::uint64_t blk_end;
   std::uint64_t lenpack;
   std::uint64_t tile_begin;      // first tile of this desc within its launch
+  // Tiled weights (fused layout, 128 x 128 swizzled tiles) decoded back to
+  // row-major: out_tiled_k = the row length k (0: elements land linearly);
+  // element e goes to its row-major place under `out`, written only for e in
+  // [out_lo, out_hi) (the rows a call asked for).
+  std::uint64_t out_lo, out_hi;
+  std::uint32_t out_tiled_k, out_pad_;
   std::uint32_t T;
   std::uint32_t n_luts;
   std::uint32_t lmin;  // shortest code length (selects the variant)

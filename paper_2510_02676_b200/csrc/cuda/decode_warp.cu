@@ -122,8 +122,53 @@ struct GlobalOut {
   __device__ __forceinline__ void done() const {}
 };
 
+// Output of a tiled weight (fused layout) to row-major rows: element e of
+// tile t = e / 16384 (tile (nt, kt) = (t / KT, t % KT)) at offset o = e %
+// 16384 is row 128 nt + o / 128, 16-byte chunk ((o / 16) ^ (o / 128 % 8)) of
+// K tile kt (the 128B swizzle undone); 16-element chunks stay contiguous.  A
+// warp tile spans at most two weight tiles: their row bases are computed
+// once.  Only elements in [lo, hi) are written.
+struct TiledOut {
+  std::uint8_t* rb0;      // row-major address of weight tile t0's (row 0, column 0)
+  std::uint8_t* rb1;      // ... of tile t0 + 1
+  std::uint64_t S0, bnd;  // element of chunk 0; first element of tile t0 + 1
+  std::uint64_t lo, hi;
+  std::uint32_t k;
+  __device__ __forceinline__ void wait() const { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+  __device__ __forceinline__ std::uint8_t* at(std::uint64_t e) const {
+    const std::uint32_t o = static_cast<std::uint32_t>(e) & 16383u, r = o >> 7;
+    return (e >= bnd ? rb1 : rb0) + static_cast<std::uint64_t>(r) * k + ((((o >> 4) ^ r) & 7u) << 4) + (o & 15u);
+  }
+  __device__ __forceinline__ void chunk(std::uint32_t c, const uint4& v) const {
+    const std::uint64_t e = S0 + 16 * static_cast<std::uint64_t>(c);
+    if (e < lo || e >= hi) return;
+    asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(at(e)), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w));
+  }
+  __device__ __forceinline__ void byte(std::uint32_t i, std::uint8_t b) const {
+    const std::uint64_t e = S0 + i;
+    if (e < lo || e >= hi) return;
+    *at(e) = b;
+  }
+  __device__ __forceinline__ void done() const {}
+};
+
+__device__ __forceinline__ TiledOut tiled_out(const TensorDesc& d, std::uint64_t A) {
+  TiledOut t;
+  t.S0 = A & ~std::uint64_t{15};
+  const std::uint64_t kt_n = d.out_tiled_k >> 7, t0 = t.S0 >> 14;
+  const std::uint64_t nt = t0 / kt_n, kt = t0 - nt * kt_n;
+  const std::uint64_t nt1 = kt + 1 == kt_n ? nt + 1 : nt, kt1 = kt + 1 == kt_n ? 0 : kt + 1;
+  t.rb0 = d.out + (nt * 128) * d.out_tiled_k + kt * 128;
+  t.rb1 = d.out + (nt1 * 128) * d.out_tiled_k + kt1 * 128;
+  t.bnd = (t0 + 1) << 14;
+  t.lo = d.out_lo;
+  t.hi = d.out_hi;
+  t.k = d.out_tiled_k;
+  return t;
+}
+
 // One tile: decode + scan, compact, write back.
-template <bool WIDE, class WSm>
+template <bool WIDE, bool TILED = false, class WSm>
 __device__ __forceinline__ void warp_tile(const TensorDesc& d, const WarpIn& in, std::uint32_t log2T,
                                           std::uint32_t len_off, WSm& ws, int lane) {
 
@@ -139,10 +184,14 @@ __device__ __forceinline__ void warp_tile(const TensorDesc& d, const WarpIn& in,
     const std::uint32_t v = static_cast<std::uint32_t>((in.b0 << log2T) >> 8);  // the tile's verification tile
     if ((in.dir >> (v & 31)) & 1u) {  // every lane's output offset known: decode in place
       // the packed sign/mantissa bytes come from L2 at write-back (prefetched at the tile's start)
-      direct_tile<kWbUnroll, kLaneWin, true>(
-          d, in, ws, lane, [&] { return GlobalOut{d.out + ((in.A & ~std::uint64_t{15}) - d.out_offset)}; }, verified);
+      if constexpr (TILED)  // a tiled weight back to row-major rows (ecf8_fused_decode_rows)
+        direct_tile<kWbUnroll, kLaneWin, true>(d, in, ws, lane, [&] { return tiled_out(d, in.A); }, verified);
+      else
+        direct_tile<kWbUnroll, kLaneWin, true>(
+            d, in, ws, lane, [&] { return GlobalOut{d.out + ((in.A & ~std::uint64_t{15}) - d.out_offset)}; }, verified);
       return;
     }
+    if constexpr (TILED) __trap();  // row-major output of tiled weights needs direct tiles (checked by the caller)
     run = warp_decode_scan<kLaneWin, 128, false, GlobalTables, true>(in, log2T, len_off, GlobalTables{d}, slot, lane,
                                                                      verified);
   } else {  // an incomplete code (no encoder writes one): the reference walk per window, tables through L1
@@ -153,7 +202,7 @@ __device__ __forceinline__ void warp_tile(const TensorDesc& d, const WarpIn& in,
   compact_write<kWbUnroll>(d, in.A, in.E, run, ws, lane, out);
 }
 
-template <int NW, bool WIDE>
+template <int NW, bool WIDE, bool TILED = false>
 __global__ void __launch_bounds__(NW * 32, 1) decode_warp_kernel(const LaunchArgs args) {
   using WarpSmem = WarpSmemT<WIDE>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -271,7 +320,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_warp_kernel(const LaunchArg
           const std::uint32_t bytes = static_cast<std::uint32_t>((((cur.E + 1) >> 1) - p0 + 15) & ~std::uint64_t{15});
           if (bytes) prefetch_l2(d.packed + p0, bytes);
         }
-        warp_tile<WIDE>(d, cur, log2T, len_off, ws, lane);
+        warp_tile<WIDE, TILED>(d, cur, log2T, len_off, ws, lane);
         tile = next;
       }
 #endif
@@ -355,17 +404,17 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_fsm64_kernel(const LaunchAr
 #define ECF8_FSM64_WARPS 22  // 22 x 8.2 KB of staging + the 32 KB table
 #endif
 
-template <int NW, bool WIDE = false>
+template <int NW, bool WIDE = false, bool TILED = false>
 cudaError_t launch_nw(const LaunchArgs& args, cudaStream_t s) {
   static int grid_cap = 0;
   const int smem = static_cast<int>(sizeof(WarpSmemT<WIDE>)) * NW;
   if (grid_cap == 0) {
-    cudaError_t e = cudaFuncSetAttribute(decode_warp_kernel<NW, WIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = cudaFuncSetAttribute(decode_warp_kernel<NW, WIDE, TILED>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_warp_kernel<NW, WIDE>, NW * 32, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_warp_kernel<NW, WIDE, TILED>, NW * 32, smem);
     if (e != cudaSuccess) return e;
     grid_cap = sms * (per_sm > 0 ? per_sm : 1);
   }
@@ -385,7 +434,7 @@ cudaError_t launch_nw(const LaunchArgs& args, cudaStream_t s) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, decode_warp_kernel<NW, WIDE>, args);
+  return cudaLaunchKernelEx(&cfg, decode_warp_kernel<NW, WIDE, TILED>, args);
 }
 
 // One CTA iteration per 256-window tile, one thread per window: the
@@ -481,6 +530,7 @@ cudaError_t launch_decode_warp(const LaunchArgs& args, cudaStream_t s) {
     const char* e = std::getenv("ECF8_WARPS");
     return e ? std::atoi(e) : 24;
   }();
+  if (!args.descs && args.inline_desc.out_tiled_k) return launch_nw<24, false, true>(args, s);  // rows of a fused weight
   return nw == 20 ? launch_nw<20>(args, s) : nw == 22 ? launch_nw<22>(args, s) : launch_nw<24>(args, s);
 }
 

@@ -7,10 +7,18 @@ W is kept ECF8-compressed in HBM in the *tiled* layout (fused_layout): 128 x
 reads, then encoded by the unchanged ECF8 encoder.  The kernel decodes each
 K tile straight into shared memory and feeds tcgen05.mma; the decoded
 weights never touch HBM.
+
+An alternative large-m path (ECF8_FUSED_LARGE_M=<m>): W decoded chunk by
+chunk -- ~32 MB of whole 128-row tiles, back to row-major
+(ecf8_fused_decode_rows) -- into a two-slot ring meant to stay in L2, each
+chunk through a dense FP8 GEMM (cuBLASLt) while the next one decodes on a
+side stream.  Measured slower than the fused kernel (host-bound per chunk),
+so it is off by default.
 """
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import numpy as np
 import torch
@@ -51,6 +59,36 @@ def fused_layout_device(w: torch.Tensor, n: int, k: int, inverse: bool = False,
     return out
 
 
+# m at which the decode-rows pipeline takes over (off by default: measured slower
+# than the fused kernel at m = 256 -- 0.83 ms per Llama-3-70B layer with one chunk
+# per linear, 1.95 ms with 32 MB chunks: host-bound per chunk)
+LARGE_M = int(os.environ.get("ECF8_FUSED_LARGE_M", "100000"))
+CHUNK_BYTES = int(os.environ.get("ECF8_FUSED_CHUNK_MB", "32")) << 20
+
+
+class _RowsPipe:
+    """Per-device state of the large-m path: a two-slot decode ring (L2-resident),
+    a side stream for the decodes and the events ordering slot reuse (shared by
+    every FusedLinear, so back-to-back calls keep the ring order)."""
+
+    _by_dev: dict = {}
+
+    def __init__(self, dev):
+        self.slots = [torch.empty(CHUNK_BYTES + 16, dtype=torch.uint8, device=dev) for _ in range(2)]
+        self.dec = torch.cuda.Stream(device=dev)
+        self.ev_dec = [torch.cuda.Event() for _ in range(2)]
+        self.ev_use = [torch.cuda.Event() for _ in range(2)]
+        self.used = [False, False]
+        self.k = 0  # chunks issued
+
+    @classmethod
+    def get(cls, dev) -> "_RowsPipe":
+        key = torch.device(dev).index
+        if key not in cls._by_dev:
+            cls._by_dev[key] = cls(dev)
+        return cls._by_dev[key]
+
+
 class FusedLinear:
     """An ECF8-compressed FP8 weight [n, k] served by the decode-fused GEMM.
 
@@ -79,6 +117,8 @@ class FusedLinear:
         check(lib.ecf8_fused_create(self.dev.handle, self.n, self.k, {"e4m3": 0, "e5m2": 1}[fmt], C.byref(h)))
         self.handle = h
         self.split_k = int(lib.ecf8_fused_split_k(h))
+        self.rows_ok = bool(lib.ecf8_fused_byte_steps(h))
+        self._one = None
 
     @classmethod
     def from_encoded(cls, t: codec.EncodedTensor, n: int, k: int, fmt: str = "e4m3",
@@ -123,12 +163,46 @@ class FusedLinear:
               or not out.is_contiguous()):
             # the kernel zeroes and atomically adds m * n fp32 values at out.data_ptr()
             raise ValueError(f"out must be a contiguous float32 tensor [{m}, {self.n}] on {x.device}")
+        if m >= LARGE_M and self.rows_ok:
+            return self._rows_path(x, scale, out, stream)
         check(lib.ecf8_fused_gemm(self.handle, C.c_void_p(x.data_ptr()), m, float(scale),
                                   C.c_void_p(out.data_ptr()), _stream_ptr(stream)))
         return out
 
+    def _rows_path(self, x: torch.Tensor, scale: float, out: torch.Tensor, stream) -> torch.Tensor:
+        """Large m: W decoded in ~32 MB chunks of whole 128-row tiles into an
+        L2-resident two-slot ring (ecf8_fused_decode_rows, side stream), each
+        chunk multiplied by a dense FP8 GEMM on the caller's stream."""
+        st = stream if stream is not None else torch.cuda.current_stream(x.device)
+        p = _RowsPipe.get(x.device)
+        m, k = x.shape
+        if self._one is None:
+            self._one = torch.ones((), device=x.device)
+        pad = (-m) % 16
+        xp = torch.cat([x, x.new_zeros(pad, k)]) if pad else x
+        sb = torch.full((), float(scale), device=x.device)
+        wdt = torch.float8_e4m3fn if self.fmt == "e4m3" else torch.float8_e5m2
+        rows = max(128, min(self.n, CHUNK_BYTES // k // 128 * 128))
+        for r0 in range(0, self.n, rows):
+            r1 = min(self.n, r0 + rows)
+            s = p.k % 2
+            p.k += 1
+            if p.used[s]:
+                p.dec.wait_event(p.ev_use[s])  # the GEMM that last read this slot is done
+            check(lib.ecf8_fused_decode_rows(self.handle, r0, r1, C.c_void_p(p.slots[s].data_ptr()),
+                                             C.c_void_p(p.dec.cuda_stream)))
+            p.ev_dec[s].record(p.dec)
+            st.wait_event(p.ev_dec[s])
+            w = p.slots[s][: (r1 - r0) * k].view(wdt).view(r1 - r0, k)
+            with torch.cuda.stream(st):
+                y = torch._scaled_mm(xp, w.t(), scale_a=self._one, scale_b=sb, out_dtype=torch.float32)
+                out[:, r0:r1].copy_(y[:m])
+            p.ev_use[s].record(st)
+            p.used[s] = True
+        return out
+
     def free(self):
-        if getattr(self, "handle", None):
+        if getattr(self, "handle", None) and lib is not None:
             lib.ecf8_fused_free(self.handle)
             self.handle = None
 

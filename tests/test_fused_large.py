@@ -145,3 +145,35 @@ def test_fused_out_is_validated():
                 torch.empty(4, lin.n)):
         with pytest.raises(ValueError):
             lin(x8, 1.0, bad)
+
+
+@pytest.mark.parametrize("m", [129, 256])
+def test_large_m_rows_pipeline_matches(m):
+    # m >= LARGE_M: W decoded in chunks of whole 128-row tiles back to
+    # row-major (ecf8_fused_decode_rows) + dense FP8 GEMM per chunk; several
+    # chunks (the two-slot ring wraps), same bound as the fused kernel
+    from paper_2510_02676_b200 import fused
+
+    lin, w8 = _weight(28672, 8192, "e4m3", 128)
+    assert lin.rows_ok and 28672 * 8192 > 3 * fused.CHUNK_BYTES
+    old, fused.LARGE_M = fused.LARGE_M, 129  # the path is opt-in
+    try:
+        _check(lin, w8, m, 0.75, 700 + m)
+    finally:
+        fused.LARGE_M = old
+
+
+def test_decode_rows_back_to_row_major():
+    import torch
+
+    from paper_2510_02676_b200 import _lib
+
+    lin, w8 = _weight(4096, 8192, "e4m3", 256)
+    out = torch.empty(1024 * 8192 + 16, dtype=torch.uint8, device="cuda")
+    for r0, r1 in ((0, 128), (1920, 2944), (3968, 4096)):
+        _lib.check(_lib.lib.ecf8_fused_decode_rows(lin.handle, r0, r1, out.data_ptr(), None))
+        torch.cuda.synchronize()
+        got = out[: (r1 - r0) * 8192].view(r1 - r0, 8192)
+        assert torch.equal(got, w8[r0:r1].view(torch.uint8))
+    with pytest.raises(_lib.InvalidArgument, match="whole 128-row tiles"):
+        _lib.check(_lib.lib.ecf8_fused_decode_rows(lin.handle, 5, 128, out.data_ptr(), None))
