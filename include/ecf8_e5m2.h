@@ -83,6 +83,9 @@ int ecf8_e5_upload(const ecf8_e5_sections *host, ecf8_e5_dev_tensor **out);
 /* Decode into device memory d_out (n_elem bytes, 16-byte aligned), stream-ordered. */
 int ecf8_e5_decode_device(const ecf8_e5_dev_tensor *t, uint8_t *d_out, void *stream);
 uint64_t ecf8_e5_dev_n_elem(const ecf8_e5_dev_tensor *t);
+/* 1 when the tensor decodes by byte steps (a complete code, T in [8, 256],
+ * every tile passed the upload check), 0 for the per-window walk. */
+int ecf8_e5_dev_byte_steps(const ecf8_e5_dev_tensor *t);
 void ecf8_e5_free(ecf8_e5_dev_tensor *t);
 /* Host spans: upload, decode, copy back (synchronous). */
 int ecf8_e5_decode_host(const ecf8_e5_sections *host, uint8_t *out, uint64_t out_len);

@@ -186,6 +186,7 @@ _SIGS = {
     "ecf8_e5_upload": (C.c_int, [C.POINTER(E5Sections), C.POINTER(_P)]),
     "ecf8_e5_decode_device": (C.c_int, [_P, _P, _P]),
     "ecf8_e5_dev_n_elem": (C.c_uint64, [_P]),
+    "ecf8_e5_dev_byte_steps": (C.c_int, [_P]),
     "ecf8_e5_free": (None, [_P]),
     "ecf8_e5_decode_host": (C.c_int, [C.POINTER(E5Sections), _P, C.c_uint64]),
 }

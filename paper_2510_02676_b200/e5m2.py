@@ -101,6 +101,7 @@ class E5DeviceTensor:
         self._h = _Handle(h, lib.ecf8_e5_free)
         self.n_elem = t.n_elem
         self.algorithmic_bytes = t.algorithmic_bytes()
+        self.byte_steps = bool(lib.ecf8_e5_dev_byte_steps(self._h.h))
 
     def decode_into(self, out, stream=None) -> None:
         import torch
