@@ -656,17 +656,20 @@ __global__ void __launch_bounds__(NW * 32, 1) e5_fsm_bytes_kernel(const Desc d) 
 // lanes' group offsets into lane_start.
 __global__ void __launch_bounds__(256) e5_verify_kernel(const Desc d, std::uint32_t* ok, std::uint32_t* lane_start) {
   __shared__ Tables tb;
-  __shared__ std::uint32_t gsum[64];
+  __shared__ std::uint32_t gsum[64], lexcl[32];
   __shared__ unsigned bad_tile;
   for (int i = threadIdx.x; i < static_cast<int>(sizeof(Tables) / 2); i += 256)
     reinterpret_cast<std::uint16_t*>(&tb)[i] = reinterpret_cast<const std::uint16_t*>(d.tables)[i];
   __syncthreads();
   const std::uint32_t log2T = 31 - __clz(d.T);
+  const std::uint32_t lpb = log2T >= 8 ? 32u : (1u << (log2T - 3));  // 8-window lanes per block
   const std::uint64_t n_tiles = (d.n_windows + 255) / 256;
+  const std::uint64_t last_blk = d.n_blocks - 1;
+  const std::uint64_t last_range = d.outpos[d.n_blocks] - d.outpos[last_blk];
   for (std::uint64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
     const std::uint64_t k = 256 * t + threadIdx.x;
     std::uint32_t cnt = 0, end = 0;
-    bool bad = false;
+    bool mismatch = false;
     if (k < d.n_windows) {
       const std::uint64_t hi = be64(d.encoded + 8 * k), lo = be64(d.encoded + 8 * k + 8);
       std::uint32_t p = (d.gaps[k >> 1] >> ((k & 1) ? 0 : 4)) & 15u;
@@ -677,11 +680,8 @@ __global__ void __launch_bounds__(256) e5_verify_kernel(const Desc d, std::uint3
         ++cnt;
       }
       end = p - 64;
-      // (the tensor's last block is exempt: past the final word its windows
-      // parse the zero padding, and every symbol a run takes past the
-      // block's range is dropped by the clamp, as the reference drops them)
-      if ((k & 7) != 7 && k + 1 < d.n_windows && (k >> log2T) + 1 < d.n_blocks)
-        bad = end != ((d.gaps[(k + 1) >> 1] >> (((k + 1) & 1) ? 0 : 4)) & 15u);
+      if ((k & 7) != 7 && k + 1 < d.n_windows)
+        mismatch = end != ((d.gaps[(k + 1) >> 1] >> (((k + 1) & 1) ? 0 : 4)) & 15u);
     }
     if (threadIdx.x == 0) bad_tile = 0;
     std::uint32_t g = cnt;
@@ -689,7 +689,6 @@ __global__ void __launch_bounds__(256) e5_verify_kernel(const Desc d, std::uint3
     g += __shfl_xor_sync(0xffffffffu, g, 2);
     if ((threadIdx.x & 3) == 0) gsum[threadIdx.x >> 2] = g;
     __syncthreads();
-    if (__ballot_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(&bad_tile, 1u);
     if (threadIdx.x < 32) {
       const std::uint32_t i = threadIdx.x, v0 = gsum[2 * i], v1 = gsum[2 * i + 1], v = v0 + v1;
       std::uint32_t incl = v;
@@ -698,8 +697,8 @@ __global__ void __launch_bounds__(256) e5_verify_kernel(const Desc d, std::uint3
         const std::uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
         if (i >= static_cast<std::uint32_t>(o)) incl += y;
       }
-      const std::uint32_t lpb = log2T >= 8 ? 32u : (1u << (log2T - 3));
       const std::uint32_t excl = incl - v - __shfl_sync(0xffffffffu, incl - v, i & ~(lpb - 1));
+      lexcl[i] = excl;
       const std::uint64_t wg = 256 * t + 8 * i;
       if (wg < d.n_windows) {
         lane_start[wg >> 3] = excl | ((excl + v0) << 16);
@@ -710,6 +709,19 @@ __global__ void __launch_bounds__(256) e5_verify_kernel(const Desc d, std::uint3
         }
       }
     }
+    __syncthreads();
+    // A window whose walk does not end where the next window's gap says
+    // breaks the lane's continuous parse -- unless the block's words already
+    // ran out (the tensor's last block, past its final word: the zero padding
+    // parses into words the block clamp drops, as the reference's does).
+    std::uint32_t incl8 = cnt;  // the window's words and those of the windows before it in its 8-window lane
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      const std::uint32_t y = __shfl_up_sync(0xffffffffu, incl8, o, 8);
+      if ((threadIdx.x & 7) >= static_cast<unsigned>(o)) incl8 += y;
+    }
+    const bool spent = (k >> log2T) == last_blk && lexcl[threadIdx.x >> 3] + incl8 >= last_range;
+    if (__ballot_sync(0xffffffffu, mismatch && !spent) && (threadIdx.x & 31) == 0) atomicOr(&bad_tile, 1u);
     __syncthreads();
     if (threadIdx.x == 0 && bad_tile) atomicAnd(ok + (t >> 5), ~(1u << (t & 31)));
     __syncthreads();

@@ -269,3 +269,25 @@ def test_gpu_rejects_inconsistent_offsets():
     bad = e5m2.E5Tensor(t.n_elem, 32, t.lengths, t.encoded, t.gaps, op, t.raw)
     with pytest.raises(InvalidArgument, match="inconsistent block offsets"):
         e5m2.decode(bad)
+
+
+@pytest.mark.gpu
+def test_gpu_corrupt_gap_in_the_last_block_takes_the_window_walk(orc):
+    # the last block is exempt from the window-end check only past its final
+    # word; a corrupted gap among its real words must still fail the check
+    x = _data(200_000, 93)
+    t = e5m2.encode(x, 64)
+    nb = len(t.outpos) - 1
+    w = (nb - 1) * 64 + 2  # a window of the last block holding real words
+    g = np.array(t.gaps)
+    sh = 4 if w % 2 == 0 else 0
+    g[w // 2] = (g[w // 2] & ~(15 << sh)) | ((((g[w // 2] >> sh) + 3) & 15) << sh)
+    bad = e5m2.E5Tensor(t.n_elem, 64, t.lengths, t.encoded, g, t.outpos, t.raw)
+    dt = e5m2.E5DeviceTensor(bad)
+    assert not dt.byte_steps
+    want = orc.decode(e5_dict(bad))
+    got = dt.decode().cpu().numpy()
+    op = np.asarray(t.outpos)
+    keep = np.ones(t.n_elem, bool)
+    keep[op[nb - 1]:] = False  # the corrupted block's tail is undefined in a reference-style decoder
+    assert np.array_equal(got[keep], want[keep])
