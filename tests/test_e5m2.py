@@ -281,7 +281,8 @@ def test_gpu_corrupt_gap_in_the_last_block_takes_the_window_walk(orc):
     w = (nb - 1) * 64 + 2  # a window of the last block holding real words
     g = np.array(t.gaps)
     sh = 4 if w % 2 == 0 else 0
-    g[w // 2] = (g[w // 2] & ~(15 << sh)) | ((((g[w // 2] >> sh) + 3) & 15) << sh)
+    v = int(g[w // 2])
+    g[w // 2] = (v & (0xFF ^ (15 << sh))) | ((((v >> sh) + 3) & 15) << sh)
     bad = e5m2.E5Tensor(t.n_elem, 64, t.lengths, t.encoded, g, t.outpos, t.raw)
     dt = e5m2.E5DeviceTensor(bad)
     assert not dt.byte_steps
