@@ -20,6 +20,12 @@
 namespace ecf8::dev {
 
 constexpr int kLaneWin = 8;     // windows per lane (Lmin >= 2)
+#ifndef ECF8_WB_ALL_LOADS
+#define ECF8_WB_ALL_LOADS 0  // 1: GPK write-back issues a pass of packed loads at once (A/B: spills, -4..-13 %)
+#endif
+#ifndef ECF8_WB_PASS
+#define ECF8_WB_PASS 8
+#endif
 #ifndef ECF8_PF_WINDOWS_ONLY
 #define ECF8_PF_WINDOWS_ONLY 0
 #endif
@@ -271,6 +277,31 @@ __device__ __forceinline__ void write_back(std::uint64_t S0, std::uint32_t off, 
   const uint2* pl = GPK ? reinterpret_cast<const uint2*>(gpk + pk_lo) + lane
                         : reinterpret_cast<const uint2*>(reinterpret_cast<const std::uint8_t*>(ws.slot) + (pk_lo - pk_a)) + lane;
   std::uint32_t k = lane;
+#if ECF8_WB_ALL_LOADS
+  if constexpr (GPK) {
+    // the packed bytes come from L2: every load of a pass is issued before
+    // its first merge, so a pass waits out one L2 round trip
+    constexpr int kPass = ECF8_WB_PASS;  // chunks per lane per pass
+    for (std::uint32_t base = 0; base < nfull; base += 32 * kPass, sl += 32 * kPass, pl += 32 * kPass) {
+      uint2 q[kPass];
+#pragma unroll
+      for (int u = 0; u < kPass; ++u)
+        if (base + lane + 32u * u < nfull) q[u] = __ldg(pl + 32 * u);
+#pragma unroll
+      for (int u = 0; u < kPass; ++u) {
+        const std::uint32_t kk = base + lane + 32u * u;
+        if (kk < nfull) {
+          const uint2 sv = sl[32 * u];
+          uint4 r;
+          merge8(sv.x, q[u].x, r.x, r.y);
+          merge8(sv.y, q[u].y, r.z, r.w);
+          out.chunk(full_lo + kk, r);
+        }
+      }
+    }
+    k = nfull + lane;  // the loops below find nothing left
+  }
+#endif
   for (; k + 32 * (UNROLL - 1) < nfull; k += 32 * UNROLL, sl += 32 * UNROLL, pl += 32 * UNROLL) {
 #pragma unroll
     for (int u = 0; u < UNROLL; ++u) {
