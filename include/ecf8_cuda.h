@@ -77,6 +77,18 @@ int ecf8_decode_host(const ecf8_sections *host, uint8_t *out, uint64_t out_len);
 int ecf8_decode_host_many(const ecf8_sections *const *host, uint8_t *const *outs, const uint64_t *out_lens,
                           int count);
 
+/* decode_parallel_into for a sequence of tensors through ONE page-locked
+ * buffer (buf_len >= the largest n_elem; decompress_streaming's reusable
+ * buffer, container.cpp:324-352): tensor i decodes into buf[0, n_elem), and
+ * fn(ctx, i, offset, n) is called -- in tensor order, offsets ascending --
+ * once bytes [offset, offset + n) of tensor i are in buf; the pipeline
+ * overwrites them only after fn returned.  The next tensor's sections cross
+ * PCIe and decode while the current one is still being handed over.  A
+ * non-zero return from fn stops the delivery (ECF8_EIO). */
+typedef int (*ecf8_chunk_fn)(void *ctx, int tensor, uint64_t offset, uint64_t n);
+int ecf8_decode_host_stream(const ecf8_sections *const *host, int count, uint8_t *buf, uint64_t buf_len,
+                            ecf8_chunk_fn fn, void *ctx);
+
 /* Page-lock / unlock a host buffer the host-span calls write into (the
  * ReusableBuffer of decompress_streaming): device-to-host copies into it run
  * at full PCIe rate instead of through a pageable bounce buffer.  Returns

@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -549,9 +550,31 @@ P rebase(P slot, std::uint64_t lo_bytes) {
 // blk_lo / blk_hi (optional): decode only blocks [blk_lo[i], blk_hi[i]) of
 // tensor i -- its elements [outpos[lo], outpos[hi]) land at the same offsets
 // of outs[i] (decode_block); only those blocks' sections cross PCIe.
+// Streaming delivery (ecf8_decode_host_stream): every tensor decodes into the
+// same pinned buffer; chunk (tensor i, [o0, o1)) is handed to `fn` once its
+// D2H completed, in order, and a D2H into the buffer waits until the earlier
+// tensors' bytes it overwrites were handed over.
+struct StreamSink {
+  ecf8_chunk_fn fn = nullptr;
+  void* ctx = nullptr;
+  struct Pending {
+    int slot, tensor;
+    std::uint64_t o0, o1;
+  };
+  std::deque<Pending> q;
+  int rc = 0;
+};
+
 int host_pipeline(const ecf8_sections* const* ss, const std::uint64_t* nbs, std::uint8_t* const* outs, int count,
-                  const std::uint64_t* blk_lo = nullptr, const std::uint64_t* blk_hi = nullptr) {
+                  const std::uint64_t* blk_lo = nullptr, const std::uint64_t* blk_hi = nullptr,
+                  StreamSink* sink = nullptr) {
   HostCtx& c = host_ctx();
+  auto deliver_front = [&]() {  // the oldest pending chunk, once its D2H completed
+    const StreamSink::Pending p = sink->q.front();
+    sink->q.pop_front();
+    cu(cudaEventSynchronize(c.slot[p.slot].out_done), "sync");
+    if (sink->rc == 0 && p.o1 > p.o0) sink->rc = sink->fn(sink->ctx, p.tensor, p.o0, p.o1 - p.o0);
+  };
   std::uint64_t k = 0, remaining = 0;
   for (int i = 0; i < count; ++i)
     remaining += blk_lo ? ss[i]->outpos[blk_hi[i]] - ss[i]->outpos[blk_lo[i]] : ss[i]->n_elem;
@@ -674,6 +697,18 @@ int host_pipeline(const ecf8_sections* const* ss, const std::uint64_t* nbs, std:
       cu(cudaEventRecord(sl.run, c.s_run), "record");
 
       cu(cudaStreamWaitEvent(c.s_out, sl.run, 0), "wait");
+      if (sink) {
+        // the slot's previous chunk, and earlier tensors' chunks this D2H
+        // overwrites in the shared buffer, are handed over first (in order)
+        while (!sink->q.empty() && (sink->q.front().slot == static_cast<int>(k % HostCtx::kSlots) ||
+                                    (sink->q.front().tensor < i && sink->q.front().o0 < o1))) {
+          deliver_front();
+        }
+        // ... and the ones already complete (keeps the host writer busy)
+        while (!sink->q.empty() && cudaEventQuery(c.slot[sink->q.front().slot].out_done) == cudaSuccess)
+          deliver_front();
+        cudaGetLastError();
+      }
       if (out_pinned) {
         if (o1 > o0)
           cu(cudaMemcpyAsync(out + o0, sl.out + (o0 - dk.out_offset), o1 - o0, cudaMemcpyDeviceToHost, c.s_out),
@@ -695,10 +730,13 @@ int host_pipeline(const ecf8_sections* const* ss, const std::uint64_t* nbs, std:
         }
       }
       cu(cudaEventRecord(sl.out_done, c.s_out), "record");
+      if (sink) sink->q.push_back({static_cast<int>(k % HostCtx::kSlots), i, o0, o1});
       lo = hi;
     }
     cu(cudaEventRecord(mt.done, c.s_run), "record");
   }
+  if (sink)
+    while (!sink->q.empty()) deliver_front();
   cu(cudaStreamSynchronize(c.s_out), "sync");
   for (auto& sl : c.slot) drain_out(sl);
   return ECF8_OK;
@@ -1073,6 +1111,32 @@ int ecf8_decode_host_many(const ecf8_sections* const* ss, uint8_t* const* outs, 
     if (!any) return ECF8_OK;
     if (int rc = require_device()) return rc;
     return host_pipeline(ss, nbs.data(), outs, count);
+  });
+}
+
+int ecf8_decode_host_stream(const ecf8_sections* const* ss, int count, uint8_t* buf, uint64_t buf_len,
+                            ecf8_chunk_fn fn, void* ctx) {
+  return guarded([&]() -> int {
+    if (count < 0 || (count > 0 && (!ss || !fn))) return fail(ECF8_EINVAL, "null argument");
+    std::vector<std::uint64_t> nbs(static_cast<std::size_t>(count));
+    bool any = false;
+    for (int i = 0; i < count; ++i) {
+      if (!ss[i]) return fail(ECF8_EINVAL, "null sections");
+      if (ss[i]->n_elem > buf_len) return fail(ECF8_EINVAL, "output size mismatch");
+      if (int rc = validate(ss[i], &nbs[i])) return rc;
+      any |= ss[i]->n_elem > 0;
+    }
+    if (!any) return ECF8_OK;
+    if (!buf) return fail(ECF8_EINVAL, "null argument");
+    if (!is_pinned(buf)) return fail(ECF8_EINVAL, "stream buffer must be page-locked");
+    if (int rc = require_device()) return rc;
+    std::vector<std::uint8_t*> outs(static_cast<std::size_t>(count), buf);
+    StreamSink sink;
+    sink.fn = fn;
+    sink.ctx = ctx;
+    if (int rc = host_pipeline(ss, nbs.data(), outs.data(), count, nullptr, nullptr, &sink)) return rc;
+    if (sink.rc) return fail(ECF8_EIO, "chunk sink failed");
+    return ECF8_OK;
   });
 }
 
