@@ -237,6 +237,8 @@ struct ecf8_fused {
   std::uint32_t split_k = 1;
   std::uint8_t* xt = nullptr;  // swizzled-X workspace (grow-only)
   std::uint64_t xt_cap = 0;
+  std::uint8_t* scratch = nullptr;  // L2-ring variant: kRingSlots K tiles per CTA
+  std::uint64_t scratch_cap = 0;
   std::uint64_t n = 0, k = 0;
   std::uint32_t w_fmt = 0;
   bool fsm = false;  // byte-step direct decode: the code has a byte-step decoder and every tile is direct
@@ -1346,6 +1348,27 @@ int ecf8_fused_gemm(const ecf8_fused* f, const uint8_t* d_x, uint32_t m, float s
     a.stages_a = ecf8::dev::fused_stages_a(
         a.m_pad, ecf8::dev::fused_warp_smem(f->w->T, f->w->desc.lmin, a.m_pad, f->fsm), f->fsm);
     a.stages_b = ecf8::dev::fused_stages_b(a.m_pad, f->fsm);
+    // byte-step weights: the L2-ring variant (decode warps as the standalone
+    // decoder, decoded K tiles through a per-CTA ring in L2); ECF8_FUSED_L2=0: the shared-memory ring
+    static const bool l2 = [] {
+      const char* e = std::getenv("ECF8_FUSED_L2");
+      return !e || std::atoi(e) != 0;
+    }();
+    a.scratch = nullptr;
+    if (l2 && f->fsm && ecf8::dev::fused_l2_stages(a.m_pad) >= 2) {
+      const std::uint64_t need = static_cast<std::uint64_t>(f->n_cta[pi]) * ecf8::dev::kRingSlots * 16384;
+      if (need > mf->scratch_cap) {
+        cu(cudaStreamSynchronize(st), "sync");
+        if (mf->scratch) cudaFree(mf->scratch);
+        mf->scratch = nullptr;
+        mf->scratch_cap = 0;
+        cu(cudaMalloc(&mf->scratch, need), "cudaMalloc(fused ring)");
+        mf->scratch_cap = need;
+      }
+      a.scratch = mf->scratch;
+      a.stages_a = ecf8::dev::fused_l2_stages(a.m_pad);
+      a.stages_b = a.stages_a;
+    }
     if (a.stages_a < 2) return fail(ECF8_EINVAL, "fused GEMM: shared memory too small for this m");
     a.acc_cols = 32;
     while (a.acc_cols < a.m_pad) a.acc_cols <<= 1;
@@ -1367,6 +1390,7 @@ void ecf8_fused_free(ecf8_fused* f) {
   for (auto* p : f->d_plan)
     if (p) cudaFree(p);
   if (f->xt) cudaFree(f->xt);
+  if (f->scratch) cudaFree(f->scratch);
   delete f;
 }
 

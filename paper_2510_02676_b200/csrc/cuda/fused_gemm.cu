@@ -642,6 +642,244 @@ __global__ void __launch_bounds__((decode_warps<LW, SLOT_ROWS, WIDE, FSM>() + ex
   }
 }
 
+// ---- L2-ring variant (byte-step weights) ---------------------------------
+//
+// The shared-memory A ring caps the decode warps in flight (a warp tile is
+// ~0.4 K tiles of ring; 12 warps fill a 5-stage ring).  Here the decode warps
+// run exactly as the standalone decoder (23 warps, direct tiles, packed bytes
+// from L2) and store merged FP8 bytes to a per-CTA ring of kRingSlots K tiles
+// in global memory, small enough to stay in L2; a loader warp moves each
+// completed K tile (and its X tile) into a shared-memory stage by bulk async
+// copy, an MMA warp multiplies.  Per K tile t, slot t % R:
+//   decode warps  wait until the loader copied slot t - R (g2_loaded), store,
+//                 fence.proxy.async.global, arrive on g2_full[slot] with their bytes
+//   loader        wait g2_full (16384 bytes), wait the stage's MMAs (g2_empty),
+//                 bulk-copy A (16 KB) + X into stage t % S (g2_sfull)
+//   MMA warp      wait g2_sfull, publish g2_loaded = t + 1, tcgen05.mma, commit g2_empty
+
+#ifndef ECF8_FUSED_L2_WARPS
+#define ECF8_FUSED_L2_WARPS 23
+#endif
+constexpr int kL2DecodeWarps = ECF8_FUSED_L2_WARPS;
+constexpr int kL2MaxStages = 6;
+__shared__ alignas(8) unsigned long long g2_full[kRingSlots];
+__shared__ alignas(8) unsigned long long g2_sfull[kL2MaxStages];
+__shared__ alignas(8) unsigned long long g2_empty[kL2MaxStages];
+__shared__ std::uint32_t g2_loaded;
+__shared__ unsigned g2_qnext;
+
+struct GRingOut {
+  std::uint8_t *cf, *cl;         // address of chunk 0 if it were in K tile tf / tf + 1 (chunk c at + 16 c)
+  std::uint64_t S0;              // element of chunk 0
+  std::uint32_t c_lo, c_hi;      // chunks inside the CTA range (e0, e1 are multiples of 16384)
+  std::uint32_t c_split;         // first chunk of K tile tf + 1
+  std::uint32_t tf, bf, bl, bar_f, bar_l;
+  const Flush* fl;
+  int lane;
+  __device__ __forceinline__ void wait_slot(std::uint32_t t) const {
+    if (t < kRingSlots) return;
+    const std::uint32_t need = t - kRingSlots + 1, addr = smem_addr(&g2_loaded);
+    for (;;) {
+      std::uint32_t v;
+      asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+      if (__all_sync(0xffffffffu, v >= need)) return;
+      (*fl)();
+      __nanosleep(64);
+    }
+  }
+  __device__ __forceinline__ void wait() const {
+    wait_slot(tf);
+    if (bl) wait_slot(tf + 1);
+  }
+  __device__ __forceinline__ void chunk(std::uint32_t c, const uint4& r) const {
+    if (c < c_lo || c >= c_hi) return;
+    std::uint8_t* p = (c < c_split ? cf : cl) + 16 * static_cast<std::uint64_t>(c);
+    asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(r.x), "r"(r.y), "r"(r.z), "r"(r.w) : "memory");
+  }
+  __device__ __forceinline__ void byte(std::uint32_t i, std::uint8_t b) const {
+    const std::uint32_t c = i >> 4;
+    if (c < c_lo || c >= c_hi) return;
+    *((c < c_split ? cf : cl) + i) = b;
+  }
+  __device__ __forceinline__ void done() const {
+    // the generic-proxy stores must be visible to the loader's bulk copies
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+      if (bf) mbar_arrive(bar_f, bf);
+      if (bl) mbar_arrive(bar_l, bl);
+    }
+  }
+};
+
+__global__ void __launch_bounds__((kL2DecodeWarps + 2) * 32, 1) fused_l2_kernel(const __grid_constant__ FusedArgs args) {
+  constexpr int kWarps = kL2DecodeWarps + 2, kLoader = kL2DecodeWarps, kMma = kL2DecodeWarps + 1;
+  using WSm = WarpPipeSmem<1, 32 * 8 * 32 / 8 + 8>;  // the staging tile (packed bytes come from L2)
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  asm volatile("griddepcontrol.launch_dependents;");
+  const FusedCta cta = args.plan[blockIdx.x];
+  const std::uint32_t n_kt = cta.tile1 - cta.tile0, KT = args.k / 128, nt0 = cta.tile0 / KT;
+  const std::uint32_t S = args.stages_a;
+  const std::uint32_t raw = smem_addr(smem_raw);
+  const std::uint32_t a_base = (raw + 1023u) & ~1023u;
+  const std::uint32_t b_base = a_base + S * kTileElems, b_bytes = args.m_pad * 128u;
+  WSm* const wsm = reinterpret_cast<WSm*>(smem_raw + (b_base + S * b_bytes - raw));
+  std::uint8_t* const ring = args.scratch + static_cast<std::uint64_t>(blockIdx.x) * kRingSlots * kTileElems;
+
+  if (threadIdx.x == 0) {
+    g_wdesc = args.w;
+    g_wdesc.blk_begin = cta.blk_begin;
+    g_wdesc.blk_end = cta.blk_end;
+    g_wdesc.tile_begin = 0;
+  }
+  if (warp == kMma) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(&g_tmem)),
+                 "r"(args.tmem_cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (warp == kLoader && lane == 0) {
+    for (std::uint32_t r = 0; r < kRingSlots; ++r) mbar_init(smem_addr(&g2_full[r]), kTileElems);
+    for (std::uint32_t s = 0; s < S; ++s) {
+      mbar_init(smem_addr(&g2_sfull[s]), 1);
+      mbar_init(smem_addr(&g2_empty[s]), 1);
+    }
+    for (std::uint32_t b = 0; b < args.acc_bufs; ++b) {
+      mbar_init(smem_addr(&g_segdone[b]), 1);
+      mbar_init(smem_addr(&g_accfree[b]), 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    g2_loaded = 0;
+    g2_qnext = kL2DecodeWarps;
+    for (int w = 0; w < 4; ++w) g_nflush[w] = 0;
+  }
+  {
+    const uint4* f4 = reinterpret_cast<const uint4*>(args.w.fsm);
+    const uint4* c4 = reinterpret_cast<const uint4*>(args.w.fsm_cm);
+    for (int i = threadIdx.x; i < 256 * kFsmStates / 4; i += kWarps * 32) reinterpret_cast<uint4*>(g_fsmf)[i] = __ldg(f4 + i);
+    for (int i = threadIdx.x; i < 256 * kFsmStates / 16; i += kWarps * 32) reinterpret_cast<uint4*>(g_cmf)[i] = __ldg(c4 + i);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const TensorDesc& d = g_wdesc;
+  const std::uint32_t tmem_d = g_tmem;
+  const std::uint32_t nseg = n_kt ? (cta.tile1 - 1) / KT - nt0 + 1 : 0;
+  const Flush fl{&args, tmem_d, nt0, nseg};
+  const std::uint32_t log2T = 31 - __clz(d.T);
+
+  if (warp < kL2DecodeWarps) {
+    // ---- decode warps: the standalone kernel's loop over the CTA's ECF8 tiles
+    const std::uint32_t m_blk = 256u >> log2T;
+    const std::uint64_t n_tiles = (cta.blk_end - cta.blk_begin + m_blk - 1) / m_blk;
+    WSm& ws = wsm[warp];
+    const FsmAt ft{smem_addr(g_fsmf), smem_addr(g_cmf)};
+    std::uint64_t tile = warp;
+    if (tile < n_tiles && lane < 5) prefetch_tile_l2(d, tile, log2T, lane);
+    while (tile < n_tiles) {
+      WarpInT<8> cur;
+      load_warp_tile<8, true>(d, tile, log2T, lane, cur);
+      unsigned claim = 0;
+      if (lane == 0) claim = atomicAdd(&g2_qnext, 1u);
+      const std::uint64_t next = __shfl_sync(0xffffffffu, claim, 0);
+      if (next < n_tiles && lane < 5) prefetch_tile_l2(d, next, log2T, lane);
+      if (lane == 0) {  // this tile's sign/mantissa bytes -> L2 (read at write-back)
+        const std::uint64_t p0 = (cur.A >> 1) & ~std::uint64_t{15};
+        const std::uint32_t bytes = static_cast<std::uint32_t>((((cur.E + 1) >> 1) - p0 + 15) & ~std::uint64_t{15});
+        if (bytes) prefetch_l2(d.packed + p0, bytes);
+      }
+      const std::uint64_t A = cur.A > cta.e0 ? cur.A : cta.e0, E = cur.E < cta.e1 ? cur.E : cta.e1;
+      if (A < E) {
+        direct_tile<4, 8, true>(
+            d, cur, ws, lane,
+            [&] {
+              GRingOut o;
+              o.S0 = cur.A & ~std::uint64_t{15};
+              o.tf = static_cast<std::uint32_t>((A - cta.e0) >> 14);
+              const std::uint32_t tl = static_cast<std::uint32_t>((E - 1 - cta.e0) >> 14);
+              const std::uint64_t bnd = cta.e0 + (static_cast<std::uint64_t>(o.tf + 1) << 14);
+              o.bf = static_cast<std::uint32_t>((E < bnd ? E : bnd) - A);
+              o.bl = tl != o.tf ? static_cast<std::uint32_t>(E - bnd) : 0u;
+              // element g of K tile t is at ring slot (t % R) + (g - e0 - 16384 t)
+              const std::int64_t s_rel = static_cast<std::int64_t>(o.S0) - static_cast<std::int64_t>(cta.e0);
+              o.cf = ring + static_cast<std::int64_t>(o.tf % kRingSlots) * kTileElems - (static_cast<std::int64_t>(o.tf) << 14) + s_rel;
+              o.cl = ring + static_cast<std::int64_t>((o.tf + 1) % kRingSlots) * kTileElems -
+                     (static_cast<std::int64_t>(o.tf + 1) << 14) + s_rel;
+              o.c_lo = s_rel >= 0 ? 0u : static_cast<std::uint32_t>((-s_rel) >> 4);
+              o.c_hi = static_cast<std::uint32_t>((static_cast<std::int64_t>(cta.e1) - static_cast<std::int64_t>(o.S0)) >> 4);
+              o.c_split = static_cast<std::uint32_t>((static_cast<std::int64_t>(bnd) - static_cast<std::int64_t>(o.S0)) >> 4);
+              o.bar_f = smem_addr(&g2_full[o.tf % kRingSlots]);
+              o.bar_l = smem_addr(&g2_full[(o.tf + 1) % kRingSlots]);
+              o.fl = &fl;
+              o.lane = lane;
+              return o;
+            },
+            tile_verified(d, cur, log2T), ft);
+      }
+      fl.run(false);  // warps 0-3: flush the segments the MMAs have finished
+      tile = next;
+    }
+    fl.run(true);
+  } else if (warp == kLoader) {
+    // ---- loader: completed K tiles of the ring + their X tiles -> shared-memory stages
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // x_tiles_kernel: X tiles written, y zeroed
+    if (lane == 0) {
+      for (std::uint32_t t = 0; t < n_kt; ++t) {
+        const std::uint32_t r = t % kRingSlots, s = t % S;
+        mbar_wait_sleep(smem_addr(&g2_full[r]), (t / kRingSlots) & 1u, 32);
+        if (t >= S) mbar_wait_sleep(smem_addr(&g2_empty[s]), ((t / S) - 1) & 1u, 32);
+        const std::uint32_t bar = smem_addr(&g2_sfull[s]);
+        const std::uint32_t kt = (cta.tile0 + t) % KT;
+        asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(bar),
+                     "r"(kTileElems + b_bytes)
+                     : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         a_base + s * kTileElems),
+                     "l"(ring + static_cast<std::uint64_t>(r) * kTileElems), "r"(kTileElems), "r"(bar)
+                     : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         b_base + s * b_bytes),
+                     "l"(args.xt + static_cast<std::uint64_t>(kt) * b_bytes), "r"(b_bytes), "r"(bar)
+                     : "memory");
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---- MMA warp
+    const std::uint32_t idesc = (1u << 4) | (args.w_fmt << 7) | (0u << 10) | ((args.m_pad >> 3) << 17) | ((128u >> 4) << 24);
+    for (std::uint32_t t = 0; t < n_kt; ++t) {
+      const std::uint32_t s = t % S;
+      const std::uint32_t g = cta.tile0 + t;
+      const std::uint32_t seg = g / KT - nt0, buf = seg % args.acc_bufs;
+      const bool first_of_seg = t == 0 || g % KT == 0, last_of_seg = t + 1 == n_kt || (g + 1) % KT == 0;
+      if (first_of_seg && seg >= args.acc_bufs)
+        mbar_wait_sleep(smem_addr(&g_accfree[buf]), ((seg / args.acc_bufs) - 1) & 1u, 32);
+      mbar_wait_sleep(smem_addr(&g2_sfull[s]), (t / S) & 1u, 32);
+      tc_fence_after();
+      if (lane == 0) {
+        // the ring slot's bytes are in shared memory: writers may reuse it
+        asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_addr(&g2_loaded)), "r"(t + 1) : "memory");
+        const std::uint32_t a_st = a_base + s * kTileElems, bdst = b_base + s * b_bytes;
+#pragma unroll
+        for (std::uint32_t k = 0; k < 4; ++k)
+          mma_f8(tmem_d + buf * args.acc_cols, smem_desc(a_st + 32 * k), smem_desc(bdst + 32 * k), idesc,
+                 !(first_of_seg && k == 0));
+        tc_commit(smem_addr(&g2_empty[s]));
+        if (last_of_seg) tc_commit(smem_addr(&g_segdone[buf]));
+      }
+      __syncwarp();
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kMma) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d), "r"(args.tmem_cols)
+                 : "memory");
+  }
+}
+
 // x [m, k] row-major -> xt [k/128][m_pad][128 B] in the 128B-swizzled
 // K-major image (rows >= m zero), so every B tile is one contiguous copy.
 // Also zeroes y (the split-K partial sums are added into it).  The fused
@@ -754,6 +992,14 @@ cudaError_t launch_geometry(const FusedArgs& args, std::uint32_t n_cta, cudaStre
   return args.w.lmin >= 2 ? launch_lw<4, 17, WIDE>(args, n_cta, s) : launch_lw<4, 33, WIDE>(args, n_cta, s);
 }
 
+std::uint32_t fused_l2_stages(std::uint32_t m_pad) {
+  // 227 KB: static ~21 KB, the decode warps' staging tiles, S x (A 16 KB + X m_pad x 128 B), 1 KB alignment
+  const std::uint32_t warps = kL2DecodeWarps * static_cast<std::uint32_t>(sizeof(WarpPipeSmem<1, 32 * 8 * 32 / 8 + 8>));
+  const std::uint32_t budget = 232448 - 22 * 1024 - warps - 1024;
+  const std::uint32_t s = budget / (kTileElems + m_pad * 128);
+  return s < 2 ? 0u : (s > static_cast<std::uint32_t>(kL2MaxStages) ? kL2MaxStages : s);
+}
+
 cudaError_t launch_fused_gemm(const FusedArgs& args, std::uint32_t n_cta, cudaStream_t s) {
   const std::uint64_t chunks = static_cast<std::uint64_t>(args.k / 128) * args.m_pad * 8;
   const unsigned blocks = static_cast<unsigned>(std::min<std::uint64_t>((chunks + 255) / 256, 4 * 148));
@@ -772,6 +1018,24 @@ cudaError_t launch_fused_gemm(const FusedArgs& args, std::uint32_t n_cta, cudaSt
                                            args.m_pad, args.k, args.y, static_cast<std::uint64_t>(args.m) * args.n);
         e != cudaSuccess)
       return e;
+  }
+  if (args.scratch) {
+    const std::uint32_t smem = 1024 + args.stages_a * (kTileElems + args.m_pad * 128) +
+                               kL2DecodeWarps * static_cast<std::uint32_t>(sizeof(WarpPipeSmem<1, 32 * 8 * 32 / 8 + 8>));
+    cudaError_t e = cudaFuncSetAttribute(fused_l2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    static const bool pdl = std::getenv("ECF8_NO_PDL") == nullptr;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(n_cta);
+    cfg.blockDim = dim3((kL2DecodeWarps + 2) * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, fused_l2_kernel, args);
   }
   return args.m_pad > 128 ? launch_geometry<true>(args, n_cta, s) : launch_geometry<false>(args, n_cta, s);
 }

@@ -39,7 +39,13 @@ struct FusedArgs {
   std::uint32_t w_fmt;       // 0 E4M3, 1 E5M2
   std::uint32_t fsm;         // 1: byte-step direct decode (lane offsets known for every tile; 8-window lanes)
   float scale;
+  std::uint8_t* scratch;     // L2-ring variant: kRingSlots x 16 KB per CTA (nullptr: the shared-memory ring kernel)
 };
+
+#ifndef ECF8_FUSED_RING
+#define ECF8_FUSED_RING 16
+#endif
+constexpr std::uint32_t kRingSlots = ECF8_FUSED_RING;  // decoded K tiles per CTA between the decode warps and the MMA (L2-resident)
 
 // Windows per decode lane for a tiled weight (4 or 8; 0 = unsupported) and
 // the shared memory of one decode warp's pipeline (fused_gemm.cu).
@@ -49,5 +55,7 @@ std::uint32_t fused_stages_b(std::uint32_t m_pad, bool fsm);
 std::uint32_t fused_stages_a(std::uint32_t m_pad, std::uint32_t warp_smem, bool fsm);
 std::uint32_t fused_smem_bytes(std::uint32_t m_pad, std::uint32_t stages_a, std::uint32_t warp_smem, bool fsm);
 cudaError_t launch_fused_gemm(const FusedArgs& args, std::uint32_t n_cta, cudaStream_t s);
+// Stages of the L2-ring variant for this m (0: it does not fit).
+std::uint32_t fused_l2_stages(std::uint32_t m_pad);
 
 }  // namespace ecf8::dev
