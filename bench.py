@@ -330,7 +330,6 @@ def run_reference_arm(args, rank, world):
     blob = ref.compress_raw(raw, T_BLOCK)
     del raw
     hs = ref.container_tensors(blob)
-    del blob
     algo = sum(ref.algorithmic_bytes(h) for h in hs)
     elems = sum(ref.n_elem(h) for h in hs)
     outs = [np.empty(ref.n_elem(h), np.uint8) for h in hs]
@@ -345,6 +344,8 @@ def run_reference_arm(args, rank, world):
             dt += t
         if i >= args.warmup:
             step_s.append(dt)
+    legs = reference_legs(ref, hs, blob, cores)
+    del blob
     for h in hs:
         ref.free(h)
     total = sum(step_s)
@@ -355,9 +356,54 @@ def run_reference_arm(args, rank, world):
               f"{algo / 1e9:.3f} GB algorithmic), inputs made by the reference's synth_raw + compress_tensors")
     line["cpu_baseline"] = {"value": round(value, 3), "unit": "GB/s", "cores": cores, "kind": "reference",
                             "sample": sample}
+    line["cpu_baseline"]["legs"] = legs
     line["work"] = {"elements_per_step": int(elems), "bytes_per_step": int(algo)}
     line["e2e"] = {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
     print(json.dumps(line), flush=True)
+
+
+def reference_legs(ref, hs, blob, cores):
+    """The other CPU baselines BASELINE.md plans, on bounded samples:
+    decode_parallel_into (codec.cpp:256-273) and decode_reference
+    (codec.cpp:125-131) on ONE thread over the layer's first tensor, and the
+    all-threads layer decode of the reference built at -march=x86-64-v4
+    (oracle/_ref/libecf8_ref_v4.so, where the CPU has AVX-512).  GB/s of
+    algorithmic bytes, like the line's value; each output checked equal to
+    the arm's own decode."""
+    from _oracle import reference_v4
+
+    h0 = hs[0]
+    n0, algo0 = ref.n_elem(h0), ref.algorithmic_bytes(h0)
+    legs = {"sample_1_thread": f"tensor 0 of the layer ({n0 / 1e6:.1f} M elements, {algo0 / 1e9:.3f} GB algorithmic)"}
+    want, _ = ref.decode(h0, n0, cores)
+    got, dt = ref.decode(h0, n0, 1)
+    assert np.array_equal(got, want)
+    legs["decode_parallel_into_1_thread_gbs"] = round(algo0 / dt / 1e9, 4)
+    got, dt = ref.decode_reference(h0, n0)
+    assert np.array_equal(got, want)
+    legs["decode_reference_1_thread_gbs"] = round(algo0 / dt / 1e9, 4)
+    ref.lib.ecf8ref_tensor_decode(h0, got.ctypes.data, cores)  # restore the arm's thread count
+    ref4 = reference_v4()
+    if ref4 is None:
+        legs["decode_parallel_into_all_threads_x86_64_v4_gbs"] = None
+        return legs
+    hs4 = ref4.container_tensors(blob)
+    algo = sum(ref4.algorithmic_bytes(h) for h in hs4)
+    dt_best = None
+    for _ in range(2):  # warm pass + timed pass
+        dt = 0.0
+        for h in hs4:
+            out = np.empty(ref4.n_elem(h), np.uint8)
+            t = ref4.lib.ecf8ref_tensor_decode(h, out.ctypes.data, cores)
+            assert t >= 0, ref4._err()
+            dt += t
+        dt_best = dt
+    got4, _ = ref4.decode(hs4[0], n0, cores)
+    assert np.array_equal(got4, want)
+    for h in hs4:
+        ref4.free(h)
+    legs["decode_parallel_into_all_threads_x86_64_v4_gbs"] = round(algo / dt_best / 1e9, 4)
+    return legs
 
 
 def timed_region(torch, dist, local, stream, batches, steps, warmup):

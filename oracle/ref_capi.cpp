@@ -206,6 +206,20 @@ double ecf8ref_tensor_decode(void* h, std::uint8_t* out, int nthreads) {
   return rc == 0 ? dt : -1.0;
 }
 
+// The reference's sequential decoder (codec.cpp:125-131) on a kept tensor;
+// returns seconds (the returned vector's allocation included: that is the API).
+double ecf8ref_tensor_decode_reference(void* h, std::uint8_t* out) {
+  auto* r = static_cast<RefTensor*>(h);
+  double dt = -1.0;
+  guarded([&] {
+    const auto t0 = std::chrono::steady_clock::now();
+    const auto v = ecf8::decode_reference(r->t, r->lut);
+    dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    std::memcpy(out, v.data(), v.size());
+  });
+  return dt;
+}
+
 int ecf8ref_max_threads() { return omp_get_max_threads(); }
 
 }  // extern "C"

@@ -204,6 +204,8 @@ class Reference:
         L.ecf8ref_tensor_free.argtypes = [_P]
         L.ecf8ref_tensor_decode.restype = C.c_double
         L.ecf8ref_tensor_decode.argtypes = [_P, _P, C.c_int]
+        L.ecf8ref_tensor_decode_reference.restype = C.c_double
+        L.ecf8ref_tensor_decode_reference.argtypes = [_P, _P]
         L.ecf8ref_container_tensors.argtypes = [_P, C.c_size_t, C.POINTER(_P), C.c_uint32, C.POINTER(C.c_uint32)]
         L.ecf8ref_tensor_n_elem.restype = C.c_uint64
         L.ecf8ref_tensor_n_elem.argtypes = [_P]
@@ -274,6 +276,13 @@ class Reference:
         assert dt >= 0, self._err()
         return out, dt
 
+    def decode_reference(self, h, n_elem):
+        """decode_reference (the sequential API decoder), single-threaded."""
+        out = np.zeros(n_elem, np.uint8)
+        dt = self.lib.ecf8ref_tensor_decode_reference(h, _p(out))
+        assert dt >= 0, self._err()
+        return out, dt
+
     def free(self, h):
         self.lib.ecf8ref_tensor_free(h)
 
@@ -298,3 +307,19 @@ def oracle() -> Oracle:
 
 def reference() -> Reference | None:
     return Reference() if os.path.exists(REF_SO) else None
+
+
+REF_SO_V4 = REF_SO.replace("libecf8_ref.so", "libecf8_ref_v4.so")
+
+
+def cpu_has_avx512() -> bool:
+    try:
+        flags = set(open("/proc/cpuinfo").read().split("flags", 2)[1].split("\n", 1)[0].split())
+    except (OSError, IndexError):
+        return False
+    return {"avx512f", "avx512bw", "avx512vl", "avx512dq", "avx512cd"} <= flags
+
+
+def reference_v4() -> Reference | None:
+    """The reference built at -march=x86-64-v4, where this CPU runs it."""
+    return Reference(REF_SO_V4) if os.path.exists(REF_SO_V4) and cpu_has_avx512() else None

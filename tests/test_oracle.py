@@ -171,3 +171,28 @@ def test_oracle_vs_reference_containers(orc, ref):
         # section bytes of tensor 0 must sit verbatim in the reference container
         assert t["encoded"].tobytes() in blob and t["packed"].tobytes() in blob
         assert np.array_equal(orc.decode_parallel(t), x)
+
+
+def test_reference_arm_legs_agree(ref):
+    """The bench reference arm's CPU legs: decode_parallel_into at 1 and all
+    threads, decode_reference, and the x86-64-v4 build decode the same bytes."""
+    from _oracle import reference_v4
+
+    from paper_2510_02676_b200.codec import raw_file
+
+    x = ref.synth(1.8, 0.05, 50000, 17)
+    blob = ref.compress_raw(raw_file([("x", [50000], x)]), 256)
+    (h,) = ref.container_tensors(blob)
+    try:
+        assert np.array_equal(ref.decode(h, x.size, 0)[0], x)
+        assert np.array_equal(ref.decode(h, x.size, 1)[0], x)
+        assert np.array_equal(ref.decode_reference(h, x.size)[0], x)
+    finally:
+        ref.free(h)
+    r4 = reference_v4()
+    if r4 is not None:
+        (h4,) = r4.container_tensors(blob)
+        try:
+            assert np.array_equal(r4.decode(h4, x.size, 0)[0], x)
+        finally:
+            r4.free(h4)
