@@ -254,8 +254,11 @@ def load_peaks():
 
 
 def kernel_name():
-    nw = os.environ.get("ECF8_WARPS", "24")
-    return "decode_kernel<4,16,3>" if os.environ.get("ECF8_NO_WARP_KERNEL") == "1" else f"decode_warp_kernel<{nw}>"
+    if os.environ.get("ECF8_NO_WARP_KERNEL") == "1":
+        return "decode_kernel<4,16,3>"
+    if os.environ.get("ECF8_NO_DIRECT_KERNEL") is None:
+        return "decode_warp_kernel<24,0,0,1> (variant 7: every tile direct)"
+    return f"decode_warp_kernel<{os.environ.get('ECF8_WARPS', '24')}>"
 
 
 def load_traffic(workload):

@@ -353,7 +353,7 @@ void upload_into(ecf8_dev_tensor* t, const ecf8_sections* s, std::uint64_t nb, c
 // keep the reference's window-by-window semantics.
 void verify_into(ecf8_dev_tensor* t, cudaStream_t st) {
   static const bool off = std::getenv("ECF8_NO_CONT_WALK") != nullptr;  // A/B runs
-  const int vid = t->n_elem ? ecf8::dev::variant_for(t->T, t->desc.lmin, t->desc.fsm != nullptr, t->desc.fsm64 != nullptr).id : -1;
+  const int vid = t->n_elem ? ecf8::dev::variant_of(t->desc).id : -1;
   if (off || (vid != 4 && vid != 5)) return;
   std::uint32_t* const ok = t->ok_bits;
   cu(cudaMemsetAsync(ok, 0xFF, 4 * ((t->n_vtiles + 31) / 32), st), "memset(tile_ok)");
@@ -365,6 +365,18 @@ void verify_into(ecf8_dev_tensor* t, cudaStream_t st) {
   if (vid == 4) {
     t->desc.lane_start = t->lane_start;
     t->desc.tile_direct = t->direct_bits;
+    // every tile placed directly: variant 7 (no fallback path; one read-back
+    // of the tile bitmap)
+    static const bool no_direct = std::getenv("ECF8_NO_DIRECT_KERNEL") != nullptr;  // A/B runs
+    if (!no_direct) {
+      const std::size_t words = (t->n_vtiles + 31) / 32;
+      std::vector<std::uint32_t> dirb(words);
+      cu(cudaMemcpyAsync(dirb.data(), t->direct_bits, 4 * words, cudaMemcpyDeviceToHost, st), "D2H tile_direct");
+      cu(cudaStreamSynchronize(st), "sync");
+      bool all = true;
+      for (std::uint64_t v = 0; v < t->n_vtiles; ++v) all &= (dirb[v >> 5] >> (v & 31)) & 1u;
+      t->desc.all_direct = all ? 1u : 0u;
+    }
   }
   // Variant 6 (1-bit codes by byte steps) places every tile directly and has
   // no per-window fallback: it is chosen only when every tile passed (one
@@ -391,7 +403,7 @@ void verify_into(ecf8_dev_tensor* t, cudaStream_t st) {
 // Single-descriptor launch: the descriptor rides in the kernel parameters.
 int launch_one(const TensorDesc& d, cudaStream_t st, int variant_override = -1) {
   if (d.blk_end <= d.blk_begin) return ECF8_OK;
-  ecf8::dev::Variant v = ecf8::dev::variant_for(d.T, d.lmin, d.fsm != nullptr, d.fsm64 != nullptr);
+  ecf8::dev::Variant v = ecf8::dev::variant_of(d);
   if (variant_override >= 0) v.id = variant_override;
   ecf8::dev::LaunchArgs a{};
   a.descs = nullptr;
@@ -405,7 +417,7 @@ int launch_one(const TensorDesc& d, cudaStream_t st, int variant_override = -1) 
 
 // Launch variant for a device tensor.
 int tensor_variant(const ecf8_dev_tensor* t) {
-  return ecf8::dev::variant_for(t->T, t->desc.lmin, t->desc.fsm != nullptr, t->desc.fsm64 != nullptr).id;
+  return ecf8::dev::variant_of(t->desc).id;
 }
 
 // Per-thread state of the host-span path: three streams (copy-in, decode,
@@ -1029,14 +1041,14 @@ int ecf8_batch_create(const ecf8_dev_tensor* const* ts, uint8_t* const* d_outs, 
     auto b = std::make_unique<ecf8_batch>();
     for (int i = 0; i < count; ++i)
       if (ts[i] && ts[i]->pooled) b->pooled.push_back(ts[i]);
-    for (int kw = 0; kw < 7; ++kw) {  // one launch per kernel variant present (ids 0..6)
+    for (int kw = 0; kw < 8; ++kw) {  // one launch per kernel variant present (ids 0..7)
       std::vector<TensorDesc> group;
       std::uint64_t tiles = 0;
       int kwin_tile = 1;
       for (int i = 0; i < count; ++i) {
         const ecf8_dev_tensor* t = ts[i];
         if (!t) return fail(ECF8_EINVAL, "null tensor");
-        const ecf8::dev::Variant v = ecf8::dev::variant_for(t->T, t->desc.lmin, t->desc.fsm != nullptr, t->desc.fsm64 != nullptr);
+        const ecf8::dev::Variant v = ecf8::dev::variant_of(t->desc);
         if (t->n_elem == 0 || tensor_variant(t) != kw) continue;
         kwin_tile = v.tile_win;
         if (!d_outs[i] || (reinterpret_cast<std::uintptr_t>(d_outs[i]) & 15))

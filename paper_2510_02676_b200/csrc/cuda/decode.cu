@@ -40,6 +40,7 @@ bool warp_variant_enabled() {
 cudaError_t launch_decode_warp(const LaunchArgs& args, cudaStream_t s);       // decode_warp.cu
 cudaError_t launch_decode_fsm64(const LaunchArgs& args, cudaStream_t s);      // decode_warp.cu
 cudaError_t launch_decode_warp_wide(const LaunchArgs& args, cudaStream_t s);  // decode_warp.cu (1-bit codes)
+cudaError_t launch_decode_warp_direct(const LaunchArgs& args, cudaStream_t s);  // decode_warp.cu (every tile direct)
 
 namespace {
 
@@ -390,6 +391,7 @@ cudaError_t launch_decode(const LaunchArgs& args, int variant, cudaStream_t stre
     case 4: return launch_decode_warp(args, stream);
     case 5: return launch_decode_warp_wide(args, stream);
     case 6: return launch_decode_fsm64(args, stream);
+    case 7: return launch_decode_warp_direct(args, stream);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -37,7 +37,8 @@ struct TensorDesc {
   // element e goes to its row-major place under `out`, written only for e in
   // [out_lo, out_hi) (the rows a call asked for).
   std::uint64_t out_lo, out_hi;
-  std::uint32_t out_tiled_k, out_pad_;
+  std::uint32_t out_tiled_k;
+  std::uint32_t all_direct;      // every tile of the tensor is direct (upload check): variant 7
   std::uint32_t T;
   std::uint32_t n_luts;
   std::uint32_t lmin;  // shortest code length (selects the variant)
@@ -60,7 +61,9 @@ constexpr std::uint64_t kTileElemsMax = 1024 * 64;
 // 256-window tile, eight windows per lane; it needs T in [8, 256] (whole
 // blocks per tile, whole lanes per block) and Lmin >= 2.  Variant 5 is the
 // same kernel for 1-bit codes: 64-symbol windows double a lane's slot and
-// the staging tile, so 12 warps per SM.
+// the staging tile, so 12 warps per SM.  Variant 7 is variant 4 for tensors
+// whose every tile passed the upload check's direct-placement test: no
+// fallback path, the staging tile is the warp's only shared memory.
 struct Variant {
   int kwin;
   int slotw;
@@ -74,7 +77,8 @@ bool warp_variant_enabled();  // false when ECF8_NO_WARP_KERNEL=1 (A/B runs)
 // which variant 4 needs; fsm64: a complete code with a 1-bit word whose
 // tensor passed the upload check on every tile (variant 6, byte steps with
 // 64-bit entries); other codes with T in [8, 256] take variant 5.
-inline Variant variant_for(std::uint32_t T, std::uint32_t lmin, bool fsm = true, bool fsm64 = false) {
+inline Variant variant_for(std::uint32_t T, std::uint32_t lmin, bool fsm = true, bool fsm64 = false, bool direct = false) {
+  if (lmin >= 2 && fsm && direct && T >= 8 && T <= 256 && warp_variant_enabled()) return {8, 32, 7, 256};
   if (lmin >= 2 && fsm && T >= 8 && T <= 256 && warp_variant_enabled()) return {8, 32, 4, 256};
   if (lmin == 1 && fsm64 && T >= 8 && T <= 256 && warp_variant_enabled()) return {8, 64, 6, 256};
   if (lmin >= 1 && T >= 8 && T <= 256 && warp_variant_enabled()) return {8, 64, 5, 256};
@@ -83,6 +87,10 @@ inline Variant variant_for(std::uint32_t T, std::uint32_t lmin, bool fsm = true,
   if (lmin >= 2) return {4, 16, 2, 4 * kThreads};
   if (T == 1024) return {4, 32, 3, 4 * kThreads};
   return {2, 16, 1, 2 * kThreads};
+}
+
+inline Variant variant_of(const TensorDesc& d) {
+  return variant_for(d.T, d.lmin, d.fsm != nullptr, d.fsm64 != nullptr, d.all_direct != 0);
 }
 
 inline std::uint64_t blocks_per_tile(std::uint32_t T, int tile_win) {

@@ -31,6 +31,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <cstdlib>
+#include <type_traits>
 
 #include "decode.cuh"
 #include "decode_common.cuh"
@@ -45,6 +46,11 @@ namespace {
 // both double: 512 nibbles per lane, 16384 per tile.
 template <bool WIDE>
 using WarpSmemT = WarpPipeSmem<WIDE ? 65 : 33, (WIDE ? 2 : 1) * 32 * kSlotWords + 8>;
+// Direct-only tiles (every tile of the launch placed directly, the packed
+// bytes from L2): the staging tile alone.
+using DirectWarpSmem = WarpPipeSmem<1, 32 * kSlotWords + 8>;
+template <bool WIDE, bool DIRECT>
+using KernelWarpSmem = std::conditional_t<DIRECT, DirectWarpSmem, WarpSmemT<WIDE>>;
 
 // Static shared memory: the tile queue, the current segment's descriptor
 // (read field by field where used: a register copy would pin ~30 registers
@@ -96,6 +102,12 @@ constexpr int kWbUnroll = ECF8_WB_UNROLL;
 #endif
 #ifndef ECF8_CLAIM_AHEAD
 #define ECF8_CLAIM_AHEAD 0  // 1: claim the next tile one tile early (A/B: slower)
+#endif
+#ifndef ECF8_PF_GROUP
+#define ECF8_PF_GROUP 1  // >1: the sections of G tiles per L2 prefetch, AHEAD tiles ahead (A/B: slower, lower clocks)
+#endif
+#ifndef ECF8_PF_AHEAD
+#define ECF8_PF_AHEAD 32  // tiles between a claim and the group it prefetches (a multiple of ECF8_PF_GROUP)
 #endif  // write-back chunks per lane and loop step
 
 // Output to global memory (d.out).  Launched with programmatic stream
@@ -168,9 +180,15 @@ __device__ __forceinline__ TiledOut tiled_out(const TensorDesc& d, std::uint64_t
 }
 
 // One tile: decode + scan, compact, write back.
-template <bool WIDE, bool TILED = false, class WSm>
+template <bool WIDE, bool TILED = false, bool DIRECT = false, class WSm>
 __device__ __forceinline__ void warp_tile(const TensorDesc& d, const WarpIn& in, std::uint32_t log2T,
                                           std::uint32_t len_off, WSm& ws, int lane) {
+  if constexpr (DIRECT) {
+    direct_tile<kWbUnroll, kLaneWin, true>(
+        d, in, ws, lane, [&] { return GlobalOut{d.out + ((in.A & ~std::uint64_t{15}) - d.out_offset)}; },
+        tile_verified(d, in, log2T));
+    return;
+  } else {
 
   // slots interleaved word by word (word j of lane L at slot[32 j + L]): the
   // lanes' slot stores and reads hit 32 different banks
@@ -200,11 +218,12 @@ __device__ __forceinline__ void warp_tile(const TensorDesc& d, const WarpIn& in,
   }
   GlobalOut out{d.out + ((in.A & ~std::uint64_t{15}) - d.out_offset)};
   compact_write<kWbUnroll>(d, in.A, in.E, run, ws, lane, out);
+  }
 }
 
-template <int NW, bool WIDE, bool TILED = false>
+template <int NW, bool WIDE, bool TILED = false, bool DIRECT = false>
 __global__ void __launch_bounds__(NW * 32, 1) decode_warp_kernel(const LaunchArgs args) {
-  using WarpSmem = WarpSmemT<WIDE>;
+  using WarpSmem = KernelWarpSmem<WIDE, DIRECT>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   WarpSmem& ws = reinterpret_cast<WarpSmem*>(smem_raw)[warp];
@@ -303,24 +322,46 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_warp_kernel(const LaunchArg
         next = next2;
       }
 #else
+#if ECF8_PF_GROUP > 1
+      // The sections go to L2 in groups of G consecutive tiles, kPfAhead
+      // tiles ahead of the claims: the claim of tile c prefetches group
+      // [c + kPfAhead, c + kPfAhead + G) when that starts a group; the warps
+      // prefetch the groups before the first claim between them.
+      constexpr std::uint32_t G = ECF8_PF_GROUP, kPfAhead = ECF8_PF_AHEAD;
+      const std::uint64_t n_rel = seg_end - seg;
+      constexpr std::uint32_t kInit = (NW + kPfAhead + G - 1) / G;  // groups before the first claim's
+      for (std::uint32_t g = warp; g < kInit && g * G < n_rel; g += NW)
+        if (lane < 5) prefetch_tile_l2(d, seg + g * G, log2T, lane, static_cast<std::uint32_t>(min(std::uint64_t{G}, n_rel - g * G)));
+#else
       if (tile < seg_end && lane < 5) prefetch_tile_l2(d, tile, log2T, lane);
+#endif
       while (tile < seg_end) {
         WarpIn cur;
         load_warp_tile<kLaneWin, true>(d, tile, log2T, lane, cur);
 #if ECF8_STATIC_TILES  // A/B: round-robin tiles (no shared atomic)
         const std::uint64_t next = tile + NW;
+        const unsigned claim = static_cast<unsigned>(next - seg);
 #else
         unsigned claim = 0;
         if (lane == 0) claim = atomicAdd(&next_tile, 1u);
-        const std::uint64_t next = seg + __shfl_sync(0xffffffffu, claim, 0);
+        claim = __shfl_sync(0xffffffffu, claim, 0);
+        const std::uint64_t next = seg + claim;
 #endif
+#if ECF8_PF_GROUP > 1
+        {
+          const std::uint64_t pf = std::uint64_t{claim} + kPfAhead;
+          if (pf % G == 0 && pf < n_rel && lane < 5)
+            prefetch_tile_l2(d, seg + pf, log2T, lane, static_cast<std::uint32_t>(min(std::uint64_t{G}, n_rel - pf)));
+        }
+#else
         if (next < seg_end && lane < 5) prefetch_tile_l2(d, next, log2T, lane);
+#endif
         if (lane == 0) {  // this tile's sign/mantissa bytes -> L2 (direct tiles read them at write-back)
           const std::uint64_t p0 = (cur.A >> 1) & ~std::uint64_t{15};
           const std::uint32_t bytes = static_cast<std::uint32_t>((((cur.E + 1) >> 1) - p0 + 15) & ~std::uint64_t{15});
           if (bytes) prefetch_l2(d.packed + p0, bytes);
         }
-        warp_tile<WIDE, TILED>(d, cur, log2T, len_off, ws, lane);
+        warp_tile<WIDE, TILED, DIRECT>(d, cur, log2T, len_off, ws, lane);
         tile = next;
       }
 #endif
@@ -400,21 +441,25 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_fsm64_kernel(const LaunchAr
   }
 }
 
+#ifndef ECF8_DIRECT_WARPS
+#define ECF8_DIRECT_WARPS 24
+#endif
+
 #ifndef ECF8_FSM64_WARPS
 #define ECF8_FSM64_WARPS 22  // 22 x 8.2 KB of staging + the 32 KB table
 #endif
 
-template <int NW, bool WIDE = false, bool TILED = false>
+template <int NW, bool WIDE = false, bool TILED = false, bool DIRECT = false>
 cudaError_t launch_nw(const LaunchArgs& args, cudaStream_t s) {
   static int grid_cap = 0;
-  const int smem = static_cast<int>(sizeof(WarpSmemT<WIDE>)) * NW;
+  const int smem = static_cast<int>(sizeof(KernelWarpSmem<WIDE, DIRECT>)) * NW;
   if (grid_cap == 0) {
-    cudaError_t e = cudaFuncSetAttribute(decode_warp_kernel<NW, WIDE, TILED>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = cudaFuncSetAttribute(decode_warp_kernel<NW, WIDE, TILED, DIRECT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_warp_kernel<NW, WIDE, TILED>, NW * 32, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_warp_kernel<NW, WIDE, TILED, DIRECT>, NW * 32, smem);
     if (e != cudaSuccess) return e;
     grid_cap = sms * (per_sm > 0 ? per_sm : 1);
   }
@@ -434,7 +479,7 @@ cudaError_t launch_nw(const LaunchArgs& args, cudaStream_t s) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, decode_warp_kernel<NW, WIDE, TILED>, args);
+  return cudaLaunchKernelEx(&cfg, decode_warp_kernel<NW, WIDE, TILED, DIRECT>, args);
 }
 
 // One CTA iteration per 256-window tile, one thread per window: the
@@ -532,6 +577,13 @@ cudaError_t launch_decode_warp(const LaunchArgs& args, cudaStream_t s) {
   }();
   if (!args.descs && args.inline_desc.out_tiled_k) return launch_nw<24, false, true>(args, s);  // rows of a fused weight
   return nw == 20 ? launch_nw<20>(args, s) : nw == 22 ? launch_nw<22>(args, s) : launch_nw<24>(args, s);
+}
+
+// Variant 7 (every tile direct): the staging tile alone per warp.  A/B
+// (70B layers): 24-28 warps the same, +1.5-2 % over variant 4; 30 warps -3 %.
+cudaError_t launch_decode_warp_direct(const LaunchArgs& args, cudaStream_t s) {
+  if (!args.descs && args.inline_desc.out_tiled_k) return launch_nw<24, false, true>(args, s);  // rows of a fused weight
+  return launch_nw<ECF8_DIRECT_WARPS, false, false, true>(args, s);
 }
 
 // Variant 5 (1-bit codes): 12 warps x 16.5 KB of warp state.

@@ -128,10 +128,11 @@ __device__ __forceinline__ void prefetch_l2(const void* p, std::uint64_t bytes) 
 }
 // Lanes 0-4 issue one section each (the descriptor reads and the address
 // math run side by side instead of one after another).
+// ntiles consecutive tiles at once: their sections are contiguous.
 __device__ __forceinline__ void prefetch_tile_l2(const TensorDesc& d, std::uint64_t tile, std::uint32_t log2T,
-                                                 int lane) {
-  const std::uint32_t m = 256u >> log2T;
-  const std::uint64_t b0 = d.blk_begin + (tile - d.tile_begin) * m;
+                                                 int lane, std::uint32_t ntiles = 1) {
+  const std::uint32_t m1 = 256u >> log2T, m = m1 * ntiles;
+  const std::uint64_t b0 = d.blk_begin + (tile - d.tile_begin) * m1;
   const std::uint64_t nb = d.blk_end - b0 < m ? d.blk_end - b0 : m;
   const std::uint64_t w0 = b0 << log2T, nw = nb << log2T;
   // branch-free: lane i picks section i (0 windows, 1 gaps, 2 block offsets,

@@ -669,13 +669,17 @@ __shared__ std::uint32_t g2_loaded;
 __shared__ unsigned g2_qnext;
 
 struct GRingOut {
-  std::uint8_t *cf, *cl;         // address of chunk 0 if it were in K tile tf / tf + 1 (chunk c at + 16 c)
-  std::uint64_t S0;              // element of chunk 0
-  std::uint32_t c_lo, c_hi;      // chunks inside the CTA range (e0, e1 are multiples of 16384)
-  std::uint32_t c_split;         // first chunk of K tile tf + 1
+  // element g of the CTA's K tile t sits in ring slot t % R at g - e0 - 16384 t,
+  // i.e. at ring + ((g - e0) mod 16384 R): R is a power of two and e0 a
+  // multiple of 16384
+  std::uint8_t* ring;
+  std::uint32_t s0r;             // (S0 - e0) mod 2^32, S0 = element of chunk 0
+  std::uint32_t c_lo, c_n;       // chunks [c_lo, c_lo + c_n) are inside the CTA range
   std::uint32_t tf, bf, bl, bar_f, bar_l;
   const Flush* fl;
   int lane;
+  static constexpr std::uint32_t kMask = kRingSlots * kTileElems - 1;
+  static_assert((kRingSlots & (kRingSlots - 1)) == 0, "ring slots: a power of two");
   __device__ __forceinline__ void wait_slot(std::uint32_t t) const {
     if (t < kRingSlots) return;
     const std::uint32_t need = t - kRingSlots + 1, addr = smem_addr(&g2_loaded);
@@ -692,14 +696,13 @@ struct GRingOut {
     if (bl) wait_slot(tf + 1);
   }
   __device__ __forceinline__ void chunk(std::uint32_t c, const uint4& r) const {
-    if (c < c_lo || c >= c_hi) return;
-    std::uint8_t* p = (c < c_split ? cf : cl) + 16 * static_cast<std::uint64_t>(c);
+    if (c - c_lo >= c_n) return;
+    std::uint8_t* p = ring + ((s0r + 16 * c) & kMask);
     asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(r.x), "r"(r.y), "r"(r.z), "r"(r.w) : "memory");
   }
   __device__ __forceinline__ void byte(std::uint32_t i, std::uint8_t b) const {
-    const std::uint32_t c = i >> 4;
-    if (c < c_lo || c >= c_hi) return;
-    *((c < c_split ? cf : cl) + i) = b;
+    if ((i >> 4) - c_lo >= c_n) return;
+    ring[(s0r + i) & kMask] = b;
   }
   __device__ __forceinline__ void done() const {
     // the generic-proxy stores must be visible to the loader's bulk copies
@@ -795,20 +798,17 @@ __global__ void __launch_bounds__((kL2DecodeWarps + 2) * 32, 1) fused_l2_kernel(
             d, cur, ws, lane,
             [&] {
               GRingOut o;
-              o.S0 = cur.A & ~std::uint64_t{15};
+              const std::uint64_t S0 = cur.A & ~std::uint64_t{15};
               o.tf = static_cast<std::uint32_t>((A - cta.e0) >> 14);
               const std::uint32_t tl = static_cast<std::uint32_t>((E - 1 - cta.e0) >> 14);
               const std::uint64_t bnd = cta.e0 + (static_cast<std::uint64_t>(o.tf + 1) << 14);
               o.bf = static_cast<std::uint32_t>((E < bnd ? E : bnd) - A);
               o.bl = tl != o.tf ? static_cast<std::uint32_t>(E - bnd) : 0u;
-              // element g of K tile t is at ring slot (t % R) + (g - e0 - 16384 t)
-              const std::int64_t s_rel = static_cast<std::int64_t>(o.S0) - static_cast<std::int64_t>(cta.e0);
-              o.cf = ring + static_cast<std::int64_t>(o.tf % kRingSlots) * kTileElems - (static_cast<std::int64_t>(o.tf) << 14) + s_rel;
-              o.cl = ring + static_cast<std::int64_t>((o.tf + 1) % kRingSlots) * kTileElems -
-                     (static_cast<std::int64_t>(o.tf + 1) << 14) + s_rel;
+              const std::int64_t s_rel = static_cast<std::int64_t>(S0) - static_cast<std::int64_t>(cta.e0);
+              o.ring = ring;
+              o.s0r = static_cast<std::uint32_t>(s_rel);
               o.c_lo = s_rel >= 0 ? 0u : static_cast<std::uint32_t>((-s_rel) >> 4);
-              o.c_hi = static_cast<std::uint32_t>((static_cast<std::int64_t>(cta.e1) - static_cast<std::int64_t>(o.S0)) >> 4);
-              o.c_split = static_cast<std::uint32_t>((static_cast<std::int64_t>(bnd) - static_cast<std::int64_t>(o.S0)) >> 4);
+              o.c_n = static_cast<std::uint32_t>((static_cast<std::int64_t>(cta.e1) - static_cast<std::int64_t>(S0)) >> 4) - o.c_lo;
               o.bar_f = smem_addr(&g2_full[o.tf % kRingSlots]);
               o.bar_l = smem_addr(&g2_full[(o.tf + 1) % kRingSlots]);
               o.fl = &fl;

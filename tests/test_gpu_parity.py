@@ -219,7 +219,8 @@ def test_device_path_continuous_walk(orc, n, T, seed):
     x = codec.synth(1.8, 0.05, n, seed)
     t = codec.encode_tensor(x, T)
     d = DeviceTensor(t)
-    assert d.kernel_variant == 4
+    # every tile places its lanes directly: the direct-only variant 7
+    assert d.kernel_variant == 7
     ok, total = d.verified_tiles()
     assert total == -(-(len(t.outpos) - 1) * T // 256)
     # every tile but possibly the last: windows of the zero padding after the
@@ -287,7 +288,9 @@ def test_block_decoding_past_its_range_is_clamped(orc, T):
     defined = np.ones(t.n_elem, bool)
     defined[op[b + 2] - 1] = False
     assert not np.array_equal(want[defined], x[defined])
-    got = DeviceTensor(t).decode().cpu().numpy()
+    dev = DeviceTensor(t)
+    assert dev.kernel_variant == 4  # a tile off the direct path: the kernel with the fallback
+    got = dev.decode().cpu().numpy()
     assert np.array_equal(got[defined], want[defined])
     assert np.array_equal(codec.decode_parallel(t)[defined], want[defined])
 
@@ -383,7 +386,7 @@ def test_one_bit_code_with_corrupt_gaps_keeps_variant_5(orc):
     assert np.array_equal(got[defined], want[defined])
 
 
-def test_batch_mixes_variants_4_and_6(orc):
+def test_batch_mixes_variants_6_and_7(orc):
     import torch
 
     from paper_2510_02676_b200.device import Batch, DeviceTensor
@@ -391,7 +394,7 @@ def test_batch_mixes_variants_4_and_6(orc):
     xs = [codec.synth(1.8, 0.05, 1_000_003, 81, fmt="e5m2"), codec.synth(1.8, 0.05, 2_000_000, 82),
           codec.synth(1.8, 0.05, 70_000, 83, fmt="e5m2")]
     ds = [DeviceTensor(codec.encode_tensor(x, 256)) for x in xs]
-    assert sorted(d.kernel_variant for d in ds) == [4, 6, 6]
+    assert sorted(d.kernel_variant for d in ds) == [6, 6, 7]
     outs = [torch.empty(x.size, dtype=torch.uint8, device="cuda") for x in xs]
     b = Batch(ds, outs)
     for _ in range(2):
@@ -399,3 +402,34 @@ def test_batch_mixes_variants_4_and_6(orc):
         torch.cuda.synchronize()
         for o, x in zip(outs, xs):
             assert np.array_equal(o.cpu().numpy(), x)
+
+
+@pytest.mark.gpu
+def test_batch_mixes_variants_4_and_7(orc):
+    # one tensor with a tile off the direct path (a block boundary moved down
+    # by one symbol, as in test_block_decoding_past_its_range_is_clamped)
+    # between two encoder outputs: one launch per variant, every output exact
+    import torch
+
+    from paper_2510_02676_b200.device import Batch, DeviceTensor
+
+    xs = [codec.synth(1.8, 0.05, 1_500_000, 91 + i) for i in range(3)]
+    ts = [codec.encode_tensor(x, 256) for x in xs]
+    t1 = ts[1].copy()
+    op = t1.outpos
+    b = (len(op) - 1) // 2
+    op[b + 1] -= 1
+    ts[1] = t1
+    want1 = orc.decode_parallel(tensor_dict(t1))
+    defined = np.ones(t1.n_elem, bool)
+    defined[op[b + 2] - 1] = False
+    ds = [DeviceTensor(t) for t in ts]
+    assert [d.kernel_variant for d in ds] == [7, 4, 7]
+    outs = [torch.empty(x.size, dtype=torch.uint8, device="cuda") for x in xs]
+    bt = Batch(ds, outs)
+    for _ in range(2):
+        bt.decode()
+        torch.cuda.synchronize()
+        assert np.array_equal(outs[0].cpu().numpy(), xs[0])
+        assert np.array_equal(outs[1].cpu().numpy()[defined], want1[defined])
+        assert np.array_equal(outs[2].cpu().numpy(), xs[2])
