@@ -668,6 +668,14 @@ __shared__ alignas(8) unsigned long long g2_empty[kL2MaxStages];
 __shared__ std::uint32_t g2_loaded;
 __shared__ unsigned g2_qnext;
 
+#ifndef ECF8_L2_PROBE
+#define ECF8_L2_PROBE 0  // timing experiments only (wrong results): 1 no MMAs, 2 no ring stores
+#endif
+
+#ifndef ECF8_SLOT_SLEEP
+#define ECF8_SLOT_SLEEP 64  // ns between a waiting ring writer's polls
+#endif
+
 struct GRingOut {
   // element g of the CTA's K tile t sits in ring slot t % R at g - e0 - 16384 t,
   // i.e. at ring + ((g - e0) mod 16384 R): R is a power of two and e0 a
@@ -675,7 +683,7 @@ struct GRingOut {
   std::uint8_t* ring;
   std::uint32_t s0r;             // (S0 - e0) mod 2^32, S0 = element of chunk 0
   std::uint32_t c_lo, c_n;       // chunks [c_lo, c_lo + c_n) are inside the CTA range
-  std::uint32_t tf, bf, bl, bar_f, bar_l;
+  std::uint32_t tf, bf, bl, bar_f, bar_l;  // first K tile of the write-back, bytes in tf / tf + 1, their full barriers
   const Flush* fl;
   int lane;
   static constexpr std::uint32_t kMask = kRingSlots * kTileElems - 1;
@@ -688,7 +696,7 @@ struct GRingOut {
       asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
       if (__all_sync(0xffffffffu, v >= need)) return;
       (*fl)();
-      __nanosleep(64);
+      __nanosleep(ECF8_SLOT_SLEEP);
     }
   }
   __device__ __forceinline__ void wait() const {
@@ -696,7 +704,7 @@ struct GRingOut {
     if (bl) wait_slot(tf + 1);
   }
   __device__ __forceinline__ void chunk(std::uint32_t c, const uint4& r) const {
-    if (c - c_lo >= c_n) return;
+    if (c - c_lo >= c_n || ECF8_L2_PROBE == 2) return;  // probe 2: no ring stores (timing only)
     std::uint8_t* p = ring + ((s0r + 16 * c) & kMask);
     asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(r.x), "r"(r.y), "r"(r.z), "r"(r.w) : "memory");
   }
@@ -704,6 +712,8 @@ struct GRingOut {
     if ((i >> 4) - c_lo >= c_n) return;
     ring[(s0r + i) & kMask] = b;
   }
+  // (A/B: deferring the fence and arrivals to after the warp's next decode
+  // phase made a 70B layer 4 % slower)
   __device__ __forceinline__ void done() const {
     // the generic-proxy stores must be visible to the loader's bulk copies
     asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -794,25 +804,28 @@ __global__ void __launch_bounds__((kL2DecodeWarps + 2) * 32, 1) fused_l2_kernel(
       }
       const std::uint64_t A = cur.A > cta.e0 ? cur.A : cta.e0, E = cur.E < cta.e1 ? cur.E : cta.e1;
       if (A < E) {
+        const std::uint32_t tf = static_cast<std::uint32_t>((A - cta.e0) >> 14);
+        const std::uint32_t tl = static_cast<std::uint32_t>((E - 1 - cta.e0) >> 14);
+        const std::uint64_t bnd = cta.e0 + (static_cast<std::uint64_t>(tf + 1) << 14);
+        const std::uint32_t bf = static_cast<std::uint32_t>((E < bnd ? E : bnd) - A);
+        const std::uint32_t bl = tl != tf ? static_cast<std::uint32_t>(E - bnd) : 0u;
         direct_tile<4, 8, true>(
             d, cur, ws, lane,
             [&] {
               GRingOut o;
               const std::uint64_t S0 = cur.A & ~std::uint64_t{15};
-              o.tf = static_cast<std::uint32_t>((A - cta.e0) >> 14);
-              const std::uint32_t tl = static_cast<std::uint32_t>((E - 1 - cta.e0) >> 14);
-              const std::uint64_t bnd = cta.e0 + (static_cast<std::uint64_t>(o.tf + 1) << 14);
-              o.bf = static_cast<std::uint32_t>((E < bnd ? E : bnd) - A);
-              o.bl = tl != o.tf ? static_cast<std::uint32_t>(E - bnd) : 0u;
               const std::int64_t s_rel = static_cast<std::int64_t>(S0) - static_cast<std::int64_t>(cta.e0);
+              o.tf = tf;
+              o.bf = bf;
+              o.bl = bl;
+              o.bar_f = smem_addr(&g2_full[tf % kRingSlots]);
+              o.bar_l = smem_addr(&g2_full[(tf + 1) % kRingSlots]);
+              o.lane = lane;
               o.ring = ring;
               o.s0r = static_cast<std::uint32_t>(s_rel);
               o.c_lo = s_rel >= 0 ? 0u : static_cast<std::uint32_t>((-s_rel) >> 4);
               o.c_n = static_cast<std::uint32_t>((static_cast<std::int64_t>(cta.e1) - static_cast<std::int64_t>(S0)) >> 4) - o.c_lo;
-              o.bar_f = smem_addr(&g2_full[o.tf % kRingSlots]);
-              o.bar_l = smem_addr(&g2_full[(o.tf + 1) % kRingSlots]);
               o.fl = &fl;
-              o.lane = lane;
               return o;
             },
             tile_verified(d, cur, log2T), ft);
@@ -862,7 +875,7 @@ __global__ void __launch_bounds__((kL2DecodeWarps + 2) * 32, 1) fused_l2_kernel(
         asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_addr(&g2_loaded)), "r"(t + 1) : "memory");
         const std::uint32_t a_st = a_base + s * kTileElems, bdst = b_base + s * b_bytes;
 #pragma unroll
-        for (std::uint32_t k = 0; k < 4; ++k)
+        for (std::uint32_t k = 0; k < (ECF8_L2_PROBE == 1 ? 0u : 4u); ++k)
           mma_f8(tmem_d + buf * args.acc_cols, smem_desc(a_st + 32 * k), smem_desc(bdst + 32 * k), idesc,
                  !(first_of_seg && k == 0));
         tc_commit(smem_addr(&g2_empty[s]));
