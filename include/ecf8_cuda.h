@@ -95,6 +95,10 @@ int ecf8_decode_host_stream(const ecf8_sections *const *host, int count, uint8_t
  * ECF8_OK also when the memory was already registered. */
 int ecf8_host_pin(void *p, uint64_t bytes);
 int ecf8_host_unpin(void *p);
+/* Page-locked host allocation (cudaMallocHost) / its release: the
+ * process-lifetime buffer decompress_streaming streams through. */
+int ecf8_host_alloc_pinned(uint64_t bytes, void **out);
+int ecf8_host_free_pinned(void *p);
 
 /* Replaces ecf8::decode_block (codec.cpp:201-254): decodes block `block`
  * into out[outpos[block], outpos[block+1]). out_len must be n_elem. */

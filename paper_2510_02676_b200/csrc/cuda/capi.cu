@@ -1433,6 +1433,28 @@ int ecf8_host_pin(void* p, uint64_t bytes) {
   });
 }
 
+int ecf8_host_alloc_pinned(uint64_t bytes, void** out) {
+  return guarded([&]() -> int {
+    if (!out) return fail(ECF8_EINVAL, "null argument");
+    *out = nullptr;
+    if (!bytes) return ECF8_OK;
+    if (int rc = require_device()) return rc;
+    if (cudaMallocHost(out, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      *out = nullptr;
+      return fail(ECF8_ENOMEM, "cudaMallocHost failed");
+    }
+    return ECF8_OK;
+  });
+}
+
+int ecf8_host_free_pinned(void* p) {
+  return guarded([&]() -> int {
+    if (p) cu(cudaFreeHost(p), "cudaFreeHost");
+    return ECF8_OK;
+  });
+}
+
 int ecf8_host_unpin(void* p) {
   return guarded([&]() -> int {
     if (!p) return ECF8_OK;

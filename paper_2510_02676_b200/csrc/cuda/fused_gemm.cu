@@ -275,6 +275,49 @@ struct Flush {
       }
     }
   }
+  // Columns [c_begin, m) step c_step of segment sg's TMEM lane quadrant q.
+  __device__ __forceinline__ void segment_cols(std::uint32_t sg, std::uint32_t q, std::uint32_t c_begin,
+                                               std::uint32_t c_step) const {
+    const int lane = threadIdx.x & 31;
+    const std::uint32_t b = sg % a->acc_bufs;
+    const std::uint64_t col = static_cast<std::uint64_t>(nt0 + sg) * 128 + q * 32 + static_cast<std::uint32_t>(lane);
+    const std::uint32_t tq = tmem_d + b * a->acc_cols + ((q * 32) << 16);
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const std::uint32_t m = a->m;
+    for (std::uint32_t c0 = c_begin; c0 < m; c0 += c_step) {
+      float v[8];
+      tmem_ld8(tq + c0, v);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const std::uint32_t mcol = c0 + j;
+        if (mcol < m) atomicAdd(a->y + static_cast<std::uint64_t>(mcol) * a->n + col, v[j] * a->scale);
+      }
+    }
+  }
+  // After the decode: the segments not flushed yet, by all nw decode warps
+  // (warp w reads TMEM lane quadrant w % 4; the warps of a quadrant split its
+  // columns 8 at a time).  Named barrier 1 over the decode warps: before
+  // (every mid-run flush is done, g_nflush final) and after each segment
+  // (its buffer's columns all read before the quadrant's arrival frees it).
+  __device__ __forceinline__ void run_final(int nw) const {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const std::uint32_t q = static_cast<std::uint32_t>(warp) & 3u, part = static_cast<std::uint32_t>(warp) >> 2;
+    const std::uint32_t parts = (static_cast<std::uint32_t>(nw) - q + 3) / 4;
+    const std::uint32_t nb = a->acc_bufs;
+    asm volatile("bar.sync 1, %0;" ::"r"(nw * 32) : "memory");
+    const std::uint32_t mine = g_nflush[q];
+    const std::uint32_t f0 = min(min(g_nflush[0], g_nflush[1]), min(g_nflush[2], g_nflush[3]));
+    for (std::uint32_t f = f0; f < nseg; ++f) {
+      if (f >= mine) {
+        mbar_wait(smem_addr(&g_segdone[f % nb]), (f / nb) & 1u);
+        tc_fence_after();
+        segment_cols(f, q, 8 * part, 8 * parts);
+        tc_fence_before();
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(nw * 32) : "memory");
+      if (f >= mine && part == 0 && lane == 0) mbar_arrive(smem_addr(&g_accfree[f % nb]), 1);
+    }
+  }
   // Flush every finished segment (block: wait for each until all are done).
   __device__ __forceinline__ void run(bool block) const {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -672,6 +715,10 @@ __shared__ unsigned g2_qnext;
 #define ECF8_L2_PROBE 0  // timing experiments only (wrong results): 1 no MMAs, 2 no ring stores
 #endif
 
+#ifndef ECF8_FUSED_FINAL_ALL
+#define ECF8_FUSED_FINAL_ALL 1  // the segments left after the decode: flushed by all decode warps (0: warps 0-3)
+#endif
+
 #ifndef ECF8_SLOT_SLEEP
 #define ECF8_SLOT_SLEEP 64  // ns between a waiting ring writer's polls
 #endif
@@ -833,7 +880,11 @@ __global__ void __launch_bounds__((kL2DecodeWarps + 2) * 32, 1) fused_l2_kernel(
       fl.run(false);  // warps 0-3: flush the segments the MMAs have finished
       tile = next;
     }
+#if ECF8_FUSED_FINAL_ALL
+    fl.run_final(kL2DecodeWarps);  // the last segments, by every decode warp
+#else
     fl.run(true);
+#endif
   } else if (warp == kLoader) {
     // ---- loader: completed K tiles of the ring + their X tiles -> shared-memory stages
     asm volatile("griddepcontrol.wait;" ::: "memory");  // x_tiles_kernel: X tiles written, y zeroed

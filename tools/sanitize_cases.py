@@ -4,14 +4,17 @@ Run on the GPU box as
     compute-sanitizer --tool racecheck --target-processes all python tools/sanitize_cases.py
 Every kernel family of the library is launched at least once on inputs small
 enough for the sanitizers' replay:
-  * decode_warp_kernel<24> (variant 4), <12, WIDE> (variant 5), the group
+  * decode_warp_kernel<24> (variant 4), its direct-only instance (variant 7),
+    <12, WIDE> (variant 5), decode_fsm64_kernel (variant 6), the group
     kernels decode_kernel (T = 1, 2, 512, 1024), verify_gaps_kernel,
     count_window_kernel;
   * a tensor with corrupted gap nibbles (window-by-window walk + exact walk);
   * a batch of tensors of mixed sizes (descriptor search, PDL back-to-back);
-  * the decode-fused GEMM with multi-K-tile CTA runs (A-ring wrap, stage
-    release, TMEM accumulation across K tiles, multi-segment epilogues),
-    m <= 128 and m > 128 (single X stage), E4M3 and E5M2;
+  * the decode-fused GEMM (fused_l2_kernel: decode warps -> per-CTA L2 ring
+    -> loader bulk copies -> tcgen05.mma; fused_gemm_kernel for 1-bit codes)
+    with multi-K-tile CTA runs (ring wrap, stage release, TMEM accumulation
+    across K tiles, multi-segment epilogues), m <= 128 and m > 128, E4M3 and
+    E5M2;
   * the device encoder (histogram, chunk scan, emit);
   * the native E5M2 decoder (e5_decode_kernel, T 8 / 256 / 1024).
 Each output is checked bit-exact against the original bytes (the encoder's
@@ -54,6 +57,19 @@ def decode_cases(scale):
     got = d.decode().cpu().numpy()
     assert np.array_equal(got, codec.decode_parallel(bad))
     print(f"corrupt gaps ok (verified tiles {d.verified_tiles()}); clean decode matches: {np.array_equal(want, x)}")
+    # a block boundary moved by one symbol: a tile off the direct path (variant 4 with its fallback)
+    x = codec.synth(1.8, 0.05, 300_000, 12)
+    mv = codec.encode_tensor(x, 256).copy()
+    op = mv.outpos
+    b = (len(op) - 1) // 2
+    op[b + 1] -= 1
+    d = DeviceTensor(mv)
+    assert d.kernel_variant == 4
+    got = d.decode().cpu().numpy()
+    ok = np.ones(x.size, bool)
+    ok[op[b + 2] - 1] = False
+    assert np.array_equal(got[ok], codec.decode_parallel(mv)[ok])
+    print("moved block boundary ok (variant 4)", flush=True)
     # batch: mixed tensors, one launch per variant, twice back to back
     xs = [codec.synth(1.8, 0.05, n, 20 + i) for i, n in enumerate([100_000, 3, 65_536, 250_000])]
     ds = [DeviceTensor(codec.encode_tensor(x, 256)) for x in xs]
