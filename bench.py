@@ -671,7 +671,7 @@ def run_fused(args, torch, dist, local, rank, world):
         line["roofline"] = {"bound": "hbm", "achieved": top["compressed_gbs"] / world, "peak": peak, "unit": "GB/s",
                             "frac": round(top["compressed_gbs"] / world / peak, 4), "traffic": None,
                             "tensor_tflops": top["tensor_tflops"] / world, "tensor_peak_tflops": fp8_peak,
-                            "kernel": "fused_gemm_kernel<8,33,*,1>"}
+                            "kernel": "fused_l2_kernel (23 decode warps, L2 ring, loader + MMA warps)"}
         line["clocks"] = probe.summary()
         line["gpu_launches"] = launches
         print(json.dumps(line), flush=True)
