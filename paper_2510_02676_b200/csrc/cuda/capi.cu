@@ -229,9 +229,9 @@ void free_arena(ecf8_dev_tensor* t) {
 
 struct ecf8_fused {
   const ecf8_dev_tensor* w = nullptr;
-  // Two CTA plans: [0] for up to 2 n-tile segments per CTA (any m), [1] for
-  // up to 4 (m <= 128: four accumulators fit the 512 TMEM columns), which
-  // lets the big weights run in one wave of the SMs.
+  // CTA plans for m > 128 ([0]) and m <= 128 ([1]): both one wave of the
+  // SMs (the accumulators are reused round-robin, so any segment count per
+  // CTA fits); they differ only under the ECF8_FUSED_SEG_CAP A/B switch.
   ecf8::dev::FusedCta* d_plan[2] = {nullptr, nullptr};
   std::uint32_t n_cta[2] = {0, 0}, max_seg[2] = {0, 0};
   std::uint32_t split_k = 1;
@@ -822,7 +822,7 @@ EncScratch& enc_scratch(std::uint64_t need, cudaStream_t st) {
   cu(cudaStreamWaitEvent(st, e.free_at, 0), "wait");
   if (need > e.cap) {
     if (e.buf) {
-      cu(cudaDeviceSynchronize(), "sync");
+      cu(cudaEventSynchronize(e.free_at), "sync");  // the scratch's last user (any stream), not the whole device
       cudaFree(e.buf);
       e.buf = nullptr;
       e.cap = 0;
