@@ -210,6 +210,9 @@ __device__ __forceinline__ void warp_tile(const TensorDesc& d, const WarpIn& in,
       return;
     }
     if constexpr (TILED) __trap();  // row-major output of tiled weights needs direct tiles (checked by the caller)
+    // the lanes' endgap words (loaded with the tile only where a direct tile
+    // does not need them): `in` is the caller's mutable tile (the byte-step loop)
+    const_cast<WarpIn&>(in).gnext = load_gnext(d, in, lane);
     run = warp_decode_scan<kLaneWin, 128, false, GlobalTables, true>(in, log2T, len_off, GlobalTables{d}, slot, lane,
                                                                      verified);
   } else {  // an incomplete code (no encoder writes one): the reference walk per window, tables through L1
@@ -312,7 +315,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_warp_kernel(const LaunchArg
       if (next < n_rel && lane < 5) prefetch_tile_l2(d, seg + next, log2T, lane);
       while (tile < seg_end) {
         WarpIn cur;
-        load_warp_tile<kLaneWin, true>(d, tile, log2T, lane, cur);
+        load_warp_tile<kLaneWin, true, false, !DIRECT>(d, tile, log2T, lane, cur);
         unsigned claim2 = 0;
         if (lane == 0 && next < n_rel) claim2 = atomicAdd(&next_tile, 1u);
         warp_tile<WIDE>(d, cur, log2T, len_off, ws, lane);
@@ -337,7 +340,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_warp_kernel(const LaunchArg
 #endif
       while (tile < seg_end) {
         WarpIn cur;
-        load_warp_tile<kLaneWin, true>(d, tile, log2T, lane, cur);
+        load_warp_tile<kLaneWin, true, false, !DIRECT>(d, tile, log2T, lane, cur);
 #if ECF8_STATIC_TILES  // A/B: round-robin tiles (no shared atomic)
         const std::uint64_t next = tile + NW;
         const unsigned claim = static_cast<unsigned>(next - seg);
@@ -423,7 +426,7 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_fsm64_kernel(const LaunchAr
     if (tile < seg_end && lane < 5) prefetch_tile_l2(d, tile, log2T, lane);
     while (tile < seg_end) {
       WarpIn cur;
-      load_warp_tile<kLaneWin, true>(d, tile, log2T, lane, cur);
+      load_warp_tile<kLaneWin, true, false, false>(d, tile, log2T, lane, cur);
       unsigned claim = 0;
       if (lane == 0) claim = atomicAdd(&g6_next_tile, 1u);
       const std::uint64_t next = seg + __shfl_sync(0xffffffffu, claim, 0);

@@ -52,9 +52,10 @@ using WarpIn = WarpInT<kLaneWin>;
 
 // A tile's inputs in two halves: the window words and gaps (issued early,
 // they fly while the previous tile is written back), and the block offsets.
-template <int LW, bool NEXT = false>
+template <int LW, bool NEXT = false, bool GNEXT = true>
 __device__ __forceinline__ void load_tile_words(const TensorDesc& d, std::uint64_t tile, std::uint32_t log2T,
                                                 int lane, WarpInT<LW>& in) {
+  constexpr bool kGnext = NEXT && GNEXT;
   const std::uint32_t m = (32u * LW) >> log2T;  // blocks per tile
   in.b0 = d.blk_begin + (tile - d.tile_begin) * m;
   in.nblk = static_cast<std::uint32_t>(d.blk_end - in.b0 < m ? d.blk_end - in.b0 : m);
@@ -70,19 +71,19 @@ __device__ __forceinline__ void load_tile_words(const TensorDesc& d, std::uint64
       in.w67 = __ldg(src + 3);
       in.w8 = __ldg(reinterpret_cast<const uint2*>(src + 4));
       in.gaps = __ldg(reinterpret_cast<const std::uint32_t*>(d.gaps + (w0g >> 1)) + lane);
-      if constexpr (NEXT)  // (no byte-step decoder -> no recorded ends)
+      if constexpr (kGnext)  // (no byte-step decoder -> no recorded ends)
         in.gnext = d.endgap ? __ldg(reinterpret_cast<const std::uint32_t*>(d.endgap + (w0g >> 1)) + lane) : 0u;
     } else {
       static_assert(LW == 4, "4 or 8 windows per lane");
       in.w8 = __ldg(reinterpret_cast<const uint2*>(src + 2));
       in.gaps = __ldg(reinterpret_cast<const std::uint16_t*>(d.gaps + (w0g >> 1)) + lane);
-      if constexpr (NEXT)
+      if constexpr (kGnext)
         in.gnext = d.endgap ? __ldg(reinterpret_cast<const std::uint16_t*>(d.endgap + (w0g >> 1)) + lane) : 0u;
     }
   }
 }
 
-template <int LW, bool NEXT = false>
+template <int LW, bool NEXT = false, bool DIR = true>
 __device__ __forceinline__ void load_tile_meta(const TensorDesc& d, std::uint32_t log2T, int lane, WarpInT<LW>& in) {
   const std::uint32_t wl = static_cast<std::uint32_t>(lane) * LW;
   in.A = __ldg(d.outpos + in.b0);
@@ -102,7 +103,7 @@ __device__ __forceinline__ void load_tile_meta(const TensorDesc& d, std::uint32_
     in.ls = in.dir = 0;
     if (d.lane_start && in.nwin) {
       const std::uint64_t w0 = in.b0 << log2T;
-      in.dir = __ldg(d.tile_direct + (w0 >> 13));
+      if constexpr (DIR) in.dir = __ldg(d.tile_direct + (w0 >> 13));
       if (wl < in.nwin) {
         if constexpr (LW == 8) in.ls = __ldg(reinterpret_cast<const std::uint32_t*>(d.lane_start + (w0 >> 2)) + lane);
         else in.ls = __ldg(d.lane_start + (w0 >> 2) + lane);
@@ -111,11 +112,22 @@ __device__ __forceinline__ void load_tile_meta(const TensorDesc& d, std::uint32_
   }
 }
 
-template <int LW, bool NEXT = false>
+// GNEXT: load the lanes' endgap words with the tile (the 8-window direct
+// tiles load them only when a tile is unverified: load_gnext); DIR: the
+// tile's tile_direct word (not needed where every tile is direct).
+template <int LW, bool NEXT = false, bool GNEXT = true, bool DIR = true>
 __device__ __forceinline__ void load_warp_tile(const TensorDesc& d, std::uint64_t tile, std::uint32_t log2T,
                                                int lane, WarpInT<LW>& in) {
-  load_tile_words<LW, NEXT>(d, tile, log2T, lane, in);
-  load_tile_meta<LW, NEXT>(d, log2T, lane, in);
+  load_tile_words<LW, NEXT, GNEXT>(d, tile, log2T, lane, in);
+  load_tile_meta<LW, NEXT, DIR>(d, log2T, lane, in);
+}
+
+// The lane's endgap word of an 8-window tile, on demand.
+__device__ __forceinline__ std::uint32_t load_gnext(const TensorDesc& d, const WarpInT<8>& in, int lane) {
+  const std::uint32_t log2T = 31 - __clz(d.T);
+  const std::uint64_t w0g = in.b0 << log2T;
+  if (!d.endgap || static_cast<std::uint32_t>(lane) * 8 >= in.nwin) return 0u;
+  return __ldg(reinterpret_cast<const std::uint32_t*>(d.endgap + (w0g >> 1)) + lane);
 }
 
 // A warp tile's input sections -> L2 (bulk prefetches, lanes 0-4): its
@@ -527,15 +539,17 @@ __device__ __forceinline__ void direct_tile(const TensorDesc& d, const WarpInT<L
         tb = xb;
         goto stored;
 #else
-        decode_two_fsm<4, 4, FT>(w, (in.gaps >> 4) & 15u, (in.gnext >> 8) & 15u, sa, w + 8, (in.gaps >> 20) & 15u,
-                                 (in.gnext >> 24) & 15u, sb, ft);
+        const std::uint32_t gn = load_gnext(d, in, lane);
+        decode_two_fsm<4, 4, FT>(w, (in.gaps >> 4) & 15u, (gn >> 8) & 15u, sa, w + 8, (in.gaps >> 20) & 15u,
+                                 (gn >> 24) & 15u, sb, ft);
 #endif
       } else {
+        const std::uint32_t gn = load_gnext(d, in, lane);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int sh = 8 * (i >> 1) + ((i & 1) ? 0 : 4);  // window 2j: high nibble of byte j
-          decode_two_fsm<1, 4, FT>(w + 2 * i, (in.gaps >> sh) & 15u, (in.gnext >> sh) & 15u, sa, w + 8 + 2 * i,
-                                   (in.gaps >> (16 + sh)) & 15u, (in.gnext >> (16 + sh)) & 15u, sb, ft);
+          decode_two_fsm<1, 4, FT>(w + 2 * i, (in.gaps >> sh) & 15u, (gn >> sh) & 15u, sa, w + 8 + 2 * i,
+                                   (in.gaps >> (16 + sh)) & 15u, (gn >> (16 + sh)) & 15u, sb, ft);
         }
       }
       tb_addr = sb.addr;

@@ -584,7 +584,7 @@ __global__ void __launch_bounds__((decode_warps<LW, SLOT_ROWS, WIDE, FSM>() + ex
     WSm& ws = wsm[warp];
     WarpInT<LW> nxt;
     std::uint64_t tile = warp;
-    if (tile < n_tiles) load_warp_tile<LW, FSM>(d, tile, log2T, lane, nxt);
+    if (tile < n_tiles) load_warp_tile<LW, FSM, LW == 4, false>(d, tile, log2T, lane, nxt);
     while (tile < n_tiles) {
       const WarpInT<LW> cur = nxt;
       unsigned claim = 0;
@@ -597,7 +597,7 @@ __global__ void __launch_bounds__((decode_warps<LW, SLOT_ROWS, WIDE, FSM>() + ex
           asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(d.packed + p0), "r"(bytes) : "memory");
       }
       const std::uint64_t next = __shfl_sync(0xffffffffu, claim, 0);
-      if (next < n_tiles) load_warp_tile<LW, FSM>(d, next, log2T, lane, nxt);
+      if (next < n_tiles) load_warp_tile<LW, FSM, LW == 4, false>(d, next, log2T, lane, nxt);
       if constexpr (FSM) ring_tile_fsm(d, cur, log2T, ws, R, lane, FsmAt{smem_addr(g_fsmf), smem_addr(g_cmf)});
       else ring_tile(d, cur, log2T, len_off, ws, R, lane);
 #if ECF8_FUSED_MIDFLUSH
@@ -839,7 +839,7 @@ __global__ void __launch_bounds__((kL2DecodeWarps + 2) * 32, 1) fused_l2_kernel(
     if (tile < n_tiles && lane < 5) prefetch_tile_l2(d, tile, log2T, lane);
     while (tile < n_tiles) {
       WarpInT<8> cur;
-      load_warp_tile<8, true>(d, tile, log2T, lane, cur);
+      load_warp_tile<8, true, false, false>(d, tile, log2T, lane, cur);
       unsigned claim = 0;
       if (lane == 0) claim = atomicAdd(&g2_qnext, 1u);
       const std::uint64_t next = __shfl_sync(0xffffffffu, claim, 0);
