@@ -117,8 +117,10 @@ int ecf8_count_window(const uint8_t window10[10], unsigned gap, const uint8_t le
 int ecf8_tensor_upload(const ecf8_sections *host, void *stream, ecf8_dev_tensor **out);
 void ecf8_tensor_free(ecf8_dev_tensor *t);
 uint64_t ecf8_tensor_n_elem(const ecf8_dev_tensor *t);
-/* Decode kernel variant the tensor launches with (decode.cuh ids; 4 = the
- * warp-tile kernel; -1 for an empty tensor). */
+/* Decode kernel variant the tensor launches with (decode.cuh ids: 4 = the
+ * warp-tile kernel, 7 = the same for tensors whose every tile is placed
+ * directly (encoder output), 5 / 6 = codes with a 1-bit word, 0-3 = T
+ * outside [8, 256]; -1 for an empty tensor). */
 int ecf8_tensor_kernel_variant(const ecf8_dev_tensor *t);
 /* Upload-time gap check (verify_gaps_kernel): how many of the tensor's
  * 256-window tiles (*total) have every window ending where the next
