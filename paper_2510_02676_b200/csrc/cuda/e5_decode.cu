@@ -318,6 +318,23 @@ __device__ __forceinline__ void decode_chains(const std::uint32_t (&w)[18], std:
   tails[3] = tb1 & ((eb & 31) ? (1u << (eb & 31)) - 1 : 0u);
 }
 
+// Bytes [lo, hi) (0 <= lo < hi <= 16) of a 16-byte output chunk at a
+// 16-byte aligned dst: whole words as word stores, the rest byte-wise.
+__device__ __forceinline__ void store_partial16(std::uint8_t* dst, const std::uint32_t (&o)[4], std::uint32_t lo,
+                                                std::uint32_t hi) {
+#pragma unroll
+  for (std::uint32_t q = 0; q < 4; ++q) {
+    const std::uint32_t a = 4 * q;
+    if (a >= lo && a + 4 <= hi) {
+      *reinterpret_cast<std::uint32_t*>(dst + a) = o[q];
+    } else if (a + 4 > lo && a < hi) {
+#pragma unroll
+      for (std::uint32_t b = 0; b < 4; ++b)
+        if (a + b >= lo && a + b < hi) dst[a + b] = static_cast<std::uint8_t>(o[q] >> (8 * b));
+    }
+  }
+}
+
 __device__ __forceinline__ std::uint32_t bswap(std::uint32_t x) { return __byte_perm(x, 0, 0x0123); }
 
 // 4 nibbles (bits 4j..4j+3 of x, j < 4) -> 4 bytes
@@ -455,9 +472,8 @@ __global__ void __launch_bounds__(NW * 32, 1) e5_fsm_kernel(const Desc d) {
       if (i0 >= off && i0 + 16 <= data_end) {
         asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(d.out + e), "r"(o[0]), "r"(o[1]), "r"(o[2]),
                      "r"(o[3]));
-      } else {
-        for (std::uint32_t j = 0; j < 16; ++j)
-          if (i0 + j >= off && i0 + j < data_end) d.out[e + j] = static_cast<std::uint8_t>(o[j >> 2] >> (8 * (j & 3)));
+      } else {  // a ragged edge chunk: bytes [lo, hi) of it
+        store_partial16(d.out + e, o, i0 < off ? off - i0 : 0u, min(16u, data_end - i0));
       }
     }
     tile = next;
@@ -640,9 +656,8 @@ __global__ void __launch_bounds__(NW * 32, 1) e5_fsm_bytes_kernel(const Desc d) 
       if (i0 >= off && i0 + 16 <= data_end) {
         asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(d.out + e), "r"(o[0]), "r"(o[1]), "r"(o[2]),
                      "r"(o[3]));
-      } else {
-        for (std::uint32_t j = 0; j < 16; ++j)
-          if (i0 + j >= off && i0 + j < data_end) d.out[e + j] = static_cast<std::uint8_t>(o[j >> 2] >> (8 * (j & 3)));
+      } else {  // a ragged edge chunk: bytes [lo, hi) of it
+        store_partial16(d.out + e, o, i0 < off ? off - i0 : 0u, min(16u, data_end - i0));
       }
     }
     tile = next;
