@@ -235,10 +235,6 @@ struct ecf8_fused {
   ecf8::dev::FusedCta* d_plan[2] = {nullptr, nullptr};
   std::uint32_t n_cta[2] = {0, 0}, max_seg[2] = {0, 0};
   std::uint32_t split_k = 1;
-  std::uint8_t* xt = nullptr;  // swizzled-X workspace (grow-only)
-  std::uint64_t xt_cap = 0;
-  std::uint8_t* scratch = nullptr;  // L2-ring variant: kRingSlots K tiles per CTA
-  std::uint64_t scratch_cap = 0;
   std::uint64_t n = 0, k = 0;
   std::uint32_t w_fmt = 0;
   bool fsm = false;  // byte-step direct decode: the code has a byte-step decoder and every tile is direct
@@ -1327,6 +1323,48 @@ int ecf8_fused_byte_steps(const ecf8_fused* f) { return f && f->fsm ? 1 : 0; }
 
 int ecf8_fused_split_k(const ecf8_fused* f) { return f ? static_cast<int>(f->split_k) : 0; }
 
+// Workspace of the fused GEMM calls on one stream, shared by every weight:
+// the swizzled X tiles (x_tiles_kernel, grow-only) and the L2-ring variant's
+// per-CTA rings (kRingSlots K tiles for each of up to one wave of CTAs,
+// allocated once at full size).  Calls on one stream may share it: the next
+// call's x_tiles_kernel writes X only after griddepcontrol.wait (the previous
+// fused grid complete), and its decode warps write the rings only after the
+// same wait (GRingOut::wait).  Calls on different streams may run at once,
+// so every stream has its own.  Never freed (a process-lifetime cache, like
+// the decode tables); growing X waits for the stream.
+struct FusedWorkspace {
+  std::uint8_t* xt = nullptr;
+  std::uint64_t xt_cap = 0;
+  std::uint8_t* ring = nullptr;
+  std::uint32_t ring_ctas = 0;
+};
+
+FusedWorkspace& fused_workspace(cudaStream_t st, std::uint64_t xt_need) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, FusedWorkspace> all;
+  int dev = 0;
+  cu(cudaGetDevice(&dev), "cudaGetDevice");
+  std::lock_guard<std::mutex> lock(mu);
+  FusedWorkspace& w = all[{dev, st}];
+  if (!w.ring) {
+    int sms = 0;
+    cu(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "attr");
+    cu(cudaMalloc(&w.ring, static_cast<std::uint64_t>(sms) * ecf8::dev::kRingSlots * 16384), "cudaMalloc(fused rings)");
+    w.ring_ctas = static_cast<std::uint32_t>(sms);
+  }
+  if (xt_need > w.xt_cap) {
+    if (w.xt) {
+      cu(cudaStreamSynchronize(st), "sync");  // the stream's earlier calls are done with it
+      cudaFree(w.xt);
+      w.xt = nullptr;
+      w.xt_cap = 0;
+    }
+    cu(cudaMalloc(&w.xt, xt_need), "cudaMalloc(x tiles)");
+    w.xt_cap = xt_need;
+  }
+  return w;
+}
+
 int ecf8_fused_gemm(const ecf8_fused* f, const uint8_t* d_x, uint32_t m, float scale, float* d_y, void* stream) {
   return guarded([&]() -> int {
     if (!f || !d_x || !d_y) return fail(ECF8_EINVAL, "null argument");
@@ -1340,17 +1378,9 @@ int ecf8_fused_gemm(const ecf8_fused* f, const uint8_t* d_x, uint32_t m, float s
     a.plan = f->d_plan[pi];
     a.x = d_x;
     a.y = d_y;
-    auto* mf = const_cast<ecf8_fused*>(f);
     const std::uint64_t xt_need = f->k * ((m + 15) / 16 * 16);
-    if (xt_need > mf->xt_cap) {
-      cu(cudaStreamSynchronize(st), "sync");
-      if (mf->xt) cudaFree(mf->xt);
-      mf->xt = nullptr;
-      mf->xt_cap = 0;
-      cu(cudaMalloc(&mf->xt, xt_need), "cudaMalloc(x tiles)");
-      mf->xt_cap = xt_need;
-    }
-    a.xt = mf->xt;
+    FusedWorkspace& ws = fused_workspace(st, xt_need);
+    a.xt = ws.xt;
     a.m = m;
     a.m_pad = (m + 15) / 16 * 16;
     a.n = static_cast<std::uint32_t>(f->n);
@@ -1367,17 +1397,9 @@ int ecf8_fused_gemm(const ecf8_fused* f, const uint8_t* d_x, uint32_t m, float s
       return !e || std::atoi(e) != 0;
     }();
     a.scratch = nullptr;
-    if (l2 && f->fsm && ecf8::dev::fused_l2_stages(a.m_pad) >= 2) {
-      const std::uint64_t need = static_cast<std::uint64_t>(f->n_cta[pi]) * ecf8::dev::kRingSlots * 16384;
-      if (need > mf->scratch_cap) {
-        cu(cudaStreamSynchronize(st), "sync");
-        if (mf->scratch) cudaFree(mf->scratch);
-        mf->scratch = nullptr;
-        mf->scratch_cap = 0;
-        cu(cudaMalloc(&mf->scratch, need), "cudaMalloc(fused ring)");
-        mf->scratch_cap = need;
-      }
-      a.scratch = mf->scratch;
+    // (plans of more than one wave -- the ECF8_FUSED_MIN_WAVES / SEG_CAP A/B switches -- use the shared-memory ring)
+    if (l2 && f->fsm && ecf8::dev::fused_l2_stages(a.m_pad) >= 2 && f->n_cta[pi] <= ws.ring_ctas) {
+      a.scratch = ws.ring;
       a.stages_a = ecf8::dev::fused_l2_stages(a.m_pad);
       a.stages_b = a.stages_a;
     }
@@ -1401,8 +1423,6 @@ void ecf8_fused_free(ecf8_fused* f) {
   if (!f) return;
   for (auto* p : f->d_plan)
     if (p) cudaFree(p);
-  if (f->xt) cudaFree(f->xt);
-  if (f->scratch) cudaFree(f->scratch);
   delete f;
 }
 

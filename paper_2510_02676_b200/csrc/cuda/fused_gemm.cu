@@ -747,6 +747,9 @@ struct GRingOut {
     }
   }
   __device__ __forceinline__ void wait() const {
+    // the rings are shared by the calls on a stream: write only once the
+    // previous call's grid is complete (x_tiles_kernel waited for it)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     wait_slot(tf);
     if (bl) wait_slot(tf + 1);
   }

@@ -177,3 +177,30 @@ def test_decode_rows_back_to_row_major():
         assert torch.equal(got, w8[r0:r1].view(torch.uint8))
     with pytest.raises(_lib.InvalidArgument, match="whole 128-row tiles"):
         _lib.check(_lib.lib.ecf8_fused_decode_rows(lin.handle, 5, 128, out.data_ptr(), None))
+
+
+def test_back_to_back_calls_share_the_stream_workspace():
+    # Calls on one stream share one workspace (swizzled X, the L2 rings) and
+    # chain by programmatic dependent launch: the same weight twice in a row
+    # and two weights alternating, every call with its own x and y, all
+    # enqueued before one synchronize -- each y within the stated bound.
+    lin_a, w_a = _weight(4096, 8192, "e4m3", 128)
+    lin_b, w_b = _weight(1024, 8192, "e4m3", 128)
+    order = [(lin_a, w_a), (lin_a, w_a), (lin_b, w_b), (lin_a, w_a), (lin_b, w_b), (lin_b, w_b), (lin_a, w_a)]
+    calls = []
+    for i, (lin, w8) in enumerate(order):
+        m = (1, 16, 64, 200)[i % 4]
+        g = torch.Generator(device="cuda").manual_seed(500 + i)
+        x8 = (torch.randn(m, lin.k, device="cuda", generator=g) * 4).to(torch.float8_e4m3fn)
+        y = torch.full((m, lin.n), float("nan"), device="cuda")
+        lin(x8, scale=1.0, out=y)
+        calls.append((x8, w8, y))
+    torch.cuda.synchronize()
+    for x8, w8, y in calls:
+        x64, w64 = x8.double(), w8.double()
+        y64 = x64 @ w64.t()
+        K = x8.shape[1]
+        gamma = K * U / (1 - K * U)
+        bound = (gamma + U) * (x64.abs() @ w64.abs().t()) + 1e-30
+        assert torch.isfinite(y).all()
+        assert ((y.double() - y64).abs() / bound).max().item() <= 1.0
