@@ -1333,13 +1333,14 @@ int ecf8_fused_split_k(const ecf8_fused* f) { return f ? static_cast<int>(f->spl
 // so every stream has its own.  Never freed (a process-lifetime cache, like
 // the decode tables); growing X waits for the stream.
 struct FusedWorkspace {
+  std::mutex mu;  // held by a call from the X growth to its launches (host threads sharing a stream)
   std::uint8_t* xt = nullptr;
   std::uint64_t xt_cap = 0;
   std::uint8_t* ring = nullptr;
   std::uint32_t ring_ctas = 0;
 };
 
-FusedWorkspace& fused_workspace(cudaStream_t st, std::uint64_t xt_need) {
+FusedWorkspace& fused_workspace(cudaStream_t st) {
   static std::mutex mu;
   static std::map<std::pair<int, cudaStream_t>, FusedWorkspace> all;
   int dev = 0;
@@ -1352,17 +1353,20 @@ FusedWorkspace& fused_workspace(cudaStream_t st, std::uint64_t xt_need) {
     cu(cudaMalloc(&w.ring, static_cast<std::uint64_t>(sms) * ecf8::dev::kRingSlots * 16384), "cudaMalloc(fused rings)");
     w.ring_ctas = static_cast<std::uint32_t>(sms);
   }
-  if (xt_need > w.xt_cap) {
-    if (w.xt) {
-      cu(cudaStreamSynchronize(st), "sync");  // the stream's earlier calls are done with it
-      cudaFree(w.xt);
-      w.xt = nullptr;
-      w.xt_cap = 0;
-    }
-    cu(cudaMalloc(&w.xt, xt_need), "cudaMalloc(x tiles)");
-    w.xt_cap = xt_need;
-  }
   return w;
+}
+
+// (caller holds w.mu)
+void grow_x_tiles(FusedWorkspace& w, std::uint64_t need, cudaStream_t st) {
+  if (need <= w.xt_cap) return;
+  if (w.xt) {
+    cu(cudaStreamSynchronize(st), "sync");  // the stream's earlier calls are done with it
+    cudaFree(w.xt);
+    w.xt = nullptr;
+    w.xt_cap = 0;
+  }
+  cu(cudaMalloc(&w.xt, need), "cudaMalloc(x tiles)");
+  w.xt_cap = need;
 }
 
 int ecf8_fused_gemm(const ecf8_fused* f, const uint8_t* d_x, uint32_t m, float scale, float* d_y, void* stream) {
@@ -1378,8 +1382,9 @@ int ecf8_fused_gemm(const ecf8_fused* f, const uint8_t* d_x, uint32_t m, float s
     a.plan = f->d_plan[pi];
     a.x = d_x;
     a.y = d_y;
-    const std::uint64_t xt_need = f->k * ((m + 15) / 16 * 16);
-    FusedWorkspace& ws = fused_workspace(st, xt_need);
+    FusedWorkspace& ws = fused_workspace(st);
+    std::lock_guard<std::mutex> ws_lock(ws.mu);
+    grow_x_tiles(ws, f->k * ((m + 15) / 16 * 16), st);
     a.xt = ws.xt;
     a.m = m;
     a.m_pad = (m + 15) / 16 * 16;
