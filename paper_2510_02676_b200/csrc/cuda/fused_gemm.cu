@@ -110,7 +110,7 @@ __shared__ alignas(8) unsigned long long g_free[kMaxStagesA];   // arrived by th
 __shared__ alignas(8) unsigned long long g_bfull[2];
 __shared__ alignas(8) unsigned long long g_segdone[kMaxAccBufs];  // arrived by tcgen05.commit after a segment's last MMA
 __shared__ alignas(8) unsigned long long g_accfree[kMaxAccBufs];  // arrived by the 4 flushing warps once they read it
-__shared__ std::uint32_t g_nflush[4];  // per flushing warp: the next segment it flushes
+__shared__ std::uint32_t g_nflush[16];  // per flushing warp: the next segment it flushes
 __shared__ std::uint32_t g_tmem;
 __shared__ std::uint32_t g_consumed;  // K tiles whose MMAs have completed (stage reusable)
 
@@ -252,6 +252,8 @@ struct Ring {
 struct Flush {
   const FusedArgs* a;  // the kernel's parameters (__grid_constant__: read in place)
   std::uint32_t tmem_d, nt0, nseg;
+  std::uint32_t nfw = 4;  // mid-run flushing warps 0 .. nfw-1 (4, 8, 12, 16): warp w flushes quadrant w % 4, column
+                          // groups w / 4, w / 4 + nfw / 4, ...; g_accfree counts nfw arrivals
 
   __device__ __forceinline__ void segment(std::uint32_t sg) const {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -303,25 +305,34 @@ struct Flush {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const std::uint32_t q = static_cast<std::uint32_t>(warp) & 3u, part = static_cast<std::uint32_t>(warp) >> 2;
     const std::uint32_t parts = (static_cast<std::uint32_t>(nw) - q + 3) / 4;
-    const std::uint32_t nb = a->acc_bufs;
+    const std::uint32_t nb = a->acc_bufs, nh = nfw / 4;
     asm volatile("bar.sync 1, %0;" ::"r"(nw * 32) : "memory");
-    const std::uint32_t mine = g_nflush[q];
-    const std::uint32_t f0 = min(min(g_nflush[0], g_nflush[1]), min(g_nflush[2], g_nflush[3]));
+    std::uint32_t f0 = g_nflush[0];
+    for (std::uint32_t w = 1; w < nfw; ++w) f0 = min(f0, g_nflush[w]);
     for (std::uint32_t f = f0; f < nseg; ++f) {
-      if (f >= mine) {
-        mbar_wait(smem_addr(&g_segdone[f % nb]), (f / nb) & 1u);
-        tc_fence_after();
-        segment_cols(f, q, 8 * part, 8 * parts);
-        tc_fence_before();
+      // the column groups of quadrant q whose mid-run flusher has not done f,
+      // split over the quadrant's warps
+      bool waited = false;
+      for (std::uint32_t h = 0; h < nh; ++h) {
+        if (f < g_nflush[q + 4 * h]) continue;
+        if (!waited) {
+          mbar_wait(smem_addr(&g_segdone[f % nb]), (f / nb) & 1u);
+          tc_fence_after();
+          waited = true;
+        }
+        segment_cols(f, q, 8 * h + 8 * nh * part, 8 * nh * parts);
       }
+      if (waited) tc_fence_before();
       asm volatile("bar.sync 1, %0;" ::"r"(nw * 32) : "memory");
-      if (f >= mine && part == 0 && lane == 0) mbar_arrive(smem_addr(&g_accfree[f % nb]), 1);
+      if (static_cast<std::uint32_t>(warp) < nfw && f >= g_nflush[warp] && lane == 0)
+        mbar_arrive(smem_addr(&g_accfree[f % nb]), 1);
     }
   }
   // Flush every finished segment (block: wait for each until all are done).
   __device__ __forceinline__ void run(bool block) const {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (warp >= 4) return;
+    if (static_cast<std::uint32_t>(warp) >= nfw) return;
+    const std::uint32_t nh = nfw / 4;
     const std::uint32_t nb = a->acc_bufs;
     for (;;) {
       const std::uint32_t f = g_nflush[warp];
@@ -330,7 +341,8 @@ struct Flush {
       if (block) mbar_wait(bar, par);
       else if (!__all_sync(0xffffffffu, mbar_test(bar, par))) return;
       tc_fence_after();
-      segment(f);
+      if (nh == 1) segment(f);
+      else segment_cols(f, static_cast<std::uint32_t>(warp) & 3u, 8 * (static_cast<std::uint32_t>(warp) >> 2), 8 * nh);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -715,6 +727,15 @@ __shared__ unsigned g2_qnext;
 #define ECF8_L2_PROBE 0  // timing experiments only (wrong results): 1 no MMAs, 2 no ring stores
 #endif
 
+// L2-ring kernel: decode warps that flush finished segments mid-run (4, 8,
+// 12 or 16).  A/B (one Llama-3-70B layer): 4 -> 8 takes M = 256 from 0.631 to
+// 0.595-0.600 ms (the flushes no longer hold back the four warps whose K tiles
+// the ring waits for), M <= 64 the same; 12 / 16 the same as 8; choosing 4 at
+// M <= 64 at run time measured slower than the constant.
+#ifndef ECF8_FLUSH_WARPS
+#define ECF8_FLUSH_WARPS 8
+#endif
+
 #ifndef ECF8_FUSED_FINAL_ALL
 #define ECF8_FUSED_FINAL_ALL 1  // the segments left after the decode: flushed by all decode warps (0: warps 0-3)
 #endif
@@ -810,12 +831,12 @@ __global__ void __launch_bounds__((kL2DecodeWarps + 2) * 32, 1) fused_l2_kernel(
     }
     for (std::uint32_t b = 0; b < args.acc_bufs; ++b) {
       mbar_init(smem_addr(&g_segdone[b]), 1);
-      mbar_init(smem_addr(&g_accfree[b]), 4);
+      mbar_init(smem_addr(&g_accfree[b]), ECF8_FLUSH_WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     g2_loaded = 0;
     g2_qnext = kL2DecodeWarps;
-    for (int w = 0; w < 4; ++w) g_nflush[w] = 0;
+    for (int w = 0; w < 16; ++w) g_nflush[w] = 0;
   }
   {
     const uint4* f4 = reinterpret_cast<const uint4*>(args.w.fsm);
@@ -829,7 +850,7 @@ __global__ void __launch_bounds__((kL2DecodeWarps + 2) * 32, 1) fused_l2_kernel(
   const TensorDesc& d = g_wdesc;
   const std::uint32_t tmem_d = g_tmem;
   const std::uint32_t nseg = n_kt ? (cta.tile1 - 1) / KT - nt0 + 1 : 0;
-  const Flush fl{&args, tmem_d, nt0, nseg};
+  const Flush fl{&args, tmem_d, nt0, nseg, ECF8_FLUSH_WARPS};
   const std::uint32_t log2T = 31 - __clz(d.T);
 
   if (warp < kL2DecodeWarps) {
