@@ -420,7 +420,10 @@ int tensor_variant(const ecf8_dev_tensor* t) {
 // copy-out) and a ring of chunk slots in HBM.  Deliberately never freed:
 // CUDA may already be torn down when thread_local destructors run at exit.
 struct HostCtx {
-  static constexpr int kSlots = 4;
+  // Chunk slots in flight (ECF8_SLOTS, 2..kMaxSlots): the H2D of chunk k
+  // waits for the D2H of chunk k - nslots.
+  static constexpr int kMaxSlots = 16;
+  int nslots = 4;
   // Chunk limits.  PCIe copies pay ~15 us each, so chunks are large (32 M
   // elements = 32 MB D2H) in the steady state and ramp from 4 M at the start
   // and towards the end of a call (short pipeline fill and drain).  Measured
@@ -448,7 +451,7 @@ struct HostCtx {
     std::uint8_t *h_in = nullptr, *h_out = nullptr;
     std::uint8_t* pend_dst = nullptr;  // pageable destination of the slot's last D2H
     std::uint64_t pend_bytes = 0;
-  } slot[kSlots]{};
+  } slot[kMaxSlots]{};
   std::uint64_t h_in_bytes = 0, h_out_bytes = 0;
   // Per-tensor gaps + outpos (one copy each per tensor, not per chunk),
   // double-buffered by tensor parity.
@@ -471,6 +474,7 @@ HostCtx& host_ctx() {
     cu(cudaStreamCreateWithFlags(&c.s_out, cudaStreamNonBlocking), "stream");
     if (const char* e = std::getenv("ECF8_CHUNK_M")) c.elem_chunk = std::min<std::uint64_t>(std::atoi(e), 128) << 20;
     if (const char* e = std::getenv("ECF8_CHUNK_MIN_M")) c.elem_min = std::min<std::uint64_t>(std::atoi(e), 16) << 20;
+    if (const char* e = std::getenv("ECF8_SLOTS")) c.nslots = std::clamp(std::atoi(e), 2, HostCtx::kMaxSlots);
     // a chunk is >= one tile and the ramp never exceeds the slot size
     c.elem_chunk = std::max<std::uint64_t>(c.elem_chunk, ecf8::dev::kTileElemsMax);
     c.elem_min = std::clamp<std::uint64_t>(c.elem_min, ecf8::dev::kTileElemsMax, c.elem_chunk);
@@ -482,7 +486,8 @@ HostCtx& host_ctx() {
     const std::uint64_t b_eg = align_up(b_enc / 16 + S, 256);              // a nibble per 8-byte window
     const std::uint64_t b_ok = align_up(4 * (b_enc / 8 / 8192 + 2), 256);  // a bit per 256 windows (+ a straddled word)
     const std::uint64_t b_ls = align_up(2 * (b_enc / 32 + 1) + S, 256);    // a u16 per 4 windows
-    for (auto& sl : c.slot) {
+    for (int si = 0; si < c.nslots; ++si) {
+      HostCtx::Slot& sl = c.slot[si];
       void* p = nullptr;
       const std::uint64_t all = b_enc + b_pak + b_out + b_eg + 2 * b_ok + b_ls;
       cu(cudaMalloc(&p, all), "cudaMalloc(staging)");
@@ -649,7 +654,7 @@ int host_pipeline(const ecf8_sections* const* ss, const std::uint64_t* nbs, std:
       (void)tile_enc;
       target = std::min(2 * target, c.elem_chunk);  // ramp up (saturating)
       remaining -= s->outpos[hi] - s->outpos[lo];
-      HostCtx::Slot& sl = c.slot[k % HostCtx::kSlots];
+      HostCtx::Slot& sl = c.slot[k % c.nslots];
       if (sl.used) cu(cudaStreamWaitEvent(c.s_in, sl.out_done, 0), "wait");
       const std::uint64_t e0 = lo * T * 8, e1 = hi * T * 8 + 2;
       const std::uint64_t o0 = s->outpos[lo], o1 = s->outpos[hi];
@@ -710,7 +715,7 @@ int host_pipeline(const ecf8_sections* const* ss, const std::uint64_t* nbs, std:
       if (sink) {
         // the slot's previous chunk, and earlier tensors' chunks this D2H
         // overwrites in the shared buffer, are handed over first (in order)
-        while (!sink->q.empty() && (sink->q.front().slot == static_cast<int>(k % HostCtx::kSlots) ||
+        while (!sink->q.empty() && (sink->q.front().slot == static_cast<int>(k % c.nslots) ||
                                     (sink->q.front().tensor < i && sink->q.front().o0 < o1))) {
           deliver_front();
         }
@@ -740,7 +745,7 @@ int host_pipeline(const ecf8_sections* const* ss, const std::uint64_t* nbs, std:
         }
       }
       cu(cudaEventRecord(sl.out_done, c.s_out), "record");
-      if (sink) sink->q.push_back({static_cast<int>(k % HostCtx::kSlots), i, o0, o1});
+      if (sink) sink->q.push_back({static_cast<int>(k % c.nslots), i, o0, o1});
       lo = hi;
     }
     cu(cudaEventRecord(mt.done, c.s_run), "record");
@@ -748,7 +753,7 @@ int host_pipeline(const ecf8_sections* const* ss, const std::uint64_t* nbs, std:
   if (sink)
     while (!sink->q.empty()) deliver_front();
   cu(cudaStreamSynchronize(c.s_out), "sync");
-  for (auto& sl : c.slot) drain_out(sl);
+  for (int si = 0; si < c.nslots; ++si) drain_out(c.slot[si]);
   return ECF8_OK;
 }
 

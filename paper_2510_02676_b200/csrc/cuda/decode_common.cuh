@@ -398,12 +398,32 @@ struct FsmAt {
 #ifndef ECF8_PUT2_PRED
 #define ECF8_PUT2_PRED 1
 #endif
+// The symbol fields of two consecutive byte-step entries joined into one run:
+// (e1 >> 16) | ((e2 >> 16) << n4(e1)).  The two right shifts run as IMAD.HI
+// (x * 2^16, high word) on the FMA pipe and the OR folds into the second one's
+// addend (the fields are disjoint), leaving one funnel shift on the ALU pipe,
+// which the byte steps keep ~73 % busy.  ECF8_JOIN_ALU=1: the plain shifts.
+#ifndef ECF8_JOIN_ALU
+#define ECF8_JOIN_ALU 0
+#endif
+__device__ __forceinline__ std::uint32_t join_pair(std::uint32_t e1, std::uint32_t e2) {
+#if ECF8_JOIN_ALU
+  return (e1 >> 16) | __funnelshift_l(0u, e2 >> 16, e1);
+#else
+  std::uint32_t t, c;
+  asm("mul.hi.u32 %0, %1, 65536;" : "=r"(t) : "r"(e2));
+  t = __funnelshift_l(0u, t, e1);  // << n4(e1) (bits 0..4 of e1)
+  asm("mad.hi.u32 %0, %1, 65536, %2;" : "=r"(c) : "r"(e1), "r"(t));
+  return c;
+#endif
+}
+
 template <int WS>
 struct PairSink {
   std::uint32_t addr;  // next slot word
   std::uint32_t lo = 0, q4 = 0;
   __device__ __forceinline__ void put2(std::uint32_t e1, std::uint32_t e2) {
-    const std::uint32_t c = (e1 >> 16) | __funnelshift_l(0u, e2 >> 16, e1);  // f2 << n4(e1)
+    const std::uint32_t c = join_pair(e1, e2);  // f2 << n4(e1)
     const std::uint32_t q = q4 + e1 + e2;
     const std::uint32_t nl = lo | __funnelshift_l(0u, c, q4);  // c << (q4 % 32)
     const std::uint32_t nh = __funnelshift_l(c, 0u, q4);       // c >> (32 - q4 % 32)
@@ -439,7 +459,7 @@ struct PairSink {
   // dropped -- the symbols a parse produces past the run's end.
   __device__ __forceinline__ void put2_bounded(std::uint32_t e1, std::uint32_t e2, std::uint32_t ew,
                                                std::uint32_t& tail) {
-    const std::uint32_t c = (e1 >> 16) | __funnelshift_l(0u, e2 >> 16, e1);
+    const std::uint32_t c = join_pair(e1, e2);
     const std::uint32_t q = q4 + e1 + e2;
     const std::uint32_t nl = lo | __funnelshift_l(0u, c, q4);
     const std::uint32_t nh = __funnelshift_l(c, 0u, q4);

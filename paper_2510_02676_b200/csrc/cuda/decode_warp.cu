@@ -358,12 +358,29 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_warp_kernel(const LaunchArg
         }
 #else
         if (next < seg_end && lane < 5) prefetch_tile_l2(d, next, log2T, lane);
+#if ECF8_WIN_L1
+        if (next < seg_end) {  // A/B: the next tile's windows into this SM's L1 too
+          const std::uint32_t m1 = 256u >> log2T;
+          const std::uint64_t b0 = d.blk_begin + (next - d.tile_begin) * m1;
+          const std::uint64_t nb = d.blk_end - b0 < m1 ? d.blk_end - b0 : m1;
+          const std::uint64_t e0 = 8 * (b0 << log2T), e1 = e0 + 8 * (nb << log2T) + 8;
+          for (std::uint64_t a = (e0 & ~std::uint64_t{127}) + 128u * lane; a < e1; a += 32u * 128u)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(d.encoded + a));
+        }
+#endif
 #endif
         if (lane == 0) {  // this tile's sign/mantissa bytes -> L2 (direct tiles read them at write-back)
           const std::uint64_t p0 = (cur.A >> 1) & ~std::uint64_t{15};
           const std::uint32_t bytes = static_cast<std::uint32_t>((((cur.E + 1) >> 1) - p0 + 15) & ~std::uint64_t{15});
           if (bytes) prefetch_l2(d.packed + p0, bytes);
         }
+#if ECF8_PK_L1
+        {  // A/B: ... and into this SM's L1, one 128-byte line per lane
+          const std::uint64_t l0 = (cur.A >> 1) & ~std::uint64_t{127}, l1 = (cur.E + 1) >> 1;
+          for (std::uint64_t a = l0 + 128u * lane; a < l1; a += 32u * 128u)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(d.packed + a));
+        }
+#endif
         warp_tile<WIDE, TILED, DIRECT>(d, cur, log2T, len_off, ws, lane);
         tile = next;
       }

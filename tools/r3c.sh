@@ -1,0 +1,13 @@
+#!/bin/bash
+# A/B: L1 prefetch of the packed bytes (pkl1), of the next tile's windows (winl1), both; then the fused sweep.
+mkdir -p gpurun_out
+TAG=r3c
+for lib in main build/var/pkl1/libecf8_b200.so build/var/winl1/libecf8_b200.so build/var/both/libecf8_b200.so \
+           main build/var/pkl1/libecf8_b200.so build/var/winl1/libecf8_b200.so build/var/both/libecf8_b200.so; do
+  if [ "$lib" = main ]; then unset ECF8_LIB; else export ECF8_LIB=$lib; fi
+  b=$(timeout 600 python bench.py --steps 5 --warmup 3 --cpu-seconds 0 --e2e-steps 0 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['verified_bit_exact'], d['clocks'])")
+  p=$(timeout 300 python tools/probe.py --n 28672000 --count 16 2>&1 | grep bit-exact | sed 's/.*T=256: //')
+  echo "$lib | bench $b | probe $p" | tee -a gpurun_out/${TAG}_ab.txt
+done
+unset ECF8_LIB
+timeout 600 python bench.py --workload llama3-70b-fused --steps 10 --warmup 3 > gpurun_out/${TAG}_fused.json 2> gpurun_out/${TAG}_fused.err; grep "fused m=" gpurun_out/${TAG}_fused.err
