@@ -315,6 +315,33 @@ __device__ __forceinline__ void write_back(std::uint64_t S0, std::uint32_t off, 
     k = nfull + lane;  // the loops below find nothing left
   }
 #endif
+#if ECF8_WB_PIPE
+  if constexpr (GPK) {
+    // the packed bytes come from L2: the next group's loads are issued before
+    // this group's merges (two groups in flight per lane)
+    uint2 q[UNROLL];
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u)
+      if (k + 32u * u < nfull) q[u] = __ldg(pl + 32 * u);
+    for (; k < nfull; k += 32 * UNROLL, sl += 32 * UNROLL, pl += 32 * UNROLL) {
+      uint2 qn[UNROLL];
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u)
+        if (k + 32u * (UNROLL + u) < nfull) qn[u] = __ldg(pl + 32 * (UNROLL + u));
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
+        if (k + 32u * u < nfull) {
+          const uint2 sv = sl[32 * u];
+          uint4 r;
+          merge8(sv.x, q[u].x, r.x, r.y);
+          merge8(sv.y, q[u].y, r.z, r.w);
+          out.chunk(full_lo + k + 32 * u, r);
+        }
+        q[u] = qn[u];
+      }
+    }
+  }
+#endif
   for (; k + 32 * (UNROLL - 1) < nfull; k += 32 * UNROLL, sl += 32 * UNROLL, pl += 32 * UNROLL) {
 #pragma unroll
     for (int u = 0; u < UNROLL; ++u) {
