@@ -15,14 +15,4 @@ timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:decode_warp -s 5 -c 1 -o gpurun_out/${TAG}_full \
     python bench.py --steps 1 --warmup 3 --layers 8 --e2e-steps 0 --cpu-seconds 0 --no-verify > /dev/null 2>&1
 for m in 1 256; do timeout 600 ncu --set full --clock-control none --import-source on -k regex:fused_ -s 2 -c 1 -o gpurun_out/${TAG}_fused_m$m python tools/fused_one.py 28672 8192 $m 3 > /dev/null 2>&1; done
-for tool in memcheck synccheck; do
-  timeout 1500 compute-sanitizer --tool $tool --target-processes all --print-limit 50 python tools/sanitize_cases.py > gpurun_out/${TAG}_san_${tool}.log 2>&1
-  echo "sanitizer $tool rc=$?"; tail -n 2 gpurun_out/${TAG}_san_${tool}.log
-done
-for part in decode encode e5; do
-  timeout 1200 compute-sanitizer --tool racecheck --target-processes all --print-limit 50 python tools/sanitize_cases.py $part > gpurun_out/${TAG}_san_racecheck_${part}.log 2>&1
-  echo "racecheck $part rc=$?"; tail -n 2 gpurun_out/${TAG}_san_racecheck_${part}.log
-done
-timeout 1200 compute-sanitizer --tool racecheck --num-cuda-barriers 32 --target-processes all --print-limit 20 python tools/sanitize_cases.py fused > gpurun_out/${TAG}_san_racecheck_fused.log 2>&1
-echo "racecheck fused rc=$?"; tail -n 2 gpurun_out/${TAG}_san_racecheck_fused.log
 ls gpurun_out/${TAG}_*
