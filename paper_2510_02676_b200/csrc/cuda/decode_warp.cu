@@ -94,7 +94,7 @@ __device__ __forceinline__ void stage_fsm(const TensorDesc& d, int tid, int nthr
 }
 
 #ifndef ECF8_WB_UNROLL
-#define ECF8_WB_UNROLL 4
+#define ECF8_WB_UNROLL 8  // A/B (r3e, r3f): 8 +0.8-1.8 % over 4; 6, 12 and the stepped remainder (ECF8_WB_STEPS) less
 #endif
 constexpr int kWbUnroll = ECF8_WB_UNROLL;
 #ifndef ECF8_STATIC_TILES

@@ -315,6 +315,28 @@ __device__ __forceinline__ void write_back(std::uint64_t S0, std::uint32_t off, 
     k = nfull + lane;  // the loops below find nothing left
   }
 #endif
+#if ECF8_WB_PRED
+  if constexpr (GPK) {
+    // groups of UNROLL chunks per lane with per-chunk predicates: a tile's
+    // ~12 chunks per lane take ceil(12 / UNROLL) L2 round trips, with no
+    // one-chunk-at-a-time remainder loop
+    for (; k < nfull; k += 32 * UNROLL, sl += 32 * UNROLL, pl += 32 * UNROLL) {
+      uint2 sv[UNROLL], q[UNROLL];
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u)
+        if (k + 32u * u < nfull) sv[u] = sl[32 * u], q[u] = __ldg(pl + 32 * u);
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
+        if (k + 32u * u < nfull) {
+          uint4 r;
+          merge8(sv[u].x, q[u].x, r.x, r.y);
+          merge8(sv[u].y, q[u].y, r.z, r.w);
+          out.chunk(full_lo + k + 32 * u, r);
+        }
+      }
+    }
+  }
+#endif
 #if ECF8_WB_PIPE
   if constexpr (GPK) {
     // the packed bytes come from L2: the next group's loads are issued before
@@ -352,6 +374,36 @@ __device__ __forceinline__ void write_back(std::uint64_t S0, std::uint32_t off, 
       out.chunk(full_lo + k + 32 * u, r);
     }
   }
+#if ECF8_WB_STEPS
+  // the rest in groups of UNROLL / 2, / 4: a lane's loads of a group are in
+  // flight together (one L2 round trip per group, not per chunk)
+  if constexpr (UNROLL >= 8) {
+    constexpr int U2 = UNROLL / 2;
+    for (; k + 32 * (U2 - 1) < nfull; k += 32 * U2, sl += 32 * U2, pl += 32 * U2) {
+#pragma unroll
+      for (int u = 0; u < U2; ++u) {
+        const uint2 s = sl[32 * u], q = GPK ? __ldg(pl + 32 * u) : pl[32 * u];
+        uint4 r;
+        merge8(s.x, q.x, r.x, r.y);
+        merge8(s.y, q.y, r.z, r.w);
+        out.chunk(full_lo + k + 32 * u, r);
+      }
+    }
+  }
+  if constexpr (UNROLL >= 4) {
+    constexpr int U4 = UNROLL >= 8 ? UNROLL / 4 : 2;
+    for (; k + 32 * (U4 - 1) < nfull; k += 32 * U4, sl += 32 * U4, pl += 32 * U4) {
+#pragma unroll
+      for (int u = 0; u < U4; ++u) {
+        const uint2 s = sl[32 * u], q = GPK ? __ldg(pl + 32 * u) : pl[32 * u];
+        uint4 r;
+        merge8(s.x, q.x, r.x, r.y);
+        merge8(s.y, q.y, r.z, r.w);
+        out.chunk(full_lo + k + 32 * u, r);
+      }
+    }
+  }
+#endif
   for (; k < nfull; k += 32, sl += 32, pl += 32) {
     const uint2 s = *sl, q = GPK ? __ldg(pl) : *pl;
     uint4 r;

@@ -44,6 +44,12 @@ extern "C" int ecf8_internal_require_device(void);
 
 namespace ecf8::dev::e5 {
 
+// Write-back chunks per lane unrolled: their raw-plane loads (L2) in flight together.
+#ifndef ECF8_E5_WB_UNROLL
+#define ECF8_E5_WB_UNROLL 1
+#endif
+constexpr int kE5WbUnroll = ECF8_E5_WB_UNROLL;
+
 constexpr int kSyms = 32;
 constexpr int kFastBits = 10;
 constexpr std::uint64_t kPad = 64;
@@ -453,6 +459,7 @@ __global__ void __launch_bounds__(NW * 32, 1) e5_fsm_kernel(const Desc d) {
     // plane and the raw planes; 128-bit stores, the ragged edges byte-wise
     asm volatile("griddepcontrol.wait;" ::: "memory");  // the previous grid (PDL) is done writing
     const std::uint32_t nch = (data_end + 15) >> 4;
+#pragma unroll kE5WbUnroll
     for (std::uint32_t c = static_cast<std::uint32_t>(lane); c < nch; c += 32) {
       const uint2 nib = reinterpret_cast<const uint2*>(w4)[c];
       const std::uint32_t hb = (w1[c >> 1] >> (16 * (c & 1))) & 0xFFFFu;
@@ -636,6 +643,7 @@ __global__ void __launch_bounds__(NW * 32, 1) e5_fsm_bytes_kernel(const Desc d) 
     // write-back: 16 symbol bytes + the raw planes' 16 bits each per lane-step
     asm volatile("griddepcontrol.wait;" ::: "memory");  // the previous grid (PDL) is done writing
     const std::uint32_t nch = (data_end + 15) >> 4;
+#pragma unroll kE5WbUnroll
     for (std::uint32_t c = static_cast<std::uint32_t>(lane); c < nch; c += 32) {
       const uint4 ex = reinterpret_cast<const uint4*>(sb_)[c];
       const std::uint64_t e = S0 + 16 * static_cast<std::uint64_t>(c);

@@ -740,6 +740,10 @@ __shared__ unsigned g2_qnext;
 #define ECF8_FUSED_FINAL_ALL 1  // the segments left after the decode: flushed by all decode warps (0: warps 0-3)
 #endif
 
+#ifndef ECF8_FUSED_WB_UNROLL
+#define ECF8_FUSED_WB_UNROLL 4  // write-back chunks per lane in flight (the ring sink)
+#endif
+
 #ifndef ECF8_SLOT_SLEEP
 #define ECF8_SLOT_SLEEP 64  // ns between a waiting ring writer's polls
 #endif
@@ -880,7 +884,7 @@ __global__ void __launch_bounds__((kL2DecodeWarps + 2) * 32, 1) fused_l2_kernel(
         const std::uint64_t bnd = cta.e0 + (static_cast<std::uint64_t>(tf + 1) << 14);
         const std::uint32_t bf = static_cast<std::uint32_t>((E < bnd ? E : bnd) - A);
         const std::uint32_t bl = tl != tf ? static_cast<std::uint32_t>(E - bnd) : 0u;
-        direct_tile<4, 8, true>(
+        direct_tile<ECF8_FUSED_WB_UNROLL, 8, true>(
             d, cur, ws, lane,
             [&] {
               GRingOut o;
