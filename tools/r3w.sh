@@ -1,7 +1,7 @@
 #!/bin/bash
-# Round-end run on the final code: GPU suite, smoke, bench + reference arm, fused / DiT / T sweeps, decompress probe, launch list + full captures, sanitizers.
+# Final run of the session (after the write-back unroll change): same steps as r3z.
 mkdir -p gpurun_out
-TAG=r3z
+TAG=r3w
 timeout 1800 python -m pytest tests -m gpu -q -x > gpurun_out/${TAG}_pytest.log 2>&1; echo "pytest rc=$?"; tail -n 2 gpurun_out/${TAG}_pytest.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -n 1
 timeout 900 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err; cat gpurun_out/${TAG}_bench.json
