@@ -418,14 +418,31 @@ __device__ __forceinline__ std::uint32_t join_pair(std::uint32_t e1, std::uint32
 #endif
 }
 
+// A/B (ECF8_SINK_FMA): the sink's adds as IMADs by a constant-bank 1 the
+// compiler cannot fold (x * c_one + y), moving two more ALU-pipe operations per
+// byte pair to the FMA pipe: q4 + e1 + e2, and the OR of the disjoint partial
+// word and shifted run.
+#if ECF8_SINK_FMA
+__constant__ std::uint32_t c_one = 1;
+__device__ __forceinline__ std::uint32_t add3_fma(std::uint32_t a, std::uint32_t b, std::uint32_t c) {
+  return b * c_one + (c * c_one + a);
+}
+__device__ __forceinline__ std::uint32_t or_disjoint(std::uint32_t a, std::uint32_t b) { return b * c_one + a; }
+#else
+__device__ __forceinline__ std::uint32_t add3_fma(std::uint32_t a, std::uint32_t b, std::uint32_t c) {
+  return a + b + c;
+}
+__device__ __forceinline__ std::uint32_t or_disjoint(std::uint32_t a, std::uint32_t b) { return a | b; }
+#endif
+
 template <int WS>
 struct PairSink {
   std::uint32_t addr;  // next slot word
   std::uint32_t lo = 0, q4 = 0;
   __device__ __forceinline__ void put2(std::uint32_t e1, std::uint32_t e2) {
     const std::uint32_t c = join_pair(e1, e2);  // f2 << n4(e1)
-    const std::uint32_t q = q4 + e1 + e2;
-    const std::uint32_t nl = lo | __funnelshift_l(0u, c, q4);  // c << (q4 % 32)
+    const std::uint32_t q = add3_fma(q4, e1, e2);
+    const std::uint32_t nl = or_disjoint(lo, __funnelshift_l(0u, c, q4));  // c << (q4 % 32)
     const std::uint32_t nh = __funnelshift_l(c, 0u, q4);       // c >> (32 - q4 % 32)
 #if ECF8_PUT2_PRED
     // one predicate for the store, the address step and the select (no
@@ -460,8 +477,8 @@ struct PairSink {
   __device__ __forceinline__ void put2_bounded(std::uint32_t e1, std::uint32_t e2, std::uint32_t ew,
                                                std::uint32_t& tail) {
     const std::uint32_t c = join_pair(e1, e2);
-    const std::uint32_t q = q4 + e1 + e2;
-    const std::uint32_t nl = lo | __funnelshift_l(0u, c, q4);
+    const std::uint32_t q = add3_fma(q4, e1, e2);
+    const std::uint32_t nl = or_disjoint(lo, __funnelshift_l(0u, c, q4));
     const std::uint32_t nh = __funnelshift_l(c, 0u, q4);
     const bool full = ((q ^ q4) & 32u) != 0;
     if (full && addr < ew) sts32(addr, nl);
