@@ -418,10 +418,13 @@ __device__ __forceinline__ std::uint32_t join_pair(std::uint32_t e1, std::uint32
 #endif
 }
 
-// A/B (ECF8_SINK_FMA): the sink's adds as IMADs by a constant-bank 1 the
-// compiler cannot fold (x * c_one + y), moving two more ALU-pipe operations per
-// byte pair to the FMA pipe: q4 + e1 + e2, and the OR of the disjoint partial
-// word and shifted run.
+// The sink's adds as IMADs by a constant-bank 1 the compiler cannot fold
+// (x * c_one + y), moving two more ALU-pipe operations per byte pair to the
+// FMA pipe: q4 + e1 + e2, and the OR of the disjoint partial word and shifted
+// run.  A/B (r3j): decode +0.1-0.9 %, fused -0.3-0.6 % time; 0 restores them.
+#ifndef ECF8_SINK_FMA
+#define ECF8_SINK_FMA 1
+#endif
 #if ECF8_SINK_FMA
 __constant__ std::uint32_t c_one = 1;
 __device__ __forceinline__ std::uint32_t add3_fma(std::uint32_t a, std::uint32_t b, std::uint32_t c) {
