@@ -406,6 +406,9 @@ struct FsmAt {
 #ifndef ECF8_JOIN_ALU
 #define ECF8_JOIN_ALU 0
 #endif
+#if ECF8_JOIN_CONST
+__constant__ std::uint32_t c_65536 = 65536;
+#endif
 __device__ __forceinline__ std::uint32_t join_pair(std::uint32_t e1, std::uint32_t e2) {
 #if ECF8_JOIN_ALU
   return (e1 >> 16) | __funnelshift_l(0u, e2 >> 16, e1);
@@ -413,7 +416,11 @@ __device__ __forceinline__ std::uint32_t join_pair(std::uint32_t e1, std::uint32
   std::uint32_t t, c;
   asm("mul.hi.u32 %0, %1, 65536;" : "=r"(t) : "r"(e2));
   t = __funnelshift_l(0u, t, e1);  // << n4(e1) (bits 0..4 of e1)
-  asm("mad.hi.u32 %0, %1, 65536, %2;" : "=r"(c) : "r"(e1), "r"(t));
+#if ECF8_JOIN_CONST
+  c = __umulhi(e1, c_65536) + t;  // IMAD.HI by a constant-bank 2^16 (ptxas keeps it on the FMA pipe)
+#else
+  asm("mad.hi.u32 %0, %1, 65536, %2;" : "=r"(c) : "r"(e1), "r"(t));  // (ptxas: LEA.HI)
+#endif
   return c;
 #endif
 }
