@@ -75,7 +75,8 @@ __shared__ __align__(1024) StaticSmem g_s;
 struct StaticSmemFsm {
   unsigned next_tile;
   TensorDesc desc;
-  unsigned char pad[kFsmAt - 0x400 - 8 - sizeof(TensorDesc)];
+  PfSec pf[5];  // the segment's section table for the L2 prefetches (ECF8_PF_TAB)
+  unsigned char pad[kFsmAt - 0x400 - 8 - sizeof(TensorDesc) - 5 * sizeof(PfSec)];
   std::uint32_t fsm[256 * kFsmStates];
   std::uint8_t cm[256 * kFsmStates];
 };
@@ -105,6 +106,9 @@ constexpr int kWbUnroll = ECF8_WB_UNROLL;
 #endif
 #ifndef ECF8_PF_GROUP
 #define ECF8_PF_GROUP 1  // >1: the sections of G tiles per L2 prefetch, AHEAD tiles ahead (A/B: slower, lower clocks)
+#endif
+#ifndef ECF8_PF_TAB
+#define ECF8_PF_TAB 1  // the next tile's L2 prefetch addresses from a per-segment section table (A/B r3n: +1.3-1.6 %)
 #endif
 #ifndef ECF8_PF_AHEAD
 #define ECF8_PF_AHEAD 32  // tiles between a claim and the group it prefetches (a multiple of ECF8_PF_GROUP)
@@ -273,6 +277,10 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_warp_kernel(const LaunchArg
     }
     const std::uint32_t len_off = (d.n_luts - 1) << 8;
     if (threadIdx.x == 0) next_tile = NW;
+#if ECF8_PF_TAB
+    if constexpr (!WIDE)
+      if (threadIdx.x < 5) g_f.pf[threadIdx.x] = pf_section(d, threadIdx.x, log2T);
+#endif
     __syncthreads();
 
     // Tiles are handed out dynamically inside the CTA (warp w starts with
@@ -335,6 +343,8 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_warp_kernel(const LaunchArg
       constexpr std::uint32_t kInit = (NW + kPfAhead + G - 1) / G;  // groups before the first claim's
       for (std::uint32_t g = warp; g < kInit && g * G < n_rel; g += NW)
         if (lane < 5) prefetch_tile_l2(d, seg + g * G, log2T, lane, static_cast<std::uint32_t>(min(std::uint64_t{G}, n_rel - g * G)));
+#elif ECF8_PF_TAB
+      if (tile < seg_end && lane < 5) prefetch_tile_l2_tab(d, g_f.pf, tile, log2T, lane);
 #else
       if (tile < seg_end && lane < 5) prefetch_tile_l2(d, tile, log2T, lane);
 #endif
@@ -356,6 +366,8 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_warp_kernel(const LaunchArg
           if (pf % G == 0 && pf < n_rel && lane < 5)
             prefetch_tile_l2(d, seg + pf, log2T, lane, static_cast<std::uint32_t>(min(std::uint64_t{G}, n_rel - pf)));
         }
+#elif ECF8_PF_TAB
+        if (next < seg_end && lane < 5) prefetch_tile_l2_tab(d, g_f.pf, next, log2T, lane);
 #else
         if (next < seg_end && lane < 5) prefetch_tile_l2(d, next, log2T, lane);
 #if ECF8_WIN_L1

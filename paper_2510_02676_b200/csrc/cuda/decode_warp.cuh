@@ -163,6 +163,35 @@ __device__ __forceinline__ void prefetch_tile_l2(const TensorDesc& d, std::uint6
   if (p && n) prefetch_l2(p, n);
 }
 
+// The same prefetches from a per-segment table (ECF8_PF_TAB): lane i < 5
+// takes its section's base pointer, byte shift per block and extra bytes
+// (prefetch_sections) -- one shared load instead of five candidate pointers
+// and a select chain.  Section i of blocks [b0, b0 + nb): base + (b0 << sh),
+// (nb << sh) + add bytes.
+struct PfSec {
+  std::uint64_t base;  // 0: the section is absent
+  std::uint32_t sh, add;
+};
+__device__ __forceinline__ PfSec pf_section(const TensorDesc& d, int i, std::uint32_t log2T) {
+  const void* p = i == 0 ? static_cast<const void*>(d.encoded)
+                  : i == 1 ? static_cast<const void*>(d.gaps)
+                  : i == 2 ? static_cast<const void*>(d.outpos)
+                  : i == 3 ? static_cast<const void*>(d.endgap)
+                           : static_cast<const void*>(d.lane_start);
+  // encoded: 8 T bytes per block (+ the 8-byte lookahead); gaps, end nibbles,
+  // group offsets: T / 2 bytes per block; outpos: 8 bytes per block (+ 1 entry)
+  const std::uint32_t sh = i == 0 ? log2T + 3 : i == 2 ? 3u : log2T - 1;
+  return PfSec{reinterpret_cast<std::uint64_t>(p), sh, (i == 0 || i == 2) ? 8u : 0u};
+}
+__device__ __forceinline__ void prefetch_tile_l2_tab(const TensorDesc& d, const PfSec* tab, std::uint64_t tile,
+                                                     std::uint32_t log2T, int lane) {
+  const std::uint32_t m1 = 256u >> log2T;
+  const std::uint64_t b0 = d.blk_begin + (tile - d.tile_begin) * m1;
+  const std::uint64_t nb = d.blk_end - b0 < m1 ? d.blk_end - b0 : m1;
+  const PfSec s = tab[lane];
+  if (s.base) prefetch_l2(reinterpret_cast<const void*>(s.base + (b0 << s.sh)), (nb << s.sh) + s.add);
+}
+
 // Were the gaps of the windows of this warp tile verified (verify_gaps_kernel)?
 // tile_ok bit v covers the boundaries after windows [256v, 256v + 256).
 template <int LW>
