@@ -800,6 +800,18 @@ struct GRingOut {
   }
 };
 
+// The decode warps' L2 prefetches of their next tile: addresses from the
+// section table (decode_warp.cuh: prefetch_tile_l2_tab) or computed per tile.
+#ifndef ECF8_FUSED_PF_TAB
+#define ECF8_FUSED_PF_TAB 0
+#endif
+#if ECF8_FUSED_PF_TAB
+__shared__ PfSec g_wpf[5];
+#define PF_TILE(d, t, l2t, ln) prefetch_tile_l2_tab(d, g_wpf, t, l2t, ln)
+#else
+#define PF_TILE(d, t, l2t, ln) prefetch_tile_l2(d, t, l2t, ln)
+#endif
+
 __global__ void __launch_bounds__((kL2DecodeWarps + 2) * 32, 1) fused_l2_kernel(const __grid_constant__ FusedArgs args) {
   constexpr int kWarps = kL2DecodeWarps + 2, kLoader = kL2DecodeWarps, kMma = kL2DecodeWarps + 1;
   using WSm = WarpPipeSmem<1, 32 * 8 * 32 / 8 + 8>;  // the staging tile (packed bytes come from L2)
@@ -815,6 +827,9 @@ __global__ void __launch_bounds__((kL2DecodeWarps + 2) * 32, 1) fused_l2_kernel(
   WSm* const wsm = reinterpret_cast<WSm*>(smem_raw + (b_base + S * b_bytes - raw));
   std::uint8_t* const ring = args.scratch + static_cast<std::uint64_t>(blockIdx.x) * kRingSlots * kTileElems;
 
+#if ECF8_FUSED_PF_TAB
+  if (threadIdx.x < 5) g_wpf[threadIdx.x] = pf_section(args.w, threadIdx.x, 31 - __clz(args.w.T));
+#endif
   if (threadIdx.x == 0) {
     g_wdesc = args.w;
     g_wdesc.blk_begin = cta.blk_begin;
@@ -864,14 +879,14 @@ __global__ void __launch_bounds__((kL2DecodeWarps + 2) * 32, 1) fused_l2_kernel(
     WSm& ws = wsm[warp];
     const FsmAt ft{smem_addr(g_fsmf), smem_addr(g_cmf)};
     std::uint64_t tile = warp;
-    if (tile < n_tiles && lane < 5) prefetch_tile_l2(d, tile, log2T, lane);
+    if (tile < n_tiles && lane < 5) PF_TILE(d, tile, log2T, lane);
     while (tile < n_tiles) {
       WarpInT<8> cur;
       load_warp_tile<8, true, false, false>(d, tile, log2T, lane, cur);
       unsigned claim = 0;
       if (lane == 0) claim = atomicAdd(&g2_qnext, 1u);
       const std::uint64_t next = __shfl_sync(0xffffffffu, claim, 0);
-      if (next < n_tiles && lane < 5) prefetch_tile_l2(d, next, log2T, lane);
+      if (next < n_tiles && lane < 5) PF_TILE(d, next, log2T, lane);
       if (lane == 0) {  // this tile's sign/mantissa bytes -> L2 (read at write-back)
         const std::uint64_t p0 = (cur.A >> 1) & ~std::uint64_t{15};
         const std::uint32_t bytes = static_cast<std::uint32_t>((((cur.E + 1) >> 1) - p0 + 15) & ~std::uint64_t{15});
