@@ -410,6 +410,7 @@ using Fsm64WarpSmem = WarpPipeSmem<1, 2 * 32 * kSlotWords + 8>;  // 16384 nibble
 __shared__ __align__(16) std::uint64_t g_fsm64[256 * kFsmStates];
 __shared__ unsigned g6_next_tile;
 __shared__ TensorDesc g6_desc;
+__shared__ PfSec g6_pf[5];  // the segment's prefetch section table (ECF8_PF_TAB)
 
 template <int NW>
 __global__ void __launch_bounds__(NW * 32, 1) decode_fsm64_kernel(const LaunchArgs args) {
@@ -450,16 +451,22 @@ __global__ void __launch_bounds__(NW * 32, 1) decode_fsm64_kernel(const LaunchAr
       for (int i = threadIdx.x; i < 256 * kFsmStates / 2; i += NW * 32) s4[i] = __ldg(f4 + i);
     }
     if (threadIdx.x == 0) g6_next_tile = NW;
+#if ECF8_PF_TAB
+    if (threadIdx.x < 5) g6_pf[threadIdx.x] = pf_section(d, threadIdx.x, log2T);
+#define PF6(t) prefetch_tile_l2_tab(d, g6_pf, t, log2T, lane)
+#else
+#define PF6(t) prefetch_tile_l2(d, t, log2T, lane)
+#endif
     __syncthreads();
     std::uint64_t tile = seg + warp;
-    if (tile < seg_end && lane < 5) prefetch_tile_l2(d, tile, log2T, lane);
+    if (tile < seg_end && lane < 5) PF6(tile);
     while (tile < seg_end) {
       WarpIn cur;
       load_warp_tile<kLaneWin, true, false, false>(d, tile, log2T, lane, cur);
       unsigned claim = 0;
       if (lane == 0) claim = atomicAdd(&g6_next_tile, 1u);
       const std::uint64_t next = seg + __shfl_sync(0xffffffffu, claim, 0);
-      if (next < seg_end && lane < 5) prefetch_tile_l2(d, next, log2T, lane);
+      if (next < seg_end && lane < 5) PF6(next);
       if (lane == 0) {  // this tile's sign/mantissa bytes -> L2 (read at write-back)
         const std::uint64_t p0 = (cur.A >> 1) & ~std::uint64_t{15};
         const std::uint32_t bytes = static_cast<std::uint32_t>((((cur.E + 1) >> 1) - p0 + 15) & ~std::uint64_t{15});
